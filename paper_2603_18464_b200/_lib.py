@@ -1,0 +1,66 @@
+"""ctypes binding of libaccel.so (the C ABI in include/accel.h).
+
+There is no fallback: if the library is missing or no CUDA device is
+present, every op raises AccelError.  Build with
+`python -m paper_2603_18464_b200.build`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_double, c_int, c_int64, c_size_t, c_uint64, c_void_p
+from pathlib import Path
+
+from .errors import AccelError, raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "libaccel.so"
+
+P = c_void_p
+# name -> (restype, argtypes)
+_SIGNATURES = {
+    "accel_last_error": (ctypes.c_char_p, []),
+    "accel_launch_count": (ctypes.c_ulonglong, []),
+    "accel_version": (c_int, []),
+    "accel_gae_workspace_size": (c_size_t, [c_int64]),
+    "accel_gae_segmented": (c_int, [P, P, P, P, c_int64, c_int64, c_double, c_double,
+                                    P, P, P, P, P, c_size_t, P]),
+    "accel_normalize_finalize": (c_int, [P, c_double, P, P]),
+    "accel_normalize_apply": (c_int, [P, c_int64, P, P, P]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise AccelError(f"{LIB_PATH} not built; run `python -m paper_2603_18464_b200.build`")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an int-status entry point; map a non-zero status to the
+    reference exception types (include/accel.h conventions)."""
+    handle = lib()
+    status = getattr(handle, name)(*args)
+    if status:
+        raise_for_status(status, handle.accel_last_error().decode(errors="replace"))
+
+
+def launch_count() -> int:
+    return int(lib().accel_launch_count())
+
+
+def exported_symbols() -> list:
+    return sorted(_SIGNATURES)
+
+
+def c_u64(x: int) -> c_uint64:
+    return c_uint64(x)

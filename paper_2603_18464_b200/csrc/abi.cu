@@ -1,0 +1,31 @@
+// Library-level C ABI: error reporting and launch accounting.
+#include <cstdarg>
+
+#include "common.cuh"
+
+namespace accel {
+
+static thread_local std::string t_last_error;
+std::atomic<unsigned long long> g_launches{0};
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  return status;
+}
+
+}  // namespace accel
+
+extern "C" const char* accel_last_error(void) { return accel::t_last_error.c_str(); }
+
+extern "C" unsigned long long accel_launch_count(void) {
+  return accel::g_launches.load(std::memory_order_relaxed);
+}
+
+extern "C" int accel_version(void) { return 1; }

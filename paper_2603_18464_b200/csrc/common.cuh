@@ -1,0 +1,93 @@
+// Shared helpers for libaccel (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/accel.h"
+
+namespace accel {
+
+enum Status : int { kOk = 0, kDomain = 1, kDimension = 2, kNonFinite = 3, kCuda = 4 };
+
+void set_error(const std::string& msg);
+int fail(int status, const char* fmt, ...);
+extern std::atomic<unsigned long long> g_launches;
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Check the launch that was just issued; count it.
+inline int post_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(kCuda, "%s: %s", what, cudaGetErrorString(e));
+  return kOk;
+}
+
+inline int check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(kCuda, "%s: %s", what, cudaGetErrorString(e));
+  return kOk;
+}
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- memory-ordering primitives for cross-CTA publication -------------------
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ---- warp reductions ---------------------------------------------------------
+template <int W = 32>
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
+  return v;
+}
+template <int W = 32>
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, W));
+  return v;
+}
+template <int W = 32>
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
+  return v;
+}
+
+// Deterministic block reduction of NV doubles per thread (fixed pairing).
+// `scratch` needs blockDim.x/32 * NV doubles. Result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum_d(double (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum_d(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[warp * NV + i] = v[i];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double x = lane < nw ? scratch[lane * NV + i] : 0.0;
+      v[i] = warp_sum_d(x);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace accel
