@@ -77,6 +77,152 @@ int accel_normalize_finalize(const double* sums, double eps, double* stats_out,
 int accel_normalize_apply(const float* adv, int64_t n, const double* stats,
                           float* adv_norm_out, void* stream);
 
+/* ---- (b) token loss --------------------------------------------------- */
+
+/* CTA count used by the token kernels for M rows (sizes their partials). */
+int accel_token_grid(int64_t M);
+
+/* Behavior log-probs — replaces `behavior_log_probs` (trainer.py:289-293).
+ *   mu f32[M, A] behavior logits, tokens i32[M] -> lp_out f32[M]
+ *   bad_part f64[grid][2]: {rows with non-finite logits (the reference's
+ *   log_softmax raises DomainError, numerics.py:138-139), tokens outside
+ *   [0, A)} per CTA (grid = accel_token_grid(M)). */
+int accel_token_logp(const float* mu, const int32_t* tokens, int64_t M, int A,
+                     float* lp_out, double* bad_part, void* stream);
+
+/* Fused token loss forward + backward over logit rows — replaces
+ * `log_prob_chunk` (models.py:219-223), `policy_surrogate`
+ * (trainer.py:183-239), `entropy_bonus` (:242-251) and the dlogits assembly
+ * of `train_step` (:425-435).
+ *   logits f32[M, A] (head GEMM output WITHOUT bias), bias f32[A] (b_head),
+ *   tokens i32[M], lp_old f32[M], adv f32[M / K] (normalized, one per
+ *   transition), algo 0 = "trust" (GIPO), 1 = "clip" (PPO),
+ *   m_global = token count over all ranks (entropy mean denominator and the
+ *   optimistic included count).
+ *   fix_stats == NULL: main pass; writes dlogits f32[M, A], lp_new f32[M],
+ *     dbias_part f32[grid][A], stat_part f64[grid][8] {sum w r a | sum min-surr,
+ *     sum H, sum r, sum w, #outside clip band, #excluded, #non-finite rows,
+ *     #bad tokens}, max_part f64[grid][2] {max r, -min w}.
+ *   fix_stats != NULL (the reduced, all-rank stat vector): FIXUP pass; if
+ *     0 < #excluded < m_global rewrites dlogits and dbias_part with the true
+ *     included count, else returns immediately (device-side decision). */
+int accel_token_loss(const float* logits, const float* bias, const int32_t* tokens,
+                     const float* lp_old, const float* adv, int64_t M, int K, int A,
+                     int algo, double sigma, double clip_eps, double lambda_h,
+                     double m_global, const double* fix_stats, float* dlogits,
+                     float* lp_new, float* dbias_part, double* stat_part,
+                     double* max_part, void* stream);
+
+/* ---- policy glue (models.py:165-209) ----------------------------------- */
+
+/* z = tanh(z + b) in place, z f32[rows, cols] — models.py:176-177. */
+int accel_bias_tanh(float* z, const float* b, int64_t rows, int cols, void* stream);
+
+/* c[i*K+k] = h2[frame_of[i]] + e_prev[prev] + e_pos[k], prev = A for k = 0
+ * else tokens[i*K+k-1] — models.py:178-181.  c_out f32[N*K, D]. */
+int accel_build_c(const float* h2, const int32_t* frame_of, const int32_t* tokens,
+                  const float* e_prev, const float* e_pos, int64_t N, int K, int A,
+                  int D, float* c_out, void* stream);
+
+/* Default CTA count for the column-reduction kernels over `rows` rows. */
+int accel_rows_grid(int64_t rows);
+
+/* From dc = dlogits @ W_head (f32[N*K, D]): dh2 = sum_k dc, dz2[frame] =
+ * dh2 (1 - h2^2) (dz2 f32[F, D], bootstrap rows left untouched — pre-zero),
+ * pos_part f32[grid][K][D] (de_pos), db1_part f32[grid][D] —
+ * models.py:196-200.  K <= 16. */
+int accel_dc_reduce(const float* dc, const float* h2, const int32_t* frame_of,
+                    int64_t N, int K, int D, float* dz2, float* pos_part,
+                    float* db1_part, int grid, void* stream);
+
+/* g = g (1 - h^2) in place over f32[R, C]; col_part f32[grid][C] —
+ * models.py:202-204 (dz1 and db0). */
+int accel_tanh_grad_colsum(float* g, const float* h, int64_t R, int C,
+                           float* col_part, int grid, void* stream);
+
+/* ---- deterministic scatter-add (np.add.at, models.py:195 and :305) ------ */
+
+int accel_prev_keys(const int32_t* tokens, int64_t N, int K, int A, int32_t* keys,
+                    void* stream);
+/* keys[r] = steps[frame_of ? frame_of[r] : r]; bad_count += out-of-range
+ * steps (the reference raises DimensionError, models.py:261-267). */
+int accel_step_keys(const int32_t* steps, const int32_t* frame_of, int64_t R,
+                    int n_steps, int32_t* keys, unsigned* bad_count, void* stream);
+size_t accel_group_workspace_size(int64_t R, int nkeys);
+int64_t accel_group_max_pieces(int64_t R, int nkeys);
+/* Stable counting sort of R keys in [0, nkeys): perm i32[R], seg_off
+ * i64[nkeys+1], piece_off i64[nkeys+1] (pieces of <= 256 rows per key). */
+int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
+                       int64_t* seg_off, int64_t* piece_off, void* workspace,
+                       size_t workspace_bytes, void* stream);
+/* out f32[nkeys, D] = sum of vals rows per key, in perm order (bitwise
+ * deterministic); piece_buf f32[accel_group_max_pieces(R, nkeys) * D]. */
+int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
+                           const int64_t* seg_off, const int64_t* piece_off, int nkeys,
+                           int64_t n_pieces, float* piece_buf, float* out, void* stream);
+
+/* ---- value head (models.py:273-314, trainer.py:438-443) ---------------- */
+
+int accel_warp_grid(int64_t rows);
+/* u = softmax_j(h_j . w_attn + b) pooled h + e_step[step]; U f32[R, D],
+ * alpha f32[R, 2]; bad_part f64[grid][2] {non-finite scores, bad steps}. */
+int accel_value_pool(const float* h1, const float* h2, const int32_t* row_frame,
+                     const int32_t* steps, int64_t R, int D, int n_steps,
+                     const float* w_attn, const float* b_attn, const float* e_step,
+                     float* U, float* alpha, double* bad_part, int grid, void* stream);
+/* zm f32[R, H] = u @ W0v^T (no bias).  targets == NULL: forward only
+ * (values_out f32[R]).  Otherwise zm <- dzm, part f32[grid][2H+1]
+ * {dw1v, db0v, db1v}, dpart f64[grid][2] {sum err^2, non-finite v}. */
+int accel_value_head(float* zm, const float* b0v, const float* w1v, const float* b1v,
+                     int64_t R, int H, const float* targets, double lambda_v,
+                     double n_global, float* values_out, float* part, double* dpart,
+                     int grid, void* stream);
+/* de f32[R, 2] attention-score gradients, part f32[grid] (db_attn). */
+int accel_value_attn_grad(const float* dU, const float* h1, const float* h2,
+                          const int32_t* row_frame, const float* alpha, int64_t R, int D,
+                          float* de, float* part, int grid, void* stream);
+/* part f32[grid][D] (dw_attn). */
+int accel_value_attn_wgrad(const float* de, const float* h1, const float* h2,
+                           const int32_t* row_frame, int64_t R, int D, float* part,
+                           int grid, void* stream);
+
+/* ---- reductions, record, optimizer ------------------------------------- */
+
+/* dst_i[j] = sum_p src_i[p * pitch_i + j] (fixed order), up to 16
+ * segments; pitches == NULL means pitch_i = len_i. */
+int accel_reduce_segments(const void* const* srcs, void* const* dsts,
+                          const int64_t* parts, const int64_t* lens,
+                          const int64_t* pitches, int nseg, void* stream);
+/* out f64[nseg][3] = {sum, sum of squares, count} per segment of x —
+ * shard_statistics (trainer.py:128-132). */
+int accel_segment_moments(const float* x, const int64_t* off, int64_t nseg,
+                          double* out, void* stream);
+/* count += rows of x f32[*, C] (rows[r], or r when rows == NULL) holding a
+ * non-finite value — TrainBatch.check_finite on obs (buffers.py:120-122). */
+int accel_count_nonfinite_rows(const float* x, const int32_t* rows, int64_t R, int C,
+                               unsigned* count, void* stream);
+/* out[c] = sum (mode 0) or max (mode 1) over p of part[p * width + c]. */
+int accel_reduce_f64(const double* part, int64_t parts, int width, int mode,
+                     double* out, void* stream);
+/* train_step record (trainer.py:417-464) -> record f64[17]:
+ * {loss, policy_loss, value_loss, entropy, excluded_tokens, ratio_mean,
+ *  ratio_max, trust_weight_mean, trust_weight_min, clipped_fraction,
+ *  dropped, bad_logit_rows, bad_tokens, bad_attention, bad_grads,
+ *  bad_steps, skip}; skip i32 gates accel_adam. */
+int accel_step_finalize(const double* loss_sums, const double* loss_max,
+                        const double* value_sums, const unsigned* bad_counts,
+                        const double* attn_bad, int algo, double lambda_v,
+                        double lambda_h, double n_tokens, double n_transitions,
+                        double* record, int* skip, void* stream);
+int accel_count_nonfinite(const float* x, int64_t n, unsigned* count, void* stream);
+/* Adam (numerics.py:95-126) over a flat buffer: [0, n0) group0, [n0, n)
+ * group1; group = f64[6] {lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t}.
+ * No-op when *skip; bad += non-finite new parameters. */
+int accel_adam(const float* p_in, const float* g, const float* m_in, const float* v_in,
+               float* p_out, float* m_out, float* v_out, int64_t n, int64_t n0,
+               const double* group0, const double* group1, const int* skip,
+               unsigned* bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

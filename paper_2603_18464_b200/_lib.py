@@ -26,6 +26,36 @@ _SIGNATURES = {
                                     P, P, P, P, P, c_size_t, P]),
     "accel_normalize_finalize": (c_int, [P, c_double, P, P]),
     "accel_normalize_apply": (c_int, [P, c_int64, P, P, P]),
+    "accel_token_grid": (c_int, [c_int64]),
+    "accel_token_logp": (c_int, [P, P, c_int64, c_int, P, P, P]),
+    "accel_token_loss": (c_int, [P, P, P, P, P, c_int64, c_int, c_int, c_int, c_double,
+                                 c_double, c_double, c_double, P, P, P, P, P, P, P]),
+    "accel_bias_tanh": (c_int, [P, P, c_int64, c_int, P]),
+    "accel_build_c": (c_int, [P, P, P, P, P, c_int64, c_int, c_int, c_int, P, P]),
+    "accel_rows_grid": (c_int, [c_int64]),
+    "accel_dc_reduce": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, P, c_int, P]),
+    "accel_tanh_grad_colsum": (c_int, [P, P, c_int64, c_int, P, c_int, P]),
+    "accel_prev_keys": (c_int, [P, c_int64, c_int, c_int, P, P]),
+    "accel_step_keys": (c_int, [P, P, c_int64, c_int, P, P, P]),
+    "accel_group_workspace_size": (c_size_t, [c_int64, c_int]),
+    "accel_group_max_pieces": (c_int64, [c_int64, c_int]),
+    "accel_group_by_key": (c_int, [P, c_int64, c_int, P, P, P, P, c_size_t, P]),
+    "accel_grouped_rows_sum": (c_int, [P, c_int64, c_int, P, P, P, c_int, c_int64, P, P, P]),
+    "accel_warp_grid": (c_int, [c_int64]),
+    "accel_value_pool": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P, P, c_int,
+                                 P]),
+    "accel_value_head": (c_int, [P, P, P, P, c_int64, c_int, P, c_double, c_double, P, P, P,
+                                 c_int, P]),
+    "accel_value_attn_grad": (c_int, [P, P, P, P, P, c_int64, c_int, P, P, c_int, P]),
+    "accel_value_attn_wgrad": (c_int, [P, P, P, P, c_int64, c_int, P, c_int, P]),
+    "accel_reduce_segments": (c_int, [P, P, P, P, P, c_int, P]),
+    "accel_segment_moments": (c_int, [P, P, c_int64, P, P]),
+    "accel_count_nonfinite_rows": (c_int, [P, P, c_int64, c_int, P, P]),
+    "accel_reduce_f64": (c_int, [P, c_int64, c_int, c_int, P, P]),
+    "accel_step_finalize": (c_int, [P, P, P, P, P, c_int, c_double, c_double, c_double,
+                                    c_double, P, P, P]),
+    "accel_count_nonfinite": (c_int, [P, c_int64, P, P]),
+    "accel_adam": (c_int, [P, P, P, P, P, P, P, c_int64, c_int64, P, P, P, P, P]),
 }
 
 _lib = None

@@ -1,0 +1,274 @@
+// Deterministic grouped row sums (the reference's np.add.at scatter-adds).
+//
+// Reference: `np.add.at(de_prev, prev.ravel(), dc)` (models.py:195) and
+// `np.add.at(de_step, t, du)` (models.py:305).  Float atomics would make the
+// result depend on scheduling; instead the keys of a batch (previous-token
+// ids, step ids — fixed per TrainBatch) are counting-sorted once, stably, at
+// batch build time, and every later grouped sum is a segmented reduction in
+// that fixed order:
+//   1. chunk histograms (one warp per 1024-row chunk, smem int atomics),
+//   2. one exclusive scan over the key-major [key][chunk] counts,
+//   3. stable scatter: each warp walks its chunk 32 rows at a time, ranking
+//      equal keys with __match_any_sync,
+//   4. grouped sums: each key segment is cut into <=256-row pieces; one CTA
+//      sums a piece (gathered rows) in fixed order, a second pass sums the
+//      pieces of each key in order.
+#include "common.cuh"
+
+namespace accel {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 1024;  // rows per warp chunk
+constexpr int kPiece = 256;   // rows per grouped-sum piece
+
+__global__ void prev_keys_kernel(const int32_t* __restrict__ tokens, int64_t M, int K, int A,
+                                 int32_t* __restrict__ keys) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < M; r += stride) {
+    const int k = (int)(r % K);
+    int key = k == 0 ? A : __ldg(tokens + r - 1);
+    keys[r] = min(max(key, 0), A);
+  }
+}
+
+__global__ void step_keys_kernel(const int32_t* __restrict__ steps,
+                                 const int32_t* __restrict__ frame_of, int64_t R, int n_steps,
+                                 int32_t* __restrict__ keys, unsigned* __restrict__ bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned nbad = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    const int64_t f = frame_of ? __ldg(frame_of + r) : r;
+    const int s = __ldg(steps + f);
+    nbad += (s < 0 || s >= n_steps);
+    keys[r] = min(max(s, 0), n_steps - 1);
+  }
+  if (nbad) atomicAdd(bad, nbad);  // integer count: order-independent
+}
+
+// counts[key * n_chunks + chunk]
+__global__ void __launch_bounds__(kThreads)
+chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
+                  int* __restrict__ counts) {
+  extern __shared__ int s_hist[];  // [kWarps][nkeys]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* h = s_hist + warp * nkeys;
+  for (int j = lane; j < nkeys; j += 32) h[j] = 0;
+  __syncwarp();
+  const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
+  if (chunk < n_chunks) {
+    const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
+    for (int64_t r = r0 + lane; r < r1; r += 32) atomicAdd(h + __ldg(keys + r), 1);
+    __syncwarp();
+    for (int j = lane; j < nkeys; j += 32) counts[(int64_t)j * n_chunks + chunk] = h[j];
+  }
+}
+
+// Single-CTA exclusive scan of counts (in place); seg_off[j] = start of key j.
+__global__ void __launch_bounds__(1024)
+scan_counts_kernel(int* __restrict__ counts, int64_t total, int nkeys, int64_t n_chunks, int64_t R,
+                   int64_t* __restrict__ seg_off, int64_t* __restrict__ piece_off) {
+  __shared__ int64_t s_part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = ceil_div(total, (int64_t)blockDim.x);
+  const int64_t a = t * per, b = min(total, a + per);
+  int64_t sum = 0;
+  for (int64_t i = a; i < b; ++i) sum += counts[i];
+  s_part[t] = sum;
+  __syncthreads();
+  if (t == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int64_t v = s_part[i];
+      s_part[i] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  int64_t run = s_part[t];
+  for (int64_t i = a; i < b; ++i) {
+    const int64_t v = counts[i];
+    counts[i] = (int)run;
+    if (i % n_chunks == 0) seg_off[i / n_chunks] = run;
+    run += v;
+  }
+  __syncthreads();
+  if (t == 0) {
+    seg_off[nkeys] = R;
+    int64_t p = 0;
+    for (int j = 0; j < nkeys; ++j) {
+      piece_off[j] = p;
+      p += ceil_div(seg_off[j + 1] - seg_off[j], (int64_t)kPiece);
+    }
+    piece_off[nkeys] = p;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
+                      const int* __restrict__ base, int32_t* __restrict__ perm) {
+  extern __shared__ int s_ctr[];  // [kWarps][nkeys]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
+  if (chunk >= n_chunks) return;
+  int* ctr = s_ctr + warp * nkeys;
+  for (int j = lane; j < nkeys; j += 32) ctr[j] = base[(int64_t)j * n_chunks + chunk];
+  __syncwarp();
+  const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t g = r0; g < r1; g += 32) {
+    const int64_t r = g + lane;
+    const bool live = r < r1;
+    const int key = live ? __ldg(keys + r) : -1 - lane;  // dead lanes never match
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (live) {
+      const int rank = __popc(peers & lt);
+      perm[ctr[key] + rank] = (int32_t)r;
+    }
+    __syncwarp();
+    if (live && (peers & lt) == 0) ctr[key] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// piece sums: one CTA per piece, rows gathered through perm.
+__global__ void __launch_bounds__(kThreads)
+piece_sum_kernel(const float* __restrict__ vals, const int32_t* __restrict__ perm,
+                 const int64_t* __restrict__ seg_off, const int64_t* __restrict__ piece_off,
+                 int nkeys, int D, float* __restrict__ piece_out) {
+  extern __shared__ float s_acc[];
+  const int64_t piece = blockIdx.x;
+  if (piece >= piece_off[nkeys]) return;  // grid is sized for the worst case
+  // key of this piece: last j with piece_off[j] <= piece
+  int lo = 0, hi = nkeys;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (piece_off[mid] <= piece) lo = mid; else hi = mid;
+  }
+  const int key = lo;
+  const int64_t r0 = seg_off[key] + (piece - piece_off[key]) * kPiece;
+  const int64_t r1 = min(seg_off[key + 1], r0 + kPiece);
+  const int span = (D <= kThreads && kThreads % D == 0) ? D : kThreads;
+  const int sub = kThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  for (int d0 = 0; d0 < D; d0 += span) {
+    const int d = d0 + lc;
+    float acc = 0.f;
+    if (d < D)
+      for (int64_t r = r0 + lr; r < r1; r += sub)
+        acc += __ldg(vals + (int64_t)__ldg(perm + r) * D + d);
+    s_acc[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D) {
+      float a = 0.f;
+      for (int s = 0; s < sub; ++s) a += s_acc[s * span + threadIdx.x];
+      piece_out[piece * D + d0 + threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void key_sum_kernel(const float* __restrict__ piece_out,
+                               const int64_t* __restrict__ piece_off, int nkeys, int D,
+                               float* __restrict__ out) {
+  const int64_t total = (int64_t)nkeys * D;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int key = (int)(e / D), d = (int)(e % D);
+    float acc = 0.f;
+    for (int64_t p = piece_off[key]; p < piece_off[key + 1]; ++p) acc += piece_out[p * D + d];
+    out[e] = acc;
+  }
+}
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+}  // namespace
+}  // namespace accel
+
+using namespace accel;
+
+extern "C" int accel_prev_keys(const int32_t* tokens, int64_t N, int K, int A, int32_t* keys,
+                               void* stream) {
+  if (N < 0 || K < 1 || A < 1) return fail(kDimension, "prev_keys: bad sizes");
+  if (N == 0) return kOk;
+  const int64_t M = N * K;
+  const int grid = (int)std::min<int64_t>(ceil_div(M, kThreads), (int64_t)kNumSMs * 8);
+  prev_keys_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(tokens, M, K, A, keys);
+  return post_launch("prev_keys_kernel");
+}
+
+extern "C" int accel_step_keys(const int32_t* steps, const int32_t* frame_of, int64_t R,
+                               int n_steps, int32_t* keys, unsigned* bad_count, void* stream) {
+  if (R < 0 || n_steps < 1) return fail(kDimension, "step_keys: bad sizes");
+  if (R == 0) return kOk;
+  if (!steps || !keys || !bad_count) return fail(kDimension, "step_keys: NULL buffer");
+  const int grid = (int)std::min<int64_t>(ceil_div(R, kThreads), (int64_t)kNumSMs * 8);
+  step_keys_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(steps, frame_of, R, n_steps, keys,
+                                                             bad_count);
+  return post_launch("step_keys_kernel");
+}
+
+extern "C" size_t accel_group_workspace_size(int64_t R, int nkeys) {
+  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
+  return align16(sizeof(int) * (size_t)nkeys * n_chunks) + 16;
+}
+
+extern "C" int64_t accel_group_max_pieces(int64_t R, int nkeys) {
+  return ceil_div(R, kPiece) + nkeys;
+}
+
+// perm[R]: row ids sorted stably by key; seg_off[nkeys+1]; piece_off[nkeys+1]
+extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
+                                  int64_t* seg_off, int64_t* piece_off, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (R < 0 || nkeys < 1) return fail(kDimension, "group_by_key: bad sizes");
+  if (nkeys * (size_t)kWarps * sizeof(int) > 200 * 1024)
+    return fail(kDimension, "group_by_key: %d keys exceed the shared-memory histogram", nkeys);
+  if (!keys || !perm || !seg_off || !piece_off || !workspace)
+    return fail(kDimension, "group_by_key: NULL buffer");
+  if (workspace_bytes < accel_group_workspace_size(R, nkeys))
+    return fail(kDimension, "group_by_key: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
+  int* counts = static_cast<int*>(workspace);
+  const size_t smem = sizeof(int) * (size_t)nkeys * kWarps;
+  const int grid = (int)ceil_div(n_chunks, kWarps);
+  int st;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(chunk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(stable_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  }
+  chunk_hist_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, counts);
+  if ((st = post_launch("chunk_hist_kernel"))) return st;
+  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, (int64_t)nkeys * n_chunks, nkeys, n_chunks, R,
+                                        seg_off, piece_off);
+  if ((st = post_launch("scan_counts_kernel"))) return st;
+  if (R == 0) return kOk;
+  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, counts, perm);
+  return post_launch("stable_scatter_kernel");
+}
+
+// out[nkeys, D] = grouped sums of vals[R, D] rows; piece_buf holds
+// accel_group_max_pieces(R, nkeys) * D floats.
+extern "C" int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
+                                      const int64_t* seg_off, const int64_t* piece_off,
+                                      int nkeys, int64_t n_pieces, float* piece_buf, float* out,
+                                      void* stream) {
+  if (R < 0 || D < 1 || nkeys < 1 || n_pieces < 0) return fail(kDimension, "grouped_rows_sum: bad sizes");
+  if (!vals || !perm || !seg_off || !piece_off || !piece_buf || !out)
+    return fail(kDimension, "grouped_rows_sum: NULL buffer");
+  cudaStream_t s = as_stream(stream);
+  int st;
+  if (n_pieces > 0) {
+    piece_sum_kernel<<<(unsigned)n_pieces, kThreads, kThreads * sizeof(float), s>>>(
+        vals, perm, seg_off, piece_off, nkeys, D, piece_buf);
+    if ((st = post_launch("piece_sum_kernel"))) return st;
+  }
+  const int64_t total = (int64_t)nkeys * D;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, kThreads), (int64_t)kNumSMs * 4);
+  key_sum_kernel<<<grid, kThreads, 0, s>>>(piece_buf, piece_off, nkeys, D, out);
+  return post_launch("key_sum_kernel");
+}

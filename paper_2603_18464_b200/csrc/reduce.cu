@@ -1,0 +1,274 @@
+// Fixed-order reductions of per-CTA partials, the step's scalar record, and
+// the Adam update.
+//
+//   reduce_segments  dst[j] = sum_p src[p][j] for up to 16 (src, dst) pairs
+//                    in one launch (bias/embedding gradients, value-head
+//                    parameter gradients) — float64 accumulation, p order.
+//   reduce_f64       sum or max over double partial records.
+//   step_finalize    the train_step record (trainer.py:417-464): policy loss
+//                    = -sum/m, entropy mean, value MSE, total_loss (:254-256),
+//                    ratio/trust/clip diagnostics, and the device-side skip
+//                    flag (dropped batch :420-424, non-finite logits or
+//                    attention -> DomainError, non-finite grads -> NonFiniteError).
+//   adam             bias-corrected Adam (numerics.py:95-126) over one flat
+//                    fp32 buffer holding two parameter groups (policy, value),
+//                    ping-pong (reads *_in, writes *_out) so a rejected update
+//                    leaves the live parameters untouched; float64 math.
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace accel {
+namespace {
+
+constexpr int kMaxSegs = 16;
+
+struct Segs {
+  const float* src[kMaxSegs];
+  float* dst[kMaxSegs];
+  int64_t parts[kMaxSegs];
+  int64_t len[kMaxSegs];
+  int64_t pitch[kMaxSegs];
+};
+
+__global__ void reduce_segments_kernel(Segs s) {
+  const int seg = blockIdx.y;
+  const int64_t len = s.len[seg], parts = s.parts[seg], pitch = s.pitch[seg];
+  const float* src = s.src[seg];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t p = 0; p < parts; ++p) acc += (double)src[p * pitch + j];
+    s.dst[seg][j] = (float)acc;
+  }
+}
+
+// moments[s] = {sum x, sum x^2, count} of x[off[s]:off[s+1]] (float64, fixed order)
+__global__ void __launch_bounds__(256)
+segment_moments_kernel(const float* __restrict__ x, const int64_t* __restrict__ off,
+                       double* __restrict__ out) {
+  __shared__ double s_red[8 * 2];
+  const int64_t a = off[blockIdx.x], b = off[blockIdx.x + 1];
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+    const double y = x[i];
+    v[0] += y;
+    v[1] = fma(y, y, v[1]);
+  }
+  block_sum_d<2>(v, s_red);
+  if (threadIdx.x == 0) {
+    out[3 * blockIdx.x] = v[0];
+    out[3 * blockIdx.x + 1] = v[1];
+    out[3 * blockIdx.x + 2] = (double)(b - a);
+  }
+}
+
+// count of rows r (row index rows[r] of x[*, C]) holding a non-finite value
+__global__ void count_nonfinite_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows,
+                                            int64_t R, int C, unsigned* __restrict__ count) {
+  unsigned c = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
+    const int64_t f = rows ? __ldg(rows + r) : r;
+    bool bad = false;
+    for (int j = lane; j < C; j += 32) bad |= !isfinite(__ldg(x + f * C + j));
+    c += __any_sync(0xffffffffu, bad) && lane == 0;
+  }
+  if (c) atomicAdd(count, c);
+}
+
+__global__ void __launch_bounds__(1024)
+reduce_f64_kernel(const double* __restrict__ part, int64_t parts, int width, int mode,
+                  double* __restrict__ out) {
+  __shared__ double s[1024];
+  for (int c = 0; c < width; ++c) {
+    double acc = mode ? -CUDART_INF : 0.0;
+    for (int64_t p = threadIdx.x; p < parts; p += blockDim.x) {
+      const double v = part[p * width + c];
+      acc = mode ? fmax(acc, v) : acc + v;
+    }
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o)
+        s[threadIdx.x] = mode ? fmax(s[threadIdx.x], s[threadIdx.x + o])
+                              : s[threadIdx.x] + s[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = s[0];
+    __syncthreads();
+  }
+}
+
+struct FinalizeParams {
+  int algo;
+  double lambda_v, lambda_h, n_tokens, n_transitions;
+};
+
+// loss_sums: token_loss kStat layout; loss_max: [ratio_max, -w_min];
+// value_sums: [sum err^2, non-finite v]; bad_counts: [attn, steps, grads]
+__global__ void step_finalize_kernel(const double* __restrict__ ls, const double* __restrict__ lm,
+                                     const double* __restrict__ vs,
+                                     const unsigned* __restrict__ bad_counts,
+                                     const double* __restrict__ attn_bad, FinalizeParams p,
+                                     double* __restrict__ rec, int* __restrict__ skip) {
+  const double excluded = ls[5];
+  const double m = p.n_tokens - excluded;
+  const bool dropped = !(m > 0.0);
+  const double policy_loss = dropped ? 0.0 : -ls[0] / m;
+  const double entropy = ls[1] / p.n_tokens;
+  const double value_loss = vs[0] / p.n_transitions;
+  rec[0] = policy_loss + p.lambda_v * value_loss - p.lambda_h * entropy;
+  rec[1] = policy_loss;
+  rec[2] = value_loss;
+  rec[3] = entropy;
+  rec[4] = excluded;
+  rec[5] = dropped ? 0.0 : ls[2] / m;                 // ratio_mean
+  rec[6] = lm[0];                                     // ratio_max
+  rec[7] = dropped ? 0.0 : ls[3] / m;                 // trust_weight_mean
+  rec[8] = -lm[1];                                    // trust_weight_min
+  rec[9] = dropped ? 0.0 : ls[4] / m;                 // clipped_fraction
+  rec[10] = dropped ? 1.0 : 0.0;
+  rec[11] = ls[6];                                    // rows with non-finite logits
+  rec[12] = ls[7];                                    // tokens outside [0, A)
+  rec[13] = attn_bad[0];                              // non-finite attention scores
+  rec[14] = (double)bad_counts[0];                    // non-finite gradients
+  rec[15] = attn_bad[1] + (double)bad_counts[1];      // step index out of range
+  const bool s = dropped || ls[6] > 0 || ls[7] > 0 || attn_bad[0] > 0 || rec[15] > 0 ||
+                 bad_counts[0] > 0;
+  rec[16] = s ? 1.0 : 0.0;
+  *skip = s ? 1 : 0;
+}
+
+__global__ void count_nonfinite_kernel(const float* __restrict__ x, int64_t n,
+                                       unsigned* __restrict__ count) {
+  unsigned c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += !isfinite(x[i]);
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+struct AdamGroup {
+  double lr, beta1, beta2, eps, bc1, bc2;  // bc = 1 - beta^t
+};
+
+__global__ void adam_kernel(const float* __restrict__ p_in, const float* __restrict__ g,
+                            const float* __restrict__ m_in, const float* __restrict__ v_in,
+                            float* __restrict__ p_out, float* __restrict__ m_out,
+                            float* __restrict__ v_out, int64_t n, int64_t n0, AdamGroup g0,
+                            AdamGroup g1, const int* __restrict__ skip,
+                            unsigned* __restrict__ bad) {
+  if (*skip) return;
+  unsigned nb = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const AdamGroup& G = i < n0 ? g0 : g1;
+    const double gr = g[i];
+    const double m = G.beta1 * (double)m_in[i] + (1.0 - G.beta1) * gr;
+    const double v = G.beta2 * (double)v_in[i] + (1.0 - G.beta2) * gr * gr;
+    const double mh = m / G.bc1, vh = v / G.bc2;
+    const double w = (double)p_in[i] - G.lr * mh / (sqrt(vh) + G.eps);
+    p_out[i] = (float)w;
+    m_out[i] = (float)m;
+    v_out[i] = (float)v;
+    nb += !isfinite((float)w);
+  }
+  nb = __reduce_add_sync(0xffffffffu, nb);
+  if ((threadIdx.x & 31) == 0 && nb) atomicAdd(bad, nb);
+}
+
+}  // namespace
+}  // namespace accel
+
+using namespace accel;
+
+extern "C" int accel_reduce_segments(const void* const* srcs, void* const* dsts,
+                                     const int64_t* parts, const int64_t* lens,
+                                     const int64_t* pitches, int nseg, void* stream) {
+  if (nseg < 0 || nseg > kMaxSegs) return fail(kDimension, "reduce_segments: 0..16 segments");
+  if (nseg == 0) return kOk;
+  Segs s{};
+  int64_t maxlen = 1;
+  for (int i = 0; i < nseg; ++i) {
+    if (!srcs[i] || !dsts[i] || parts[i] < 0 || lens[i] < 0)
+      return fail(kDimension, "reduce_segments: bad segment %d", i);
+    s.src[i] = static_cast<const float*>(srcs[i]);
+    s.dst[i] = static_cast<float*>(dsts[i]);
+    s.parts[i] = parts[i];
+    s.len[i] = lens[i];
+    s.pitch[i] = pitches ? pitches[i] : lens[i];
+    if (s.pitch[i] < lens[i]) return fail(kDimension, "reduce_segments: pitch < len");
+    maxlen = std::max(maxlen, lens[i]);
+  }
+  dim3 grid((unsigned)std::min<int64_t>(ceil_div(maxlen, 256), 64), (unsigned)nseg);
+  reduce_segments_kernel<<<grid, 256, 0, as_stream(stream)>>>(s);
+  return post_launch("reduce_segments_kernel");
+}
+
+extern "C" int accel_reduce_f64(const double* part, int64_t parts, int width, int mode,
+                                double* out, void* stream) {
+  if (parts < 0 || width < 1 || (mode != 0 && mode != 1))
+    return fail(kDimension, "reduce_f64: bad arguments");
+  if (!part || !out) return fail(kDimension, "reduce_f64: NULL buffer");
+  reduce_f64_kernel<<<1, 1024, 0, as_stream(stream)>>>(part, parts, width, mode, out);
+  return post_launch("reduce_f64_kernel");
+}
+
+extern "C" int accel_step_finalize(const double* loss_sums, const double* loss_max,
+                                   const double* value_sums, const unsigned* bad_counts,
+                                   const double* attn_bad, int algo, double lambda_v,
+                                   double lambda_h, double n_tokens, double n_transitions,
+                                   double* record, int* skip, void* stream) {
+  if (!loss_sums || !loss_max || !value_sums || !bad_counts || !attn_bad || !record || !skip)
+    return fail(kDimension, "step_finalize: NULL buffer");
+  FinalizeParams p{algo, lambda_v, lambda_h, n_tokens, n_transitions};
+  step_finalize_kernel<<<1, 1, 0, as_stream(stream)>>>(loss_sums, loss_max, value_sums,
+                                                       bad_counts, attn_bad, p, record, skip);
+  return post_launch("step_finalize_kernel");
+}
+
+extern "C" int accel_count_nonfinite(const float* x, int64_t n, unsigned* count, void* stream) {
+  if (n < 0 || !count) return fail(kDimension, "count_nonfinite: bad arguments");
+  if (n == 0) return kOk;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 4);
+  count_nonfinite_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, n, count);
+  return post_launch("count_nonfinite_kernel");
+}
+
+extern "C" int accel_adam(const float* p_in, const float* g, const float* m_in, const float* v_in,
+                          float* p_out, float* m_out, float* v_out, int64_t n, int64_t n0,
+                          const double* group0, const double* group1, const int* skip,
+                          unsigned* bad, void* stream) {
+  if (n < 0 || n0 < 0 || n0 > n) return fail(kDimension, "adam: bad sizes");
+  if (!group0 || !group1 || !skip || !bad) return fail(kDimension, "adam: NULL buffer");
+  AdamGroup a{group0[0], group0[1], group0[2], group0[3], group0[4], group0[5]};
+  AdamGroup b{group1[0], group1[1], group1[2], group1[3], group1[4], group1[5]};
+  for (const AdamGroup* G : {&a, &b}) {
+    if (!(G->bc1 > 0 && G->bc2 > 0)) return fail(kDomain, "adam: bias correction must be > 0");
+  }
+  if (n == 0) return kOk;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 4);
+  adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(p_in, g, m_in, v_in, p_out, m_out, v_out, n,
+                                                   n0, a, b, skip, bad);
+  return post_launch("adam_kernel");
+}
+
+extern "C" int accel_segment_moments(const float* x, const int64_t* off, int64_t nseg,
+                                     double* out, void* stream) {
+  if (nseg < 0 || !x || !off || !out) return fail(kDimension, "segment_moments: bad arguments");
+  if (nseg == 0) return kOk;
+  segment_moments_kernel<<<(unsigned)nseg, 256, 0, as_stream(stream)>>>(x, off, out);
+  return post_launch("segment_moments_kernel");
+}
+
+extern "C" int accel_count_nonfinite_rows(const float* x, const int32_t* rows, int64_t R, int C,
+                                          unsigned* count, void* stream) {
+  if (R < 0 || C < 1 || !x || !count) return fail(kDimension, "count_nonfinite_rows: bad arguments");
+  if (R == 0) return kOk;
+  const int grid = (int)std::min<int64_t>(ceil_div(R, 8), (int64_t)kNumSMs * 8);
+  count_nonfinite_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, rows, R, C, count);
+  return post_launch("count_nonfinite_rows_kernel");
+}

@@ -1,0 +1,294 @@
+// Value head: attention pooling over detached (h1, h2), step embedding,
+// tanh MLP to a scalar; MSE loss and its backward.
+//
+// Reference: ValueHead.forward_batch (models.py:273-290), backward_batch
+// (models.py:292-314), value loss in train_step (trainer.py:438-443), and
+// revaluation `state_values_batch` (models.py:411-415, trainer.py:352-356).
+// The two GEMMs u@W0v^T and dzm^T@u / dzm@W0v are library GEMMs; the
+// row-wise parts are here:
+//   value_pool        e_j = h_j.w_attn + b, alpha = softmax(e), u = sum_j alpha_j h_j + e_step[t]
+//   value_head        m = tanh(z + b0v), v = w1v.m + b1v; err, dv = lambda_v 2 err / N;
+//                     dzm = dv w1v (1 - m^2); partial sums for dw1v, db0v, db1v, sum err^2
+//   value_attn_grad   dalpha_j = du.h_j; de = alpha (dalpha - sum alpha dalpha)
+//   value_attn_wgrad  dw_attn = sum_i sum_j de_ij h_ij (column layout)
+// Rows may be transitions (row_frame maps them to frame rows of h1/h2/steps)
+// or frames (row_frame == NULL).
+#include "common.cuh"
+
+namespace accel {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxHPL = 4;  // mlp_hidden <= 128
+
+__global__ void __launch_bounds__(kThreads)
+value_pool_kernel(const float* __restrict__ h1, const float* __restrict__ h2,
+                  const int32_t* __restrict__ row_frame, const int32_t* __restrict__ steps,
+                  int64_t R, int D, int n_steps, const float* __restrict__ w_attn,
+                  const float* __restrict__ b_attn, const float* __restrict__ e_step,
+                  float* __restrict__ U, float* __restrict__ alpha, double* __restrict__ bad_part) {
+  __shared__ double s_bad[kWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float b = __ldg(b_attn);
+  double bad_attn = 0.0, bad_step = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  for (int64_t r = (int64_t)blockIdx.x * kWarps + warp; r < R; r += stride) {
+    const int64_t f = row_frame ? __ldg(row_frame + r) : r;
+    const float* a = h1 + f * D;
+    const float* c = h2 + f * D;
+    float e0 = 0.f, e1 = 0.f;
+    for (int d = lane; d < D; d += 32) {
+      const float w = __ldg(w_attn + d);
+      e0 = fmaf(__ldg(a + d), w, e0);
+      e1 = fmaf(__ldg(c + d), w, e1);
+    }
+    e0 = warp_sum(e0) + b;
+    e1 = warp_sum(e1) + b;
+    const bool bad = !isfinite(e0) || !isfinite(e1);
+    const float mx = fmaxf(e0, e1);
+    const float x0 = __expf(e0 - mx), x1 = __expf(e1 - mx);
+    const float inv = 1.f / (x0 + x1);
+    const float a0 = x0 * inv, a1 = x1 * inv;
+    int st = __ldg(steps + f);
+    const bool bst = st < 0 || st >= n_steps;
+    st = min(max(st, 0), n_steps - 1);
+    const float* es = e_step + (int64_t)st * D;
+    float* u = U + r * D;
+    for (int d = lane; d < D; d += 32) u[d] = fmaf(a0, __ldg(a + d), fmaf(a1, __ldg(c + d), __ldg(es + d)));
+    if (lane == 0) {
+      alpha[2 * r] = a0;
+      alpha[2 * r + 1] = a1;
+    }
+    bad_attn += bad;
+    bad_step += bst;
+  }
+  if (lane == 0) {
+    s_bad[warp][0] = bad_attn;
+    s_bad[warp][1] = bad_step;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < kWarps; ++w) {
+      x += s_bad[w][0];
+      y += s_bad[w][1];
+    }
+    bad_part[2 * (int64_t)blockIdx.x] = x;
+    bad_part[2 * (int64_t)blockIdx.x + 1] = y;
+  }
+}
+
+// part layout per block: [dw1v (H) | db0v (H) | db1v (1)]; dpart: [sum err^2, non-finite v]
+__global__ void __launch_bounds__(kThreads)
+value_head_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
+                  const float* __restrict__ w1v, const float* __restrict__ b1v, int64_t R, int H,
+                  const float* __restrict__ targets, float lambda_v, double inv_n,
+                  float* __restrict__ values_out, float* __restrict__ part,
+                  double* __restrict__ dpart) {
+  __shared__ float s_part[kWarps][2 * 32 * kMaxHPL + 1];
+  __shared__ double s_err[kWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float bias1 = __ldg(b1v);
+  float bz[kMaxHPL], w1[kMaxHPL], gw1[kMaxHPL], gb0[kMaxHPL];
+#pragma unroll
+  for (int j = 0; j < kMaxHPL; ++j) {
+    const int h = lane + 32 * j;
+    bz[j] = h < H ? __ldg(b0v + h) : 0.f;
+    w1[j] = h < H ? __ldg(w1v + h) : 0.f;
+    gw1[j] = 0.f;
+    gb0[j] = 0.f;
+  }
+  float gb1 = 0.f;
+  double err2 = 0.0, bad = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  for (int64_t r = (int64_t)blockIdx.x * kWarps + warp; r < R; r += stride) {
+    float m[kMaxHPL];
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxHPL; ++j) {
+      const int h = lane + 32 * j;
+      m[j] = h < H ? tanhf(zm[r * H + h] + bz[j]) : 0.f;
+      acc = fmaf(w1[j], m[j], acc);
+    }
+    const float v = warp_sum(acc) + bias1;
+    if (values_out && lane == 0) values_out[r] = v;
+    if (targets) {
+      const float err = v - __ldg(targets + r);
+      const float dv = (float)((double)lambda_v * 2.0 * (double)err * inv_n);
+      err2 += (double)err * (double)err;
+      bad += !isfinite(v);
+      gb1 += dv;
+#pragma unroll
+      for (int j = 0; j < kMaxHPL; ++j) {
+        const int h = lane + 32 * j;
+        if (h < H) {
+          const float g = dv * w1[j] * (1.f - m[j] * m[j]);
+          zm[r * H + h] = g;
+          gw1[j] = fmaf(dv, m[j], gw1[j]);
+          gb0[j] += g;
+        }
+      }
+    }
+  }
+  if (!targets) return;
+#pragma unroll
+  for (int j = 0; j < kMaxHPL; ++j) {
+    s_part[warp][lane + 32 * j] = gw1[j];
+    s_part[warp][32 * kMaxHPL + lane + 32 * j] = gb0[j];
+  }
+  if (lane == 0) {
+    s_part[warp][2 * 32 * kMaxHPL] = gb1;
+    s_err[warp][0] = err2;
+    s_err[warp][1] = bad;
+  }
+  __syncthreads();
+  float* out = part + (int64_t)blockIdx.x * (2 * H + 1);
+  for (int e = threadIdx.x; e < 2 * H + 1; e += kThreads) {
+    int src;
+    if (e < H) src = e;
+    else if (e < 2 * H) src = 32 * kMaxHPL + (e - H);
+    else src = 2 * 32 * kMaxHPL;
+    float a = 0.f;
+    for (int w = 0; w < kWarps; ++w) a += s_part[w][src];
+    out[e] = a;
+  }
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < kWarps; ++w) {
+      x += s_err[w][0];
+      y += s_err[w][1];
+    }
+    dpart[2 * (int64_t)blockIdx.x] = x;
+    dpart[2 * (int64_t)blockIdx.x + 1] = y;
+  }
+}
+
+// de[r] = alpha * (dalpha - sum alpha dalpha); part[blk] = sum of de over rows (db_attn)
+__global__ void __launch_bounds__(kThreads)
+value_attn_grad_kernel(const float* __restrict__ dU, const float* __restrict__ h1,
+                       const float* __restrict__ h2, const int32_t* __restrict__ row_frame,
+                       const float* __restrict__ alpha, int64_t R, int D, float* __restrict__ de,
+                       float* __restrict__ part) {
+  __shared__ float s_b[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float gb = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  for (int64_t r = (int64_t)blockIdx.x * kWarps + warp; r < R; r += stride) {
+    const int64_t f = row_frame ? __ldg(row_frame + r) : r;
+    const float* du = dU + r * D;
+    float d0 = 0.f, d1 = 0.f;
+    for (int d = lane; d < D; d += 32) {
+      const float g = __ldg(du + d);
+      d0 = fmaf(g, __ldg(h1 + f * D + d), d0);
+      d1 = fmaf(g, __ldg(h2 + f * D + d), d1);
+    }
+    d0 = warp_sum(d0);
+    d1 = warp_sum(d1);
+    const float a0 = __ldg(alpha + 2 * r), a1 = __ldg(alpha + 2 * r + 1);
+    const float s = a0 * d0 + a1 * d1;
+    const float e0 = a0 * (d0 - s), e1 = a1 * (d1 - s);
+    if (lane == 0) {
+      de[2 * r] = e0;
+      de[2 * r + 1] = e1;
+    }
+    gb += e0 + e1;
+  }
+  if (lane == 0) s_b[warp] = gb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f;
+    for (int w = 0; w < kWarps; ++w) a += s_b[w];
+    part[blockIdx.x] = a;
+  }
+}
+
+// part[blk][d] = sum over the block's rows of de0 h1[f, d] + de1 h2[f, d]
+__global__ void __launch_bounds__(kThreads)
+value_attn_wgrad_kernel(const float* __restrict__ de, const float* __restrict__ h1,
+                        const float* __restrict__ h2, const int32_t* __restrict__ row_frame,
+                        int64_t R, int D, float* __restrict__ part) {
+  extern __shared__ float s_acc[];
+  const int span = (D <= kThreads && kThreads % D == 0) ? D : kThreads;
+  const int sub = kThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  const int64_t per = ceil_div(R, (int64_t)gridDim.x);
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(R, r0 + per);
+  for (int d0 = 0; d0 < D; d0 += span) {
+    const int d = d0 + lc;
+    float acc = 0.f;
+    if (d < D)
+      for (int64_t r = r0 + lr; r < r1; r += sub) {
+        const int64_t f = row_frame ? __ldg(row_frame + r) : r;
+        acc = fmaf(__ldg(de + 2 * r), __ldg(h1 + f * D + d),
+                   fmaf(__ldg(de + 2 * r + 1), __ldg(h2 + f * D + d), acc));
+      }
+    s_acc[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D) {
+      float a = 0.f;
+      for (int s = 0; s < sub; ++s) a += s_acc[s * span + threadIdx.x];
+      part[(int64_t)blockIdx.x * D + d0 + threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+}
+
+int warp_grid(int64_t rows) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, kWarps), (int64_t)kNumSMs * 8));
+}
+
+}  // namespace
+}  // namespace accel
+
+using namespace accel;
+
+extern "C" int accel_warp_grid(int64_t rows) { return warp_grid(rows); }
+
+extern "C" int accel_value_pool(const float* h1, const float* h2, const int32_t* row_frame,
+                                const int32_t* steps, int64_t R, int D, int n_steps,
+                                const float* w_attn, const float* b_attn, const float* e_step,
+                                float* U, float* alpha, double* bad_part, int grid, void* stream) {
+  if (R < 0 || D < 1 || n_steps < 1 || grid < 1) return fail(kDimension, "value_pool: bad sizes");
+  if (R == 0) return kOk;
+  if (!h1 || !h2 || !steps || !w_attn || !b_attn || !e_step || !U || !alpha || !bad_part)
+    return fail(kDimension, "value_pool: NULL buffer");
+  value_pool_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(
+      h1, h2, row_frame, steps, R, D, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part);
+  return post_launch("value_pool_kernel");
+}
+
+extern "C" int accel_value_head(float* zm, const float* b0v, const float* w1v, const float* b1v,
+                                int64_t R, int H, const float* targets, double lambda_v,
+                                double n_global, float* values_out, float* part, double* dpart,
+                                int grid, void* stream) {
+  if (R < 0 || H < 1 || grid < 1) return fail(kDimension, "value_head: bad sizes");
+  if (H > 32 * kMaxHPL) return fail(kDimension, "value mlp_hidden=%d exceeds %d", H, 32 * kMaxHPL);
+  if (R == 0) return kOk;
+  if (!zm || !b0v || !w1v || !b1v || (targets && (!part || !dpart)))
+    return fail(kDimension, "value_head: NULL buffer");
+  value_head_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(
+      zm, b0v, w1v, b1v, R, H, targets, (float)lambda_v, n_global > 0 ? 1.0 / n_global : 0.0,
+      values_out, part, dpart);
+  return post_launch("value_head_kernel");
+}
+
+extern "C" int accel_value_attn_grad(const float* dU, const float* h1, const float* h2,
+                                     const int32_t* row_frame, const float* alpha, int64_t R,
+                                     int D, float* de, float* part, int grid, void* stream) {
+  if (R < 0 || D < 1 || grid < 1) return fail(kDimension, "value_attn_grad: bad sizes");
+  if (R == 0) return kOk;
+  value_attn_grad_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(dU, h1, h2, row_frame, alpha,
+                                                                   R, D, de, part);
+  return post_launch("value_attn_grad_kernel");
+}
+
+extern "C" int accel_value_attn_wgrad(const float* de, const float* h1, const float* h2,
+                                      const int32_t* row_frame, int64_t R, int D, float* part,
+                                      int grid, void* stream) {
+  if (R < 0 || D < 1 || grid < 1) return fail(kDimension, "value_attn_wgrad: bad sizes");
+  if (R == 0) return kOk;
+  value_attn_wgrad_kernel<<<grid, kThreads, kThreads * sizeof(float), as_stream(stream)>>>(
+      de, h1, h2, row_frame, R, D, part);
+  return post_launch("value_attn_wgrad_kernel");
+}

@@ -95,3 +95,189 @@ def normalize_apply(adv, stats, out=None):
     out = torch.empty_like(adv) if out is None else out
     _lib.call("accel_normalize_apply", _p(adv), adv.numel(), _p(stats), _p(out), _stream())
     return out
+
+
+# ---------------------------------------------------------------------------
+# (b) token loss
+
+
+def token_grid(M: int) -> int:
+    return int(_lib.lib().accel_token_grid(int(M)))
+
+
+def token_logp(mu, tokens, lp_out=None, bad_part=None):
+    """Behavior log-probs (trainer.py:289-293); mu f32[M, A], tokens i32[M]."""
+    M, A = mu.shape
+    _check(mu, "mu", F32)
+    _check(tokens, "tokens", I32)
+    if tokens.numel() != M:
+        raise DimensionError(f"tokens has {tokens.numel()} entries, expected {M}")
+    lp_out = torch.empty(M, dtype=F32, device=mu.device) if lp_out is None else lp_out
+    g = token_grid(M)
+    bad_part = torch.empty(g, 2, dtype=F64, device=mu.device) if bad_part is None else bad_part
+    _lib.call("accel_token_logp", _p(mu), _p(tokens), M, A, _p(lp_out), _p(bad_part), _stream())
+    return lp_out, bad_part
+
+
+def token_loss(logits, bias, tokens, lp_old, adv, K, algo, sigma, clip_eps, lambda_h, m_global,
+               dlogits, lp_new, dbias_part, stat_part, max_part, fix_stats=None):
+    """Fused GIPO/PPO + entropy forward/backward (see accel.h)."""
+    M, A = logits.shape
+    _lib.call("accel_token_loss", _p(logits), _p(bias), _p(tokens), _p(lp_old), _p(adv), M, int(K),
+              A, int(algo), float(sigma), float(clip_eps), float(lambda_h), float(m_global),
+              _p(fix_stats), _p(dlogits), _p(lp_new), _p(dbias_part), _p(stat_part),
+              _p(max_part), _stream())
+
+
+# ---------------------------------------------------------------------------
+# policy glue
+
+
+def bias_tanh(z, b):
+    _lib.call("accel_bias_tanh", _p(z), _p(b), z.shape[0], z.shape[1], _stream())
+    return z
+
+
+def build_c(h2, frame_of, tokens, e_prev, e_pos, N, K, A, out):
+    _lib.call("accel_build_c", _p(h2), _p(frame_of), _p(tokens), _p(e_prev), _p(e_pos), N, K, A,
+              h2.shape[1], _p(out), _stream())
+    return out
+
+
+def rows_grid(rows: int) -> int:
+    return int(_lib.lib().accel_rows_grid(int(rows)))
+
+
+def warp_grid(rows: int) -> int:
+    return int(_lib.lib().accel_warp_grid(int(rows)))
+
+
+def dc_reduce(dc, h2, frame_of, N, K, D, dz2, pos_part, db1_part, grid):
+    _lib.call("accel_dc_reduce", _p(dc), _p(h2), _p(frame_of), N, K, D, _p(dz2), _p(pos_part),
+              _p(db1_part), int(grid), _stream())
+
+
+def tanh_grad_colsum(g, h, col_part, grid):
+    _lib.call("accel_tanh_grad_colsum", _p(g), _p(h), g.shape[0], g.shape[1], _p(col_part),
+              int(grid), _stream())
+
+
+# ---------------------------------------------------------------------------
+# deterministic grouping (np.add.at)
+
+
+class Grouping:
+    """A stable counting sort of R keys in [0, nkeys) (fixed per batch)."""
+
+    def __init__(self, keys, nkeys: int):
+        R = keys.numel()
+        dev = keys.device
+        self.R, self.nkeys = R, int(nkeys)
+        self.perm = torch.empty(max(R, 1), dtype=I32, device=dev)
+        self.seg_off = torch.empty(nkeys + 1, dtype=I64, device=dev)
+        self.piece_off = torch.empty(nkeys + 1, dtype=I64, device=dev)
+        self.max_pieces = int(_lib.lib().accel_group_max_pieces(R, nkeys))
+        nbytes = _lib.lib().accel_group_workspace_size(R, nkeys)
+        buf = workspace("group").get(nbytes)
+        _lib.call("accel_group_by_key", _p(keys), R, nkeys, _p(self.perm), _p(self.seg_off),
+                  _p(self.piece_off), _p(buf), buf.numel(), _stream())
+
+    def rows_sum(self, vals, out, piece_buf=None):
+        D = vals.shape[1]
+        if piece_buf is None:
+            piece_buf = workspace("group_pieces_f32").get(4 * max(self.max_pieces, 1) * D)
+        _lib.call("accel_grouped_rows_sum", _p(vals), self.R, D, _p(self.perm), _p(self.seg_off),
+                  _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
+                  _stream())
+        return out
+
+
+def prev_keys(tokens, N, K, A, out=None):
+    out = torch.empty(N * K, dtype=I32, device=tokens.device) if out is None else out
+    _lib.call("accel_prev_keys", _p(tokens), N, K, A, _p(out), _stream())
+    return out
+
+
+def step_keys(steps, frame_of, R, n_steps, bad_count, out=None):
+    out = torch.empty(R, dtype=I32, device=steps.device) if out is None else out
+    _lib.call("accel_step_keys", _p(steps), _p(frame_of), R, int(n_steps), _p(out), _p(bad_count),
+              _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# value head
+
+
+def value_pool(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part,
+               grid):
+    _lib.call("accel_value_pool", _p(h1), _p(h2), _p(row_frame), _p(steps), R, h1.shape[1],
+              int(n_steps), _p(w_attn), _p(b_attn), _p(e_step), _p(U), _p(alpha), _p(bad_part),
+              int(grid), _stream())
+
+
+def value_head(zm, b0v, w1v, b1v, targets, lambda_v, n_global, values_out, part, dpart, grid):
+    _lib.call("accel_value_head", _p(zm), _p(b0v), _p(w1v), _p(b1v), zm.shape[0], zm.shape[1],
+              _p(targets), float(lambda_v), float(n_global), _p(values_out), _p(part), _p(dpart),
+              int(grid), _stream())
+
+
+def value_attn_grad(dU, h1, h2, row_frame, alpha, de, part, grid):
+    _lib.call("accel_value_attn_grad", _p(dU), _p(h1), _p(h2), _p(row_frame), _p(alpha),
+              dU.shape[0], dU.shape[1], _p(de), _p(part), int(grid), _stream())
+
+
+def value_attn_wgrad(de, h1, h2, row_frame, R, part, grid):
+    _lib.call("accel_value_attn_wgrad", _p(de), _p(h1), _p(h2), _p(row_frame), R, h1.shape[1],
+              _p(part), int(grid), _stream())
+
+
+# ---------------------------------------------------------------------------
+# reductions / record / optimizer
+
+
+def reduce_segments(segs):
+    """segs: list of (src_tensor, dst_tensor, parts, len, pitch) (<= 16)."""
+    n = len(segs)
+    if n == 0:
+        return
+    srcs = (ctypes.c_void_p * n)(*[s[0].data_ptr() for s in segs])
+    dsts = (ctypes.c_void_p * n)(*[s[1].data_ptr() for s in segs])
+    parts = (ctypes.c_int64 * n)(*[int(s[2]) for s in segs])
+    lens = (ctypes.c_int64 * n)(*[int(s[3]) for s in segs])
+    pitches = (ctypes.c_int64 * n)(*[int(s[4]) for s in segs])
+    _lib.call("accel_reduce_segments", srcs, dsts, parts, lens, pitches, n, _stream())
+
+
+def reduce_f64(part, parts, width, mode, out):
+    _lib.call("accel_reduce_f64", _p(part), int(parts), int(width), int(mode), _p(out), _stream())
+    return out
+
+
+def segment_moments(x, off, out=None):
+    n = off.numel() - 1
+    out = torch.empty(n, 3, dtype=F64, device=x.device) if out is None else out
+    _lib.call("accel_segment_moments", _p(x), _p(off), n, _p(out), _stream())
+    return out
+
+
+def count_nonfinite_rows(x, rows, R, count):
+    _lib.call("accel_count_nonfinite_rows", _p(x), _p(rows), int(R), x.shape[1], _p(count),
+              _stream())
+
+
+def count_nonfinite(x, count):
+    _lib.call("accel_count_nonfinite", _p(x), x.numel(), _p(count), _stream())
+
+
+def step_finalize(loss_sums, loss_max, value_sums, bad_counts, attn_bad, algo, lambda_v, lambda_h,
+                  n_tokens, n_transitions, record, skip):
+    _lib.call("accel_step_finalize", _p(loss_sums), _p(loss_max), _p(value_sums), _p(bad_counts),
+              _p(attn_bad), int(algo), float(lambda_v), float(lambda_h), float(n_tokens),
+              float(n_transitions), _p(record), _p(skip), _stream())
+
+
+def adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, group0, group1, skip, bad):
+    n = p_in.numel()
+    _lib.call("accel_adam", _p(p_in), _p(g), _p(m_in), _p(v_in), _p(p_out), _p(m_out), _p(v_out),
+              n, int(n0), _p(group0), _p(group1), _p(skip), _p(bad), _stream())

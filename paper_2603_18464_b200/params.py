@@ -1,0 +1,156 @@
+"""Device-resident parameters, gradients and Adam moments in one flat buffer.
+
+Layout (fp32, each tensor 16-byte aligned): the policy tensors of the
+reference `PolicyModel` (models.py:103-109) followed by the `ValueHead`
+tensors (models.py:247-255).  One flat buffer lets a single kernel run Adam
+over both parameter groups (two step counters, as the reference keeps two
+`AdamState`s, trainer.py:312-315) and lets data-parallel ranks reduce all
+gradients with one collective.
+
+Parameters and moments are ping-ponged: Adam reads generation `cur` and
+writes `1 - cur`; the host flips `cur` only after the step's record shows a
+valid update, so a rejected step (dropped batch, non-finite gradients or
+results) leaves the live parameters untouched, like the reference's pure
+`adam_step` (numerics.py:95-126).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+POLICY_NAMES = ("w0", "b0", "w1", "b1", "e_prev", "e_pos", "w_head", "b_head")
+VALUE_NAMES = ("w_attn", "b_attn", "e_step", "w0v", "b0v", "w1v", "b1v")
+
+
+@dataclass(frozen=True)
+class Dims:
+    obs_dim: int      # O
+    hidden: int       # D
+    chunk_len: int    # K
+    n_actions: int    # A
+    n_steps: int      # S (value step table)
+    mlp_hidden: int   # H
+
+    def shapes(self) -> dict:
+        O, D, K, A, S, H = (self.obs_dim, self.hidden, self.chunk_len, self.n_actions,
+                            self.n_steps, self.mlp_hidden)
+        return {
+            "w0": (D, O), "b0": (D,), "w1": (D, D), "b1": (D,), "e_prev": (A + 1, D),
+            "e_pos": (K, D), "w_head": (A, D), "b_head": (A,),
+            "w_attn": (D,), "b_attn": (1,), "e_step": (S, D), "w0v": (H, D), "b0v": (H,),
+            "w1v": (1, H), "b1v": (1,),
+        }
+
+    @classmethod
+    def from_models(cls, policy, value) -> "Dims":
+        pc, vc = policy.cfg, value.cfg
+        if vc.hidden_dim != pc.hidden_dim:
+            from .errors import DimensionError
+            raise DimensionError(f"value hidden_dim {vc.hidden_dim} != policy {pc.hidden_dim}")
+        return cls(pc.obs_dim, pc.hidden_dim, pc.chunk_len, pc.n_actions, vc.n_steps,
+                   vc.mlp_hidden)
+
+
+class FlatLayout:
+    def __init__(self, dims: Dims) -> None:
+        self.dims = dims
+        shapes = dims.shapes()
+        self.offsets, self.shapes = {}, {}
+        off = 0
+        for name in POLICY_NAMES + VALUE_NAMES:
+            if name == VALUE_NAMES[0]:
+                self.n_policy = off
+            n = int(np.prod(shapes[name]))
+            self.offsets[name] = off
+            self.shapes[name] = shapes[name]
+            off += (n + 3) // 4 * 4
+        self.total = off
+
+    def views(self, buf: torch.Tensor) -> dict:
+        out = {}
+        for name, off in self.offsets.items():
+            n = int(np.prod(self.shapes[name]))
+            out[name] = buf[off:off + n].view(self.shapes[name])
+        return out
+
+    def n_params(self, names) -> int:
+        return int(sum(np.prod(self.shapes[k]) for k in names))
+
+
+class DeviceParams:
+    """Ping-pong parameter / moment buffers plus one gradient buffer."""
+
+    def __init__(self, layout: FlatLayout, device) -> None:
+        self.layout = layout
+        z = lambda: torch.zeros(layout.total, dtype=torch.float32, device=device)
+        self.p = [z(), z()]
+        self.m = [z(), z()]
+        self.v = [z(), z()]
+        self.g = z()
+        self.cur = 0
+        self._views = [layout.views(self.p[0]), layout.views(self.p[1])]
+        self.gv = layout.views(self.g)
+
+    @property
+    def pv(self) -> dict:
+        return self._views[self.cur]
+
+    def flip(self) -> None:
+        self.cur ^= 1
+
+    def load(self, policy_tensors: dict, value_tensors: dict) -> None:
+        host = np.zeros(self.layout.total, dtype=np.float32)
+        for src, names in ((policy_tensors, POLICY_NAMES), (value_tensors, VALUE_NAMES)):
+            for k in names:
+                off = self.layout.offsets[k]
+                arr = np.asarray(src[k], dtype=np.float32)
+                if arr.shape != tuple(self.layout.shapes[k]):
+                    from .errors import DimensionError
+                    raise DimensionError(f"parameter {k!r}: shape {arr.shape} != "
+                                         f"{self.layout.shapes[k]}")
+                host[off:off + arr.size] = arr.ravel()
+        self.p[self.cur].copy_(torch.from_numpy(host))
+
+    def _split(self, flat: np.ndarray) -> tuple:
+        out = ({}, {})
+        for i, names in enumerate((POLICY_NAMES, VALUE_NAMES)):
+            for k in names:
+                off = self.layout.offsets[k]
+                n = int(np.prod(self.layout.shapes[k]))
+                out[i][k] = flat[off:off + n].astype(np.float64).reshape(self.layout.shapes[k])
+        return out
+
+    def to_host(self) -> tuple:
+        return self._split(self.p[self.cur].cpu().numpy())
+
+    def moments_to_host(self) -> tuple:
+        return self._split(self.m[self.cur].cpu().numpy()), self._split(self.v[self.cur].cpu().numpy())
+
+    def grads_to_host(self) -> tuple:
+        return self._split(self.g.cpu().numpy())
+
+
+class AdamStateView:
+    """Reference-shaped view of one Adam group (numerics.py:75-92)."""
+
+    def __init__(self, owner, group: int, lr: float, beta1: float, beta2: float,
+                 eps: float = 1e-8) -> None:
+        self._owner = owner
+        self._group = group
+        self.step = 0
+        self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
+
+    def hyper(self, t: int) -> torch.Tensor:
+        return torch.tensor([self.lr, self.beta1, self.beta2, self.eps,
+                             1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t], dtype=torch.float64)
+
+    @property
+    def m(self) -> dict:
+        return self._owner.params.moments_to_host()[0][self._group]
+
+    @property
+    def v(self) -> dict:
+        return self._owner.params.moments_to_host()[1][self._group]

@@ -1,0 +1,753 @@
+"""B200 drop-in for the reference trainer hot path (`asyncrl.trainer`).
+
+Same public surface as the reference module (`trainer.py:44-560`):
+`GaeConfig`, `LossConfig`, `TrainerConfig`, `compute_gae`,
+`shard_statistics`, `ShardStats`, `global_normalize`, `trust_weight`,
+`chunk_ratio`, `policy_surrogate`, `entropy_bonus`, `total_loss`,
+`behavior_log_probs` and `Trainer` with `build_train_batch`, `train_step`,
+`recompute_values`, `run`, `publish_*` and the same attributes, record keys,
+metric events and error types.  The math runs in libaccel.so (sm_100a); the
+GEMMs between the custom kernels are plain cuBLAS calls through torch with
+TF32 disabled.  There is no CPU path.
+
+`Trainer.build_train_batch` accepts the reference's `list[Trajectory]` (any
+objects with those fields) or an already packed `workload.PackedBatch`, and
+returns a `DeviceTrainBatch` (lazy host views of the reference TrainBatch
+fields) or None.  `Trainer.train_step` accepts that batch or any
+reference-shaped host TrainBatch.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Any, Generator
+
+import numpy as np
+import torch
+
+from . import ops
+from .batch import DeviceTrainBatch
+from .errors import AccelError, DimensionError, DomainError, NonFiniteError
+from .params import AdamStateView, DeviceParams, Dims, FlatLayout, POLICY_NAMES, VALUE_NAMES
+from .publish import POLICY, VersionedWeights
+from .workload import PackedBatch, pack_trajectories
+
+F32, F64, I32 = torch.float32, torch.float64, torch.int32
+
+
+# ---------------------------------------------------------------------------
+# configuration — trainer.py:44-72, :263-286
+
+
+@dataclass(frozen=True)
+class GaeConfig:
+    gamma: float = 0.99
+    lam: float = 0.95
+
+    def __post_init__(self) -> None:
+        if not 0.0 < self.gamma <= 1.0:
+            raise DomainError(f"gamma must be in (0, 1], got {self.gamma}")
+        if not 0.0 <= self.lam <= 1.0:
+            raise DomainError(f"lam must be in [0, 1], got {self.lam}")
+
+
+@dataclass(frozen=True)
+class LossConfig:
+    algorithm: str = "trust"
+    sigma: float = 0.3
+    clip_eps: float = 0.2
+    lambda_v: float = 0.5
+    lambda_h: float = 0.01
+
+    def __post_init__(self) -> None:
+        if self.algorithm not in ("trust", "clip"):
+            raise DomainError(f"unknown algorithm {self.algorithm!r}")
+        if self.sigma <= 0:
+            raise DomainError(f"sigma must be > 0, got {self.sigma}")
+        if not 0.0 < self.clip_eps < 1.0:
+            raise DomainError(f"clip_eps must be in (0, 1), got {self.clip_eps}")
+        if self.lambda_v < 0 or self.lambda_h < 0:
+            raise DomainError("loss coefficients must be >= 0")
+
+
+@dataclass(frozen=True)
+class TrainerConfig:
+    gae: GaeConfig = GaeConfig()
+    loss: LossConfig = LossConfig()
+    lr: float = 3e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    k_shards: int = 4
+    eps_norm: float = 1e-8
+    revalue: bool = True
+    world_model: bool = False
+    t_obs: int = 4
+    t_reward: int = 8
+    wm_batch_episodes: int = 8
+    wm_max_transitions: int = 512
+    reward_neg_ratio: int = 4
+    poll_interval: float = 0.002
+    train_service_time: float = 0.0
+
+    def __post_init__(self) -> None:
+        if self.k_shards < 1:
+            raise DomainError("k_shards must be >= 1")
+        if self.t_obs < 1 or self.t_reward < 1:
+            raise DomainError("world-model schedules must be >= 1")
+
+
+def _algo_id(cfg: LossConfig) -> int:
+    return 0 if cfg.algorithm == "trust" else 1
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise AccelError("the B200 trainer needs a CUDA device (there is no CPU path)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _dev(a, dtype, device):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device, non_blocking=True)
+
+
+# ---------------------------------------------------------------------------
+# module-level functions (reference trainer.py:79-256, :289-293)
+
+
+def compute_gae(rewards, values, done: bool, cfg: GaeConfig):
+    """One trajectory through the segmented GAE kernel (trainer.py:79-101)."""
+    r = np.asarray(rewards, dtype=np.float64)
+    v = np.asarray(values, dtype=np.float64)
+    t_len = r.shape[0]
+    if v.shape != (t_len + 1,):
+        raise DomainError(f"values must have length T+1={t_len + 1}, got {v.shape}")
+    if t_len == 0:
+        raise DomainError("empty trajectory")
+    dev = _device()
+    off = torch.tensor([0, t_len], dtype=torch.int64, device=dev)
+    adv, ret, _ = ops.gae_segmented(_dev(r, np.float32, dev), _dev(v, np.float32, dev), off,
+                                    torch.tensor([1 if done else 0], dtype=torch.uint8, device=dev),
+                                    cfg.gamma, cfg.lam)
+    return adv.double().cpu().numpy(), ret.double().cpu().numpy()
+
+
+@dataclass(frozen=True)
+class ShardStats:
+    """Per-shard (sum, sum-of-squares, count) — trainer.py:108-125."""
+
+    s: np.ndarray
+    q: np.ndarray
+    n: np.ndarray
+
+    def __post_init__(self) -> None:
+        s, q, n = (np.asarray(a, dtype=np.float64) for a in (self.s, self.q, self.n))
+        if not (s.shape == q.shape == n.shape):
+            raise DomainError("shard stat arrays must share one shape")
+        if np.any(n * q - s * s < -1e-9):
+            raise DomainError("inconsistent shard stats: N*Q < S^2")
+        object.__setattr__(self, "s", s)
+        object.__setattr__(self, "q", q)
+        object.__setattr__(self, "n", n)
+
+
+def _moments(shards) -> np.ndarray:
+    dev = _device()
+    arrs = [np.asarray(a, dtype=np.float64).ravel() for a in shards]
+    sizes = np.array([a.size for a in arrs], dtype=np.int64)
+    off = np.zeros(len(arrs) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=off[1:])
+    flat = np.concatenate(arrs) if arrs else np.zeros(0)
+    out = ops.segment_moments(_dev(flat if flat.size else np.zeros(1), np.float32, dev),
+                              _dev(off, np.int64, dev))
+    return out.cpu().numpy()
+
+
+def shard_statistics(shards) -> ShardStats:
+    """trainer.py:128-132 on the GPU (segmented float64 moments)."""
+    mom = _moments(shards) if len(shards) else np.zeros((0, 3))
+    return ShardStats(mom[:, 0], mom[:, 1], mom[:, 2])
+
+
+def global_normalize(shards, eps: float = 1e-8):
+    """Pooled normalization from shard sums — trainer.py:135-158."""
+    stats = shard_statistics(list(shards))
+    dev = _device()
+    sums = torch.tensor([float(np.sum(stats.s)), float(np.sum(stats.q)), float(np.sum(stats.n))],
+                        dtype=F64, device=dev)
+    st = ops.normalize_finalize(sums, eps).cpu().numpy()
+    if st[3] == 1:
+        raise DomainError("cannot normalize zero advantages")
+    if st[3] == 2:
+        raise DomainError(f"negative pooled variance {st[1]}")
+    out = []
+    st_dev = torch.from_numpy(st).to(dev)
+    for a in shards:
+        a = np.asarray(a, dtype=np.float64)
+        if a.size == 0:
+            out.append(np.zeros(0))
+            continue
+        x = _dev(a, np.float32, dev)
+        out.append(ops.normalize_apply(x, st_dev).double().cpu().numpy())
+    return out, {"mean": float(st[0]), "std": float(st[1]), "n": int(np.sum(stats.n)),
+                 "shard_sizes": tuple(int(k) for k in stats.n)}
+
+
+def trust_weight(ratio, sigma: float):
+    """exp(-log(r)^2 / (2 sigma^2)) — trainer.py:165-175 (float64, on device)."""
+    r = np.asarray(ratio, dtype=np.float64)
+    if np.any(r <= 0) or not np.all(np.isfinite(r)):
+        raise DomainError("trust weight needs finite ratios > 0")
+    t = torch.from_numpy(np.atleast_1d(r).copy()).to(_device())
+    w = torch.exp(-0.5 * torch.square(torch.log(t) / sigma)).cpu().numpy()
+    return float(w[0]) if np.isscalar(ratio) else w.reshape(r.shape)
+
+
+def chunk_ratio(logp_new, logp_old):
+    """Joint chunk ratio exp(sum_k (lp_new - lp_old)) — trainer.py:178-180."""
+    a = torch.from_numpy(np.asarray(logp_new, dtype=np.float64).copy()).to(_device())
+    b = torch.from_numpy(np.asarray(logp_old, dtype=np.float64).copy()).to(_device())
+    return torch.exp((a - b).sum(dim=-1)).cpu().numpy()
+
+
+def policy_surrogate(logp_new, logp_old, advantages, cfg: LossConfig, trust_weights=None):
+    """Token surrogate and its lp gradient — trainer.py:183-239 (float64 on device).
+
+    The trainer itself never calls this: it runs the fused logits-level
+    kernel (accel_token_loss).  This function keeps the reference's
+    log-prob-level API, including the pinned `trust_weights` override."""
+    dev = _device()
+    lpn = torch.from_numpy(np.asarray(logp_new, dtype=np.float64).copy()).to(dev)
+    lpo = torch.from_numpy(np.asarray(logp_old, dtype=np.float64).copy()).to(dev)
+    adv = torch.from_numpy(np.asarray(advantages, dtype=np.float64).copy()).to(dev)
+    a_tok = adv[:, None].expand_as(lpn)
+    ratios = torch.exp(lpn - lpo)
+    inc = torch.isfinite(ratios) & (ratios > 0)
+    n_inc = int(inc.sum().item())
+    diag: dict[str, Any] = {"excluded_tokens": int(inc.numel() - n_inc), "dropped": False}
+    if n_inc == 0:
+        diag["dropped"] = True
+        return 0.0, np.zeros(lpn.shape), diag
+    m = float(n_inc)
+    r = torch.where(inc, ratios, torch.ones_like(ratios))
+    a = torch.where(inc, a_tok, torch.zeros_like(a_tok))
+    if cfg.algorithm == "trust":
+        if trust_weights is None:
+            w = torch.exp(-0.5 * torch.square(torch.log(r) / cfg.sigma))
+        else:
+            w = torch.from_numpy(np.broadcast_to(np.asarray(trust_weights, dtype=np.float64),
+                                                 tuple(lpn.shape)).copy()).to(dev)
+        w = torch.where(inc, w, torch.zeros_like(w))
+        loss = -float((w * r * a)[inc].sum().item()) / m
+        dlogp = torch.where(inc, -(w * r * a) / m, torch.zeros_like(r))
+        diag["trust_weight_mean"] = float(w[inc].mean().item())
+        diag["trust_weight_min"] = float(w[inc].min().item())
+    else:
+        lo, hi = 1.0 - cfg.clip_eps, 1.0 + cfg.clip_eps
+        rc = torch.clamp(r, lo, hi)
+        loss = -float(torch.minimum(r * a, rc * a)[inc].sum().item()) / m
+        dlogp = torch.where((r * a <= rc * a) & inc, -(r * a) / m, torch.zeros_like(r))
+        diag["clipped_fraction"] = float(((r < lo) | (r > hi))[inc].double().mean().item())
+    diag["ratio_mean"] = float(r[inc].mean().item())
+    diag["ratio_max"] = float(r[inc].max().item())
+    return loss, dlogp.cpu().numpy(), diag
+
+
+def entropy_bonus(logits):
+    """Mean token entropy and its logits gradient — trainer.py:242-251 (float64, device)."""
+    z = torch.from_numpy(np.asarray(logits, dtype=np.float64).copy()).to(_device())
+    if z.numel() == 0 or not bool(torch.isfinite(z).all().item()):
+        raise DomainError("log_softmax input contains non-finite values")
+    lp = torch.log_softmax(z, dim=-1)
+    p = torch.exp(lp)
+    h_tok = -(p * lp).sum(dim=-1)
+    n = float(h_tok.numel())
+    return float(h_tok.sum().item()) / n, (-p * (lp + h_tok[..., None]) / n).cpu().numpy()
+
+
+def total_loss(policy_term: float, value_term: float, entropy: float, cfg: LossConfig) -> float:
+    """L = L_policy + lambda_v L_value - lambda_h H — trainer.py:254-256."""
+    return policy_term + cfg.lambda_v * value_term - cfg.lambda_h * entropy
+
+
+def behavior_log_probs(behavior_logits, tokens):
+    """(T, K) chosen-token log-probs through accel_token_logp (trainer.py:289-293)."""
+    mu = np.asarray(behavior_logits, dtype=np.float64)
+    t = np.asarray(tokens, dtype=np.int64)
+    if mu.shape[:-1] != t.shape:
+        raise DimensionError(f"tokens {t.shape} do not index logits {mu.shape}")
+    dev = _device()
+    A = mu.shape[-1]
+    lp, bad = ops.token_logp(_dev(mu.reshape(-1, A), np.float32, dev),
+                             _dev(t.reshape(-1), np.int32, dev))
+    bad = bad.sum(dim=0).cpu().numpy()
+    if bad[0] > 0:
+        raise DomainError("log_softmax input contains non-finite values")
+    if bad[1] > 0:
+        raise DimensionError("token index outside the action vocabulary")
+    return lp.double().cpu().numpy().reshape(t.shape)
+
+
+# ---------------------------------------------------------------------------
+# scratch buffers
+
+
+class _Scratch:
+    """Grow-only named device buffers (shapes change with every batch)."""
+
+    def __init__(self, device) -> None:
+        self.device = device
+        self._bufs: dict = {}
+
+    def get(self, name: str, shape, dtype=F32) -> torch.Tensor:
+        n = int(np.prod(shape)) if len(shape) else 1
+        buf = self._bufs.get(name)
+        if buf is None or buf.dtype != dtype or buf.numel() < n:
+            buf = torch.empty(max(n, 1) + (n >> 4), dtype=dtype, device=self.device)
+            self._bufs[name] = buf
+        return buf[:n].view(*shape) if len(shape) else buf[:1]
+
+
+def _mm(a, b, out):
+    torch.mm(a, b, out=out)
+    return out
+
+
+def _array_split_sizes(n: int, k: int) -> tuple:
+    base, extra = divmod(n, k)
+    return tuple(base + 1 if i < extra else base for i in range(k))
+
+
+# ---------------------------------------------------------------------------
+# the trainer
+
+
+class Trainer:
+    """Owns the live models on the device; consumes TrainBatches; publishes.
+
+    Reference: trainer.py:296-560.  `comm` (optional) is a data-parallel
+    communicator (`dp.DataParallel`); without it the trainer is one GPU.
+    """
+
+    def __init__(self, bundle, cfg: TrainerConfig, service: Any = None, metrics: Any = None,
+                 seed: int = 0, comm: Any = None) -> None:
+        if cfg.world_model:
+            raise NotImplementedError(
+                "world-model training sub-steps (trainer.py:469-535) are outside this build's "
+                "hot path; run them with the reference trainer")
+        self.cfg = cfg
+        self.service = service
+        self.metrics = metrics
+        self.comm = comm
+        self.device = _device()
+        self.rng = np.random.default_rng(np.random.SeedSequence([seed, 7]))
+        self._bundle = bundle
+        self.dims = Dims.from_models(bundle.policy, bundle.value)
+        self.layout = FlatLayout(self.dims)
+        self.params = DeviceParams(self.layout, self.device)
+        self.params.load(bundle.policy.params.tensors, bundle.value.params.tensors)
+        self._policy_version = int(getattr(bundle.policy.params, "version", 0))
+        self._value_version = int(getattr(bundle.value.params, "version", 0))
+        self._host_stale = False
+        self.adam_policy = AdamStateView(self, 0, cfg.lr, cfg.beta1, cfg.beta2)
+        self.adam_value = AdamStateView(self, 1, cfg.lr, cfg.beta1, cfg.beta2)
+        self.publish_version = 0
+        self.cycles = 0
+        self.skipped = 0
+        self.obs_updates = 0
+        self.reward_updates = 0
+        self.scratch = _Scratch(self.device)
+        self._rec_host = torch.zeros(32, dtype=F64).pin_memory()
+        self.torch_stream = None
+        torch.backends.cuda.matmul.allow_tf32 = False
+        torch.backends.cudnn.allow_tf32 = False
+
+    # -- bundle <-> device ---------------------------------------------------------
+    @property
+    def bundle(self):
+        if self._host_stale:
+            pol, val = self.params.to_host()
+            b = self._bundle
+            b.policy.params = type(b.policy.params)(pol, self._policy_version)
+            b.value.params = type(b.value.params)(val, self._value_version)
+            self._host_stale = False
+        return self._bundle
+
+    @bundle.setter
+    def bundle(self, new) -> None:
+        dims = Dims.from_models(new.policy, new.value)
+        if dims != self.dims:
+            raise DimensionError(f"bundle dims {dims} != trainer dims {self.dims}")
+        self._bundle = new
+        self.params.load(new.policy.params.tensors, new.value.params.tensors)
+        self._policy_version = int(getattr(new.policy.params, "version", 0))
+        self._value_version = int(getattr(new.value.params, "version", 0))
+        self._host_stale = False
+
+    # -- publication (trainer.py:328-348) -------------------------------------------
+    def snapshot(self) -> VersionedWeights:
+        return VersionedWeights.from_device(POLICY, self.publish_version, self)
+
+    def publish_policy(self) -> None:
+        if self.service is None:
+            return
+        self.service.update_weights(self.snapshot())
+
+    def publish_world_model(self, kind: str) -> None:
+        if self.service is None or kind not in getattr(self.service, "configs", {}):
+            return
+        raise NotImplementedError("world-model publication is outside this build's hot path")
+
+    def publish_initial(self) -> None:
+        self.publish_policy()
+
+    # -- shared forward pieces -------------------------------------------------------
+    def _backbone(self, frames, tag: str):
+        P = self.params.pv
+        F = frames.shape[0]
+        D = self.dims.hidden
+        h1 = _mm(frames, P["w0"].t(), self.scratch.get(tag + "h1", (F, D)))
+        ops.bias_tanh(h1, P["b0"])
+        h2 = _mm(h1, P["w1"].t(), self.scratch.get(tag + "h2", (F, D)))
+        ops.bias_tanh(h2, P["b1"])
+        return h1, h2
+
+    def _frame_values(self, frames, steps, out, bad_part):
+        """V(o) on every frame: state_values_batch (models.py:411-415)."""
+        P = self.params.pv
+        F = frames.shape[0]
+        d = self.dims
+        h1, h2 = self._backbone(frames, "rv.")
+        U = self.scratch.get("rv.U", (F, d.hidden))
+        alpha = self.scratch.get("rv.alpha", (F, 2))
+        g = ops.warp_grid(F)
+        ops.value_pool(h1, h2, None, steps, F, d.n_steps, P["w_attn"], P["b_attn"], P["e_step"], U,
+                       alpha, bad_part, g)
+        zm = _mm(U, P["w0v"].t(), self.scratch.get("rv.zm", (F, d.mlp_hidden)))
+        ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], None, 0.0, 0.0, out, None, None,
+                       ops.warp_grid(F))
+        return g
+
+    def recompute_values(self, traj) -> np.ndarray:
+        """V(o_t) for all T+1 frames under the current critic (trainer.py:352-356)."""
+        assert self.publish_version >= traj.behavior_version
+        frames = _dev(np.asarray(traj.observations), np.float32, self.device)
+        steps = _dev(np.asarray(traj.steps), np.int32, self.device)
+        if frames.shape[1] != self.dims.obs_dim:
+            raise DimensionError(f"observations have dim {frames.shape[1]}, "
+                                 f"expected {self.dims.obs_dim}")
+        F = frames.shape[0]
+        out = torch.empty(F, dtype=F32, device=self.device)
+        bad_part = self.scratch.get("rv.bad", (ops.warp_grid(F), 2), F64)
+        g = self._frame_values(frames, steps, out, bad_part)
+        bad = bad_part[:g].sum(dim=0).cpu().numpy()
+        if bad[0] > 0:
+            raise DomainError("softmax input contains non-finite values")
+        if bad[1] > 0:
+            raise DimensionError(f"step index outside value-step table [0, {self.dims.n_steps})")
+        return out.double().cpu().numpy()
+
+    # -- batch construction (trainer.py:358-403) --------------------------------------
+    def upload(self, pb: PackedBatch) -> dict:
+        d = self.dims
+        if pb.obs_dim != d.obs_dim or pb.chunk_len != d.chunk_len or pb.n_actions != d.n_actions:
+            raise DimensionError(
+                f"batch (obs {pb.obs_dim}, K {pb.chunk_len}, A {pb.n_actions}) does not match "
+                f"the policy (obs {d.obs_dim}, K {d.chunk_len}, A {d.n_actions})")
+        dev = self.device
+        return {
+            "traj_off": _dev(pb.traj_off, np.int64, dev),
+            "frames": _dev(pb.frames, np.float32, dev),
+            "steps": _dev(pb.steps, np.int32, dev),
+            "values": _dev(pb.values, np.float32, dev),
+            "tokens": _dev(pb.tokens.reshape(-1), np.int32, dev),
+            "rewards": _dev(pb.rewards, np.float32, dev),
+            "mu": _dev(pb.mu.reshape(-1, pb.n_actions), np.float32, dev),
+            "done": _dev(pb.done, np.uint8, dev),
+        }
+
+    def build_train_batch(self, trajs) -> DeviceTrainBatch | None:
+        """Recompute, estimate advantages, normalize globally, tensorize."""
+        if isinstance(trajs, PackedBatch):
+            pb = trajs
+        else:
+            for t in trajs:
+                if self.cfg.revalue:
+                    assert self.publish_version >= t.behavior_version
+            pb = pack_trajectories(trajs)
+        dev_batch = self.upload(pb)
+        return self.build_from_device(dev_batch, n_real=int(pb.real.sum()),
+                                      behavior_version=pb.behavior_version)
+
+    def build_from_device(self, b: dict, n_real: int, behavior_version) -> DeviceTrainBatch | None:
+        """The device half of build_train_batch on an uploaded CSR batch."""
+        cfg, d = self.cfg, self.dims
+        n = int(b["traj_off"].shape[0] - 1)
+        N = int(b["rewards"].shape[0])
+        F = N + n
+        M = N * d.chunk_len
+        dev = self.device
+        flags = torch.zeros(16, dtype=F64, device=dev)
+        cnt = torch.zeros(4, dtype=torch.int32, device=dev)
+        if cfg.revalue:
+            values = torch.empty(F, dtype=F32, device=dev)
+            bad_part = self.scratch.get("b.vbad", (ops.warp_grid(F), 2), F64)
+            g = self._frame_values(b["frames"], b["steps"], values, bad_part)
+            ops.reduce_f64(bad_part, g, 2, 0, flags[10:12])
+        else:
+            values = b["values"]
+        frame_of = torch.empty(N, dtype=I32, device=dev)
+        adv_raw, ret, _ = ops.gae_segmented(b["rewards"], values, b["traj_off"], b["done"],
+                                            cfg.gae.gamma, cfg.gae.lam, frame_of=frame_of,
+                                            sums=flags[0:4])
+        sums = self._allreduce_sum(flags[0:3].clone()) if self.comm is not None else flags[0:3]
+        ops.normalize_finalize(sums, cfg.eps_norm, flags[4:8])
+        adv = ops.normalize_apply(adv_raw, flags[4:8])
+        lp_old, lbad = ops.token_logp(b["mu"], b["tokens"])
+        ops.reduce_f64(lbad, ops.token_grid(M), 2, 0, flags[8:10])
+        ops.count_nonfinite_rows(b["frames"], frame_of, N, cnt[0:1])
+        batch = DeviceTrainBatch(
+            frames=b["frames"], steps=b["steps"], tokens=b["tokens"], frame_of=frame_of,
+            lp_old=lp_old, adv=adv, ret=ret, n_actions=d.n_actions, chunk_len=d.chunk_len,
+            critic_version=self.publish_version, n_real=n_real, n_imagined=n - n_real,
+            norm_mean=0.0, norm_std=0.0, norm_count=N,
+            shard_sizes=_array_split_sizes(N, cfg.k_shards),
+            behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
+        batch.ensure_groupings(d.n_steps, cnt[1:2])
+        host = torch.cat([flags, cnt.double()]).cpu().numpy()  # the one host sync
+        if host[7] == 1:
+            raise DomainError("cannot normalize zero advantages")
+        if host[7] == 2:
+            raise DomainError(f"negative pooled variance {host[5] ** 2}")
+        if host[10] > 0:
+            raise DomainError("softmax input contains non-finite values")
+        if host[11] > 0 or host[17] > 0:
+            raise DimensionError(f"step index outside value-step table [0, {d.n_steps})")
+        if host[8] > 0:
+            raise DomainError("log_softmax input contains non-finite values")
+        if host[9] > 0:
+            raise DimensionError("token index outside the action vocabulary")
+        batch.norm_mean, batch.norm_std = float(host[4]), float(host[5])
+        batch.norm_count = int(host[2])
+        finite = host[3] == 0 and host[16] == 0
+        batch._finite = bool(finite)
+        return batch if finite else None
+
+    # -- optimization (trainer.py:407-467) ---------------------------------------------
+    def _allreduce_sum(self, t):
+        return self.comm.all_reduce_sum(t) if self.comm is not None else t
+
+    def train_step(self, batch) -> dict | None:
+        """One policy + value update from a TrainBatch; publishes.
+
+        Returns the reference record dict, or None when every token was
+        excluded (the batch is skipped, trainer.py:420-424)."""
+        if not isinstance(batch, DeviceTrainBatch):
+            batch = DeviceTrainBatch.from_host(batch, self.device)
+        if batch.n_actions < 0:
+            batch.n_actions = self.dims.n_actions
+        record = self._step_device(batch)
+        return self._finish_step(batch, record)
+
+    def _step_device(self, batch: DeviceTrainBatch) -> torch.Tensor:
+        """Launch the whole step on the current stream; returns the device record."""
+        cfg, d = self.cfg, self.dims
+        lc = cfg.loss
+        P, G = self.params.pv, self.params.gv
+        S = self.scratch
+        dev = self.device
+        N, F, K, A, D, H = (batch.n_transitions, batch.n_frames, d.chunk_len, d.n_actions,
+                            d.hidden, d.mlp_hidden)
+        M = N * K
+        if batch.frames.shape[1] != d.obs_dim:
+            raise DimensionError(f"obs dim {batch.frames.shape[1]} != {d.obs_dim}")
+        cnt = S.get("st.cnt", (4,), torch.int32)
+        cnt.zero_()
+        batch.ensure_groupings(d.n_steps, cnt[1:2])
+        n_glob = self.comm.global_counts(N) if self.comm is not None else (N, M)
+        N_glob, M_glob = n_glob
+
+        # forward: backbone over frames, c, head GEMM
+        h1, h2 = self._backbone(batch.frames, "st.")
+        c = ops.build_c(h2, batch.frame_of, batch.tokens_dev, P["e_prev"], P["e_pos"], N, K, A,
+                        S.get("st.c", (M, D)))
+        logits = _mm(c, P["w_head"].t(), S.get("st.logits", (M, A)))
+
+        # fused loss forward + backward
+        gl = ops.token_grid(M)
+        dlogits = S.get("st.dlogits", (M, A))
+        lp_new = S.get("st.lp_new", (M,))
+        dbias_part = S.get("st.dbias", (gl, A))
+        stat_part = S.get("st.stat", (gl, 8), F64)
+        max_part = S.get("st.max", (gl, 2), F64)
+        algo = _algo_id(lc)
+        ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K, algo,
+                       lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, lp_new, dbias_part,
+                       stat_part, max_part)
+        loss_sums = S.get("st.lsum", (8,), F64)
+        loss_max = S.get("st.lmax", (2,), F64)
+        ops.reduce_f64(stat_part, gl, 8, 0, loss_sums)
+        ops.reduce_f64(max_part, gl, 2, 1, loss_max)
+        if self.comm is not None:
+            self.comm.all_reduce_sum(loss_sums)
+            self.comm.all_reduce_max(loss_max)
+        ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K, algo,
+                       lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None, dbias_part,
+                       None, None, fix_stats=loss_sums)
+
+        # value head (hiddens detached)
+        gw = ops.warp_grid(N)
+        U = S.get("st.U", (N, D))
+        alpha = S.get("st.alpha", (N, 2))
+        vbad_part = S.get("st.vbad", (gw, 2), F64)
+        ops.value_pool(h1, h2, batch.frame_of, batch.frame_steps, N, d.n_steps, P["w_attn"],
+                       P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
+        zm = _mm(U, P["w0v"].t(), S.get("st.zm", (N, H)))
+        vpart = S.get("st.vpart", (gw, 2 * H + 1))
+        vdpart = S.get("st.vdpart", (gw, 2), F64)
+        ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
+                       vpart, vdpart, gw)
+        _mm(zm.t(), U, G["w0v"])
+        dU = _mm(zm, P["w0v"], S.get("st.dU", (N, D)))
+        de = S.get("st.de", (N, 2))
+        battn_part = S.get("st.battn", (gw,))
+        ops.value_attn_grad(dU, h1, h2, batch.frame_of, alpha, de, battn_part, gw)
+        gr = ops.rows_grid(N)
+        wattn_part = S.get("st.wattn", (gr, D))
+        ops.value_attn_wgrad(de, h1, h2, batch.frame_of, N, wattn_part, gr)
+        batch.step_group.rows_sum(dU, G["e_step"])
+
+        # policy backward
+        _mm(dlogits.t(), c, G["w_head"])
+        dc = _mm(dlogits, P["w_head"], c)  # c is dead after dW_head: reuse its storage
+        dz2 = S.get("st.dz2", (F, D))
+        if F != N:
+            dz2.zero_()
+        gd = ops.rows_grid(N)
+        pos_part = S.get("st.pos", (gd, K, D))
+        db1_part = S.get("st.db1", (gd, D))
+        ops.dc_reduce(dc, h2, batch.frame_of, N, K, D, dz2, pos_part, db1_part, gd)
+        batch.prev_group.rows_sum(dc, G["e_prev"])
+        _mm(dz2.t(), h1, G["w1"])
+        dh1 = _mm(dz2, P["w1"], h2)  # h2 is dead: reuse its storage
+        gt = ops.rows_grid(F)
+        db0_part = S.get("st.db0", (gt, D))
+        ops.tanh_grad_colsum(dh1, h1, db0_part, gt)
+        _mm(dh1.t(), batch.frames, G["w0"])
+
+        ops.reduce_segments([
+            (dbias_part, G["b_head"], gl, A, A),
+            (pos_part, G["e_pos"], gd, K * D, K * D),
+            (db1_part, G["b1"], gd, D, D),
+            (db0_part, G["b0"], gt, D, D),
+            (vpart, G["w1v"], gw, H, 2 * H + 1),
+            (vpart[:, H:], G["b0v"], gw, H, 2 * H + 1),
+            (vpart[:, 2 * H:], G["b1v"], gw, 1, 2 * H + 1),
+            (battn_part, G["b_attn"], gw, 1, 1),
+            (wattn_part, G["w_attn"], gr, D, D),
+        ])
+        value_sums = S.get("st.vsum", (2,), F64)
+        attn_bad = S.get("st.abad", (2,), F64)
+        ops.reduce_f64(vdpart, gw, 2, 0, value_sums)
+        ops.reduce_f64(vbad_part, gw, 2, 0, attn_bad)
+        if self.comm is not None:
+            self.comm.reduce_grads(self.params.g)
+            self.comm.all_reduce_sum(value_sums)
+            self.comm.all_reduce_sum(attn_bad)
+        ops.count_nonfinite(self.params.g, cnt[0:1])
+        record = S.get("st.record", (17,), F64)
+        skip = S.get("st.skip", (1,), torch.int32)
+        ops.step_finalize(loss_sums, loss_max, value_sums, cnt, attn_bad, algo, lc.lambda_v,
+                          lc.lambda_h, M_glob, N_glob, record, skip)
+
+        # Adam on both groups (ping-pong; no-op when skip)
+        t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
+        hyp = torch.cat([self.adam_policy.hyper(t_pol), self.adam_value.hyper(t_val)]).to(
+            dev, non_blocking=True)
+        cur, nxt = self.params.cur, self.params.cur ^ 1
+        adam_bad = cnt[2:3]
+        if self.comm is not None:
+            self.comm.adam(self.params, hyp, skip, adam_bad)
+        else:
+            ops.adam(self.params.p[cur], self.params.g, self.params.m[cur], self.params.v[cur],
+                     self.params.p[nxt], self.params.m[nxt], self.params.v[nxt],
+                     self.layout.n_policy, hyp[0:6], hyp[6:12], skip, adam_bad)
+        out = S.get("st.out", (18,), F64)
+        out[:17].copy_(record)
+        out[17:18].copy_(adam_bad.double())
+        return out
+
+    def _finish_step(self, batch, record_dev: torch.Tensor) -> dict | None:
+        host = self._rec_host[:18]
+        host.copy_(record_dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        rec = host.numpy().copy()
+        if rec[11] > 0:
+            raise DomainError("log_softmax input contains non-finite values")
+        if rec[12] > 0:
+            raise DimensionError("token index outside the action vocabulary")
+        if rec[13] > 0:
+            raise DomainError("softmax input contains non-finite values")
+        if rec[15] > 0:
+            raise DimensionError(f"step index outside value-step table [0, {self.dims.n_steps})")
+        if rec[10] > 0:
+            self.skipped += 1
+            if self.metrics is not None:
+                self.metrics.emit("train_skip", skipped=self.skipped)
+            return None
+        if rec[14] > 0:
+            raise NonFiniteError("gradient contains non-finite values")
+        if rec[17] > 0:
+            raise NonFiniteError("parameter update produced non-finite values")
+        self.params.flip()
+        self.adam_policy.step += 1
+        self.adam_value.step += 1
+        self._policy_version += 1
+        self._value_version += 1
+        self._host_stale = True
+        self.cycles += 1
+        self.publish_version += 1
+        self.publish_policy()
+        out = {
+            "loss": float(rec[0]), "policy_loss": float(rec[1]), "value_loss": float(rec[2]),
+            "entropy": float(rec[3]), "version": self.publish_version,
+            "critic_version": batch.critic_version, "behavior_lag": batch.behavior_lag_mean,
+            "n_real": batch.n_real, "n_imagined": batch.n_imagined,
+            "excluded_tokens": int(rec[4]),
+        }
+        if self.cfg.loss.algorithm == "trust":
+            out["trust_weight_mean"] = float(rec[7])
+            out["trust_weight_min"] = float(rec[8])
+        else:
+            out["clipped_fraction"] = float(rec[9])
+        out["ratio_mean"] = float(rec[5])
+        out["ratio_max"] = float(rec[6])
+        if self.metrics is not None:
+            self.metrics.emit("train_step", **out)
+        return out
+
+    # -- loop (trainer.py:539-560) -------------------------------------------------------
+    def run(self, cache, wm_buffer, stop) -> Generator:
+        """Consume TrainBatches from the prefetch channel until stopped.
+
+        Yields the reference runtime's effects (`Get`, `Sleep`), so it runs
+        on the reference `Scheduler` unchanged; effect classes are taken from
+        the channel's module to stay duck-typed."""
+        from importlib import import_module
+        rt = import_module(type(cache).__module__)
+        cfg = self.cfg
+        while not stop.is_set:
+            item = yield rt.Get(cache, timeout=cfg.poll_interval)
+            if item is rt.CLOSED:
+                return
+            if item is rt.TIMEOUT:
+                continue
+            if cfg.train_service_time > 0:
+                yield rt.Sleep(cfg.train_service_time)
+            self.train_step(item)
+
+
+__all__ = [
+    "GaeConfig", "LossConfig", "TrainerConfig", "Trainer", "ShardStats", "compute_gae",
+    "shard_statistics", "global_normalize", "trust_weight", "chunk_ratio", "policy_surrogate",
+    "entropy_bonus", "total_loss", "behavior_log_probs", "POLICY_NAMES", "VALUE_NAMES",
+]
