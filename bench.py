@@ -1,0 +1,389 @@
+"""Trainer-step benchmark (driver contract).
+
+One step = `Trainer.build_train_batch` + `Trainer.train_step` (revaluation,
+segmented GAE, pooled normalization, behavior log-probs, policy + value
+forward/backward with the fused GIPO token loss, Adam) over one synthetic
+cfg2 batch per GPU:
+  4096 LIBERO-Long-like ragged trajectories (50% successes, T ~ U[1,520],
+  done; 50% truncations at T = 520), K = 7 action tokens x A = 256 bins,
+  policy D = 64, obs 195, value head n_steps 522 / mlp 32, random init.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value`  = transitions of all ranks / device-timed seconds (inputs resident in HBM).
+`e2e`    = the same step through the public API from pinned HOST buffers, H2D of
+           every input and the D2H of the record inside the timed region.
+`--impl reference` times the float64 CPU restatement of the reference trainer
+(oracle/, the reference itself is pure NumPy) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "trainer transitions/sec"
+UNIT = "transitions/s"
+WORKLOAD = ("cfg2 trainer step: LIBERO-Long ragged trajectories (50% success T~U[1,520] done, "
+            "50% truncated T=520), K=7, A=256, D=64, obs 195, GIPO trust arm, revalue on")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-traj", type=int, default=4096, help="trajectories per GPU")
+    ap.add_argument("--horizon", type=int, default=520)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-traj", type=int, default=64, help="cpu_baseline sample size")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dims():
+    return dict(K=7, A=256, D=64, O=195, H=32)
+
+
+def make_bundle(seed: int, n_steps: int):
+    from paper_2603_18464_b200.types import (ModelBundle, PolicyConfig, PolicyModel, ValueConfig,
+                                             ValueHead)
+    d = dims()
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 3]))
+    pc = PolicyConfig(obs_dim=d["O"], hidden_dim=d["D"], chunk_len=d["K"], n_actions=d["A"],
+                      vocab_size=32000, action_start=31744)
+    vc = ValueConfig(hidden_dim=d["D"], n_steps=n_steps, mlp_hidden=d["H"])
+    return ModelBundle(PolicyModel.init(rng, pc), ValueHead.init(rng, vc))
+
+
+def lengths_for(seed: int, rank: int, n: int, horizon: int):
+    from paper_2603_18464_b200.workload import libero_long_lengths
+    return libero_long_lengths(np.random.default_rng(np.random.SeedSequence([seed, rank, 11])), n,
+                               horizon)
+
+
+def device_inputs(lens, done, seed: int, device):
+    """Synthetic packed batch generated directly in HBM (N(0,1) values, U[0,A) tokens)."""
+    import torch
+    d = dims()
+    n = len(lens)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    N = int(off[-1])
+    F = N + n
+    steps = (np.arange(F) - np.repeat(off[:-1] + np.arange(n), lens + 1)).astype(np.int32)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    f32 = torch.float32
+    return {
+        "traj_off": torch.from_numpy(off).to(device),
+        "frames": torch.randn(F, d["O"], generator=g, device=device, dtype=f32),
+        "steps": torch.from_numpy(steps).to(device),
+        "values": torch.randn(F, generator=g, device=device, dtype=f32),
+        "tokens": torch.randint(0, d["A"], (N * d["K"],), generator=g, device=device,
+                                dtype=torch.int32),
+        "rewards": torch.randn(N, generator=g, device=device, dtype=f32),
+        "mu": torch.randn(N * d["K"], d["A"], generator=g, device=device, dtype=f32),
+        "done": torch.from_numpy(np.asarray(done, dtype=np.uint8)).to(device),
+    }
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.summary = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return False
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if sm:
+            self.summary = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)),
+                            "reasons": sorted(reasons), "samples": len(sm)}
+        return False
+
+
+def cpu_baseline(bundle, inputs_host, lens, done, n_cpu: int, n_steps: int, reps: int = 1):
+    """The float64 oracle (reference restatement) on a bounded sample, host cores."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle.trainer_ref import OracleConfig, OracleTrainer
+    from paper_2603_18464_b200.workload import PackedBatch, unpack_trajectories
+    d = dims()
+    n = min(n_cpu, len(lens))
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens[:n], out=off[1:])
+    N = int(off[-1])
+    F = N + n
+    pb = PackedBatch(traj_off=off, frames=inputs_host["frames"][:F], steps=inputs_host["steps"][:F],
+                     values=inputs_host["values"][:F],
+                     tokens=inputs_host["tokens"][:N * d["K"]].reshape(N, d["K"]),
+                     rewards=inputs_host["rewards"][:N],
+                     mu=inputs_host["mu"][:N * d["K"]].reshape(N, d["K"], d["A"]),
+                     done=np.asarray(done[:n], dtype=np.uint8), real=np.ones(n, np.uint8),
+                     behavior_version=np.zeros(n, np.int64))
+    trajs = unpack_trajectories(pb)
+    cores = os.cpu_count() or 1
+    best = None
+    with threadpool_limits(limits=cores):
+        for _ in range(reps + 1):
+            orc = OracleTrainer(bundle.policy.params.tensors, bundle.value.params.tensors,
+                                d["A"], n_steps, OracleConfig())
+            t0 = time.perf_counter()
+            b = orc.build_train_batch(trajs)
+            orc.train_step(b)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+    return {"value": N / best, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n} trajectories / {N} transitions of the same workload, oracle "
+                      f"build_train_batch + train_step (float64 NumPy, OpenBLAS {cores} threads), "
+                      f"best of {reps} after 1 warm-up"}
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the CPU restatement of the reference trainer (rank 0)."""
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (device-free: generation on the host)
+    d = dims()
+    lens, done = lengths_for(args.seed, 0, args.n_traj, args.horizon)
+    n_steps = args.horizon + 2
+    bundle = make_bundle(args.seed, n_steps)
+    from paper_2603_18464_b200.workload import synthetic_packed, unpack_trajectories
+    from threadpoolctl import threadpool_limits
+
+    from oracle.trainer_ref import OracleConfig, OracleTrainer
+    n = min(16, args.n_traj)
+    pb = synthetic_packed(args.seed, lens[:n], done[:n], d["K"], d["A"], d["O"])
+    trajs = unpack_trajectories(pb)
+    N = pb.n_transitions
+    cores = os.cpu_count() or 1
+    times = []
+    with threadpool_limits(limits=cores):
+        orc = OracleTrainer(bundle.policy.params.tensors, bundle.value.params.tensors, d["A"],
+                            n_steps, OracleConfig())
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            b = orc.build_train_batch(trajs)
+            orc.train_step(b)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    sec = float(np.sum(times)) / max(1, len(times))
+    value = N / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) values/logits, U[0,A) tokens)",
+        "config": {"workload": WORKLOAD, "sample_trajectories": n, "sample_transitions": N},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{n} trajectories / {N} transitions per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_18464_b200 import _lib
+    from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_2603_18464_b200.dp import DataParallel
+        comm = DataParallel()
+    d = dims()
+    n_steps = args.horizon + 2
+    lens, done = lengths_for(args.seed, rank, args.n_traj, args.horizon)
+    N = int(lens.sum())
+    n = len(lens)
+    M = N * d["K"]
+    bundle = make_bundle(args.seed, n_steps)
+    tr = Trainer(bundle, TrainerConfig(), comm=comm)
+    inputs = device_inputs(lens, done, args.seed * 1000 + rank, dev)
+    bver = np.zeros(n, dtype=np.int64)
+
+    def step(inp):
+        batch = tr.build_from_device(inp, n_real=n, behavior_version=bver)
+        return tr.train_step(batch)
+
+    for _ in range(args.warmup):
+        step(inputs)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region -------------------------------------------
+    tr.profile_events = []
+    launches0 = _lib.launch_count()
+    if comm is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            rec = step(inputs)
+        e1.record()
+        torch.cuda.synchronize()
+    if comm is not None:
+        dist.barrier()
+    launches = _lib.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    kern = {}
+    for name, a, b in tr.profile_events:
+        kern.setdefault(name, []).append(a.elapsed_time(b))
+    tr.profile_events = None
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(N)], dtype=torch.float64, device=dev)
+    if comm is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms = float(ms_t.item())
+    value = float(tot.item()) / (ms / 1e3)
+
+    # ---- e2e: public API from pinned host buffers --------------------------------
+    e2e = None
+    host = {k: v.cpu().pin_memory() if k != "traj_off" else v.cpu() for k, v in inputs.items()}
+    if not args.no_e2e:
+        h2d = sum(v.numel() * v.element_size() for v in host.values())
+        dev_in = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+        for _ in range(1):
+            for k in host:
+                dev_in[k].copy_(host[k], non_blocking=True)
+            step(dev_in)
+        if comm is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            for k in host:
+                dev_in[k].copy_(host[k], non_blocking=True)
+            step(dev_in)
+        a1.record()
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device=dev)
+        if comm is not None:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        e2e = {"value": float(tot.item()) / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": (18 + 20) * 8, "ms_per_step": e_ms,
+               "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
+        del dev_in
+
+    if rank != 0:
+        if comm is not None:
+            dist.destroy_process_group()
+        return
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
+    peak = float(peaks["hbm_gbs"])
+    A = d["A"]
+    loss_bytes = M * (8 * A + 12) + 4 * N
+    t_loss = float(np.mean(kern.get("token_loss", [float("nan")]))) / 1e3
+    achieved = loss_bytes / t_loss / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("token_loss_dram_bytes_per_launch")
+    gae_bytes = 20 * N + 13 * n
+    t_gae = float(np.mean(kern.get("gae", [float("nan")]))) / 1e3
+    logp_bytes = M * (4 * A + 8)
+    t_logp = float(np.mean(kern.get("token_logp", [float("nan")]))) / 1e3
+
+    cpu = None
+    if not args.no_cpu:
+        host_np = {k: v.numpy() for k, v in host.items()}
+        cpu = cpu_baseline(bundle, host_np, lens, done, args.cpu_traj, n_steps)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded N(0,1) obs/values/rewards/behavior logits, U[0,A) tokens, "
+                "random-init policy/value heads)",
+        "config": {"workload": WORKLOAD, "trajectories_per_gpu": n, "transitions_per_gpu": N,
+                   "tokens_per_gpu": M, "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (behavior logits alone 11+ GB per GPU)"},
+        "roofline": {"kernel": "token_loss (fused GIPO fwd+bwd)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "bytes_per_launch": loss_bytes, "ms_per_launch": t_loss * 1e3,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "roofline_gae": {"bytes_per_launch": gae_bytes, "ms_per_launch": t_gae * 1e3,
+                         "achieved": gae_bytes / t_gae / 1e9,
+                         "frac": gae_bytes / t_gae / 1e9 / peak, "unit": "GB/s"},
+        "roofline_token_logp": {"bytes_per_launch": logp_bytes, "ms_per_launch": t_logp * 1e3,
+                                "achieved": logp_bytes / t_logp / 1e9,
+                                "frac": logp_bytes / t_logp / 1e9 / peak, "unit": "GB/s"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary,
+        "last_record": {k: rec[k] for k in ("loss", "policy_loss", "value_loss", "entropy")},
+    }
+    print(json.dumps(line), flush=True)
+    if comm is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -216,7 +216,7 @@ int accel_step_finalize(const double* loss_sums, const double* loss_max,
                         double* record, int* skip, void* stream);
 int accel_count_nonfinite(const float* x, int64_t n, unsigned* count, void* stream);
 /* Adam (numerics.py:95-126) over a flat buffer: [0, n0) group0, [n0, n)
- * group1; group = f64[6] {lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t}.
+ * group1; group = HOST f64[6] {lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t}.
  * No-op when *skip; bad += non-finite new parameters. */
 int accel_adam(const float* p_in, const float* g, const float* m_in, const float* v_in,
                float* p_out, float* m_out, float* v_out, int64_t n, int64_t n0,

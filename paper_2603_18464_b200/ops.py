@@ -278,6 +278,9 @@ def step_finalize(loss_sums, loss_max, value_sums, bad_counts, attn_bad, algo, l
 
 
 def adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, group0, group1, skip, bad):
+    """group0/group1: HOST sequences {lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t}."""
     n = p_in.numel()
+    h0 = (ctypes.c_double * 6)(*[float(x) for x in group0])
+    h1 = (ctypes.c_double * 6)(*[float(x) for x in group1])
     _lib.call("accel_adam", _p(p_in), _p(g), _p(m_in), _p(v_in), _p(p_out), _p(m_out), _p(v_out),
-              n, int(n0), _p(group0), _p(group1), _p(skip), _p(bad), _stream())
+              n, int(n0), h0, h1, _p(skip), _p(bad), _stream())

@@ -143,9 +143,10 @@ class AdamStateView:
         self.step = 0
         self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
 
-    def hyper(self, t: int) -> torch.Tensor:
-        return torch.tensor([self.lr, self.beta1, self.beta2, self.eps,
-                             1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t], dtype=torch.float64)
+    def hyper(self, t: int) -> tuple:
+        """{lr, beta1, beta2, eps, 1 - beta1^t, 1 - beta2^t} for step t (host)."""
+        return (self.lr, self.beta1, self.beta2, self.eps,
+                1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t)
 
     @property
     def m(self) -> dict:

@@ -357,7 +357,7 @@ class Trainer:
         self.reward_updates = 0
         self.scratch = _Scratch(self.device)
         self._rec_host = torch.zeros(32, dtype=F64).pin_memory()
-        self.torch_stream = None
+        self.profile_events = None  # list -> CUDA-event brackets of the hot kernels
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
 
@@ -496,13 +496,15 @@ class Trainer:
         else:
             values = b["values"]
         frame_of = torch.empty(N, dtype=I32, device=dev)
-        adv_raw, ret, _ = ops.gae_segmented(b["rewards"], values, b["traj_off"], b["done"],
-                                            cfg.gae.gamma, cfg.gae.lam, frame_of=frame_of,
-                                            sums=flags[0:4])
+        with self._timed("gae"):
+            adv_raw, ret, _ = ops.gae_segmented(b["rewards"], values, b["traj_off"], b["done"],
+                                                cfg.gae.gamma, cfg.gae.lam, frame_of=frame_of,
+                                                sums=flags[0:4])
         sums = self._allreduce_sum(flags[0:3].clone()) if self.comm is not None else flags[0:3]
         ops.normalize_finalize(sums, cfg.eps_norm, flags[4:8])
         adv = ops.normalize_apply(adv_raw, flags[4:8])
-        lp_old, lbad = ops.token_logp(b["mu"], b["tokens"])
+        with self._timed("token_logp"):
+            lp_old, lbad = ops.token_logp(b["mu"], b["tokens"])
         ops.reduce_f64(lbad, ops.token_grid(M), 2, 0, flags[8:10])
         ops.count_nonfinite_rows(b["frames"], frame_of, N, cnt[0:1])
         batch = DeviceTrainBatch(
@@ -533,6 +535,25 @@ class Trainer:
         return batch if finite else None
 
     # -- optimization (trainer.py:407-467) ---------------------------------------------
+    def _timed(self, name: str):
+        """CUDA-event bracket around one launch when `profile_events` is a list."""
+        trainer = self
+
+        class _Ctx:
+            def __enter__(self_):
+                if trainer.profile_events is not None:
+                    self_.e0 = torch.cuda.Event(enable_timing=True)
+                    self_.e0.record()
+
+            def __exit__(self_, *exc):
+                if trainer.profile_events is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    trainer.profile_events.append((name, self_.e0, e1))
+                return False
+
+        return _Ctx()
+
     def _allreduce_sum(self, t):
         return self.comm.all_reduce_sum(t) if self.comm is not None else t
 
@@ -580,9 +601,10 @@ class Trainer:
         stat_part = S.get("st.stat", (gl, 8), F64)
         max_part = S.get("st.max", (gl, 2), F64)
         algo = _algo_id(lc)
-        ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K, algo,
-                       lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, lp_new, dbias_part,
-                       stat_part, max_part)
+        with self._timed("token_loss"):
+            ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K,
+                           algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, lp_new,
+                           dbias_part, stat_part, max_part)
         loss_sums = S.get("st.lsum", (8,), F64)
         loss_max = S.get("st.lmax", (2,), F64)
         ops.reduce_f64(stat_part, gl, 8, 0, loss_sums)
@@ -661,8 +683,7 @@ class Trainer:
 
         # Adam on both groups (ping-pong; no-op when skip)
         t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
-        hyp = torch.cat([self.adam_policy.hyper(t_pol), self.adam_value.hyper(t_val)]).to(
-            dev, non_blocking=True)
+        hyp = (self.adam_policy.hyper(t_pol), self.adam_value.hyper(t_val))
         cur, nxt = self.params.cur, self.params.cur ^ 1
         adam_bad = cnt[2:3]
         if self.comm is not None:
@@ -670,7 +691,7 @@ class Trainer:
         else:
             ops.adam(self.params.p[cur], self.params.g, self.params.m[cur], self.params.v[cur],
                      self.params.p[nxt], self.params.m[nxt], self.params.v[nxt],
-                     self.layout.n_policy, hyp[0:6], hyp[6:12], skip, adam_bad)
+                     self.layout.n_policy, hyp[0], hyp[1], skip, adam_bad)
         out = S.get("st.out", (18,), F64)
         out[:17].copy_(record)
         out[17:18].copy_(adam_bad.double())

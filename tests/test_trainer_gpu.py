@@ -21,10 +21,21 @@ ADV_TOL = 1e-5
 GRAD_TOL = 1e-4
 
 
-def grad_err(x, y) -> float:
+def grad_err(x, y, floor: float = 0.0) -> float:
+    """max |x - y| relative to the tensor's max |y|; `floor` (1e-3 of the
+    model-wide gradient scale) keeps analytically-zero gradients such as
+    b_attn (softmax shift invariance: pure round-off in both) comparable."""
     x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
-    scale = max(float(np.max(np.abs(y))), 1e-30)
+    scale = max(float(np.max(np.abs(y))), floor, 1e-30)
     return float(np.max(np.abs(x - y))) / scale
+
+
+def check_grads(dev_pol, dev_val, g_pol, g_val, tag=""):
+    gscale = max(float(np.max(np.abs(v))) for d in (g_pol, g_val) for v in d.values())
+    for mine, want in ((dev_pol, g_pol), (dev_val, g_val)):
+        for k in want:
+            e = grad_err(mine[k], want[k], 1e-3 * gscale)
+            assert e < GRAD_TOL, (tag, k, e)
 
 
 def make_bundle(policy: dict, value: dict, meta: dict):
@@ -103,9 +114,7 @@ def test_trainer_matches_reference_golden(name):
         orc = oracle_for(g, before_pol, before_val)
         _, g_pol, g_val = orc.step_gradients(oracle_batch(g, s))
         dev_pol, dev_val = tr.params.grads_to_host()
-        for mine, want in ((dev_pol, g_pol), (dev_val, g_val)):
-            for k in want:
-                assert grad_err(mine[k], want[k]) < GRAD_TOL, (name, s, k, grad_err(mine[k], want[k]))
+        check_grads(dev_pol, dev_val, g_pol, g_val, (name, s))
 
         # parameters after Adam: exact up to float32 storage, except entries
         # whose reference gradient is ~0 (their first Adam step is +-lr by sign)
@@ -161,9 +170,7 @@ def test_random_batch_matches_oracle(algo):
     for k, v in orec.items():
         assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
     dev_pol, dev_val = tr.params.grads_to_host()
-    for mine, want in ((dev_pol, g_pol), (dev_val, g_val)):
-        for k in want:
-            assert grad_err(mine[k], want[k]) < GRAD_TOL, (k, grad_err(mine[k], want[k]))
+    check_grads(dev_pol, dev_val, g_pol, g_val, algo)
 
 
 def test_partial_exclusion_runs_fixup_pass():
@@ -182,9 +189,8 @@ def test_partial_exclusion_runs_fixup_pass():
     assert rec["excluded_tokens"] == orec["excluded_tokens"] > 0
     for k, v in orec.items():
         assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
-    dev_pol, _ = tr.params.grads_to_host()
-    for k in g_pol:
-        assert grad_err(dev_pol[k], g_pol[k]) < GRAD_TOL, k
+    dev_pol, dev_val = tr.params.grads_to_host()
+    check_grads(dev_pol, dev_val, g_pol, g_val, "fixup")
     assert isinstance(DeviceTrainBatch.from_host(ob, tr.device), DeviceTrainBatch)
 
 
