@@ -113,6 +113,28 @@ int accel_token_loss(const float* logits, const float* bias, const int32_t* toke
                      float* lp_new, float* dbias_part, double* stat_part,
                      double* max_part, void* stream);
 
+/* Factorized-head variant (the production path for 128 <= A <= 1024,
+ * A % 4 == 0, K <= 32): logits are never materialized.  logits[i,k] =
+ * h2w[frame_of[i]] + ep[prev] + pp[k] + bias with h2w = h2 W_head^T (f32[F, A]),
+ * ep = e_prev W_head^T (f32[A+1, A]), pp = e_pos W_head^T (f32[K, A]) —
+ * models.py:181-182 distributed over c = h2 + e_prev[prev] + e_pos.
+ * Writes dz f32[N*K, A] (per-token dlogits), g_frame f32[F, A] rows
+ * frame_of[i] = sum_k dz[i, k] (pre-zero the bootstrap rows), lp_new,
+ * stat_part/max_part as accel_token_loss (grid = accel_fact_grid(N)).
+ * fix_stats: FIXUP pass as accel_token_loss. */
+int accel_fact_grid(int64_t N);
+int accel_token_loss_fact(const float* h2w, const float* ep, const float* pp,
+                          const float* bias, const int32_t* frame_of, const int32_t* tokens,
+                          const float* lp_old, const float* adv, int64_t N, int K, int A,
+                          int algo, double sigma, double clip_eps, double lambda_h,
+                          double m_global, const double* fix_stats, float* dz,
+                          float* g_frame, float* lp_new, double* stat_part,
+                          double* max_part, void* stream);
+/* Dprev f32[A+1, A] = sum_k dpk[j, k]; Dpos f32[K, A] = sum_j dpk[j, k]
+ * from the (prev, k)-grouped dz sums dpk f32[(A+1)*K, A]. */
+int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, float* dpos,
+                       void* stream);
+
 /* ---- policy glue (models.py:165-209) ----------------------------------- */
 
 /* z = tanh(z + b) in place, z f32[rows, cols] — models.py:176-177. */
@@ -142,8 +164,10 @@ int accel_tanh_grad_colsum(float* g, const float* h, int64_t R, int C,
 
 /* ---- deterministic scatter-add (np.add.at, models.py:195 and :305) ------ */
 
-int accel_prev_keys(const int32_t* tokens, int64_t N, int K, int A, int32_t* keys,
-                    void* stream);
+/* keys[i*K+k] = prev (with_pos = 0) or prev*K + k (with_pos = 1), prev = A
+ * at k = 0 else tokens[i*K+k-1] (models.py:178-180). */
+int accel_prev_keys(const int32_t* tokens, int64_t N, int K, int A, int with_pos,
+                    int32_t* keys, void* stream);
 /* keys[r] = steps[frame_of ? frame_of[r] : r]; bad_count += out-of-range
  * steps (the reference raises DimensionError, models.py:261-267). */
 int accel_step_keys(const int32_t* steps, const int32_t* frame_of, int64_t R,

@@ -35,7 +35,12 @@ _SIGNATURES = {
     "accel_rows_grid": (c_int, [c_int64]),
     "accel_dc_reduce": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, P, c_int, P]),
     "accel_tanh_grad_colsum": (c_int, [P, P, c_int64, c_int, P, c_int, P]),
-    "accel_prev_keys": (c_int, [P, c_int64, c_int, c_int, P, P]),
+    "accel_prev_keys": (c_int, [P, c_int64, c_int, c_int, c_int, P, P]),
+    "accel_fact_grid": (c_int, [c_int64]),
+    "accel_token_loss_fact": (c_int, [P, P, P, P, P, P, P, P, c_int64, c_int, c_int, c_int,
+                                      c_double, c_double, c_double, c_double, P, P, P, P, P, P,
+                                      P]),
+    "accel_pk_marginals": (c_int, [P, c_int, c_int, P, P, P]),
     "accel_step_keys": (c_int, [P, P, c_int64, c_int, P, P, P]),
     "accel_group_workspace_size": (c_size_t, [c_int64, c_int]),
     "accel_group_max_pieces": (c_int64, [c_int64, c_int]),

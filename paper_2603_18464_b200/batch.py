@@ -42,6 +42,7 @@ class DeviceTrainBatch:
         self.behavior_lag_mean = behavior_lag_mean
         self._finite = bool(finite)
         self.prev_group = prev_group
+        self.pk_group = None
         self.step_group = step_group
         self.n_steps = n_steps
         self._host = {}
@@ -95,10 +96,15 @@ class DeviceTrainBatch:
     def value_targets(self) -> np.ndarray:
         return self._get("ret", lambda: self.ret.double().cpu().numpy())
 
-    def ensure_groupings(self, n_steps: int, bad_count) -> None:
-        """Stable key sorts for the deterministic scatter-adds (fixed per batch)."""
+    def ensure_groupings(self, n_steps: int, bad_count, factorized: bool = True) -> None:
+        """Stable key sorts for the deterministic scatter-adds (fixed per batch):
+        (prev token, chunk position) for the factorized head, prev token for the
+        materialized head, step index for the value head's e_step."""
         N, K, A = self.n_transitions, self.chunk_len, self.n_actions
-        if self.prev_group is None:
+        if factorized and self.pk_group is None:
+            self.pk_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A, with_pos=True),
+                                         (A + 1) * K)
+        if not factorized and self.prev_group is None:
             self.prev_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A), A + 1)
         if self.step_group is None or self.n_steps != n_steps:
             keys = ops.step_keys(self.frame_steps, self.frame_of, N, n_steps, bad_count)

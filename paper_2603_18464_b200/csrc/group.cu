@@ -3,16 +3,18 @@
 // Reference: `np.add.at(de_prev, prev.ravel(), dc)` (models.py:195) and
 // `np.add.at(de_step, t, du)` (models.py:305).  Float atomics would make the
 // result depend on scheduling; instead the keys of a batch (previous-token
-// ids, step ids — fixed per TrainBatch) are counting-sorted once, stably, at
-// batch build time, and every later grouped sum is a segmented reduction in
-// that fixed order:
-//   1. chunk histograms (one warp per 1024-row chunk, smem int atomics),
-//   2. one exclusive scan over the key-major [key][chunk] counts,
+// ids x chunk positions, step ids — fixed per TrainBatch) are counting-sorted
+// once, stably, at batch build time, and every later grouped sum is a
+// segmented reduction in that fixed order:
+//   1. chunk histograms (one warp per 16K-row chunk, smem int atomics),
+//   2. exclusive scan of the key-major [key][chunk] counts (CUB DeviceScan),
 //   3. stable scatter: each warp walks its chunk 32 rows at a time, ranking
 //      equal keys with __match_any_sync,
 //   4. grouped sums: each key segment is cut into <=256-row pieces; one CTA
-//      sums a piece (gathered rows) in fixed order, a second pass sums the
-//      pieces of each key in order.
+//      sums a piece (gathered rows, coalesced within a row) in fixed order, a
+//      second pass sums the pieces of each key in order.
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 
 namespace accel {
@@ -20,16 +22,18 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 1024;  // rows per warp chunk
-constexpr int kPiece = 256;   // rows per grouped-sum piece
+constexpr int kChunk = 16384;  // rows per warp chunk
+constexpr int kPiece = 256;    // rows per grouped-sum piece
 
+// key = prev (with_pos == 0) or prev * K + k (with_pos == 1); prev = A at k == 0
 __global__ void prev_keys_kernel(const int32_t* __restrict__ tokens, int64_t M, int K, int A,
-                                 int32_t* __restrict__ keys) {
+                                 int with_pos, int32_t* __restrict__ keys) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < M; r += stride) {
     const int k = (int)(r % K);
-    int key = k == 0 ? A : __ldg(tokens + r - 1);
-    keys[r] = min(max(key, 0), A);
+    int prev = k == 0 ? A : __ldg(tokens + r - 1);
+    prev = min(max(prev, 0), A);
+    keys[r] = with_pos ? prev * K + k : prev;
   }
 }
 
@@ -65,44 +69,20 @@ chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_
   }
 }
 
-// Single-CTA exclusive scan of counts (in place); seg_off[j] = start of key j.
-__global__ void __launch_bounds__(1024)
-scan_counts_kernel(int* __restrict__ counts, int64_t total, int nkeys, int64_t n_chunks, int64_t R,
-                   int64_t* __restrict__ seg_off, int64_t* __restrict__ piece_off) {
-  __shared__ int64_t s_part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = ceil_div(total, (int64_t)blockDim.x);
-  const int64_t a = t * per, b = min(total, a + per);
-  int64_t sum = 0;
-  for (int64_t i = a; i < b; ++i) sum += counts[i];
-  s_part[t] = sum;
-  __syncthreads();
-  if (t == 0) {
-    int64_t run = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      const int64_t v = s_part[i];
-      s_part[i] = run;
-      run += v;
-    }
+__global__ void segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks,
+                                       int64_t R, int64_t* __restrict__ seg_off,
+                                       int64_t* __restrict__ piece_off) {
+  if (threadIdx.x != 0) return;
+  int64_t p = 0;
+  for (int j = 0; j < nkeys; ++j) {
+    const int64_t a = base[(int64_t)j * n_chunks];
+    const int64_t b = j + 1 < nkeys ? (int64_t)base[(int64_t)(j + 1) * n_chunks] : R;
+    seg_off[j] = a;
+    piece_off[j] = p;
+    p += ceil_div(b - a, (int64_t)kPiece);
   }
-  __syncthreads();
-  int64_t run = s_part[t];
-  for (int64_t i = a; i < b; ++i) {
-    const int64_t v = counts[i];
-    counts[i] = (int)run;
-    if (i % n_chunks == 0) seg_off[i / n_chunks] = run;
-    run += v;
-  }
-  __syncthreads();
-  if (t == 0) {
-    seg_off[nkeys] = R;
-    int64_t p = 0;
-    for (int j = 0; j < nkeys; ++j) {
-      piece_off[j] = p;
-      p += ceil_div(seg_off[j + 1] - seg_off[j], (int64_t)kPiece);
-    }
-    piece_off[nkeys] = p;
-  }
+  seg_off[nkeys] = R;
+  piece_off[nkeys] = p;
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -149,6 +129,35 @@ piece_sum_kernel(const float* __restrict__ vals, const int32_t* __restrict__ per
   const int key = lo;
   const int64_t r0 = seg_off[key] + (piece - piece_off[key]) * kPiece;
   const int64_t r1 = min(seg_off[key + 1], r0 + kPiece);
+  if ((D & 3) == 0) {
+    // float4 columns: a row is D/4 lanes wide
+    const int D4 = D >> 2;
+    const int span = (D4 <= kThreads && kThreads % D4 == 0) ? D4 : kThreads;
+    const int sub = kThreads / span;
+    const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+    float4* s4 = reinterpret_cast<float4*>(s_acc);
+    for (int d0 = 0; d0 < D4; d0 += span) {
+      const int d = d0 + lc;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (d < D4)
+        for (int64_t r = r0 + lr; r < r1; r += sub) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(vals + (int64_t)__ldg(perm + r) * D) + d);
+          acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+        }
+      s4[threadIdx.x] = acc;
+      __syncthreads();
+      if (threadIdx.x < span && d0 + threadIdx.x < D4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < sub; ++s) {
+          const float4 y = s4[s * span + threadIdx.x];
+          a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
+        }
+        reinterpret_cast<float4*>(piece_out + piece * D)[d0 + threadIdx.x] = a;
+      }
+      __syncthreads();
+    }
+    return;
+  }
   const int span = (D <= kThreads && kThreads % D == 0) ? D : kThreads;
   const int sub = kThreads / span;
   const int lr = threadIdx.x / span, lc = threadIdx.x % span;
@@ -182,20 +191,27 @@ __global__ void key_sum_kernel(const float* __restrict__ piece_out,
   }
 }
 
-size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t cub_scan_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const int*>(nullptr),
+                                static_cast<int*>(nullptr), (int)std::max<int64_t>(n, 1));
+  return bytes;
+}
 
 }  // namespace
 }  // namespace accel
 
 using namespace accel;
 
-extern "C" int accel_prev_keys(const int32_t* tokens, int64_t N, int K, int A, int32_t* keys,
-                               void* stream) {
+extern "C" int accel_prev_keys(const int32_t* tokens, int64_t N, int K, int A, int with_pos,
+                               int32_t* keys, void* stream) {
   if (N < 0 || K < 1 || A < 1) return fail(kDimension, "prev_keys: bad sizes");
   if (N == 0) return kOk;
   const int64_t M = N * K;
   const int grid = (int)std::min<int64_t>(ceil_div(M, kThreads), (int64_t)kNumSMs * 8);
-  prev_keys_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(tokens, M, K, A, keys);
+  prev_keys_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(tokens, M, K, A, with_pos, keys);
   return post_launch("prev_keys_kernel");
 }
 
@@ -212,7 +228,8 @@ extern "C" int accel_step_keys(const int32_t* steps, const int32_t* frame_of, in
 
 extern "C" size_t accel_group_workspace_size(int64_t R, int nkeys) {
   const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
-  return align16(sizeof(int) * (size_t)nkeys * n_chunks) + 16;
+  const int64_t n = (int64_t)nkeys * n_chunks;
+  return 2 * align256(sizeof(int) * (size_t)n) + align256(cub_scan_bytes(n)) + 256;
 }
 
 extern "C" int64_t accel_group_max_pieces(int64_t R, int nkeys) {
@@ -226,13 +243,20 @@ extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int
   if (R < 0 || nkeys < 1) return fail(kDimension, "group_by_key: bad sizes");
   if (nkeys * (size_t)kWarps * sizeof(int) > 200 * 1024)
     return fail(kDimension, "group_by_key: %d keys exceed the shared-memory histogram", nkeys);
+  if (R >= ((int64_t)1 << 31)) return fail(kDimension, "group_by_key: R exceeds int32 range");
   if (!keys || !perm || !seg_off || !piece_off || !workspace)
     return fail(kDimension, "group_by_key: NULL buffer");
   if (workspace_bytes < accel_group_workspace_size(R, nkeys))
     return fail(kDimension, "group_by_key: workspace too small");
   cudaStream_t s = as_stream(stream);
   const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
-  int* counts = static_cast<int*>(workspace);
+  const int64_t n = (int64_t)nkeys * n_chunks;
+  if (n >= ((int64_t)1 << 31)) return fail(kDimension, "group_by_key: too many counters");
+  char* ws = static_cast<char*>(workspace);
+  int* counts = reinterpret_cast<int*>(ws);
+  int* base = reinterpret_cast<int*>(ws + align256(sizeof(int) * (size_t)n));
+  void* cub_tmp = ws + 2 * align256(sizeof(int) * (size_t)n);
+  size_t cub_bytes = cub_scan_bytes(n);
   const size_t smem = sizeof(int) * (size_t)nkeys * kWarps;
   const int grid = (int)ceil_div(n_chunks, kWarps);
   int st;
@@ -243,11 +267,13 @@ extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int
   }
   chunk_hist_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, counts);
   if ((st = post_launch("chunk_hist_kernel"))) return st;
-  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, (int64_t)nkeys * n_chunks, nkeys, n_chunks, R,
-                                        seg_off, piece_off);
-  if ((st = post_launch("scan_counts_kernel"))) return st;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, counts, base, (int)n, s);
+  if (e != cudaSuccess) return fail(kCuda, "DeviceScan: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  segment_offsets_kernel<<<1, 32, 0, s>>>(base, nkeys, n_chunks, R, seg_off, piece_off);
+  if ((st = post_launch("segment_offsets_kernel"))) return st;
   if (R == 0) return kOk;
-  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, counts, perm);
+  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, base, perm);
   return post_launch("stable_scatter_kernel");
 }
 
@@ -260,10 +286,12 @@ extern "C" int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const
   if (R < 0 || D < 1 || nkeys < 1 || n_pieces < 0) return fail(kDimension, "grouped_rows_sum: bad sizes");
   if (!vals || !perm || !seg_off || !piece_off || !piece_buf || !out)
     return fail(kDimension, "grouped_rows_sum: NULL buffer");
+  if ((D & 3) == 0 && ((reinterpret_cast<uintptr_t>(vals) | reinterpret_cast<uintptr_t>(piece_buf)) & 15))
+    return fail(kDimension, "grouped_rows_sum: vals/piece_buf must be 16B aligned");
   cudaStream_t s = as_stream(stream);
   int st;
   if (n_pieces > 0) {
-    piece_sum_kernel<<<(unsigned)n_pieces, kThreads, kThreads * sizeof(float), s>>>(
+    piece_sum_kernel<<<(unsigned)n_pieces, kThreads, kThreads * sizeof(float4), s>>>(
         vals, perm, seg_off, piece_off, nkeys, D, piece_buf);
     if ((st = post_launch("piece_sum_kernel"))) return st;
   }

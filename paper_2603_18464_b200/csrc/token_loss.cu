@@ -7,14 +7,22 @@
 //                    entropy_bonus (:242-251) + the dlogits assembly of
 //                    train_step (:425-435), forward AND backward in one pass:
 //                    each logit row is read once and its dlogits row written
-//                    once (2*A*4 + 13 B/token, HBM-bound).
+//                    once (2*A*4 + 12 B/token, HBM-bound).
 //
-// Layout: warp-per-row; each lane holds VPL logits of the row (float4 loads
-// when A % 4 == 0).  Row statistics (max, sum-exp, entropy) use xor-shuffle
-// butterflies (deterministic).  Per-token scalar algebra is float except the
-// rare tails (|log-ratio| >= 60 or a trust weight below e^-75) which switch
-// to float64 so ratio overflow/underflow follows the reference's float64
-// exclusion rule (isfinite(r) & r > 0, trainer.py:204-205).
+// Layout: warp-per-row; each lane holds VPL logits of the row.  When rows
+// are 16-byte multiples (A % 4 == 0, A >= 128) the rows are streamed into a
+// per-warp shared-memory ring by the TMA bulk-copy engine
+// (cp.async.bulk + mbarrier complete_tx, STAGES rows in flight per warp), so
+// memory-level parallelism does not cost registers; otherwise rows are
+// loaded straight into registers.  Row statistics use xor-shuffle
+// butterflies (deterministic).  exp(z - max) is evaluated once per logit and
+// reused for the partition function, the entropy and the gradient:
+//   H = log s - (sum e d)/s,  dz = p (lambda_h/NK (d - sum e d / s) - c) + c [a == tok]
+// with d = z - max, e = exp(d), p = e / s, c = the token's surrogate coefficient.
+// Per-token scalar algebra is float except the rare tails (|log-ratio| >= 60
+// or a trust weight below e^-75), which switch to float64 so ratio
+// overflow/underflow follows the reference's float64 exclusion rule
+// (isfinite(r) & r > 0, trainer.py:204-205).
 //
 // The surrogate gradient carries 1/m, m = #included tokens — a GLOBAL count
 // (all ranks).  The kernel writes dlogits with the optimistic m0 = M_global
@@ -30,9 +38,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRows = 2;  // rows in flight per warp
+constexpr int kRows = 2;     // rows in flight per warp (register path)
+constexpr int kStages = 4;   // rows in flight per warp (TMA path)
 
-// per-block float64 partial sums (order matters: see accel.h LOSS_STAT_*)
+// per-block float64 partial sums (layout documented in accel.h)
 enum : int {
   kLossNum = 0,    // sum over included tokens of w*r*a (trust) or min(r a, clip(r) a)
   kEntSum = 1,     // sum of per-token entropy over ALL tokens
@@ -69,21 +78,22 @@ struct RowLayout {
       v = tok >> 5;
     }
   }
+  // global or shared source (generic pointers)
   __device__ __forceinline__ static void load(const float* __restrict__ row, int lane, int A,
-                                              float (&z)[VPL]) {
+                                              float (&z)[VPL], bool streaming) {
     if (VEC) {
 #pragma unroll
       for (int q = 0; q < VPL / 4; ++q) {
         const int c = q * 128 + lane * 4;
-        float4 x = c < A ? __ldcs(reinterpret_cast<const float4*>(row + c))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4* p = reinterpret_cast<const float4*>(row + c);
+        float4 x = c < A ? (streaming ? __ldcs(p) : *p) : make_float4(0.f, 0.f, 0.f, 0.f);
         z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
       }
     } else {
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int c = v * 32 + lane;
-        z[v] = c < A ? __ldcs(row + c) : 0.f;
+        z[v] = c < A ? (streaming ? __ldcs(row + c) : row[c]) : 0.f;
       }
     }
   }
@@ -107,15 +117,15 @@ struct RowLayout {
   }
 };
 
+// Row statistics; on return z[] holds d = z - max and e[] holds exp(d).
 struct RowStats {
-  float mx, lse, inv_s, H, z_tok;
+  float log_s, inv_s, sd_over_s, H, d_tok;
   bool bad;
 };
 
-// log-sum-exp, softmax denominator, entropy and the chosen-token logit.
 template <int VPL, bool VEC>
-__device__ __forceinline__ RowStats row_stats(const float (&z)[VPL], int lane, int A, int tok,
-                                              bool with_entropy) {
+__device__ __forceinline__ RowStats row_stats(float (&z)[VPL], float (&e)[VPL], int lane, int A,
+                                              int tok, bool with_entropy) {
   using L = RowLayout<VPL, VEC>;
   RowStats s;
   float mx = -CUDART_INF_F;
@@ -129,30 +139,34 @@ __device__ __forceinline__ RowStats row_stats(const float (&z)[VPL], int lane, i
   }
   s.bad = __any_sync(0xffffffffu, bad);
   mx = warp_max(mx);
-  float sum = 0.f;
+  float sum = 0.f, sed = 0.f;
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) sum += L::col(lane, v) < A ? __expf(z[v] - mx) : 0.f;
-  sum = warp_sum(sum);
-  s.mx = mx;
-  s.inv_s = 1.f / sum;
-  s.lse = mx + __logf(sum);
-  s.H = 0.f;
-  if (with_entropy) {
-    float acc = 0.f;
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      if (L::col(lane, v) < A) {
-        const float p = __expf(z[v] - mx) * s.inv_s;
-        acc = fmaf(p, z[v] - s.lse, acc);
-      }
-    s.H = -warp_sum(acc);
+  for (int v = 0; v < VPL; ++v) {
+    const bool ok = L::col(lane, v) < A;
+    z[v] = ok ? z[v] - mx : 0.f;
+    e[v] = ok ? __expf(z[v]) : 0.f;
+    sum += e[v];
+    sed = fmaf(e[v], z[v], sed);
   }
+  if (with_entropy) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      sed += __shfl_xor_sync(0xffffffffu, sed, o);
+    }
+  } else {
+    sum = warp_sum(sum);
+  }
+  s.inv_s = 1.f / sum;
+  s.log_s = __logf(sum);
+  s.sd_over_s = sed * s.inv_s;
+  s.H = s.log_s - s.sd_over_s;
   int tl, tv;
   L::locate(tok, tl, tv);
   float pick = 0.f;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) pick = (v == tv) ? z[v] : pick;
-  s.z_tok = __shfl_sync(0xffffffffu, pick, tl);
+  s.d_tok = __shfl_sync(0xffffffffu, pick, tl);
   return s;
 }
 
@@ -178,6 +192,169 @@ __device__ __forceinline__ void token_scalars(T delta, T a, const LossParams& p,
   }
 }
 
+template <int VPL>
+struct LossAcc {
+  float dbias[VPL];
+  double loss_num, ent_sum, ratio_sum, w_sum, rmax, negwmin;
+  int n_out, n_excl, n_bad, n_badtok;
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) dbias[v] = 0.f;
+    loss_num = ent_sum = ratio_sum = w_sum = 0.0;
+    rmax = negwmin = -CUDART_INF;
+    n_out = n_excl = n_bad = n_badtok = 0;
+  }
+};
+
+struct RowCtx {
+  LossParams prm;
+  float inv_m, ent_scale;
+  double inv_m_d;
+  bool fixup;
+};
+
+// Everything after the logits of one row are in registers (bias not yet added).
+template <int VPL, bool VEC>
+__device__ __forceinline__ void loss_row(float (&z)[VPL], const float* __restrict__ s_bias,
+                                         int64_t row, int lane, int A, int K,
+                                         const int32_t* __restrict__ tokens,
+                                         const float* __restrict__ lp_old,
+                                         const float* __restrict__ adv, const RowCtx& cx,
+                                         float* __restrict__ dlogits, float* __restrict__ lp_new,
+                                         LossAcc<VPL>& acc) {
+  using L = RowLayout<VPL, VEC>;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) z[v] += s_bias[L::col(lane, v)];
+  int tok = __ldg(tokens + row);
+  const bool bad_tok = tok < 0 || tok >= A;
+  if (bad_tok) tok = 0;
+  float e[VPL];
+  const RowStats rs = row_stats<VPL, VEC>(z, e, lane, A, tok, true);
+  const float lpn = rs.d_tok - rs.log_s;
+  const float dlt = lpn - __ldg(lp_old + row);
+  const float a = __ldg(adv + row / K);
+  // reference exclusion: exp(delta) in float64 finite and > 0
+  const bool inc = !bad_tok && !rs.bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
+  float coef = 0.f;
+  double term_d = 0.0, r_d = 1.0, w_d = 1.0;
+  bool outside = false;
+  if (inc) {
+    const float qq = dlt / cx.prm.sigma;
+    if (fabsf(dlt) < 60.f && (cx.prm.algo != 0 || qq * qq < 150.f)) {
+      float cf, tf, rf, wf;
+      token_scalars<float>(dlt, a, cx.prm, cf, tf, rf, wf, outside);
+      coef = cf * cx.inv_m;
+      term_d = tf; r_d = rf; w_d = wf;
+    } else {
+      double cd;
+      token_scalars<double>((double)dlt, (double)a, cx.prm, cd, term_d, r_d, w_d, outside);
+      coef = (float)(cd * cx.inv_m_d);
+    }
+  }
+  // dz = p (ent_scale (d - sd/s) - coef) + coef [a == tok]
+  float g[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int c = L::col(lane, v);
+    const float p = e[v] * rs.inv_s;
+    const float t = fmaf(cx.ent_scale, z[v] - rs.sd_over_s, -coef);
+    float x = fmaf(p, t, c == tok ? coef : 0.f);
+    x = c < A ? x : 0.f;
+    g[v] = x;
+    acc.dbias[v] += x;
+  }
+  L::store(dlogits + row * A, lane, A, g);
+  if (!cx.fixup) {
+    if (lane == 0) lp_new[row] = lpn;
+    acc.ent_sum += (double)rs.H;
+    acc.n_bad += rs.bad;
+    acc.n_badtok += bad_tok;
+    if (inc) {
+      acc.loss_num += term_d;
+      acc.ratio_sum += r_d;
+      acc.w_sum += w_d;
+      acc.n_out += outside;
+      acc.rmax = fmax(acc.rmax, r_d);
+      acc.negwmin = fmax(acc.negwmin, -w_d);
+    } else {
+      ++acc.n_excl;
+    }
+  }
+}
+
+__device__ __forceinline__ bool setup_ctx(const LossParams& prm, const double* fix_stats,
+                                          RowCtx& cx) {
+  cx.prm = prm;
+  cx.fixup = fix_stats != nullptr;
+  double m_eff = prm.m_global;
+  if (cx.fixup) {
+    const double excl = fix_stats[kExcluded];
+    if (excl == 0.0 || excl >= prm.m_global) return false;  // uniform early exit
+    m_eff = prm.m_global - excl;
+  }
+  cx.inv_m = (float)(1.0 / m_eff);
+  cx.inv_m_d = 1.0 / m_eff;
+  cx.ent_scale = prm.lambda_h * (float)prm.inv_nk;
+  return true;
+}
+
+// fixed-order block reduction of the bias gradient and the token statistics
+template <int VPL, bool VEC>
+__device__ __forceinline__ void loss_epilogue(const LossAcc<VPL>& acc, int A, bool fixup,
+                                              float* s_dbias /*[kWarps][VPL*32]*/,
+                                              double* s_stat /*[kWarps][10]*/,
+                                              float* __restrict__ dbias_part,
+                                              double* __restrict__ stat_part,
+                                              double* __restrict__ max_part) {
+  using L = RowLayout<VPL, VEC>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NS = kNumStat + kNumMax;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) s_dbias[warp * VPL * 32 + v * 32 + lane] = acc.dbias[v];
+  if (!fixup && lane == 0) {
+    double* st = s_stat + warp * NS;
+    st[kLossNum] = acc.loss_num;
+    st[kEntSum] = acc.ent_sum;
+    st[kRatioSum] = acc.ratio_sum;
+    st[kWSum] = acc.w_sum;
+    st[kOutside] = acc.n_out;
+    st[kExcluded] = acc.n_excl;
+    st[kBadRows] = acc.n_bad;
+    st[kBadTok] = acc.n_badtok;
+    st[kNumStat + kRatioMax] = acc.rmax;
+    st[kNumStat + kNegWMin] = acc.negwmin;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < VPL * 32; idx += kThreads) {
+    const int v = idx >> 5, ln = idx & 31;
+    const int c = L::col(ln, v);
+    if (c < A) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += s_dbias[w * VPL * 32 + idx];
+      dbias_part[(int64_t)blockIdx.x * A + c] = s;
+    }
+  }
+  if (!fixup && threadIdx.x == 0) {
+    double sum[NS];
+#pragma unroll
+    for (int i = 0; i < kNumStat; ++i) sum[i] = 0.0;
+    sum[kNumStat + kRatioMax] = -CUDART_INF;
+    sum[kNumStat + kNegWMin] = -CUDART_INF;
+    for (int w = 0; w < kWarps; ++w) {
+#pragma unroll
+      for (int i = 0; i < kNumStat; ++i) sum[i] += s_stat[w * NS + i];
+#pragma unroll
+      for (int i = kNumStat; i < NS; ++i) sum[i] = fmax(sum[i], s_stat[w * NS + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kNumStat; ++i) stat_part[(int64_t)blockIdx.x * kNumStat + i] = sum[i];
+    max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = sum[kNumStat + kRatioMax];
+    max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = sum[kNumStat + kNegWMin];
+  }
+}
+
+// ---- register path (any A <= 1024) -----------------------------------------------
 template <int VPL, bool VEC>
 __global__ void __launch_bounds__(kThreads, 3)
 token_loss_kernel(const float* __restrict__ logits, const float* __restrict__ bias,
@@ -187,182 +364,330 @@ token_loss_kernel(const float* __restrict__ logits, const float* __restrict__ bi
                   float* __restrict__ lp_new, float* __restrict__ dbias_part,
                   double* __restrict__ stat_part, double* __restrict__ max_part) {
   using L = RowLayout<VPL, VEC>;
-  __shared__ float s_dbias[kWarps][VPL * 32];
-  __shared__ double s_stat[kWarps][kNumStat + kNumMax];
-
-  const bool fixup = fix_stats != nullptr;
-  double m_eff = prm.m_global;
-  if (fixup) {
-    const double excl = fix_stats[kExcluded];
-    if (excl == 0.0 || excl >= prm.m_global) return;  // uniform early exit
-    m_eff = prm.m_global - excl;
-  }
-  const float inv_m = (float)(1.0 / m_eff);
-  const double inv_m_d = 1.0 / m_eff;
-  const float ent_scale = prm.lambda_h * (float)prm.inv_nk;
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ float s_dbias[kWarps * VPL * 32];
+  __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
   __shared__ float s_bias[VPL * 32];
+  RowCtx cx;
+  if (!setup_ctx(prm, fix_stats, cx)) return;
   for (int c = threadIdx.x; c < VPL * 32; c += kThreads) s_bias[c] = c < A ? __ldg(bias + c) : 0.f;
   __syncthreads();
-  float dbias[VPL];
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) dbias[v] = 0.f;
-  // float64 sums; integer counters
-  double loss_num = 0.0, ent_sum = 0.0, ratio_sum = 0.0, w_sum = 0.0;
-  int n_out = 0, n_excl = 0, n_bad = 0, n_badtok = 0;
-  double rmax = -CUDART_INF, negwmin = -CUDART_INF;
-
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  LossAcc<VPL> acc;
+  acc.init();
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t stride = (int64_t)gridDim.x * kWarps * kRows;
   for (int64_t base = gw * kRows; base < M; base += stride) {
     float z[kRows][VPL];
 #pragma unroll
     for (int r = 0; r < kRows; ++r)
-      if (base + r < M) L::load(logits + (base + r) * A, lane, A, z[r]);
+      if (base + r < M) L::load(logits + (base + r) * A, lane, A, z[r], true);
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
-      const int64_t row = base + r;
-      if (row >= M) break;
+      if (base + r >= M) break;
+      loss_row<VPL, VEC>(z[r], s_bias, base + r, lane, A, K, tokens, lp_old, adv, cx, dlogits,
+                         lp_new, acc);
+    }
+  }
+  loss_epilogue<VPL, VEC>(acc, A, cx.fixup, s_dbias, s_stat, dbias_part, stat_part, max_part);
+}
+
+// ---- TMA bulk-copy path (A % 4 == 0, 128 <= A <= 1024) ----------------------------
+// dynamic smem: [kWarps][kStages][VPL*32] floats, then [kWarps][kStages] mbarriers
+template <int VPL>
+__global__ void __launch_bounds__(kThreads, 3)
+token_loss_tma_kernel(const float* __restrict__ logits, const float* __restrict__ bias,
+                      const int32_t* __restrict__ tokens, const float* __restrict__ lp_old,
+                      const float* __restrict__ adv, int64_t M, int K, int A, LossParams prm,
+                      const double* __restrict__ fix_stats, float* __restrict__ dlogits,
+                      float* __restrict__ lp_new, float* __restrict__ dbias_part,
+                      double* __restrict__ stat_part, double* __restrict__ max_part) {
+  using L = RowLayout<VPL, true>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ float s_dbias[kWarps * VPL * 32];
+  __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
+  __shared__ float s_bias[VPL * 32];
+  RowCtx cx;
+  if (!setup_ctx(prm, fix_stats, cx)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * VPL * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * VPL * 32 * 4) +
+                   warp * kStages;
+  for (int c = threadIdx.x; c < VPL * 32; c += kThreads) s_bias[c] = c < A ? __ldg(bias + c) : 0.f;
+  const unsigned row_bytes = (unsigned)A * 4u;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  if (lane == 0) {
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) z[r][v] += s_bias[L::col(lane, v)];
-      int tok = __ldg(tokens + row);
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t row = gw + s * nw;
+      if (row < M) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * VPL * 32, logits + row * A, row_bytes, &bars[s]);
+      }
+    }
+  }
+  __syncthreads();
+  LossAcc<VPL> acc;
+  acc.init();
+  int j = 0;
+  for (int64_t row = gw; row < M; row += nw, ++j) {
+    const int s = j % kStages;
+    mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    float z[VPL];
+    L::load(ring + s * VPL * 32, lane, A, z, false);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t next = row + kStages * nw;
+      if (next < M) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * VPL * 32, logits + next * A, row_bytes, &bars[s]);
+      }
+    }
+    loss_row<VPL, true>(z, s_bias, row, lane, A, K, tokens, lp_old, adv, cx, dlogits, lp_new,
+                        acc);
+  }
+  loss_epilogue<VPL, true>(acc, A, cx.fixup, s_dbias, s_stat, dbias_part, stat_part, max_part);
+}
+
+// ---- factorized head: logits never materialized ----------------------------------------
+// logits[i, k] = H2W[frame_of[i]] + EP[prev(i, k)] + PP[k] + b_head, with
+//   H2W = h2 @ W_head^T (frame rows), EP = e_prev @ W_head^T, PP = e_pos @ W_head^T
+// (models.py:181-182 distributed over the sum c = h2 + e_prev[prev] + e_pos).
+// One warp owns a whole transition (K consecutive token rows): the H2W row is
+// streamed once into the warp's smem ring by the bulk-copy engine, EP rows
+// come from L2 (prefetched one token ahead), PP + bias sit in smem.  Outputs:
+//   dz      f32[M, A]  per-token dlogits (token-major), consumed by the
+//                      (prev, k)-grouped row sum for the e_prev / e_pos / W_head terms
+//   g_frame f32[F, A]  G = sum_k dz[i, k] written to the transition's frame row
+//                      (bootstrap rows are left untouched: pre-zero), consumed
+//                      by dW_head += G^T h2 and dh2 = G W_head.
+template <int VPL>
+__global__ void __launch_bounds__(kThreads, 2)
+token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ ep,
+                       const float* __restrict__ pp, const float* __restrict__ bias,
+                       const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
+                       const float* __restrict__ lp_old, const float* __restrict__ adv, int64_t N,
+                       int K, int A, LossParams prm, const double* __restrict__ fix_stats,
+                       float* __restrict__ dz, float* __restrict__ g_frame,
+                       float* __restrict__ lp_new, double* __restrict__ stat_part,
+                       double* __restrict__ max_part) {
+  using L = RowLayout<VPL, true>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
+  RowCtx cx;
+  if (!setup_ctx(prm, fix_stats, cx)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // smem: ring [kWarps][kStages][VPL*32] | s_pp [K][VPL*32] | bars [kWarps][kStages]
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * VPL * 32;
+  float* s_pp = reinterpret_cast<float*>(smem) + (size_t)kWarps * kStages * VPL * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_pp + (size_t)K * VPL * 32) + warp * kStages;
+  for (int e = threadIdx.x; e < K * VPL * 32; e += kThreads) {
+    const int k = e / (VPL * 32), c = e % (VPL * 32);
+    s_pp[e] = c < A ? __ldg(pp + (int64_t)k * A + c) + __ldg(bias + c) : 0.f;
+  }
+  const unsigned row_bytes = (unsigned)A * 4u;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  int f_ahead = 0;  // lane 0: frame row of the transition kStages iterations ahead
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t i = gw + s * nw;
+      if (i < N) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * VPL * 32, h2w + (int64_t)__ldg(frame_of + i) * A, row_bytes,
+                 &bars[s]);
+      }
+    }
+    const int64_t i2 = gw + kStages * nw;
+    if (i2 < N) f_ahead = __ldg(frame_of + i2);
+  }
+  __syncthreads();
+  LossAcc<VPL> acc;
+  acc.init();
+  int j = 0;
+  for (int64_t i = gw; i < N; i += nw, ++j) {
+    const int s = j % kStages;
+    const int fi = __ldg(frame_of + i);
+    const int tok_l = lane < K ? __ldg(tokens + i * K + lane) : 0;
+    mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    float h[VPL];
+    L::load(ring + s * VPL * 32, lane, A, h, false);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t next = i + kStages * nw;
+      if (next < N) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * VPL * 32, h2w + (int64_t)f_ahead * A, row_bytes, &bars[s]);
+        const int64_t i2 = next + nw;
+        if (i2 < N) f_ahead = __ldg(frame_of + i2);
+      }
+    }
+    float g[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) g[v] = 0.f;
+    float epn[VPL];
+    {
+      const float* er = ep + (int64_t)A * A;  // k = 0: chunk-start row
+#pragma unroll
+      for (int q = 0; q < VPL / 4; ++q) {
+        const int c = q * 128 + lane * 4;
+        float4 x = c < A ? __ldg(reinterpret_cast<const float4*>(er + c))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        epn[4 * q] = x.x; epn[4 * q + 1] = x.y; epn[4 * q + 2] = x.z; epn[4 * q + 3] = x.w;
+      }
+    }
+    for (int k = 0; k < K; ++k) {
+      float z[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) z[v] = h[v] + epn[v] + s_pp[k * VPL * 32 + L::col(lane, v)];
+      const int tok_k = __shfl_sync(0xffffffffu, tok_l, k);
+      if (k + 1 < K) {  // prefetch next token's EP row (prev = this token)
+        const int pv = min(max(tok_k, 0), A);
+        const float* er = ep + (int64_t)pv * A;
+#pragma unroll
+        for (int q = 0; q < VPL / 4; ++q) {
+          const int c = q * 128 + lane * 4;
+          float4 x = c < A ? __ldg(reinterpret_cast<const float4*>(er + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          epn[4 * q] = x.x; epn[4 * q + 1] = x.y; epn[4 * q + 2] = x.z; epn[4 * q + 3] = x.w;
+        }
+      }
+      // one token row: same algebra as loss_row (bias already folded into s_pp)
+      const int64_t row = i * K + k;
+      int tok = tok_k;
       const bool bad_tok = tok < 0 || tok >= A;
       if (bad_tok) tok = 0;
-      const RowStats rs = row_stats<VPL, VEC>(z[r], lane, A, tok, true);
-      const float lpn = rs.z_tok - rs.lse;
+      float e[VPL];
+      const RowStats rs = row_stats<VPL, true>(z, e, lane, A, tok, true);
+      const float lpn = rs.d_tok - rs.log_s;
       const float dlt = lpn - __ldg(lp_old + row);
-      const float a = __ldg(adv + row / K);
-      // reference exclusion: exp(delta) in float64 finite and > 0
+      const float a = __ldg(adv + i);
       const bool inc = !bad_tok && !rs.bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
       float coef = 0.f;
       double term_d = 0.0, r_d = 1.0, w_d = 1.0;
       bool outside = false;
       if (inc) {
-        const float qq = dlt / prm.sigma;
-        if (fabsf(dlt) < 60.f && (prm.algo != 0 || qq * qq < 150.f)) {
+        const float qq = dlt / cx.prm.sigma;
+        if (fabsf(dlt) < 60.f && (cx.prm.algo != 0 || qq * qq < 150.f)) {
           float cf, tf, rf, wf;
-          token_scalars<float>(dlt, a, prm, cf, tf, rf, wf, outside);
-          coef = cf * inv_m;
+          token_scalars<float>(dlt, a, cx.prm, cf, tf, rf, wf, outside);
+          coef = cf * cx.inv_m;
           term_d = tf; r_d = rf; w_d = wf;
         } else {
           double cd;
-          token_scalars<double>((double)dlt, (double)a, prm, cd, term_d, r_d, w_d, outside);
-          coef = (float)(cd * inv_m_d);
+          token_scalars<double>((double)dlt, (double)a, cx.prm, cd, term_d, r_d, w_d, outside);
+          coef = (float)(cd * cx.inv_m_d);
         }
       }
-      // dlogits = dlogp (onehot - p) + lambda_h p (lp + H) / (N K)
       float d[VPL];
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int c = L::col(lane, v);
-        const float p = __expf(z[r][v] - rs.mx) * rs.inv_s;
-        const float lp = z[r][v] - rs.lse;
-        float g = coef * ((c == tok ? 1.f : 0.f) - p) + ent_scale * p * (lp + rs.H);
-        g = c < A ? g : 0.f;
-        d[v] = g;
-        dbias[v] += g;
+        const float p = e[v] * rs.inv_s;
+        const float t = fmaf(cx.ent_scale, z[v] - rs.sd_over_s, -coef);
+        float x = fmaf(p, t, c == tok ? coef : 0.f);
+        x = c < A ? x : 0.f;
+        d[v] = x;
+        g[v] += x;
       }
-      L::store(dlogits + row * A, lane, A, d);
-      if (!fixup) {
+      L::store(dz + row * A, lane, A, d);
+      if (!cx.fixup) {
         if (lane == 0) lp_new[row] = lpn;
-        ent_sum += (double)rs.H;
-        n_bad += rs.bad;
-        n_badtok += bad_tok;
+        acc.ent_sum += (double)rs.H;
+        acc.n_bad += rs.bad;
+        acc.n_badtok += bad_tok;
         if (inc) {
-          loss_num += term_d;
-          ratio_sum += r_d;
-          w_sum += w_d;
-          n_out += outside;
-          rmax = fmax(rmax, r_d);
-          negwmin = fmax(negwmin, -w_d);
+          acc.loss_num += term_d;
+          acc.ratio_sum += r_d;
+          acc.w_sum += w_d;
+          acc.n_out += outside;
+          acc.rmax = fmax(acc.rmax, r_d);
+          acc.negwmin = fmax(acc.negwmin, -w_d);
         } else {
-          ++n_excl;
+          ++acc.n_excl;
         }
       }
     }
+    L::store(g_frame + (int64_t)fi * A, lane, A, g);
   }
-
-  // fixed-order block reduction of the bias gradient
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) s_dbias[warp][v * 32 + lane] = dbias[v];
-  if (!fixup && lane == 0) {
-    s_stat[warp][kLossNum] = loss_num;
-    s_stat[warp][kEntSum] = ent_sum;
-    s_stat[warp][kRatioSum] = ratio_sum;
-    s_stat[warp][kWSum] = w_sum;
-    s_stat[warp][kOutside] = n_out;
-    s_stat[warp][kExcluded] = n_excl;
-    s_stat[warp][kBadRows] = n_bad;
-    s_stat[warp][kBadTok] = n_badtok;
-    s_stat[warp][kNumStat + kRatioMax] = rmax;
-    s_stat[warp][kNumStat + kNegWMin] = negwmin;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < VPL * 32; idx += kThreads) {
-    const int v = idx >> 5, ln = idx & 31;
-    const int c = L::col(ln, v);
-    if (c < A) {
-      float acc = 0.f;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) acc += s_dbias[w][idx];
-      dbias_part[(int64_t)blockIdx.x * A + c] = acc;
+  // statistics epilogue (dbias is not produced here: db_head = sum_k Dpos[k])
+  if (!cx.fixup) {
+    constexpr int NS = kNumStat + kNumMax;
+    if (lane == 0) {
+      double* st = s_stat + warp * NS;
+      st[kLossNum] = acc.loss_num;
+      st[kEntSum] = acc.ent_sum;
+      st[kRatioSum] = acc.ratio_sum;
+      st[kWSum] = acc.w_sum;
+      st[kOutside] = acc.n_out;
+      st[kExcluded] = acc.n_excl;
+      st[kBadRows] = acc.n_bad;
+      st[kBadTok] = acc.n_badtok;
+      st[kNumStat + kRatioMax] = acc.rmax;
+      st[kNumStat + kNegWMin] = acc.negwmin;
     }
-  }
-  if (!fixup && threadIdx.x == 0) {
-    double acc[kNumStat + kNumMax];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sum[NS];
 #pragma unroll
-    for (int i = 0; i < kNumStat; ++i) acc[i] = 0.0;
-    acc[kNumStat + kRatioMax] = -CUDART_INF;
-    acc[kNumStat + kNegWMin] = -CUDART_INF;
-    for (int w = 0; w < kWarps; ++w) {
+      for (int q = 0; q < kNumStat; ++q) sum[q] = 0.0;
+      sum[kNumStat + kRatioMax] = -CUDART_INF;
+      sum[kNumStat + kNegWMin] = -CUDART_INF;
+      for (int w = 0; w < kWarps; ++w) {
 #pragma unroll
-      for (int i = 0; i < kNumStat; ++i) acc[i] += s_stat[w][i];
-      acc[kNumStat + kRatioMax] = fmax(acc[kNumStat + kRatioMax], s_stat[w][kNumStat + kRatioMax]);
-      acc[kNumStat + kNegWMin] = fmax(acc[kNumStat + kNegWMin], s_stat[w][kNumStat + kNegWMin]);
+        for (int q = 0; q < kNumStat; ++q) sum[q] += s_stat[w * NS + q];
+#pragma unroll
+        for (int q = kNumStat; q < NS; ++q) sum[q] = fmax(sum[q], s_stat[w * NS + q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kNumStat; ++q) stat_part[(int64_t)blockIdx.x * kNumStat + q] = sum[q];
+      max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = sum[kNumStat + kRatioMax];
+      max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = sum[kNumStat + kNegWMin];
     }
-#pragma unroll
-    for (int i = 0; i < kNumStat; ++i) stat_part[(int64_t)blockIdx.x * kNumStat + i] = acc[i];
-    max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = acc[kNumStat + kRatioMax];
-    max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = acc[kNumStat + kNegWMin];
   }
 }
 
-template <int VPL, bool VEC>
-__global__ void __launch_bounds__(kThreads)
-token_logp_kernel(const float* __restrict__ mu, const int32_t* __restrict__ tokens, int64_t M,
-                  int A, float* __restrict__ lp_out, double* __restrict__ bad_part) {
-  using L = RowLayout<VPL, VEC>;
-  __shared__ double s_bad[kWarps][2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double bad_rows = 0.0, bad_tok = 0.0;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
-  const int64_t stride = (int64_t)gridDim.x * kWarps * kRows;
-  for (int64_t base = gw * kRows; base < M; base += stride) {
-    float z[kRows][VPL];
-#pragma unroll
-    for (int r = 0; r < kRows; ++r)
-      if (base + r < M) L::load(mu + (base + r) * A, lane, A, z[r]);
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int64_t row = base + r;
-      if (row >= M) break;
-      int tok = __ldg(tokens + row);
-      const bool bt = tok < 0 || tok >= A;
-      if (bt) tok = 0;
-      const RowStats rs = row_stats<VPL, VEC>(z[r], lane, A, tok, false);
-      if (lane == 0) lp_out[row] = rs.z_tok - rs.lse;
-      bad_rows += rs.bad ? 1.0 : 0.0;
-      bad_tok += bt ? 1.0 : 0.0;
+// Dprev[j] = sum_k Dpk[j, k], Dpos[k] = sum_j Dpk[j, k]  (Dpk f32[(A+1), K, A])
+__global__ void pk_marginals_kernel(const float* __restrict__ dpk, int K, int A, int nprev,
+                                    float* __restrict__ dprev, float* __restrict__ dpos) {
+  const int64_t total = (int64_t)(nprev + K) * A;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(e % A);
+    const int64_t r = e / A;
+    float s = 0.f;
+    if (r < nprev) {
+      for (int k = 0; k < K; ++k) s += dpk[(r * K + k) * A + a];
+      dprev[r * A + a] = s;
+    } else {
+      const int k = (int)(r - nprev);
+      for (int jj = 0; jj < nprev; ++jj) s += dpk[((int64_t)jj * K + k) * A + a];
+      dpos[(int64_t)k * A + a] = s;
     }
   }
+}
+
+// ---- behavior log-probs ---------------------------------------------------------------
+__device__ __forceinline__ void logp_block_epilogue(int bad_rows, int bad_tok,
+                                                    double* __restrict__ bad_part) {
+  __shared__ int s_bad[kWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) {
     s_bad[warp][0] = bad_rows;
     s_bad[warp][1] = bad_tok;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
+    int a = 0, b = 0;
     for (int w = 0; w < kWarps; ++w) {
       a += s_bad[w][0];
       b += s_bad[w][1];
@@ -372,10 +697,99 @@ token_logp_kernel(const float* __restrict__ mu, const int32_t* __restrict__ toke
   }
 }
 
+template <int VPL, bool VEC>
+__device__ __forceinline__ void logp_row(float (&z)[VPL], int64_t row, int lane, int A,
+                                         const int32_t* __restrict__ tokens,
+                                         float* __restrict__ lp_out, int& bad_rows, int& bad_tok) {
+  int tok = __ldg(tokens + row);
+  const bool bt = tok < 0 || tok >= A;
+  if (bt) tok = 0;
+  float e[VPL];
+  const RowStats rs = row_stats<VPL, VEC>(z, e, lane, A, tok, false);
+  if (lane == 0) lp_out[row] = rs.d_tok - rs.log_s;
+  bad_rows += rs.bad;
+  bad_tok += bt;
+}
+
+template <int VPL, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+token_logp_kernel(const float* __restrict__ mu, const int32_t* __restrict__ tokens, int64_t M,
+                  int A, float* __restrict__ lp_out, double* __restrict__ bad_part) {
+  using L = RowLayout<VPL, VEC>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bad_rows = 0, bad_tok = 0;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * kWarps * kRows;
+  for (int64_t base = gw * kRows; base < M; base += stride) {
+    float z[kRows][VPL];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+      if (base + r < M) L::load(mu + (base + r) * A, lane, A, z[r], true);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      if (base + r >= M) break;
+      logp_row<VPL, VEC>(z[r], base + r, lane, A, tokens, lp_out, bad_rows, bad_tok);
+    }
+  }
+  logp_block_epilogue(bad_rows, bad_tok, bad_part);
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(kThreads, 3)
+token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ tokens, int64_t M,
+                      int A, float* __restrict__ lp_out, double* __restrict__ bad_part) {
+  using L = RowLayout<VPL, true>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * VPL * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * VPL * 32 * 4) +
+                   warp * kStages;
+  const unsigned row_bytes = (unsigned)A * 4u;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t row = gw + s * nw;
+      if (row < M) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * VPL * 32, mu + row * A, row_bytes, &bars[s]);
+      }
+    }
+  }
+  __syncwarp();
+  int bad_rows = 0, bad_tok = 0, j = 0;
+  for (int64_t row = gw; row < M; row += nw, ++j) {
+    const int s = j % kStages;
+    mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    float z[VPL];
+    L::load(ring + s * VPL * 32, lane, A, z, false);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t next = row + kStages * nw;
+      if (next < M) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * VPL * 32, mu + next * A, row_bytes, &bars[s]);
+      }
+    }
+    logp_row<VPL, true>(z, row, lane, A, tokens, lp_out, bad_rows, bad_tok);
+  }
+  logp_block_epilogue(bad_rows, bad_tok, bad_part);
+}
+
+// ---- launch plumbing -------------------------------------------------------------------
 int grid_for_rows(int64_t M) {
   const int64_t warps_needed = ceil_div(M, kRows);
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps_needed, kWarps),
-                                                     (int64_t)kNumSMs * 6));
+                                                     (int64_t)kNumSMs * 3));
+}
+
+size_t tma_smem(int VPL) {
+  return (size_t)kWarps * kStages * (VPL * 32 * 4 + sizeof(uint64_t));
 }
 
 template <template <int, bool> class Launch, typename... Args>
@@ -390,6 +804,19 @@ int dispatch_vpl(int A, Args... args) {
   return fail(kDimension, "n_actions=%d exceeds the supported maximum of 1024", A);
 }
 
+template <typename KernelT>
+int launch_tma(KernelT kernel, int VPL, int grid, cudaStream_t s, const char* name,
+               auto... args) {
+  const size_t smem = tma_smem(VPL);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return fail(kCuda, "%s smem attribute: %s", name, cudaGetErrorString(e));
+  }
+  kernel<<<grid, kThreads, smem, s>>>(args...);
+  return post_launch(name);
+}
+
 template <int VPL, bool VEC>
 struct LossLaunch {
   static int run(const float* logits, const float* bias, const int32_t* tokens,
@@ -397,10 +824,16 @@ struct LossLaunch {
                  LossParams prm, const double* fix, float* dlogits, float* lp_new,
                  float* dbias_part, double* stat_part, double* max_part, int grid,
                  cudaStream_t s) {
-    token_loss_kernel<VPL, VEC><<<grid, kThreads, 0, s>>>(logits, bias, tokens, lp_old, adv, M,
-                                                          K, A, prm, fix, dlogits, lp_new,
-                                                          dbias_part, stat_part, max_part);
-    return post_launch("token_loss_kernel");
+    if constexpr (VEC && VPL >= 4) {
+      return launch_tma(token_loss_tma_kernel<VPL>, VPL, grid, s, "token_loss_tma_kernel",
+                        logits, bias, tokens, lp_old, adv, M, K, A, prm, fix, dlogits, lp_new,
+                        dbias_part, stat_part, max_part);
+    } else {
+      token_loss_kernel<VPL, VEC><<<grid, kThreads, 0, s>>>(logits, bias, tokens, lp_old, adv, M,
+                                                            K, A, prm, fix, dlogits, lp_new,
+                                                            dbias_part, stat_part, max_part);
+      return post_launch("token_loss_kernel");
+    }
   }
 };
 
@@ -408,8 +841,13 @@ template <int VPL, bool VEC>
 struct LogpLaunch {
   static int run(const float* mu, const int32_t* tokens, int64_t M, int A, float* lp,
                  double* bad_part, int grid, cudaStream_t s) {
-    token_logp_kernel<VPL, VEC><<<grid, kThreads, 0, s>>>(mu, tokens, M, A, lp, bad_part);
-    return post_launch("token_logp_kernel");
+    if constexpr (VEC && VPL >= 4) {
+      return launch_tma(token_logp_tma_kernel<VPL>, VPL, grid, s, "token_logp_tma_kernel", mu,
+                        tokens, M, A, lp, bad_part);
+    } else {
+      token_logp_kernel<VPL, VEC><<<grid, kThreads, 0, s>>>(mu, tokens, M, A, lp, bad_part);
+      return post_launch("token_logp_kernel");
+    }
   }
 };
 
@@ -421,6 +859,70 @@ bool misaligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) & 15; }
 using namespace accel;
 
 extern "C" int accel_token_grid(int64_t M) { return M > 0 ? grid_for_rows(M) : 1; }
+
+extern "C" int accel_fact_grid(int64_t N) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, kWarps), (int64_t)kNumSMs * 2));
+}
+
+extern "C" int accel_token_loss_fact(const float* h2w, const float* ep, const float* pp,
+                                     const float* bias, const int32_t* frame_of,
+                                     const int32_t* tokens, const float* lp_old, const float* adv,
+                                     int64_t N, int K, int A, int algo, double sigma,
+                                     double clip_eps, double lambda_h, double m_global,
+                                     const double* fix_stats, float* dz, float* g_frame,
+                                     float* lp_new, double* stat_part, double* max_part,
+                                     void* stream) {
+  if (algo != 0 && algo != 1) return fail(kDomain, "unknown algorithm %d", algo);
+  if (!(sigma > 0)) return fail(kDomain, "sigma must be > 0, got %g", sigma);
+  if (!(clip_eps > 0 && clip_eps < 1)) return fail(kDomain, "clip_eps must be in (0, 1)");
+  if (lambda_h < 0) return fail(kDomain, "loss coefficients must be >= 0");
+  if (N < 0 || K < 1 || K > 32 || A < 1) return fail(kDimension, "token_loss_fact: bad sizes");
+  if (A % 4 != 0 || A < 128 || A > 1024)
+    return fail(kDimension, "token_loss_fact needs 128 <= A <= 1024, A %% 4 == 0 (got %d)", A);
+  if (N == 0) return kOk;
+  if (!(m_global >= (double)(N * K))) return fail(kDimension, "m_global < local token count");
+  if (!h2w || !ep || !pp || !bias || !frame_of || !tokens || !lp_old || !adv || !dz || !g_frame ||
+      (!fix_stats && (!lp_new || !stat_part || !max_part)))
+    return fail(kDimension, "token_loss_fact: NULL buffer");
+  if (misaligned16(h2w) || misaligned16(ep) || misaligned16(dz) || misaligned16(g_frame))
+    return fail(kDimension, "token_loss_fact: buffers must be 16B aligned");
+  LossParams prm;
+  prm.algo = algo;
+  prm.sigma = (float)sigma;
+  prm.clip_lo = (float)(1.0 - clip_eps);
+  prm.clip_hi = (float)(1.0 + clip_eps);
+  prm.lambda_h = (float)lambda_h;
+  prm.inv_nk = 1.0 / m_global;
+  prm.m_global = m_global;
+  cudaStream_t s = as_stream(stream);
+  const int grid = accel_fact_grid(N);
+  auto go = [&](auto kernel, int VPL) -> int {
+    const size_t smem = (size_t)kWarps * kStages * (VPL * 32 * 4 + sizeof(uint64_t)) +
+                        (size_t)K * VPL * 32 * 4 + 16;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return fail(kCuda, "token_loss_fact smem: %s", cudaGetErrorString(e));
+    }
+    kernel<<<grid, kThreads, smem, s>>>(h2w, ep, pp, bias, frame_of, tokens, lp_old, adv, N, K, A,
+                                        prm, fix_stats, dz, g_frame, lp_new, stat_part, max_part);
+    return post_launch("token_loss_fact_kernel");
+  };
+  if (A <= 128) return go(token_loss_fact_kernel<4>, 4);
+  if (A <= 256) return go(token_loss_fact_kernel<8>, 8);
+  if (A <= 512) return go(token_loss_fact_kernel<16>, 16);
+  return go(token_loss_fact_kernel<32>, 32);
+}
+
+extern "C" int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, float* dpos,
+                                  void* stream) {
+  if (K < 1 || A < 1 || !dpk || !dprev || !dpos) return fail(kDimension, "pk_marginals: bad args");
+  const int nprev = A + 1;
+  const int64_t total = (int64_t)(nprev + K) * A;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)kNumSMs * 4);
+  pk_marginals_kernel<<<grid, 256, 0, as_stream(stream)>>>(dpk, K, A, nprev, dprev, dpos);
+  return post_launch("pk_marginals_kernel");
+}
 
 extern "C" int accel_token_logp(const float* mu, const int32_t* tokens, int64_t M, int A,
                                 float* lp_out, double* bad_part, void* stream) {

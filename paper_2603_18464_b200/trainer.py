@@ -358,6 +358,9 @@ class Trainer:
         self.scratch = _Scratch(self.device)
         self._rec_host = torch.zeros(32, dtype=F64).pin_memory()
         self.profile_events = None  # list -> CUDA-event brackets of the hot kernels
+        A, K = self.dims.n_actions, self.dims.chunk_len
+        # factorized head (no [M, A] logits) wherever the kernel supports the shape
+        self.factorized = A % 4 == 0 and 128 <= A <= 1024 and K <= 32
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
 
@@ -514,7 +517,7 @@ class Trainer:
             norm_mean=0.0, norm_std=0.0, norm_count=N,
             shard_sizes=_array_split_sizes(N, cfg.k_shards),
             behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
-        batch.ensure_groupings(d.n_steps, cnt[1:2])
+        batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized)
         host = torch.cat([flags, cnt.double()]).cpu().numpy()  # the one host sync
         if host[7] == 1:
             raise DomainError("cannot normalize zero advantages")
@@ -583,38 +586,59 @@ class Trainer:
             raise DimensionError(f"obs dim {batch.frames.shape[1]} != {d.obs_dim}")
         cnt = S.get("st.cnt", (4,), torch.int32)
         cnt.zero_()
-        batch.ensure_groupings(d.n_steps, cnt[1:2])
+        fact = self.factorized
+        batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=fact)
         n_glob = self.comm.global_counts(N) if self.comm is not None else (N, M)
         N_glob, M_glob = n_glob
-
-        # forward: backbone over frames, c, head GEMM
-        h1, h2 = self._backbone(batch.frames, "st.")
-        c = ops.build_c(h2, batch.frame_of, batch.tokens_dev, P["e_prev"], P["e_pos"], N, K, A,
-                        S.get("st.c", (M, D)))
-        logits = _mm(c, P["w_head"].t(), S.get("st.logits", (M, A)))
-
-        # fused loss forward + backward
-        gl = ops.token_grid(M)
-        dlogits = S.get("st.dlogits", (M, A))
-        lp_new = S.get("st.lp_new", (M,))
-        dbias_part = S.get("st.dbias", (gl, A))
-        stat_part = S.get("st.stat", (gl, 8), F64)
-        max_part = S.get("st.max", (gl, 2), F64)
         algo = _algo_id(lc)
-        with self._timed("token_loss"):
-            ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K,
-                           algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, lp_new,
-                           dbias_part, stat_part, max_part)
+        lp_new = S.get("st.lp_new", (M,))
         loss_sums = S.get("st.lsum", (8,), F64)
         loss_max = S.get("st.lmax", (2,), F64)
+
+        h1, h2 = self._backbone(batch.frames, "st.")
+        if fact:
+            # logits = H2W[frame] + EP[prev] + PP[k] + b: three small GEMMs, no [M, A] logits
+            h2w = _mm(h2, P["w_head"].t(), S.get("st.h2w", (F, A)))
+            ep = _mm(P["e_prev"], P["w_head"].t(), S.get("st.ep", (A + 1, A)))
+            pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
+            gf = ops.fact_grid(N)
+            dz = S.get("st.dz", (M, A))
+            g_frame = S.get("st.gframe", (F, A))
+            if F != N:
+                g_frame.zero_()
+            stat_part = S.get("st.stat", (gf, 8), F64)
+            max_part = S.get("st.max", (gf, 2), F64)
+            loss_args = (h2w, ep, pp, P["b_head"], batch.frame_of, batch.tokens_dev, batch.lp_old,
+                         batch.adv, N, K, algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dz,
+                         g_frame)
+            with self._timed("token_loss"):
+                ops.token_loss_fact(*loss_args, lp_new, stat_part, max_part)
+            gl = gf
+        else:
+            c = ops.build_c(h2, batch.frame_of, batch.tokens_dev, P["e_prev"], P["e_pos"], N, K,
+                            A, S.get("st.c", (M, D)))
+            logits = _mm(c, P["w_head"].t(), S.get("st.logits", (M, A)))
+            gl = ops.token_grid(M)
+            dlogits = S.get("st.dlogits", (M, A))
+            dbias_part = S.get("st.dbias", (gl, A))
+            stat_part = S.get("st.stat", (gl, 8), F64)
+            max_part = S.get("st.max", (gl, 2), F64)
+            with self._timed("token_loss"):
+                ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K,
+                               algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, lp_new,
+                               dbias_part, stat_part, max_part)
         ops.reduce_f64(stat_part, gl, 8, 0, loss_sums)
         ops.reduce_f64(max_part, gl, 2, 1, loss_max)
         if self.comm is not None:
             self.comm.all_reduce_sum(loss_sums)
             self.comm.all_reduce_max(loss_max)
-        ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K, algo,
-                       lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None, dbias_part,
-                       None, None, fix_stats=loss_sums)
+        # FIXUP: only does work when 0 < excluded < M_global (decided on the device)
+        if fact:
+            ops.token_loss_fact(*loss_args, None, None, None, fix_stats=loss_sums)
+        else:
+            ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K,
+                           algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None,
+                           dbias_part, None, None, fix_stats=loss_sums)
 
         # value head (hiddens detached)
         gw = ops.warp_grid(N)
@@ -639,16 +663,36 @@ class Trainer:
         batch.step_group.rows_sum(dU, G["e_step"])
 
         # policy backward
-        _mm(dlogits.t(), c, G["w_head"])
-        dc = _mm(dlogits, P["w_head"], c)  # c is dead after dW_head: reuse its storage
-        dz2 = S.get("st.dz2", (F, D))
-        if F != N:
-            dz2.zero_()
-        gd = ops.rows_grid(N)
-        pos_part = S.get("st.pos", (gd, K, D))
-        db1_part = S.get("st.db1", (gd, D))
-        ops.dc_reduce(dc, h2, batch.frame_of, N, K, D, dz2, pos_part, db1_part, gd)
-        batch.prev_group.rows_sum(dc, G["e_prev"])
+        segs = []
+        if fact:
+            # D(prev,k) = grouped sums of dz; Dprev / Dpos marginals
+            dpk = batch.pk_group.rows_sum(dz, S.get("st.dpk", ((A + 1) * K, A)))
+            dprev = S.get("st.dprev", (A + 1, A))
+            dpos = S.get("st.dpos", (K, A))
+            ops.pk_marginals(dpk, K, A, dprev, dpos)
+            # dW_head = G^T h2 + Dprev^T e_prev + Dpos^T e_pos   (sum_t dz_t (x) c_t)
+            _mm(g_frame.t(), h2, G["w_head"])
+            G["w_head"].addmm_(dprev.t(), P["e_prev"])
+            G["w_head"].addmm_(dpos.t(), P["e_pos"])
+            _mm(dprev, P["w_head"], G["e_prev"])
+            _mm(dpos, P["w_head"], G["e_pos"])
+            dz2 = _mm(g_frame, P["w_head"], S.get("st.dz2", (F, D)))  # dh2 (0 on bootstrap rows)
+            gd = ops.rows_grid(F)
+            db1_part = S.get("st.db1", (gd, D))
+            ops.tanh_grad_colsum(dz2, h2, db1_part, gd)
+            segs.append((dpos, G["b_head"], K, A, A))
+        else:
+            _mm(dlogits.t(), c, G["w_head"])
+            dc = _mm(dlogits, P["w_head"], c)  # c is dead after dW_head: reuse its storage
+            dz2 = S.get("st.dz2", (F, D))
+            if F != N:
+                dz2.zero_()
+            gd = ops.rows_grid(N)
+            pos_part = S.get("st.pos", (gd, K, D))
+            db1_part = S.get("st.db1", (gd, D))
+            ops.dc_reduce(dc, h2, batch.frame_of, N, K, D, dz2, pos_part, db1_part, gd)
+            batch.prev_group.rows_sum(dc, G["e_prev"])
+            segs += [(dbias_part, G["b_head"], gl, A, A), (pos_part, G["e_pos"], gd, K * D, K * D)]
         _mm(dz2.t(), h1, G["w1"])
         dh1 = _mm(dz2, P["w1"], h2)  # h2 is dead: reuse its storage
         gt = ops.rows_grid(F)
@@ -656,9 +700,7 @@ class Trainer:
         ops.tanh_grad_colsum(dh1, h1, db0_part, gt)
         _mm(dh1.t(), batch.frames, G["w0"])
 
-        ops.reduce_segments([
-            (dbias_part, G["b_head"], gl, A, A),
-            (pos_part, G["e_pos"], gd, K * D, K * D),
+        ops.reduce_segments(segs + [
             (db1_part, G["b1"], gd, D, D),
             (db0_part, G["b0"], gt, D, D),
             (vpart, G["w1v"], gw, H, 2 * H + 1),
