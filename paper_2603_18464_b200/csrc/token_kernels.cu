@@ -453,19 +453,151 @@ token_loss_tma_kernel(const float* __restrict__ logits, const float* __restrict_
   loss_epilogue<VPL, true>(acc, A, cx.fixup, s_dbias, s_stat, dbias_part, stat_part, max_part);
 }
 
+// ---- full-row fast path helpers (A == VPL * 32, VEC layout) -----------------------------
+// No per-element column masks; a non-finite logit is detected through the
+// FMA pipe: 0 * z is NaN for z = +-inf or NaN, so `chk` (and the entropy sum
+// sum e*d) turns NaN exactly when the reference's log_softmax would raise.
+template <int VPL>
+__device__ __forceinline__ RowStats row_stats_full(float (&z)[VPL], float (&e)[VPL],
+                                                   float chk, bool with_entropy) {
+  RowStats s;
+  float mx = z[0];
+#pragma unroll
+  for (int v = 1; v < VPL; ++v) mx = fmaxf(mx, z[v]);
+  mx = warp_max(mx);
+  float sum = 0.f, sed = 0.f;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    chk = fmaf(z[v], 0.f, chk);
+    z[v] -= mx;
+    e[v] = __expf(z[v]);
+    sum += e[v];
+    if (with_entropy) sed = fmaf(e[v], z[v], sed);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (with_entropy) sed += __shfl_xor_sync(0xffffffffu, sed, o);
+    chk += __shfl_xor_sync(0xffffffffu, chk, o);
+  }
+  s.inv_s = 1.f / sum;
+  s.log_s = __logf(sum);
+  s.sd_over_s = sed * s.inv_s;
+  s.H = s.log_s - s.sd_over_s;
+  s.bad = !isfinite(chk) || !isfinite(mx);
+  s.d_tok = mx;  // caller subtracts: d_tok = z_tok - mx
+  return s;
+}
+
+// Per-token coefficient c (= dloss/dlogp * m) and the statistics terms.
+__device__ __forceinline__ float token_coef(float dlt, float a, bool inc, const RowCtx& cx,
+                                            double& term_d, double& r_d, double& w_d,
+                                            bool& outside) {
+  float coef = 0.f;
+  term_d = 0.0; r_d = 1.0; w_d = 1.0;
+  outside = false;
+  if (inc) {
+    const float qq = dlt / cx.prm.sigma;
+    if (fabsf(dlt) < 60.f && (cx.prm.algo != 0 || qq * qq < 150.f)) {
+      float cf, tf, rf, wf;
+      token_scalars<float>(dlt, a, cx.prm, cf, tf, rf, wf, outside);
+      coef = cf * cx.inv_m;
+      term_d = tf; r_d = rf; w_d = wf;
+    } else {
+      double cd;
+      token_scalars<double>((double)dlt, (double)a, cx.prm, cd, term_d, r_d, w_d, outside);
+      coef = (float)(cd * cx.inv_m_d);
+    }
+  }
+  return coef;
+}
+
+template <int VPL>
+__device__ __forceinline__ void acc_token(LossAcc<VPL>& acc, bool inc, bool bad, bool bad_tok,
+                                          float H, double term_d, double r_d, double w_d,
+                                          bool outside) {
+  acc.ent_sum += (double)H;
+  acc.n_bad += bad;
+  acc.n_badtok += bad_tok;
+  if (inc) {
+    acc.loss_num += term_d;
+    acc.ratio_sum += r_d;
+    acc.w_sum += w_d;
+    acc.n_out += outside;
+    acc.rmax = fmax(acc.rmax, r_d);
+    acc.negwmin = fmax(acc.negwmin, -w_d);
+  } else {
+    ++acc.n_excl;
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void stats_epilogue(const LossAcc<VPL>& acc, double* s_stat,
+                                               double* __restrict__ stat_part,
+                                               double* __restrict__ max_part) {
+  constexpr int NS = kNumStat + kNumMax;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    double* st = s_stat + warp * NS;
+    st[kLossNum] = acc.loss_num;
+    st[kEntSum] = acc.ent_sum;
+    st[kRatioSum] = acc.ratio_sum;
+    st[kWSum] = acc.w_sum;
+    st[kOutside] = acc.n_out;
+    st[kExcluded] = acc.n_excl;
+    st[kBadRows] = acc.n_bad;
+    st[kBadTok] = acc.n_badtok;
+    st[kNumStat + kRatioMax] = acc.rmax;
+    st[kNumStat + kNegWMin] = acc.negwmin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum[NS];
+#pragma unroll
+    for (int q = 0; q < kNumStat; ++q) sum[q] = 0.0;
+    sum[kNumStat + kRatioMax] = -CUDART_INF;
+    sum[kNumStat + kNegWMin] = -CUDART_INF;
+    for (int w = 0; w < kWarps; ++w) {
+#pragma unroll
+      for (int q = 0; q < kNumStat; ++q) sum[q] += s_stat[w * NS + q];
+#pragma unroll
+      for (int q = kNumStat; q < NS; ++q) sum[q] = fmax(sum[q], s_stat[w * NS + q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kNumStat; ++q) stat_part[(int64_t)blockIdx.x * kNumStat + q] = sum[q];
+    max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = sum[kNumStat + kRatioMax];
+    max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = sum[kNumStat + kNegWMin];
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void load_row4(const float* __restrict__ row, int lane, int A,
+                                          float (&x)[VPL], bool full) {
+#pragma unroll
+  for (int q = 0; q < VPL / 4; ++q) {
+    const int c = q * 128 + lane * 4;
+    float4 y = (full || c < A) ? __ldg(reinterpret_cast<const float4*>(row + c))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    x[4 * q] = y.x; x[4 * q + 1] = y.y; x[4 * q + 2] = y.z; x[4 * q + 3] = y.w;
+  }
+}
+
 // ---- factorized head: logits never materialized ----------------------------------------
 // logits[i, k] = H2W[frame_of[i]] + EP[prev(i, k)] + PP[k] + b_head, with
 //   H2W = h2 @ W_head^T (frame rows), EP = e_prev @ W_head^T, PP = e_pos @ W_head^T
 // (models.py:181-182 distributed over the sum c = h2 + e_prev[prev] + e_pos).
 // One warp owns a whole transition (K consecutive token rows): the H2W row is
-// streamed once into the warp's smem ring by the bulk-copy engine, EP rows
-// come from L2 (prefetched one token ahead), PP + bias sit in smem.  Outputs:
+// streamed once into the warp's smem ring by the bulk-copy engine (kStages
+// transitions in flight), EP rows come from L2 (prefetched one token ahead),
+// PP + bias sit in smem.  The chosen-token column is handled once per row
+// (scalar re-evaluation + single-lane fix-up store), not per element.
+// Outputs:
 //   dz      f32[M, A]  per-token dlogits (token-major), consumed by the
 //                      (prev, k)-grouped row sum for the e_prev / e_pos / W_head terms
 //   g_frame f32[F, A]  G = sum_k dz[i, k] written to the transition's frame row
 //                      (bootstrap rows are left untouched: pre-zero), consumed
 //                      by dW_head += G^T h2 and dh2 = G W_head.
-template <int VPL>
+template <int VPL, bool FULL>
 __global__ void __launch_bounds__(kThreads, 2)
 token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ ep,
                        const float* __restrict__ pp, const float* __restrict__ bias,
@@ -476,23 +608,26 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
                        float* __restrict__ lp_new, double* __restrict__ stat_part,
                        double* __restrict__ max_part) {
   using L = RowLayout<VPL, true>;
+  constexpr int W = VPL * 32;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
   RowCtx cx;
   if (!setup_ctx(prm, fix_stats, cx)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // smem: ring [kWarps][kStages][VPL*32] | s_pp [K][VPL*32] | bars [kWarps][kStages]
-  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * VPL * 32;
-  float* s_pp = reinterpret_cast<float*>(smem) + (size_t)kWarps * kStages * VPL * 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_pp + (size_t)K * VPL * 32) + warp * kStages;
-  for (int e = threadIdx.x; e < K * VPL * 32; e += kThreads) {
-    const int k = e / (VPL * 32), c = e % (VPL * 32);
+  // smem: ring [kWarps][kStages][W] | s_pp [K][W] | s_oh [kWarps][W] | bars [kWarps][kStages]
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * W;
+  float* s_pp = reinterpret_cast<float*>(smem) + (size_t)kWarps * kStages * W;
+  float* s_oh = s_pp + (size_t)K * W + (size_t)warp * W;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_pp + (size_t)K * W + (size_t)kWarps * W) +
+                   warp * kStages;
+  for (int e = threadIdx.x; e < K * W; e += kThreads) {
+    const int k = e / W, c = e % W;
     s_pp[e] = c < A ? __ldg(pp + (int64_t)k * A + c) + __ldg(bias + c) : 0.f;
   }
+  for (int c = lane; c < W; c += 32) s_oh[c] = 0.f;
   const unsigned row_bytes = (unsigned)A * 4u;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
-  int f_ahead = 0;  // lane 0: frame row of the transition kStages iterations ahead
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
@@ -502,12 +637,9 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
       const int64_t i = gw + s * nw;
       if (i < N) {
         mbar_expect_tx(&bars[s], row_bytes);
-        bulk_g2s(ring + s * VPL * 32, h2w + (int64_t)__ldg(frame_of + i) * A, row_bytes,
-                 &bars[s]);
+        bulk_g2s(ring + s * W, h2w + (int64_t)__ldg(frame_of + i) * A, row_bytes, &bars[s]);
       }
     }
-    const int64_t i2 = gw + kStages * nw;
-    if (i2 < N) f_ahead = __ldg(frame_of + i2);
   }
   __syncthreads();
   LossAcc<VPL> acc;
@@ -515,145 +647,91 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
   int j = 0;
   for (int64_t i = gw; i < N; i += nw, ++j) {
     const int s = j % kStages;
+    const float* hrow = ring + s * W;
     const int fi = __ldg(frame_of + i);
     const int tok_l = lane < K ? __ldg(tokens + i * K + lane) : 0;
+    const int64_t next = i + kStages * nw;
+    const int f_next = (lane == 0 && next < N) ? __ldg(frame_of + next) : 0;
+    const float a = __ldg(adv + i);
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
-    float h[VPL];
-    L::load(ring + s * VPL * 32, lane, A, h, false);
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-      const int64_t next = i + kStages * nw;
-      if (next < N) {
-        mbar_expect_tx(&bars[s], row_bytes);
-        bulk_g2s(ring + s * VPL * 32, h2w + (int64_t)f_ahead * A, row_bytes, &bars[s]);
-        const int64_t i2 = next + nw;
-        if (i2 < N) f_ahead = __ldg(frame_of + i2);
-      }
-    }
-    float g[VPL];
+    float h[VPL], epn[VPL], g[VPL];
+    L::load(hrow, lane, A, h, false);
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[v] = 0.f;
-    float epn[VPL];
-    {
-      const float* er = ep + (int64_t)A * A;  // k = 0: chunk-start row
-#pragma unroll
-      for (int q = 0; q < VPL / 4; ++q) {
-        const int c = q * 128 + lane * 4;
-        float4 x = c < A ? __ldg(reinterpret_cast<const float4*>(er + c))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        epn[4 * q] = x.x; epn[4 * q + 1] = x.y; epn[4 * q + 2] = x.z; epn[4 * q + 3] = x.w;
-      }
-    }
+    load_row4<VPL>(ep + (int64_t)A * A, lane, A, epn, FULL);  // k = 0: chunk-start row
+    float coef_l = 0.f;  // lane k keeps token k's coefficient for the G one-hot pass
     for (int k = 0; k < K; ++k) {
+      const int tok_raw = __shfl_sync(0xffffffffu, tok_l, k);
+      const int prev = k == 0 ? A : min(max(__shfl_sync(0xffffffffu, tok_l, k - 1), 0), A);
       float z[VPL];
+      const float* ppk = s_pp + k * W;
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) z[v] = h[v] + epn[v] + s_pp[k * VPL * 32 + L::col(lane, v)];
-      const int tok_k = __shfl_sync(0xffffffffu, tok_l, k);
-      if (k + 1 < K) {  // prefetch next token's EP row (prev = this token)
-        const int pv = min(max(tok_k, 0), A);
-        const float* er = ep + (int64_t)pv * A;
-#pragma unroll
-        for (int q = 0; q < VPL / 4; ++q) {
-          const int c = q * 128 + lane * 4;
-          float4 x = c < A ? __ldg(reinterpret_cast<const float4*>(er + c))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-          epn[4 * q] = x.x; epn[4 * q + 1] = x.y; epn[4 * q + 2] = x.z; epn[4 * q + 3] = x.w;
-        }
-      }
-      // one token row: same algebra as loss_row (bias already folded into s_pp)
-      const int64_t row = i * K + k;
-      int tok = tok_k;
-      const bool bad_tok = tok < 0 || tok >= A;
-      if (bad_tok) tok = 0;
+      for (int v = 0; v < VPL; ++v) z[v] = (h[v] + epn[v]) + ppk[L::col(lane, v)];
+      const bool bad_tok = tok_raw < 0 || tok_raw >= A;
+      const int tok = bad_tok ? 0 : tok_raw;
+      // the chosen column, evaluated exactly as z[] is: (h + ep) + pp
+      const float z_tok = (hrow[tok] + __ldg(ep + (int64_t)prev * A + tok)) + ppk[tok];
+      if (k + 1 < K) load_row4<VPL>(ep + (int64_t)(bad_tok ? 0 : tok) * A, lane, A, epn, FULL);
       float e[VPL];
-      const RowStats rs = row_stats<VPL, true>(z, e, lane, A, tok, true);
+      RowStats rs;
+      if (FULL) {
+        rs = row_stats_full<VPL>(z, e, 0.f, true);
+        rs.d_tok = z_tok - rs.d_tok;
+      } else {
+        rs = row_stats<VPL, true>(z, e, lane, A, tok, true);
+      }
+      const int64_t row = i * K + k;
       const float lpn = rs.d_tok - rs.log_s;
       const float dlt = lpn - __ldg(lp_old + row);
-      const float a = __ldg(adv + i);
       const bool inc = !bad_tok && !rs.bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
-      float coef = 0.f;
-      double term_d = 0.0, r_d = 1.0, w_d = 1.0;
-      bool outside = false;
-      if (inc) {
-        const float qq = dlt / cx.prm.sigma;
-        if (fabsf(dlt) < 60.f && (cx.prm.algo != 0 || qq * qq < 150.f)) {
-          float cf, tf, rf, wf;
-          token_scalars<float>(dlt, a, cx.prm, cf, tf, rf, wf, outside);
-          coef = cf * cx.inv_m;
-          term_d = tf; r_d = rf; w_d = wf;
-        } else {
-          double cd;
-          token_scalars<double>((double)dlt, (double)a, cx.prm, cd, term_d, r_d, w_d, outside);
-          coef = (float)(cd * cx.inv_m_d);
-        }
-      }
+      double term_d, r_d, w_d;
+      bool outside;
+      const float coef = token_coef(dlt, a, inc, cx, term_d, r_d, w_d, outside);
+      // dz = p (ent_scale (d - sd/s) - coef); the +coef at the token column is applied below
       float d[VPL];
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
-        const int c = L::col(lane, v);
         const float p = e[v] * rs.inv_s;
-        const float t = fmaf(cx.ent_scale, z[v] - rs.sd_over_s, -coef);
-        float x = fmaf(p, t, c == tok ? coef : 0.f);
-        x = c < A ? x : 0.f;
+        float x = p * fmaf(cx.ent_scale, z[v] - rs.sd_over_s, -coef);
+        if (!FULL) x = L::col(lane, v) < A ? x : 0.f;
         d[v] = x;
         g[v] += x;
       }
-      L::store(dz + row * A, lane, A, d);
-      if (!cx.fixup) {
-        if (lane == 0) lp_new[row] = lpn;
-        acc.ent_sum += (double)rs.H;
-        acc.n_bad += rs.bad;
-        acc.n_badtok += bad_tok;
-        if (inc) {
-          acc.loss_num += term_d;
-          acc.ratio_sum += r_d;
-          acc.w_sum += w_d;
-          acc.n_out += outside;
-          acc.rmax = fmax(acc.rmax, r_d);
-          acc.negwmin = fmax(acc.negwmin, -w_d);
-        } else {
-          ++acc.n_excl;
-        }
+      float* drow = dz + row * A;
+      L::store(drow, lane, A, d);
+      if (lane == k) coef_l = coef;
+      __syncwarp();
+      if (lane == 0) {
+        const float p_tok = __expf(rs.d_tok) * rs.inv_s;
+        drow[tok] = fmaf(p_tok, fmaf(cx.ent_scale, rs.d_tok - rs.sd_over_s, -coef), coef);
+        if (!cx.fixup) lp_new[row] = lpn;
       }
+      if (!cx.fixup) acc_token(acc, inc, rs.bad, bad_tok, rs.H, term_d, r_d, w_d, outside);
     }
-    L::store(g_frame + (int64_t)fi * A, lane, A, g);
-  }
-  // statistics epilogue (dbias is not produced here: db_head = sum_k Dpos[k])
-  if (!cx.fixup) {
-    constexpr int NS = kNumStat + kNumMax;
+    // slot s is free: refill it with the transition kStages ahead
+    fence_proxy_async();
+    __syncwarp();
     if (lane == 0) {
-      double* st = s_stat + warp * NS;
-      st[kLossNum] = acc.loss_num;
-      st[kEntSum] = acc.ent_sum;
-      st[kRatioSum] = acc.ratio_sum;
-      st[kWSum] = acc.w_sum;
-      st[kOutside] = acc.n_out;
-      st[kExcluded] = acc.n_excl;
-      st[kBadRows] = acc.n_bad;
-      st[kBadTok] = acc.n_badtok;
-      st[kNumStat + kRatioMax] = acc.rmax;
-      st[kNumStat + kNegWMin] = acc.negwmin;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double sum[NS];
-#pragma unroll
-      for (int q = 0; q < kNumStat; ++q) sum[q] = 0.0;
-      sum[kNumStat + kRatioMax] = -CUDART_INF;
-      sum[kNumStat + kNegWMin] = -CUDART_INF;
-      for (int w = 0; w < kWarps; ++w) {
-#pragma unroll
-        for (int q = 0; q < kNumStat; ++q) sum[q] += s_stat[w * NS + q];
-#pragma unroll
-        for (int q = kNumStat; q < NS; ++q) sum[q] = fmax(sum[q], s_stat[w * NS + q]);
+      if (next < N) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * W, h2w + (int64_t)f_next * A, row_bytes, &bars[s]);
       }
-#pragma unroll
-      for (int q = 0; q < kNumStat; ++q) stat_part[(int64_t)blockIdx.x * kNumStat + q] = sum[q];
-      max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = sum[kNumStat + kRatioMax];
-      max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = sum[kNumStat + kNegWMin];
     }
+    // one-hot contributions (serial over k in lane order: duplicates accumulate)
+    for (int k = 0; k < K; ++k) {
+      const int tk = __shfl_sync(0xffffffffu, tok_l, k);
+      const float ck = __shfl_sync(0xffffffffu, coef_l, k);
+      if (lane == 0 && tk >= 0 && tk < A) s_oh[tk] += ck;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) g[v] += s_oh[L::col(lane, v)];
+    L::store(g_frame + (int64_t)fi * A, lane, A, g);
+    __syncwarp();
+    if (lane < K && tok_l >= 0 && tok_l < A) s_oh[tok_l] = 0.f;
+    __syncwarp();
   }
+  if (!cx.fixup) stats_epilogue<VPL>(acc, s_stat, stat_part, max_part);
 }
 
 // Dprev[j] = sum_k Dpk[j, k], Dpos[k] = sum_j Dpk[j, k]  (Dpk f32[(A+1), K, A])
@@ -734,15 +812,16 @@ token_logp_kernel(const float* __restrict__ mu, const int32_t* __restrict__ toke
   logp_block_epilogue(bad_rows, bad_tok, bad_part);
 }
 
-template <int VPL>
+template <int VPL, bool FULL>
 __global__ void __launch_bounds__(kThreads, 3)
 token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ tokens, int64_t M,
                       int A, float* __restrict__ lp_out, double* __restrict__ bad_part) {
   using L = RowLayout<VPL, true>;
+  constexpr int W = VPL * 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * VPL * 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * VPL * 32 * 4) +
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * W;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * W * 4) +
                    warp * kStages;
   const unsigned row_bytes = (unsigned)A * 4u;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
@@ -756,7 +835,7 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
       const int64_t row = gw + s * nw;
       if (row < M) {
         mbar_expect_tx(&bars[s], row_bytes);
-        bulk_g2s(ring + s * VPL * 32, mu + row * A, row_bytes, &bars[s]);
+        bulk_g2s(ring + s * W, mu + row * A, row_bytes, &bars[s]);
       }
     }
   }
@@ -764,19 +843,32 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
   int bad_rows = 0, bad_tok = 0, j = 0;
   for (int64_t row = gw; row < M; row += nw, ++j) {
     const int s = j % kStages;
+    const float* slot = ring + s * W;
+    const int tok_raw = __ldg(tokens + row);
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
-    float z[VPL];
-    L::load(ring + s * VPL * 32, lane, A, z, false);
+    float z[VPL], e[VPL];
+    L::load(slot, lane, A, z, false);
+    const bool bt = tok_raw < 0 || tok_raw >= A;
+    const int tok = bt ? 0 : tok_raw;
+    RowStats rs;
+    if (FULL) {
+      rs = row_stats_full<VPL>(z, e, 0.f, false);
+      rs.d_tok = slot[tok] - rs.d_tok;
+    } else {
+      rs = row_stats<VPL, true>(z, e, lane, A, tok, false);
+    }
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
+      lp_out[row] = rs.d_tok - rs.log_s;
       const int64_t next = row + kStages * nw;
       if (next < M) {
         mbar_expect_tx(&bars[s], row_bytes);
-        bulk_g2s(ring + s * VPL * 32, mu + next * A, row_bytes, &bars[s]);
+        bulk_g2s(ring + s * W, mu + next * A, row_bytes, &bars[s]);
       }
     }
-    logp_row<VPL, true>(z, row, lane, A, tokens, lp_out, bad_rows, bad_tok);
+    bad_rows += rs.bad;
+    bad_tok += bt;
   }
   logp_block_epilogue(bad_rows, bad_tok, bad_part);
 }
@@ -842,8 +934,11 @@ struct LogpLaunch {
   static int run(const float* mu, const int32_t* tokens, int64_t M, int A, float* lp,
                  double* bad_part, int grid, cudaStream_t s) {
     if constexpr (VEC && VPL >= 4) {
-      return launch_tma(token_logp_tma_kernel<VPL>, VPL, grid, s, "token_logp_tma_kernel", mu,
-                        tokens, M, A, lp, bad_part);
+      if (A == VPL * 32)
+        return launch_tma(token_logp_tma_kernel<VPL, true>, VPL, grid, s,
+                          "token_logp_tma_kernel", mu, tokens, M, A, lp, bad_part);
+      return launch_tma(token_logp_tma_kernel<VPL, false>, VPL, grid, s, "token_logp_tma_kernel",
+                        mu, tokens, M, A, lp, bad_part);
     } else {
       token_logp_kernel<VPL, VEC><<<grid, kThreads, 0, s>>>(mu, tokens, M, A, lp, bad_part);
       return post_launch("token_logp_kernel");
@@ -898,7 +993,7 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* ep, const fl
   const int grid = accel_fact_grid(N);
   auto go = [&](auto kernel, int VPL) -> int {
     const size_t smem = (size_t)kWarps * kStages * (VPL * 32 * 4 + sizeof(uint64_t)) +
-                        (size_t)K * VPL * 32 * 4 + 16;
+                        (size_t)K * VPL * 32 * 4 + (size_t)kWarps * VPL * 32 * 4 + 16;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
@@ -908,10 +1003,11 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* ep, const fl
                                         prm, fix_stats, dz, g_frame, lp_new, stat_part, max_part);
     return post_launch("token_loss_fact_kernel");
   };
-  if (A <= 128) return go(token_loss_fact_kernel<4>, 4);
-  if (A <= 256) return go(token_loss_fact_kernel<8>, 8);
-  if (A <= 512) return go(token_loss_fact_kernel<16>, 16);
-  return go(token_loss_fact_kernel<32>, 32);
+  const bool full = A == 128 || A == 256 || A == 512 || A == 1024;
+  if (A <= 128) return full ? go(token_loss_fact_kernel<4, true>, 4) : go(token_loss_fact_kernel<4, false>, 4);
+  if (A <= 256) return full ? go(token_loss_fact_kernel<8, true>, 8) : go(token_loss_fact_kernel<8, false>, 8);
+  if (A <= 512) return full ? go(token_loss_fact_kernel<16, true>, 16) : go(token_loss_fact_kernel<16, false>, 16);
+  return full ? go(token_loss_fact_kernel<32, true>, 32) : go(token_loss_fact_kernel<32, false>, 32);
 }
 
 extern "C" int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, float* dpos,
