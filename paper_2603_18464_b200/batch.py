@@ -44,6 +44,9 @@ class DeviceTrainBatch:
         self.prev_group = prev_group
         self.pk_group = None
         self.step_group = step_group
+        # (param generation, h1, h2) from revaluation; reused by train_step when
+        # the parameters have not changed since the batch was built
+        self.h_cache = None
         self.n_steps = n_steps
         self._host = {}
 

@@ -69,20 +69,43 @@ chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_
   }
 }
 
-__global__ void segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks,
-                                       int64_t R, int64_t* __restrict__ seg_off,
-                                       int64_t* __restrict__ piece_off) {
-  if (threadIdx.x != 0) return;
-  int64_t p = 0;
-  for (int j = 0; j < nkeys; ++j) {
+// seg_off / piece_off from the scanned counts: one 1024-thread block, each
+// thread owns a contiguous run of keys; a fixed-order scan of the per-thread
+// piece totals gives the piece offsets.
+__global__ void __launch_bounds__(1024)
+segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks, int64_t R,
+                       int64_t* __restrict__ seg_off, int64_t* __restrict__ piece_off) {
+  __shared__ int64_t s_tot[1024];
+  const int t = threadIdx.x;
+  const int per = (nkeys + blockDim.x - 1) / blockDim.x;
+  const int j0 = min(nkeys, t * per), j1 = min(nkeys, j0 + per);
+  int64_t mine = 0;
+  for (int j = j0; j < j1; ++j) {
     const int64_t a = base[(int64_t)j * n_chunks];
     const int64_t b = j + 1 < nkeys ? (int64_t)base[(int64_t)(j + 1) * n_chunks] : R;
     seg_off[j] = a;
+    mine += ceil_div(b - a, (int64_t)kPiece);
+  }
+  s_tot[t] = mine;
+  __syncthreads();
+  if (t == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int64_t v = s_tot[i];
+      s_tot[i] = run;
+      run += v;
+    }
+    seg_off[nkeys] = R;
+    piece_off[nkeys] = run;
+  }
+  __syncthreads();
+  int64_t p = s_tot[t];
+  for (int j = j0; j < j1; ++j) {
     piece_off[j] = p;
+    const int64_t a = seg_off[j];
+    const int64_t b = j + 1 < nkeys ? (int64_t)base[(int64_t)(j + 1) * n_chunks] : R;
     p += ceil_div(b - a, (int64_t)kPiece);
   }
-  seg_off[nkeys] = R;
-  piece_off[nkeys] = p;
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -270,7 +293,7 @@ extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, counts, base, (int)n, s);
   if (e != cudaSuccess) return fail(kCuda, "DeviceScan: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  segment_offsets_kernel<<<1, 32, 0, s>>>(base, nkeys, n_chunks, R, seg_off, piece_off);
+  segment_offsets_kernel<<<1, 1024, 0, s>>>(base, nkeys, n_chunks, R, seg_off, piece_off);
   if ((st = post_launch("segment_offsets_kernel"))) return st;
   if (R == 0) return kOk;
   stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, base, perm);

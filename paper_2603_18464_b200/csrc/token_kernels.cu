@@ -457,34 +457,40 @@ token_loss_tma_kernel(const float* __restrict__ logits, const float* __restrict_
 // No per-element column masks; a non-finite logit is detected through the
 // FMA pipe: 0 * z is NaN for z = +-inf or NaN, so `chk` (and the entropy sum
 // sum e*d) turns NaN exactly when the reference's log_softmax would raise.
+// warp max of floats in one CREDUX (sm_100a), NaN-propagating
+__device__ __forceinline__ float warp_max_nan(float v) {
+  float r;
+  asm volatile("redux.sync.max.NaN.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 template <int VPL>
 __device__ __forceinline__ RowStats row_stats_full(float (&z)[VPL], float (&e)[VPL],
-                                                   float chk, bool with_entropy) {
+                                                   bool with_entropy) {
   RowStats s;
   float mx = z[0];
 #pragma unroll
   for (int v = 1; v < VPL; ++v) mx = fmaxf(mx, z[v]);
-  mx = warp_max(mx);
+  mx = warp_max_nan(mx);  // NaN logit -> NaN max; +inf -> inf - inf = NaN below
   float sum = 0.f, sed = 0.f;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    chk = fmaf(z[v], 0.f, chk);
-    z[v] -= mx;
+    const float zo = z[v];
+    z[v] = zo - mx;
     e[v] = __expf(z[v]);
-    sum += e[v];
+    sum += fmaf(zo, 0.f, e[v]);  // 0 * (-inf) = NaN: a -inf logit poisons the sum
     if (with_entropy) sed = fmaf(e[v], z[v], sed);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (with_entropy) sed += __shfl_xor_sync(0xffffffffu, sed, o);
-    chk += __shfl_xor_sync(0xffffffffu, chk, o);
   }
   s.inv_s = 1.f / sum;
   s.log_s = __logf(sum);
   s.sd_over_s = sed * s.inv_s;
   s.H = s.log_s - s.sd_over_s;
-  s.bad = !isfinite(chk) || !isfinite(mx);
+  s.bad = !isfinite(sum) || !isfinite(mx);
   s.d_tok = mx;  // caller subtracts: d_tok = z_tok - mx
   return s;
 }
@@ -644,25 +650,43 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
   __syncthreads();
   LossAcc<VPL> acc;
   acc.init();
+  // per-transition scalars are prefetched one transition ahead (lane k < K holds
+  // token k and its behavior log-prob)
   int j = 0;
+  int fi_n = 0, tok_n = 0;
+  float lpo_n = 0.f, a_n = 0.f;
+  if (gw < N) {
+    fi_n = __ldg(frame_of + gw);
+    tok_n = lane < K ? __ldg(tokens + gw * K + lane) : 0;
+    lpo_n = lane < K ? __ldg(lp_old + gw * K + lane) : 0.f;
+    a_n = __ldg(adv + gw);
+  }
   for (int64_t i = gw; i < N; i += nw, ++j) {
     const int s = j % kStages;
     const float* hrow = ring + s * W;
-    const int fi = __ldg(frame_of + i);
-    const int tok_l = lane < K ? __ldg(tokens + i * K + lane) : 0;
+    const int fi = fi_n, tok_l = tok_n;
+    const float lpo_l = lpo_n, a = a_n;
     const int64_t next = i + kStages * nw;
     const int f_next = (lane == 0 && next < N) ? __ldg(frame_of + next) : 0;
-    const float a = __ldg(adv + i);
+    if (i + nw < N) {
+      const int64_t i2 = i + nw;
+      fi_n = __ldg(frame_of + i2);
+      tok_n = lane < K ? __ldg(tokens + i2 * K + lane) : 0;
+      lpo_n = lane < K ? __ldg(lp_old + i2 * K + lane) : 0.f;
+      a_n = __ldg(adv + i2);
+    }
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
     float h[VPL], epn[VPL], g[VPL];
     L::load(hrow, lane, A, h, false);
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[v] = 0.f;
     load_row4<VPL>(ep + (int64_t)A * A, lane, A, epn, FULL);  // k = 0: chunk-start row
+    int tok0 = __shfl_sync(0xffffffffu, tok_l, 0);
+    float ep_tok_n = __ldg(ep + (int64_t)A * A + min(max(tok0, 0), A - 1));
     float coef_l = 0.f;  // lane k keeps token k's coefficient for the G one-hot pass
     for (int k = 0; k < K; ++k) {
       const int tok_raw = __shfl_sync(0xffffffffu, tok_l, k);
-      const int prev = k == 0 ? A : min(max(__shfl_sync(0xffffffffu, tok_l, k - 1), 0), A);
+      const float lpo = __shfl_sync(0xffffffffu, lpo_l, k);
       float z[VPL];
       const float* ppk = s_pp + k * W;
 #pragma unroll
@@ -670,19 +694,24 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
       const bool bad_tok = tok_raw < 0 || tok_raw >= A;
       const int tok = bad_tok ? 0 : tok_raw;
       // the chosen column, evaluated exactly as z[] is: (h + ep) + pp
-      const float z_tok = (hrow[tok] + __ldg(ep + (int64_t)prev * A + tok)) + ppk[tok];
-      if (k + 1 < K) load_row4<VPL>(ep + (int64_t)(bad_tok ? 0 : tok) * A, lane, A, epn, FULL);
+      const float z_tok = (hrow[tok] + ep_tok_n) + ppk[tok];
+      if (k + 1 < K) {  // prefetch the next token's EP row (prev = this token) and column
+        const int tn = __shfl_sync(0xffffffffu, tok_l, k + 1);
+        const float* er = ep + (int64_t)tok * A;
+        load_row4<VPL>(er, lane, A, epn, FULL);
+        ep_tok_n = __ldg(er + min(max(tn, 0), A - 1));
+      }
       float e[VPL];
       RowStats rs;
       if (FULL) {
-        rs = row_stats_full<VPL>(z, e, 0.f, true);
+        rs = row_stats_full<VPL>(z, e, true);
         rs.d_tok = z_tok - rs.d_tok;
       } else {
         rs = row_stats<VPL, true>(z, e, lane, A, tok, true);
       }
       const int64_t row = i * K + k;
       const float lpn = rs.d_tok - rs.log_s;
-      const float dlt = lpn - __ldg(lp_old + row);
+      const float dlt = lpn - lpo;
       const bool inc = !bad_tok && !rs.bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
       double term_d, r_d, w_d;
       bool outside;
@@ -841,10 +870,12 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
   }
   __syncwarp();
   int bad_rows = 0, bad_tok = 0, j = 0;
+  int tok_next = gw < M ? __ldg(tokens + gw) : 0;  // token ids prefetched one row ahead
   for (int64_t row = gw; row < M; row += nw, ++j) {
     const int s = j % kStages;
     const float* slot = ring + s * W;
-    const int tok_raw = __ldg(tokens + row);
+    const int tok_raw = tok_next;
+    if (row + nw < M) tok_next = __ldg(tokens + row + nw);
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
     float z[VPL], e[VPL];
     L::load(slot, lane, A, z, false);
@@ -852,7 +883,7 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
     const int tok = bt ? 0 : tok_raw;
     RowStats rs;
     if (FULL) {
-      rs = row_stats_full<VPL>(z, e, 0.f, false);
+      rs = row_stats_full<VPL>(z, e, false);
       rs.d_tok = slot[tok] - rs.d_tok;
     } else {
       rs = row_stats<VPL, true>(z, e, lane, A, tok, false);

@@ -79,6 +79,152 @@ value_pool_kernel(const float* __restrict__ h1, const float* __restrict__ h2,
   }
 }
 
+// Vectorized variant for D = 4 * LPR (LPR lanes per row, 32 / LPR rows per
+// warp, two row groups in flight): same arithmetic as value_pool_kernel.
+template <int LPR>
+__global__ void __launch_bounds__(kThreads)
+value_pool4_kernel(const float* __restrict__ h1, const float* __restrict__ h2,
+                   const int32_t* __restrict__ row_frame, const int32_t* __restrict__ steps,
+                   int64_t R, int n_steps, const float* __restrict__ w_attn,
+                   const float* __restrict__ b_attn, const float* __restrict__ e_step,
+                   float* __restrict__ U, float* __restrict__ alpha, double* __restrict__ bad_part) {
+  constexpr int RPW = 32 / LPR;
+  constexpr int D4 = LPR;
+  __shared__ double s_bad[kWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sl = lane % LPR;
+  const float4 w = __ldg(reinterpret_cast<const float4*>(w_attn) + sl);
+  const float b = __ldg(b_attn);
+  int bad_attn = 0, bad_step = 0;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t step = (int64_t)gridDim.x * kWarps * RPW * 2;
+  for (int64_t r0 = gw * RPW * 2; r0 < R; r0 += step) {
+    int64_t r[2] = {r0 + slot, r0 + RPW + slot};
+    float4 a[2], c[2];
+    float e0[2], e1[2];
+    int64_t f[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const bool ok = r[q] < R;
+      f[q] = ok ? (row_frame ? __ldg(row_frame + r[q]) : r[q]) : 0;
+      a[q] = __ldg(reinterpret_cast<const float4*>(h1 + f[q] * 4 * D4) + sl);
+      c[q] = __ldg(reinterpret_cast<const float4*>(h2 + f[q] * 4 * D4) + sl);
+      e0[q] = a[q].x * w.x + a[q].y * w.y + a[q].z * w.z + a[q].w * w.w;
+      e1[q] = c[q].x * w.x + c[q].y * w.y + c[q].z * w.z + c[q].w * w.w;
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        e0[q] += __shfl_xor_sync(0xffffffffu, e0[q], o);
+        e1[q] += __shfl_xor_sync(0xffffffffu, e1[q], o);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (r[q] >= R) continue;
+      const float x0 = e0[q] + b, x1 = e1[q] + b;
+      const bool bad = !isfinite(x0) || !isfinite(x1);
+      const float mx = fmaxf(x0, x1);
+      const float p0 = __expf(x0 - mx), p1 = __expf(x1 - mx);
+      const float inv = 1.f / (p0 + p1);
+      const float a0 = p0 * inv, a1 = p1 * inv;
+      int st = __ldg(steps + f[q]);
+      const bool bst = st < 0 || st >= n_steps;
+      st = min(max(st, 0), n_steps - 1);
+      const float4 es = __ldg(reinterpret_cast<const float4*>(e_step + (int64_t)st * 4 * D4) + sl);
+      float4 u;
+      u.x = fmaf(a0, a[q].x, fmaf(a1, c[q].x, es.x));
+      u.y = fmaf(a0, a[q].y, fmaf(a1, c[q].y, es.y));
+      u.z = fmaf(a0, a[q].z, fmaf(a1, c[q].z, es.z));
+      u.w = fmaf(a0, a[q].w, fmaf(a1, c[q].w, es.w));
+      reinterpret_cast<float4*>(U + r[q] * 4 * D4)[sl] = u;
+      if (sl == 0) {
+        alpha[2 * r[q]] = a0;
+        alpha[2 * r[q] + 1] = a1;
+        bad_attn += bad;
+        bad_step += bst;
+      }
+    }
+  }
+  bad_attn = __reduce_add_sync(0xffffffffu, bad_attn);
+  bad_step = __reduce_add_sync(0xffffffffu, bad_step);
+  if (lane == 0) {
+    s_bad[warp][0] = bad_attn;
+    s_bad[warp][1] = bad_step;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) {
+      x += s_bad[w2][0];
+      y += s_bad[w2][1];
+    }
+    bad_part[2 * (int64_t)blockIdx.x] = x;
+    bad_part[2 * (int64_t)blockIdx.x + 1] = y;
+  }
+}
+
+// Vectorized attention backward for D = 4 * LPR (see value_attn_grad_kernel).
+template <int LPR>
+__global__ void __launch_bounds__(kThreads)
+value_attn_grad4_kernel(const float* __restrict__ dU, const float* __restrict__ h1,
+                        const float* __restrict__ h2, const int32_t* __restrict__ row_frame,
+                        const float* __restrict__ alpha, int64_t R, float* __restrict__ de,
+                        float* __restrict__ part) {
+  constexpr int RPW = 32 / LPR;
+  constexpr int D4 = LPR;
+  __shared__ float s_b[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sl = lane % LPR;
+  float gb = 0.f;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t step = (int64_t)gridDim.x * kWarps * RPW * 2;
+  for (int64_t r0 = gw * RPW * 2; r0 < R; r0 += step) {
+    int64_t r[2] = {r0 + slot, r0 + RPW + slot};
+    float d0[2], d1[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const bool ok = r[q] < R;
+      const int64_t rr = ok ? r[q] : 0;
+      const int64_t f = row_frame ? __ldg(row_frame + rr) : rr;
+      const float4 g = __ldg(reinterpret_cast<const float4*>(dU + rr * 4 * D4) + sl);
+      const float4 a = __ldg(reinterpret_cast<const float4*>(h1 + f * 4 * D4) + sl);
+      const float4 c = __ldg(reinterpret_cast<const float4*>(h2 + f * 4 * D4) + sl);
+      d0[q] = g.x * a.x + g.y * a.y + g.z * a.z + g.w * a.w;
+      d1[q] = g.x * c.x + g.y * c.y + g.z * c.z + g.w * c.w;
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        d0[q] += __shfl_xor_sync(0xffffffffu, d0[q], o);
+        d1[q] += __shfl_xor_sync(0xffffffffu, d1[q], o);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (r[q] >= R || sl != 0) continue;
+      const float a0 = __ldg(alpha + 2 * r[q]), a1 = __ldg(alpha + 2 * r[q] + 1);
+      const float s = a0 * d0[q] + a1 * d1[q];
+      const float x0 = a0 * (d0[q] - s), x1 = a1 * (d1[q] - s);
+      de[2 * r[q]] = x0;
+      de[2 * r[q] + 1] = x1;
+      gb += x0 + x1;
+    }
+  }
+  // fixed-order warp reduction (xor butterfly), then warps in order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) gb += __shfl_xor_sync(0xffffffffu, gb, o);
+  if (lane == 0) s_b[warp] = gb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f;
+    for (int w2 = 0; w2 < kWarps; ++w2) a += s_b[w2];
+    part[blockIdx.x] = a;
+  }
+}
+
 // part layout per block: [dw1v (H) | db0v (H) | db1v (1)]; dpart: [sum err^2, non-finite v]
 __global__ void __launch_bounds__(kThreads)
 value_head_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
@@ -253,6 +399,19 @@ extern "C" int accel_value_pool(const float* h1, const float* h2, const int32_t*
   if (R == 0) return kOk;
   if (!h1 || !h2 || !steps || !w_attn || !b_attn || !e_step || !U || !alpha || !bad_part)
     return fail(kDimension, "value_pool: NULL buffer");
+  const uintptr_t al = reinterpret_cast<uintptr_t>(h1) | reinterpret_cast<uintptr_t>(h2) |
+                       reinterpret_cast<uintptr_t>(w_attn) | reinterpret_cast<uintptr_t>(e_step) |
+                       reinterpret_cast<uintptr_t>(U);
+  if ((al & 15) == 0 && (D == 16 || D == 32 || D == 64 || D == 128)) {
+    cudaStream_t s = as_stream(stream);
+    switch (D / 4) {
+      case 4: value_pool4_kernel<4><<<grid, kThreads, 0, s>>>(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part); break;
+      case 8: value_pool4_kernel<8><<<grid, kThreads, 0, s>>>(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part); break;
+      case 16: value_pool4_kernel<16><<<grid, kThreads, 0, s>>>(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part); break;
+      default: value_pool4_kernel<32><<<grid, kThreads, 0, s>>>(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part); break;
+    }
+    return post_launch("value_pool4_kernel");
+  }
   value_pool_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(
       h1, h2, row_frame, steps, R, D, n_steps, w_attn, b_attn, e_step, U, alpha, bad_part);
   return post_launch("value_pool_kernel");
@@ -278,6 +437,18 @@ extern "C" int accel_value_attn_grad(const float* dU, const float* h1, const flo
                                      int D, float* de, float* part, int grid, void* stream) {
   if (R < 0 || D < 1 || grid < 1) return fail(kDimension, "value_attn_grad: bad sizes");
   if (R == 0) return kOk;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(h1) | reinterpret_cast<uintptr_t>(h2) |
+                       reinterpret_cast<uintptr_t>(dU);
+  if ((al & 15) == 0 && (D == 16 || D == 32 || D == 64 || D == 128)) {
+    cudaStream_t s = as_stream(stream);
+    switch (D / 4) {
+      case 4: value_attn_grad4_kernel<4><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, part); break;
+      case 8: value_attn_grad4_kernel<8><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, part); break;
+      case 16: value_attn_grad4_kernel<16><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, part); break;
+      default: value_attn_grad4_kernel<32><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, part); break;
+    }
+    return post_launch("value_attn_grad4_kernel");
+  }
   value_attn_grad_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(dU, h1, h2, row_frame, alpha,
                                                                    R, D, de, part);
   return post_launch("value_attn_grad_kernel");

@@ -348,6 +348,8 @@ class Trainer:
         self._policy_version = int(getattr(bundle.policy.params, "version", 0))
         self._value_version = int(getattr(bundle.value.params, "version", 0))
         self._host_stale = False
+        self._param_gen = 0  # bumps whenever the device parameters change
+        self._last_h = None
         self.adam_policy = AdamStateView(self, 0, cfg.lr, cfg.beta1, cfg.beta2)
         self.adam_value = AdamStateView(self, 1, cfg.lr, cfg.beta1, cfg.beta2)
         self.publish_version = 0
@@ -385,6 +387,7 @@ class Trainer:
         self._policy_version = int(getattr(new.policy.params, "version", 0))
         self._value_version = int(getattr(new.value.params, "version", 0))
         self._host_stale = False
+        self._param_gen += 1
 
     # -- publication (trainer.py:328-348) -------------------------------------------
     def snapshot(self) -> VersionedWeights:
@@ -404,22 +407,33 @@ class Trainer:
         self.publish_policy()
 
     # -- shared forward pieces -------------------------------------------------------
-    def _backbone(self, frames, tag: str):
+    def _backbone(self, frames, tag: str | None):
+        """h1, h2 over frame rows (models.py:176-177); tag None -> fresh tensors."""
         P = self.params.pv
         F = frames.shape[0]
         D = self.dims.hidden
-        h1 = _mm(frames, P["w0"].t(), self.scratch.get(tag + "h1", (F, D)))
+
+        def buf(name):
+            if tag is None:
+                return torch.empty(F, D, dtype=F32, device=self.device)
+            return self.scratch.get(tag + name, (F, D))
+
+        h1 = _mm(frames, P["w0"].t(), buf("h1"))
         ops.bias_tanh(h1, P["b0"])
-        h2 = _mm(h1, P["w1"].t(), self.scratch.get(tag + "h2", (F, D)))
+        h2 = _mm(h1, P["w1"].t(), buf("h2"))
         ops.bias_tanh(h2, P["b1"])
         return h1, h2
 
-    def _frame_values(self, frames, steps, out, bad_part):
-        """V(o) on every frame: state_values_batch (models.py:411-415)."""
+    def _frame_values(self, frames, steps, out, bad_part, keep: bool = False):
+        """V(o) on every frame: state_values_batch (models.py:411-415).
+
+        keep=True returns the backbone activations (fresh tensors) so a
+        train_step under the same parameters can reuse them."""
         P = self.params.pv
         F = frames.shape[0]
         d = self.dims
-        h1, h2 = self._backbone(frames, "rv.")
+        h1, h2 = self._backbone(frames, None if keep else "rv.")
+        self._last_h = (h1, h2) if keep else None
         U = self.scratch.get("rv.U", (F, d.hidden))
         alpha = self.scratch.get("rv.alpha", (F, 2))
         g = ops.warp_grid(F)
@@ -494,10 +508,12 @@ class Trainer:
         if cfg.revalue:
             values = torch.empty(F, dtype=F32, device=dev)
             bad_part = self.scratch.get("b.vbad", (ops.warp_grid(F), 2), F64)
-            g = self._frame_values(b["frames"], b["steps"], values, bad_part)
+            g = self._frame_values(b["frames"], b["steps"], values, bad_part, keep=True)
+            h_cache = (self._param_gen, *self._last_h)
             ops.reduce_f64(bad_part, g, 2, 0, flags[10:12])
         else:
             values = b["values"]
+            h_cache = None
         frame_of = torch.empty(N, dtype=I32, device=dev)
         with self._timed("gae"):
             adv_raw, ret, _ = ops.gae_segmented(b["rewards"], values, b["traj_off"], b["done"],
@@ -518,6 +534,7 @@ class Trainer:
             shard_sizes=_array_split_sizes(N, cfg.k_shards),
             behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
         batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized)
+        batch.h_cache = h_cache
         host = torch.cat([flags, cnt.double()]).cpu().numpy()  # the one host sync
         if host[7] == 1:
             raise DomainError("cannot normalize zero advantages")
@@ -595,7 +612,11 @@ class Trainer:
         loss_sums = S.get("st.lsum", (8,), F64)
         loss_max = S.get("st.lmax", (2,), F64)
 
-        h1, h2 = self._backbone(batch.frames, "st.")
+        hc = getattr(batch, "h_cache", None)
+        if hc is not None and hc[0] == self._param_gen:
+            h1, h2 = hc[1], hc[2]  # revaluation ran under these exact parameters
+        else:
+            h1, h2 = self._backbone(batch.frames, "st.")
         if fact:
             # logits = H2W[frame] + EP[prev] + PP[k] + b: three small GEMMs, no [M, A] logits
             h2w = _mm(h2, P["w_head"].t(), S.get("st.h2w", (F, A)))
@@ -694,7 +715,7 @@ class Trainer:
             batch.prev_group.rows_sum(dc, G["e_prev"])
             segs += [(dbias_part, G["b_head"], gl, A, A), (pos_part, G["e_pos"], gd, K * D, K * D)]
         _mm(dz2.t(), h1, G["w1"])
-        dh1 = _mm(dz2, P["w1"], h2)  # h2 is dead: reuse its storage
+        dh1 = _mm(dz2, P["w1"], S.get("st.dh1", (F, D)))
         gt = ops.rows_grid(F)
         db0_part = S.get("st.db0", (gt, D))
         ops.tanh_grad_colsum(dh1, h1, db0_part, gt)
@@ -762,6 +783,7 @@ class Trainer:
         if rec[17] > 0:
             raise NonFiniteError("parameter update produced non-finite values")
         self.params.flip()
+        self._param_gen += 1
         self.adam_policy.step += 1
         self.adam_value.step += 1
         self._policy_version += 1
