@@ -115,20 +115,22 @@ int accel_token_loss(const float* logits, const float* bias, const int32_t* toke
 
 /* Factorized-head variant (the production path for 128 <= A <= 1024,
  * A % 4 == 0, K <= 32): logits are never materialized.  logits[i,k] =
- * h2w[frame_of[i]] + ep[prev] + pp[k] + bias with h2w = h2 W_head^T (f32[F, A]),
- * ep = e_prev W_head^T (f32[A+1, A]), pp = e_pos W_head^T (f32[K, A]) —
- * models.py:181-182 distributed over c = h2 + e_prev[prev] + e_pos.
- * Writes dz f32[N*K, A] (per-token dlogits), g_frame f32[F, A] rows
- * frame_of[i] = sum_k dz[i, k] (pre-zero the bootstrap rows), lp_new,
+ * h2w[frame_of[i]] + epp[prev*K + k] with h2w = h2 W_head^T (f32[F, A]) and
+ * epp = e_prev W_head^T + e_pos W_head^T + b_head (f32[(A+1)*K, A],
+ * accel_ep_plus) — models.py:181-182 distributed over c = h2 + e_prev[prev]
+ * + e_pos.  Writes dz f32[N*K, A] (per-token dlogits), g_frame f32[F, A]
+ * rows frame_of[i] = sum_k dz[i, k] (pre-zero the bootstrap rows), lp_new,
  * stat_part/max_part as accel_token_loss (grid = accel_fact_grid(N)).
  * fix_stats: FIXUP pass as accel_token_loss. */
 int accel_fact_grid(int64_t N);
-int accel_token_loss_fact(const float* h2w, const float* ep, const float* pp,
-                          const float* bias, const int32_t* frame_of, const int32_t* tokens,
-                          const float* lp_old, const float* adv, int64_t N, int K, int A,
-                          int algo, double sigma, double clip_eps, double lambda_h,
-                          double m_global, const double* fix_stats, float* dz,
-                          float* g_frame, float* lp_new, double* stat_part,
+/* epp[(prev*K+k)*A + a] = ep[prev*A + a] + pp[k*A + a] + bias[a] */
+int accel_ep_plus(const float* ep, const float* pp, const float* bias, int A, int K,
+                  float* epp, void* stream);
+int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* frame_of,
+                          const int32_t* tokens, const float* lp_old, const float* adv,
+                          int64_t N, int K, int A, int algo, double sigma, double clip_eps,
+                          double lambda_h, double m_global, const double* fix_stats,
+                          float* dz, float* g_frame, float* lp_new, double* stat_part,
                           double* max_part, void* stream);
 /* Dprev f32[A+1, A] = sum_k dpk[j, k]; Dpos f32[K, A] = sum_j dpk[j, k]
  * from the (prev, k)-grouped dz sums dpk f32[(A+1)*K, A]. */

@@ -1,0 +1,392 @@
+// (b) Fused token loss with a factorized policy head: logits never exist in HBM.
+//
+// Reference: log_prob_chunk (models.py:219-223), policy_surrogate
+// (trainer.py:183-239), entropy_bonus (trainer.py:242-251) and the dlogits
+// assembly of train_step (trainer.py:425-435), with the head's logits
+// (models.py:181-182) distributed over c = h2 + e_prev[prev] + e_pos:
+//   logits[i, k] = H2W[frame_of[i]] + EPP[prev(i, k) * K + k]
+//   H2W = h2 @ W_head^T (one row per frame)
+//   EPP = e_prev @ W_head^T + e_pos @ W_head^T + b_head   ((A+1) * K rows, L2-resident)
+// One warp owns a whole transition (K consecutive token rows).  Its H2W row is
+// streamed once into a per-warp shared-memory ring by the bulk-copy (TMA)
+// engine, kStages transitions in flight; the EPP row of the next token is
+// prefetched into registers while the current token is processed.
+//
+// Per logit: 1 FADD (z), 1 FFMA + ex2 (p in the log2 domain, ftz), 1 FADD +
+// 1 FFMA (partition sums), 1 FFMA + 1 FMUL (gradient), 1 FADD (G): the row
+// max is one CREDUX, the chosen-token column is evaluated once per row and
+// patched by a single lane, the float64 statistics are accumulated once per
+// transition per lane.  Non-finite logits surface as a non-finite max, sum
+// or sum(e*d) (0 * -inf = NaN), exactly where the reference's log_softmax
+// raises.  Outputs:
+//   dz      f32[M, A]  per-token dlogits (token-major) for the (prev, k)-grouped sums
+//   g_frame f32[F, A]  G = sum_k dz[i, k] on the transition's frame row
+#include "token_common.cuh"
+
+namespace accel {
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// epp[(prev * K + k) * A + a] = ep[prev * A + a] + pp[k * A + a] + bias[a]
+__global__ void ep_plus_kernel(const float* __restrict__ ep, const float* __restrict__ pp,
+                               const float* __restrict__ bias, int A, int K,
+                               float* __restrict__ epp) {
+  const int64_t total = (int64_t)(A + 1) * K * A;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(e % A);
+    const int64_t r = e / A;
+    const int k = (int)(r % K);
+    const int64_t prev = r / K;
+    epp[e] = ep[prev * A + a] + pp[(int64_t)k * A + a] + bias[a];
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void load_vec(const float* __restrict__ row, int lane, int A,
+                                         float (&x)[VPL], bool full) {
+#pragma unroll
+  for (int q = 0; q < VPL / 4; ++q) {
+    const int c = q * 128 + lane * 4;
+    const float4 y = (full || c < A) ? __ldg(reinterpret_cast<const float4*>(row + c))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    x[4 * q] = y.x; x[4 * q + 1] = y.y; x[4 * q + 2] = y.z; x[4 * q + 3] = y.w;
+  }
+}
+
+template <int VPL, bool FULL>
+__global__ void __launch_bounds__(kThreads, 2)
+token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
+                       const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
+                       const float* __restrict__ lp_old, const float* __restrict__ adv, int64_t N,
+                       int K, int A, LossParams prm, const double* __restrict__ fix_stats,
+                       float* __restrict__ dz, float* __restrict__ g_frame,
+                       float* __restrict__ lp_new, double* __restrict__ stat_part,
+                       double* __restrict__ max_part) {
+  using L = RowLayout<VPL, true>;
+  constexpr int W = VPL * 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
+  RowCtx cx;
+  if (!setup_ctx(prm, fix_stats, cx)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // smem: ring [kWarps][kStages][W] | s_oh [kWarps][W] | bars [kWarps][kStages]
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * W;
+  float* s_oh = reinterpret_cast<float*>(smem) + (size_t)kWarps * kStages * W + (size_t)warp * W;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem) +
+                                               (size_t)kWarps * (kStages + 1) * W) +
+                   warp * kStages;
+  for (int c = lane; c < W; c += 32) s_oh[c] = 0.f;
+  const unsigned row_bytes = (unsigned)A * 4u;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t i = gw + s * nw;
+      if (i < N) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(ring + s * W, h2w + (int64_t)__ldg(frame_of + i) * A, row_bytes, &bars[s]);
+      }
+    }
+  }
+  __syncwarp();
+  const float ent2 = cx.ent_scale * kLn2;
+  // per-lane statistics (lane k accumulates token k of every transition)
+  double st_loss = 0.0, st_ent = 0.0, st_r = 0.0, st_w = 0.0;
+  double st_rmax = -CUDART_INF, st_negw = -CUDART_INF;
+  int st_out = 0, st_excl = 0, st_bad = 0, st_badtok = 0;
+
+  // per-transition scalars prefetched one transition ahead
+  int fi_n = 0, tok_n = 0;
+  float lpo_n = 0.f, a_n = 0.f;
+  if (gw < N) {
+    fi_n = __ldg(frame_of + gw);
+    tok_n = lane < K ? __ldg(tokens + gw * K + lane) : 0;
+    lpo_n = lane < K ? __ldg(lp_old + gw * K + lane) : 0.f;
+    a_n = __ldg(adv + gw);
+  }
+  int j = 0;
+  for (int64_t i = gw; i < N; i += nw, ++j) {
+    const int s = j % kStages;
+    const float* hrow = ring + s * W;
+    const int fi = fi_n, tok_l = tok_n;
+    const float lpo_l = lpo_n, a = a_n;
+    const int64_t next = i + kStages * nw;
+    const int f_next = (lane == 0 && next < N) ? __ldg(frame_of + next) : 0;
+    if (i + nw < N) {
+      const int64_t i2 = i + nw;
+      fi_n = __ldg(frame_of + i2);
+      tok_n = lane < K ? __ldg(tokens + i2 * K + lane) : 0;
+      lpo_n = lane < K ? __ldg(lp_old + i2 * K + lane) : 0.f;
+      a_n = __ldg(adv + i2);
+    }
+    // EPP row of token 0 (prev = chunk start A) and its chosen column
+    const int tok0 = min(max(__shfl_sync(0xffffffffu, tok_l, 0), 0), A - 1);
+    float epn[VPL];
+    const float* er0 = epp + (int64_t)A * K * A;
+    load_vec<VPL>(er0, lane, A, epn, FULL);
+    float ep_tok = __ldg(er0 + tok0);
+    mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    float h[VPL], g[VPL];
+    L::load(hrow, lane, A, h, false);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) g[v] = 0.f;
+    float my_coef = 0.f, my_H = 0.f;
+    double my_term = 0.0, my_r = 1.0, my_w = 1.0;
+    bool my_inc = false, my_bad = false, my_badtok = false, my_out = false;
+    for (int k = 0; k < K; ++k) {
+      const int tok_raw = __shfl_sync(0xffffffffu, tok_l, k);
+      const float lpo = __shfl_sync(0xffffffffu, lpo_l, k);
+      const bool bad_tok = tok_raw < 0 || tok_raw >= A;
+      const int tok = bad_tok ? 0 : tok_raw;
+      float z[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) z[v] = h[v] + epn[v];
+      const float z_tok = hrow[tok] + ep_tok;  // same arithmetic as z[] at column tok
+      if (k + 1 < K) {  // prefetch the next token's EPP row (prev = this token) and column
+        const int tn = min(max(__shfl_sync(0xffffffffu, tok_l, k + 1), 0), A - 1);
+        const float* er = epp + ((int64_t)tok * K + k + 1) * A;
+        load_vec<VPL>(er, lane, A, epn, FULL);
+        ep_tok = __ldg(er + tn);
+      }
+      // row max (one CREDUX), partition sums in the log2 domain
+      float mx = z[0];
+#pragma unroll
+      for (int v = 1; v < VPL; ++v) mx = fmaxf(mx, FULL || L::col(lane, v) < A ? z[v] : mx);
+      mx = warp_max_nan(mx);
+      const float nm2 = -mx * kLog2e;
+      float e[VPL], sum = 0.f, sed = 0.f;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        z[v] = fmaf(z[v], kLog2e, nm2);  // d2 = (z - max) log2(e)
+        e[v] = (FULL || L::col(lane, v) < A) ? ex2_ftz(z[v]) : 0.f;
+        sum += e[v];
+        sed = fmaf(e[v], z[v], sed);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        sed += __shfl_xor_sync(0xffffffffu, sed, o);
+      }
+      const bool bad = !isfinite(sum) || !isfinite(sed) || !isfinite(mx);
+      const float inv_s = 1.f / sum;
+      const float log_s = __logf(sum);
+      const float sd2 = sed * inv_s;  // sum_a p_a d2_a
+      const float H = log_s - sd2 * kLn2;
+      const float d_tok = z_tok - mx;
+      const float lpn = d_tok - log_s;
+      const float dlt = lpn - lpo;
+      const bool inc = !bad_tok && !bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
+      double term_d, r_d, w_d;
+      bool outside;
+      const float coef = token_coef(dlt, a, inc, cx, term_d, r_d, w_d, outside);
+      // dz = p (ent (d - sum p d) - coef) = e * (Ac d2 + Cc)   (+coef at the token column)
+      const float Ac = ent2 * inv_s;
+      const float Cc = -(Ac * sd2) - coef * inv_s;
+      float d[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const float x = e[v] * fmaf(Ac, z[v], Cc);
+        d[v] = x;
+        g[v] += x;
+      }
+      const int64_t row = i * K + k;
+      float* drow = dz + row * A;
+      L::store(drow, lane, A, d);
+      __syncwarp();
+      if (lane == 0) {
+        const float d2t = fmaf(z_tok, kLog2e, nm2);
+        drow[tok] = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
+        if (!cx.fixup) lp_new[row] = lpn;
+      }
+      if (lane == k) {
+        my_coef = coef;
+        my_H = H;
+        my_term = term_d;
+        my_r = r_d;
+        my_w = w_d;
+        my_inc = inc;
+        my_bad = bad;
+        my_badtok = bad_tok;
+        my_out = outside;
+      }
+    }
+    // slot s is free: refill it with the transition kStages ahead
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && next < N) {
+      mbar_expect_tx(&bars[s], row_bytes);
+      bulk_g2s(ring + s * W, h2w + (int64_t)f_next * A, row_bytes, &bars[s]);
+    }
+    // one-hot part of G: sum_k coef_k [a == tok_k] (lane order: duplicates accumulate)
+    for (int k = 0; k < K; ++k) {
+      const int tk = __shfl_sync(0xffffffffu, tok_l, k);
+      const float ck = __shfl_sync(0xffffffffu, my_coef, k);
+      if (lane == 0 && tk >= 0 && tk < A) s_oh[tk] += ck;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) g[v] += s_oh[L::col(lane, v)];
+    L::store(g_frame + (int64_t)fi * A, lane, A, g);
+    __syncwarp();
+    if (lane < K && tok_l >= 0 && tok_l < A) s_oh[tok_l] = 0.f;
+    __syncwarp();
+    if (!cx.fixup && lane < K) {
+      st_ent += (double)my_H;
+      st_bad += my_bad;
+      st_badtok += my_badtok;
+      if (my_inc) {
+        st_loss += my_term;
+        st_r += my_r;
+        st_w += my_w;
+        st_out += my_out;
+        st_rmax = fmax(st_rmax, my_r);
+        st_negw = fmax(st_negw, -my_w);
+      } else {
+        ++st_excl;
+      }
+    }
+  }
+  if (cx.fixup) return;
+  // warp reduction of the per-lane statistics (fixed xor order), then CTA
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
+    st_ent += __shfl_xor_sync(0xffffffffu, st_ent, o);
+    st_r += __shfl_xor_sync(0xffffffffu, st_r, o);
+    st_w += __shfl_xor_sync(0xffffffffu, st_w, o);
+    st_rmax = fmax(st_rmax, __shfl_xor_sync(0xffffffffu, st_rmax, o));
+    st_negw = fmax(st_negw, __shfl_xor_sync(0xffffffffu, st_negw, o));
+  }
+  st_out = __reduce_add_sync(0xffffffffu, st_out);
+  st_excl = __reduce_add_sync(0xffffffffu, st_excl);
+  st_bad = __reduce_add_sync(0xffffffffu, st_bad);
+  st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
+  LossAcc<1> acc;
+  acc.init();
+  acc.loss_num = st_loss;
+  acc.ent_sum = st_ent;
+  acc.ratio_sum = st_r;
+  acc.w_sum = st_w;
+  acc.rmax = st_rmax;
+  acc.negwmin = st_negw;
+  acc.n_out = st_out;
+  acc.n_excl = st_excl;
+  acc.n_bad = st_bad;
+  acc.n_badtok = st_badtok;
+  stats_epilogue<1>(acc, s_stat, stat_part, max_part);
+}
+
+// Dprev[j] = sum_k Dpk[j, k], Dpos[k] = sum_j Dpk[j, k]  (Dpk f32[(A+1), K, A])
+__global__ void pk_marginals_kernel(const float* __restrict__ dpk, int K, int A, int nprev,
+                                    float* __restrict__ dprev, float* __restrict__ dpos) {
+  const int64_t total = (int64_t)(nprev + K) * A;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(e % A);
+    const int64_t r = e / A;
+    float s = 0.f;
+    if (r < nprev) {
+      for (int k = 0; k < K; ++k) s += dpk[(r * K + k) * A + a];
+      dprev[r * A + a] = s;
+    } else {
+      const int k = (int)(r - nprev);
+      for (int jj = 0; jj < nprev; ++jj) s += dpk[((int64_t)jj * K + k) * A + a];
+      dpos[(int64_t)k * A + a] = s;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace accel
+
+using namespace accel;
+
+extern "C" int accel_fact_grid(int64_t N) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, kWarps), (int64_t)kNumSMs * 2));
+}
+
+extern "C" int accel_ep_plus(const float* ep, const float* pp, const float* bias, int A, int K,
+                             float* epp, void* stream) {
+  if (A < 1 || K < 1 || !ep || !pp || !bias || !epp) return fail(kDimension, "ep_plus: bad args");
+  const int64_t total = (int64_t)(A + 1) * K * A;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)kNumSMs * 4);
+  ep_plus_kernel<<<grid, 256, 0, as_stream(stream)>>>(ep, pp, bias, A, K, epp);
+  return post_launch("ep_plus_kernel");
+}
+
+extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* frame_of,
+                                     const int32_t* tokens, const float* lp_old, const float* adv,
+                                     int64_t N, int K, int A, int algo, double sigma,
+                                     double clip_eps, double lambda_h, double m_global,
+                                     const double* fix_stats, float* dz, float* g_frame,
+                                     float* lp_new, double* stat_part, double* max_part,
+                                     void* stream) {
+  if (algo != 0 && algo != 1) return fail(kDomain, "unknown algorithm %d", algo);
+  if (!(sigma > 0)) return fail(kDomain, "sigma must be > 0, got %g", sigma);
+  if (!(clip_eps > 0 && clip_eps < 1)) return fail(kDomain, "clip_eps must be in (0, 1)");
+  if (lambda_h < 0) return fail(kDomain, "loss coefficients must be >= 0");
+  if (N < 0 || K < 1 || K > 32 || A < 1) return fail(kDimension, "token_loss_fact: bad sizes");
+  if (A % 4 != 0 || A < 128 || A > 1024)
+    return fail(kDimension, "token_loss_fact needs 128 <= A <= 1024, A %% 4 == 0 (got %d)", A);
+  if (N == 0) return kOk;
+  if (!(m_global >= (double)(N * K))) return fail(kDimension, "m_global < local token count");
+  if (!h2w || !epp || !frame_of || !tokens || !lp_old || !adv || !dz || !g_frame ||
+      (!fix_stats && (!lp_new || !stat_part || !max_part)))
+    return fail(kDimension, "token_loss_fact: NULL buffer");
+  if (misaligned16(h2w) || misaligned16(epp) || misaligned16(dz) || misaligned16(g_frame))
+    return fail(kDimension, "token_loss_fact: buffers must be 16B aligned");
+  LossParams prm;
+  prm.algo = algo;
+  prm.sigma = (float)sigma;
+  prm.clip_lo = (float)(1.0 - clip_eps);
+  prm.clip_hi = (float)(1.0 + clip_eps);
+  prm.lambda_h = (float)lambda_h;
+  prm.inv_nk = 1.0 / m_global;
+  prm.m_global = m_global;
+  cudaStream_t s = as_stream(stream);
+  const int grid = accel_fact_grid(N);
+  auto go = [&](auto kernel, int VPL) -> int {
+    const size_t smem = (size_t)kWarps * (kStages + 1) * VPL * 32 * 4 +
+                        (size_t)kWarps * kStages * sizeof(uint64_t) + 16;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return fail(kCuda, "token_loss_fact smem: %s", cudaGetErrorString(e));
+    }
+    kernel<<<grid, kThreads, smem, s>>>(h2w, epp, frame_of, tokens, lp_old, adv, N, K, A, prm,
+                                        fix_stats, dz, g_frame, lp_new, stat_part, max_part);
+    return post_launch("token_loss_fact_kernel");
+  };
+  const bool full = A == 128 || A == 256 || A == 512 || A == 1024;
+  if (A <= 128)
+    return full ? go(token_loss_fact_kernel<4, true>, 4) : go(token_loss_fact_kernel<4, false>, 4);
+  if (A <= 256)
+    return full ? go(token_loss_fact_kernel<8, true>, 8) : go(token_loss_fact_kernel<8, false>, 8);
+  if (A <= 512)
+    return full ? go(token_loss_fact_kernel<16, true>, 16)
+                : go(token_loss_fact_kernel<16, false>, 16);
+  return full ? go(token_loss_fact_kernel<32, true>, 32) : go(token_loss_fact_kernel<32, false>, 32);
+}
+
+extern "C" int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, float* dpos,
+                                  void* stream) {
+  if (K < 1 || A < 1 || !dpk || !dprev || !dpos) return fail(kDimension, "pk_marginals: bad args");
+  const int nprev = A + 1;
+  const int64_t total = (int64_t)(nprev + K) * A;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)kNumSMs * 4);
+  pk_marginals_kernel<<<grid, 256, 0, as_stream(stream)>>>(dpk, K, A, nprev, dprev, dpos);
+  return post_launch("pk_marginals_kernel");
+}

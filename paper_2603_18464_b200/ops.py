@@ -202,15 +202,21 @@ def fact_grid(N: int) -> int:
     return int(_lib.lib().accel_fact_grid(int(N)))
 
 
-def token_loss_fact(h2w, ep, pp, bias, frame_of, tokens, lp_old, adv, N, K, algo, sigma, clip_eps,
+def ep_plus(ep, pp, bias, K, out):
+    A = ep.shape[1]
+    _lib.call("accel_ep_plus", _p(ep), _p(pp), _p(bias), A, int(K), _p(out), _stream())
+    return out
+
+
+def token_loss_fact(h2w, epp, frame_of, tokens, lp_old, adv, N, K, algo, sigma, clip_eps,
                     lambda_h, m_global, dz, g_frame, lp_new, stat_part, max_part,
                     fix_stats=None):
     """Factorized-head fused loss (see accel.h accel_token_loss_fact)."""
     A = h2w.shape[1]
-    _lib.call("accel_token_loss_fact", _p(h2w), _p(ep), _p(pp), _p(bias), _p(frame_of),
-              _p(tokens), _p(lp_old), _p(adv), int(N), int(K), A, int(algo), float(sigma),
-              float(clip_eps), float(lambda_h), float(m_global), _p(fix_stats), _p(dz),
-              _p(g_frame), _p(lp_new), _p(stat_part), _p(max_part), _stream())
+    _lib.call("accel_token_loss_fact", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(lp_old),
+              _p(adv), int(N), int(K), A, int(algo), float(sigma), float(clip_eps),
+              float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(g_frame), _p(lp_new),
+              _p(stat_part), _p(max_part), _stream())
 
 
 def pk_marginals(dpk, K, A, dprev, dpos):

@@ -622,6 +622,7 @@ class Trainer:
             h2w = _mm(h2, P["w_head"].t(), S.get("st.h2w", (F, A)))
             ep = _mm(P["e_prev"], P["w_head"].t(), S.get("st.ep", (A + 1, A)))
             pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
+            epp = ops.ep_plus(ep, pp, P["b_head"], K, S.get("st.epp", ((A + 1) * K, A)))
             gf = ops.fact_grid(N)
             dz = S.get("st.dz", (M, A))
             g_frame = S.get("st.gframe", (F, A))
@@ -629,9 +630,8 @@ class Trainer:
                 g_frame.zero_()
             stat_part = S.get("st.stat", (gf, 8), F64)
             max_part = S.get("st.max", (gf, 2), F64)
-            loss_args = (h2w, ep, pp, P["b_head"], batch.frame_of, batch.tokens_dev, batch.lp_old,
-                         batch.adv, N, K, algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dz,
-                         g_frame)
+            loss_args = (h2w, epp, batch.frame_of, batch.tokens_dev, batch.lp_old, batch.adv, N,
+                         K, algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dz, g_frame)
             with self._timed("token_loss"):
                 ops.token_loss_fact(*loss_args, lp_new, stat_part, max_part)
             gl = gf
