@@ -243,6 +243,16 @@ __device__ __forceinline__ RowStats row_stats_full(float (&z)[VPL], float (&e)[V
   return s;
 }
 
+// The rare float64 tail of token_coef, kept out of line so its register
+// footprint does not size the hot loop.
+__device__ __noinline__ float token_coef_f64(float dlt, float a, LossParams prm, double inv_m_d,
+                                             double* term_d, double* r_d, double* w_d,
+                                             bool* outside) {
+  double cd;
+  token_scalars<double>((double)dlt, (double)a, prm, cd, *term_d, *r_d, *w_d, *outside);
+  return (float)(cd * inv_m_d);
+}
+
 // Per-token coefficient c (= dloss/dlogp * m) and the statistics terms.
 __device__ __forceinline__ float token_coef(float dlt, float a, bool inc, const RowCtx& cx,
                                             double& term_d, double& r_d, double& w_d,
@@ -258,9 +268,7 @@ __device__ __forceinline__ float token_coef(float dlt, float a, bool inc, const 
       coef = cf * cx.inv_m;
       term_d = tf; r_d = rf; w_d = wf;
     } else {
-      double cd;
-      token_scalars<double>((double)dlt, (double)a, cx.prm, cd, term_d, r_d, w_d, outside);
-      coef = (float)(cd * cx.inv_m_d);
+      coef = token_coef_f64(dlt, a, cx.prm, cx.inv_m_d, &term_d, &r_d, &w_d, &outside);
     }
   }
   return coef;

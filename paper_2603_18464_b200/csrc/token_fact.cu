@@ -28,6 +28,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kGS = 2;  // H2W ring depth (transitions in flight per group) of the grouped kernel
 
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
@@ -139,8 +140,7 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
     load_vec<VPL>(er0, lane, A, epn, FULL);
     float ep_tok = __ldg(er0 + tok0);
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
-    float h[VPL], g[VPL];
-    L::load(hrow, lane, A, h, false);
+    float g[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[v] = 0.f;
     float my_coef = 0.f, my_H = 0.f;
@@ -152,8 +152,9 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
       const bool bad_tok = tok_raw < 0 || tok_raw >= A;
       const int tok = bad_tok ? 0 : tok_raw;
       float z[VPL];
+      L::load(hrow, lane, A, z, false);  // H2W row from the smem ring (re-read per token)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) z[v] = h[v] + epn[v];
+      for (int v = 0; v < VPL; ++v) z[v] += epn[v];
       const float z_tok = hrow[tok] + ep_tok;  // same arithmetic as z[] at column tok
       if (k + 1 < K) {  // prefetch the next token's EPP row (prev = this token) and column
         const int tn = min(max(__shfl_sync(0xffffffffu, tok_l, k + 1), 0), A - 1);
@@ -195,33 +196,31 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
       // dz = p (ent (d - sum p d) - coef) = e * (Ac d2 + Cc)   (+coef at the token column)
       const float Ac = ent2 * inv_s;
       const float Cc = -(Ac * sd2) - coef * inv_s;
-      float d[VPL];
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
-        const float x = e[v] * fmaf(Ac, z[v], Cc);
-        d[v] = x;
-        g[v] += x;
+        e[v] *= fmaf(Ac, z[v], Cc);  // e[] now holds this row's dlogits
+        g[v] += e[v];
       }
       const int64_t row = i * K + k;
       float* drow = dz + row * A;
-      L::store(drow, lane, A, d);
+      L::store(drow, lane, A, e);
       __syncwarp();
       if (lane == 0) {
         const float d2t = fmaf(z_tok, kLog2e, nm2);
         drow[tok] = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
         if (!cx.fixup) lp_new[row] = lpn;
       }
-      if (lane == k) {
-        my_coef = coef;
-        my_H = H;
-        my_term = term_d;
-        my_r = r_d;
-        my_w = w_d;
-        my_inc = inc;
-        my_bad = bad;
-        my_badtok = bad_tok;
-        my_out = outside;
-      }
+      // lane k keeps token k's scalars (predicated selects, no branch)
+      const bool mine = lane == k;
+      my_coef = mine ? coef : my_coef;
+      my_H = mine ? H : my_H;
+      my_term = mine ? term_d : my_term;
+      my_r = mine ? r_d : my_r;
+      my_w = mine ? w_d : my_w;
+      my_inc = mine ? inc : my_inc;
+      my_bad = mine ? bad : my_bad;
+      my_badtok = mine ? bad_tok : my_badtok;
+      my_out = mine ? outside : my_out;
     }
     // slot s is free: refill it with the transition kStages ahead
     fence_proxy_async();
@@ -261,6 +260,285 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
   }
   if (cx.fixup) return;
   // warp reduction of the per-lane statistics (fixed xor order), then CTA
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
+    st_ent += __shfl_xor_sync(0xffffffffu, st_ent, o);
+    st_r += __shfl_xor_sync(0xffffffffu, st_r, o);
+    st_w += __shfl_xor_sync(0xffffffffu, st_w, o);
+    st_rmax = fmax(st_rmax, __shfl_xor_sync(0xffffffffu, st_rmax, o));
+    st_negw = fmax(st_negw, __shfl_xor_sync(0xffffffffu, st_negw, o));
+  }
+  st_out = __reduce_add_sync(0xffffffffu, st_out);
+  st_excl = __reduce_add_sync(0xffffffffu, st_excl);
+  st_bad = __reduce_add_sync(0xffffffffu, st_bad);
+  st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
+  LossAcc<1> acc;
+  acc.init();
+  acc.loss_num = st_loss;
+  acc.ent_sum = st_ent;
+  acc.ratio_sum = st_r;
+  acc.w_sum = st_w;
+  acc.rmax = st_rmax;
+  acc.negwmin = st_negw;
+  acc.n_out = st_out;
+  acc.n_excl = st_excl;
+  acc.n_bad = st_bad;
+  acc.n_badtok = st_badtok;
+  stats_epilogue<1>(acc, s_stat, stat_part, max_part);
+}
+
+// ---- grouped variant: LPT lanes per transition, TPW = 32 / LPT transitions per warp ----
+// Full rows only (A == 4 * LPT * (VPL / 4)) and K <= LPT.  Every lane holds VPL
+// logits of its group's current token, so the per-token scalar algebra (log-sum,
+// ratio, trust weight, fix-up store) is issued once for TPW tokens.  Group-local
+// reductions use xor shuffles below LPT and group-masked CREDUX.
+template <int VPL, int LPT>
+__global__ void __launch_bounds__(kThreads, 2)
+token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
+                           const int32_t* __restrict__ frame_of,
+                           const int32_t* __restrict__ tokens, const float* __restrict__ lp_old,
+                           const float* __restrict__ adv, int64_t N, int K, int A,
+                           LossParams prm, const double* __restrict__ fix_stats,
+                           float* __restrict__ dz, float* __restrict__ g_frame,
+                           float* __restrict__ lp_new, double* __restrict__ stat_part,
+                           double* __restrict__ max_part) {
+  constexpr int TPW = 32 / LPT;
+  constexpr int W = VPL * LPT;  // == A
+  constexpr int Q = VPL / 4;    // float4 chunks per lane
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
+  RowCtx cx;
+  if (!setup_ctx(prm, fix_stats, cx)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / LPT, gl = lane % LPT, gbase = grp * LPT;
+  const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << gbase);
+  // smem: ring [kWarps][kGS][TPW][W] | s_oh [kWarps][TPW][W] | bars [kWarps][kGS][TPW]
+  float* ring = reinterpret_cast<float*>(smem) + ((size_t)warp * kGS * TPW + grp) * W;
+  float* s_oh = reinterpret_cast<float*>(smem) + (size_t)kWarps * kGS * TPW * W +
+                ((size_t)warp * TPW + grp) * W;
+  // EPP rows: s_ep[2] = the chunk-start row (prev = A, k = 0), s_ep[0]/[1] a
+  // double buffer for tokens k >= 1, each filled by a bulk copy one token ahead
+  float* s_ep = reinterpret_cast<float*>(smem) + (size_t)kWarps * (kGS + 1) * TPW * W +
+                ((size_t)warp * TPW + grp) * 3 * W;
+  uint64_t* bar_base =
+      reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem) + (size_t)kWarps * (kGS + 4) * TPW * W);
+  uint64_t* bars = bar_base + ((size_t)warp * kGS) * TPW + grp;
+  uint64_t* ebars = bar_base + (size_t)kWarps * kGS * TPW + ((size_t)warp * TPW + grp) * 2;
+  for (int c = gl; c < W; c += LPT) {
+    s_oh[c] = 0.f;
+    s_ep[2 * W + c] = __ldg(epp + (int64_t)A * K * A + c);
+  }
+  const unsigned row_bytes = (unsigned)A * 4u;
+  // transition of group `grp` at iteration j: i = gi0 + j * gstride
+  const int64_t gi0 = ((int64_t)blockIdx.x * kWarps + warp) * TPW + grp;
+  const int64_t gstride = (int64_t)gridDim.x * kWarps * TPW;
+  unsigned eph = 0;  // ebars[0/1] phase bits
+  if (gl == 0) {
+    mbar_init(&ebars[0], 1);
+    mbar_init(&ebars[1], 1);
+#pragma unroll
+    for (int s = 0; s < kGS; ++s) mbar_init(&bars[s * TPW], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < kGS; ++s) {
+      const int64_t i = gi0 + s * gstride;
+      if (i < N) {
+        mbar_expect_tx(&bars[s * TPW], row_bytes);
+        bulk_g2s(ring + (size_t)s * TPW * W, h2w + (int64_t)__ldg(frame_of + i) * A, row_bytes,
+                 &bars[s * TPW]);
+      }
+    }
+  }
+  __syncwarp();
+  const float ent2 = cx.ent_scale * kLn2;
+  double st_loss = 0.0, st_ent = 0.0, st_r = 0.0, st_w = 0.0;
+  double st_rmax = -CUDART_INF, st_negw = -CUDART_INF;
+  int st_out = 0, st_excl = 0, st_bad = 0, st_badtok = 0;
+
+  auto colof = [&](int q, int r) { return q * 4 * LPT + gl * 4 + r; };
+  auto load_grp = [&](const float* __restrict__ row, float (&x)[VPL], bool global) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const float4* p = reinterpret_cast<const float4*>(row + q * 4 * LPT + gl * 4);
+      const float4 y = global ? __ldg(p) : *p;
+      x[4 * q] = y.x; x[4 * q + 1] = y.y; x[4 * q + 2] = y.z; x[4 * q + 3] = y.w;
+    }
+  };
+
+  // per-transition scalars, prefetched one iteration ahead (lane gl < K: token gl)
+  int fi_n = 0, tok_n = 0;
+  float lpo_n = 0.f, a_n = 0.f;
+  if (gi0 < N) {
+    fi_n = __ldg(frame_of + gi0);
+    tok_n = gl < K ? __ldg(tokens + gi0 * K + gl) : 0;
+    lpo_n = gl < K ? __ldg(lp_old + gi0 * K + gl) : 0.f;
+    a_n = __ldg(adv + gi0);
+  }
+  const int64_t n_iter = gi0 - grp < N ? ceil_div(N - (gi0 - grp), gstride) : 0;  // group 0's count
+  for (int64_t j = 0; j < n_iter; ++j) {
+    const int64_t i = gi0 + j * gstride;
+    const bool act = i < N;
+    const int s = (int)(j % kGS);
+    const float* hrow = ring + (size_t)s * TPW * W;
+    const int fi = fi_n, tok_l = tok_n;
+    const float lpo_l = lpo_n, a = a_n;
+    const int64_t next = i + kGS * gstride;
+    const int f_next = (gl == 0 && next < N) ? __ldg(frame_of + next) : 0;
+    if (i + gstride < N) {
+      const int64_t i2 = i + gstride;
+      fi_n = __ldg(frame_of + i2);
+      tok_n = gl < K ? __ldg(tokens + i2 * K + gl) : 0;
+      lpo_n = gl < K ? __ldg(lp_old + i2 * K + gl) : 0.f;
+      a_n = __ldg(adv + i2);
+    }
+    // token 1's EPP row (prev = token 0) into slot 1; slot 1's last reader is done
+    fence_proxy_async();
+    __syncwarp();
+    if (act && gl == 0 && K > 1) {
+      const int t0 = min(max(tok_l, 0), A - 1);
+      mbar_expect_tx(&ebars[1], row_bytes);
+      bulk_g2s(s_ep + W, epp + ((int64_t)t0 * K + 1) * A, row_bytes, &ebars[1]);
+    }
+    if (act) mbar_wait(&bars[s * TPW], (unsigned)(j / kGS) & 1u);
+    float g[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) g[v] = 0.f;
+    float my_coef = 0.f, my_H = 0.f;
+    double my_term = 0.0, my_r = 1.0, my_w = 1.0;
+    bool my_inc = false, my_bad = false, my_badtok = false, my_out = false;
+    for (int k = 0; k < K; ++k) {
+      const int tok_raw = __shfl_sync(0xffffffffu, tok_l, gbase + k);
+      const float lpo = __shfl_sync(0xffffffffu, lpo_l, gbase + k);
+      const bool bad_tok = tok_raw < 0 || tok_raw >= A;
+      const int tok = bad_tok ? 0 : tok_raw;
+      const float* erow = s_ep + (k == 0 ? 2 : (k & 1)) * W;
+      if (k > 0) {
+        if (act) mbar_wait(&ebars[k & 1], (eph >> (k & 1)) & 1u);
+        eph ^= 1u << (k & 1);
+        // token k+1's row goes into the slot token k-1 used (fully read by now)
+        fence_proxy_async();
+        __syncwarp();
+        if (act && gl == 0 && k + 1 < K) {
+          const int sl = (k + 1) & 1;
+          mbar_expect_tx(&ebars[sl], row_bytes);
+          bulk_g2s(s_ep + sl * W, epp + ((int64_t)tok * K + k + 1) * A, row_bytes, &ebars[sl]);
+        }
+      }
+      float z[VPL], ez[VPL];
+      load_grp(hrow, z, false);
+      load_grp(erow, ez, false);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) z[v] += ez[v];
+      const float z_tok = hrow[tok] + erow[tok];
+      float mx = fmaxf(fmaxf(z[0], z[1]), z[2]);
+#pragma unroll
+      for (int v = 3; v < VPL; v += 2) mx = fmaxf(mx, v + 1 < VPL ? fmaxf(z[v], z[v + 1]) : z[v]);
+      {
+        float r;
+        asm volatile("redux.sync.max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(mx), "r"(gmask));
+        mx = r;
+      }
+      const float nm2 = -mx * kLog2e;
+      float e[VPL], sum = 0.f, sed = 0.f;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        z[v] = fmaf(z[v], kLog2e, nm2);
+        e[v] = ex2_ftz(z[v]);
+        sum += e[v];
+        sed = fmaf(e[v], z[v], sed);
+      }
+#pragma unroll
+      for (int o = LPT / 2; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        sed += __shfl_xor_sync(0xffffffffu, sed, o);
+      }
+      const bool bad = !isfinite(sum) || !isfinite(sed) || !isfinite(mx);
+      const float inv_s = 1.f / sum;
+      const float log_s = __logf(sum);
+      const float sd2 = sed * inv_s;
+      const float H = log_s - sd2 * kLn2;
+      const float d_tok = z_tok - mx;
+      const float lpn = d_tok - log_s;
+      const float dlt = lpn - lpo;
+      const bool inc = act && !bad_tok && !bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
+      double term_d, r_d, w_d;
+      bool outside;
+      const float coef = token_coef(dlt, a, inc, cx, term_d, r_d, w_d, outside);
+      const float Ac = ent2 * inv_s;
+      const float Cc = -(Ac * sd2) - coef * inv_s;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        e[v] *= fmaf(Ac, z[v], Cc);
+        g[v] += e[v];
+      }
+      const int64_t row = i * K + k;
+      float* drow = dz + row * A;
+      if (act) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          __stcs(reinterpret_cast<float4*>(drow + colof(q, 0)),
+                 make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]));
+      }
+      __syncwarp();
+      if (act && gl == 0) {
+        const float d2t = fmaf(z_tok, kLog2e, nm2);
+        drow[tok] = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
+        if (!cx.fixup) lp_new[row] = lpn;
+      }
+      const bool mine = gl == k;
+      my_coef = mine ? coef : my_coef;
+      my_H = mine ? H : my_H;
+      my_term = mine ? term_d : my_term;
+      my_r = mine ? r_d : my_r;
+      my_w = mine ? w_d : my_w;
+      my_inc = mine ? inc : my_inc;
+      my_bad = mine ? bad : my_bad;
+      my_badtok = mine ? bad_tok : my_badtok;
+      my_out = mine ? outside : my_out;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (gl == 0 && next < N) {
+      mbar_expect_tx(&bars[s * TPW], row_bytes);
+      bulk_g2s(ring + (size_t)s * TPW * W, h2w + (int64_t)f_next * A, row_bytes, &bars[s * TPW]);
+    }
+    // one-hot part of G (group leader, serial over k: duplicates accumulate)
+    for (int k = 0; k < K; ++k) {
+      const int tk = __shfl_sync(0xffffffffu, tok_l, gbase + k);
+      const float ck = __shfl_sync(0xffffffffu, my_coef, gbase + k);
+      if (gl == 0 && tk >= 0 && tk < A) s_oh[tk] += ck;
+    }
+    __syncwarp();
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float4 o = *reinterpret_cast<const float4*>(s_oh + colof(q, 0));
+        __stcs(reinterpret_cast<float4*>(g_frame + (int64_t)fi * A + colof(q, 0)),
+               make_float4(g[4 * q] + o.x, g[4 * q + 1] + o.y, g[4 * q + 2] + o.z,
+                           g[4 * q + 3] + o.w));
+      }
+    }
+    __syncwarp();
+    if (gl < K && tok_l >= 0 && tok_l < A) s_oh[tok_l] = 0.f;
+    __syncwarp();
+    if (!cx.fixup && act && gl < K) {
+      st_ent += (double)my_H;
+      st_bad += my_bad;
+      st_badtok += my_badtok;
+      if (my_inc) {
+        st_loss += my_term;
+        st_r += my_r;
+        st_w += my_w;
+        st_out += my_out;
+        st_rmax = fmax(st_rmax, my_r);
+        st_negw = fmax(st_negw, -my_w);
+      } else {
+        ++st_excl;
+      }
+    }
+  }
+  if (cx.fixup) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
@@ -358,9 +636,15 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
   prm.m_global = m_global;
   cudaStream_t s = as_stream(stream);
   const int grid = accel_fact_grid(N);
-  auto go = [&](auto kernel, int VPL) -> int {
-    const size_t smem = (size_t)kWarps * (kStages + 1) * VPL * 32 * 4 +
-                        (size_t)kWarps * kStages * sizeof(uint64_t) + 16;
+  // TPW == 0: per-warp kernel (ring kStages deep); TPW >= 1: grouped kernel
+  // (ring kGS deep + s_oh + 3 EPP rows per group, 2 extra mbarriers per group)
+  auto go = [&](auto kernel, int VPL, int TPW = 0) -> int {
+    const size_t row_floats = (size_t)VPL * 32;  // floats per warp per stage
+    const size_t smem =
+        TPW == 0 ? (size_t)kWarps * (kStages + 1) * row_floats * 4 +
+                       (size_t)kWarps * kStages * sizeof(uint64_t) + 16
+                 : (size_t)kWarps * (kGS + 4) * row_floats * 4 +
+                       (size_t)kWarps * (kGS + 2) * TPW * sizeof(uint64_t) + 16;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
@@ -371,6 +655,11 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
     return post_launch("token_loss_fact_kernel");
   };
   const bool full = A == 128 || A == 256 || A == 512 || A == 1024;
+  // grouped kernel: 16 (32 at A = 1024) logits per lane, A / that lanes per transition
+  if (A == 128 && K <= 8) return go(token_loss_fact_grp_kernel<16, 8>, 16, 4);
+  if (A == 256 && K <= 16) return go(token_loss_fact_grp_kernel<16, 16>, 16, 2);
+  if (A == 512 && K <= 32) return go(token_loss_fact_grp_kernel<16, 32>, 16, 1);
+  if (A == 1024 && K <= 32) return go(token_loss_fact_grp_kernel<32, 32>, 32, 1);
   if (A <= 128)
     return full ? go(token_loss_fact_kernel<4, true>, 4) : go(token_loss_fact_kernel<4, false>, 4);
   if (A <= 256)
