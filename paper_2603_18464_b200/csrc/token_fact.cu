@@ -140,6 +140,7 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
     load_vec<VPL>(er0, lane, A, epn, FULL);
     float ep_tok = __ldg(er0 + tok0);
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    __syncwarp();  // reconverge: lanes may leave the spin-wait at different times
     float g[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[v] = 0.f;
@@ -401,6 +402,7 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       bulk_g2s(s_ep + W, epp + ((int64_t)t0 * K + 1) * A, row_bytes, &ebars[1]);
     }
     if (act) mbar_wait(&bars[s * TPW], (unsigned)(j / kGS) & 1u);
+    __syncwarp();  // reconverge both groups before the element loop
     float g[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[v] = 0.f;
@@ -415,6 +417,7 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       const float* erow = s_ep + (k == 0 ? 2 : (k & 1)) * W;
       if (k > 0) {
         if (act) mbar_wait(&ebars[k & 1], (eph >> (k & 1)) & 1u);
+        __syncwarp();
         eph ^= 1u << (k & 1);
         // token k+1's row goes into the slot token k-1 used (fully read by now)
         fence_proxy_async();

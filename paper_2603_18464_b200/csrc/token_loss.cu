@@ -241,6 +241,7 @@ token_loss_tma_kernel(const float* __restrict__ logits, const float* __restrict_
   for (int64_t row = gw; row < M; row += nw, ++j) {
     const int s = j % kStages;
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    __syncwarp();  // reconverge: lanes may leave the spin-wait at different times
     float z[VPL];
     L::load(ring + s * VPL * 32, lane, A, z, false);
     fence_proxy_async();
@@ -352,6 +353,7 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
     const int tok_raw = tok_next;
     if (row + nw < M) tok_next = __ldg(tokens + row + nw);
     mbar_wait(&bars[s], (unsigned)(j / kStages) & 1u);
+    __syncwarp();  // reconverge: lanes may leave the spin-wait at different times
     float z[VPL], e[VPL];
     L::load(slot, lane, A, z, false);
     const bool bt = tok_raw < 0 || tok_raw >= A;
