@@ -313,7 +313,6 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
   if (!setup_ctx(prm, fix_stats, cx)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / LPT, gl = lane % LPT, gbase = grp * LPT;
-  const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << gbase);
   // smem: ring [kWarps][kGS][TPW][W] | s_oh [kWarps][TPW][W] | bars [kWarps][kGS][TPW]
   float* ring = reinterpret_cast<float*>(smem) + ((size_t)warp * kGS * TPW + grp) * W;
   float* s_oh = reinterpret_cast<float*>(smem) + (size_t)kWarps * kGS * TPW * W +
@@ -437,10 +436,16 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       float mx = fmaxf(fmaxf(z[0], z[1]), z[2]);
 #pragma unroll
       for (int v = 3; v < VPL; v += 2) mx = fmaxf(mx, v + 1 < VPL ? fmaxf(z[v], z[v + 1]) : z[v]);
-      {
-        float r;
-        asm volatile("redux.sync.max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(mx), "r"(gmask));
-        mx = r;
+      if (LPT == 32) {
+        mx = warp_max_nan(mx);
+      } else {
+        // group max with full-warp xor shuffles: a group-masked CREDUX would split
+        // the warp into its groups for the rest of the row (each ran the row alone)
+#pragma unroll
+        for (int o = LPT / 2; o > 0; o >>= 1) {
+          const float y = __shfl_xor_sync(0xffffffffu, mx, o);
+          mx = (mx != mx || y != y) ? __int_as_float(0x7fffffff) : fmaxf(mx, y);  // NaN-propagating
+        }
       }
       const float nm2 = -mx * kLog2e;
       float e[VPL], sum = 0.f, sed = 0.f;
