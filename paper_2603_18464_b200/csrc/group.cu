@@ -201,16 +201,32 @@ piece_sum_kernel(const float* __restrict__ vals, const int32_t* __restrict__ per
   }
 }
 
-__global__ void key_sum_kernel(const float* __restrict__ piece_out,
-                               const int64_t* __restrict__ piece_off, int nkeys, int D,
-                               float* __restrict__ out) {
-  const int64_t total = (int64_t)nkeys * D;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int key = (int)(e / D), d = (int)(e % D);
+// One CTA per key: `sub` row-lanes split the key's pieces round-robin (fixed
+// order), then the row-lanes are combined in order.  A key with thousands of
+// pieces (the chunk-start token holds one row per transition) is summed by a
+// whole CTA instead of one serial thread per column.
+__global__ void __launch_bounds__(kThreads)
+key_sum_kernel(const float* __restrict__ piece_out, const int64_t* __restrict__ piece_off,
+               int nkeys, int D, float* __restrict__ out) {
+  extern __shared__ float s_acc[];
+  const int key = blockIdx.x;
+  const int64_t p0 = piece_off[key], p1 = piece_off[key + 1];
+  const int span = (D <= kThreads && kThreads % D == 0) ? D : kThreads;
+  const int sub = kThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  for (int d0 = 0; d0 < D; d0 += span) {
+    const int d = d0 + lc;
     float acc = 0.f;
-    for (int64_t p = piece_off[key]; p < piece_off[key + 1]; ++p) acc += piece_out[p * D + d];
-    out[e] = acc;
+    if (d < D)
+      for (int64_t p = p0 + lr; p < p1; p += sub) acc += piece_out[p * D + d];
+    s_acc[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D) {
+      float a = 0.f;
+      for (int s = 0; s < sub; ++s) a += s_acc[s * span + threadIdx.x];
+      out[(int64_t)key * D + d0 + threadIdx.x] = a;
+    }
+    __syncthreads();
   }
 }
 
@@ -318,8 +334,7 @@ extern "C" int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const
         vals, perm, seg_off, piece_off, nkeys, D, piece_buf);
     if ((st = post_launch("piece_sum_kernel"))) return st;
   }
-  const int64_t total = (int64_t)nkeys * D;
-  const int grid = (int)std::min<int64_t>(ceil_div(total, kThreads), (int64_t)kNumSMs * 4);
-  key_sum_kernel<<<grid, kThreads, 0, s>>>(piece_buf, piece_off, nkeys, D, out);
+  key_sum_kernel<<<nkeys, kThreads, kThreads * sizeof(float), s>>>(piece_buf, piece_off, nkeys, D,
+                                                                   out);
   return post_launch("key_sum_kernel");
 }

@@ -187,6 +187,58 @@ tanh_grad_colsum_kernel(float* __restrict__ g, const float* __restrict__ h, int6
   }
 }
 
+// float4 variant (C % 4 == 0, 256 % (C/4) == 0): same fixed summation order
+// per (row-lane, column), four rows in flight per thread.
+__global__ void __launch_bounds__(kThreads)
+tanh_grad_colsum4_kernel(float4* __restrict__ g, const float4* __restrict__ h, int64_t R, int C4,
+                         float* __restrict__ col_part) {
+  extern __shared__ float4 s_acc4[];  // [sub][C4]
+  const int sub = kThreads / C4;
+  const int lr = threadIdx.x / C4, lc = threadIdx.x % C4;
+  const int64_t per = ceil_div(R, (int64_t)gridDim.x);
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(R, r0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t r = r0 + lr;
+  for (; r + 3 * sub < r1; r += 4 * sub) {
+    float4 gv[4], hv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      gv[u] = g[(r + u * sub) * C4 + lc];
+      hv[u] = __ldg(h + (r + u * sub) * C4 + lc);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float4 v;
+      v.x = gv[u].x * (1.f - hv[u].x * hv[u].x);
+      v.y = gv[u].y * (1.f - hv[u].y * hv[u].y);
+      v.z = gv[u].z * (1.f - hv[u].z * hv[u].z);
+      v.w = gv[u].w * (1.f - hv[u].w * hv[u].w);
+      g[(r + u * sub) * C4 + lc] = v;
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  for (; r < r1; r += sub) {
+    const float4 gv = g[r * C4 + lc], hv = __ldg(h + r * C4 + lc);
+    float4 v;
+    v.x = gv.x * (1.f - hv.x * hv.x);
+    v.y = gv.y * (1.f - hv.y * hv.y);
+    v.z = gv.z * (1.f - hv.z * hv.z);
+    v.w = gv.w * (1.f - hv.w * hv.w);
+    g[r * C4 + lc] = v;
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  s_acc4[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < C4) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < sub; ++s) {
+      const float4 y = s_acc4[s * C4 + threadIdx.x];
+      a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
+    }
+    reinterpret_cast<float4*>(col_part + (int64_t)blockIdx.x * C4 * 4)[threadIdx.x] = a;
+  }
+}
+
 int row_grid(int64_t rows) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)kNumSMs * 4));
 }
@@ -263,6 +315,13 @@ extern "C" int accel_tanh_grad_colsum(float* g, const float* h, int64_t R, int C
   if (R == 0) return kOk;
   if (!g || !h || !col_part) return fail(kDimension, "tanh_grad_colsum: NULL buffer");
   if (grid < 1) return fail(kDimension, "tanh_grad_colsum: grid < 1");
+  const uintptr_t al = reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(h) |
+                       reinterpret_cast<uintptr_t>(col_part);
+  if (C % 4 == 0 && C / 4 <= kThreads && kThreads % (C / 4) == 0 && (al & 15) == 0) {
+    tanh_grad_colsum4_kernel<<<grid, kThreads, kThreads * sizeof(float4), as_stream(stream)>>>(
+        reinterpret_cast<float4*>(g), reinterpret_cast<const float4*>(h), R, C / 4, col_part);
+    return post_launch("tanh_grad_colsum4_kernel");
+  }
   const ColLayout L = ColLayout::make(C);
   const size_t smem = sizeof(float) * (size_t)L.sub * L.span;
   tanh_grad_colsum_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(g, h, R, C, col_part);
