@@ -55,7 +55,9 @@ class Dims:
 
 
 class FlatLayout:
-    def __init__(self, dims: Dims) -> None:
+    def __init__(self, dims: Dims, pad_to: int = 4) -> None:
+        """pad_to: the total is rounded up to a multiple of it (4 * world for
+        ZeRO-2 so every rank's shard is equal and 16-byte aligned)."""
         self.dims = dims
         shapes = dims.shapes()
         self.offsets, self.shapes = {}, {}
@@ -67,7 +69,7 @@ class FlatLayout:
             self.offsets[name] = off
             self.shapes[name] = shapes[name]
             off += (n + 3) // 4 * 4
-        self.total = off
+        self.total = (off + pad_to - 1) // pad_to * pad_to
 
     def views(self, buf: torch.Tensor) -> dict:
         out = {}

@@ -342,7 +342,7 @@ class Trainer:
         self.rng = np.random.default_rng(np.random.SeedSequence([seed, 7]))
         self._bundle = bundle
         self.dims = Dims.from_models(bundle.policy, bundle.value)
-        self.layout = FlatLayout(self.dims)
+        self.layout = FlatLayout(self.dims, pad_to=4 * (comm.world if comm is not None else 1))
         self.params = DeviceParams(self.layout, self.device)
         self.params.load(bundle.policy.params.tensors, bundle.value.params.tensors)
         self._policy_version = int(getattr(bundle.policy.params, "version", 0))
@@ -535,7 +535,16 @@ class Trainer:
             behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
         batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized)
         batch.h_cache = h_cache
-        host = torch.cat([flags, cnt.double()]).cpu().numpy()  # the one host sync
+        host_dev = torch.cat([flags, cnt.double()])
+        if self.comm is not None:
+            # data parallel: the batch is one shard of the global batch; every
+            # accept/reject decision and the count are global (all ranks agree)
+            idx = torch.tensor([3, 8, 9, 10, 11, 16, 17], device=dev)
+            dec = host_dev.index_select(0, idx)
+            self.comm.all_reduce_sum(dec)
+            host_dev.index_copy_(0, idx, dec)
+            host_dev[2:3].copy_(sums[2:3])
+        host = host_dev.cpu().numpy()  # the one host sync
         if host[7] == 1:
             raise DomainError("cannot normalize zero advantages")
         if host[7] == 2:
@@ -550,6 +559,7 @@ class Trainer:
             raise DimensionError("token index outside the action vocabulary")
         batch.norm_mean, batch.norm_std = float(host[4]), float(host[5])
         batch.norm_count = int(host[2])
+        batch.global_n = int(host[2])
         finite = host[3] == 0 and host[16] == 0
         batch._finite = bool(finite)
         return batch if finite else None
@@ -605,8 +615,12 @@ class Trainer:
         cnt.zero_()
         fact = self.factorized
         batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=fact)
-        n_glob = self.comm.global_counts(N) if self.comm is not None else (N, M)
-        N_glob, M_glob = n_glob
+        if self.comm is None:
+            N_glob, M_glob = N, M
+        elif getattr(batch, "global_n", None) is not None:
+            N_glob, M_glob = batch.global_n, batch.global_n * K
+        else:
+            N_glob, M_glob = self.comm.global_counts(N, K)
         algo = _algo_id(lc)
         lp_new = S.get("st.lp_new", (M,))
         loss_sums = S.get("st.lsum", (8,), F64)
@@ -734,11 +748,15 @@ class Trainer:
         attn_bad = S.get("st.abad", (2,), F64)
         ops.reduce_f64(vdpart, gw, 2, 0, value_sums)
         ops.reduce_f64(vbad_part, gw, 2, 0, attn_bad)
-        if self.comm is not None:
-            self.comm.reduce_grads(self.params.g)
-            self.comm.all_reduce_sum(value_sums)
-            self.comm.all_reduce_sum(attn_bad)
         ops.count_nonfinite(self.params.g, cnt[0:1])
+        if self.comm is not None:
+            # C5 scalars in one fp64 all-reduce; local grads all finite on every
+            # rank <=> the reduced grads are finite (barring overflow)
+            sc = torch.cat([value_sums, attn_bad, cnt[0:2].double()])
+            self.comm.all_reduce_sum(sc)
+            value_sums.copy_(sc[0:2])
+            attn_bad.copy_(sc[2:4])
+            cnt[0:2].copy_(sc[4:6].to(torch.int32))
         record = S.get("st.record", (17,), F64)
         skip = S.get("st.skip", (1,), torch.int32)
         ops.step_finalize(loss_sums, loss_max, value_sums, cnt, attn_bad, algo, lc.lambda_v,
@@ -750,7 +768,10 @@ class Trainer:
         cur, nxt = self.params.cur, self.params.cur ^ 1
         adam_bad = cnt[2:3]
         if self.comm is not None:
-            self.comm.adam(self.params, hyp, skip, adam_bad)
+            # ZeRO-2: reduce-scatter grads, Adam on this rank's shard, all-gather
+            self.comm.adam(self.params, self.layout.n_policy, hyp, skip, adam_bad,
+                           adam_fn=ops.adam)
+            ops.count_nonfinite(self.params.p[nxt], adam_bad)
         else:
             ops.adam(self.params.p[cur], self.params.g, self.params.m[cur], self.params.v[cur],
                      self.params.p[nxt], self.params.m[nxt], self.params.v[nxt],

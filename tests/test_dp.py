@@ -1,0 +1,149 @@
+"""Data-parallel (ZeRO-2) host logic on CPU with the gloo backend, world_size 2.
+
+The GPU kernels are not involved: Adam is injected as a float64 torch
+function so the ZeRO-2 plumbing (shard bounds, padding, reduce-scatter,
+per-shard Adam with the policy/value group split, all-gather) is checked
+against a single-process Adam over the summed gradients.  The end-to-end
+multi-GPU parity check (R-rank step == one-process step on the concatenated
+batch) is tests/dp_gpu_check.py, run by test_dp_gpu_two_ranks on >= 2 GPUs.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def torch_adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, g0, g1, skip, bad):
+    """float64 restatement of accel_adam on CPU tensors (numerics.py:95-126)."""
+    if int(skip[0]):
+        return
+    n = p_in.numel()
+    for lo, hi, hp in ((0, n0, g0), (n0, n, g1)):
+        if hi <= lo:
+            continue
+        lr, b1, b2, eps, bc1, bc2 = hp
+        gg = g[lo:hi].double()
+        m = b1 * m_in[lo:hi].double() + (1 - b1) * gg
+        v = b2 * v_in[lo:hi].double() + (1 - b2) * gg * gg
+        w = p_in[lo:hi].double() - lr * (m / bc1) / (torch.sqrt(v / bc2) + eps)
+        p_out[lo:hi] = w.float()
+        m_out[lo:hi] = m.float()
+        v_out[lo:hi] = v.float()
+
+
+class _Params:
+    def __init__(self, total, seed):
+        gen = torch.Generator().manual_seed(seed)
+        self.p = [torch.randn(total, generator=gen), torch.zeros(total)]
+        self.m = [torch.randn(total, generator=gen).abs() * 1e-3, torch.zeros(total)]
+        self.v = [torch.rand(total, generator=gen) * 1e-4, torch.zeros(total)]
+        self.g = torch.zeros(total)
+        self.cur = 0
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_18464_b200.dp import DataParallel
+        dp = DataParallel(adam_fn=torch_adam)
+        total, n_policy = 40, 22  # padded to a multiple of 4 * world
+        params = _Params(total, seed=5)
+        grads = [torch.randn(total, generator=torch.Generator().manual_seed(100 + r))
+                 for r in range(world)]
+        params.g.copy_(grads[rank])
+        hyp = ((3e-4, 0.9, 0.999, 1e-8, 1 - 0.9, 1 - 0.999),
+               (1e-3, 0.8, 0.99, 1e-8, 1 - 0.8, 1 - 0.99))
+        skip = torch.zeros(1, dtype=torch.int32)
+        bad = torch.zeros(1, dtype=torch.int32)
+        dp.adam(params, n_policy, hyp, skip, bad)
+        # C1: pooled statistics from per-rank sums
+        x = torch.arange(10, dtype=torch.float64) * (rank + 1)
+        sums = torch.tensor([x.sum().item(), (x * x).sum().item(), float(x.numel())],
+                            dtype=torch.float64)
+        dp.all_reduce_sum(sums)
+        mx = torch.tensor([float(rank)], dtype=torch.float64)
+        dp.all_reduce_max(mx)
+        out_q.put((rank, params.p[1].clone(), sums, mx, dp.shard_bounds(total),
+                   dp.global_counts(7 + rank, 3)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zero2_adam_and_collectives_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, p_new, sums, mx, bounds, counts = q.get(timeout=120)
+        res[rank] = (p_new, sums, mx, bounds, counts)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # single-process reference: full Adam on the summed gradients
+    total, n_policy = 40, 22
+    ref = _Params(total, seed=5)
+    g_sum = sum(torch.randn(total, generator=torch.Generator().manual_seed(100 + r))
+                for r in range(world))
+    hyp = ((3e-4, 0.9, 0.999, 1e-8, 1 - 0.9, 1 - 0.999),
+           (1e-3, 0.8, 0.99, 1e-8, 1 - 0.8, 1 - 0.99))
+    torch_adam(ref.p[0], g_sum, ref.m[0], ref.v[0], ref.p[1], ref.m[1], ref.v[1], n_policy,
+               hyp[0], hyp[1], torch.zeros(1, dtype=torch.int32), None)
+    for r in range(world):
+        torch.testing.assert_close(res[r][0], ref.p[1], rtol=0, atol=1e-7)
+        xs = [torch.arange(10, dtype=torch.float64) * (q_ + 1) for q_ in range(world)]
+        allx = torch.cat(xs)
+        assert res[r][1].tolist() == pytest.approx([allx.sum().item(), (allx * allx).sum().item(),
+                                                    20.0])
+        assert res[r][2].item() == world - 1
+        assert res[r][4] == (7 + 8, (7 + 8) * 3)
+    assert res[0][3] == (0, 20) and res[1][3] == (20, 40)
+
+
+def test_partition_trajectories_is_contiguous_and_balanced():
+    from paper_2603_18464_b200.dp import partition_trajectories
+    rng = np.random.default_rng(0)
+    lens = rng.integers(1, 521, size=1000)
+    for world in (1, 2, 4, 8):
+        spans = [partition_trajectories(lens, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == 1000
+        for a, b in zip(spans, spans[1:]):
+            assert a[1] == b[0]
+        loads = [int(lens[a:b].sum()) for a, b in spans]
+        assert max(loads) - min(loads) <= 2 * 520
+
+
+@pytest.mark.gpu
+def test_dp_gpu_two_ranks():
+    """R=2 ZeRO-2 step over NCCL == one-process step on the concatenated batch."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(ROOT / "tests" / "dp_gpu_check.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "DP PARITY OK" in res.stdout
