@@ -243,6 +243,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
+    # keep stdout for the single JSON line: library banners (NCCL) go to stderr
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         from paper_2603_18464_b200.dp import DataParallel
@@ -380,6 +383,8 @@ def main():
         "clocks": clocks.summary,
         "last_record": {k: rec[k] for k in ("loss", "policy_loss", "value_loss", "entropy")},
     }
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
     print(json.dumps(line), flush=True)
     if comm is not None:
         dist.destroy_process_group()
