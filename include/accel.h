@@ -249,6 +249,33 @@ int accel_adam(const float* p_in, const float* g, const float* m_in, const float
                const double* group0, const double* group1, const int* skip,
                unsigned* bad, void* stream);
 
+/* ---- (c) world-model imagination (rollout.py:295-362) ------------------ */
+
+/* Shared memory per 4-trajectory CTA (float64 activations). */
+size_t accel_imagine_smem_bytes(int O, int D, int A, int HV, int HO, int HR);
+
+/* H imagined steps for n trajectories in one launch, float64 throughout:
+ * per step sample_chunk + state_value (models.py:135-150, :406-408),
+ * ObsModel.predict (:349-355), snap_observation (env.py:259-283),
+ * RewardModel.predict (models.py:375-377), r = p' - p, stop at p' >= threshold.
+ *   weights  23 device pointers, f64, weight matrices TRANSPOSED ([in][out]):
+ *            w0t b0 w1t b1 e_prev e_pos w_headt b_head | w_attn b_attn e_step
+ *            w0vt b0v w1v b1v | ow0t ob0 ow1t ob1 | rw0t rb0 rw1 rb1
+ *   dims     {O, D, K, A, n_steps, value_hidden, obs_hidden, reward_hidden,
+ *             grid_h, grid_w, snap}
+ *   uniforms f64[n, H+1, K] (request r of episode e uses uniforms[e, r]) or
+ *            NULL for a Philox stream keyed by (seed, e)
+ *   outputs  obs f64[n, H+1, O], steps i32[n, H+1], tokens i32[n, H, K],
+ *            logits f64[n, H, K, A], values f64[n, H], rewards f64[n, H],
+ *            boot f64[n], len i32[n], done u8[n], status i32[n]
+ *            (0 ok, 1 non-finite obs prediction, 2 non-finite reward). */
+int accel_imagine(const void* const* weights, const int* dims, int H, double threshold,
+                  unsigned long long seed, const double* start_obs, const int32_t* start_step,
+                  const double* uniforms, int64_t n, double* obs_out, int32_t* steps_out,
+                  int32_t* tokens_out, double* logits_out, double* values_out,
+                  double* rewards_out, double* boot_out, int32_t* len_out, uint8_t* done_out,
+                  int32_t* status_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

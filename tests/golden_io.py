@@ -69,3 +69,32 @@ class Golden:
 
     def batch_meta(self, step: int) -> dict:
         return self.meta["batch_meta"][step]
+
+
+IMAGINE_CASES = ("imagine_small", "imagine_default_dims", "imagine_done_hat", "imagine_nan_obs")
+
+
+class ImagineGolden:
+    def __init__(self, name: str) -> None:
+        self.name = name
+        self.z = dict(np.load(GOLDEN / f"{name}.npz"))
+        self.meta = json.loads((GOLDEN / f"{name}.json").read_text())
+
+    def params(self, which: str) -> dict:
+        pre = which + "."
+        return {k[len(pre):]: v for k, v in self.z.items() if k.startswith(pre)}
+
+    @property
+    def episodes(self) -> list:
+        return self.meta["episodes"]
+
+    def start(self, e: int):
+        ep = self.episodes[e]
+        return self.z[f"e{e}.start_vec"], ep["start_step"], ep["task_id"]
+
+    def uniforms(self, e: int):
+        return self.z[f"e{e}.uniforms"]
+
+    def traj(self, e: int) -> dict:
+        pre = f"e{e}."
+        return {k[len(pre):]: v for k, v in self.z.items() if k.startswith(pre)}
