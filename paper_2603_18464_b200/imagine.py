@@ -62,12 +62,24 @@ class Imaginer:
         self.version = version
 
     def imagine(self, start_vecs, start_steps, h_img: int, uniforms=None, seed: int = 0) -> dict:
-        """Device-side batch; returns host numpy arrays keyed like the kernel outputs."""
-        x = torch.as_tensor(np.asarray(start_vecs, dtype=np.float64), device=self.device)
+        """One batch; returns host numpy arrays keyed like the kernel outputs."""
+        out = self.imagine_device(start_vecs, start_steps, h_img, uniforms, seed)
+        return {k: v.cpu().numpy() for k, v in out.items()}
+
+    def imagine_device(self, start_vecs, start_steps, h_img: int, uniforms=None,
+                       seed: int = 0) -> dict:
+        """Launch on the current stream; returns the device output tensors."""
+        if isinstance(start_vecs, torch.Tensor):
+            x = start_vecs.to(self.device, torch.float64).contiguous()
+        else:
+            x = torch.as_tensor(np.asarray(start_vecs, dtype=np.float64), device=self.device)
         n = x.shape[0]
         if x.shape != (n, self.O):
             raise DimensionError(f"start observations {tuple(x.shape)} != (n, {self.O})")
-        st = torch.as_tensor(np.asarray(start_steps, dtype=np.int32), device=self.device)
+        if isinstance(start_steps, torch.Tensor):
+            st = start_steps.to(self.device, torch.int32).contiguous()
+        else:
+            st = torch.as_tensor(np.asarray(start_steps, dtype=np.int32), device=self.device)
         u = None
         if uniforms is not None:
             u = torch.as_tensor(np.asarray(uniforms, dtype=np.float64), device=self.device)
@@ -97,7 +109,7 @@ class Imaginer:
                   P(out["tokens"]), P(out["behavior_logits"]), P(out["values"]),
                   P(out["rewards"]), P(out["bootstrap_value"]), P(out["t_len"]), P(out["done"]),
                   P(out["status"]), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
-        return {k: v.cpu().numpy() for k, v in out.items()}
+        return out
 
     def imagine_trajectories(self, starts, h_img: int, uniforms=None, seed: int = 0) -> list:
         """starts: objects with .vec, .step, .task_id (env.Observation)."""
