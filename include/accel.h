@@ -249,6 +249,17 @@ int accel_adam(const float* p_in, const float* g, const float* m_in, const float
                const double* group0, const double* group1, const int* skip,
                unsigned* bad, void* stream);
 
+/* ---- tensor-core GEMM (tcgen05, 3xTF32: fp32-accurate) ----------------- */
+
+size_t accel_tc_gemm_smem(int N);
+/* C[M, N] = act(A . B^T + bias) (+ C if accumulate), fp32 in/out, N <= 256.
+ * a_trans: A stored [K, M] (lda = M stride); b_trans: B stored [K, N].
+ * kslices > 1 (split-K): C receives [kslices][M][N] partial products for a
+ * fixed-order reduction by the caller (no bias/act/accumulate). */
+int accel_tc_gemm(const float* A, const float* B, float* C, const float* bias, int64_t M,
+                  int64_t K, int N, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
+                  int b_trans, int act_tanh, int accumulate, int kslices, void* stream);
+
 /* ---- (c) world-model imagination (rollout.py:295-362) ------------------ */
 
 /* Shared memory per 4-trajectory CTA (float64 activations). */

@@ -309,3 +309,47 @@ def adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, group0, group1, skip, bad
     h1 = (ctypes.c_double * 6)(*[float(x) for x in group1])
     _lib.call("accel_adam", _p(p_in), _p(g), _p(m_in), _p(v_in), _p(p_out), _p(m_out), _p(v_out),
               n, int(n0), h0, h1, _p(skip), _p(bad), _stream())
+
+
+# ---------------------------------------------------------------------------
+# tensor-core GEMM (tcgen05, 3xTF32)
+
+
+def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
+    """out[M, N] = act(x[M, K] . w[N, K]^T + bias) (+ out): y = x W^T as in models.py."""
+    M, K = x.shape
+    N = w.shape[0]
+    out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
+    _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
+              w.stride(0), out.stride(0), 0, 0, int(tanh), int(accumulate), 1, _stream())
+    return out
+
+
+def tc_matmul_nn(x, w, out=None, accumulate=False):
+    """out[M, N] = x[M, K] . w[K, N] (w row-major, i.e. B given transposed)."""
+    M, K = x.shape
+    N = w.shape[1]
+    out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
+    _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), None, M, K, N, x.stride(0), w.stride(0),
+              out.stride(0), 0, 1, 0, int(accumulate), 1, _stream())
+    return out
+
+
+def tc_wgrad(dy, x, out, kslices=None, partial=None):
+    """out[n, k] = dy[F, n]^T . x[F, k] (reduction over the F rows), split-K over
+    `kslices` CTAs per output tile and reduced in fixed order (deterministic)."""
+    F, n = dy.shape
+    k = x.shape[1]
+    if n > 256:
+        raise DimensionError("tc_wgrad: n > 256")
+    if kslices is None:
+        kslices = max(1, min(64, F // 8192))
+    if kslices == 1:
+        _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(out), None, n, F, k, dy.stride(0),
+                  x.stride(0), out.stride(0), 1, 1, 0, 0, 1, _stream())
+        return out
+    partial = torch.empty(kslices, n, k, dtype=F32, device=dy.device) if partial is None else partial
+    _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
+              x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
+    reduce_segments([(partial, out, kslices, n * k, n * k)])
+    return out

@@ -1,0 +1,55 @@
+"""tcgen05 3xTF32 GEMM vs a float64 torch reference (fp32-level accuracy)."""
+
+from __future__ import annotations
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(x, ref):
+    return float((x.double() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 8, 16), (300, 64, 256), (1000, 195, 64), (4097, 64, 64),
+                                   (513, 64, 32), (128, 256, 64), (777, 96, 195)])
+def test_tc_linear_matches_fp64(M, K, N):
+    from paper_2603_18464_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + K + N)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    w = torch.randn(N, K, device="cuda", generator=g)
+    b = torch.randn(N, device="cuda", generator=g)
+    ref = x.double() @ w.double().t()
+    y = ops.tc_linear(x, w)
+    assert rel_err(y, ref) < 2e-6
+    yb = ops.tc_linear(x, w, bias=b, tanh=True)
+    assert rel_err(yb, torch.tanh(ref + b.double())) < 2e-6
+    acc = torch.randn(M, N, device="cuda", generator=g)
+    ya = ops.tc_linear(x, w, out=acc.clone(), accumulate=True)
+    assert rel_err(ya, ref + acc.double()) < 2e-6
+
+
+@pytest.mark.parametrize("M,K,N", [(1000, 256, 64), (4096, 32, 256)])
+def test_tc_matmul_nn(M, K, N):
+    from paper_2603_18464_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    w = torch.randn(K, N, device="cuda", generator=g)
+    assert rel_err(ops.tc_matmul_nn(x, w), x.double() @ w.double()) < 2e-6
+
+
+@pytest.mark.parametrize("F,n,k,slices", [(5000, 64, 64, 1), (100000, 256, 64, 8),
+                                          (70000, 64, 195, 4), (3000, 32, 64, None)])
+def test_tc_wgrad_matches_fp64(F, n, k, slices):
+    from paper_2603_18464_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(F)
+    dy = torch.randn(F, n, device="cuda", generator=g)
+    x = torch.randn(F, k, device="cuda", generator=g)
+    out = torch.empty(n, k, device="cuda")
+    ops.tc_wgrad(dy, x, out, kslices=slices)
+    ref = dy.double().t() @ x.double()
+    assert rel_err(out, ref) < 5e-6
+    out2 = torch.empty_like(out)
+    ops.tc_wgrad(dy, x, out2, kslices=slices)
+    assert torch.equal(out, out2)  # deterministic
