@@ -62,8 +62,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// x = hi + lo exactly; hi is x rounded to nearest TF32 (the tensor core reads
+// only its top 19 bits), lo the (fp32-exact) remainder
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
   lo = x - hi;
 }
 

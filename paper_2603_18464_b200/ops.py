@@ -343,7 +343,9 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     if n > 256:
         raise DimensionError("tc_wgrad: n > 256")
     if kslices is None:
-        kslices = max(1, min(64, F // 8192))
+        # short K slices: the tensor core's fp32 accumulation error grows with
+        # the reduction length, the fixed-order fp64 slice reduction does not
+        kslices = max(1, min(8192, -(-F // 512)))
     if kslices == 1:
         _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(out), None, n, F, k, dy.stride(0),
                   x.stride(0), out.stride(0), 1, 1, 0, 0, 1, _stream())
