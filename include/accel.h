@@ -251,11 +251,18 @@ int accel_adam(const float* p_in, const float* g, const float* m_in, const float
 
 /* ---- tensor-core GEMM (tcgen05, 3xTF32: fp32-accurate) ----------------- */
 
-size_t accel_tc_gemm_smem(int N);
-/* C[M, N] = act(A . B^T + bias) (+ C if accumulate), fp32 in/out, N <= 256.
- * a_trans: A stored [K, M] (lda = M stride); b_trans: B stored [K, N].
- * kslices > 1 (split-K): C receives [kslices][M][N] partial products for a
- * fixed-order reduction by the caller (no bias/act/accumulate). */
+/* Streaming multiprocessors on the current device (persistent-grid size;
+ * the weight-gradient mode takes kslices <= this). */
+int accel_tc_sm_count(void);
+/* Dense products of the policy/value heads (models.py:176-204, :283-314).
+ *   a_trans = 0 (row transform): C[M, N] = act(A[M, K] . B^T + bias) (+ C if
+ *     accumulate); B stored [N, K] (b_trans = 0) or [K, N] (b_trans = 1);
+ *     kslices must be 1.  Persistent; B stays resident in shared memory.
+ *   a_trans = b_trans = 1 (weight gradient, reduction over the K rows):
+ *     A stored [K, M], B stored [K, N], M <= 256; C receives [2 * kslices][M][N]
+ *     fp32 partials (two per persistent CTA, kslices <= accel_tc_sm_count())
+ *     for a fixed-order reduction by the caller; no bias/act/accumulate.
+ * fp32 in/out, N <= 256, any strides. */
 int accel_tc_gemm(const float* A, const float* B, float* C, const float* bias, int64_t M,
                   int64_t K, int N, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
                   int b_trans, int act_tanh, int accumulate, int kslices, void* stream);

@@ -1,69 +1,200 @@
-// fp32-accurate tensor-core GEMM for the trainer's tall-skinny products (tcgen05, 3xTF32).
-//
-//   C[M, N] (+)= A[M, K] . B[N, K]^T  (+ bias[N], tanh)       "row transform"
+// fp32-accurate tensor-core GEMMs for the trainer's tall-skinny products (tcgen05, 3xTF32).
 //
 // The policy/value heads' dense products (models.py:176-182 forward, :191-204
-// backward; value head :283-314) are GEMMs with one huge dimension (frames,
-// ~1.6 M at the bench size) and the others <= 256.  The 1e-4 gradient
-// tolerance rules out plain TF32 (10-bit mantissa), so each fp32 operand is
-// split in shared memory into a TF32 head (low 13 mantissa bits cleared) and
-// an fp32 tail, and every k-step issues three tcgen05.mma.kind::tf32:
-// A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (the dropped A_lo.B_lo term is ~2^-22
-// relative), accumulating in TMEM (fp32).
+// backward; value head :283-314) have one huge dimension (frame rows, ~1.6 M
+// at the bench size) and the others <= 256, so they are HBM-bound: the job is
+// to stream the big operand once at full bandwidth while the tensor cores do
+// the (small) math.  The 1e-4 gradient tolerance rules out plain TF32, so each
+// fp32 operand x is used as x_hi + x_lo and every k-step accumulates
+// x_hi.y_hi + x_hi.y_lo + x_lo.y_hi in TMEM (the dropped lo.lo term is
+// ~2^-21 relative).  The tensor core reads only the top 19 bits of an fp32
+// word, so the raw fp32 tile that TMA lands in shared memory IS the hi
+// operand (truncated); converter warps only compute lo = x - trunc19(x).
 //
-// Structure (one 128-row M tile per CTA, 128 threads):
-//   * all threads stage the next K block (32 fp32) of A and B from global
-//     memory (coalesced float4 loads; A may be given transposed, i.e. with M
-//     contiguous, for the weight-gradient products) and write the hi/lo
-//     halves straight into the canonical no-swizzle K-major UMMA layout
-//     (8-row x 16-byte core matrices, LBO = 128 B, SBO = BK*32 B);
-//   * thread 0 issues the MMAs and commits them to an mbarrier; the next
-//     block's loads are issued before waiting on it, so global loads overlap
-//     the tensor-core work; two CTAs per SM overlap further;
-//   * epilogue: tcgen05.ld 32x32b rows -> bias / tanh -> global stores.
-// Split-K (`kslices` > 1) writes per-slice partial tiles that the caller
-// reduces in fixed order (deterministic), for the reduction-over-frames
-// products dW = dY^T X.
+// Two persistent, warp-specialised kernels (one CTA per SM, 320 threads):
+//
+//   tc_rows    Y[M, N] = act(X[M, K] . W^T + bias) (+ Y)       "row transform"
+//              W ([N, K] or [K, N]) is split (round-to-nearest hi, lo) once per
+//              CTA and stays resident in shared memory as [W_hi; W_lo] (2N
+//              rows, K-major, no swizzle), so one MMA with N' = 2N computes
+//              X_hi.W_hi and X_hi.W_lo side by side in TMEM and a second one
+//              adds X_lo.W_hi; the epilogue sums the two halves.  X streams
+//              through TMA (128 rows x 32 fp32, SWIZZLE_128B, K-major).
+//   tc_wgrad   C[Mc, Nc] = sum_f P[f, :Mc]^T Q[f, :Nc]          "weight gradient"
+//              the reduction runs over the frame rows; both operands stream
+//              through TMA as MN-major SWIZZLE_128B_ATOM_32B slabs (32 columns
+//              x SR rows), again with [Q_hi | Q_lo] concatenated along N.  Each
+//              CTA accumulates its share of row blocks in TMEM and flushes to a
+//              per-CTA fp32 partial every 512 rows (bounds the fp32
+//              accumulation error); the caller reduces the partials in fixed
+//              order: deterministic.
+//
+// Roles: warp 0 lane 0 issues TMA loads into a stage ring; warps 2-5 compute
+// the lo halves; warp 1 lane 0 issues the MMAs and commits them to mbarriers;
+// warps 6-9 drain the double-buffered TMEM accumulators (tcgen05.ld) while the
+// next tile is being multiplied.  TMA bulk loads do not allocate in L1, so the
+// bytes in flight are bounded by the stage ring, not by the ~23 KB of L1 left
+// beside 229 KB of shared memory (the limit a register-staged loader hits).
+#include <cuda.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace accel {
 namespace {
 
-constexpr int BM = 128;      // rows per CTA (UMMA M)
-constexpr int BK = 32;       // fp32 elements per K block (4 UMMA k-steps of 8)
-constexpr int kTC = 128;     // threads per CTA
+constexpr int BM = 128;                    // UMMA M: rows per tile / accumulator
+constexpr int BK = 32;                     // row kernel: fp32 K elements per stage
+constexpr int kThreads = 320;              // 10 warps
+constexpr int kConvWarp0 = 2, kConvWarps = 4, kConv = kConvWarps * 32;
+constexpr int kEpiWarp0 = 6, kEpiWarps = 4;
+constexpr int kMaxRaw = 12;                // raw (TMA) ring slots
+constexpr int kNL = 2;                     // lo ring slots
+constexpr size_t kSmemBudget = 225 * 1024;
+constexpr uint32_t kTile = BM * BK * 4;    // one 128 x 32 fp32 tile (16 KB)
+constexpr int kFlushRows = 512;            // wgrad: TMEM flush period (rows)
 
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// ---- PTX helpers ------------------------------------------------------------
+
+// shared-memory matrix descriptor; layout 0 = SWIZZLE_NONE, 1 = 128B_BASE32B, 2 = 128B
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                               uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
-  return d;                // base offset 0, lbo mode 0, SWIZZLE_NONE
+  d |= (uint64_t)layout << 61;
+  return d;  // base offset 0: swizzle atoms are aligned to their period
 }
 
-// kind::tf32, D fp32, A/B tf32 K-major, M = 128, N = n
-__device__ __forceinline__ uint32_t make_idesc(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// kind::tf32, D fp32, M = 128, N = n; a_mn / b_mn: operand is MN-major
+__device__ __forceinline__ uint32_t make_idesc(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
+// warp-wide issue: every lane executes (uniform control flow, operands in
+// uniform registers), one elected lane issues the MMA / commit
+__device__ __forceinline__ void mma_tf32_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
                : "memory");
 }
 
-// x = hi + lo exactly; hi is x rounded to nearest TF32 (the tensor core reads
-// only its top 19 bits), lo the (fp32-exact) remainder
+// lo = x - trunc19(x): the part of x the tensor core drops when it reads x as TF32
+__device__ __forceinline__ float4 tf32_lo(float4 v) {
+  float4 l;
+  l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  return l;
+}
+
+// x = hi + lo exactly, hi = x rounded to nearest TF32 (resident weights)
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   uint32_t h;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
@@ -71,178 +202,675 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-// byte offset of element (r, k) in a canonical K-major no-swizzle tile of BK columns
-__device__ __forceinline__ uint32_t canon_off(int r, int k) {
+// tanh via one ex2 and one fast divide: |error| ~1e-7 (the products' own error is ~1e-6)
+__device__ __forceinline__ float fast_tanh(float x) {
+  const float t = __expf(2.f * x);
+  return 1.f - __fdividef(2.f, t + 1.f);
+}
+
+// byte offset of element (r, k) in a K-major no-swizzle tile of BK columns
+__device__ __forceinline__ uint32_t canon_k(int r, int k) {
   return (uint32_t)((r >> 3) * (BK * 32) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
 
-struct TcArgs {
-  const float* A;  // [M, K] row-major (a_trans == 0) or [K, M] (a_trans == 1)
-  const float* B;  // [N, K] row-major (b_trans == 0) or [K, N] (b_trans == 1)
-  float* C;        // [M, N] (ldc), or partials [kslices][M][N] when kslices > 1
-  const float* bias;
-  int64_t M, K;
-  int N, Npad;     // Npad: N rounded up to 16 (UMMA N), TMEM columns = pow2 >= Npad
-  int64_t lda, ldb, ldc;
-  int a_trans, b_trans, act_tanh, accumulate, kslices;
-  int tmem_cols;
-};
-
-// stage rows [r0, r0 + R) x K block [k0, k0 + BK) of X into hi/lo canonical tiles
-__device__ __forceinline__ void stage(const float* __restrict__ X, int64_t ld, int trans,
-                                      int64_t rows_total, int64_t k_total, int64_t r0, int R,
-                                      int64_t k0, unsigned char* hi, unsigned char* lo) {
-  if (!trans) {
-    // R rows x 8 float4 per row
-    for (int idx = threadIdx.x; idx < R * (BK / 4); idx += kTC) {
-      const int r = idx / (BK / 4), c4 = (idx % (BK / 4)) * 4;
-      const int64_t gr = r0 + r, gk = k0 + c4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < rows_total) {
-        const float* src = X + gr * ld + gk;
-        if (gk + 3 < k_total && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-          v = __ldg(reinterpret_cast<const float4*>(src));
-        } else {
-          v.x = gk < k_total ? __ldg(src) : 0.f;
-          v.y = gk + 1 < k_total ? __ldg(src + 1) : 0.f;
-          v.z = gk + 2 < k_total ? __ldg(src + 2) : 0.f;
-          v.w = gk + 3 < k_total ? __ldg(src + 3) : 0.f;
-        }
-      }
-      float4 h, l;
-      split_tf32(v.x, h.x, l.x);
-      split_tf32(v.y, h.y, l.y);
-      split_tf32(v.z, h.z, l.z);
-      split_tf32(v.w, h.w, l.w);
-      const uint32_t off = canon_off(r, c4);
-      *reinterpret_cast<float4*>(hi + off) = h;
-      *reinterpret_cast<float4*>(lo + off) = l;
-    }
-  } else {
-    // X[k][r] with r contiguous: threads walk r (coalesced), scatter 4 k's? no: one element
-    for (int idx = threadIdx.x; idx < R * BK; idx += kTC) {
-      const int k = idx / R, r = idx % R;
-      const int64_t gr = r0 + r, gk = k0 + k;
-      const float v = (gr < rows_total && gk < k_total) ? __ldg(X + gk * ld + gr) : 0.f;
-      float h, l;
-      split_tf32(v, h, l);
-      const uint32_t off = canon_off(r, k);
-      *reinterpret_cast<float*>(hi + off) = h;
-      *reinterpret_cast<float*>(lo + off) = l;
-    }
-  }
+// converters: lo[i] = tf32_lo(raw[i]) over `bytes` (multiple of 16) of a stage
+__device__ __forceinline__ void convert_lo(const unsigned char* raw, unsigned char* lo,
+                                           uint32_t bytes, int t) {
+  for (uint32_t i = (uint32_t)t * 16; i < bytes; i += kConv * 16)
+    *reinterpret_cast<float4*>(lo + i) = tf32_lo(*reinterpret_cast<const float4*>(raw + i));
 }
 
-__global__ void __launch_bounds__(kTC)
-tc_gemm_kernel(TcArgs p) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  const int Npad = p.Npad;
-  const uint32_t a_bytes = BM * BK * 4, b_bytes = (uint32_t)Npad * BK * 4;
-  unsigned char* a_hi = smem;
-  unsigned char* a_lo = a_hi + a_bytes;
-  unsigned char* b_hi = a_lo + a_bytes;
-  unsigned char* b_lo = b_hi + b_bytes;
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t tmem_base;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Pipeline state of one ring: slot index and mbarrier phase of the current stage.
+struct Ring {
+  int slot = 0, n;
+  unsigned ph = 0;
+  __device__ explicit Ring(int n_) : n(n_) {}
+  __device__ void next() {
+    if (++slot == n) {
+      slot = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int slice = blockIdx.y;
-  const int64_t kb_total = ceil_div(p.K, (int64_t)BK);
-  const int64_t kb_per = ceil_div(kb_total, (int64_t)p.kslices);
-  const int64_t kb_begin = slice * kb_per, kb_end = min(kb_total, kb_begin + kb_per);
+// Barriers: raw ring (TMA -> converters, MMA), lo ring (converters -> MMA),
+// double-buffered TMEM accumulators (MMA -> epilogue).
+struct Bars {
+  uint64_t raw_full[kMaxRaw], raw_empty[kMaxRaw], lo_full[kNL], lo_empty[kNL], tfull[2], tempty[2];
+};
+
+__device__ __forceinline__ void init_bars(Bars& b, int nraw) {
+  for (int s = 0; s < nraw; ++s) {
+    mbar_init(&b.raw_full[s], 1);
+    mbar_init(&b.raw_empty[s], 1);
+  }
+  for (int s = 0; s < kNL; ++s) {
+    mbar_init(&b.lo_full[s], kConv);
+    mbar_init(&b.lo_empty[s], 1);
+  }
+  for (int s = 0; s < 2; ++s) {
+    mbar_init(&b.tfull[s], 1);
+    mbar_init(&b.tempty[s], kEpiWarps);
+  }
+  fence_mbar_init();
+}
+
+// ============================================================================
+// row transform
+
+struct RowArgs {
+  const float* W;
+  float* Y;
+  const float* bias;
+  int64_t M, ntiles, ldw, ldy;
+  int K, N, Npad, kblocks, last_ksteps, concat;
+  int w_trans, act_tanh, accumulate, y_vec, nraw, tma_store, nstg, has_bias;
+  uint32_t tmem_cols, acc_cols;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+               RowArgs p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ Bars bars;
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(16) float s_bias[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Npad = p.Npad;
+  if (smem_u32(smem) & 1023) __trap();  // SWIZZLE_128B atoms need 1 KB alignment
+  const uint32_t wblk = (uint32_t)Npad * BK * 4 * 2;  // one K block of [W_hi; W_lo]
+  unsigned char* wres = smem;
+  unsigned char* raw_ring = smem + (size_t)p.kblocks * wblk;
+  unsigned char* lo_ring = raw_ring + (size_t)p.nraw * kTile;
+  unsigned char* staging = lo_ring + (size_t)kNL * kTile;  // epilogue: nstg boxes per warp
+
+  // W resident: split once, K-major, [hi rows | lo rows] per K block
+  const int Kpad = p.kblocks * BK;
+  for (int idx = threadIdx.x; idx < Npad * Kpad; idx += kThreads) {
+    const int n = idx / Kpad, k = idx - n * Kpad;
+    float v = 0.f;
+    if (n < p.N && k < p.K)
+      v = p.w_trans ? __ldg(p.W + (int64_t)k * p.ldw + n) : __ldg(p.W + (int64_t)n * p.ldw + k);
+    float h, l;
+    split_tf32(v, h, l);
+    unsigned char* blk = wres + (size_t)(k / BK) * wblk;
+    *reinterpret_cast<float*>(blk + canon_k(n, k % BK)) = h;
+    *reinterpret_cast<float*>(blk + canon_k(Npad + n, k % BK)) = l;
+  }
+  for (int c = threadIdx.x; c < 256; c += kThreads)
+    s_bias[c] = (p.bias && c < p.N) ? __ldg(p.bias + c) : 0.f;
+  if (warp == 1) tmem_alloc(&tmem_base, p.tmem_cols);
+  if (threadIdx.x == 0) {
+    init_bars(bars, p.nraw);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int64_t my_tiles =
+      p.ntiles > (int64_t)blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_tiles * p.kblocks;
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base)),
-                 "r"(p.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_base;
-  const uint32_t idesc = make_idesc(Npad);
-  const uint32_t sa_hi = smem_u32(a_hi), sa_lo = smem_u32(a_lo);
-  const uint32_t sb_hi = smem_u32(b_hi), sb_lo = smem_u32(b_lo);
-  const uint32_t SBO = BK * 32, LBO = 128;
-
-  unsigned phase = 0;
-  bool any = false;
-  for (int64_t kb = kb_begin; kb < kb_end; ++kb) {
-    if (any) {  // the previous block's MMAs must finish reading smem
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
-    }
-    stage(p.A, p.lda, p.a_trans, p.M, p.K, m0, BM, kb * BK, a_hi, a_lo);
-    stage(p.B, p.ldb, p.b_trans, p.N, p.K, 0, Npad, kb * BK, b_hi, b_lo);
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int s = 0; s < BK / 8; ++s) {
-        const uint32_t koff = s * 2 * 128;
-        const uint64_t ah = make_sdesc(sa_hi + koff, LBO, SBO), al = make_sdesc(sa_lo + koff, LBO, SBO);
-        const uint64_t bh = make_sdesc(sb_hi + koff, LBO, SBO), bl = make_sdesc(sb_lo + koff, LBO, SBO);
-        const uint32_t acc0 = (kb > kb_begin || s > 0) ? 1u : 0u;
-        mma_tf32(tmem, ah, bh, idesc, acc0);
-        mma_tf32(tmem, ah, bl, idesc, 1u);
-        mma_tf32(tmem, al, bh, idesc, 1u);
-      }
-      mma_commit(&bar);
-    }
-    __syncwarp();
-    any = true;
-  }
-  if (any) mbar_wait(&bar, phase);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-  // epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
-  const int64_t row = m0 + warp * 32 + lane;
-  float* out = p.kslices > 1 ? p.C + ((int64_t)slice * p.M + row) * p.N : p.C + row * p.ldc;
-  for (int c0 = 0; c0 < Npad; c0 += 16) {
-    uint32_t r[16];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < p.M && any) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int c = c0 + j;
-        if (c < p.N) {
-          float v = __uint_as_float(r[j]);
-          if (p.kslices == 1) {
-            if (p.bias) v += __ldg(p.bias + c);
-            if (p.act_tanh) v = tanhf(v);
-            if (p.accumulate) v += out[c];
-          }
-          out[c] = v;
+    if (lane == 0) {  // ---- TMA producer
+      Ring r(p.nraw);
+      int64_t tile = blockIdx.x;
+      int kb = 0;
+      for (int64_t s = 0; s < total; ++s, r.next()) {
+        mbar_wait(&bars.raw_empty[r.slot], r.ph ^ 1u);
+        mbar_expect_tx(&bars.raw_full[r.slot], kTile);
+        tma_load_2d(raw_ring + (size_t)r.slot * kTile, &xmap, kb * BK, (int)(tile * BM),
+                    &bars.raw_full[r.slot]);
+        if (++kb == p.kblocks) {
+          kb = 0;
+          tile += gridDim.x;
         }
       }
-    } else if (row < p.M && !any) {
-      for (int j = 0; j < 16; ++j) {
-        const int c = c0 + j;
-        if (c < p.N) out[c] = 0.f;
+    }
+  } else if (warp == 1) {
+    {  // ---- MMA issuer (warp-wide loop, one elected lane issues)
+      const int n1 = p.concat ? 2 * Npad : Npad;
+      const uint32_t id1 = make_idesc(n1, 0, 0), id2 = make_idesc(Npad, 0, 0);
+      Ring r(p.nraw), l(kNL);
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int b = (int)(t & 1);
+        mbar_wait(&bars.tempty[b], ((unsigned)(t >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)b * p.acc_cols;
+        for (int kb = 0; kb < p.kblocks; ++kb, r.next(), l.next()) {
+          mbar_wait(&bars.raw_full[r.slot], r.ph);
+          mbar_wait(&bars.lo_full[l.slot], l.ph);
+          tc_fence_after();
+          const uint32_t a_raw = smem_u32(raw_ring + (size_t)r.slot * kTile);
+          const uint32_t a_lo = smem_u32(lo_ring + (size_t)l.slot * kTile);
+          const uint32_t wb = smem_u32(wres + (size_t)kb * wblk);
+          const int nsteps = kb == p.kblocks - 1 ? p.last_ksteps : BK / 8;
+          for (int s = 0; s < nsteps; ++s) {
+            const uint64_t ar = make_sdesc(a_raw + s * 32, 16, 1024, 2);
+            const uint64_t al = make_sdesc(a_lo + s * 32, 16, 1024, 2);
+            const uint64_t wh = make_sdesc(wb + s * 256, 128, 1024, 0);
+            const uint32_t acc = (kb > 0 || s > 0) ? 1u : 0u;
+            if (p.concat) {
+              mma_tf32_w(d, ar, wh, id1, acc);  // [X.W_hi | X.W_lo]
+            } else {
+              const uint64_t wl = make_sdesc(wb + (uint32_t)Npad * 128 + s * 256, 128, 1024, 0);
+              mma_tf32_w(d, ar, wh, id2, acc);
+              mma_tf32_w(d, ar, wl, id2, 1u);
+            }
+            mma_tf32_w(d, al, wh, id2, 1u);  // + X_lo.W_hi
+          }
+          mma_commit_w(&bars.raw_empty[r.slot]);
+          mma_commit_w(&bars.lo_empty[l.slot]);
+        }
+        mma_commit_w(&bars.tfull[b]);
+      }
+    }
+  } else if (warp < kEpiWarp0) {
+    // ---- converters
+    const int t = threadIdx.x - kConvWarp0 * 32;
+    Ring r(p.nraw), l(kNL);
+    for (int64_t s = 0; s < total; ++s, r.next(), l.next()) {
+      mbar_wait(&bars.raw_full[r.slot], r.ph);
+      mbar_wait(&bars.lo_empty[l.slot], l.ph ^ 1u);
+      convert_lo(raw_ring + (size_t)r.slot * kTile, lo_ring + (size_t)l.slot * kTile, kTile, t);
+      fence_proxy_async();
+      mbar_arrive(&bars.lo_full[l.slot]);
+    }
+  } else {
+    // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows, 32
+    // columns at a time; rows go out through a swizzled staging box + TMA store
+    const int q = warp & 3;
+    unsigned char* stg0 = staging + (size_t)(warp - kEpiWarp0) * p.nstg * 4096;
+    int sb = 0;
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int b = (int)(t & 1);
+      mbar_wait(&bars.tfull[b], (unsigned)(t >> 1) & 1u);
+      tc_fence_after();
+      const int64_t row0 = (blockIdx.x + t * gridDim.x) * BM + q * 32;
+      const int64_t row = row0 + lane;
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)b * p.acc_cols;
+      for (int c0 = 0; c0 < Npad; c0 += 32) {
+        uint32_t r[32];
+        float v[32];
+        tmem_ld32(tb + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (p.concat) {
+          tmem_ld32(tb + Npad + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+        }
+        if (p.has_bias) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(&s_bias[c0 + j]);
+            v[j] += bb.x;
+            v[j + 1] += bb.y;
+            v[j + 2] += bb.z;
+            v[j + 3] += bb.w;
+          }
+        }
+        if (p.act_tanh) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fast_tanh(v[j]);
+        }
+        if (p.tma_store) {
+          unsigned char* stg = stg0 + sb * 4096;
+          if (lane == 0) tma_store_wait_read();  // this box's previous store has read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&ymap, c0, (int)row0, stg);
+          if (++sb == p.nstg) sb = 0;
+        } else if (row < p.M) {
+          float* out = p.Y + row * p.ldy;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < p.N) out[c0 + j] = p.accumulate ? out[c0 + j] + v[j] : v[j];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.tempty[b]);
+    }
+    if (p.tma_store && lane == 0) tma_store_wait_all();
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// ============================================================================
+// weight gradient (reduction over rows), MN-major operands
+
+struct WgArgs {
+  float* C;  // partials [2 * gridDim.x][Mc][Nc] (or [..][Nc][Mc] when out_t)
+  int64_t F, nblocks;
+  int Mc, Nc, Mt, MSl, NSl, SR, Npad, concat, stacked, out_t, nraw, nbuf, flush_blocks, sum_col;
+  int p_full, q_full;  // slabs loaded by the 3-D maps (the rest: one 2-D box each)
+  uint32_t tmem_cols, acc_cols;
+};
+
+// Two operand arrangements (one 32-column slab = SR rows x 128 B, MN-major):
+//  * stacked (Mc <= 64): raw slot [P raw (2 slabs) | P lo (2) | Q raw (NSl) | Q lo (NSl)];
+//    the M = 128 A operand is [P_raw ; P_lo] and B is [Q_raw | Q_lo], so ONE
+//    MMA per k-step yields all four products (incl. the tiny lo.lo); accumulator
+//    rows 64.. hold the P_lo products and go to the CTA's second partial slice.
+//  * split (Mc > 64, Mt <= 2 M tiles): raw slot [P raw (MSl) | Q raw | Q lo], lo ring
+//    slot [P lo (MSl)]; per M tile and k-step P_raw.[Q_raw | Q_lo] + P_lo.Q_raw.
+//    An M tile's MMA reads 4 slabs from its start: rows past Mc come from the
+//    following regions (or the tail pad) and only feed rows that are never stored.
+__global__ void __launch_bounds__(kThreads, 1)
+tc_wgrad_kernel(const __grid_constant__ CUtensorMap pmap3, const __grid_constant__ CUtensorMap qmap3,
+                const __grid_constant__ CUtensorMap pmap, const __grid_constant__ CUtensorMap qmap,
+                WgArgs p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ Bars bars;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Mt = p.Mt;
+  if (smem_u32(smem) & 1023) __trap();
+  const uint32_t slab = (uint32_t)p.SR * 128;
+  const uint32_t a_bytes = (uint32_t)(p.stacked ? 4 : p.MSl) * slab;  // A region in the raw slot
+  const uint32_t b_bytes = (uint32_t)p.NSl * slab;
+  const uint32_t lo_bytes = p.stacked ? 0u : (uint32_t)p.MSl * slab;  // lo ring slot
+  const uint32_t raw_bytes = a_bytes + 2 * b_bytes;
+  unsigned char* raw_ring = smem;
+  unsigned char* lo_ring = smem + (size_t)p.nraw * raw_bytes;
+
+  if (warp == 1) tmem_alloc(&tmem_base, p.tmem_cols);
+  if (threadIdx.x == 0) {
+    init_bars(bars, p.nraw);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&pmap3)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap3)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int64_t my_blocks =
+      p.nblocks > (int64_t)blockIdx.x ? (p.nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t rounds = (my_blocks + p.flush_blocks - 1) / p.flush_blocks;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      const uint32_t tx = (uint32_t)(p.MSl + p.NSl) * slab;
+      Ring r(p.nraw);
+      int64_t blk = blockIdx.x;
+      for (int64_t s = 0; s < my_blocks; ++s, blk += gridDim.x, r.next()) {
+        mbar_wait(&bars.raw_empty[r.slot], r.ph ^ 1u);
+        unsigned char* base = raw_ring + (size_t)r.slot * raw_bytes;
+        uint64_t* bar = &bars.raw_full[r.slot];
+        mbar_expect_tx(bar, tx);
+        const int r0 = (int)(blk * p.SR);
+        // full 32-column slabs: one 3-D box per operand; a partial last slab: one 2-D box
+        if (p.p_full) tma_load_3d(base, &pmap3, 0, r0, 0, bar);
+        if (p.p_full < p.MSl) tma_load_2d(base + p.p_full * slab, &pmap, p.p_full * 32, r0, bar);
+        unsigned char* bq = base + a_bytes;
+        if (p.q_full) tma_load_3d(bq, &qmap3, 0, r0, 0, bar);
+        if (p.q_full < p.NSl) tma_load_2d(bq + p.q_full * slab, &qmap, p.q_full * 32, r0, bar);
+      }
+    }
+  } else if (warp == 1) {
+    {  // ---- MMA issuer (warp-wide loop, one elected lane issues)
+      const int nq = p.NSl * 32;
+      const uint32_t id1 = make_idesc(p.concat ? 2 * nq : p.Npad, 1, 1), id2 = make_idesc(p.Npad, 1, 1);
+      Ring r(p.nraw), l(kNL);
+      int64_t blk = 0;
+      for (int64_t rd = 0; rd < rounds; ++rd) {
+        const int b = p.nbuf == 2 ? (int)(rd & 1) : 0;
+        const unsigned use = p.nbuf == 2 ? (unsigned)(rd >> 1) & 1u : (unsigned)rd & 1u;
+        mbar_wait(&bars.tempty[b], use ^ 1u);
+        tc_fence_after();
+        const int64_t blk_end = blk + p.flush_blocks < my_blocks ? blk + p.flush_blocks : my_blocks;
+        const int64_t blk0 = blk;
+        for (; blk < blk_end; ++blk, r.next(), l.next()) {
+          mbar_wait(&bars.raw_full[r.slot], r.ph);
+          mbar_wait(&bars.lo_full[l.slot], l.ph);
+          tc_fence_after();
+          const uint32_t a_raw = smem_u32(raw_ring + (size_t)r.slot * raw_bytes);
+          const uint32_t a_lo = smem_u32(lo_ring + (size_t)l.slot * lo_bytes);
+          const uint32_t b_raw = a_raw + a_bytes, b_lo = b_raw + b_bytes;
+          for (int s = 0; s < p.SR / 8; ++s) {
+            const uint32_t ko = s * 1024;  // two 4-row K atoms per k-step
+            const uint64_t br = make_sdesc(b_raw + ko, slab, 512, 1);
+            const uint32_t acc = (blk > blk0 || s > 0) ? 1u : 0u;
+            if (p.stacked) {
+              const uint32_t d = tmem + (uint32_t)(b * p.acc_cols);
+              const uint64_t ar = make_sdesc(a_raw + ko, slab, 512, 1);  // [P_raw ; P_lo]
+              if (p.concat) {
+                mma_tf32_w(d, ar, br, id1, acc);
+              } else {
+                mma_tf32_w(d, ar, br, id2, acc);
+                mma_tf32_w(d, ar, make_sdesc(b_lo + ko, slab, 512, 1), id2, 1u);
+              }
+              continue;
+            }
+            for (int t = 0; t < Mt; ++t) {
+              const uint32_t d = tmem + (uint32_t)((b * Mt + t) * p.acc_cols);
+              const uint32_t ao = (uint32_t)t * 4 * slab + ko;
+              const uint64_t ar = make_sdesc(a_raw + ao, slab, 512, 1);
+              const uint64_t al = make_sdesc(a_lo + ao, slab, 512, 1);
+              if (p.concat) {
+                mma_tf32_w(d, ar, br, id1, acc);  // [P.Q_hi | P.Q_lo]
+              } else {
+                mma_tf32_w(d, ar, br, id2, acc);
+                mma_tf32_w(d, ar, make_sdesc(b_lo + ko, slab, 512, 1), id2, 1u);
+              }
+              mma_tf32_w(d, al, br, id2, 1u);  // + P_lo.Q_hi
+            }
+          }
+          mma_commit_w(&bars.raw_empty[r.slot]);
+          mma_commit_w(&bars.lo_empty[l.slot]);
+        }
+        mma_commit_w(&bars.tfull[b]);
+      }
+    }
+  } else if (warp < kEpiWarp0) {
+    // ---- converters: lo halves (P lo into the raw slot when stacked, else the lo ring)
+    const int t = threadIdx.x - kConvWarp0 * 32;
+    Ring r(p.nraw), l(kNL);
+    for (int64_t s = 0; s < my_blocks; ++s, r.next(), l.next()) {
+      mbar_wait(&bars.raw_full[r.slot], r.ph);
+      mbar_wait(&bars.lo_empty[l.slot], l.ph ^ 1u);
+      unsigned char* base = raw_ring + (size_t)r.slot * raw_bytes;
+      if (p.stacked)
+        convert_lo(base, base + 2 * slab, 2 * slab, t);
+      else
+        convert_lo(base, lo_ring + (size_t)l.slot * lo_bytes, lo_bytes, t);
+      convert_lo(base + a_bytes, base + a_bytes + b_bytes, b_bytes, t);
+      fence_proxy_async();
+      mbar_arrive(&bars.lo_full[l.slot]);
+    }
+  } else {
+    // ---- epilogue: fold each flushed accumulator into a running fp32 sum kept
+    // in TMEM (columns sum_col..), write this CTA's partials once at the end
+    const int q = warp & 3;
+    const int nq = p.NSl * 32;
+    const int tiles = p.stacked ? 1 : Mt;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    for (int64_t rd = 0; rd < rounds; ++rd) {
+      const int b = p.nbuf == 2 ? (int)(rd & 1) : 0;
+      const unsigned use = p.nbuf == 2 ? (unsigned)(rd >> 1) & 1u : (unsigned)rd & 1u;
+      mbar_wait(&bars.tfull[b], use);
+      tc_fence_after();
+      for (int t = 0; t < tiles; ++t) {
+        const uint32_t tb = lane_base + (uint32_t)((b * tiles + t) * p.acc_cols);
+        const uint32_t sb = lane_base + p.sum_col + (uint32_t)(t * p.Npad);
+        for (int c0 = 0; c0 < p.Npad; c0 += 16) {
+          uint32_t r[16], r2[16], acc[16];
+          tmem_ld16(tb + c0, r);
+          if (p.concat) tmem_ld16(tb + nq + c0, r2);
+          if (rd > 0) tmem_ld16(sb + c0, acc);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float v = __uint_as_float(r[j]) + (p.concat ? __uint_as_float(r2[j]) : 0.f);
+            if (rd > 0) v += __uint_as_float(acc[j]);
+            acc[j] = __float_as_uint(v);
+          }
+          tmem_st16(sb + c0, acc);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.tempty[b]);
+    }
+    // this CTA's two partial slices, fixed order (deterministic): stacked rows
+    // 64.. (the P_lo products) go to the second slice, otherwise it is zero
+    const int64_t slice = (int64_t)p.Mc * p.Nc;
+    float* part = p.C + (int64_t)blockIdx.x * 2 * slice;
+    if (!p.stacked)
+      for (int i = (warp - kEpiWarp0) * 32 + lane; i < slice; i += kEpiWarps * 32) part[slice + i] = 0.f;
+    for (int t = 0; t < tiles; ++t) {
+      const int lrow = t * BM + q * 32 + lane;
+      const int m = p.stacked ? (lrow & 63) : lrow;
+      float* dstp = part + (p.stacked && lrow >= 64 ? slice : 0);
+      const uint32_t sb = lane_base + p.sum_col + (uint32_t)(t * p.Npad);
+      for (int c0 = 0; c0 < p.Npad; c0 += 16) {
+        uint32_t acc[16];
+        if (rounds > 0) {
+          tmem_ld16(sb + c0, acc);
+          tmem_wait_ld();
+        }
+        if (m < p.Mc) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = c0 + j;
+            if (c < p.Nc)
+              dstp[p.out_t ? (int64_t)c * p.Mc + m : (int64_t)m * p.Nc + c] =
+                  rounds > 0 ? __uint_as_float(acc[j]) : 0.f;
+          }
+        }
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncwarp();
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(p.tmem_cols)
-                 : "memory");
+  if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// ---- host ---------------------------------------------------------------------
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+uint32_t tmem_cols_for(int cols) {
+  uint32_t c = 32;
+  while ((int)c < cols) c <<= 1;
+  return c;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map over rows x cols (row pitch ld floats), box = box_cols x box_rows
+int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld,
+             int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(kCuda, "tc_gemm: cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld % 4) || ld < cols)
+    return fail(kDimension, "tc_gemm: streamed operand needs 16-byte aligned rows (ld %% 4 == 0)");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kCuda, "tc_gemm: tensor map encode failed (%d)", (int)r);
+  return kOk;
+}
+
+// 3-D fp32 map viewing the first `slabs` 32-column slabs of a rows x cols matrix as
+// {32 columns, rows, slabs}: one box = all slabs of `box_rows` rows, slab-major in
+// shared memory (each slab a box_rows x 128 B swizzled block)
+int make_map3(CUtensorMap* map, const float* base, int64_t rows, int slabs, int64_t ld,
+              int box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(kCuda, "tc_gemm: cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld % 4))
+    return fail(kDimension, "tc_gemm: streamed operand needs 16-byte aligned rows (ld %% 4 == 0)");
+  const cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)slabs};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+  const cuuint32_t box[3] = {32, (cuuint32_t)box_rows, (cuuint32_t)slabs};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kCuda, "tc_gemm: 3-D tensor map encode failed (%d)", (int)r);
+  return kOk;
+}
+
+int launch_rows(const float* X, const float* W, float* Y, const float* bias, int64_t M, int64_t K,
+                int N, int64_t ldx, int64_t ldw, int64_t ldy, int w_trans, int act_tanh,
+                int accumulate, cudaStream_t st) {
+  const int Npad = (N + 31) / 32 * 32;  // the epilogue drains 32 columns at a time
+  const int kblocks = (int)ceil_div(K, BK);
+  const size_t wbytes = (size_t)kblocks * Npad * BK * 4 * 2;
+  const size_t fixed = (size_t)kNL * kTile + (size_t)kEpiWarps * 4096;  // lo ring + 1 staging box
+  if (wbytes + fixed + 3 * kTile > kSmemBudget && N > 32) {
+    // resident [W_hi; W_lo] too large for a useful ring: split the output columns
+    const int n1 = (N / 2 + 31) / 32 * 32;
+    const float* W2 = w_trans ? W + n1 : W + (int64_t)n1 * ldw;
+    if (int e = launch_rows(X, W, Y, bias, M, K, n1, ldx, ldw, ldy, w_trans, act_tanh, accumulate, st))
+      return e;
+    return launch_rows(X, W2, Y + n1, bias ? bias + n1 : nullptr, M, K, N - n1, ldx, ldw, ldy,
+                       w_trans, act_tanh, accumulate, st);
+  }
+  if (wbytes + fixed + 2 * kTile > kSmemBudget)
+    return fail(kDimension, "tc_gemm: resident weight %d x %lld too large", N, (long long)K);
+  CUtensorMap xmap, ymap;
+  if (int e = make_map(&xmap, X, M, K, ldx, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B)) return e;
+  RowArgs p;
+  p.W = W; p.Y = Y; p.bias = bias;
+  p.has_bias = bias ? 1 : 0;
+  p.M = M; p.K = (int)K; p.N = N;
+  p.Npad = Npad;
+  p.concat = 2 * Npad <= 256 ? 1 : 0;
+  p.kblocks = kblocks;
+  p.last_ksteps = (int)ceil_div(K - (int64_t)(kblocks - 1) * BK, 8);
+  p.ldw = ldw; p.ldy = ldy;
+  p.w_trans = w_trans; p.act_tanh = act_tanh; p.accumulate = accumulate;
+  p.y_vec = (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0) ? 1 : 0;
+  p.tma_store = (p.y_vec && !accumulate) ? 1 : 0;
+  if (p.tma_store) {
+    if (int e = make_map(&ymap, Y, M, N, ldy, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return e;
+  } else {
+    ymap = xmap;  // unused
+  }
+  p.ntiles = ceil_div(M, BM);
+  p.acc_cols = p.concat ? 2 * Npad : Npad;
+  p.tmem_cols = tmem_cols_for(2 * (int)p.acc_cols);
+  // staging: two boxes per epilogue warp when the raw ring keeps >= 6 slots
+  p.nstg = p.tma_store ? 2 : 0;
+  if (p.tma_store && wbytes + (size_t)kNL * kTile + (size_t)kEpiWarps * 2 * 4096 + 6 * kTile > kSmemBudget)
+    p.nstg = 1;
+  const size_t sbytes = (size_t)kEpiWarps * p.nstg * 4096;
+  p.nraw = (int)std::min<size_t>(kMaxRaw, (kSmemBudget - wbytes - sbytes - kNL * kTile) / kTile);
+  const size_t smem = wbytes + (size_t)(p.nraw + kNL) * kTile + sbytes;
+  cudaError_t e = cudaFuncSetAttribute(tc_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return fail(kCuda, "tc_rows smem: %s", cudaGetErrorString(e));
+  const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
+  tc_rows_kernel<<<grid, kThreads, smem, st>>>(xmap, ymap, p);
+  return post_launch("tc_rows_kernel");
+}
+
+// C partials [2 * slices][n][k] of dY[F, n]^T X[F, k]
+int launch_wgrad(const float* dY, const float* X, float* C, int64_t F, int n, int k,
+                 int64_t ldy, int64_t ldx, int slices, cudaStream_t st) {
+  // pick orientation (which side is the UMMA M side) and arrangement by the
+  // tensor-core cycles per k-step (measured: an M = 128 MMA of N columns takes
+  // max(48, N / 2) cycles)
+  auto mma = [](int nc) { return std::max(48, nc / 2); };
+  auto plan = [&](int mc, int nc, bool stacked) -> int {
+    const int nsl = (nc + 31) / 32, npad = (nc + 15) / 16 * 16;
+    const bool concat = 2 * nsl * 32 <= 256;
+    if (stacked) return mc <= 64 ? (concat ? mma(2 * nsl * 32) : 2 * mma(npad)) : 1 << 30;
+    const int mt = (mc + BM - 1) / BM;
+    if (mt > 2 || nsl > 8) return 1 << 30;
+    return mt * (concat ? mma(2 * nsl * 32) + mma(npad) : 3 * mma(npad));
+  };
+  int best = 1 << 30;
+  bool swap = false, stacked = false;
+  for (int sw = 0; sw < 2; ++sw)
+    for (int stk = 1; stk >= 0; --stk) {
+      const int c = sw ? plan(k, n, stk) : plan(n, k, stk);
+      if (c < best) best = c, swap = sw, stacked = stk;
+    }
+  if (best == 1 << 30) return fail(kDimension, "tc_wgrad: output %d x %d too large", n, k);
+  WgArgs p;
+  const float* P = swap ? X : dY;
+  const float* Q = swap ? dY : X;
+  const int64_t ldp = swap ? ldx : ldy, ldq = swap ? ldy : ldx;
+  p.Mc = swap ? k : n;
+  p.Nc = swap ? n : k;
+  p.out_t = swap ? 1 : 0;
+  p.stacked = stacked ? 1 : 0;
+  p.C = C;
+  p.F = F;
+  p.Mt = stacked ? 1 : (p.Mc + BM - 1) / BM;
+  p.MSl = (p.Mc + 31) / 32;
+  p.NSl = (p.Nc + 31) / 32;
+  p.Npad = (p.Nc + 15) / 16 * 16;
+  p.concat = 2 * p.NSl * 32 <= 256 ? 1 : 0;
+  p.acc_cols = p.concat ? 2 * p.NSl * 32 : p.Npad;
+  // TMEM: nbuf x Mt accumulators, then Mt running sums of Npad columns
+  const int acc_total = p.Mt * (int)p.acc_cols, sum_total = p.Mt * p.Npad;
+  if (acc_total + sum_total > 512) return fail(kDimension, "tc_wgrad: accumulator exceeds TMEM");
+  p.nbuf = 2 * acc_total + sum_total <= 512 ? 2 : 1;
+  p.sum_col = p.nbuf * acc_total;
+  p.tmem_cols = tmem_cols_for(p.nbuf * acc_total + sum_total);
+  // stage rows: the largest of 64 / 32 / 16 that leaves >= 3 raw slots
+  const int a_slabs = stacked ? 4 : p.MSl, lo_slabs = stacked ? 0 : p.MSl;
+  auto raw_of = [&](int sr) { return (size_t)(a_slabs + 2 * p.NSl) * sr * 128; };
+  auto lo_of = [&](int sr) { return (size_t)lo_slabs * sr * 128; };
+  // split mode: the last lo slot's M-tile reads may run (4 * Mt - MSl) slabs past the ring
+  auto pad_of = [&](int sr) { return stacked ? (size_t)0 : (size_t)(4 * p.Mt - p.MSl) * sr * 128; };
+  p.SR = 16;
+  for (int sr : {64, 32}) {
+    if ((kSmemBudget - kNL * lo_of(sr) - pad_of(sr)) / raw_of(sr) >= 3) {
+      p.SR = sr;
+      break;
+    }
+  }
+  p.nraw = (int)std::min<size_t>(kMaxRaw, (kSmemBudget - kNL * lo_of(p.SR) - pad_of(p.SR)) / raw_of(p.SR));
+  if (p.nraw < 2) return fail(kDimension, "tc_wgrad: stage too large");
+  p.nblocks = ceil_div(F, p.SR);
+  p.flush_blocks = kFlushRows / p.SR;
+  p.p_full = p.Mc / 32;
+  p.q_full = p.Nc / 32;
+  CUtensorMap pmap3, qmap3, pmap, qmap;
+  if (int e = make_map(&pmap, P, F, p.Mc, ldp, 32, p.SR, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return e;
+  if (int e = make_map(&qmap, Q, F, p.Nc, ldq, 32, p.SR, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return e;
+  pmap3 = pmap;
+  qmap3 = qmap;
+  if (p.p_full)
+    if (int e = make_map3(&pmap3, P, F, p.p_full, ldp, p.SR)) return e;
+  if (p.q_full)
+    if (int e = make_map3(&qmap3, Q, F, p.q_full, ldq, p.SR)) return e;
+  const size_t smem = (size_t)p.nraw * raw_of(p.SR) + kNL * lo_of(p.SR) + pad_of(p.SR);
+  cudaError_t e = cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return fail(kCuda, "tc_wgrad smem: %s", cudaGetErrorString(e));
+  const int grid = std::max(1, slices);
+  tc_wgrad_kernel<<<grid, kThreads, smem, st>>>(pmap3, qmap3, pmap, qmap, p);
+  return post_launch("tc_wgrad_kernel");
 }
 
 }  // namespace
@@ -250,14 +878,11 @@ tc_gemm_kernel(TcArgs p) {
 
 using namespace accel;
 
-extern "C" size_t accel_tc_gemm_smem(int N) {
-  const int Npad = (N + 15) / 16 * 16;
-  return (size_t)2 * BM * BK * 4 + (size_t)2 * Npad * BK * 4;
-}
+extern "C" int accel_tc_sm_count(void) { return sm_count(); }
 
 // C[M, N] = act(A . B^T + bias) (+ C if accumulate).  a_trans: A stored [K, M];
-// b_trans: B stored [K, N].  kslices > 1: C receives [kslices][M][N] partial
-// products (no bias / act / accumulate) to be reduced by the caller.
+// b_trans: B stored [K, N].  a_trans && b_trans (weight gradient, reduction over
+// the K rows): C receives [2 * kslices][M][N] fp32 partials, two per persistent CTA.
 extern "C" int accel_tc_gemm(const float* A, const float* B, float* C, const float* bias,
                              int64_t M, int64_t K, int N, int64_t lda, int64_t ldb, int64_t ldc,
                              int a_trans, int b_trans, int act_tanh, int accumulate, int kslices,
@@ -266,21 +891,15 @@ extern "C" int accel_tc_gemm(const float* A, const float* B, float* C, const flo
     return fail(kDimension, "tc_gemm: bad sizes M=%lld K=%lld N=%d", (long long)M, (long long)K, N);
   if (M == 0) return kOk;
   if (!A || !B || !C) return fail(kDimension, "tc_gemm: NULL buffer");
-  TcArgs p;
-  p.A = A; p.B = B; p.C = C; p.bias = bias;
-  p.M = M; p.K = K; p.N = N;
-  p.Npad = (N + 15) / 16 * 16;
-  p.lda = lda; p.ldb = ldb; p.ldc = ldc;
-  p.a_trans = a_trans; p.b_trans = b_trans; p.act_tanh = act_tanh; p.accumulate = accumulate;
-  p.kslices = kslices;
-  int cols = 32;
-  while (cols < p.Npad) cols <<= 1;
-  p.tmem_cols = cols;
-  const size_t smem = accel_tc_gemm_smem(N);
-  cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return fail(kCuda, "tc_gemm smem: %s", cudaGetErrorString(e));
-  dim3 grid((unsigned)ceil_div(M, (int64_t)BM), (unsigned)kslices);
-  tc_gemm_kernel<<<grid, kTC, smem, as_stream(stream)>>>(p);
-  return post_launch("tc_gemm_kernel");
+  if (K > INT32_MAX) return fail(kDimension, "tc_gemm: K too large");
+  if (a_trans && b_trans) {
+    if (M > 256 || bias || act_tanh || accumulate)
+      return fail(kDimension, "tc_gemm: weight-gradient mode takes M <= 256, no epilogue");
+    return launch_wgrad(A, B, C, K, (int)M, N, lda, ldb, kslices, as_stream(stream));
+  }
+  if (a_trans || kslices != 1)
+    return fail(kDimension, "tc_gemm: unsupported operand layout");
+  if (M > INT32_MAX) return fail(kDimension, "tc_gemm: M too large");
+  return launch_rows(A, B, C, bias, M, K, N, lda, ldb, ldc, b_trans, act_tanh, accumulate,
+                     as_stream(stream));
 }

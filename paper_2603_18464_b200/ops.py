@@ -315,8 +315,27 @@ def adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, group0, group1, skip, bad
 # tensor-core GEMM (tcgen05, 3xTF32)
 
 
+def pitched(x):
+    """x (2-D fp32) with 16-byte aligned rows: x itself when its row pitch is a
+    multiple of 4 floats, else a copy with the pitch rounded up (the tensor-core
+    GEMMs stream operands through TMA, which needs aligned rows).  Producers on
+    the hot path allocate pitched storage up front (`alloc_pitched`)."""
+    if x.stride(1) == 1 and x.stride(0) % 4 == 0 and x.data_ptr() % 16 == 0:
+        return x
+    out = alloc_pitched(x.shape[0], x.shape[1], x.device)
+    out.copy_(x)
+    return out
+
+
+def alloc_pitched(rows, cols, device, dtype=F32):
+    """[rows, cols] view of a [rows, round_up(cols, 4)] buffer (aligned rows)."""
+    pitch = -(-int(cols) // 4) * 4
+    return torch.empty(rows, pitch, dtype=dtype, device=device)[:, :cols]
+
+
 def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
     """out[M, N] = act(x[M, K] . w[N, K]^T + bias) (+ out): y = x W^T as in models.py."""
+    x = pitched(x)
     M, K = x.shape
     N = w.shape[0]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
@@ -327,6 +346,7 @@ def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
 
 def tc_matmul_nn(x, w, out=None, accumulate=False):
     """out[M, N] = x[M, K] . w[K, N] (w row-major, i.e. B given transposed)."""
+    x = pitched(x)
     M, K = x.shape
     N = w.shape[1]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
@@ -335,21 +355,33 @@ def tc_matmul_nn(x, w, out=None, accumulate=False):
     return out
 
 
+def tc_sm_count() -> int:
+    return int(_lib.lib().accel_tc_sm_count())
+
+
 def tc_wgrad(dy, x, out, kslices=None, partial=None):
-    """out[n, k] = dy[F, n]^T . x[F, k] (reduction over the F rows), split-K over
-    `kslices` CTAs per output tile and reduced in fixed order (deterministic)."""
+    """out[n, k] = dy[F, n]^T . x[F, k] (reduction over the F rows): `kslices`
+    persistent CTAs each produce two fp32 partials, reduced in fixed order
+    (deterministic)."""
+    dy, x = pitched(dy), pitched(x)
     F, n = dy.shape
     k = x.shape[1]
     if n > 256:
         raise DimensionError("tc_wgrad: n > 256")
     if kslices is None:
-        # short K slices: the tensor core's fp32 accumulation error grows with
-        # the reduction length, the fixed-order fp64 slice reduction does not
-        kslices = max(1, min(8192, -(-F // 512)))
-    if kslices == 1:
-        _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(out), None, n, F, k, dy.stride(0),
-                  x.stride(0), out.stride(0), 1, 1, 0, 0, 1, _stream())
-        return out
+        kslices = max(1, min(tc_sm_count(), -(-F // 32)))
+    if partial is None:
+        partial = torch.empty(2 * kslices, n, k, dtype=F32, device=dy.device)
+    _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
+              x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
+    reduce_segments([(partial, out, 2 * kslices, n * k, n * k)])
+    return out
+    if partial is None:
+        partial = torch.empty(kslices, n, k, dtype=F32, device=dy.device)
+    _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
+              x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
+    reduce_segments([(partial, out, kslices, n * k, n * k)])
+    return out
     partial = torch.empty(kslices, n, k, dtype=F32, device=dy.device) if partial is None else partial
     _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
               x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())

@@ -35,7 +35,13 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = False
     dev = torch.device("cuda")
     g = torch.Generator(device=dev).manual_seed(0)
-    rn = lambda *s: torch.randn(*s, generator=g, device=dev)
+    def rn(*s):
+        t = torch.randn(*s, generator=g, device=dev)
+        if len(s) == 2 and s[0] > 4096 and s[1] % 4:  # frame rows: pitched storage
+            t2 = ops.alloc_pitched(s[0], s[1], dev)
+            t2.copy_(t)
+            return t2
+        return t
     D, O, A, H = 64, 195, 256, 64
     rows = []
     # row transforms: y[F, n] = x[F, k] W[n, k]^T
