@@ -84,12 +84,15 @@ def device_inputs(lens, done, seed: int, device):
     N = int(off[-1])
     F = N + n
     steps = (np.arange(F) - np.repeat(off[:-1] + np.arange(n), lens + 1)).astype(np.int32)
+    from paper_2603_18464_b200 import ops
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     f32 = torch.float32
+    frames = ops.alloc_pitched(F, d["O"], device)  # aligned rows: the GEMMs stream via TMA
+    frames.normal_(generator=g)
     return {
         "traj_off": torch.from_numpy(off).to(device),
-        "frames": torch.randn(F, d["O"], generator=g, device=device, dtype=f32),
+        "frames": frames,
         "steps": torch.from_numpy(steps).to(device),
         "values": torch.randn(F, generator=g, device=device, dtype=f32),
         "tokens": torch.randint(0, d["A"], (N * d["K"],), generator=g, device=device,
@@ -237,7 +240,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2603_18464_b200 import _lib
+    from paper_2603_18464_b200 import _lib, ops
     from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
 
     torch.cuda.set_device(local)
@@ -305,10 +308,19 @@ def main():
     if not args.no_e2e:
         h2d = sum(v.numel() * v.element_size() for v in host.values())
         dev_in = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
-        for _ in range(1):
+        staging = dev_in["frames"]  # contiguous landing buffer for the frame rows
+        dev_in["frames"] = ops.alloc_pitched(*host["frames"].shape, dev)
+
+        def upload():
             for k in host:
-                dev_in[k].copy_(host[k], non_blocking=True)
-            step(dev_in)
+                if k == "frames":  # contiguous DMA, then re-pitch on the device
+                    staging.copy_(host[k], non_blocking=True)
+                    dev_in[k].copy_(staging)
+                else:
+                    dev_in[k].copy_(host[k], non_blocking=True)
+
+        upload()
+        step(dev_in)
         if comm is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -317,8 +329,7 @@ def main():
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()
         for _ in range(args.steps):
-            for k in host:
-                dev_in[k].copy_(host[k], non_blocking=True)
+            upload()
             step(dev_in)
         a1.record()
         torch.cuda.synchronize()
@@ -340,7 +351,10 @@ def main():
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
     peak = float(peaks["hbm_gbs"])
     A = d["A"]
-    loss_bytes = M * (8 * A + 12) + 4 * N
+    # factorized head (trainer default): per token dz write (4A) + token/lp_old/lp_new
+    # (12); per transition the H2W row read and the g_frame row write (8A) + adv and
+    # frame index (8).  DESIGN.md "Kernels / token_loss_fact".
+    loss_bytes = M * (4 * A + 12) + N * (8 * A + 8) if tr.factorized else M * (8 * A + 12) + 4 * N
     t_loss = float(np.mean(kern.get("token_loss", [float("nan")]))) / 1e3
     achieved = loss_bytes / t_loss / 1e9
     traffic = None
@@ -366,7 +380,8 @@ def main():
         "config": {"workload": WORKLOAD, "trajectories_per_gpu": n, "transitions_per_gpu": N,
                    "tokens_per_gpu": M, "parallelism": f"dp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (behavior logits alone 11+ GB per GPU)"},
-        "roofline": {"kernel": "token_loss (fused GIPO fwd+bwd)", "bound": "hbm",
+        "roofline": {"kernel": "token_loss_fact (fused GIPO fwd+bwd, factorized head)"
+                     if tr.factorized else "token_loss (fused GIPO fwd+bwd)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_launch": loss_bytes, "ms_per_launch": t_loss * 1e3,

@@ -37,6 +37,12 @@ const char* accel_last_error(void);
 unsigned long long accel_launch_count(void);
 int accel_version(void);
 
+/* One strided copy (cudaMemcpy2DAsync, any direction): `height` rows of
+ * `width` bytes from src (row pitch spitch) to dst (row pitch dpitch).  Used to
+ * upload frame rows into pitched device storage. */
+int accel_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                  size_t height, void* stream);
+
 /* ---- (a) advantages ---------------------------------------------------- */
 
 /* Workspace bytes for accel_gae_segmented over n_transitions steps. */

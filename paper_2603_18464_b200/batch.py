@@ -130,7 +130,7 @@ class DeviceTrainBatch:
         finite = all(np.all(np.isfinite(np.asarray(a))) for a in
                      (obs, lp, batch.advantages, batch.value_targets))
         return cls(
-            frames=t(obs, np.float32), steps=t(batch.steps, np.int32),
+            frames=ops.upload_pitched(obs.astype(np.float32), device), steps=t(batch.steps, np.int32),
             tokens=t(tokens.reshape(-1), np.int32),
             frame_of=torch.arange(N, dtype=torch.int32, device=device),
             lp_old=t(lp.reshape(-1), np.float32), adv=t(batch.advantages, np.float32),

@@ -29,3 +29,15 @@ extern "C" unsigned long long accel_launch_count(void) {
 }
 
 extern "C" int accel_version(void) { return 1; }
+
+// One strided DMA (host <-> device or device <-> device): uploads row-major
+// host arrays into pitched device storage (16-byte aligned rows for TMA).
+extern "C" int accel_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch,
+                             size_t width, size_t height, void* stream) {
+  if (height == 0 || width == 0) return accel::kOk;
+  if (!dst || !src || dpitch < width || spitch < width)
+    return accel::fail(accel::kDimension, "copy_2d: bad arguments");
+  return accel::check_cuda(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height,
+                                             cudaMemcpyDefault, accel::as_stream(stream)),
+                           "copy_2d");
+}

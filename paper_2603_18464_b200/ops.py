@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -325,6 +326,32 @@ def pitched(x):
     out = alloc_pitched(x.shape[0], x.shape[1], x.device)
     out.copy_(x)
     return out
+
+
+def copy_2d(dst, src):
+    """dst[:] = src for 2-D tensors with unit column stride and any row pitch,
+    one strided DMA (host <-> device)."""
+    if dst.shape != src.shape or dst.stride(1) != 1 or src.stride(1) != 1:
+        raise DimensionError("copy_2d: shapes/strides")
+    es = dst.element_size()
+    _lib.call("accel_copy_2d", _p(dst), dst.stride(0) * es, _p(src), src.stride(0) * es,
+              dst.shape[1] * es, dst.shape[0], _stream())
+    return dst
+
+
+def upload_pitched(a, device, dtype=F32, staging=None):
+    """Host array/tensor [rows, cols] -> pitched device storage (aligned rows):
+    one contiguous H2D copy (full DMA rate; a row-strided DMA of short rows is
+    several times slower) into `staging` (or a temporary), then a device-side
+    re-pitch."""
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    t = t.to(dtype).contiguous()
+    out = alloc_pitched(t.shape[0], t.shape[1], device, dtype)
+    if out.is_contiguous():
+        return out.copy_(t, non_blocking=True)
+    tmp = torch.empty(t.shape, dtype=dtype, device=device) if staging is None else staging
+    tmp.copy_(t, non_blocking=True)
+    return out.copy_(tmp)
 
 
 def alloc_pitched(rows, cols, device, dtype=F32):

@@ -25,7 +25,7 @@ from typing import Any, Generator
 import numpy as np
 import torch
 
-from . import ops
+from . import _lib, ops
 from .batch import DeviceTrainBatch
 from .errors import AccelError, DimensionError, DomainError, NonFiniteError
 from .params import AdamStateView, DeviceParams, Dims, FlatLayout, POLICY_NAMES, VALUE_NAMES
@@ -418,10 +418,8 @@ class Trainer:
                 return torch.empty(F, D, dtype=F32, device=self.device)
             return self.scratch.get(tag + name, (F, D))
 
-        h1 = _mm(frames, P["w0"].t(), buf("h1"))
-        ops.bias_tanh(h1, P["b0"])
-        h2 = _mm(h1, P["w1"].t(), buf("h2"))
-        ops.bias_tanh(h2, P["b1"])
+        h1 = ops.tc_linear(frames, P["w0"], buf("h1"), bias=P["b0"], tanh=True)
+        h2 = ops.tc_linear(h1, P["w1"], buf("h2"), bias=P["b1"], tanh=True)
         return h1, h2
 
     def _frame_values(self, frames, steps, out, bad_part, keep: bool = False):
@@ -439,7 +437,7 @@ class Trainer:
         g = ops.warp_grid(F)
         ops.value_pool(h1, h2, None, steps, F, d.n_steps, P["w_attn"], P["b_attn"], P["e_step"], U,
                        alpha, bad_part, g)
-        zm = _mm(U, P["w0v"].t(), self.scratch.get("rv.zm", (F, d.mlp_hidden)))
+        zm = ops.tc_linear(U, P["w0v"], self.scratch.get("rv.zm", (F, d.mlp_hidden)))
         ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], None, 0.0, 0.0, out, None, None,
                        ops.warp_grid(F))
         return g
@@ -447,7 +445,7 @@ class Trainer:
     def recompute_values(self, traj) -> np.ndarray:
         """V(o_t) for all T+1 frames under the current critic (trainer.py:352-356)."""
         assert self.publish_version >= traj.behavior_version
-        frames = _dev(np.asarray(traj.observations), np.float32, self.device)
+        frames = ops.upload_pitched(np.asarray(traj.observations, dtype=np.float32), self.device)
         steps = _dev(np.asarray(traj.steps), np.int32, self.device)
         if frames.shape[1] != self.dims.obs_dim:
             raise DimensionError(f"observations have dim {frames.shape[1]}, "
@@ -473,7 +471,7 @@ class Trainer:
         dev = self.device
         return {
             "traj_off": _dev(pb.traj_off, np.int64, dev),
-            "frames": _dev(pb.frames, np.float32, dev),
+            "frames": ops.upload_pitched(np.asarray(pb.frames, dtype=np.float32), dev),
             "steps": _dev(pb.steps, np.int32, dev),
             "values": _dev(pb.values, np.float32, dev),
             "tokens": _dev(pb.tokens.reshape(-1), np.int32, dev),
@@ -584,6 +582,18 @@ class Trainer:
 
         return _Ctx()
 
+    def _wgrad(self, dy, x, out, tag: str, extra: int = 0):
+        """Tensor-core dW = dy^T x into per-CTA partial slices (+ `extra` slices
+        the caller fills); returns the reduce_segments entry that sums them."""
+        dy, x = ops.pitched(dy), ops.pitched(x)  # no-ops at aligned widths
+        F, n = dy.shape
+        k = x.shape[1]
+        ks = max(1, min(ops.tc_sm_count(), -(-F // 32)))
+        part = self.scratch.get("wg." + tag, (2 * ks + extra, n, k))
+        _lib.call("accel_tc_gemm", ops._p(dy), ops._p(x), ops._p(part), None, n, F, k,
+                  dy.stride(0), x.stride(0), k, 1, 1, 0, 0, ks, ops._stream())
+        return (part, out, 2 * ks + extra, n * k, n * k)
+
     def _allreduce_sum(self, t):
         return self.comm.all_reduce_sum(t) if self.comm is not None else t
 
@@ -633,7 +643,7 @@ class Trainer:
             h1, h2 = self._backbone(batch.frames, "st.")
         if fact:
             # logits = H2W[frame] + EP[prev] + PP[k] + b: three small GEMMs, no [M, A] logits
-            h2w = _mm(h2, P["w_head"].t(), S.get("st.h2w", (F, A)))
+            h2w = ops.tc_linear(h2, P["w_head"], S.get("st.h2w", (F, A)))
             ep = _mm(P["e_prev"], P["w_head"].t(), S.get("st.ep", (A + 1, A)))
             pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
             epp = ops.ep_plus(ep, pp, P["b_head"], K, S.get("st.epp", ((A + 1) * K, A)))
@@ -652,7 +662,7 @@ class Trainer:
         else:
             c = ops.build_c(h2, batch.frame_of, batch.tokens_dev, P["e_prev"], P["e_pos"], N, K,
                             A, S.get("st.c", (M, D)))
-            logits = _mm(c, P["w_head"].t(), S.get("st.logits", (M, A)))
+            logits = ops.tc_linear(c, P["w_head"], S.get("st.logits", (M, A)))
             gl = ops.token_grid(M)
             dlogits = S.get("st.dlogits", (M, A))
             dbias_part = S.get("st.dbias", (gl, A))
@@ -682,13 +692,13 @@ class Trainer:
         vbad_part = S.get("st.vbad", (gw, 2), F64)
         ops.value_pool(h1, h2, batch.frame_of, batch.frame_steps, N, d.n_steps, P["w_attn"],
                        P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
-        zm = _mm(U, P["w0v"].t(), S.get("st.zm", (N, H)))
+        zm = ops.tc_linear(U, P["w0v"], S.get("st.zm", (N, H)))
         vpart = S.get("st.vpart", (gw, 2 * H + 1))
         vdpart = S.get("st.vdpart", (gw, 2), F64)
         ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
                        vpart, vdpart, gw)
-        _mm(zm.t(), U, G["w0v"])
-        dU = _mm(zm, P["w0v"], S.get("st.dU", (N, D)))
+        segs = [self._wgrad(zm, U, G["w0v"], "w0v")]  # dzm^T U
+        dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (N, D)))
         de = S.get("st.de", (N, 2))
         battn_part = S.get("st.battn", (gw,))
         ops.value_attn_grad(dU, h1, h2, batch.frame_of, alpha, de, battn_part, gw)
@@ -698,27 +708,29 @@ class Trainer:
         batch.step_group.rows_sum(dU, G["e_step"])
 
         # policy backward
-        segs = []
         if fact:
             # D(prev,k) = grouped sums of dz; Dprev / Dpos marginals
             dpk = batch.pk_group.rows_sum(dz, S.get("st.dpk", ((A + 1) * K, A)))
             dprev = S.get("st.dprev", (A + 1, A))
             dpos = S.get("st.dpos", (K, A))
             ops.pk_marginals(dpk, K, A, dprev, dpos)
-            # dW_head = G^T h2 + Dprev^T e_prev + Dpos^T e_pos   (sum_t dz_t (x) c_t)
-            _mm(g_frame.t(), h2, G["w_head"])
-            G["w_head"].addmm_(dprev.t(), P["e_prev"])
-            G["w_head"].addmm_(dpos.t(), P["e_pos"])
+            # dW_head = G^T h2 + Dprev^T e_prev + Dpos^T e_pos   (sum_t dz_t (x) c_t):
+            # the two small products ride along as one extra partial slice
+            seg = self._wgrad(g_frame, h2, G["w_head"], "w_head", extra=1)
+            small = seg[0][seg[2] - 1]
+            torch.mm(dprev.t(), P["e_prev"], out=small)
+            small.addmm_(dpos.t(), P["e_pos"])
+            segs.append(seg)
             _mm(dprev, P["w_head"], G["e_prev"])
             _mm(dpos, P["w_head"], G["e_pos"])
-            dz2 = _mm(g_frame, P["w_head"], S.get("st.dz2", (F, D)))  # dh2 (0 on bootstrap rows)
+            dz2 = ops.tc_matmul_nn(g_frame, P["w_head"], S.get("st.dz2", (F, D)))  # dh2
             gd = ops.rows_grid(F)
             db1_part = S.get("st.db1", (gd, D))
             ops.tanh_grad_colsum(dz2, h2, db1_part, gd)
             segs.append((dpos, G["b_head"], K, A, A))
         else:
-            _mm(dlogits.t(), c, G["w_head"])
-            dc = _mm(dlogits, P["w_head"], c)  # c is dead after dW_head: reuse its storage
+            segs.append(self._wgrad(dlogits, c, G["w_head"], "w_head"))
+            dc = ops.tc_matmul_nn(dlogits, P["w_head"], c)  # c is dead after dW_head: reuse it
             dz2 = S.get("st.dz2", (F, D))
             if F != N:
                 dz2.zero_()
@@ -728,12 +740,12 @@ class Trainer:
             ops.dc_reduce(dc, h2, batch.frame_of, N, K, D, dz2, pos_part, db1_part, gd)
             batch.prev_group.rows_sum(dc, G["e_prev"])
             segs += [(dbias_part, G["b_head"], gl, A, A), (pos_part, G["e_pos"], gd, K * D, K * D)]
-        _mm(dz2.t(), h1, G["w1"])
-        dh1 = _mm(dz2, P["w1"], S.get("st.dh1", (F, D)))
+        segs.append(self._wgrad(dz2, h1, G["w1"], "w1"))
+        dh1 = ops.tc_matmul_nn(dz2, P["w1"], S.get("st.dh1", (F, D)))
         gt = ops.rows_grid(F)
         db0_part = S.get("st.db0", (gt, D))
         ops.tanh_grad_colsum(dh1, h1, db0_part, gt)
-        _mm(dh1.t(), batch.frames, G["w0"])
+        segs.append(self._wgrad(dh1, batch.frames, G["w0"], "w0"))
 
         ops.reduce_segments(segs + [
             (db1_part, G["b1"], gd, D, D),
