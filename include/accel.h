@@ -124,10 +124,13 @@ int accel_token_loss(const float* logits, const float* bias, const int32_t* toke
  * h2w[frame_of[i]] + epp[prev*K + k] with h2w = h2 W_head^T (f32[F, A]) and
  * epp = e_prev W_head^T + e_pos W_head^T + b_head (f32[(A+1)*K, A],
  * accel_ep_plus) — models.py:181-182 distributed over c = h2 + e_prev[prev]
- * + e_pos.  Writes dz f32[N*K, A] (per-token dlogits), g_frame f32[F, A]
- * rows frame_of[i] = sum_k dz[i, k] (pre-zero the bootstrap rows), lp_new,
- * stat_part/max_part as accel_token_loss (grid = accel_fact_grid(N)).
- * fix_stats: FIXUP pass as accel_token_loss. */
+ * + e_pos.  Writes either dz f32[N*K, A] (per-token dlogits) or, with dz =
+ * NULL, tsc f32x4[N*K] = {nm2, Ac, Cc, coef} per token, from which
+ * dz = 2^d2 (Ac d2 + Cc) (+ coef at the token), d2 = logit log2(e) + nm2 is
+ * recomputed by accel_fact_group_sum (A in {128, 256, 512, 1024}); plus
+ * g_frame f32[F, A] rows frame_of[i] = sum_k dz[i, k] (pre-zero the bootstrap
+ * rows), lp_new, stat_part/max_part as accel_token_loss (grid =
+ * accel_fact_grid(N)).  fix_stats: FIXUP pass as accel_token_loss. */
 int accel_fact_grid(int64_t N);
 /* epp[(prev*K+k)*A + a] = ep[prev*A + a] + pp[k*A + a] + bias[a] */
 int accel_ep_plus(const float* ep, const float* pp, const float* bias, int A, int K,
@@ -136,8 +139,17 @@ int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* fra
                           const int32_t* tokens, const float* lp_old, const float* adv,
                           int64_t N, int K, int A, int algo, double sigma, double clip_eps,
                           double lambda_h, double m_global, const double* fix_stats,
-                          float* dz, float* g_frame, float* lp_new, double* stat_part,
+                          float* dz, void* tsc, float* g_frame, float* lp_new, double* stat_part,
                           double* max_part, void* stream);
+/* Grouped dz sums over the (prev, position) keys without dz in HBM: piece
+ * partials f32[n_pieces, A] (then accel_grouped_rows_sum's key pass) of the dz
+ * rows recomputed from h2w/epp and the tsc scalars, rows in the stable key
+ * order of accel_group_by_key (perm/seg_off/piece_off; piece_rows = 256).
+ * Reference: the np.add.at of models.py:195 (dc rows grouped by prev token). */
+int accel_fact_group_sum(const float* h2w, const float* epp, const int32_t* frame_of,
+                         const int32_t* tokens, const void* tsc, const int32_t* perm,
+                         const int64_t* seg_off, const int64_t* piece_off, int nkeys, int K,
+                         int A, int piece_rows, int64_t n_pieces, float* piece_out, void* stream);
 /* Dprev f32[A+1, A] = sum_k dpk[j, k]; Dpos f32[K, A] = sum_j dpk[j, k]
  * from the (prev, k)-grouped dz sums dpk f32[(A+1)*K, A]. */
 int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, float* dpos,
@@ -188,7 +200,9 @@ int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
                        int64_t* seg_off, int64_t* piece_off, void* workspace,
                        size_t workspace_bytes, void* stream);
 /* out f32[nkeys, D] = sum of vals rows per key, in perm order (bitwise
- * deterministic); piece_buf f32[accel_group_max_pieces(R, nkeys) * D]. */
+ * deterministic); piece_buf f32[accel_group_max_pieces(R, nkeys) * D].
+ * vals = NULL: only the key pass (piece_buf already filled, e.g. by
+ * accel_fact_group_sum). */
 int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
                            const int64_t* seg_off, const int64_t* piece_off, int nkeys,
                            int64_t n_pieces, float* piece_buf, float* out, void* stream);

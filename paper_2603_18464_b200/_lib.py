@@ -41,7 +41,9 @@ _SIGNATURES = {
     "accel_ep_plus": (c_int, [P, P, P, c_int, c_int, P, P]),
     "accel_token_loss_fact": (c_int, [P, P, P, P, P, P, c_int64, c_int, c_int, c_int,
                                       c_double, c_double, c_double, c_double, P, P, P, P, P, P,
-                                      P]),
+                                      P, P]),
+    "accel_fact_group_sum": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_int64,
+                                     P, P]),
     "accel_pk_marginals": (c_int, [P, c_int, c_int, P, P, P]),
     "accel_step_keys": (c_int, [P, P, c_int64, c_int, P, P, P]),
     "accel_group_workspace_size": (c_size_t, [c_int64, c_int]),

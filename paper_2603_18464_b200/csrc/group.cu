@@ -230,6 +230,55 @@ key_sum_kernel(const float* __restrict__ piece_out, const int64_t* __restrict__ 
   }
 }
 
+// float4 columns, 1024 threads: `sub` = 1024 / (D / 4) row-lanes, each with 4
+// independent partial sums (fixed assignment, fixed combine order).  The
+// chunk-start key holds one row per transition (thousands of pieces): this
+// keeps ~64 loads in flight per column group instead of a serial chain.
+constexpr int kKeyThreads = 1024;
+__global__ void __launch_bounds__(kKeyThreads)
+key_sum4_kernel(const float4* __restrict__ piece_out, const int64_t* __restrict__ piece_off,
+                int nkeys, int D4, float4* __restrict__ out) {
+  extern __shared__ float4 s4[];
+  const int key = blockIdx.x;
+  const int64_t p0 = piece_off[key], p1 = piece_off[key + 1];
+  const int span = D4 <= kKeyThreads && kKeyThreads % D4 == 0 ? D4 : kKeyThreads;
+  const int sub = kKeyThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  for (int d0 = 0; d0 < D4; d0 += span) {
+    const int d = d0 + lc;
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (d < D4) {
+      int64_t p = p0 + lr;
+      for (; p + 3 * sub < p1; p += 4 * sub) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 x = __ldg(piece_out + (p + u * sub) * D4 + d);
+          a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+        }
+      }
+      for (int u = 0; p < p1; p += sub, ++u) {
+        const float4 x = __ldg(piece_out + p * D4 + d);
+        a[u & 3].x += x.x; a[u & 3].y += x.y; a[u & 3].z += x.z; a[u & 3].w += x.w;
+      }
+    }
+    float4 t = a[0];
+    for (int u = 1; u < 4; ++u) { t.x += a[u].x; t.y += a[u].y; t.z += a[u].z; t.w += a[u].w; }
+    s4[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D4) {
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s2 = 0; s2 < sub; ++s2) {
+        const float4 y = s4[s2 * span + threadIdx.x];
+        r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
+      }
+      out[(int64_t)key * D4 + d0 + threadIdx.x] = r;
+    }
+    __syncthreads();
+  }
+}
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t cub_scan_bytes(int64_t n) {
@@ -323,16 +372,22 @@ extern "C" int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const
                                       int nkeys, int64_t n_pieces, float* piece_buf, float* out,
                                       void* stream) {
   if (R < 0 || D < 1 || nkeys < 1 || n_pieces < 0) return fail(kDimension, "grouped_rows_sum: bad sizes");
-  if (!vals || !perm || !seg_off || !piece_off || !piece_buf || !out)
+  if (!perm || !seg_off || !piece_off || !piece_buf || !out)
     return fail(kDimension, "grouped_rows_sum: NULL buffer");
   if ((D & 3) == 0 && ((reinterpret_cast<uintptr_t>(vals) | reinterpret_cast<uintptr_t>(piece_buf)) & 15))
     return fail(kDimension, "grouped_rows_sum: vals/piece_buf must be 16B aligned");
   cudaStream_t s = as_stream(stream);
   int st;
-  if (n_pieces > 0) {
+  if (vals && n_pieces > 0) {  // vals == NULL: piece_buf already holds the piece sums
     piece_sum_kernel<<<(unsigned)n_pieces, kThreads, kThreads * sizeof(float4), s>>>(
         vals, perm, seg_off, piece_off, nkeys, D, piece_buf);
     if ((st = post_launch("piece_sum_kernel"))) return st;
+  }
+  if ((D & 3) == 0 && ((reinterpret_cast<uintptr_t>(piece_buf) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    key_sum4_kernel<<<nkeys, kKeyThreads, kKeyThreads * sizeof(float4), s>>>(
+        reinterpret_cast<const float4*>(piece_buf), piece_off, nkeys, D / 4,
+        reinterpret_cast<float4*>(out));
+    return post_launch("key_sum4_kernel");
   }
   key_sum_kernel<<<nkeys, kThreads, kThreads * sizeof(float), s>>>(piece_buf, piece_off, nkeys, D,
                                                                    out);

@@ -294,14 +294,16 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
 // logits of its group's current token, so the per-token scalar algebra (log-sum,
 // ratio, trust weight, fix-up store) is issued once for TPW tokens.  Group-local
 // reductions use xor shuffles below LPT and group-masked CREDUX.
-template <int VPL, int LPT>
+// SC: write per-token scalars {nm2, Ac, Cc, coef} (tsc) instead of the dz rows;
+// the grouped-sum pass recomputes dz from them (fact_group_sum_kernel)
+template <int VPL, int LPT, bool SC>
 __global__ void __launch_bounds__(kThreads, 2)
 token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
                            const int32_t* __restrict__ frame_of,
                            const int32_t* __restrict__ tokens, const float* __restrict__ lp_old,
                            const float* __restrict__ adv, int64_t N, int K, int A,
                            LossParams prm, const double* __restrict__ fix_stats,
-                           float* __restrict__ dz, float* __restrict__ g_frame,
+                           float* __restrict__ dz, float4* __restrict__ tsc, float* __restrict__ g_frame,
                            float* __restrict__ lp_new, double* __restrict__ stat_part,
                            double* __restrict__ max_part) {
   constexpr int TPW = 32 / LPT;
@@ -481,18 +483,25 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
         g[v] += e[v];
       }
       const int64_t row = i * K + k;
-      float* drow = dz + row * A;
-      if (act) {
+      if constexpr (SC) {
+        if (act && gl == 0) {
+          tsc[row] = make_float4(nm2, Ac, Cc, coef);
+          if (!cx.fixup) lp_new[row] = lpn;
+        }
+      } else {
+        float* drow = dz + row * A;
+        if (act) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
-          __stcs(reinterpret_cast<float4*>(drow + colof(q, 0)),
-                 make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]));
-      }
-      __syncwarp();
-      if (act && gl == 0) {
-        const float d2t = fmaf(z_tok, kLog2e, nm2);
-        drow[tok] = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
-        if (!cx.fixup) lp_new[row] = lpn;
+          for (int q = 0; q < Q; ++q)
+            __stcs(reinterpret_cast<float4*>(drow + colof(q, 0)),
+                   make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]));
+        }
+        __syncwarp();
+        if (act && gl == 0) {
+          const float d2t = fmaf(z_tok, kLog2e, nm2);
+          drow[tok] = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
+          if (!cx.fixup) lp_new[row] = lpn;
+        }
       }
       const bool mine = gl == k;
       my_coef = mine ? coef : my_coef;
@@ -595,10 +604,118 @@ __global__ void pk_marginals_kernel(const float* __restrict__ dpk, int K, int A,
   }
 }
 
+// Grouped sums of dz over the (prev token, position) keys without dz in HBM:
+// one CTA per piece (<= 256 tokens of one key, in the batch's stable key order)
+// recomputes each token's dz row from its H2W row (gathered, 1 KB), the key's
+// EPP row (shared memory) and the token scalars {nm2, Ac, Cc, coef} written by
+// the SC loss pass -- the same float operations as the loss kernel:
+//   d2 = (h + ep) log2(e) + nm2,  dz = 2^d2 (Ac d2 + Cc)  (+ coef at the token)
+// Row-lanes of A/4 threads, 4 rows in flight per lane, fixed combine order.
+constexpr int kGsThreads = 256;
+constexpr int kGsRows = 256;  // piece rows (== the grouping's piece size)
+__global__ void __launch_bounds__(kGsThreads)
+fact_group_sum_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
+                      const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
+                      const float4* __restrict__ tsc, const int32_t* __restrict__ perm,
+                      const int64_t* __restrict__ seg_off, const int64_t* __restrict__ piece_off,
+                      int nkeys, int K, int A, int piece_rows, float* __restrict__ piece_out) {
+  // smem: epp row [A] | partials [kGsThreads] float4 | per-token frame, token, scalars
+  extern __shared__ __align__(16) float s_gs[];
+  __shared__ int s_frame[kGsRows], s_tok[kGsRows];
+  __shared__ float4 s_sc[kGsRows];
+  const int64_t piece = blockIdx.x;
+  if (piece >= piece_off[nkeys]) return;
+  int lo = 0, hi = nkeys;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (piece_off[mid] <= piece) lo = mid; else hi = mid;
+  }
+  const int key = lo;
+  const int64_t r0 = seg_off[key] + (piece - piece_off[key]) * piece_rows;
+  const int nr = (int)min(seg_off[key + 1] - r0, (int64_t)piece_rows);
+  float* s_ep = s_gs;
+  float4* s_part = reinterpret_cast<float4*>(s_gs + A);
+  for (int c = threadIdx.x; c < A; c += kGsThreads) s_ep[c] = __ldg(epp + (int64_t)key * A + c);
+  // the piece's token metadata, gathered once (one token per thread)
+  for (int r = threadIdx.x; r < nr; r += kGsThreads) {
+    const int64_t t = __ldg(perm + r0 + r);
+    s_frame[r] = __ldg(frame_of + t / K);
+    s_tok[r] = __ldg(tokens + t);
+    s_sc[r] = __ldg(tsc + t);
+  }
+  __syncthreads();
+  const int A4 = A >> 2;
+  const int span = A4 <= kGsThreads && kGsThreads % A4 == 0 ? A4 : kGsThreads;
+  const int sub = kGsThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  auto row = [&](int r, int c4, const float4& ep, float4& acc) {
+    const float4 h = __ldg(reinterpret_cast<const float4*>(h2w + (int64_t)s_frame[r] * A) + c4);
+    const float4 sc = s_sc[r];
+    const int tok = s_tok[r];
+    const float d[4] = {h.x + ep.x, h.y + ep.y, h.z + ep.z, h.w + ep.w};
+    float o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float d2 = fmaf(d[u], kLog2e, sc.x);
+      o[u] = ex2_ftz(d2) * fmaf(sc.y, d2, sc.z);
+    }
+    if ((tok >> 2) == c4) o[tok & 3] += sc.w;
+    acc.x += o[0]; acc.y += o[1]; acc.z += o[2]; acc.w += o[3];
+  };
+  for (int c0 = 0; c0 < A4; c0 += span) {
+    const int c4 = c0 + lc;
+    float4 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c4 < A4) {
+      const float4 ep = reinterpret_cast<const float4*>(s_ep)[c4];
+      int r = lr;
+      for (; r + 3 * sub < nr; r += 4 * sub) {  // four independent row loads in flight
+#pragma unroll
+        for (int u = 0; u < 4; ++u) row(r + u * sub, c4, ep, acc[u]);
+      }
+      for (; r < nr; r += sub) row(r, c4, ep, acc[0]);
+    }
+    float4 t = acc[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) { t.x += acc[u].x; t.y += acc[u].y; t.z += acc[u].z; t.w += acc[u].w; }
+    s_part[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x < span && c0 + threadIdx.x < A4) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s2 = 0; s2 < sub; ++s2) {
+        const float4 y = s_part[s2 * span + threadIdx.x];
+        a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
+      }
+      reinterpret_cast<float4*>(piece_out + piece * A)[c0 + threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 }  // namespace accel
 
 using namespace accel;
+
+extern "C" int accel_fact_group_sum(const float* h2w, const float* epp, const int32_t* frame_of,
+                                    const int32_t* tokens, const void* tsc, const int32_t* perm,
+                                    const int64_t* seg_off, const int64_t* piece_off, int nkeys,
+                                    int K, int A, int piece_rows, int64_t n_pieces,
+                                    float* piece_out, void* stream) {
+  if (K < 1 || A < 4 || A % 4 || nkeys < 1 || piece_rows < 1 || piece_rows > kGsRows)
+    return fail(kDimension, "fact_group_sum: bad sizes");
+  if (n_pieces == 0) return kOk;
+  if (!h2w || !epp || !frame_of || !tokens || !tsc || !perm || !seg_off || !piece_off || !piece_out)
+    return fail(kDimension, "fact_group_sum: NULL buffer");
+  if (misaligned16(h2w) || misaligned16(epp) || misaligned16(tsc) || misaligned16(piece_out))
+    return fail(kDimension, "fact_group_sum: buffers must be 16B aligned");
+  const size_t smem = (size_t)A * 4 + kGsThreads * sizeof(float4);
+  fact_group_sum_kernel<<<(unsigned)n_pieces, kGsThreads, smem, as_stream(stream)>>>(
+      h2w, epp, frame_of, tokens, static_cast<const float4*>(tsc), perm, seg_off, piece_off, nkeys,
+      K, A, piece_rows, piece_out);
+  return post_launch("fact_group_sum_kernel");
+}
 
 extern "C" int accel_fact_grid(int64_t N) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, kWarps), (int64_t)kNumSMs * 2));
@@ -617,9 +734,9 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
                                      const int32_t* tokens, const float* lp_old, const float* adv,
                                      int64_t N, int K, int A, int algo, double sigma,
                                      double clip_eps, double lambda_h, double m_global,
-                                     const double* fix_stats, float* dz, float* g_frame,
-                                     float* lp_new, double* stat_part, double* max_part,
-                                     void* stream) {
+                                     const double* fix_stats, float* dz, void* tsc,
+                                     float* g_frame, float* lp_new, double* stat_part,
+                                     double* max_part, void* stream) {
   if (algo != 0 && algo != 1) return fail(kDomain, "unknown algorithm %d", algo);
   if (!(sigma > 0)) return fail(kDomain, "sigma must be > 0, got %g", sigma);
   if (!(clip_eps > 0 && clip_eps < 1)) return fail(kDomain, "clip_eps must be in (0, 1)");
@@ -629,10 +746,11 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
     return fail(kDimension, "token_loss_fact needs 128 <= A <= 1024, A %% 4 == 0 (got %d)", A);
   if (N == 0) return kOk;
   if (!(m_global >= (double)(N * K))) return fail(kDimension, "m_global < local token count");
-  if (!h2w || !epp || !frame_of || !tokens || !lp_old || !adv || !dz || !g_frame ||
+  if (!h2w || !epp || !frame_of || !tokens || !lp_old || !adv || (!dz && !tsc) || !g_frame ||
       (!fix_stats && (!lp_new || !stat_part || !max_part)))
     return fail(kDimension, "token_loss_fact: NULL buffer");
-  if (misaligned16(h2w) || misaligned16(epp) || misaligned16(dz) || misaligned16(g_frame))
+  if (misaligned16(h2w) || misaligned16(epp) || misaligned16(dz) || misaligned16(tsc) ||
+      misaligned16(g_frame))
     return fail(kDimension, "token_loss_fact: buffers must be 16B aligned");
   LossParams prm;
   prm.algo = algo;
@@ -662,12 +780,34 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
                                         fix_stats, dz, g_frame, lp_new, stat_part, max_part);
     return post_launch("token_loss_fact_kernel");
   };
+  // grouped kernel in scalar mode or dz mode
+  auto grp = [&](auto kernel_dz, auto kernel_sc, int VPL, int TPW) -> int {
+    const size_t smem = (size_t)kWarps * (kGS + 4) * VPL * 32 * 4 +
+                        (size_t)kWarps * (kGS + 2) * TPW * sizeof(uint64_t) + 16;
+    auto launch = [&](auto kernel) -> int {
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(kCuda, "token_loss_fact smem: %s", cudaGetErrorString(e));
+      }
+      kernel<<<grid, kThreads, smem, s>>>(h2w, epp, frame_of, tokens, lp_old, adv, N, K, A, prm,
+                                          fix_stats, dz, static_cast<float4*>(tsc), g_frame, lp_new,
+                                          stat_part, max_part);
+      return post_launch("token_loss_fact_grp_kernel");
+    };
+    return tsc ? launch(kernel_sc) : launch(kernel_dz);
+  };
   const bool full = A == 128 || A == 256 || A == 512 || A == 1024;
   // grouped kernel: 16 (32 at A = 1024) logits per lane, A / that lanes per transition
-  if (A == 128 && K <= 8) return go(token_loss_fact_grp_kernel<16, 8>, 16, 4);
-  if (A == 256 && K <= 16) return go(token_loss_fact_grp_kernel<16, 16>, 16, 2);
-  if (A == 512 && K <= 32) return go(token_loss_fact_grp_kernel<16, 32>, 16, 1);
-  if (A == 1024 && K <= 32) return go(token_loss_fact_grp_kernel<32, 32>, 32, 1);
+  if (A == 128 && K <= 8)
+    return grp(token_loss_fact_grp_kernel<16, 8, false>, token_loss_fact_grp_kernel<16, 8, true>, 16, 4);
+  if (A == 256 && K <= 16)
+    return grp(token_loss_fact_grp_kernel<16, 16, false>, token_loss_fact_grp_kernel<16, 16, true>, 16, 2);
+  if (A == 512 && K <= 32)
+    return grp(token_loss_fact_grp_kernel<16, 32, false>, token_loss_fact_grp_kernel<16, 32, true>, 16, 1);
+  if (A == 1024 && K <= 32)
+    return grp(token_loss_fact_grp_kernel<32, 32, false>, token_loss_fact_grp_kernel<32, 32, true>, 32, 1);
+  if (tsc) return fail(kDimension, "token_loss_fact: scalar output needs A in {128, 256, 512, 1024}");
   if (A <= 128)
     return full ? go(token_loss_fact_kernel<4, true>, 4) : go(token_loss_fact_kernel<4, false>, 4);
   if (A <= 256)

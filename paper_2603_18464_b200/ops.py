@@ -183,6 +183,20 @@ class Grouping:
         _lib.call("accel_group_by_key", _p(keys), R, nkeys, _p(self.perm), _p(self.seg_off),
                   _p(self.piece_off), _p(buf), buf.numel(), _stream())
 
+    def fact_rows_sum(self, h2w, epp, frame_of, tokens, tsc, K, out, piece_buf=None):
+        """Grouped dz sums with dz recomputed from the loss pass's token scalars
+        (accel_fact_group_sum, then the key pass)."""
+        A = h2w.shape[1]
+        if piece_buf is None:
+            piece_buf = workspace("group_pieces_f32").get(4 * max(self.max_pieces, 1) * A)
+        _lib.call("accel_fact_group_sum", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(tsc),
+                  _p(self.perm), _p(self.seg_off), _p(self.piece_off), self.nkeys, int(K), A, 256,
+                  self.max_pieces, _p(piece_buf), _stream())
+        _lib.call("accel_grouped_rows_sum", None, self.R, A, _p(self.perm), _p(self.seg_off),
+                  _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
+                  _stream())
+        return out
+
     def rows_sum(self, vals, out, piece_buf=None):
         D = vals.shape[1]
         if piece_buf is None:
@@ -211,13 +225,14 @@ def ep_plus(ep, pp, bias, K, out):
 
 def token_loss_fact(h2w, epp, frame_of, tokens, lp_old, adv, N, K, algo, sigma, clip_eps,
                     lambda_h, m_global, dz, g_frame, lp_new, stat_part, max_part,
-                    fix_stats=None):
-    """Factorized-head fused loss (see accel.h accel_token_loss_fact)."""
+                    fix_stats=None, tsc=None):
+    """Factorized-head fused loss (see accel.h accel_token_loss_fact); dz=None
+    with tsc (f32[M, 4]) writes the per-token scalars instead of dz rows."""
     A = h2w.shape[1]
     _lib.call("accel_token_loss_fact", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(lp_old),
               _p(adv), int(N), int(K), A, int(algo), float(sigma), float(clip_eps),
-              float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(g_frame), _p(lp_new),
-              _p(stat_part), _p(max_part), _stream())
+              float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(tsc), _p(g_frame),
+              _p(lp_new), _p(stat_part), _p(max_part), _stream())
 
 
 def pk_marginals(dpk, K, A, dprev, dpos):

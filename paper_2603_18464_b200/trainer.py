@@ -363,6 +363,7 @@ class Trainer:
         A, K = self.dims.n_actions, self.dims.chunk_len
         # factorized head (no [M, A] logits) wherever the kernel supports the shape
         self.factorized = A % 4 == 0 and 128 <= A <= 1024 and K <= 32
+        self.recompute_dz = False
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
 
@@ -533,6 +534,8 @@ class Trainer:
             behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
         batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized)
         batch.h_cache = h_cache
+        # frame row of each trajectory's bootstrap observation (t = T)
+        batch.boot_rows = b["traj_off"][1:] + torch.arange(n, dtype=torch.int64, device=dev)
         host_dev = torch.cat([flags, cnt.double()])
         if self.comm is not None:
             # data parallel: the batch is one shard of the global batch; every
@@ -648,16 +651,27 @@ class Trainer:
             pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
             epp = ops.ep_plus(ep, pp, P["b_head"], K, S.get("st.epp", ((A + 1) * K, A)))
             gf = ops.fact_grid(N)
-            dz = S.get("st.dz", (M, A))
+            # recompute_dz: per-token scalars instead of dz rows, the grouped sums
+            # recompute dz (saves the 4A bytes/token dz write+read, costs the
+            # recompute; off by default: the loss kernel is issue-bound, so the
+            # dz stores are nearly free and the gathered recompute is slower)
+            if self.recompute_dz:
+                tsc, dz = S.get("st.tsc", (M, 4)), None
+            else:
+                tsc, dz = None, S.get("st.dz", (M, A))
             g_frame = S.get("st.gframe", (F, A))
-            if F != N:
-                g_frame.zero_()
+            if F != N:  # bootstrap frames have no transition: their G rows are zero
+                boot = getattr(batch, "boot_rows", None)
+                if boot is not None:
+                    g_frame.index_fill_(0, boot, 0.0)
+                else:
+                    g_frame.zero_()
             stat_part = S.get("st.stat", (gf, 8), F64)
             max_part = S.get("st.max", (gf, 2), F64)
             loss_args = (h2w, epp, batch.frame_of, batch.tokens_dev, batch.lp_old, batch.adv, N,
                          K, algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dz, g_frame)
             with self._timed("token_loss"):
-                ops.token_loss_fact(*loss_args, lp_new, stat_part, max_part)
+                ops.token_loss_fact(*loss_args, lp_new, stat_part, max_part, tsc=tsc)
             gl = gf
         else:
             c = ops.build_c(h2, batch.frame_of, batch.tokens_dev, P["e_prev"], P["e_pos"], N, K,
@@ -679,7 +693,7 @@ class Trainer:
             self.comm.all_reduce_max(loss_max)
         # FIXUP: only does work when 0 < excluded < M_global (decided on the device)
         if fact:
-            ops.token_loss_fact(*loss_args, None, None, None, fix_stats=loss_sums)
+            ops.token_loss_fact(*loss_args, None, None, None, fix_stats=loss_sums, tsc=tsc)
         else:
             ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K,
                            algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None,
@@ -710,7 +724,13 @@ class Trainer:
         # policy backward
         if fact:
             # D(prev,k) = grouped sums of dz; Dprev / Dpos marginals
-            dpk = batch.pk_group.rows_sum(dz, S.get("st.dpk", ((A + 1) * K, A)))
+            with self._timed("group_sum"):
+                dpk_buf = S.get("st.dpk", ((A + 1) * K, A))
+                if self.recompute_dz:
+                    dpk = batch.pk_group.fact_rows_sum(h2w, epp, batch.frame_of, batch.tokens_dev,
+                                                       tsc, K, dpk_buf)
+                else:
+                    dpk = batch.pk_group.rows_sum(dz, dpk_buf)
             dprev = S.get("st.dprev", (A + 1, A))
             dpos = S.get("st.dpos", (K, A))
             ops.pk_marginals(dpk, K, A, dprev, dpos)

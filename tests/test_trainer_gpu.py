@@ -159,10 +159,11 @@ def _oracle_from(cfg, pol0, val0, A, S):
 
 
 @pytest.mark.parametrize("algo", ["trust", "clip"])
-@pytest.mark.parametrize("factorized", [True, False])
+@pytest.mark.parametrize("factorized", [True, False, "recompute"])
 def test_random_batch_matches_oracle(algo, factorized):
     tr, trajs, pol0, val0, cfg = _random_setup(seed=3, algo=algo)
-    tr.factorized = factorized
+    tr.factorized = bool(factorized)
+    tr.recompute_dz = factorized == "recompute"  # dz rebuilt from token scalars
     orc = _oracle_from(cfg, pol0, val0, 256, tr.dims.n_steps)
     ob = orc.build_train_batch(trajs)
     batch = tr.build_train_batch(trajs)
@@ -175,14 +176,15 @@ def test_random_batch_matches_oracle(algo, factorized):
     check_grads(dev_pol, dev_val, g_pol, g_val, algo)
 
 
-@pytest.mark.parametrize("factorized", [True, False])
+@pytest.mark.parametrize("factorized", [True, False, "recompute"])
 def test_partial_exclusion_runs_fixup_pass(factorized):
     """Some tokens with log-ratio < -745 are excluded: the surrogate mean is
     over the included count (trainer.py:211), entropy still over all tokens."""
     from paper_2603_18464_b200.batch import DeviceTrainBatch
 
     tr, trajs, pol0, val0, cfg = _random_setup(seed=5)
-    tr.factorized = factorized
+    tr.factorized = bool(factorized)
+    tr.recompute_dz = factorized == "recompute"
     orc = _oracle_from(cfg, pol0, val0, 256, tr.dims.n_steps)
     ob = orc.build_train_batch(trajs)
     poisoned = ob.behavior_logp.copy()
