@@ -184,7 +184,7 @@ struct LossAcc {
 
 struct RowCtx {
   LossParams prm;
-  float inv_m, ent_scale;
+  float inv_m, ent_scale, inv_sigma;
   double inv_m_d;
   bool fixup;
 };
@@ -202,6 +202,7 @@ __device__ __forceinline__ bool setup_ctx(const LossParams& prm, const double* f
   cx.inv_m = (float)(1.0 / m_eff);
   cx.inv_m_d = 1.0 / m_eff;
   cx.ent_scale = prm.lambda_h * (float)prm.inv_nk;
+  cx.inv_sigma = 1.f / prm.sigma;
   return true;
 }
 
@@ -244,31 +245,63 @@ __device__ __forceinline__ RowStats row_stats_full(float (&z)[VPL], float (&e)[V
 }
 
 // The rare float64 tail of token_coef, kept out of line so its register
-// footprint does not size the hot loop.
-__device__ __noinline__ float token_coef_f64(float dlt, float a, LossParams prm, double inv_m_d,
-                                             double* term_d, double* r_d, double* w_d,
-                                             bool* outside) {
+// footprint does not size the hot loop; results come back by value (taking the
+// callers' addresses would push their statistics to local memory every token).
+struct CoefTail {
+  double term, r, w;
+  float coef;
+  int outside;
+};
+__device__ __noinline__ CoefTail token_coef_f64(float dlt, float a, LossParams prm, double inv_m_d) {
+  CoefTail o;
   double cd;
-  token_scalars<double>((double)dlt, (double)a, prm, cd, *term_d, *r_d, *w_d, *outside);
-  return (float)(cd * inv_m_d);
+  bool out;
+  token_scalars<double>((double)dlt, (double)a, prm, cd, o.term, o.r, o.w, out);
+  o.coef = (float)(cd * inv_m_d);
+  o.outside = out;
+  return o;
 }
 
-// Per-token coefficient c (= dloss/dlogp * m) and the statistics terms.
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp)
+__device__ __forceinline__ float ex2_sfu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Per-token coefficient c (= dloss/dlogp * m) and the statistics terms.  The
+// common path is float with SFU exponentials (r = e^dlt, w = e^(-q^2/2)); the
+// float64 tail takes |dlt| >= 60 or trust weights below e^-75.
 __device__ __forceinline__ float token_coef(float dlt, float a, bool inc, const RowCtx& cx,
                                             double& term_d, double& r_d, double& w_d,
                                             bool& outside) {
+  constexpr float kL2e = 1.4426950408889634f;
   float coef = 0.f;
   term_d = 0.0; r_d = 1.0; w_d = 1.0;
   outside = false;
   if (inc) {
-    const float qq = dlt / cx.prm.sigma;
+    const float qq = dlt * cx.inv_sigma;
     if (fabsf(dlt) < 60.f && (cx.prm.algo != 0 || qq * qq < 150.f)) {
-      float cf, tf, rf, wf;
-      token_scalars<float>(dlt, a, cx.prm, cf, tf, rf, wf, outside);
+      const float r = ex2_sfu(dlt * kL2e);
+      float w = 1.f, term, cf;
+      if (cx.prm.algo == 0) {
+        w = ex2_sfu(-0.5f * kL2e * qq * qq);
+        term = w * r * a;
+        cf = -term;
+      } else {
+        const float rc = fminf(fmaxf(r, cx.prm.clip_lo), cx.prm.clip_hi);
+        const float ra = r * a, rca = rc * a;
+        term = fminf(ra, rca);
+        cf = ra <= rca ? -ra : 0.f;
+        outside = r < cx.prm.clip_lo || r > cx.prm.clip_hi;
+      }
       coef = cf * cx.inv_m;
-      term_d = tf; r_d = rf; w_d = wf;
+      term_d = term; r_d = r; w_d = w;
     } else {
-      coef = token_coef_f64(dlt, a, cx.prm, cx.inv_m_d, &term_d, &r_d, &w_d, &outside);
+      const CoefTail o = token_coef_f64(dlt, a, cx.prm, cx.inv_m_d);
+      coef = o.coef;
+      term_d = o.term; r_d = o.r; w_d = o.w;
+      outside = o.outside;
     }
   }
   return coef;

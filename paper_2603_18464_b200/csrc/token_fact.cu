@@ -224,7 +224,8 @@ token_loss_fact_kernel(const float* __restrict__ h2w, const float* __restrict__ 
       my_out = mine ? outside : my_out;
     }
     // slot s is free: refill it with the transition kStages ahead
-    fence_proxy_async();
+    // (no proxy fence: the slot's generic reads were consumed before this point;
+    // a bulk copy issued after them cannot overtake them -- WAR, as in TMA pipelines)
     __syncwarp();
     if (lane == 0 && next < N) {
       mbar_expect_tx(&bars[s], row_bytes);
@@ -310,11 +311,25 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
   constexpr int W = VPL * LPT;  // == A
   constexpr int Q = VPL / 4;    // float4 chunks per lane
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_stat[kWarps * (kNumStat + kNumMax)];
+  // per-token statistics, recorded by the group leader and folded into the
+  // group's running sums once per transition (shared memory, not registers:
+  // the k-loop's live set stays within the 128-register budget)
+  constexpr int G = kWarps * TPW;
+  __shared__ double s_td[G][LPT][3];  // term, r, w
+  __shared__ float s_tf[G][LPT][2];   // coef, H
+  __shared__ int s_ti[G][LPT];        // inc | bad << 1 | bad_tok << 2 | outside << 3
+  __shared__ double s_gacc[G][6];     // loss, ent, r, w, rmax, -wmin
+  __shared__ int s_gcnt[G][4];        // outside, excluded, bad rows, bad tokens
   RowCtx cx;
   if (!setup_ctx(prm, fix_stats, cx)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / LPT, gl = lane % LPT, gbase = grp * LPT;
+  const int gidx = warp * TPW + grp;
+  if (gl == 0) {
+    s_gacc[gidx][0] = s_gacc[gidx][1] = s_gacc[gidx][2] = s_gacc[gidx][3] = 0.0;
+    s_gacc[gidx][4] = s_gacc[gidx][5] = -CUDART_INF;
+    s_gcnt[gidx][0] = s_gcnt[gidx][1] = s_gcnt[gidx][2] = s_gcnt[gidx][3] = 0;
+  }
   // smem: ring [kWarps][kGS][TPW][W] | s_oh [kWarps][TPW][W] | bars [kWarps][kGS][TPW]
   float* ring = reinterpret_cast<float*>(smem) + ((size_t)warp * kGS * TPW + grp) * W;
   float* s_oh = reinterpret_cast<float*>(smem) + (size_t)kWarps * kGS * TPW * W +
@@ -354,9 +369,6 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
   }
   __syncwarp();
   const float ent2 = cx.ent_scale * kLn2;
-  double st_loss = 0.0, st_ent = 0.0, st_r = 0.0, st_w = 0.0;
-  double st_rmax = -CUDART_INF, st_negw = -CUDART_INF;
-  int st_out = 0, st_excl = 0, st_bad = 0, st_badtok = 0;
 
   auto colof = [&](int q, int r) { return q * 4 * LPT + gl * 4 + r; };
   auto load_grp = [&](const float* __restrict__ row, float (&x)[VPL], bool global) {
@@ -395,7 +407,8 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       a_n = __ldg(adv + i2);
     }
     // token 1's EPP row (prev = token 0) into slot 1; slot 1's last reader is done
-    fence_proxy_async();
+    // (no proxy fence: the slot's generic reads were consumed before this point;
+    // a bulk copy issued after them cannot overtake them -- WAR, as in TMA pipelines)
     __syncwarp();
     if (act && gl == 0 && K > 1) {
       const int t0 = min(max(tok_l, 0), A - 1);
@@ -407,9 +420,8 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
     float g[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[v] = 0.f;
-    float my_coef = 0.f, my_H = 0.f;
-    double my_term = 0.0, my_r = 1.0, my_w = 1.0;
-    bool my_inc = false, my_bad = false, my_badtok = false, my_out = false;
+    const int64_t row0 = i * K;  // this transition's first token row
+    float* dz_i = SC ? nullptr : dz + row0 * A;
     for (int k = 0; k < K; ++k) {
       const int tok_raw = __shfl_sync(0xffffffffu, tok_l, gbase + k);
       const float lpo = __shfl_sync(0xffffffffu, lpo_l, gbase + k);
@@ -421,7 +433,8 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
         __syncwarp();
         eph ^= 1u << (k & 1);
         // token k+1's row goes into the slot token k-1 used (fully read by now)
-        fence_proxy_async();
+        // (no proxy fence: the slot's generic reads were consumed before this point;
+        // a bulk copy issued after them cannot overtake them -- WAR, as in TMA pipelines)
         __syncwarp();
         if (act && gl == 0 && k + 1 < K) {
           const int sl = (k + 1) & 1;
@@ -443,11 +456,10 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       } else {
         // group max with full-warp xor shuffles: a group-masked CREDUX would split
         // the warp into its groups for the rest of the row (each ran the row alone)
+        // (a NaN logit is dropped by FMNMX here but still poisons the partition
+        // sum below, as +inf does through inf - inf and -inf through 0 * -inf)
 #pragma unroll
-        for (int o = LPT / 2; o > 0; o >>= 1) {
-          const float y = __shfl_xor_sync(0xffffffffu, mx, o);
-          mx = (mx != mx || y != y) ? __int_as_float(0x7fffffff) : fmaxf(mx, y);  // NaN-propagating
-        }
+        for (int o = LPT / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       }
       const float nm2 = -mx * kLog2e;
       float e[VPL], sum = 0.f, sed = 0.f;
@@ -482,14 +494,14 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
         e[v] *= fmaf(Ac, z[v], Cc);
         g[v] += e[v];
       }
-      const int64_t row = i * K + k;
+      const int64_t row = row0 + k;
       if constexpr (SC) {
         if (act && gl == 0) {
           tsc[row] = make_float4(nm2, Ac, Cc, coef);
           if (!cx.fixup) lp_new[row] = lpn;
         }
       } else {
-        float* drow = dz + row * A;
+        float* drow = dz_i + k * A;
         if (act) {
 #pragma unroll
           for (int q = 0; q < Q; ++q)
@@ -503,18 +515,17 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
           if (!cx.fixup) lp_new[row] = lpn;
         }
       }
-      const bool mine = gl == k;
-      my_coef = mine ? coef : my_coef;
-      my_H = mine ? H : my_H;
-      my_term = mine ? term_d : my_term;
-      my_r = mine ? r_d : my_r;
-      my_w = mine ? w_d : my_w;
-      my_inc = mine ? inc : my_inc;
-      my_bad = mine ? bad : my_bad;
-      my_badtok = mine ? bad_tok : my_badtok;
-      my_out = mine ? outside : my_out;
+      if (gl == 0) {
+        s_td[gidx][k][0] = term_d;
+        s_td[gidx][k][1] = r_d;
+        s_td[gidx][k][2] = w_d;
+        s_tf[gidx][k][0] = coef;
+        s_tf[gidx][k][1] = H;
+        s_ti[gidx][k] = (int)inc | ((int)bad << 1) | ((int)bad_tok << 2) | ((int)outside << 3);
+      }
     }
-    fence_proxy_async();
+    // (no proxy fence: the slot's generic reads were consumed before this point;
+    // a bulk copy issued after them cannot overtake them -- WAR, as in TMA pipelines)
     __syncwarp();
     if (gl == 0 && next < N) {
       mbar_expect_tx(&bars[s * TPW], row_bytes);
@@ -523,8 +534,7 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
     // one-hot part of G (group leader, serial over k: duplicates accumulate)
     for (int k = 0; k < K; ++k) {
       const int tk = __shfl_sync(0xffffffffu, tok_l, gbase + k);
-      const float ck = __shfl_sync(0xffffffffu, my_coef, gbase + k);
-      if (gl == 0 && tk >= 0 && tk < A) s_oh[tk] += ck;
+      if (gl == 0 && tk >= 0 && tk < A) s_oh[tk] += s_tf[gidx][k][0];
     }
     __syncwarp();
     if (act) {
@@ -539,49 +549,58 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
     __syncwarp();
     if (gl < K && tok_l >= 0 && tok_l < A) s_oh[tok_l] = 0.f;
     __syncwarp();
-    if (!cx.fixup && act && gl < K) {
-      st_ent += (double)my_H;
-      st_bad += my_bad;
-      st_badtok += my_badtok;
-      if (my_inc) {
-        st_loss += my_term;
-        st_r += my_r;
-        st_w += my_w;
-        st_out += my_out;
-        st_rmax = fmax(st_rmax, my_r);
-        st_negw = fmax(st_negw, -my_w);
-      } else {
-        ++st_excl;
+    if (!cx.fixup && act && gl == 0) {  // fold this transition's token statistics
+      double loss = s_gacc[gidx][0], ent = s_gacc[gidx][1], rs = s_gacc[gidx][2];
+      double ws = s_gacc[gidx][3], rmax = s_gacc[gidx][4], negw = s_gacc[gidx][5];
+      int nout = 0, nex = 0, nbad = 0, nbt = 0;
+      for (int k = 0; k < K; ++k) {
+        const int fl = s_ti[gidx][k];
+        ent += (double)s_tf[gidx][k][1];
+        nbad += (fl >> 1) & 1;
+        nbt += (fl >> 2) & 1;
+        if (fl & 1) {
+          const double r = s_td[gidx][k][1], w = s_td[gidx][k][2];
+          loss += s_td[gidx][k][0];
+          rs += r;
+          ws += w;
+          nout += (fl >> 3) & 1;
+          rmax = fmax(rmax, r);
+          negw = fmax(negw, -w);
+        } else {
+          ++nex;
+        }
       }
+      s_gacc[gidx][0] = loss; s_gacc[gidx][1] = ent; s_gacc[gidx][2] = rs;
+      s_gacc[gidx][3] = ws; s_gacc[gidx][4] = rmax; s_gacc[gidx][5] = negw;
+      s_gcnt[gidx][0] += nout; s_gcnt[gidx][1] += nex;
+      s_gcnt[gidx][2] += nbad; s_gcnt[gidx][3] += nbt;
     }
+    __syncwarp();
   }
   if (cx.fixup) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // groups in fixed order: deterministic
+    double sum[kNumStat];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
-    st_ent += __shfl_xor_sync(0xffffffffu, st_ent, o);
-    st_r += __shfl_xor_sync(0xffffffffu, st_r, o);
-    st_w += __shfl_xor_sync(0xffffffffu, st_w, o);
-    st_rmax = fmax(st_rmax, __shfl_xor_sync(0xffffffffu, st_rmax, o));
-    st_negw = fmax(st_negw, __shfl_xor_sync(0xffffffffu, st_negw, o));
+    for (int q = 0; q < kNumStat; ++q) sum[q] = 0.0;
+    double rmax = -CUDART_INF, negw = -CUDART_INF;
+    for (int g = 0; g < G; ++g) {
+      sum[kLossNum] += s_gacc[g][0];
+      sum[kEntSum] += s_gacc[g][1];
+      sum[kRatioSum] += s_gacc[g][2];
+      sum[kWSum] += s_gacc[g][3];
+      rmax = fmax(rmax, s_gacc[g][4]);
+      negw = fmax(negw, s_gacc[g][5]);
+      sum[kOutside] += s_gcnt[g][0];
+      sum[kExcluded] += s_gcnt[g][1];
+      sum[kBadRows] += s_gcnt[g][2];
+      sum[kBadTok] += s_gcnt[g][3];
+    }
+#pragma unroll
+    for (int q = 0; q < kNumStat; ++q) stat_part[(int64_t)blockIdx.x * kNumStat + q] = sum[q];
+    max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = rmax;
+    max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = negw;
   }
-  st_out = __reduce_add_sync(0xffffffffu, st_out);
-  st_excl = __reduce_add_sync(0xffffffffu, st_excl);
-  st_bad = __reduce_add_sync(0xffffffffu, st_bad);
-  st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
-  LossAcc<1> acc;
-  acc.init();
-  acc.loss_num = st_loss;
-  acc.ent_sum = st_ent;
-  acc.ratio_sum = st_r;
-  acc.w_sum = st_w;
-  acc.rmax = st_rmax;
-  acc.negwmin = st_negw;
-  acc.n_out = st_out;
-  acc.n_excl = st_excl;
-  acc.n_bad = st_bad;
-  acc.n_badtok = st_badtok;
-  stats_epilogue<1>(acc, s_stat, stat_part, max_part);
 }
 
 // Dprev[j] = sum_k Dpk[j, k], Dpos[k] = sum_j Dpk[j, k]  (Dpk f32[(A+1), K, A])

@@ -365,7 +365,8 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
     } else {
       rs = row_stats<VPL, true>(z, e, lane, A, tok, false);
     }
-    fence_proxy_async();
+    // (no proxy fence: the slot's reads were consumed by row_stats above; the bulk
+    // copy refilling it is issued after them -- WAR ordering as in TMA pipelines)
     __syncwarp();
     if (lane == 0) {
       lp_out[row] = rs.d_tok - rs.log_s;
