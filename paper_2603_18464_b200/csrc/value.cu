@@ -380,6 +380,159 @@ value_attn_wgrad_kernel(const float* __restrict__ de, const float* __restrict__ 
   }
 }
 
+// value_head with LPR lanes per row (CPL = H / LPR columns each, float4 I/O):
+// the row's dot product is an LPR-lane reduction instead of a full-warp one,
+// the column sums stay in registers, tanh uses one ex2 + one fast divide.
+template <int LPR, int CPL>
+__global__ void __launch_bounds__(kThreads)
+value_head4_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
+                   const float* __restrict__ w1v, const float* __restrict__ b1v, int64_t R,
+                   const float* __restrict__ targets, float lambda_v, double inv_n,
+                   float* __restrict__ values_out, float* __restrict__ part,
+                   double* __restrict__ dpart) {
+  constexpr int H = LPR * CPL, RPW = 32 / LPR, Q = CPL / 4;
+  __shared__ float s_part[kWarps][2 * H + 1];
+  __shared__ double s_err[kWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rsub = lane / LPR, lc = lane % LPR;
+  const float bias1 = __ldg(b1v);
+  float bz[CPL], w1[CPL], gw1[CPL], gb0[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) {
+    bz[j] = __ldg(b0v + lc * CPL + j);
+    w1[j] = __ldg(w1v + lc * CPL + j);
+    gw1[j] = 0.f;
+    gb0[j] = 0.f;
+  }
+  float gb1 = 0.f;
+  double err2 = 0.0, bad = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kWarps * RPW;
+  for (int64_t r = ((int64_t)blockIdx.x * kWarps + warp) * RPW + rsub; r - rsub < R; r += stride) {
+    const bool act = r < R;
+    float m[CPL];
+    float acc = 0.f;
+    float4* row = reinterpret_cast<float4*>(zm + r * H + lc * CPL);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const float4 z = act ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float x = zz[u] + bz[4 * q + u];
+        const float t = __expf(2.f * x);
+        m[4 * q + u] = 1.f - __fdividef(2.f, t + 1.f);
+        acc = fmaf(w1[4 * q + u], m[4 * q + u], acc);
+      }
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const float v = acc + bias1;
+    if (act && values_out && lc == 0) values_out[r] = v;
+    if (targets && act) {
+      const float err = v - __ldg(targets + r);
+      const float dv = (float)((double)lambda_v * 2.0 * (double)err * inv_n);
+      if (lc == 0) {
+        err2 += (double)err * (double)err;
+        bad += !isfinite(v);
+        gb1 += dv;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        float g4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          g4[u] = dv * w1[j] * (1.f - m[j] * m[j]);
+          gw1[j] = fmaf(dv, m[j], gw1[j]);
+          gb0[j] += g4[u];
+        }
+        row[q] = make_float4(g4[0], g4[1], g4[2], g4[3]);
+      }
+    }
+  }
+  if (!targets) return;
+  // rows of the warp -> one set of column sums (fixed xor order), then warps in order
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      gw1[j] += __shfl_xor_sync(0xffffffffu, gw1[j], o);
+      gb0[j] += __shfl_xor_sync(0xffffffffu, gb0[j], o);
+    }
+  }
+  gb1 = warp_sum(gb1);
+  err2 = warp_sum_d(err2);
+  bad = warp_sum_d(bad);
+  if (rsub == 0) {
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      s_part[warp][lc * CPL + j] = gw1[j];
+      s_part[warp][H + lc * CPL + j] = gb0[j];
+    }
+  }
+  if (lane == 0) {
+    s_part[warp][2 * H] = gb1;
+    s_err[warp][0] = err2;
+    s_err[warp][1] = bad;
+  }
+  __syncthreads();
+  float* out = part + (int64_t)blockIdx.x * (2 * H + 1);
+  for (int e = threadIdx.x; e < 2 * H + 1; e += kThreads) {
+    float a = 0.f;
+    for (int w = 0; w < kWarps; ++w) a += s_part[w][e];
+    out[e] = a;
+  }
+  if (threadIdx.x < 2) {
+    double a = 0.0;
+    for (int w = 0; w < kWarps; ++w) a += s_err[w][threadIdx.x];
+    dpart[(int64_t)blockIdx.x * 2 + threadIdx.x] = a;
+  }
+}
+
+// dw_attn partials with float4 columns and four independent row accumulators
+template <int D4>
+__global__ void __launch_bounds__(kThreads)
+value_attn_wgrad4_kernel(const float* __restrict__ de, const float4* __restrict__ h1,
+                         const float4* __restrict__ h2, const int32_t* __restrict__ row_frame,
+                         int64_t R, float* __restrict__ part) {
+  constexpr int SUB = kThreads / D4;
+  __shared__ float4 s_acc[kThreads];
+  const int lr = threadIdx.x / D4, lc = threadIdx.x % D4;
+  const int64_t per = ceil_div(R, (int64_t)gridDim.x);
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(R, r0 + per);
+  float4 acc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto one = [&](int64_t r, float4& a) {
+    const int64_t f = row_frame ? __ldg(row_frame + r) : r;
+    const float2 d = __ldg(reinterpret_cast<const float2*>(de) + r);
+    const float4 x = __ldg(h1 + f * D4 + lc), y = __ldg(h2 + f * D4 + lc);
+    a.x = fmaf(d.x, x.x, fmaf(d.y, y.x, a.x));
+    a.y = fmaf(d.x, x.y, fmaf(d.y, y.y, a.y));
+    a.z = fmaf(d.x, x.z, fmaf(d.y, y.z, a.z));
+    a.w = fmaf(d.x, x.w, fmaf(d.y, y.w, a.w));
+  };
+  int64_t r = r0 + lr;
+  for (; r + 3 * SUB < r1; r += 4 * SUB) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) one(r + u * SUB, acc[u]);
+  }
+  for (; r < r1; r += SUB) one(r, acc[0]);
+  float4 t = acc[0];
+#pragma unroll
+  for (int u = 1; u < 4; ++u) { t.x += acc[u].x; t.y += acc[u].y; t.z += acc[u].z; t.w += acc[u].w; }
+  s_acc[threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x < D4) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s2 = 0; s2 < SUB; ++s2) {
+      const float4 y = s_acc[s2 * D4 + threadIdx.x];
+      a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
+    }
+    reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * D4 * 4)[threadIdx.x] = a;
+  }
+}
+
 int warp_grid(int64_t rows) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, kWarps), (int64_t)kNumSMs * 8));
 }
@@ -426,9 +579,22 @@ extern "C" int accel_value_head(float* zm, const float* b0v, const float* w1v, c
   if (R == 0) return kOk;
   if (!zm || !b0v || !w1v || !b1v || (targets && (!part || !dpart)))
     return fail(kDimension, "value_head: NULL buffer");
-  value_head_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(
-      zm, b0v, w1v, b1v, R, H, targets, (float)lambda_v, n_global > 0 ? 1.0 / n_global : 0.0,
-      values_out, part, dpart);
+  const double inv_n = n_global > 0 ? 1.0 / n_global : 0.0;
+  cudaStream_t st = as_stream(stream);
+  if ((reinterpret_cast<uintptr_t>(zm) & 15) == 0 && (H == 32 || H == 64 || H == 128)) {
+    if (H == 32)
+      value_head4_kernel<8, 4><<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, targets,
+                                                          (float)lambda_v, inv_n, values_out, part, dpart);
+    else if (H == 64)
+      value_head4_kernel<8, 8><<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, targets,
+                                                          (float)lambda_v, inv_n, values_out, part, dpart);
+    else
+      value_head4_kernel<16, 8><<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, targets,
+                                                           (float)lambda_v, inv_n, values_out, part, dpart);
+    return post_launch("value_head4_kernel");
+  }
+  value_head_kernel<<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, H, targets, (float)lambda_v,
+                                               inv_n, values_out, part, dpart);
   return post_launch("value_head_kernel");
 }
 
@@ -459,7 +625,18 @@ extern "C" int accel_value_attn_wgrad(const float* de, const float* h1, const fl
                                       int grid, void* stream) {
   if (R < 0 || D < 1 || grid < 1) return fail(kDimension, "value_attn_wgrad: bad sizes");
   if (R == 0) return kOk;
-  value_attn_wgrad_kernel<<<grid, kThreads, kThreads * sizeof(float), as_stream(stream)>>>(
-      de, h1, h2, row_frame, R, D, part);
+  const uintptr_t al = reinterpret_cast<uintptr_t>(h1) | reinterpret_cast<uintptr_t>(h2) |
+                       reinterpret_cast<uintptr_t>(de) | reinterpret_cast<uintptr_t>(part);
+  cudaStream_t st = as_stream(stream);
+  if ((al & 15) == 0 && (D == 32 || D == 64 || D == 128)) {
+    const float4* a4 = reinterpret_cast<const float4*>(h1);
+    const float4* b4 = reinterpret_cast<const float4*>(h2);
+    if (D == 32) value_attn_wgrad4_kernel<8><<<grid, kThreads, 0, st>>>(de, a4, b4, row_frame, R, part);
+    else if (D == 64) value_attn_wgrad4_kernel<16><<<grid, kThreads, 0, st>>>(de, a4, b4, row_frame, R, part);
+    else value_attn_wgrad4_kernel<32><<<grid, kThreads, 0, st>>>(de, a4, b4, row_frame, R, part);
+    return post_launch("value_attn_wgrad4_kernel");
+  }
+  value_attn_wgrad_kernel<<<grid, kThreads, kThreads * sizeof(float), st>>>(de, h1, h2, row_frame,
+                                                                             R, D, part);
   return post_launch("value_attn_wgrad_kernel");
 }
