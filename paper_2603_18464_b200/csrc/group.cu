@@ -153,26 +153,46 @@ piece_sum_kernel(const float* __restrict__ vals, const int32_t* __restrict__ per
   const int64_t r0 = seg_off[key] + (piece - piece_off[key]) * kPiece;
   const int64_t r1 = min(seg_off[key + 1], r0 + kPiece);
   if ((D & 3) == 0) {
-    // float4 columns: a row is D/4 lanes wide
+    // float4 columns: a row is D/4 lanes wide; the piece's row ids are staged in
+    // shared memory first so four independent row loads per lane stay in flight
+    __shared__ int s_rows[kPiece];
+    const int nr = (int)(r1 - r0);
+    for (int r = threadIdx.x; r < nr; r += kThreads) s_rows[r] = __ldg(perm + r0 + r);
+    __syncthreads();
     const int D4 = D >> 2;
     const int span = (D4 <= kThreads && kThreads % D4 == 0) ? D4 : kThreads;
     const int sub = kThreads / span;
     const int lr = threadIdx.x / span, lc = threadIdx.x % span;
     float4* s4 = reinterpret_cast<float4*>(s_acc);
+    const float4* v4 = reinterpret_cast<const float4*>(vals);
     for (int d0 = 0; d0 < D4; d0 += span) {
       const int d = d0 + lc;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (d < D4)
-        for (int64_t r = r0 + lr; r < r1; r += sub) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(vals + (int64_t)__ldg(perm + r) * D) + d);
-          acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      float4 acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (d < D4) {
+        int r = lr;
+        for (; r + 3 * sub < nr; r += 4 * sub) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 x = __ldg(v4 + (int64_t)s_rows[r + u * sub] * D4 + d);
+            acc[u].x += x.x; acc[u].y += x.y; acc[u].z += x.z; acc[u].w += x.w;
+          }
         }
-      s4[threadIdx.x] = acc;
+        for (; r < nr; r += sub) {
+          const float4 x = __ldg(v4 + (int64_t)s_rows[r] * D4 + d);
+          acc[0].x += x.x; acc[0].y += x.y; acc[0].z += x.z; acc[0].w += x.w;
+        }
+      }
+      float4 t = acc[0];
+#pragma unroll
+      for (int u = 1; u < 4; ++u) { t.x += acc[u].x; t.y += acc[u].y; t.z += acc[u].z; t.w += acc[u].w; }
+      s4[threadIdx.x] = t;
       __syncthreads();
       if (threadIdx.x < span && d0 + threadIdx.x < D4) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < sub; ++s) {
-          const float4 y = s4[s * span + threadIdx.x];
+        for (int s2 = 0; s2 < sub; ++s2) {
+          const float4 y = s4[s2 * span + threadIdx.x];
           a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
         }
         reinterpret_cast<float4*>(piece_out + piece * D)[d0 + threadIdx.x] = a;
