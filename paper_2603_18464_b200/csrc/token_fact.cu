@@ -417,9 +417,11 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
     }
     if (act) mbar_wait(&bars[s * TPW], (unsigned)(j / kGS) & 1u);
     __syncwarp();  // reconverge both groups before the element loop
-    float g[VPL];
+    // packed fp32x2 arithmetic (FFMA2/FADD2/FMUL2): half the elementwise instructions
+    constexpr int P = VPL / 2;
+    float2 g2[P];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) g[v] = 0.f;
+    for (int p = 0; p < P; ++p) g2[p] = make_float2(0.f, 0.f);
     const int64_t row0 = i * K;  // this transition's first token row
     float* dz_i = SC ? nullptr : dz + row0 * A;
     for (int k = 0; k < K; ++k) {
@@ -442,15 +444,18 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
           bulk_g2s(s_ep + sl * W, epp + ((int64_t)tok * K + k + 1) * A, row_bytes, &ebars[sl]);
         }
       }
-      float z[VPL], ez[VPL];
-      load_grp(hrow, z, false);
-      load_grp(erow, ez, false);
+      float2 z2[P];
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) z[v] += ez[v];
+      for (int q = 0; q < Q; ++q) {
+        const float4 h = *reinterpret_cast<const float4*>(hrow + colof(q, 0));
+        const float4 ep = *reinterpret_cast<const float4*>(erow + colof(q, 0));
+        z2[2 * q] = __fadd2_rn(make_float2(h.x, h.y), make_float2(ep.x, ep.y));
+        z2[2 * q + 1] = __fadd2_rn(make_float2(h.z, h.w), make_float2(ep.z, ep.w));
+      }
       const float z_tok = hrow[tok] + erow[tok];
-      float mx = fmaxf(fmaxf(z[0], z[1]), z[2]);
+      float mx = fmaxf(z2[0].x, z2[0].y);
 #pragma unroll
-      for (int v = 3; v < VPL; v += 2) mx = fmaxf(mx, v + 1 < VPL ? fmaxf(z[v], z[v + 1]) : z[v]);
+      for (int p = 1; p < P; ++p) mx = fmaxf(mx, fmaxf(z2[p].x, z2[p].y));
       if (LPT == 32) {
         mx = warp_max_nan(mx);
       } else {
@@ -462,14 +467,16 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
         for (int o = LPT / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       }
       const float nm2 = -mx * kLog2e;
-      float e[VPL], sum = 0.f, sed = 0.f;
+      const float2 l2e = make_float2(kLog2e, kLog2e), n2 = make_float2(nm2, nm2);
+      float2 e2[P], sum2 = make_float2(0.f, 0.f), sed2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        z[v] = fmaf(z[v], kLog2e, nm2);
-        e[v] = ex2_ftz(z[v]);
-        sum += e[v];
-        sed = fmaf(e[v], z[v], sed);
+      for (int p = 0; p < P; ++p) {
+        z2[p] = __ffma2_rn(z2[p], l2e, n2);  // d2 = (z - max) log2(e)
+        e2[p] = make_float2(ex2_ftz(z2[p].x), ex2_ftz(z2[p].y));
+        sum2 = __fadd2_rn(sum2, e2[p]);
+        sed2 = __ffma2_rn(e2[p], z2[p], sed2);
       }
+      float sum = sum2.x + sum2.y, sed = sed2.x + sed2.y;
 #pragma unroll
       for (int o = LPT / 2; o > 0; o >>= 1) {
         sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -489,10 +496,11 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       const float coef = token_coef(dlt, a, inc, cx, term_d, r_d, w_d, outside);
       const float Ac = ent2 * inv_s;
       const float Cc = -(Ac * sd2) - coef * inv_s;
+      const float2 A2 = make_float2(Ac, Ac), C2 = make_float2(Cc, Cc);
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        e[v] *= fmaf(Ac, z[v], Cc);
-        g[v] += e[v];
+      for (int p = 0; p < P; ++p) {
+        e2[p] = __fmul2_rn(e2[p], __ffma2_rn(A2, z2[p], C2));
+        g2[p] = __fadd2_rn(g2[p], e2[p]);
       }
       const int64_t row = row0 + k;
       if constexpr (SC) {
@@ -506,7 +514,7 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
 #pragma unroll
           for (int q = 0; q < Q; ++q)
             __stcs(reinterpret_cast<float4*>(drow + colof(q, 0)),
-                   make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]));
+                   make_float4(e2[2 * q].x, e2[2 * q].y, e2[2 * q + 1].x, e2[2 * q + 1].y));
         }
         __syncwarp();
         if (act && gl == 0) {
@@ -542,8 +550,8 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
       for (int q = 0; q < Q; ++q) {
         const float4 o = *reinterpret_cast<const float4*>(s_oh + colof(q, 0));
         __stcs(reinterpret_cast<float4*>(g_frame + (int64_t)fi * A + colof(q, 0)),
-               make_float4(g[4 * q] + o.x, g[4 * q + 1] + o.y, g[4 * q + 2] + o.z,
-                           g[4 * q + 3] + o.w));
+               make_float4(g2[2 * q].x + o.x, g2[2 * q].y + o.y, g2[2 * q + 1].x + o.z,
+                           g2[2 * q + 1].y + o.w));
       }
     }
     __syncwarp();
