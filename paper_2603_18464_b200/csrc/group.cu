@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 16384;  // rows per warp chunk
+constexpr int kChunk = 4096;   // rows per warp chunk (more chunks: more warps in the scatter)
 constexpr int kPiece = 256;    // rows per grouped-sum piece
 
 // key = prev (with_pos == 0) or prev * K + k (with_pos == 1); prev = A at k == 0
