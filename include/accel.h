@@ -219,7 +219,8 @@ int accel_value_pool(const float* h1, const float* h2, const int32_t* row_frame,
 /* zm f32[R, H] = u @ W0v^T (no bias).  targets == NULL: forward only
  * (values_out f32[R]).  Otherwise zm <- dzm, part f32[grid][2H+1]
  * {dw1v, db0v, db1v}, dpart f64[grid][2] {sum err^2, non-finite v}. */
-int accel_value_head(float* zm, const float* b0v, const float* w1v, const float* b1v,
+int accel_value_head(float* zm, const int32_t* row_frame, const float* b0v, const float* w1v,
+                     const float* b1v,
                      int64_t R, int H, const float* targets, double lambda_v,
                      double n_global, float* values_out, float* part, double* dpart,
                      int grid, void* stream);
@@ -283,6 +284,16 @@ int accel_tc_sm_count(void);
  *     fp32 partials (two per persistent CTA, kslices <= accel_tc_sm_count())
  *     for a fixed-order reduction by the caller; no bias/act/accumulate.
  * fp32 in/out, N <= 256, any strides. */
+/* Persistent-grid size of the row-transform kernel for M rows. */
+int accel_tc_rows_grid(int64_t M);
+/* C[M, N] = (A[M, K] . B^T) * (1 - H[M, N]^2) -- a backward product fused with
+ * the tanh derivative of the layer it feeds (models.py:197-200: dpre = dh (1 -
+ * h^2)) -- and col_part f32[accel_tc_rows_grid(M)][N] = per-CTA column sums of C
+ * (the bias gradient, reduced in fixed order by the caller).  B as in
+ * accel_tc_gemm (b_trans); C and H need 16-byte aligned rows, N <= 256. */
+int accel_tc_gemm_dtanh(const float* A, const float* B, float* C, const float* H,
+                        float* col_part, int64_t M, int64_t K, int N, int64_t lda, int64_t ldb,
+                        int64_t ldc, int64_t ldh, int b_trans, void* stream);
 int accel_tc_gemm(const float* A, const float* B, float* C, const float* bias, int64_t M,
                   int64_t K, int N, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
                   int b_trans, int act_tanh, int accumulate, int kslices, void* stream);

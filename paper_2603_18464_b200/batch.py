@@ -44,6 +44,8 @@ class DeviceTrainBatch:
         self.prev_group = prev_group
         self.pk_group = None
         self.step_group = step_group
+        self.frame_step_group = None  # e_step grouping over frames (frame-space value path)
+        self.n_steps_f = None
         # (param generation, h1, h2) from revaluation; reused by train_step when
         # the parameters have not changed since the batch was built
         self.h_cache = None
@@ -99,17 +101,25 @@ class DeviceTrainBatch:
     def value_targets(self) -> np.ndarray:
         return self._get("ret", lambda: self.ret.double().cpu().numpy())
 
-    def ensure_groupings(self, n_steps: int, bad_count, factorized: bool = True) -> None:
+    def ensure_groupings(self, n_steps: int, bad_count, factorized: bool = True,
+                         frame_space: bool = False) -> None:
         """Stable key sorts for the deterministic scatter-adds (fixed per batch):
         (prev token, chunk position) for the factorized head, prev token for the
-        materialized head, step index for the value head's e_step."""
+        materialized head, step index for the value head's e_step (over
+        transitions, or over all frames when the value backward runs in frame
+        space)."""
         N, K, A = self.n_transitions, self.chunk_len, self.n_actions
         if factorized and self.pk_group is None:
             self.pk_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A, with_pos=True),
                                          (A + 1) * K)
         if not factorized and self.prev_group is None:
             self.prev_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A), A + 1)
-        if self.step_group is None or self.n_steps != n_steps:
+        if frame_space:
+            if self.frame_step_group is None or self.n_steps_f != n_steps:
+                keys = ops.step_keys(self.frame_steps, None, self.n_frames, n_steps, bad_count)
+                self.frame_step_group = ops.Grouping(keys, n_steps)
+                self.n_steps_f = n_steps
+        elif self.step_group is None or self.n_steps != n_steps:
             keys = ops.step_keys(self.frame_steps, self.frame_of, N, n_steps, bad_count)
             self.step_group = ops.Grouping(keys, n_steps)
             self.n_steps = n_steps

@@ -51,7 +51,8 @@ constexpr int kConvWarp0 = 2, kConvWarps = 4, kConv = kConvWarps * 32;
 constexpr int kEpiWarp0 = 6, kEpiWarps = 4;
 constexpr int kMaxRaw = 12;                // raw (TMA) ring slots
 constexpr int kNL = 2;                     // lo ring slots
-constexpr size_t kSmemBudget = 225 * 1024;
+constexpr size_t kSmemBudget = 225 * 1024;  // dynamic shared memory (wgrad)
+constexpr size_t kRowsBudget = 219 * 1024;  // tc_rows also holds ~6 KB of static smem
 constexpr uint32_t kTile = BM * BK * 4;    // one 128 x 32 fp32 tile (16 KB)
 constexpr int kFlushRows = 512;            // wgrad: TMEM flush period (rows)
 
@@ -237,6 +238,7 @@ struct Ring {
 // double-buffered TMEM accumulators (MMA -> epilogue).
 struct Bars {
   uint64_t raw_full[kMaxRaw], raw_empty[kMaxRaw], lo_full[kNL], lo_empty[kNL], tfull[2], tempty[2];
+  uint64_t hbar[kEpiWarps][2];  // dtanh epilogue: per-warp H box loads
 };
 
 __device__ __forceinline__ void init_bars(Bars& b, int nraw) {
@@ -252,6 +254,10 @@ __device__ __forceinline__ void init_bars(Bars& b, int nraw) {
     mbar_init(&b.tfull[s], 1);
     mbar_init(&b.tempty[s], kEpiWarps);
   }
+  for (int w = 0; w < kEpiWarps; ++w) {
+    mbar_init(&b.hbar[w][0], 1);
+    mbar_init(&b.hbar[w][1], 1);
+  }
   fence_mbar_init();
 }
 
@@ -265,16 +271,19 @@ struct RowArgs {
   int64_t M, ntiles, ldw, ldy;
   int K, N, Npad, kblocks, last_ksteps, concat;
   int w_trans, act_tanh, accumulate, y_vec, nraw, tma_store, nstg, has_bias;
+  int dtanh;          // Y = (X.W^T) * (1 - H^2), per-CTA column sums of Y into col_part
+  float* col_part;    // [gridDim.x][N]
   uint32_t tmem_cols, acc_cols;
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
 tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
-               RowArgs p) {
+               const __grid_constant__ CUtensorMap hmap, RowArgs p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ Bars bars;
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float s_bias[256];
+  __shared__ float s_csum[kEpiWarps][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Npad = p.Npad;
   if (smem_u32(smem) & 1023) __trap();  // SWIZZLE_128B atoms need 1 KB alignment
@@ -380,10 +389,15 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     }
   } else {
     // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows, 32
-    // columns at a time; rows go out through a swizzled staging box + TMA store
-    const int q = warp & 3;
-    unsigned char* stg0 = staging + (size_t)(warp - kEpiWarp0) * p.nstg * 4096;
+    // columns at a time; rows go out through a swizzled staging box + TMA store.
+    // dtanh: the box is first filled with the matching H box by TMA, read back
+    // (same swizzle), overwritten with y = acc (1 - h^2), stored; column sums of
+    // y are read column-wise from the box (conflict-free) into lane registers.
+    const int q = warp & 3, ew = warp - kEpiWarp0;
+    unsigned char* stg0 = staging + (size_t)ew * p.nstg * 4096;
     int sb = 0;
+    unsigned hph = 0;  // per-box H barrier phases
+    for (int c = lane; c < 256; c += 32) s_csum[ew][c] = 0.f;  // dtanh column sums
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int b = (int)(t & 1);
       mbar_wait(&bars.tfull[b], (unsigned)(t >> 1) & 1u);
@@ -391,7 +405,17 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
       const int64_t row0 = (blockIdx.x + t * gridDim.x) * BM + q * 32;
       const int64_t row = row0 + lane;
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)b * p.acc_cols;
+#pragma unroll 1
       for (int c0 = 0; c0 < Npad; c0 += 32) {
+        unsigned char* stg = stg0 + sb * 4096;
+        if (p.tma_store) {
+          if (lane == 0) tma_store_wait_read();  // this box's previous store has read it
+          __syncwarp();
+          if (p.dtanh && lane == 0) {
+            mbar_expect_tx(&bars.hbar[ew][sb], 4096);
+            tma_load_2d(stg, &hmap, c0, (int)row0, &bars.hbar[ew][sb]);
+          }
+        }
         uint32_t r[32];
         float v[32];
         tmem_ld32(tb + c0, r);
@@ -419,9 +443,22 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
           for (int j = 0; j < 32; ++j) v[j] = fast_tanh(v[j]);
         }
         if (p.tma_store) {
-          unsigned char* stg = stg0 + sb * 4096;
-          if (lane == 0) tma_store_wait_read();  // this box's previous store has read it
-          __syncwarp();
+          if (p.dtanh) {
+            mbar_wait(&bars.hbar[ew][sb], (hph >> sb) & 1u);
+            hph ^= 1u << sb;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 h = *reinterpret_cast<const float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16));
+              v[4 * j] *= 1.f - h.x * h.x;
+              v[4 * j + 1] *= 1.f - h.y * h.y;
+              v[4 * j + 2] *= 1.f - h.z * h.z;
+              v[4 * j + 3] *= 1.f - h.w * h.w;
+            }
+            if (row >= p.M) {  // rows past M (zero-filled H) must not enter the sums
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) =
@@ -429,6 +466,12 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) tma_store_2d(&ymap, c0, (int)row0, stg);
+          if (p.dtanh) {  // column c0 + lane of this box: 32 rows, fixed order
+            float cs = 0.f;
+            for (int rr = 0; rr < 32; ++rr)
+              cs += *reinterpret_cast<const float*>(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7)) * 16) + (lane & 3) * 4));
+            s_csum[ew][c0 + lane] += cs;  // lane-owned slot
+          }
           if (++sb == p.nstg) sb = 0;
         } else if (row < p.M) {
           float* out = p.Y + row * p.ldy;
@@ -446,6 +489,13 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if (p.dtanh) {  // the CTA's column sums, epilogue warps in fixed order
+    for (int c = threadIdx.x; c < p.N; c += kThreads) {
+      float a = 0.f;
+      for (int w = 0; w < kEpiWarps; ++w) a += s_csum[w][c];
+      p.col_part[(int64_t)blockIdx.x * p.N + c] = a;
+    }
+  }
   if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
 }
 
@@ -738,12 +788,13 @@ int make_map3(CUtensorMap* map, const float* base, int64_t rows, int slabs, int6
 
 int launch_rows(const float* X, const float* W, float* Y, const float* bias, int64_t M, int64_t K,
                 int N, int64_t ldx, int64_t ldw, int64_t ldy, int w_trans, int act_tanh,
-                int accumulate, cudaStream_t st) {
+                int accumulate, cudaStream_t st, const float* H = nullptr, int64_t ldh = 0,
+                float* col_part = nullptr) {
   const int Npad = (N + 31) / 32 * 32;  // the epilogue drains 32 columns at a time
   const int kblocks = (int)ceil_div(K, BK);
   const size_t wbytes = (size_t)kblocks * Npad * BK * 4 * 2;
   const size_t fixed = (size_t)kNL * kTile + (size_t)kEpiWarps * 4096;  // lo ring + 1 staging box
-  if (wbytes + fixed + 3 * kTile > kSmemBudget && N > 32) {
+  if (wbytes + fixed + 3 * kTile > kRowsBudget && N > 32 && !H) {
     // resident [W_hi; W_lo] too large for a useful ring: split the output columns
     const int n1 = (N / 2 + 31) / 32 * 32;
     const float* W2 = w_trans ? W + n1 : W + (int64_t)n1 * ldw;
@@ -752,7 +803,7 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
     return launch_rows(X, W2, Y + n1, bias ? bias + n1 : nullptr, M, K, N - n1, ldx, ldw, ldy,
                        w_trans, act_tanh, accumulate, st);
   }
-  if (wbytes + fixed + 2 * kTile > kSmemBudget)
+  if (wbytes + fixed + 2 * kTile > kRowsBudget)
     return fail(kDimension, "tc_gemm: resident weight %d x %lld too large", N, (long long)K);
   CUtensorMap xmap, ymap;
   if (int e = make_map(&xmap, X, M, K, ldx, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B)) return e;
@@ -773,21 +824,29 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   } else {
     ymap = xmap;  // unused
   }
+  CUtensorMap hmap = xmap;  // unused unless dtanh
+  p.dtanh = H ? 1 : 0;
+  p.col_part = col_part;
+  if (H) {
+    if (!p.tma_store || !col_part || act_tanh || bias || N > 256)
+      return fail(kDimension, "tc_gemm dtanh: needs an aligned output, col_part, no bias/act");
+    if (int e = make_map(&hmap, H, M, N, ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return e;
+  }
   p.ntiles = ceil_div(M, BM);
   p.acc_cols = p.concat ? 2 * Npad : Npad;
   p.tmem_cols = tmem_cols_for(2 * (int)p.acc_cols);
   // staging: two boxes per epilogue warp when the raw ring keeps >= 6 slots
   p.nstg = p.tma_store ? 2 : 0;
-  if (p.tma_store && wbytes + (size_t)kNL * kTile + (size_t)kEpiWarps * 2 * 4096 + 6 * kTile > kSmemBudget)
+  if (p.tma_store && wbytes + (size_t)kNL * kTile + (size_t)kEpiWarps * 2 * 4096 + 6 * kTile > kRowsBudget)
     p.nstg = 1;
   const size_t sbytes = (size_t)kEpiWarps * p.nstg * 4096;
-  p.nraw = (int)std::min<size_t>(kMaxRaw, (kSmemBudget - wbytes - sbytes - kNL * kTile) / kTile);
+  p.nraw = (int)std::min<size_t>(kMaxRaw, (kRowsBudget - wbytes - sbytes - kNL * kTile) / kTile);
   const size_t smem = wbytes + (size_t)(p.nraw + kNL) * kTile + sbytes;
   cudaError_t e = cudaFuncSetAttribute(tc_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return fail(kCuda, "tc_rows smem: %s", cudaGetErrorString(e));
   const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
-  tc_rows_kernel<<<grid, kThreads, smem, st>>>(xmap, ymap, p);
+  tc_rows_kernel<<<grid, kThreads, smem, st>>>(xmap, ymap, hmap, p);
   return post_launch("tc_rows_kernel");
 }
 
@@ -879,6 +938,25 @@ int launch_wgrad(const float* dY, const float* X, float* C, int64_t F, int n, in
 using namespace accel;
 
 extern "C" int accel_tc_sm_count(void) { return sm_count(); }
+
+extern "C" int accel_tc_rows_grid(int64_t M) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(M, BM), sm_count()));
+}
+
+// C[M, N] = (A[M, K] . B^T) * (1 - H[M, N]^2) -- a GEMM fused with the tanh
+// derivative of its output rows -- and col_part[accel_tc_rows_grid(M)][N] = the
+// per-CTA column sums of C (fixed order; the caller reduces them).
+extern "C" int accel_tc_gemm_dtanh(const float* A, const float* B, float* C, const float* H,
+                                   float* col_part, int64_t M, int64_t K, int N, int64_t lda,
+                                   int64_t ldb, int64_t ldc, int64_t ldh, int b_trans,
+                                   void* stream) {
+  if (M < 0 || K < 1 || N < 1 || N > 256) return fail(kDimension, "tc_gemm_dtanh: bad sizes");
+  if (M == 0) return kOk;
+  if (!A || !B || !C || !H || !col_part) return fail(kDimension, "tc_gemm_dtanh: NULL buffer");
+  if (K > INT32_MAX || M > INT32_MAX) return fail(kDimension, "tc_gemm_dtanh: too large");
+  return launch_rows(A, B, C, nullptr, M, K, N, lda, ldb, ldc, b_trans, 0, 0, as_stream(stream), H,
+                     ldh, col_part);
+}
 
 // C[M, N] = act(A . B^T + bias) (+ C if accumulate).  a_trans: A stored [K, M];
 // b_trans: B stored [K, N].  a_trans && b_trans (weight gradient, reduction over

@@ -227,7 +227,8 @@ value_attn_grad4_kernel(const float* __restrict__ dU, const float* __restrict__ 
 
 // part layout per block: [dw1v (H) | db0v (H) | db1v (1)]; dpart: [sum err^2, non-finite v]
 __global__ void __launch_bounds__(kThreads)
-value_head_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
+value_head_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame,
+                  const float* __restrict__ b0v,
                   const float* __restrict__ w1v, const float* __restrict__ b1v, int64_t R, int H,
                   const float* __restrict__ targets, float lambda_v, double inv_n,
                   float* __restrict__ values_out, float* __restrict__ part,
@@ -251,10 +252,11 @@ value_head_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
   for (int64_t r = (int64_t)blockIdx.x * kWarps + warp; r < R; r += stride) {
     float m[kMaxHPL];
     float acc = 0.f;
+    const int64_t zr = row_frame ? __ldg(row_frame + r) : r;
 #pragma unroll
     for (int j = 0; j < kMaxHPL; ++j) {
       const int h = lane + 32 * j;
-      m[j] = h < H ? tanhf(zm[r * H + h] + bz[j]) : 0.f;
+      m[j] = h < H ? tanhf(zm[zr * H + h] + bz[j]) : 0.f;
       acc = fmaf(w1[j], m[j], acc);
     }
     const float v = warp_sum(acc) + bias1;
@@ -270,7 +272,7 @@ value_head_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
         const int h = lane + 32 * j;
         if (h < H) {
           const float g = dv * w1[j] * (1.f - m[j] * m[j]);
-          zm[r * H + h] = g;
+          zm[zr * H + h] = g;
           gw1[j] = fmaf(dv, m[j], gw1[j]);
           gb0[j] += g;
         }
@@ -385,7 +387,8 @@ value_attn_wgrad_kernel(const float* __restrict__ de, const float* __restrict__ 
 // the column sums stay in registers, tanh uses one ex2 + one fast divide.
 template <int LPR, int CPL>
 __global__ void __launch_bounds__(kThreads)
-value_head4_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
+value_head4_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame,
+                   const float* __restrict__ b0v,
                    const float* __restrict__ w1v, const float* __restrict__ b1v, int64_t R,
                    const float* __restrict__ targets, float lambda_v, double inv_n,
                    float* __restrict__ values_out, float* __restrict__ part,
@@ -411,7 +414,8 @@ value_head4_kernel(float* __restrict__ zm, const float* __restrict__ b0v,
     const bool act = r < R;
     float m[CPL];
     float acc = 0.f;
-    float4* row = reinterpret_cast<float4*>(zm + r * H + lc * CPL);
+    const int64_t zr = act && row_frame ? __ldg(row_frame + r) : r;
+    float4* row = reinterpret_cast<float4*>(zm + zr * H + lc * CPL);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const float4 z = act ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -570,7 +574,8 @@ extern "C" int accel_value_pool(const float* h1, const float* h2, const int32_t*
   return post_launch("value_pool_kernel");
 }
 
-extern "C" int accel_value_head(float* zm, const float* b0v, const float* w1v, const float* b1v,
+extern "C" int accel_value_head(float* zm, const int32_t* row_frame, const float* b0v,
+                                const float* w1v, const float* b1v,
                                 int64_t R, int H, const float* targets, double lambda_v,
                                 double n_global, float* values_out, float* part, double* dpart,
                                 int grid, void* stream) {
@@ -583,17 +588,17 @@ extern "C" int accel_value_head(float* zm, const float* b0v, const float* w1v, c
   cudaStream_t st = as_stream(stream);
   if ((reinterpret_cast<uintptr_t>(zm) & 15) == 0 && (H == 32 || H == 64 || H == 128)) {
     if (H == 32)
-      value_head4_kernel<8, 4><<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, targets,
+      value_head4_kernel<8, 4><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets,
                                                           (float)lambda_v, inv_n, values_out, part, dpart);
     else if (H == 64)
-      value_head4_kernel<8, 8><<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, targets,
+      value_head4_kernel<8, 8><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets,
                                                           (float)lambda_v, inv_n, values_out, part, dpart);
     else
-      value_head4_kernel<16, 8><<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, targets,
+      value_head4_kernel<16, 8><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets,
                                                            (float)lambda_v, inv_n, values_out, part, dpart);
     return post_launch("value_head4_kernel");
   }
-  value_head_kernel<<<grid, kThreads, 0, st>>>(zm, b0v, w1v, b1v, R, H, targets, (float)lambda_v,
+  value_head_kernel<<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, H, targets, (float)lambda_v,
                                                inv_n, values_out, part, dpart);
   return post_launch("value_head_kernel");
 }

@@ -257,10 +257,14 @@ def value_pool(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, 
               int(grid), _stream())
 
 
-def value_head(zm, b0v, w1v, b1v, targets, lambda_v, n_global, values_out, part, dpart, grid):
-    _lib.call("accel_value_head", _p(zm), _p(b0v), _p(w1v), _p(b1v), zm.shape[0], zm.shape[1],
-              _p(targets), float(lambda_v), float(n_global), _p(values_out), _p(part), _p(dpart),
-              int(grid), _stream())
+def value_head(zm, b0v, w1v, b1v, targets, lambda_v, n_global, values_out, part, dpart, grid,
+               row_frame=None, rows=None):
+    """rows R (default zm rows); row_frame: zm row of each of the R rows (the
+    dzm rows are written back there)."""
+    R = zm.shape[0] if rows is None else int(rows)
+    _lib.call("accel_value_head", _p(zm), _p(row_frame), _p(b0v), _p(w1v), _p(b1v), R,
+              zm.shape[1], _p(targets), float(lambda_v), float(n_global), _p(values_out),
+              _p(part), _p(dpart), int(grid), _stream())
 
 
 def value_attn_grad(dU, h1, h2, row_frame, alpha, de, part, grid):
@@ -395,6 +399,34 @@ def tc_matmul_nn(x, w, out=None, accumulate=False):
     _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), None, M, K, N, x.stride(0), w.stride(0),
               out.stride(0), 0, 1, 0, int(accumulate), 1, _stream())
     return out
+
+
+def tc_rows_grid(M: int) -> int:
+    return int(_lib.lib().accel_tc_rows_grid(int(M)))
+
+
+def _aligned_rows(t) -> bool:
+    return t.stride(1) == 1 and t.stride(0) % 4 == 0 and t.data_ptr() % 16 == 0
+
+
+def tc_matmul_nn_dtanh(x, w, h, out, part_fn):
+    """out = (x . w) * (1 - h^2) with per-CTA column sums of out; returns
+    (out, col_part, n_parts).  part_fn(n) -> f32[n, N] buffer.  Falls back to
+    the unfused product + accel_tanh_grad_colsum at unaligned widths."""
+    x = pitched(x)
+    M, K = x.shape
+    N = w.shape[1]
+    if N <= 256 and _aligned_rows(out) and _aligned_rows(h):
+        n = tc_rows_grid(M)
+        part = part_fn(n)
+        _lib.call("accel_tc_gemm_dtanh", _p(x), _p(w), _p(out), _p(h), _p(part), M, K, N,
+                  x.stride(0), w.stride(0), out.stride(0), h.stride(0), 1, _stream())
+        return out, part, n
+    tc_matmul_nn(x, w, out)
+    n = rows_grid(M)
+    part = part_fn(n)
+    tanh_grad_colsum(out, h, part, n)
+    return out, part, n
 
 
 def tc_sm_count() -> int:

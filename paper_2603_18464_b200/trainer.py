@@ -432,15 +432,19 @@ class Trainer:
         F = frames.shape[0]
         d = self.dims
         h1, h2 = self._backbone(frames, None if keep else "rv.")
-        self._last_h = (h1, h2) if keep else None
-        U = self.scratch.get("rv.U", (F, d.hidden))
-        alpha = self.scratch.get("rv.alpha", (F, 2))
+        fresh = lambda shape: torch.empty(*shape, dtype=F32, device=self.device)
+        U = fresh((F, d.hidden)) if keep else self.scratch.get("rv.U", (F, d.hidden))
+        alpha = fresh((F, 2)) if keep else self.scratch.get("rv.alpha", (F, 2))
         g = ops.warp_grid(F)
         ops.value_pool(h1, h2, None, steps, F, d.n_steps, P["w_attn"], P["b_attn"], P["e_step"], U,
                        alpha, bad_part, g)
-        zm = ops.tc_linear(U, P["w0v"], self.scratch.get("rv.zm", (F, d.mlp_hidden)))
+        zm = ops.tc_linear(U, P["w0v"], fresh((F, d.mlp_hidden)) if keep
+                           else self.scratch.get("rv.zm", (F, d.mlp_hidden)))
         ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], None, 0.0, 0.0, out, None, None,
                        ops.warp_grid(F))
+        # keep: the train step under the same parameters reuses the backbone and
+        # the value head's pooling / first layer (frame space)
+        self._last_h = (h1, h2, U, alpha, zm) if keep else None
         return g
 
     def recompute_values(self, traj) -> np.ndarray:
@@ -532,7 +536,8 @@ class Trainer:
             norm_mean=0.0, norm_std=0.0, norm_count=N,
             shard_sizes=_array_split_sizes(N, cfg.k_shards),
             behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
-        batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized)
+        batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized,
+                               frame_space=h_cache is not None)
         batch.h_cache = h_cache
         # frame row of each trajectory's bootstrap observation (t = T)
         batch.boot_rows = b["traj_off"][1:] + torch.arange(n, dtype=torch.int64, device=dev)
@@ -627,7 +632,14 @@ class Trainer:
         cnt = S.get("st.cnt", (4,), torch.int32)
         cnt.zero_()
         fact = self.factorized
-        batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=fact)
+        hc = getattr(batch, "h_cache", None)
+        vcache = None
+        if hc is not None and hc[0] == self._param_gen:
+            h1, h2 = hc[1], hc[2]  # revaluation ran under these exact parameters
+            vcache = hc[3:]        # (U, alpha, zm) over all frames
+            batch.h_cache = None   # consumed: the value backward overwrites zm in place
+        batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=fact,
+                               frame_space=vcache is not None)
         if self.comm is None:
             N_glob, M_glob = N, M
         elif getattr(batch, "global_n", None) is not None:
@@ -639,10 +651,7 @@ class Trainer:
         loss_sums = S.get("st.lsum", (8,), F64)
         loss_max = S.get("st.lmax", (2,), F64)
 
-        hc = getattr(batch, "h_cache", None)
-        if hc is not None and hc[0] == self._param_gen:
-            h1, h2 = hc[1], hc[2]  # revaluation ran under these exact parameters
-        else:
+        if vcache is None:
             h1, h2 = self._backbone(batch.frames, "st.")
         if fact:
             # logits = H2W[frame] + EP[prev] + PP[k] + b: three small GEMMs, no [M, A] logits
@@ -701,25 +710,43 @@ class Trainer:
 
         # value head (hiddens detached)
         gw = ops.warp_grid(N)
-        U = S.get("st.U", (N, D))
-        alpha = S.get("st.alpha", (N, 2))
-        vbad_part = S.get("st.vbad", (gw, 2), F64)
-        ops.value_pool(h1, h2, batch.frame_of, batch.frame_steps, N, d.n_steps, P["w_attn"],
-                       P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
-        zm = ops.tc_linear(U, P["w0v"], S.get("st.zm", (N, H)))
         vpart = S.get("st.vpart", (gw, 2 * H + 1))
         vdpart = S.get("st.vdpart", (gw, 2), F64)
-        ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
-                       vpart, vdpart, gw)
+        if vcache is not None:
+            # frame space: the revaluation pass already pooled (U, alpha) and ran the
+            # first layer (zm) on every frame; the loss covers the transition
+            # frames, bootstrap rows carry zero gradient
+            U, alpha, zm = vcache
+            ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
+                           vpart, vdpart, gw, row_frame=batch.frame_of, rows=N)
+            if F != N:
+                zm.index_fill_(0, batch.boot_rows, 0.0)
+            R, row_frame, step_group = F, None, batch.frame_step_group
+            ga = ops.warp_grid(F)
+            vbad_part = S.get("st.vbad", (1, 2), F64)
+            vbad_part.zero_()  # attention / step checks ran in the revaluation pass
+            nbad = 1
+        else:
+            U = S.get("st.U", (N, D))
+            alpha = S.get("st.alpha", (N, 2))
+            vbad_part = S.get("st.vbad", (gw, 2), F64)
+            nbad = gw
+            ops.value_pool(h1, h2, batch.frame_of, batch.frame_steps, N, d.n_steps, P["w_attn"],
+                           P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
+            zm = ops.tc_linear(U, P["w0v"], S.get("st.zm", (N, H)))
+            ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
+                           vpart, vdpart, gw)
+            R, row_frame, step_group = N, batch.frame_of, batch.step_group
+            ga = gw
         segs = [self._wgrad(zm, U, G["w0v"], "w0v")]  # dzm^T U
-        dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (N, D)))
-        de = S.get("st.de", (N, 2))
-        battn_part = S.get("st.battn", (gw,))
-        ops.value_attn_grad(dU, h1, h2, batch.frame_of, alpha, de, battn_part, gw)
-        gr = ops.rows_grid(N)
+        dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (R, D)))
+        de = S.get("st.de", (R, 2))
+        battn_part = S.get("st.battn", (ga,))
+        ops.value_attn_grad(dU, h1, h2, row_frame, alpha, de, battn_part, ga)
+        gr = ops.rows_grid(R)
         wattn_part = S.get("st.wattn", (gr, D))
-        ops.value_attn_wgrad(de, h1, h2, batch.frame_of, N, wattn_part, gr)
-        batch.step_group.rows_sum(dU, G["e_step"])
+        ops.value_attn_wgrad(de, h1, h2, row_frame, R, wattn_part, gr)
+        step_group.rows_sum(dU, G["e_step"])
 
         # policy backward
         if fact:
@@ -743,10 +770,10 @@ class Trainer:
             segs.append(seg)
             _mm(dprev, P["w_head"], G["e_prev"])
             _mm(dpos, P["w_head"], G["e_pos"])
-            dz2 = ops.tc_matmul_nn(g_frame, P["w_head"], S.get("st.dz2", (F, D)))  # dh2
-            gd = ops.rows_grid(F)
-            db1_part = S.get("st.db1", (gd, D))
-            ops.tanh_grad_colsum(dz2, h2, db1_part, gd)
+            # dpre2 = (G W_head) (1 - h2^2) and its column sums (db1), one kernel
+            dz2, db1_part, gd = ops.tc_matmul_nn_dtanh(
+                g_frame, P["w_head"], h2, S.get("st.dz2", (F, D)),
+                lambda n: S.get("st.db1", (n, D)))
             segs.append((dpos, G["b_head"], K, A, A))
         else:
             segs.append(self._wgrad(dlogits, c, G["w_head"], "w_head"))
@@ -761,10 +788,9 @@ class Trainer:
             batch.prev_group.rows_sum(dc, G["e_prev"])
             segs += [(dbias_part, G["b_head"], gl, A, A), (pos_part, G["e_pos"], gd, K * D, K * D)]
         segs.append(self._wgrad(dz2, h1, G["w1"], "w1"))
-        dh1 = ops.tc_matmul_nn(dz2, P["w1"], S.get("st.dh1", (F, D)))
-        gt = ops.rows_grid(F)
-        db0_part = S.get("st.db0", (gt, D))
-        ops.tanh_grad_colsum(dh1, h1, db0_part, gt)
+        # dpre1 = (dpre2 W1) (1 - h1^2) and its column sums (db0)
+        dh1, db0_part, gt = ops.tc_matmul_nn_dtanh(dz2, P["w1"], h1, S.get("st.dh1", (F, D)),
+                                                   lambda n: S.get("st.db0", (n, D)))
         segs.append(self._wgrad(dh1, batch.frames, G["w0"], "w0"))
 
         ops.reduce_segments(segs + [
@@ -773,13 +799,13 @@ class Trainer:
             (vpart, G["w1v"], gw, H, 2 * H + 1),
             (vpart[:, H:], G["b0v"], gw, H, 2 * H + 1),
             (vpart[:, 2 * H:], G["b1v"], gw, 1, 2 * H + 1),
-            (battn_part, G["b_attn"], gw, 1, 1),
+            (battn_part, G["b_attn"], ga, 1, 1),
             (wattn_part, G["w_attn"], gr, D, D),
         ])
         value_sums = S.get("st.vsum", (2,), F64)
         attn_bad = S.get("st.abad", (2,), F64)
         ops.reduce_f64(vdpart, gw, 2, 0, value_sums)
-        ops.reduce_f64(vbad_part, gw, 2, 0, attn_bad)
+        ops.reduce_f64(vbad_part, nbad, 2, 0, attn_bad)
         ops.count_nonfinite(self.params.g, cnt[0:1])
         if self.comm is not None:
             # C5 scalars in one fp64 all-reduce; local grads all finite on every

@@ -54,3 +54,22 @@ def test_tc_wgrad_matches_fp64(F, n, k, slices):
     out2 = torch.empty_like(out)
     ops.tc_wgrad(dy, x, out2, kslices=slices)
     assert torch.equal(out, out2)  # deterministic
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,K,N", [(5000, 256, 64), (3001, 64, 64), (700, 64, 32)])
+def test_tc_dtanh_fused_epilogue(M, K, N):
+    """(x.w) * (1 - h^2) and its column sums in the GEMM epilogue (dpre = dh (1 - h^2))."""
+    from paper_2603_18464_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    w = torch.randn(K, N, device="cuda", generator=g) * 0.1
+    h = torch.tanh(torch.randn(M, N, device="cuda", generator=g))
+    out = torch.empty(M, N, device="cuda")
+    parts = {}
+    y, part, n = ops.tc_matmul_nn_dtanh(x, w, h, out, lambda k: parts.setdefault(
+        "p", torch.empty(k, N, device="cuda")))
+    ref = (x.double() @ w.double()) * (1 - h.double() ** 2)
+    assert rel_err(y, ref) < 4e-6
+    colsum = part[:n].double().sum(0)
+    assert float((colsum - ref.sum(0)).abs().max()) < 1e-4 * float(ref.abs().sum(0).max())
