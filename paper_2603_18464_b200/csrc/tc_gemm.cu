@@ -52,7 +52,7 @@ constexpr int kEpiWarp0 = 6, kEpiWarps = 4;
 constexpr int kMaxRaw = 12;                // raw (TMA) ring slots
 constexpr int kNL = 2;                     // lo ring slots
 constexpr size_t kSmemBudget = 225 * 1024;  // dynamic shared memory (wgrad)
-constexpr size_t kRowsBudget = 219 * 1024;  // tc_rows also holds ~6 KB of static smem
+constexpr size_t kRowsBudget = 224 * 1024;  // tc_rows also holds ~2 KB of static smem (<= 227 KB)
 constexpr uint32_t kTile = BM * BK * 4;    // one 128 x 32 fp32 tile (16 KB)
 constexpr int kFlushRows = 512;            // wgrad: TMEM flush period (rows)
 
@@ -283,7 +283,6 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
   __shared__ Bars bars;
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float s_bias[256];
-  __shared__ float s_csum[kEpiWarps][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Npad = p.Npad;
   if (smem_u32(smem) & 1023) __trap();  // SWIZZLE_128B atoms need 1 KB alignment
@@ -292,6 +291,8 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
   unsigned char* raw_ring = smem + (size_t)p.kblocks * wblk;
   unsigned char* lo_ring = raw_ring + (size_t)p.nraw * kTile;
   unsigned char* staging = lo_ring + (size_t)kNL * kTile;  // epilogue: nstg boxes per warp
+  // dtanh only: per-epilogue-warp column sums [kEpiWarps][256] after the staging boxes
+  float (*s_csum)[256] = reinterpret_cast<float (*)[256]>(staging + (size_t)kEpiWarps * p.nstg * 4096);
 
   // W resident: split once, K-major, [hi rows | lo rows] per K block
   const int Kpad = p.kblocks * BK;
@@ -397,7 +398,20 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     unsigned char* stg0 = staging + (size_t)ew * p.nstg * 4096;
     int sb = 0;
     unsigned hph = 0;  // per-box H barrier phases
-    for (int c = lane; c < 256; c += 32) s_csum[ew][c] = 0.f;  // dtanh column sums
+    if (p.dtanh)
+      for (int c = lane; c < 256; c += 32) s_csum[ew][c] = 0.f;  // dtanh column sums
+    // dtanh with all of a tile's chunks fitting the boxes: H boxes of the next
+    // tile are loaded as soon as this tile's stores have read the boxes, so the
+    // load latency hides behind the MMAs instead of stalling every chunk
+    const bool hpre = p.dtanh && Npad == 32 * p.nstg;
+    auto load_h = [&](int64_t tt) {
+      const int64_t r0h = (blockIdx.x + tt * gridDim.x) * BM + q * 32;
+      for (int c = 0; c < p.nstg; ++c) {
+        mbar_expect_tx(&bars.hbar[ew][c], 4096);
+        tma_load_2d(stg0 + c * 4096, &hmap, c * 32, (int)r0h, &bars.hbar[ew][c]);
+      }
+    };
+    if (hpre && my_tiles > 0 && lane == 0) load_h(0);
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int b = (int)(t & 1);
       mbar_wait(&bars.tfull[b], (unsigned)(t >> 1) & 1u);
@@ -409,9 +423,9 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
       for (int c0 = 0; c0 < Npad; c0 += 32) {
         unsigned char* stg = stg0 + sb * 4096;
         if (p.tma_store) {
-          if (lane == 0) tma_store_wait_read();  // this box's previous store has read it
+          if (lane == 0 && !hpre) tma_store_wait_read();  // this box's previous store has read it
           __syncwarp();
-          if (p.dtanh && lane == 0) {
+          if (p.dtanh && !hpre && lane == 0) {
             mbar_expect_tx(&bars.hbar[ew][sb], 4096);
             tma_load_2d(stg, &hmap, c0, (int)row0, &bars.hbar[ew][sb]);
           }
@@ -483,6 +497,10 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.tempty[b]);
+      if (hpre && t + 1 < my_tiles && lane == 0) {
+        tma_store_wait_read();  // every box's store has read it
+        load_h(t + 1);
+      }
     }
     if (p.tma_store && lane == 0) tma_store_wait_all();
   }
@@ -794,7 +812,7 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   const int kblocks = (int)ceil_div(K, BK);
   const size_t wbytes = (size_t)kblocks * Npad * BK * 4 * 2;
   const size_t fixed = (size_t)kNL * kTile + (size_t)kEpiWarps * 4096;  // lo ring + 1 staging box
-  if (wbytes + fixed + 3 * kTile > kRowsBudget && N > 32 && !H) {
+  if (wbytes + fixed + 2 * kTile > kRowsBudget && N > 32 && !H) {
     // resident [W_hi; W_lo] too large for a useful ring: split the output columns
     const int n1 = (N / 2 + 31) / 32 * 32;
     const float* W2 = w_trans ? W + n1 : W + (int64_t)n1 * ldw;
@@ -839,7 +857,7 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   p.nstg = p.tma_store ? 2 : 0;
   if (p.tma_store && wbytes + (size_t)kNL * kTile + (size_t)kEpiWarps * 2 * 4096 + 6 * kTile > kRowsBudget)
     p.nstg = 1;
-  const size_t sbytes = (size_t)kEpiWarps * p.nstg * 4096;
+  const size_t sbytes = (size_t)kEpiWarps * p.nstg * 4096 + (H ? (size_t)kEpiWarps * 256 * 4 : 0);
   p.nraw = (int)std::min<size_t>(kMaxRaw, (kRowsBudget - wbytes - sbytes - kNL * kTile) / kTile);
   const size_t smem = wbytes + (size_t)(p.nraw + kNL) * kTile + sbytes;
   cudaError_t e = cudaFuncSetAttribute(tc_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -416,7 +416,9 @@ def tc_matmul_nn_dtanh(x, w, h, out, part_fn):
     x = pitched(x)
     M, K = x.shape
     N = w.shape[1]
-    if N <= 256 and _aligned_rows(out) and _aligned_rows(h):
+    # fused for short K (the resident [W_hi; W_lo] leaves room for two staging boxes
+    # per epilogue warp); at K = 256 the unfused pair is faster
+    if N <= 256 and K <= 128 and _aligned_rows(out) and _aligned_rows(h):
         n = tc_rows_grid(M)
         part = part_fn(n)
         _lib.call("accel_tc_gemm_dtanh", _p(x), _p(w), _p(out), _p(h), _p(part), M, K, N,
