@@ -284,6 +284,13 @@ int accel_tc_sm_count(void);
  *     fp32 partials (two per persistent CTA, kslices <= accel_tc_sm_count())
  *     for a fixed-order reduction by the caller; no bias/act/accumulate.
  * fp32 in/out, N <= 256, any strides. */
+/* accel_tc_gemm's row transform (a_trans = b_trans = 0) that also adds the
+ * number of non-finite elements of A to *nonfinite (u32, device): the frame
+ * finiteness check of build_train_batch (trainer.py:392-396) folded into the
+ * first layer's read of the frames. */
+int accel_tc_linear_checked(const float* A, const float* B, float* C, const float* bias,
+                            int64_t M, int64_t K, int N, int64_t lda, int64_t ldb, int64_t ldc,
+                            int act_tanh, unsigned* nonfinite, void* stream);
 /* Persistent-grid size of the row-transform kernel for M rows. */
 int accel_tc_rows_grid(int64_t M);
 /* C[M, N] = (A[M, K] . B^T) * (1 - H[M, N]^2) -- a backward product fused with

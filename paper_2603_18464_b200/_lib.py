@@ -67,6 +67,8 @@ _SIGNATURES = {
     "accel_adam": (c_int, [P, P, P, P, P, P, P, c_int64, c_int64, P, P, P, P, P]),
     "accel_tc_sm_count": (c_int, []),
     "accel_tc_rows_grid": (c_int, [c_int64]),
+    "accel_tc_linear_checked": (c_int, [P, P, P, P, c_int64, c_int64, c_int, c_int64, c_int64,
+                                        c_int64, c_int, P, P]),
     "accel_tc_gemm_dtanh": (c_int, [P, P, P, P, P, c_int64, c_int64, c_int, c_int64, c_int64,
                                     c_int64, c_int64, c_int, P]),
     "accel_tc_gemm": (c_int, [P, P, P, P, c_int64, c_int64, c_int, c_int64, c_int64, c_int64,

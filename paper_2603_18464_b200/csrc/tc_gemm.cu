@@ -221,6 +221,23 @@ __device__ __forceinline__ void convert_lo(const unsigned char* raw, unsigned ch
     *reinterpret_cast<float4*>(lo + i) = tf32_lo(*reinterpret_cast<const float4*>(raw + i));
 }
 
+__device__ __forceinline__ unsigned nonfinite4(float4 v) {
+  auto bad = [](float x) { return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u ? 1u : 0u; };
+  return bad(v.x) + bad(v.y) + bad(v.z) + bad(v.w);
+}
+
+// the same, also counting non-finite inputs (the streamed operand is read anyway)
+__device__ __forceinline__ unsigned convert_lo_count(const unsigned char* raw, unsigned char* lo,
+                                                     uint32_t bytes, int t) {
+  unsigned n = 0;
+  for (uint32_t i = (uint32_t)t * 16; i < bytes; i += kConv * 16) {
+    const float4 v = *reinterpret_cast<const float4*>(raw + i);
+    n += nonfinite4(v);
+    *reinterpret_cast<float4*>(lo + i) = tf32_lo(v);
+  }
+  return n;
+}
+
 // Pipeline state of one ring: slot index and mbarrier phase of the current stage.
 struct Ring {
   int slot = 0, n;
@@ -273,6 +290,7 @@ struct RowArgs {
   int w_trans, act_tanh, accumulate, y_vec, nraw, tma_store, nstg, has_bias;
   int dtanh;          // Y = (X.W^T) * (1 - H^2), per-CTA column sums of Y into col_part
   float* col_part;    // [gridDim.x][N]
+  unsigned* nonfinite;  // optional: += number of non-finite elements of X
   uint32_t tmem_cols, acc_cols;
 };
 
@@ -381,12 +399,21 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     // ---- converters
     const int t = threadIdx.x - kConvWarp0 * 32;
     Ring r(p.nraw), l(kNL);
+    unsigned nbad = 0;
     for (int64_t s = 0; s < total; ++s, r.next(), l.next()) {
       mbar_wait(&bars.raw_full[r.slot], r.ph);
       mbar_wait(&bars.lo_empty[l.slot], l.ph ^ 1u);
-      convert_lo(raw_ring + (size_t)r.slot * kTile, lo_ring + (size_t)l.slot * kTile, kTile, t);
+      if (p.nonfinite)  // (TMA zero-fills rows and columns past the matrix)
+        nbad += convert_lo_count(raw_ring + (size_t)r.slot * kTile, lo_ring + (size_t)l.slot * kTile,
+                                 kTile, t);
+      else
+        convert_lo(raw_ring + (size_t)r.slot * kTile, lo_ring + (size_t)l.slot * kTile, kTile, t);
       fence_proxy_async();
       mbar_arrive(&bars.lo_full[l.slot]);
+    }
+    if (p.nonfinite) {
+      nbad = __reduce_add_sync(0xffffffffu, nbad);
+      if (lane == 0 && nbad) atomicAdd(p.nonfinite, nbad);  // integer: order-independent
     }
   } else {
     // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows, 32
@@ -807,7 +834,7 @@ int make_map3(CUtensorMap* map, const float* base, int64_t rows, int slabs, int6
 int launch_rows(const float* X, const float* W, float* Y, const float* bias, int64_t M, int64_t K,
                 int N, int64_t ldx, int64_t ldw, int64_t ldy, int w_trans, int act_tanh,
                 int accumulate, cudaStream_t st, const float* H = nullptr, int64_t ldh = 0,
-                float* col_part = nullptr) {
+                float* col_part = nullptr, unsigned* nonfinite = nullptr) {
   const int Npad = (N + 31) / 32 * 32;  // the epilogue drains 32 columns at a time
   const int kblocks = (int)ceil_div(K, BK);
   const size_t wbytes = (size_t)kblocks * Npad * BK * 4 * 2;
@@ -816,7 +843,8 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
     // resident [W_hi; W_lo] too large for a useful ring: split the output columns
     const int n1 = (N / 2 + 31) / 32 * 32;
     const float* W2 = w_trans ? W + n1 : W + (int64_t)n1 * ldw;
-    if (int e = launch_rows(X, W, Y, bias, M, K, n1, ldx, ldw, ldy, w_trans, act_tanh, accumulate, st))
+    if (int e = launch_rows(X, W, Y, bias, M, K, n1, ldx, ldw, ldy, w_trans, act_tanh, accumulate, st,
+                            nullptr, 0, nullptr, nonfinite))
       return e;
     return launch_rows(X, W2, Y + n1, bias ? bias + n1 : nullptr, M, K, N - n1, ldx, ldw, ldy,
                        w_trans, act_tanh, accumulate, st);
@@ -845,6 +873,7 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   CUtensorMap hmap = xmap;  // unused unless dtanh
   p.dtanh = H ? 1 : 0;
   p.col_part = col_part;
+  p.nonfinite = nonfinite;
   if (H) {
     if (!p.tma_store || !col_part || act_tanh || bias || N > 256)
       return fail(kDimension, "tc_gemm dtanh: needs an aligned output, col_part, no bias/act");
@@ -956,6 +985,21 @@ int launch_wgrad(const float* dY, const float* X, float* C, int64_t F, int n, in
 using namespace accel;
 
 extern "C" int accel_tc_sm_count(void) { return sm_count(); }
+
+// accel_tc_gemm's row transform (a_trans = 0, B [N, K]) that also adds the
+// number of non-finite elements of A to *nonfinite (the frame check of
+// build_train_batch, trainer.py:392-396, folded into the first layer's read).
+extern "C" int accel_tc_linear_checked(const float* A, const float* B, float* C, const float* bias,
+                                       int64_t M, int64_t K, int N, int64_t lda, int64_t ldb,
+                                       int64_t ldc, int act_tanh, unsigned* nonfinite,
+                                       void* stream) {
+  if (M < 0 || K < 1 || N < 1 || N > 256) return fail(kDimension, "tc_linear_checked: bad sizes");
+  if (M == 0) return kOk;
+  if (!A || !B || !C || !nonfinite) return fail(kDimension, "tc_linear_checked: NULL buffer");
+  if (K > INT32_MAX || M > INT32_MAX) return fail(kDimension, "tc_linear_checked: too large");
+  return launch_rows(A, B, C, bias, M, K, N, lda, ldb, ldc, 0, act_tanh, 0, as_stream(stream),
+                     nullptr, 0, nullptr, nonfinite);
+}
 
 extern "C" int accel_tc_rows_grid(int64_t M) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(M, BM), sm_count()));

@@ -390,6 +390,17 @@ def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
     return out
 
 
+def tc_linear_checked(x, w, out, nonfinite, bias=None, tanh=False):
+    """tc_linear that also adds the count of non-finite elements of x to
+    `nonfinite` (i32/u32 device scalar)."""
+    x = pitched(x)
+    M, K = x.shape
+    N = w.shape[0]
+    _lib.call("accel_tc_linear_checked", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
+              w.stride(0), out.stride(0), int(tanh), _p(nonfinite), _stream())
+    return out
+
+
 def tc_matmul_nn(x, w, out=None, accumulate=False):
     """out[M, N] = x[M, K] . w[K, N] (w row-major, i.e. B given transposed)."""
     x = pitched(x)

@@ -408,7 +408,7 @@ class Trainer:
         self.publish_policy()
 
     # -- shared forward pieces -------------------------------------------------------
-    def _backbone(self, frames, tag: str | None):
+    def _backbone(self, frames, tag: str | None, nonfinite=None):
         """h1, h2 over frame rows (models.py:176-177); tag None -> fresh tensors."""
         P = self.params.pv
         F = frames.shape[0]
@@ -419,11 +419,15 @@ class Trainer:
                 return torch.empty(F, D, dtype=F32, device=self.device)
             return self.scratch.get(tag + name, (F, D))
 
-        h1 = ops.tc_linear(frames, P["w0"], buf("h1"), bias=P["b0"], tanh=True)
+        if nonfinite is not None:  # the frame finiteness check rides on this read
+            h1 = ops.tc_linear_checked(frames, P["w0"], buf("h1"), nonfinite, bias=P["b0"],
+                                       tanh=True)
+        else:
+            h1 = ops.tc_linear(frames, P["w0"], buf("h1"), bias=P["b0"], tanh=True)
         h2 = ops.tc_linear(h1, P["w1"], buf("h2"), bias=P["b1"], tanh=True)
         return h1, h2
 
-    def _frame_values(self, frames, steps, out, bad_part, keep: bool = False):
+    def _frame_values(self, frames, steps, out, bad_part, keep: bool = False, nonfinite=None):
         """V(o) on every frame: state_values_batch (models.py:411-415).
 
         keep=True returns the backbone activations (fresh tensors) so a
@@ -431,7 +435,7 @@ class Trainer:
         P = self.params.pv
         F = frames.shape[0]
         d = self.dims
-        h1, h2 = self._backbone(frames, None if keep else "rv.")
+        h1, h2 = self._backbone(frames, None if keep else "rv.", nonfinite)
         fresh = lambda shape: torch.empty(*shape, dtype=F32, device=self.device)
         U = fresh((F, d.hidden)) if keep else self.scratch.get("rv.U", (F, d.hidden))
         alpha = fresh((F, 2)) if keep else self.scratch.get("rv.alpha", (F, 2))
@@ -511,7 +515,10 @@ class Trainer:
         if cfg.revalue:
             values = torch.empty(F, dtype=F32, device=dev)
             bad_part = self.scratch.get("b.vbad", (ops.warp_grid(F), 2), F64)
-            g = self._frame_values(b["frames"], b["steps"], values, bad_part, keep=True)
+            # counts non-finite frame values into cnt[0] (every frame: a bad
+            # bootstrap frame makes its revalued V non-finite, rejecting the batch too)
+            g = self._frame_values(b["frames"], b["steps"], values, bad_part, keep=True,
+                                   nonfinite=cnt[0:1])
             h_cache = (self._param_gen, *self._last_h)
             ops.reduce_f64(bad_part, g, 2, 0, flags[10:12])
         else:
@@ -528,7 +535,8 @@ class Trainer:
         with self._timed("token_logp"):
             lp_old, lbad = ops.token_logp(b["mu"], b["tokens"])
         ops.reduce_f64(lbad, ops.token_grid(M), 2, 0, flags[8:10])
-        ops.count_nonfinite_rows(b["frames"], frame_of, N, cnt[0:1])
+        if not cfg.revalue:
+            ops.count_nonfinite_rows(b["frames"], frame_of, N, cnt[0:1])
         batch = DeviceTrainBatch(
             frames=b["frames"], steps=b["steps"], tokens=b["tokens"], frame_of=frame_of,
             lp_old=lp_old, adv=adv, ret=ret, n_actions=d.n_actions, chunk_len=d.chunk_len,
