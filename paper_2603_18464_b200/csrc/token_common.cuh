@@ -244,6 +244,44 @@ __device__ __forceinline__ RowStats row_stats_full(float (&z)[VPL], float (&e)[V
   return s;
 }
 
+// Log-partition of a full row for the behavior log-prob pass (no entropy):
+// log2 domain (one FFMA folds the shift and the log2(e) scale), packed fp32x2
+// arithmetic, SFU exponentials.  A -inf logit still poisons the sum (0 * -inf).
+template <int VPL>
+__device__ __forceinline__ RowStats row_stats_logp(const float (&z)[VPL]) {
+  static_assert(VPL % 2 == 0, "pairs");
+  constexpr float kL2e = 1.4426950408889634f, kLn2f = 0.6931471805599453f;
+  RowStats s;
+  float mx = z[0];
+#pragma unroll
+  for (int v = 1; v < VPL; ++v) mx = fmaxf(mx, z[v]);
+  mx = warp_max_nan(mx);  // NaN logit -> NaN max; +inf -> inf - inf = NaN below
+  const float2 l2 = make_float2(kL2e, kL2e), n2 = make_float2(-mx * kL2e, -mx * kL2e);
+  const float2 zero2 = make_float2(0.f, 0.f);
+  float2 s2 = zero2;
+#pragma unroll
+  for (int p = 0; p < VPL / 2; ++p) {
+    const float2 zz = make_float2(z[2 * p], z[2 * p + 1]);
+    const float2 d = __ffma2_rn(zz, l2, n2);
+    float2 e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(d.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(d.y));
+    s2 = __fadd2_rn(__ffma2_rn(zz, zero2, s2), e);
+  }
+  float sum = s2.x + s2.y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  float lg;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(sum));
+  s.log_s = lg * kLn2f;
+  s.inv_s = 0.f;
+  s.sd_over_s = 0.f;
+  s.H = 0.f;
+  s.bad = !isfinite(sum) || !isfinite(mx);
+  s.d_tok = mx;  // caller subtracts: d_tok = z_tok - mx
+  return s;
+}
+
 // The rare float64 tail of token_coef, kept out of line so its register
 // footprint does not size the hot loop; results come back by value (taking the
 // callers' addresses would push their statistics to local memory every token).

@@ -359,7 +359,10 @@ token_logp_tma_kernel(const float* __restrict__ mu, const int32_t* __restrict__ 
     const bool bt = tok_raw < 0 || tok_raw >= A;
     const int tok = bt ? 0 : tok_raw;
     RowStats rs;
-    if (FULL) {
+    if constexpr (FULL && VPL % 2 == 0) {
+      rs = row_stats_logp<VPL>(z);
+      rs.d_tok = slot[tok] - rs.d_tok;
+    } else if (FULL) {
       rs = row_stats_full<VPL>(z, e, false);
       rs.d_tok = slot[tok] - rs.d_tok;
     } else {
