@@ -217,7 +217,16 @@ __device__ __forceinline__ uint32_t canon_k(int r, int k) {
 // converters: lo[i] = tf32_lo(raw[i]) over `bytes` (multiple of 16) of a stage
 __device__ __forceinline__ void convert_lo(const unsigned char* raw, unsigned char* lo,
                                            uint32_t bytes, int t) {
-  for (uint32_t i = (uint32_t)t * 16; i < bytes; i += kConv * 16)
+  constexpr uint32_t kStep = kConv * 16;
+  uint32_t i = (uint32_t)t * 16;
+  for (; i + 3 * kStep < bytes; i += 4 * kStep) {  // four shared loads in flight
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(raw + i + u * kStep);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) *reinterpret_cast<float4*>(lo + i + u * kStep) = tf32_lo(v[u]);
+  }
+  for (; i < bytes; i += kStep)
     *reinterpret_cast<float4*>(lo + i) = tf32_lo(*reinterpret_cast<const float4*>(raw + i));
 }
 
@@ -229,8 +238,20 @@ __device__ __forceinline__ unsigned nonfinite4(float4 v) {
 // the same, also counting non-finite inputs (the streamed operand is read anyway)
 __device__ __forceinline__ unsigned convert_lo_count(const unsigned char* raw, unsigned char* lo,
                                                      uint32_t bytes, int t) {
+  constexpr uint32_t kStep = kConv * 16;
   unsigned n = 0;
-  for (uint32_t i = (uint32_t)t * 16; i < bytes; i += kConv * 16) {
+  uint32_t i = (uint32_t)t * 16;
+  for (; i + 3 * kStep < bytes; i += 4 * kStep) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(raw + i + u * kStep);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      n += nonfinite4(v[u]);
+      *reinterpret_cast<float4*>(lo + i + u * kStep) = tf32_lo(v[u]);
+    }
+  }
+  for (; i < bytes; i += kStep) {
     const float4 v = *reinterpret_cast<const float4*>(raw + i);
     n += nonfinite4(v);
     *reinterpret_cast<float4*>(lo + i) = tf32_lo(v);
