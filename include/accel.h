@@ -244,10 +244,11 @@ int accel_reduce_segments(const void* const* srcs, void* const* dsts,
  * shard_statistics (trainer.py:128-132). */
 int accel_segment_moments(const float* x, const int64_t* off, int64_t nseg,
                           double* out, void* stream);
-/* count += rows of x f32[*, C] (rows[r], or r when rows == NULL) holding a
- * non-finite value — TrainBatch.check_finite on obs (buffers.py:120-122). */
+/* count += rows of x f32[*, C] (row pitch ld >= C; rows[r], or r when rows ==
+ * NULL) holding a non-finite value — TrainBatch.check_finite on obs
+ * (buffers.py:120-122). */
 int accel_count_nonfinite_rows(const float* x, const int32_t* rows, int64_t R, int C,
-                               unsigned* count, void* stream);
+                                int64_t ld, unsigned* count, void* stream);
 /* out[c] = sum (mode 0) or max (mode 1) over p of part[p * width + c]. */
 int accel_reduce_f64(const double* part, int64_t parts, int width, int mode,
                      double* out, void* stream);

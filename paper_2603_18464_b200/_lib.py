@@ -59,7 +59,7 @@ _SIGNATURES = {
     "accel_value_attn_wgrad": (c_int, [P, P, P, P, c_int64, c_int, P, c_int, P]),
     "accel_reduce_segments": (c_int, [P, P, P, P, P, c_int, P]),
     "accel_segment_moments": (c_int, [P, P, c_int64, P, P]),
-    "accel_count_nonfinite_rows": (c_int, [P, P, c_int64, c_int, P, P]),
+    "accel_count_nonfinite_rows": (c_int, [P, P, c_int64, c_int, c_int64, P, P]),
     "accel_reduce_f64": (c_int, [P, c_int64, c_int, c_int, P, P]),
     "accel_step_finalize": (c_int, [P, P, P, P, P, c_int, c_double, c_double, c_double,
                                     c_double, P, P, P]),

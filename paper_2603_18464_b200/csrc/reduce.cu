@@ -65,14 +65,14 @@ segment_moments_kernel(const float* __restrict__ x, const int64_t* __restrict__ 
 
 // count of rows r (row index rows[r] of x[*, C]) holding a non-finite value
 __global__ void count_nonfinite_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows,
-                                            int64_t R, int C, unsigned* __restrict__ count) {
+                                            int64_t R, int C, int64_t ld, unsigned* __restrict__ count) {
   unsigned c = 0;
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
     const int64_t f = rows ? __ldg(rows + r) : r;
     bool bad = false;
-    for (int j = lane; j < C; j += 32) bad |= !isfinite(__ldg(x + f * C + j));
+    for (int j = lane; j < C; j += 32) bad |= !isfinite(__ldg(x + f * ld + j));
     c += __any_sync(0xffffffffu, bad) && lane == 0;
   }
   if (c) atomicAdd(count, c);
@@ -265,10 +265,11 @@ extern "C" int accel_segment_moments(const float* x, const int64_t* off, int64_t
 }
 
 extern "C" int accel_count_nonfinite_rows(const float* x, const int32_t* rows, int64_t R, int C,
-                                          unsigned* count, void* stream) {
-  if (R < 0 || C < 1 || !x || !count) return fail(kDimension, "count_nonfinite_rows: bad arguments");
+                                          int64_t ld, unsigned* count, void* stream) {
+  if (R < 0 || C < 1 || ld < C || !x || !count)
+    return fail(kDimension, "count_nonfinite_rows: bad arguments");
   if (R == 0) return kOk;
   const int grid = (int)std::min<int64_t>(ceil_div(R, 8), (int64_t)kNumSMs * 8);
-  count_nonfinite_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, rows, R, C, count);
+  count_nonfinite_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, rows, R, C, ld, count);
   return post_launch("count_nonfinite_rows_kernel");
 }

@@ -307,7 +307,8 @@ def segment_moments(x, off, out=None):
 
 
 def count_nonfinite_rows(x, rows, R, count):
-    _lib.call("accel_count_nonfinite_rows", _p(x), _p(rows), int(R), x.shape[1], _p(count),
+    _lib.call("accel_count_nonfinite_rows", _p(x), _p(rows), int(R), x.shape[1], x.stride(0),
+              _p(count),
               _stream())
 
 
@@ -379,12 +380,32 @@ def alloc_pitched(rows, cols, device, dtype=F32):
     return torch.empty(rows, pitch, dtype=dtype, device=device)[:, :cols]
 
 
+def tc_rows_supported(K: int, N: int) -> bool:
+    """Shapes the tensor-core row transform takes (resident split weight):
+    K, N <= 256.  Wider products (cfg4's D = 4096) use cuBLAS fp32 (TF32 off)."""
+    return K <= 256 and N <= 256
+
+
+def _mm_fallback(x, w_t, out, bias=None, tanh=False, accumulate=False):
+    if accumulate:
+        out.addmm_(x, w_t)
+    else:
+        torch.mm(x, w_t, out=out)
+    if bias is not None:
+        out.add_(bias)
+    if tanh:
+        out.tanh_()
+    return out
+
+
 def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
     """out[M, N] = act(x[M, K] . w[N, K]^T + bias) (+ out): y = x W^T as in models.py."""
-    x = pitched(x)
     M, K = x.shape
     N = w.shape[0]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
+    if not tc_rows_supported(K, N):
+        return _mm_fallback(x, w.t(), out, bias, tanh, accumulate)
+    x = pitched(x)
     _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
               w.stride(0), out.stride(0), 0, 0, int(tanh), int(accumulate), 1, _stream())
     return out
@@ -393,9 +414,12 @@ def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
 def tc_linear_checked(x, w, out, nonfinite, bias=None, tanh=False):
     """tc_linear that also adds the count of non-finite elements of x to
     `nonfinite` (i32/u32 device scalar)."""
-    x = pitched(x)
     M, K = x.shape
     N = w.shape[0]
+    if not tc_rows_supported(K, N):
+        count_nonfinite_rows(x, None, M, nonfinite)  # counts rows, same decision
+        return _mm_fallback(x, w.t(), out, bias, tanh)
+    x = pitched(x)
     _lib.call("accel_tc_linear_checked", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
               w.stride(0), out.stride(0), int(tanh), _p(nonfinite), _stream())
     return out
@@ -403,10 +427,12 @@ def tc_linear_checked(x, w, out, nonfinite, bias=None, tanh=False):
 
 def tc_matmul_nn(x, w, out=None, accumulate=False):
     """out[M, N] = x[M, K] . w[K, N] (w row-major, i.e. B given transposed)."""
-    x = pitched(x)
     M, K = x.shape
     N = w.shape[1]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
+    if not tc_rows_supported(K, N):
+        return _mm_fallback(x, w, out, accumulate=accumulate)
+    x = pitched(x)
     _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), None, M, K, N, x.stride(0), w.stride(0),
               out.stride(0), 0, 1, 0, int(accumulate), 1, _stream())
     return out
@@ -450,11 +476,11 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     """out[n, k] = dy[F, n]^T . x[F, k] (reduction over the F rows): `kslices`
     persistent CTAs each produce two fp32 partials, reduced in fixed order
     (deterministic)."""
-    dy, x = pitched(dy), pitched(x)
     F, n = dy.shape
     k = x.shape[1]
-    if n > 256:
-        raise DimensionError("tc_wgrad: n > 256")
+    if n > 256 or k > 256:
+        return torch.mm(dy.t(), x, out=out)
+    dy, x = pitched(dy), pitched(x)
     if kslices is None:
         kslices = max(1, min(tc_sm_count(), -(-F // 32)))
     if partial is None:

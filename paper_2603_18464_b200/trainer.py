@@ -601,9 +601,13 @@ class Trainer:
     def _wgrad(self, dy, x, out, tag: str, extra: int = 0):
         """Tensor-core dW = dy^T x into per-CTA partial slices (+ `extra` slices
         the caller fills); returns the reduce_segments entry that sums them."""
-        dy, x = ops.pitched(dy), ops.pitched(x)  # no-ops at aligned widths
         F, n = dy.shape
         k = x.shape[1]
+        if n > 256 or k > 256:  # wide layers (cfg4): cuBLAS fp32, one "partial" = the result
+            part = self.scratch.get("wg." + tag, (1 + extra, n, k))
+            torch.mm(dy.t(), x, out=part[0])
+            return (part, out, 1 + extra, n * k, n * k)
+        dy, x = ops.pitched(dy), ops.pitched(x)  # no-ops at aligned widths
         ks = max(1, min(ops.tc_sm_count(), -(-F // 32)))
         part = self.scratch.get("wg." + tag, (2 * ks + extra, n, k))
         _lib.call("accel_tc_gemm", ops._p(dy), ops._p(x), ops._p(part), None, n, F, k,

@@ -272,3 +272,22 @@ def test_publication_versions():
         rec = tr.train_step(tr.build_train_batch(trajs))
         assert rec["version"] == v
     assert tr.service.published == [("policy", 1), ("policy", 2), ("policy", 3)]
+
+
+@pytest.mark.parametrize("D,O", [(512, 320), (4096, 4096)])
+def test_wide_layers_match_oracle(D, O):
+    """cfg4-style widths (O = D = 4096): products wider than the
+    tensor-core row kernel's resident weight fall back to cuBLAS fp32; the step
+    still matches the float64 oracle."""
+    tr, trajs, pol0, val0, cfg = _random_setup(seed=11, n_traj=4, K=7, A=256, D=D, O=O,
+                                               max_len=12)
+    orc = _oracle_from(cfg, pol0, val0, 256, tr.dims.n_steps)
+    ob = orc.build_train_batch(trajs)
+    batch = tr.build_train_batch(trajs)
+    assert scaled_err(batch.advantages, ob.advantages) < ADV_TOL
+    rec = tr.train_step(batch)
+    orec, g_pol, g_val = orc.step_gradients(ob)
+    for k, v in orec.items():
+        assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
+    dev_pol, dev_val = tr.params.grads_to_host()
+    check_grads(dev_pol, dev_val, g_pol, g_val, "trust")
