@@ -216,14 +216,16 @@ int accel_value_pool(const float* h1, const float* h2, const int32_t* row_frame,
                      const int32_t* steps, int64_t R, int D, int n_steps,
                      const float* w_attn, const float* b_attn, const float* e_step,
                      float* U, float* alpha, double* bad_part, int grid, void* stream);
-/* zm f32[R, H] = u @ W0v^T (no bias).  targets == NULL: forward only
- * (values_out f32[R]).  Otherwise zm <- dzm, part f32[grid][2H+1]
- * {dw1v, db0v, db1v}, dpart f64[grid][2] {sum err^2, non-finite v}. */
+/* zm f32[R, H] = u @ W0v^T (no bias); rows row_frame[r] (or r).  targets ==
+ * NULL: forward only (values_out f32[R]).  Otherwise zm <- dzm, part
+ * f32[grid][2H+1] {dw1v, db0v, db1v}, dpart f64[grid][2] {sum loss, non-finite
+ * v}.  Loss: MSE (trainer.py:438-443), or with v_old f32[R] the PPO value-clip
+ * loss max((v-R)^2, (v_old + clip(v - v_old, +-vclip) - R)^2) of the north star
+ * (no reference counterpart; float64 checker oracle/trainer_ref.py). */
 int accel_value_head(float* zm, const int32_t* row_frame, const float* b0v, const float* w1v,
-                     const float* b1v,
-                     int64_t R, int H, const float* targets, double lambda_v,
-                     double n_global, float* values_out, float* part, double* dpart,
-                     int grid, void* stream);
+                     const float* b1v, int64_t R, int H, const float* targets,
+                     const float* v_old, double vclip, double lambda_v, double n_global,
+                     float* values_out, float* part, double* dpart, int grid, void* stream);
 /* de f32[R, 2] attention-score gradients, part f32[grid] (db_attn). */
 int accel_value_attn_grad(const float* dU, const float* h1, const float* h2,
                           const int32_t* row_frame, const float* alpha, int64_t R, int D,

@@ -330,6 +330,20 @@ class OracleConfig:
     k_shards: int = 4
     eps_norm: float = 1e-8
     revalue: bool = True
+    value_clip: float | None = None  # north-star value-clip loss (no reference counterpart)
+
+
+def value_loss_clipped(v, ret, v_old, eps):
+    """PPO value clipping: mean(max((v - R)^2, (v_old + clip(v - v_old, +-eps) - R)^2)) and
+    dL/dv (per element, before the 1/N mean).  Not in the reference (trainer.py:438-443 is
+    plain MSE): restated here so the opt-in kernel path has a float64 checker."""
+    v, ret, v_old = (np.asarray(a, dtype=np.float64) for a in (v, ret, v_old))
+    d = v - v_old
+    vc = v_old + np.clip(d, -eps, eps)
+    l1, l2 = (v - ret) ** 2, (vc - ret) ** 2
+    loss = np.maximum(l1, l2)
+    g = np.where(l1 >= l2, 2.0 * (v - ret), np.where(np.abs(d) < eps, 2.0 * (vc - ret), 0.0))
+    return float(np.mean(loss)), g
 
 
 @dataclass
@@ -349,6 +363,7 @@ class OracleBatch:
     norm_count: int
     shard_sizes: tuple
     behavior_lag_mean: float
+    old_values: np.ndarray | None = None  # rollout-time V per transition (value clipping)
 
     @property
     def n_transitions(self) -> int:
@@ -392,7 +407,7 @@ class OracleTrainer:
     def build_train_batch(self, trajs):
         """trainer.py:358-403."""
         c = self.cfg
-        parts = {k: [] for k in ("obs", "steps", "tokens", "logp", "adv", "ret")}
+        parts = {k: [] for k in ("obs", "steps", "tokens", "logp", "adv", "ret", "vold")}
         lags, n_real = [], 0
         for tr in trajs:
             if c.revalue:
@@ -406,6 +421,7 @@ class OracleTrainer:
             parts["logp"].append(chosen_logp(tr.behavior_logits, tr.tokens))
             parts["adv"].append(adv)
             parts["ret"].append(ret)
+            parts["vold"].append(np.asarray(tr.values, dtype=np.float64))
             lags.append(self.publish_version - tr.behavior_version)
             n_real += tr.source == "real"
         normalized, summ = pooled_normalize(np.array_split(np.concatenate(parts["adv"]),
@@ -420,7 +436,8 @@ class OracleTrainer:
             critic_version=self.publish_version, n_real=n_real,
             n_imagined=len(trajs) - n_real, norm_mean=summ["mean"],
             norm_std=summ["std"], norm_count=summ["n"],
-            shard_sizes=summ["shard_sizes"], behavior_lag_mean=float(np.mean(lags)))
+            shard_sizes=summ["shard_sizes"], behavior_lag_mean=float(np.mean(lags)),
+            old_values=np.concatenate(parts["vold"]))
         return batch if batch.check_finite() else None
 
     def step_gradients(self, batch):
@@ -439,8 +456,12 @@ class OracleTrainer:
         hs = np.stack([cache["h1"], cache["h2"]], axis=1)
         v, vcache = value_forward(self.value, self.n_steps, hs, batch.steps)
         err = v - batch.value_targets
-        l_v = float(np.mean(err ** 2))
-        g_val = value_backward(self.value, vcache, c.lambda_v * 2.0 * err / err.size)
+        if c.value_clip is not None:
+            l_v, gv = value_loss_clipped(v, batch.value_targets, batch.old_values, c.value_clip)
+            g_val = value_backward(self.value, vcache, c.lambda_v * gv / err.size)
+        else:
+            l_v = float(np.mean(err ** 2))
+            g_val = value_backward(self.value, vcache, c.lambda_v * 2.0 * err / err.size)
         rec = {"loss": l_pi + c.lambda_v * l_v - c.lambda_h * h_mean,
                "policy_loss": l_pi, "value_loss": l_v, "entropy": h_mean,
                **{k: val for k, val in diag.items() if k != "dropped"}}

@@ -53,8 +53,8 @@ _SIGNATURES = {
     "accel_warp_grid": (c_int, [c_int64]),
     "accel_value_pool": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P, P, c_int,
                                  P]),
-    "accel_value_head": (c_int, [P, P, P, P, P, c_int64, c_int, P, c_double, c_double, P, P,
-                                 P, c_int, P]),
+    "accel_value_head": (c_int, [P, P, P, P, P, c_int64, c_int, P, P, c_double, c_double,
+                                 c_double, P, P, P, c_int, P]),
     "accel_value_attn_grad": (c_int, [P, P, P, P, P, c_int64, c_int, P, P, c_int, P]),
     "accel_value_attn_wgrad": (c_int, [P, P, P, P, c_int64, c_int, P, c_int, P]),
     "accel_reduce_segments": (c_int, [P, P, P, P, P, c_int, P]),

@@ -139,7 +139,7 @@ class DeviceTrainBatch:
         t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
         finite = all(np.all(np.isfinite(np.asarray(a))) for a in
                      (obs, lp, batch.advantages, batch.value_targets))
-        return cls(
+        out = cls(
             frames=ops.upload_pitched(obs.astype(np.float32), device), steps=t(batch.steps, np.int32),
             tokens=t(tokens.reshape(-1), np.int32),
             frame_of=torch.arange(N, dtype=torch.int32, device=device),
@@ -149,3 +149,7 @@ class DeviceTrainBatch:
             n_imagined=batch.n_imagined, norm_mean=batch.norm_mean, norm_std=batch.norm_std,
             norm_count=batch.norm_count, shard_sizes=batch.shard_sizes,
             behavior_lag_mean=batch.behavior_lag_mean, finite=finite)
+        old = getattr(batch, "old_values", None)  # rollout-time V (value clipping)
+        if old is not None:
+            out.v_old = t(old, np.float32)
+        return out

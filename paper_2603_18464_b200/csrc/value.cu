@@ -18,6 +18,25 @@
 namespace accel {
 namespace {
 
+// MSE (trainer.py:438-443) or, with v_old, the PPO value-clip loss of the north
+// star: max((v - R)^2, (v_old + clip(v - v_old, +-eps) - R)^2).  Returns the loss
+// term (float64) and dL/dv.
+__device__ __forceinline__ double value_loss_term(float v, float t, const float* v_old, int64_t r,
+                                                  float eps, double& g) {
+  const double e = (double)v - (double)t;
+  if (!v_old) {
+    g = 2.0 * e;
+    return e * e;
+  }
+  const float vo = __ldg(v_old + r);
+  const float d = v - vo;
+  const double vc = (double)vo + (double)fminf(fmaxf(d, -eps), eps);
+  const double ec = vc - (double)t;
+  const double l1 = e * e, l2 = ec * ec;
+  g = l1 >= l2 ? 2.0 * e : (fabsf(d) < eps ? 2.0 * ec : 0.0);
+  return fmax(l1, l2);
+}
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxHPL = 4;  // mlp_hidden <= 128
@@ -230,9 +249,9 @@ __global__ void __launch_bounds__(kThreads)
 value_head_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame,
                   const float* __restrict__ b0v,
                   const float* __restrict__ w1v, const float* __restrict__ b1v, int64_t R, int H,
-                  const float* __restrict__ targets, float lambda_v, double inv_n,
-                  float* __restrict__ values_out, float* __restrict__ part,
-                  double* __restrict__ dpart) {
+                  const float* __restrict__ targets, const float* __restrict__ v_old, float vclip,
+                  float lambda_v, double inv_n, float* __restrict__ values_out,
+                  float* __restrict__ part, double* __restrict__ dpart) {
   __shared__ float s_part[kWarps][2 * 32 * kMaxHPL + 1];
   __shared__ double s_err[kWarps][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -262,9 +281,9 @@ value_head_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame,
     const float v = warp_sum(acc) + bias1;
     if (values_out && lane == 0) values_out[r] = v;
     if (targets) {
-      const float err = v - __ldg(targets + r);
-      const float dv = (float)((double)lambda_v * 2.0 * (double)err * inv_n);
-      err2 += (double)err * (double)err;
+      double gl;
+      err2 += value_loss_term(v, __ldg(targets + r), v_old, r, vclip, gl);
+      const float dv = (float)((double)lambda_v * gl * inv_n);
       bad += !isfinite(v);
       gb1 += dv;
 #pragma unroll
@@ -390,9 +409,9 @@ __global__ void __launch_bounds__(kThreads)
 value_head4_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame,
                    const float* __restrict__ b0v,
                    const float* __restrict__ w1v, const float* __restrict__ b1v, int64_t R,
-                   const float* __restrict__ targets, float lambda_v, double inv_n,
-                   float* __restrict__ values_out, float* __restrict__ part,
-                   double* __restrict__ dpart) {
+                   const float* __restrict__ targets, const float* __restrict__ v_old,
+                   float vclip, float lambda_v, double inv_n, float* __restrict__ values_out,
+                   float* __restrict__ part, double* __restrict__ dpart) {
   constexpr int H = LPR * CPL, RPW = 32 / LPR, Q = CPL / 4;
   __shared__ float s_part[kWarps][2 * H + 1];
   __shared__ double s_err[kWarps][2];
@@ -433,10 +452,11 @@ value_head4_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame
     const float v = acc + bias1;
     if (act && values_out && lc == 0) values_out[r] = v;
     if (targets && act) {
-      const float err = v - __ldg(targets + r);
-      const float dv = (float)((double)lambda_v * 2.0 * (double)err * inv_n);
+      double gl;
+      const double lterm = value_loss_term(v, __ldg(targets + r), v_old, r, vclip, gl);
+      const float dv = (float)((double)lambda_v * gl * inv_n);
       if (lc == 0) {
-        err2 += (double)err * (double)err;
+        err2 += lterm;
         bad += !isfinite(v);
         gb1 += dv;
       }
@@ -576,7 +596,8 @@ extern "C" int accel_value_pool(const float* h1, const float* h2, const int32_t*
 
 extern "C" int accel_value_head(float* zm, const int32_t* row_frame, const float* b0v,
                                 const float* w1v, const float* b1v,
-                                int64_t R, int H, const float* targets, double lambda_v,
+                                int64_t R, int H, const float* targets, const float* v_old,
+                                double vclip, double lambda_v,
                                 double n_global, float* values_out, float* part, double* dpart,
                                 int grid, void* stream) {
   if (R < 0 || H < 1 || grid < 1) return fail(kDimension, "value_head: bad sizes");
@@ -584,21 +605,23 @@ extern "C" int accel_value_head(float* zm, const int32_t* row_frame, const float
   if (R == 0) return kOk;
   if (!zm || !b0v || !w1v || !b1v || (targets && (!part || !dpart)))
     return fail(kDimension, "value_head: NULL buffer");
+  if (v_old && !(vclip > 0)) return fail(kDomain, "value clip epsilon must be > 0");
   const double inv_n = n_global > 0 ? 1.0 / n_global : 0.0;
   cudaStream_t st = as_stream(stream);
   if ((reinterpret_cast<uintptr_t>(zm) & 15) == 0 && (H == 32 || H == 64 || H == 128)) {
     if (H == 32)
-      value_head4_kernel<8, 4><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets,
+      value_head4_kernel<8, 4><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets, v_old, (float)vclip,
                                                           (float)lambda_v, inv_n, values_out, part, dpart);
     else if (H == 64)
-      value_head4_kernel<8, 8><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets,
+      value_head4_kernel<8, 8><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets, v_old, (float)vclip,
                                                           (float)lambda_v, inv_n, values_out, part, dpart);
     else
-      value_head4_kernel<16, 8><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets,
+      value_head4_kernel<16, 8><<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, targets, v_old, (float)vclip,
                                                            (float)lambda_v, inv_n, values_out, part, dpart);
     return post_launch("value_head4_kernel");
   }
-  value_head_kernel<<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, H, targets, (float)lambda_v,
+  value_head_kernel<<<grid, kThreads, 0, st>>>(zm, row_frame, b0v, w1v, b1v, R, H, targets, v_old,
+                                               (float)vclip, (float)lambda_v,
                                                inv_n, values_out, part, dpart);
   return post_launch("value_head_kernel");
 }

@@ -258,13 +258,13 @@ def value_pool(h1, h2, row_frame, steps, R, n_steps, w_attn, b_attn, e_step, U, 
 
 
 def value_head(zm, b0v, w1v, b1v, targets, lambda_v, n_global, values_out, part, dpart, grid,
-               row_frame=None, rows=None):
+               row_frame=None, rows=None, v_old=None, vclip=0.0):
     """rows R (default zm rows); row_frame: zm row of each of the R rows (the
-    dzm rows are written back there)."""
+    dzm rows are written back there); v_old (+ vclip > 0): value-clip loss."""
     R = zm.shape[0] if rows is None else int(rows)
     _lib.call("accel_value_head", _p(zm), _p(row_frame), _p(b0v), _p(w1v), _p(b1v), R,
-              zm.shape[1], _p(targets), float(lambda_v), float(n_global), _p(values_out),
-              _p(part), _p(dpart), int(grid), _stream())
+              zm.shape[1], _p(targets), _p(v_old), float(vclip), float(lambda_v),
+              float(n_global), _p(values_out), _p(part), _p(dpart), int(grid), _stream())
 
 
 def value_attn_grad(dU, h1, h2, row_frame, alpha, de, part, grid):

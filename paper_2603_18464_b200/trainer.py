@@ -58,8 +58,13 @@ class LossConfig:
     clip_eps: float = 0.2
     lambda_v: float = 0.5
     lambda_h: float = 0.01
+    # PPO value clipping (north star (b)); None = the reference's plain MSE
+    # (trainer.py:438-443), which has no clipped variant
+    value_clip: float | None = None
 
     def __post_init__(self) -> None:
+        if self.value_clip is not None and not self.value_clip > 0:
+            raise DomainError(f"value_clip must be > 0, got {self.value_clip}")
         if self.algorithm not in ("trust", "clip"):
             raise DomainError(f"unknown algorithm {self.algorithm!r}")
         if self.sigma <= 0:
@@ -549,6 +554,8 @@ class Trainer:
         batch.h_cache = h_cache
         # frame row of each trajectory's bootstrap observation (t = T)
         batch.boot_rows = b["traj_off"][1:] + torch.arange(n, dtype=torch.int64, device=dev)
+        if cfg.loss.value_clip is not None:  # rollout-time V per transition
+            batch.v_old = b["values"].index_select(0, frame_of)
         host_dev = torch.cat([flags, cnt.double()])
         if self.comm is not None:
             # data parallel: the batch is one shard of the global batch; every
@@ -721,6 +728,12 @@ class Trainer:
                            dbias_part, None, None, fix_stats=loss_sums)
 
         # value head (hiddens detached)
+        vclip = {}
+        if lc.value_clip is not None:
+            v_old = getattr(batch, "v_old", None)
+            if v_old is None:
+                raise DomainError("value_clip needs the rollout-time values of the batch")
+            vclip = {"v_old": v_old, "vclip": lc.value_clip}
         gw = ops.warp_grid(N)
         vpart = S.get("st.vpart", (gw, 2 * H + 1))
         vdpart = S.get("st.vdpart", (gw, 2), F64)
@@ -730,7 +743,7 @@ class Trainer:
             # frames, bootstrap rows carry zero gradient
             U, alpha, zm = vcache
             ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
-                           vpart, vdpart, gw, row_frame=batch.frame_of, rows=N)
+                           vpart, vdpart, gw, row_frame=batch.frame_of, rows=N, **vclip)
             if F != N:
                 zm.index_fill_(0, batch.boot_rows, 0.0)
             R, row_frame, step_group = F, None, batch.frame_step_group
@@ -747,7 +760,7 @@ class Trainer:
                            P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
             zm = ops.tc_linear(U, P["w0v"], S.get("st.zm", (N, H)))
             ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
-                           vpart, vdpart, gw)
+                           vpart, vdpart, gw, **vclip)
             R, row_frame, step_group = N, batch.frame_of, batch.step_group
             ga = gw
         segs = [self._wgrad(zm, U, G["w0v"], "w0v")]  # dzm^T U

