@@ -57,6 +57,38 @@ def dims():
     return dict(K=7, A=256, D=64, O=195, H=32)
 
 
+def trainer_roofline(N: int, n: int, peaks: dict) -> dict:
+    """T_roof = sum over the step's stages of max(bytes / BW, flops / F_peak)
+    (SURVEY 8(d)), with each stage's algorithmic bytes (fp32 activations, i32
+    indices) and, for the GEMMs, 3xTF32 tensor flops against half the measured
+    bf16 dense rate.  Passes a fused design avoids (the frame finiteness read,
+    the tanh derivatives) are not counted.  roofline time / achieved time is
+    the trainer's fraction of roofline."""
+    d = dims()
+    K, A, D, O, H = d["K"], d["A"], d["D"], d["O"], d["H"]
+    M, F = N * K, N + n
+    bw = float(peaks["hbm_gbs"]) * 1e9
+    tf32 = 0.5 * float(peaks.get("bf16_tflops_sustained", 1420.9)) * 1e12
+    gemm = [  # (rows, K, N): backbone, values (revaluation), head, value head, backward
+        (F, O, D), (F, D, D), (F, D, H), (F, D, A), (F, A, D), (F, D, D), (F, H, D),
+        (F, A, D), (F, D, D), (F, O, D), (F, H, D)]
+    stages = {
+        "token_logp": (M * (4 * A + 8), 0.0),
+        "gae": (20 * N + 13 * n, 0.0),
+        "loss_fact": (M * (4 * A + 12) + N * (8 * A + 8), 0.0),
+        "grouped_sums": (M * (4 * A + 4), 0.0),
+        "gemms": (sum(4 * r * (k + c) for r, k, c in gemm),
+                  sum(3 * 2 * r * k * c for r, k, c in gemm)),
+        "value_head": (4 * F * (2 * D + D) + 4 * 3 * F * H + 4 * F * (3 * D + 2) + 4 * F * (2 * D + 2),
+                       0.0),
+    }
+    t = sum(max(b / bw, f / tf32) for b, f in stages.values())
+    return {"t_roof_ms": t * 1e3, "bytes": sum(b for b, _ in stages.values()),
+            "tensor_flops": sum(f for _, f in stages.values()),
+            "stages_ms": {k: 1e3 * max(b / bw, f / tf32) for k, (b, f) in stages.items()},
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs; TF32 = bf16 dense sustained / 2"}
+
+
 def make_bundle(seed: int, n_steps: int):
     from paper_2603_18464_b200.types import (ModelBundle, PolicyConfig, PolicyModel, ValueConfig,
                                              ValueHead)
@@ -349,6 +381,7 @@ def main():
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
+    tr_roof = trainer_roofline(N, n, peaks)
     peak = float(peaks["hbm_gbs"])
     A = d["A"]
     # factorized head (trainer default): per token dz write (4A) + token/lp_old/lp_new
@@ -389,6 +422,7 @@ def main():
         "roofline_gae": {"bytes_per_launch": gae_bytes, "ms_per_launch": t_gae * 1e3,
                          "achieved": gae_bytes / t_gae / 1e9,
                          "frac": gae_bytes / t_gae / 1e9 / peak, "unit": "GB/s"},
+        "trainer_roofline": dict(tr_roof, achieved_ms=ms, frac=tr_roof["t_roof_ms"] / ms),
         "roofline_token_logp": {"bytes_per_launch": logp_bytes, "ms_per_launch": t_logp * 1e3,
                                 "achieved": logp_bytes / t_logp / 1e9,
                                 "frac": logp_bytes / t_logp / 1e9 / peak, "unit": "GB/s"},
