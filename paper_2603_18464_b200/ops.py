@@ -75,7 +75,7 @@ def gae_segmented(rewards, values_frames, traj_off, done, gamma, lam, *, adv=Non
     sums = torch.empty(4, dtype=F64, device=rewards.device) if sums is None else sums
     if frame_of is not None:
         _check(frame_of, "frame_of", I32, (n,))
-    nbytes = _lib.lib().accel_gae_workspace_size(n)
+    nbytes = _lib.lib().accel_gae_workspace_size(n_traj, n)
     buf = (ws or workspace("gae")).get(nbytes)
     _lib.call("accel_gae_segmented", _p(rewards), _p(values_frames), _p(traj_off), _p(done),
               n_traj, n, float(gamma), float(lam), _p(adv), _p(ret), _p(frame_of), _p(sums),

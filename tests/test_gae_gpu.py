@@ -59,15 +59,24 @@ def test_gae_matches_oracle_small_ragged():
     assert abs(sums[0] - exp_adv.sum()) < 1e-4 * max(1.0, np.abs(exp_adv).sum())
 
 
-@pytest.mark.parametrize("case", ["one_long", "all_ones", "libero_mix", "tile_edges"])
+@pytest.mark.parametrize("case", ["one_long", "all_ones", "libero_mix", "tile_edges",
+                                  "pass_edges", "with_empty"])
 def test_gae_matches_c_oracle_edge_cases(case):
     rng = np.random.default_rng(7)
     if case == "one_long":          # one trajectory spanning many tiles (look-back chain)
         lens, done = [50_000], [False]
     elif case == "all_ones":        # every transition is its own trajectory
         lens, done = [1] * 5000, rng.random(5000) < 0.5
-    elif case == "tile_edges":      # boundaries exactly on 2048-tile edges
+    elif case == "tile_edges":      # boundaries exactly on 2048-frame segment strides
         lens, done = [2048, 2047, 1, 4096, 2049, 3], [True, False, True, False, True, False]
+    elif case == "pass_edges":      # trajectories around the 3072-frame pass size
+        lens = [3071, 3072, 3073, 6143, 6144, 1, 2, 9215, 5, 3070]
+        done = [True, False, True, True, False, False, True, False, True, False]
+    elif case == "with_empty":      # zero-step trajectories (bootstrap frame only)
+        lens = rng.integers(0, 6, size=3000)
+        lens[:7] = 0
+        lens[-5:] = 0
+        done = rng.random(3000) < 0.5
     else:
         from paper_2603_18464_b200.workload import libero_long_lengths
         lens, done = libero_long_lengths(rng, 512)
