@@ -611,6 +611,386 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
   }
 }
 
+// ---- two-phase kernel: a warp per transition, lane k owns token k's scalars ----
+// The per-token scalar chain (log-partition, ratio, trust weight / clip, the
+// float64 statistics) was the issue bottleneck of the kernels above: it ran
+// once per token on every lane.  Here a warp owns a transition (A = 32 VPL
+// logits per token, VPL per lane):
+//   phase A: for every token k: z = H2W[frame] + EPP[prev, k], exact row max
+//            (one CREDUX), d2 = (z - max) log2(e), partition sums
+//            sum_k = sum 2^d2 and sed_k = sum 2^d2 d2 -- K independent rows, so
+//            the unrolled loop overlaps them; d2 of tokens k >= 1 is written
+//            back over the token's EPP slot (each lane its own columns);
+//   a transposed butterfly reduces all 2K partial sums in 2K - 1 + 5 - log2(2K)
+//            shuffles and leaves token k's totals on lane k;
+//   lane k runs token k's scalar algebra (all K tokens in one pass);
+//   phase C: for every token: broadcast (Ac, Cc), reload d2 (token 0:
+//            recompute from the resident chunk-start row), 2^d2 (SFU),
+//            dz = 2^d2 (Ac d2 + Cc), G += dz, streaming stores; lane k then
+//            patches dz[tok_k] (+coef) after one warp barrier.
+// The transition's H2W row and EPP rows k >= 1 land in shared memory by bulk
+// copy, double-buffered a whole transition ahead (one mbarrier per buffer);
+// the chunk-start row EPP[A, 0] (every transition's token 0) is resident per CTA.
+constexpr int kF2MaxWarps = 7;
+constexpr int kF2Chunk = 8;  // transitions per dynamically claimed chunk
+__device__ unsigned g_fact2_ctr[2];  // work counters (main pass, fixup pass)
+
+// After the call lane l holds the warp total of value index l / (32 / NV).
+template <int NV>
+__device__ __forceinline__ float transpose_reduce(float (&x)[NV], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 5; ++lvl) {
+    const int o = 16 >> lvl;
+    const int n = NV >> lvl;
+    if (n > 1) {
+      const int half = n / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const float send = up ? x[j] : x[j + half];
+        const float keep = up ? x[j + half] : x[j];
+        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      x[0] += __shfl_xor_sync(0xffffffffu, x[0], o);
+    }
+  }
+  return x[0];
+}
+
+// shared memory floats per warp: 2 buffers x {H row, EPP rows 1..K-1} + one-hot row
+__host__ __device__ constexpr int fact2_warp_floats(int K, int A) { return (2 * K + 1) * A; }
+
+// KT > 0: K == KT at compile time (no per-token guards: the unrolled token loops
+// interleave); KT == 0: runtime K <= KMAX.
+template <int VPL, int KMAX, int KT>
+__global__ void __launch_bounds__(kF2MaxWarps * 32, 2)
+token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
+                        const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
+                        const float* __restrict__ lp_old, const float* __restrict__ adv,
+                        int64_t N, int K_rt, LossParams prm, const double* __restrict__ fix_stats,
+                        float* __restrict__ dz, float* __restrict__ g_frame,
+                        float* __restrict__ lp_new, double* __restrict__ stat_part,
+                        double* __restrict__ max_part, unsigned* __restrict__ work_ctr) {
+  constexpr int A = VPL * 32;
+  constexpr int Q = VPL / 4;  // float4 chunks per lane (column q * 128 + lane * 4 + r)
+  constexpr int P = VPL / 2;  // float2 pairs per lane
+  constexpr int NV = 2 * KMAX;
+  constexpr int kHold = 32 / NV;  // lane stride of the reduced values
+  static_assert(NV <= 32 && VPL % 4 == 0 && KT <= KMAX, "layout");
+  const int K = KT > 0 ? KT : K_rt;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_stat[kF2MaxWarps][kNumStat + kNumMax];
+  __shared__ __align__(16) float s_e0[A];       // EPP[A, 0]: token 0 of every transition
+  __shared__ float s_cf[kF2MaxWarps][32];       // per-lane coef (one-hot part of G)
+  RowCtx cx;
+  if (!setup_ctx(prm, fix_stats, cx)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int c = threadIdx.x; c < A; c += blockDim.x) s_e0[c] = __ldg(epp + (int64_t)A * K * A + c);
+  // smem per warp: buf[2] = {H row [A], d2/EPP rows 1..K-1 [K-1][A]} | s_oh [A];
+  // mbarriers after all warps
+  const int per_warp = fact2_warp_floats(K, A);
+  const int buf_floats = K * A;
+  float* wbase = reinterpret_cast<float*>(smem) + (size_t)warp * per_warp;
+  float* s_oh = wbase + 2 * buf_floats;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem) +
+                                               (size_t)nwarps * per_warp) + 2 * warp;
+  for (int c = lane; c < A; c += 32) s_oh[c] = 0.f;
+  const unsigned row_bytes = (unsigned)A * 4u;
+  if (lane == 0) {
+    mbar_init(&bars[0], 32);
+    mbar_init(&bars[1], 32);
+    fence_mbar_init();
+  }
+  __syncthreads();  // s_e0 and the barriers
+
+  // transition scalars: lane k < K holds token k / lp_old k; all lanes frame + advantage
+  struct Sc { int tok, fi; float lpo, a; };
+  auto load_sc = [&](int64_t i) {
+    Sc s{0, 0, 0.f, 0.f};
+    if (i < N) {
+      s.fi = __ldg(frame_of + i);
+      s.a = __ldg(adv + i);
+      if (lane < K) {
+        s.tok = __ldg(tokens + i * K + lane);
+        s.lpo = __ldg(lp_old + i * K + lane);
+      }
+    }
+    return s;
+  };
+  // 16-B cp.async copies of transition i's H2W row (slot 0) and EPP rows
+  // 1..K-1 (token k's row is EPP[tok_{k-1}, k]) into buffer b.  Lane l copies
+  // exactly the columns it later reads and overwrites (q * 128 + l * 4), so the
+  // d2 write-back and the refill two transitions on are ordered by the lane's
+  // own program order.  Every lane arrives (noinc) when its copies land.
+  auto issue = [&](int b, const Sc& s) {
+    float* hb = wbase + b * buf_floats;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (KT > 0 ? k < KT : k < K) {
+        const float* src;
+        if (k == 0) {
+          src = h2w + (int64_t)s.fi * A;
+        } else {
+          const int prev = min(max(__shfl_sync(0xffffffffu, s.tok, k - 1), 0), A - 1);
+          src = epp + ((int64_t)prev * K + k) * A;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           smem_u32(hb + k * A + q * 128 + lane * 4)),
+                       "l"(src + q * 128 + lane * 4)
+                       : "memory");
+      }
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[b]))
+                 : "memory");
+  };
+  // dynamic schedule: warps claim chunks of kF2Chunk consecutive transitions
+  // from a device counter (zeroed by the host before the launch), one chunk
+  // ahead, so SMs that run faster take more chunks; next(x) is the transition
+  // after x in this warp's sequence (N = none)
+  unsigned pend = 0;  // lane 0: the pre-claimed next chunk (resolved lazily)
+  auto claim = [&]() -> unsigned { return lane == 0 ? atomicAdd(work_ctr, 1u) : 0u; };
+  auto next_of = [&](int64_t x) -> int64_t {
+    if (x >= N) return N;
+    if ((x + 1) % kF2Chunk != 0 && x + 1 < N) return x + 1;
+    const int64_t y = (int64_t)__shfl_sync(0xffffffffu, pend, 0) * kF2Chunk;
+    pend = claim();
+    return y < N ? y : N;
+  };
+  const float ent2 = cx.ent_scale * kLn2;
+  const float2 l2e2 = make_float2(kLog2e, kLog2e);
+  double st_loss = 0.0, st_ent = 0.0, st_r = 0.0, st_w = 0.0;
+  double st_rmax = -CUDART_INF, st_negw = -CUDART_INF;
+  int st_out = 0, st_excl = 0, st_bad = 0, st_badtok = 0;
+
+  int64_t i = (int64_t)__shfl_sync(0xffffffffu, claim(), 0) * kF2Chunk;
+  i = i < N ? i : N;
+  pend = claim();
+  int64_t i1 = next_of(i);
+  Sc cur = load_sc(i);
+  Sc nxt = load_sc(i1);
+  if (i < N) issue(0, cur);
+  for (int64_t j = 0; i < N; ++j) {
+    const int b = (int)(j & 1);
+    // the other buffer was last read by transition j - 1: refill it with j + 1
+    __syncwarp();
+    if (i1 < N) issue(b ^ 1, nxt);
+    const int64_t i2 = next_of(i1);
+    const Sc nn = load_sc(i2);
+    float* hrow = wbase + b * buf_floats;  // slot 0: H2W row; slots 1..K-1: EPP rows -> d2
+    mbar_wait(&bars[b], (unsigned)(j >> 1) & 1u);
+    __syncwarp();  // reconverge after the spin-wait
+
+    const int kl = lane < K ? lane : 0;  // token owned by this lane
+    const bool own = lane < K;
+    const bool bad_tok = cur.tok < 0 || cur.tok >= A;
+    const int tok = bad_tok ? 0 : cur.tok;
+    // chosen-token logit, read before the EPP slots are overwritten with d2
+    const float z_tok = hrow[tok] + (kl == 0 ? s_e0[tok] : hrow[kl * A + tok]);
+    float2 h2[P];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const float4 h = *reinterpret_cast<const float4*>(hrow + q * 128 + lane * 4);
+      h2[2 * q] = make_float2(h.x, h.y);
+      h2[2 * q + 1] = make_float2(h.z, h.w);
+    }
+    __syncwarp();  // every lane has read z_tok before any d2 store
+    // ---- phase A: row max and partition sums of every token ----
+    float mx0 = 0.f, mx_l = 0.f, red[NV];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      red[k] = 0.f;
+      red[KMAX + k] = 0.f;
+      if (KT > 0 ? k < KT : k < K) {
+        const float* er = k == 0 ? s_e0 : hrow + k * A;
+        float2 z2[P];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const float4 ep = *reinterpret_cast<const float4*>(er + q * 128 + lane * 4);
+          z2[2 * q] = __fadd2_rn(h2[2 * q], make_float2(ep.x, ep.y));
+          z2[2 * q + 1] = __fadd2_rn(h2[2 * q + 1], make_float2(ep.z, ep.w));
+        }
+        float m2[P];  // max tree (short dependency chains)
+#pragma unroll
+        for (int p = 0; p < P; ++p) m2[p] = fmaxf(z2[p].x, z2[p].y);
+#pragma unroll
+        for (int w = 1; w < P; w *= 2)
+#pragma unroll
+          for (int p = 0; p + w < P; p += 2 * w) m2[p] = fmaxf(m2[p], m2[p + w]);
+        const float mx = warp_max_nan(m2[0]);  // NaN logit -> NaN max; +inf -> NaN below
+        if (k == 0) mx0 = mx;
+        mx_l = kl == k ? mx : mx_l;
+        const float2 n2 = make_float2(-mx * kLog2e, -mx * kLog2e);
+        float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 sd2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          z2[p] = __ffma2_rn(z2[p], l2e2, n2);  // d2
+          const float2 e2 = make_float2(ex2_ftz(z2[p].x), ex2_ftz(z2[p].y));
+          s2[p & 1] = __fadd2_rn(s2[p & 1], e2);
+          sd2[p & 1] = __ffma2_rn(e2, z2[p], sd2[p & 1]);  // 0 * (-inf) = NaN: -inf poisons it
+        }
+        if (k > 0) {
+          float* dr = hrow + k * A;
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+            *reinterpret_cast<float4*>(dr + q * 128 + lane * 4) =
+                make_float4(z2[2 * q].x, z2[2 * q].y, z2[2 * q + 1].x, z2[2 * q + 1].y);
+        }
+        const float2 s = __fadd2_rn(s2[0], s2[1]), sd = __fadd2_rn(sd2[0], sd2[1]);
+        red[k] = s.x + s.y;
+        red[KMAX + k] = sd.x + sd.y;
+      }
+    }
+    transpose_reduce<NV>(red, lane);
+    const float sum = __shfl_sync(0xffffffffu, red[0], (kl * kHold) & 31);
+    const float sed = __shfl_sync(0xffffffffu, red[0], ((KMAX + kl) * kHold) & 31);
+    // ---- lane k: token k's scalar algebra ----
+    const bool bad = !isfinite(sum) || !isfinite(sed) || !isfinite(mx_l);
+    const float inv_s = 1.f / sum;
+    const float log_s = __logf(sum);
+    const float sdn = sed * inv_s;  // sum_a p_a d2_a
+    const float Hk = log_s - sdn * kLn2;
+    const float lpn = (z_tok - mx_l) - log_s;
+    const float dlt = lpn - cur.lpo;
+    const bool inc = own && !bad_tok && !bad && dlt <= 709.78271289f && dlt >= -745.13321910f;
+    double term_d, r_d, w_d;
+    bool outside;
+    const float coef = token_coef(dlt, cur.a, inc, cx, term_d, r_d, w_d, outside);
+    const float Ac = ent2 * inv_s;
+    const float Cc = -(Ac * sdn) - coef * inv_s;
+    const float d2t = fmaf(z_tok, kLog2e, -mx_l * kLog2e);  // == the row's d2 at column tok
+    const float patch = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
+    if (own && !cx.fixup) {
+      lp_new[i * K + lane] = lpn;
+      st_ent += (double)Hk;
+      st_bad += bad;
+      st_badtok += bad_tok;
+      if (inc) {
+        st_loss += term_d;
+        st_r += r_d;
+        st_w += w_d;
+        st_out += outside;
+        st_rmax = fmax(st_rmax, r_d);
+        st_negw = fmax(st_negw, -w_d);
+      } else {
+        ++st_excl;
+      }
+    }
+    // ---- phase C: dlogits rows, G accumulation ----
+    float2 g2[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) g2[p] = make_float2(0.f, 0.f);
+    float* dz_i = dz + i * K * A;
+    const float2 n20 = make_float2(-mx0 * kLog2e, -mx0 * kLog2e);
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (KT > 0 ? k < KT : k < K) {
+        const float Ak = __shfl_sync(0xffffffffu, Ac, k);
+        const float Ck = __shfl_sync(0xffffffffu, Cc, k);
+        const float2 A2 = make_float2(Ak, Ak), C2 = make_float2(Ck, Ck);
+        float2 d2[P];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          if (k == 0) {  // recompute from the resident chunk-start row
+            const float4 ep = *reinterpret_cast<const float4*>(s_e0 + q * 128 + lane * 4);
+            d2[2 * q] = __ffma2_rn(__fadd2_rn(h2[2 * q], make_float2(ep.x, ep.y)), l2e2, n20);
+            d2[2 * q + 1] =
+                __ffma2_rn(__fadd2_rn(h2[2 * q + 1], make_float2(ep.z, ep.w)), l2e2, n20);
+          } else {
+            const float4 v = *reinterpret_cast<const float4*>(hrow + k * A + q * 128 + lane * 4);
+            d2[2 * q] = make_float2(v.x, v.y);
+            d2[2 * q + 1] = make_float2(v.z, v.w);
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float2 e2 = make_float2(ex2_ftz(d2[p].x), ex2_ftz(d2[p].y));
+          d2[p] = __fmul2_rn(e2, __ffma2_rn(A2, d2[p], C2));
+          g2[p] = __fadd2_rn(g2[p], d2[p]);
+        }
+        float* drow = dz_i + k * A;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          __stcs(reinterpret_cast<float4*>(drow + q * 128 + lane * 4),
+                 make_float4(d2[2 * q].x, d2[2 * q].y, d2[2 * q + 1].x, d2[2 * q + 1].y));
+      }
+    }
+    // one-hot part: dz[tok_k] += coef_k (after every lane's row stores) and
+    // G[tok_k] += coef_k, duplicates summed in token order by their first lane
+    s_cf[warp][lane] = coef;
+    __syncwarp();
+    if (own) dz_i[lane * A + tok] = patch;
+    const unsigned same = __match_any_sync(0xffffffffu, own && !bad_tok ? tok : -1 - lane);
+    if (own && !bad_tok && (same & ((1u << lane) - 1u)) == 0) {
+      float acc = coef;
+      for (unsigned m = same & (same - 1u); m; m &= m - 1u) acc += s_cf[warp][__ffs(m) - 1];
+      s_oh[tok] = acc;
+    }
+    __syncwarp();
+    float* grow = g_frame + (int64_t)cur.fi * A;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const float4 o = *reinterpret_cast<const float4*>(s_oh + q * 128 + lane * 4);
+      __stcs(reinterpret_cast<float4*>(grow + q * 128 + lane * 4),
+             make_float4(g2[2 * q].x + o.x, g2[2 * q].y + o.y, g2[2 * q + 1].x + o.z,
+                         g2[2 * q + 1].y + o.w));
+    }
+    __syncwarp();
+    if (own && !bad_tok) s_oh[tok] = 0.f;
+    cur = nxt;
+    nxt = nn;
+    i = i1;
+    i1 = i2;
+  }
+  if (cx.fixup) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
+    st_ent += __shfl_xor_sync(0xffffffffu, st_ent, o);
+    st_r += __shfl_xor_sync(0xffffffffu, st_r, o);
+    st_w += __shfl_xor_sync(0xffffffffu, st_w, o);
+    st_rmax = fmax(st_rmax, __shfl_xor_sync(0xffffffffu, st_rmax, o));
+    st_negw = fmax(st_negw, __shfl_xor_sync(0xffffffffu, st_negw, o));
+  }
+  st_out = __reduce_add_sync(0xffffffffu, st_out);
+  st_excl = __reduce_add_sync(0xffffffffu, st_excl);
+  st_bad = __reduce_add_sync(0xffffffffu, st_bad);
+  st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
+  if (lane == 0) {
+    double* st = s_stat[warp];
+    st[kLossNum] = st_loss;
+    st[kEntSum] = st_ent;
+    st[kRatioSum] = st_r;
+    st[kWSum] = st_w;
+    st[kOutside] = st_out;
+    st[kExcluded] = st_excl;
+    st[kBadRows] = st_bad;
+    st[kBadTok] = st_badtok;
+    st[kNumStat + kRatioMax] = st_rmax;
+    st[kNumStat + kNegWMin] = st_negw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // warps in fixed order: deterministic
+    double sum[kNumStat + kNumMax];
+#pragma unroll
+    for (int q = 0; q < kNumStat; ++q) sum[q] = 0.0;
+    sum[kNumStat + kRatioMax] = sum[kNumStat + kNegWMin] = -CUDART_INF;
+    for (int w = 0; w < nwarps; ++w) {
+#pragma unroll
+      for (int q = 0; q < kNumStat; ++q) sum[q] += s_stat[w][q];
+#pragma unroll
+      for (int q = kNumStat; q < kNumStat + kNumMax; ++q) sum[q] = fmax(sum[q], s_stat[w][q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kNumStat; ++q) stat_part[(int64_t)blockIdx.x * kNumStat + q] = sum[q];
+    max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = sum[kNumStat + kRatioMax];
+    max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = sum[kNumStat + kNegWMin];
+  }
+}
+
 // Dprev[j] = sum_k Dpk[j, k], Dpos[k] = sum_j Dpk[j, k]  (Dpk f32[(A+1), K, A])
 __global__ void pk_marginals_kernel(const float* __restrict__ dpk, int K, int A, int nprev,
                                     float* __restrict__ dprev, float* __restrict__ dpos) {
@@ -824,6 +1204,34 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
     };
     return tsc ? launch(kernel_sc) : launch(kernel_dz);
   };
+  // two-phase warp-per-transition kernel (dz output, K <= 8, A in {128, 256})
+  auto two_phase = [&](auto kernel) -> int {
+    // two CTAs per SM: 2 x (dynamic + ~5 KB static + 1 KB reserved) <= 228 KB
+    const size_t per_warp = (size_t)fact2_warp_floats(K, A) * 4 + 2 * sizeof(uint64_t);
+    const int nw = (int)std::max<size_t>(
+        1, std::min<size_t>(kF2MaxWarps, (size_t)(107 * 1024) / per_warp));
+    const size_t smem = (size_t)nw * per_warp + 16;
+    if (smem > 48 * 1024) {
+      cudaError_t e =
+          cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return fail(kCuda, "token_loss_fact2 smem: %s", cudaGetErrorString(e));
+    }
+    // the work counter of this pass (a fix-up launch uses the second one, so a
+    // skipped fix-up never races the next step's main pass)
+    unsigned* ctr = nullptr;
+    if (cudaGetSymbolAddress(reinterpret_cast<void**>(&ctr), g_fact2_ctr) != cudaSuccess)
+      return fail(kCuda, "token_loss_fact2: counter symbol");
+    ctr += fix_stats ? 1 : 0;
+    if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess)
+      return fail(kCuda, "token_loss_fact2: counter reset");
+    kernel<<<grid, nw * 32, smem, s>>>(h2w, epp, frame_of, tokens, lp_old, adv, N, K, prm,
+                                       fix_stats, dz, g_frame, lp_new, stat_part, max_part, ctr);
+    return post_launch("token_loss_fact2_kernel");
+  };
+  if (!tsc && K == 7 && A == 256) return two_phase(token_loss_fact2_kernel<8, 8, 7>);
+  if (!tsc && K <= 8 && A == 256) return two_phase(token_loss_fact2_kernel<8, 8, 0>);
+  if (!tsc && K == 7 && A == 128) return two_phase(token_loss_fact2_kernel<4, 8, 7>);
+  if (!tsc && K <= 8 && A == 128) return two_phase(token_loss_fact2_kernel<4, 8, 0>);
   const bool full = A == 128 || A == 256 || A == 512 || A == 1024;
   // grouped kernel: 16 (32 at A = 1024) logits per lane, A / that lanes per transition
   if (A == 128 && K <= 8)

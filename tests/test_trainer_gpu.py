@@ -176,6 +176,21 @@ def test_random_batch_matches_oracle(algo, factorized):
     check_grads(dev_pol, dev_val, g_pol, g_val, algo)
 
 
+@pytest.mark.parametrize("K,A", [(3, 128), (8, 256), (1, 256), (9, 256), (7, 512)])
+def test_loss_kernel_shapes_match_oracle(K, A):
+    """Two-phase loss kernel (K <= 8, A in {128, 256}) and the grouped kernel
+    beyond it (K = 9, A = 512) against the float64 oracle."""
+    tr, trajs, pol0, val0, cfg = _random_setup(seed=11, K=K, A=A, n_traj=10, max_len=30)
+    orc = _oracle_from(cfg, pol0, val0, A, tr.dims.n_steps)
+    ob = orc.build_train_batch(trajs)
+    rec = tr.train_step(tr.build_train_batch(trajs))
+    orec, g_pol, g_val = orc.step_gradients(ob)
+    for k, v in orec.items():
+        assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
+    dev_pol, dev_val = tr.params.grads_to_host()
+    check_grads(dev_pol, dev_val, g_pol, g_val, (K, A))
+
+
 @pytest.mark.parametrize("factorized", [True, False, "recompute"])
 def test_partial_exclusion_runs_fixup_pass(factorized):
     """Some tokens with log-ratio < -745 are excluded: the surrogate mean is
