@@ -46,7 +46,8 @@ int accel_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size
 /* ---- (a) advantages ---------------------------------------------------- */
 
 /* Workspace bytes for accel_gae_segmented over n_traj trajectories holding
- * n_transitions steps (one 64-B record per 2048 value frames). */
+ * n_transitions steps (per-CTA float64 partials + an arrival counter; the
+ * size does not depend on the batch). */
 size_t accel_gae_workspace_size(int64_t n_traj, int64_t n_transitions);
 
 /* Segmented reverse-scan GAE over a ragged CSR batch.

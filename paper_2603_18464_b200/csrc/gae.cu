@@ -3,29 +3,29 @@
 // Reference: trainer.py:79-101 (compute_gae, one Python loop per
 // trajectory), trainer.py:128-158 (shard sums -> pooled mean/std).
 //
-// Design (single pass over HBM, 20 B/transition + 13 B/trajectory):
+// Design (single pass over HBM, 20 B/transition + 17 B/trajectory):
 //   * The ragged batch is one flat array of N transitions; trajectory s
 //     owns transitions [off[s], off[s+1]) and value frames
 //     [off[s]+s, off[s+1]+s] (T+1 values, bootstrap last).
 //   * A_t = delta_t + c_t * A_{t+1} with c_t = gamma*lam, or 0 at the last
-//     step of a trajectory, is a linear recurrence; the scan operator is the
+//     step of a trajectory, is a linear recurrence; its scan operator is the
 //     affine map (b, c): A_left = b + c * A_right.
-//   * Work is cut in value-frame space into segments of whole trajectories
-//     (those whose first frame falls in a 2560-frame stride), swept by
-//     persistent CTAs: a segment ends on a trajectory end, so no carry
-//     crosses CTAs -- no look-back, no ticket, no inter-CTA wait.  Inside a
-//     CTA the affine maps are suffix-scanned (thread, warp, block); a
-//     trajectory reaching past a pass (3328 frames) is swept in several
-//     right-to-left passes with the carry in shared memory.
-//   * Loads are 16-B cp.async copies of aligned runs (segments start at
-//     arbitrary offsets), all in flight at once; stores are staged through
-//     shared memory into coalesced 16-B vectors.
-//   * The issue budget is the limit (~20 B of HBM per transition), so the
-//     recurrence runs in fp32; the TD error is formed with gamma split into
+//   * A warp owns a contiguous range of whole trajectories: the ones whose
+//     first transition falls in its 1/W share of [0, N) (found by a 16-ary
+//     half-warp search on the offsets; balanced by transition count and fixed
+//     for a given grid, so the pooled sums are bitwise deterministic).
+//   * A trajectory is one chunk when it has <= 544 steps (longer ones: 544-step
+//     chunks from the right, carry between them).  The chunk's r and v land in
+//     shared memory by 4-byte cp.async copies (coalesced rows), double-buffered
+//     one chunk ahead; lane l then owns kd = ceil(T / 32) consecutive steps:
+//     a serial right-to-left fold of its affine maps, ONE 5-level shuffle
+//     suffix scan of the 32 lane maps, a serial resolve, and the outputs go
+//     back through shared memory to coalesced row stores.  No block barriers,
+//     no inter-CTA traffic.
+//   * The recurrence runs in fp32; the TD error is formed with gamma split into
 //     two floats (see the kernel), so rounding stays relative to the TD error
-//     and the advantage, never to |v|.  Per-CTA (sum A, sum A^2) partials
-//     feed the pooled statistics (float64) in a fixed order: bitwise
-//     deterministic for a given device.
+//     and the advantage, never to |v|.  Per-CTA (sum A, sum A^2) partials in
+//     float64 feed the pooled statistics in CTA order.
 #include <cfloat>
 
 #include "common.cuh"
@@ -35,344 +35,256 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 13;                // odd: item-strided smem reads are conflict-free
-constexpr int kChunk = kThreads * kItems;  // value frames per pass (3328)
-constexpr int kSeg = 2560;                 // segment stride in frame space (single pass
-                                           // while trajectories stay under 769 frames)
-constexpr int kPad = 8;                    // float4 alignment slack in the staging arrays
-constexpr int kVec = (kChunk + kPad + 4 + 4 * kThreads - 1) / (4 * kThreads);  // float4 / thread
-constexpr size_t kSegSmem = sizeof(float) * (3 * (kChunk + kPad) + 4);
-constexpr int kDoneBit = 1 << 30;          // packed beside a trajectory end in s_end
-constexpr int kEndMask = kDoneBit - 1;
-
-struct Map {
-  float b, c;
-};
-
-// l covers the earlier (left) range, r the later one.
-__device__ __forceinline__ Map compose(const Map& l, const Map& r) {
-  return {fmaf(l.c, r.b, l.b), l.c * r.c};
-}
-
-__device__ __forceinline__ Map shfl_down_map(const Map& m, int d) {
-  return {__shfl_down_sync(0xffffffffu, m.b, d), __shfl_down_sync(0xffffffffu, m.c, d)};
-}
-
-// first frame of trajectory s (g is strictly increasing: T_s + 1 >= 1 frames)
-__device__ __forceinline__ int64_t first_frame(const int64_t* off, int64_t s) {
-  return __ldg(off + s) + s;
-}
-
-// async 16-B copy of elements [e, e + 4) of x into shared memory, zero-filled
-// past `end` (e < end; x + e is 16-B aligned)
-__device__ __forceinline__ void copy4(float* dst, const float* x, int64_t e, int64_t end) {
-  const int bytes = e + 4 <= end ? 16 : 4 * (int)(end - e);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)),
-               "l"(x + e), "r"(bytes)
-               : "memory");
-}
-
-constexpr int kMaxGrid = 148 * 8;  // persistent grid bound (partials capacity)
+constexpr int kItems = 17;                 // max consecutive steps per lane
+constexpr int kChunkSteps = 32 * kItems;   // max steps per warp chunk (one chunk per
+                                           // trajectory up to 544 steps)
+constexpr int kPitch = kChunkSteps + 4;
+constexpr int kMaxGrid = 148 * 8;          // persistent grid bound (partials capacity)
 
 struct Workspace {
-  double* partials;     // [grid][3]
-  unsigned* counters;   // [1] arrival ticket (zeroed by the index kernel)
-  int64_t* seg_first;   // [segs + 1]: first trajectory of each segment
-  int64_t* seg_frame;   // [segs + 1]: its first value frame
+  double* partials;   // [grid][3]
+  unsigned* counter;  // [1] arrival ticket (zeroed before the launch)
 };
 
-size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+size_t workspace_bytes() { return 3 * sizeof(double) * kMaxGrid + 16; }
 
-Workspace carve(void* base, int64_t segs) {
-  char* p = static_cast<char*>(base);
+constexpr size_t kGaeSmem = sizeof(float) * kWarps * 2 * 2 * kPitch;
+
+Workspace carve(void* base) {
   Workspace w;
-  w.partials = reinterpret_cast<double*>(p);
-  size_t o = 3 * sizeof(double) * kMaxGrid;
-  w.counters = reinterpret_cast<unsigned*>(p + o);
-  o += 16;
-  w.seg_first = reinterpret_cast<int64_t*>(p + o);
-  o += align_up(sizeof(int64_t) * (size_t)(segs + 1), 16);
-  w.seg_frame = reinterpret_cast<int64_t*>(p + o);
+  w.partials = static_cast<double*>(base);
+  w.counter = reinterpret_cast<unsigned*>(static_cast<char*>(base) +
+                                          3 * sizeof(double) * kMaxGrid);
   return w;
 }
 
-size_t workspace_bytes(int64_t segs) {
-  return 3 * sizeof(double) * kMaxGrid + 16 +
-         2 * align_up(sizeof(int64_t) * (size_t)(segs + 1), 16);
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
 }
 
-// Segment k = the trajectories whose first value frame g(s) = off[s] + s lies
-// in [k kSeg, (k+1) kSeg): seg_first[k] = min{s : g(s) >= k kSeg}.  Thread s
-// (0..n_traj; s = n_traj is the end sentinel, g = F) writes the k in
-// (g(s-1) / kSeg, g(s) / kSeg]; every k < segs is written exactly once.
-__global__ void gae_segment_index_kernel(const int64_t* __restrict__ off, int64_t n_traj,
-                                         int64_t segs, Workspace ws) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s == 0) ws.counters[0] = 0u;
-  if (s > n_traj) return;
-  int64_t* seg_first = ws.seg_first;
-  int64_t* seg_frame = ws.seg_frame;
-  const int64_t g = first_frame(off, s);
-  const int64_t k0 = s == 0 ? 0 : first_frame(off, s - 1) / kSeg + 1;
-  const int64_t k1 = min(g / kSeg, segs - 1);
-  for (int64_t k = k0; k <= k1; ++k) {
-    seg_first[k] = s;
-    seg_frame[k] = g;
-  }
-  if (s == n_traj) {
-    seg_first[segs] = n_traj;
-    seg_frame[segs] = g;
-  }
-}
-
-// Persistent CTAs stride over the segments.  A segment holds whole
-// trajectories, so its right edge is a trajectory end (A = 0 beyond it) and
-// no carry crosses CTAs: there is no look-back, ticket or inter-CTA wait.
-// The segment is swept right to left in passes of <= kChunk value frames (one
-// pass unless a trajectory straddles more than kChunk - kSeg frames past the
-// stride), the carry between passes held in shared memory.
-//
-// Frame-space items: frame f of trajectory s is transition t = f - s, except
-// the trajectory's last frame (the bootstrap value), which is the map (0, 0).
-// Transition t has delta = r[t] + gamma * v[f+1] * (1 - last * done) - v[f]
-// and c = gamma * lam, or 0 at the trajectory's last transition.
-__global__ void __launch_bounds__(kThreads, 4)
-gae_segment_kernel(const float* __restrict__ rewards, const float* __restrict__ vals,
-                   const int64_t* __restrict__ off, const uint8_t* __restrict__ done,
-                   int64_t n_frames, float g_hi, float g_lo, float decay,
-                   float* __restrict__ adv_out, float* __restrict__ ret_out,
-                   int32_t* __restrict__ frame_out, Workspace ws,
-                   int64_t segs, int64_t n_transitions, double* __restrict__ sums_out) {
-  extern __shared__ __align__(16) float s_dyn[];
-  float* s_r = s_dyn;                    // rewards, then advantages
-  float* s_v = s_r + kChunk + kPad;      // values [f0, f1], then frame ids
-  float* s_ret = s_v + kChunk + kPad + 4;
-  int* s_end = reinterpret_cast<int*>(s_ret);  // trajectory ends (| done bit), then returns
-  __shared__ Map s_warp[kWarps];
-  __shared__ float s_carry;
-  __shared__ double s_red[kWarps * 3];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double S = 0.0, Q = 0.0, bad = 0.0;
-  // persistent: segments blockIdx.x, + gridDim.x, ...; the next segment's
-  // bounds are fetched while the current one is processed
-  int64_t seg = blockIdx.x;
-  int64_t nxt[4] = {0, 0, 0, 0};
-  if (seg < segs) {
-    nxt[0] = __ldcg(ws.seg_first + seg);
-    nxt[1] = __ldcg(ws.seg_first + seg + 1);
-    nxt[2] = __ldcg(ws.seg_frame + seg);
-    nxt[3] = __ldcg(ws.seg_frame + seg + 1);
-  }
-  for (; seg < segs; seg += gridDim.x) {
-    const int64_t a = nxt[0], b = nxt[1], Fa = nxt[2], Fb = nxt[3];
-    if (seg + gridDim.x < segs) {
-      const int64_t sn = seg + gridDim.x;
-      nxt[0] = __ldcg(ws.seg_first + sn);
-      nxt[1] = __ldcg(ws.seg_first + sn + 1);
-      nxt[2] = __ldcg(ws.seg_frame + sn);
-      nxt[3] = __ldcg(ws.seg_frame + sn + 1);
+// First s in [0, n] with off[s] >= target (off[n] >= target), searched by the
+// 16 lanes of a half-warp: 16-ary narrowing, one dependent load per round.  The
+// two half-warps search different targets; the loop runs until both are done.
+__device__ __forceinline__ int64_t half_warp_lower_bound(const int64_t* __restrict__ off,
+                                                         int64_t n, int64_t target, int hl,
+                                                         unsigned hmask, int hshift) {
+  int64_t lo = 0, hi = n;
+  bool fin = lo >= hi;
+  while (__any_sync(0xffffffffu, !fin)) {
+    int64_t q = hi, step = 1;
+    bool ge = true;
+    if (!fin) {
+      step = (hi - lo + 16) / 16;  // ceil((hi - lo + 1) / 16)
+      q = min(lo + (int64_t)(hl + 1) * step - 1, hi);
+      ge = __ldg(off + q) >= target;
     }
-    if (tid == 0) s_carry = 0.f;
-    int64_t f1 = Fb, jb = b;
-    while (f1 > Fa) {
-      const int64_t f0 = max(Fa, f1 - (int64_t)kChunk);
-      int64_t ja = a;
-      if (f0 > Fa) {  // long-trajectory pass: last s in [a, jb) with g(s) <= f0
-        int64_t lo = a, hi = jb;
-        while (hi - lo > 1) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (first_frame(off, mid) <= f0) lo = mid; else hi = mid;
-        }
-        ja = lo;
-      }
-      const int nf = (int)(f1 - f0);
-      const int nt = (int)(jb - ja);
-      const int64_t t_first = f0 - ja;
-      const int64_t t_end = (f1 == Fb || f1 == first_frame(off, jb)) ? f1 - jb : f1 - jb + 1;
-      // (f1 on a trajectory start: frame f1 - 1 is jb-1's bootstrap, else a transition)
-      // stage values [f0, f1] and rewards as aligned 16-B async copies: every
-      // load of the pass is in flight at once (one HBM round trip per pass)
-      const int64_t vb = f0 & ~3ll, ve = min(f1 + 1, n_frames);
-      const int vsh = (int)(f0 - vb);
-      const int nv4 = (int)((ve - vb + 3) >> 2);
-      const int64_t rb = t_first & ~3ll;
-      const int rsh = (int)(t_first - rb);
-      const int nr4 = (int)((t_end - rb + 3) >> 2);
-  #pragma unroll
-      for (int u = 0; u < kVec; ++u) {
-        const int q = tid + u * kThreads;
-        if (q < nv4) copy4(s_v + 4 * q, vals, vb + 4 * (int64_t)q, ve);
-        if (q < nr4) copy4(s_r + 4 * q, rewards, rb + 4 * (int64_t)q, t_end);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      // trajectory frame ends (clipped past the pass: never 'last' inside it)
-      for (int j = tid; j < nt; j += kThreads)
-        s_end[j] = (int)min(first_frame(off, ja + j + 1) - f0, (int64_t)kChunk + 2) |
-                   (__ldg(done + ja + j) ? kDoneBit : 0);
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncthreads();
-
-      // pass 1: this thread's items [i0, i0 + kItems).  j0 = trajectories
-      // ending before i0 = bootstrap frames before i0, so transition index
-      // (relative to t_first) of item i is i - j0 - (bootstraps in [i0, i)).
-      const int i0 = tid * kItems;
-      int j0 = 0;
-      unsigned boot = 0, last = 0, zero_next = 0;
-      const unsigned all = (1u << kItems) - 1u;
-      const unsigned pad = i0 >= nf ? all
-                                    : (i0 + kItems > nf ? all & ~((1u << (nf - i0)) - 1u) : 0u);
-      if (i0 < nf) {
-        int lo = 0, hi = nt - 1;  // first j with end(j) > i0
-        while (lo < hi) {
-          const int m = (lo + hi) >> 1;
-          if ((s_end[m] & kEndMask) > i0) hi = m; else lo = m + 1;
-        }
-        j0 = lo;
-        // the (few) trajectory ends touching this thread's window
-        for (int j = j0; j < nt; ++j) {
-          const int ed = s_end[j], e = ed & kEndMask;
-          if (e - 2 >= i0 + kItems) break;
-          if (e - 1 < i0 + kItems) boot |= 1u << (e - 1 - i0);
-          if (e - 2 >= i0) {
-            last |= 1u << (e - 2 - i0);
-            if (ed & kDoneBit) zero_next |= 1u << (e - 2 - i0);
-          }
-        }
-      }
-      // deltas and the thread's map.  delta = r + gamma v' - v with gamma split
-      // into two floats: fma(g_hi, v', -v) is exact before its one rounding, so
-      // the result carries fp32 rounding relative to the TD error itself, not to
-      // |v| (values much larger than the advantages lose nothing).
-      const unsigned cz = boot | last;  // c = 0 (bootstrap and last steps), else decay
-      float dl[kItems], vc[kItems];
-      Map m{0.f, 1.f};
-      if (i0 < nf) {
-        float vn = s_v[vsh + min(i0 + kItems, nf)];  // unused when frame f1 is past the end
-        // live items hold consecutive transition indices [i0 - j0, i0 - j0 + L)
-        int tr = i0 - j0 + kItems - __popc(boot) - __popc(pad);
-  #pragma unroll
-        for (int k = kItems - 1; k >= 0; --k) {
-          const unsigned bit = 1u << k;
-          const bool live = !((boot | pad) & bit);
-          tr -= live ? 1 : 0;
-          const float vi = (pad & bit) ? vn : s_v[vsh + i0 + k];
-          const float vnext = (zero_next & bit) ? 0.f : vn;
-          const float d = fmaf(g_lo, vnext, fmaf(g_hi, vnext, -vi)) + s_r[rsh + tr];
-          dl[k] = live ? d : 0.f;
-          vc[k] = vi;
-          vn = vi;
-          const float c = (pad & bit) ? 1.f : ((cz & bit) ? 0.f : decay);
-          m.b = fmaf(c, m.b, dl[k]);
-          m.c *= c;
-        }
-      }
-      // suffix scan of the maps: warp, then block (warp 0)
-      Map incl = m;
-  #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const Map o = shfl_down_map(incl, d);
-        if (lane + d < 32) incl = compose(incl, o);
-      }
-      Map excl = shfl_down_map(incl, 1);
-      if (lane == 31) excl = Map{0.f, 1.f};
-      if (lane == 0) s_warp[warp] = incl;
-      __syncthreads();
-      if (warp == 0) {
-        const Map w = lane < kWarps ? s_warp[lane] : Map{0.f, 1.f};
-        Map wi = w;
-  #pragma unroll
-        for (int d = 1; d < kWarps; d <<= 1) {
-          const Map o = shfl_down_map(wi, d);
-          if (lane + d < kWarps) wi = compose(wi, o);
-        }
-        Map we = shfl_down_map(wi, 1);
-        if (lane >= kWarps - 1) we = Map{0.f, 1.f};
-        __syncwarp();
-        if (lane < kWarps) s_warp[lane] = we;  // exclusive suffix of the warps to the right
-      }
-      __syncthreads();
-
-      // pass 2: resolve the right-hand context and emit into shared memory
-      // (advantages over the reward slots, returns over the trajectory ends,
-      // frame ids over the values -- each slot is read back by its owner only)
-      const Map right = compose(excl, s_warp[warp]);
-      float A = fmaf(right.c, s_carry, right.b);
-      float Sf = 0.f, Qf = 0.f;
-      int nbad = 0;
-      if (i0 < nf) {
-        int tr = i0 - j0 + kItems - __popc(boot) - __popc(pad);
-  #pragma unroll
-        for (int k = kItems - 1; k >= 0; --k) {
-          const unsigned bit = 1u << k;
-          // bootstrap: c = 0, delta = 0 -> A = 0; padding: c = 1, delta = 0
-          const float c = (pad & bit) ? 1.f : ((cz & bit) ? 0.f : decay);
-          A = fmaf(c, A, dl[k]);
-          if (!((boot | pad) & bit)) {
-            --tr;
-            const float rf = A + vc[k];
-            s_r[rsh + tr] = A;
-            s_ret[rsh + tr] = rf;
-            reinterpret_cast<int*>(s_v)[rsh + tr] = (int)(f0 + i0 + k);
-            Sf += A;
-            Qf = fmaf(A, A, Qf);
-            nbad += (fabsf(A) <= FLT_MAX && fabsf(rf) <= FLT_MAX) ? 0 : 1;
-          }
-        }
-      }
-      S += (double)Sf;
-      Q += (double)Qf;
-      bad += (double)nbad;
-      __syncthreads();
-      if (tid == 0) s_carry = A;  // A at frame f0, carried into the pass to the left
-
-      // coalesced write-back of [t_first, t_end): aligned float4 body, scalar edges
-      const int64_t body0 = (t_first + 3) & ~3ll, body1 = t_end & ~3ll;
-      if (body0 < body1) {
-        const int q0 = (int)((body0 - rb) >> 2), q1 = (int)((body1 - rb) >> 2);
-        for (int q = q0 + tid; q < q1; q += kThreads) {
-          const int64_t e = rb + 4 * (int64_t)q;
-          __stcs(reinterpret_cast<float4*>(adv_out + e), reinterpret_cast<const float4*>(s_r)[q]);
-          __stcs(reinterpret_cast<float4*>(ret_out + e), reinterpret_cast<const float4*>(s_ret)[q]);
-          if (frame_out != nullptr)
-            __stcs(reinterpret_cast<int4*>(frame_out + e), reinterpret_cast<const int4*>(s_v)[q]);
-        }
-        int64_t e = -1;
-        if (tid < body0 - t_first) e = t_first + tid;
-        else if (tid >= 4 && tid - 4 < t_end - body1) e = body1 + tid - 4;
-        if (e >= 0) {
-          const int x = (int)(e - rb);
-          adv_out[e] = s_r[x];
-          ret_out[e] = s_ret[x];
-          if (frame_out != nullptr) frame_out[e] = reinterpret_cast<const int*>(s_v)[x];
-        }
+    const unsigned m = (__ballot_sync(0xffffffffu, ge) & hmask) >> hshift;
+    const int f = __ffs(m) - 1;  // lane 15 probes hi: always set
+    const int64_t qf = __shfl_sync(0xffffffffu, q, hshift + f);
+    const int64_t qp = __shfl_sync(0xffffffffu, q, hshift + max(f - 1, 0));
+    if (!fin) {
+      const int64_t nlo = f == 0 ? lo : qp + 1;
+      if (qf == nlo || step == 1) {
+        lo = hi = qf;
+        fin = true;
       } else {
-        for (int64_t e = t_first + tid; e < t_end; e += kThreads) {
-          const int x = (int)(e - rb);
-          adv_out[e] = s_r[x];
-          ret_out[e] = s_ret[x];
-          if (frame_out != nullptr) frame_out[e] = reinterpret_cast<const int*>(s_v)[x];
-        }
+        lo = nlo;
+        hi = qf;
       }
-      // next pass to the left
-      const int64_t gja = first_frame(off, ja);
-      jb = gja == f0 ? ja : ja + 1;
-      f1 = f0;
-      __syncthreads();
     }
   }
+  return lo;
+}
 
-  // statistics: one partial per CTA (its segments in a fixed order), then the
-  // last CTA to arrive sums the partials in CTA order -- the grid size is
-  // fixed for a device, so the pooled sums are bitwise deterministic
+__global__ void __launch_bounds__(kThreads, 2)
+gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ vals,
+                const int64_t* __restrict__ off, const uint8_t* __restrict__ done,
+                int64_t n_traj, float g_hi, float g_lo, float decay,
+                float* __restrict__ adv_out, float* __restrict__ ret_out,
+                int32_t* __restrict__ frame_out, Workspace ws, int64_t n_transitions,
+                double* __restrict__ sums_out) {
+  __shared__ double s_red[kWarps * 3];
+  extern __shared__ __align__(16) float s_dyn[];  // [warp][buffer][r | v][kPitch]
+  auto s_buf = reinterpret_cast<float (*)[2][2][kPitch]>(s_dyn);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t w = (int64_t)blockIdx.x * kWarps + warp;
+  // this warp's trajectories [sa, sb): the ones starting in its 1/W share of
+  // the transitions (balanced by transition count, fixed for a given grid)
+  int64_t sa, sb;
+  {
+    const int half = lane >> 4, hl = lane & 15;
+    const int64_t target = (int64_t)(((__int128)(w + half) * n_transitions + W - 1) / W);
+    const int64_t x = half_warp_lower_bound(off, n_traj, target, hl,
+                                            half ? 0xffff0000u : 0x0000ffffu, half ? 16 : 0);
+    sa = __shfl_sync(0xffffffffu, x, 0);
+    sb = w + 1 == W ? n_traj : __shfl_sync(0xffffffffu, x, 16);
+  }
+  double S = 0.0, Q = 0.0;
+  int nbad = 0;
+
+  // chunk sequence: trajectory s from its end leftwards, chunks [cb, e), e -= 256.
+  // Offsets and the done flag are prefetched one trajectory ahead (off[s+1]
+  // is already known when s starts, so one new load per trajectory).
+  struct Ck { int64_t s, t0, T, cb, e; bool dn; };
+  int64_t pf_t0 = 0, pf_t1 = 0;
+  int pf_dn = 0;
+  if (sa < sb) {
+    pf_t0 = __ldg(off + sa);
+    pf_t1 = __ldg(off + sa + 1);
+    pf_dn = __ldg(done + sa);
+  }
+  auto first_chunk = [&](int64_t s) -> Ck {  // s = the prefetched trajectory
+    Ck c{s, 0, 0, 0, 0, false};
+    if (s < sb) {
+      c.t0 = pf_t0;
+      c.T = pf_t1 - pf_t0;
+      c.dn = pf_dn != 0;
+      c.e = c.T;
+      c.cb = c.e > kChunkSteps ? c.e - kChunkSteps : 0;
+      if (s + 1 < sb) {
+        pf_t0 = pf_t1;
+        pf_t1 = __ldg(off + s + 2);
+        pf_dn = __ldg(done + s + 1);
+      }
+    }
+    return c;
+  };
+  auto next_chunk = [&](const Ck& c) -> Ck {
+    if (c.cb > 0) {
+      Ck n = c;
+      n.e = c.cb;
+      n.cb = n.e > kChunkSteps ? n.e - kChunkSteps : 0;
+      return n;
+    }
+    return first_chunk(c.s + 1);
+  };
+  // stage chunk c (r[cb, e), v[cb, e]) into buffer b: 4-byte async copies,
+  // step i at slot i (rows coalesced), the value after the chunk at slot nv
+  auto stage = [&](const Ck& c, int b) {
+    if (c.s >= sb) return;
+    const int nv = (int)(c.e - c.cb);
+    const float* rc = rewards + c.t0 + c.cb + lane;
+    const float* vc = vals + c.t0 + c.s + c.cb;
+    float* sr = s_buf[warp][b][0] + lane;
+    float* sv = s_buf[warp][b][1] + lane;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      if (32 * j < nv) {  // warp-uniform row guard, lane predicate inside
+        if (32 * j + lane < nv) {
+          cp_async4(sr + 32 * j, rc + 32 * j);
+          cp_async4(sv + 32 * j, vc + lane + 32 * j);
+        }
+      }
+    }
+    if (lane == 0) cp_async4(s_buf[warp][b][1] + nv, vc + nv);
+  };
+
+  Ck cur = first_chunk(sa);
+  stage(cur, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  float carry = 0.f;  // A right of the current chunk (0 past a trajectory's end)
+  for (int it = 0; cur.s < sb; ++it) {
+    const int b = it & 1;
+    const Ck nxt = next_chunk(cur);
+    stage(nxt, b ^ 1);  // its buffer was drained by the previous chunk
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const int nv = (int)(cur.e - cur.cb);
+    const int kd = (nv + 31) >> 5;  // steps per lane (warp-uniform)
+    float* sr = s_buf[warp][b][0] + kd * lane;  // this lane's steps kd*l .. kd*l + kd - 1
+    float* sv = s_buf[warp][b][1] + kd * lane;
+    const int nl = nv - kd * lane;                          // this lane's valid steps
+    const int kl = (int)(cur.T - 1 - cur.cb) - kd * lane;   // lane-relative last step
+    const bool dn = cur.dn;
+    float dl[kItems];
+    float vnext = sv[min(kd, max(nl, 0))];  // v after the lane's last valid step
+    float B = 0.f, C = 1.f;  // the lane's composed map (right to left)
+#pragma unroll
+    for (int k = kItems - 1; k >= 0; --k) {
+      if (k < kd) {
+        const float vi = sv[k];
+        const float ri = sr[k];
+        const bool ok = k < nl;
+        const bool last = k == kl;
+        // delta = r + gamma v' - v with gamma = g_hi + g_lo: fma(g_hi, v', -v) is
+        // exact before its one rounding, so the error is relative to the TD
+        // error, not to |v| (done: the bootstrap value is 0, trainer.py:92-93)
+        const float vx = (last && dn) ? 0.f : vnext;
+        const float d = fmaf(g_lo, vx, fmaf(g_hi, vx, -vi)) + ri;
+        dl[k] = ok ? d : 0.f;
+        const float ck = ok ? (last ? 0.f : decay) : 1.f;
+        vnext = vi;
+        B = fmaf(ck, B, dl[k]);
+        C *= ck;
+      }
+    }
+    // exclusive suffix scan of the lane maps: the map of lanes (lane, 31]
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float ob = __shfl_down_sync(0xffffffffu, B, o);
+      const float oc = __shfl_down_sync(0xffffffffu, C, o);
+      if (lane + o < 32) {
+        B = fmaf(C, ob, B);
+        C *= oc;
+      }
+    }
+    float eb = __shfl_down_sync(0xffffffffu, B, 1), ec = __shfl_down_sync(0xffffffffu, C, 1);
+    if (lane == 31) { eb = 0.f; ec = 1.f; }
+    float A = fmaf(ec, carry, eb);
+    __syncwarp();  // every lane has read its neighbour's v before slots turn into outputs
+    float Sf = 0.f, Qf = 0.f;
+#pragma unroll
+    for (int k = kItems - 1; k >= 0; --k) {
+      if (k < kd && k < nl) {
+        A = fmaf(k == kl ? 0.f : decay, A, dl[k]);
+        const float rt = A + sv[k];
+        sr[k] = A;
+        sv[k] = rt;
+        Sf += A;
+        Qf = fmaf(A, A, Qf);
+        nbad += (fabsf(A) <= FLT_MAX && fabsf(rt) <= FLT_MAX) ? 0 : 1;
+      }
+    }
+    S += (double)Sf;
+    Q += (double)Qf;
+    carry = __shfl_sync(0xffffffffu, A, 0);  // A at the chunk's first step
+    __syncwarp();
+    // coalesced write-back of the chunk
+    const float* sr0 = s_buf[warp][b][0] + lane;
+    const float* sv0 = s_buf[warp][b][1] + lane;
+    float* ac = adv_out + cur.t0 + cur.cb + lane;
+    float* rtc = ret_out + cur.t0 + cur.cb + lane;
+    int32_t* fc = frame_out != nullptr ? frame_out + cur.t0 + cur.cb + lane : nullptr;
+    const int32_t fb = (int32_t)(cur.t0 + cur.s + cur.cb) + lane;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      if (32 * j >= nv) break;  // warp-uniform
+      if (32 * j + lane < nv) {
+        __stcs(ac + 32 * j, sr0[32 * j]);
+        __stcs(rtc + 32 * j, sv0[32 * j]);
+        if (fc != nullptr) __stcs(fc + 32 * j, fb + 32 * j);
+      }
+    }
+    __syncwarp();  // the buffer is restaged two chunks on
+    if (nxt.s != cur.s) carry = 0.f;  // next chunk starts a new trajectory at its end
+    cur = nxt;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+
+  // statistics: one partial per CTA (its warps' trajectories in a fixed order),
+  // then the last CTA to arrive sums the partials in CTA order -- the grid size
+  // is fixed for a device, so the pooled sums are bitwise deterministic
   __shared__ bool s_last;
-  double v3[3] = {S, Q, bad};
+  double v3[3] = {S, Q, (double)nbad};
   block_sum_d<3>(v3, s_red);
   if (tid == 0) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) ws.partials[3 * blockIdx.x + c] = v3[c];
     __threadfence();
-    s_last = atomicAdd(ws.counters, 1u) == gridDim.x - 1u;
+    s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1u;
   }
   __syncthreads();
   if (!s_last) return;
@@ -433,8 +345,9 @@ __global__ void normalize_apply_kernel(const float* __restrict__ adv, int64_t n,
 using namespace accel;
 
 extern "C" size_t accel_gae_workspace_size(int64_t n_traj, int64_t n_transitions) {
-  if (n_transitions <= 0 || n_traj <= 0) return 16;
-  return workspace_bytes(ceil_div(n_transitions + n_traj, kSeg));
+  (void)n_traj;
+  (void)n_transitions;
+  return workspace_bytes();
 }
 
 extern "C" int accel_gae_segmented(const float* rewards, const float* values_frames,
@@ -461,40 +374,33 @@ extern "C" int accel_gae_segmented(const float* rewards, const float* values_fra
   }
   if (!rewards || !values_frames || !traj_off || !done || !adv_out || !ret_out || !workspace)
     return fail(kDimension, "NULL buffer passed to accel_gae_segmented");
-  if ((reinterpret_cast<uintptr_t>(rewards) | reinterpret_cast<uintptr_t>(adv_out) |
-       reinterpret_cast<uintptr_t>(ret_out) | reinterpret_cast<uintptr_t>(values_frames) |
-       reinterpret_cast<uintptr_t>(frame_of_out)) & 15)
-    return fail(kDimension, "GAE needs 16-byte aligned rewards/values/adv/ret/frame buffers");
-  const int64_t n_frames = n_transitions + n_traj;
-  const int64_t segs = ceil_div(n_frames, kSeg);
-  if (workspace_bytes_ < workspace_bytes(segs))
+  if (workspace_bytes_ < workspace_bytes())
     return fail(kDimension, "GAE workspace too small (%zu < %zu)", workspace_bytes_,
-                workspace_bytes(segs));
-  Workspace ws = carve(workspace, segs);
-  gae_segment_index_kernel<<<(unsigned)ceil_div(n_traj + 1, 256), 256, 0, s>>>(traj_off, n_traj,
-                                                                            segs, ws);
-  int st = post_launch("gae_segment_index_kernel");
+                workspace_bytes());
+  Workspace ws = carve(workspace);
+  int st = check_cuda(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), s), "gae counter");
   if (st) return st;
   static int grid = 0;
   if (grid == 0) {
-    st = check_cuda(cudaFuncSetAttribute(gae_segment_kernel,
+    st = check_cuda(cudaFuncSetAttribute(gae_warp_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSegSmem), "gae smem");
+                                         (int)kGaeSmem), "gae smem");
     if (st) return st;
     int per_sm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_segment_kernel,
-                                                                  kThreads, kSegSmem),
+    st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_warp_kernel,
+                                                                  kThreads, kGaeSmem),
                     "gae occupancy");
     if (st) return st;
     grid = std::max(1, std::min(per_sm * sms, kMaxGrid));
   }
-  gae_segment_kernel<<<(unsigned)std::min<int64_t>(grid, segs), kThreads, kSegSmem, s>>>(
-      rewards, values_frames, traj_off, done, n_frames, (float)gamma,
+  const int64_t need = ceil_div(ceil_div(n_transitions, 64), kWarps);  // >= 64 steps per warp
+  gae_warp_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, need)), kThreads, kGaeSmem, s>>>(
+      rewards, values_frames, traj_off, done, n_traj, (float)gamma,
       (float)(gamma - (double)(float)gamma), (float)(gamma * lam), adv_out, ret_out,
-      frame_of_out, ws, segs, n_transitions, sums_out);
-  return post_launch("gae_segment_kernel");
+      frame_of_out, ws, n_transitions, sums_out);
+  return post_launch("gae_warp_kernel");
 }
 
 extern "C" int accel_normalize_finalize(const double* sums, double eps, double* stats_out,
