@@ -181,6 +181,54 @@ class ClockSampler:
         return False
 
 
+def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20) -> dict:
+    """cfg2 (BASELINE.json configs[1]): K1 over LIBERO-Long mixes of 4K-64K
+    trajectories (up to 25.5 M transitions, 0.5 GB), device-resident inputs,
+    CUDA events over `reps` back-to-back launches (inputs > L2 at 16K+)."""
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    from paper_2603_18464_b200.workload import libero_long_lengths
+
+    rows = []
+    for n in sizes:
+        lens, dn = libero_long_lengths(np.random.default_rng(n), n)
+        off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens, out=off[1:])
+        N = int(off[-1])
+        g = torch.Generator(device=dev).manual_seed(n)
+        r = torch.randn(N, device=dev, generator=g)
+        v = torch.randn(N + n, device=dev, generator=g)
+        t_off = torch.from_numpy(off).to(dev)
+        d_dev = torch.from_numpy(dn.astype(np.uint8)).to(dev)
+        adv, ret = torch.empty_like(r), torch.empty_like(r)
+        fo = torch.empty(N, dtype=torch.int32, device=dev)
+        sums = torch.empty(4, dtype=torch.float64, device=dev)
+
+        def run():
+            ops.gae_segmented(r, v, t_off, d_dev, 0.99, 0.95, adv=adv, ret=ret, frame_of=fo,
+                              sums=sums)
+
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        byt = 20 * N + 13 * n
+        rows.append({"trajectories": n, "transitions": N, "bytes_per_launch": byt,
+                     "ms_per_launch": ms, "achieved": byt / ms / 1e6,
+                     "frac": byt / ms / 1e6 / peak})
+        del r, v, adv, ret, fo
+    return {"kernel": "accel_gae_segmented (K1)", "unit": "GB/s", "peak": peak,
+            "config": "cfg2: LIBERO-Long mix (50% done T~U[1,520], 50% truncated at 520)",
+            "rows": rows}
+
+
 def cpu_baseline(bundle, inputs_host, lens, done, n_cpu: int, n_steps: int, reps: int = 1):
     """The float64 oracle (reference restatement) on a bounded sample, host cores."""
     from threadpoolctl import threadpool_limits
@@ -399,6 +447,7 @@ def main():
     logp_bytes = M * (4 * A + 8)
     t_logp = float(np.mean(kern.get("token_logp", [float("nan")]))) / 1e3
 
+    sweep = gae_sweep(dev, peak)
     cpu = None
     if not args.no_cpu:
         host_np = {k: v.numpy() for k, v in host.items()}
@@ -421,7 +470,10 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "roofline_gae": {"bytes_per_launch": gae_bytes, "ms_per_launch": t_gae * 1e3,
                          "achieved": gae_bytes / t_gae / 1e9,
-                         "frac": gae_bytes / t_gae / 1e9 / peak, "unit": "GB/s"},
+                         "frac": gae_bytes / t_gae / 1e9 / peak, "unit": "GB/s",
+                         "note": "in-step size (32 MB, L2-resident, latency-bound); "
+                                 "see gae_sweep for the cfg2 sizes"},
+        "gae_sweep": sweep,
         "trainer_roofline": dict(tr_roof, achieved_ms=ms, frac=tr_roof["t_roof_ms"] / ms),
         "roofline_token_logp": {"bytes_per_launch": logp_bytes, "ms_per_launch": t_logp * 1e3,
                                 "achieved": logp_bytes / t_logp / 1e9,
