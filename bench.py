@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-traj", type=int, default=64, help="cpu_baseline sample size")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dz", default="store", choices=["store", "recompute"],
+                    help="store: K4 writes dz rows; recompute: token scalars + frame-blocked "
+                         "recomputing grouped sums")
+    ap.add_argument("--block-chunks", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -341,6 +345,8 @@ def main():
     M = N * d["K"]
     bundle = make_bundle(args.seed, n_steps)
     tr = Trainer(bundle, TrainerConfig(), comm=comm)
+    tr.recompute_dz = args.dz == "recompute"
+    tr.group_block_chunks = args.block_chunks
     inputs = device_inputs(lens, done, args.seed * 1000 + rank, dev)
     bver = np.zeros(n, dtype=np.int64)
 
@@ -435,7 +441,12 @@ def main():
     # factorized head (trainer default): per token dz write (4A) + token/lp_old/lp_new
     # (12); per transition the H2W row read and the g_frame row write (8A) + adv and
     # frame index (8).  DESIGN.md "Kernels / token_loss_fact".
-    loss_bytes = M * (4 * A + 12) + N * (8 * A + 8) if tr.factorized else M * (8 * A + 12) + 4 * N
+    if not tr.factorized:
+        loss_bytes = M * (8 * A + 12) + 4 * N
+    elif tr.recompute_dz:  # 16 B of token scalars replace the 4A-byte dz row
+        loss_bytes = M * (16 + 12) + N * (8 * A + 8)
+    else:
+        loss_bytes = M * (4 * A + 12) + N * (8 * A + 8)
     t_loss = float(np.mean(kern.get("token_loss", [float("nan")]))) / 1e3
     achieved = loss_bytes / t_loss / 1e9
     traffic = None

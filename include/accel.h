@@ -137,6 +137,14 @@ int accel_fact_grid(int64_t N);
 /* epp[(prev*K+k)*A + a] = ep[prev*A + a] + pp[k*A + a] + bias[a] */
 int accel_ep_plus(const float* ep, const float* pp, const float* bias, int A, int K,
                   float* epp, void* stream);
+/* accel_token_loss_fact with tsc_pos (nullable): token t's scalars go to
+ * tsc[tsc_pos[t]] (the sorted position of a frame-blocked grouping). */
+int accel_token_loss_fact2(const float* h2w, const float* epp, const int32_t* frame_of,
+                           const int32_t* tokens, const float* lp_old, const float* adv,
+                           int64_t N, int K, int A, int algo, double sigma, double clip_eps,
+                           double lambda_h, double m_global, const double* fix_stats, float* dz,
+                           void* tsc, const int32_t* tsc_pos, float* g_frame, float* lp_new,
+                           double* stat_part, double* max_part, void* stream);
 int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* frame_of,
                           const int32_t* tokens, const float* lp_old, const float* adv,
                           int64_t N, int K, int A, int algo, double sigma, double clip_eps,
@@ -150,8 +158,13 @@ int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* fra
  * Reference: the np.add.at of models.py:195 (dc rows grouped by prev token). */
 int accel_fact_group_sum(const float* h2w, const float* epp, const int32_t* frame_of,
                          const int32_t* tokens, const void* tsc, const int32_t* perm,
-                         const int64_t* seg_off, const int64_t* piece_off, int nkeys, int K,
-                         int A, int piece_rows, int64_t n_pieces, float* piece_out, void* stream);
+                         const int64_t* seg_off, const int64_t* piece_off, int nkeys,
+                         int key_mod, int K, int A, int piece_rows, int64_t n_pieces,
+                         float* piece_out, void* stream);
+/* key_mod > 0: the grouping is frame-blocked (accel_group_by_key_blocked), its
+ * composite key is block * key_mod + (prev * K + k) and the EPP row is
+ * key % key_mod; consecutive pieces then gather H2W rows of one block of
+ * frames, which stays L2-resident. */
 /* Dprev f32[A+1, A] = sum_k dpk[j, k]; Dpos f32[K, A] = sum_j dpk[j, k]
  * from the (prev, k)-grouped dz sums dpk f32[(A+1)*K, A]. */
 int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, float* dpos,
@@ -205,6 +218,36 @@ int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
  * deterministic); piece_buf f32[accel_group_max_pieces(R, nkeys) * D].
  * vals = NULL: only the key pass (piece_buf already filled, e.g. by
  * accel_fact_group_sum). */
+/* Frame-blocked variant: rows are cut into blocks of cpb 4096-row chunks
+ * (cpb <= 0: one block) and sorted stably by (block, key); seg_off and
+ * piece_off cover the blocks * nkeys composite keys (block-major). */
+size_t accel_group_workspace_size_blocked(int64_t R, int nkeys, int64_t cpb);
+int64_t accel_group_max_pieces_blocked(int64_t R, int nkeys, int64_t cpb);
+int64_t accel_group_blocks(int64_t R, int64_t cpb);
+int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nkeys, int64_t cpb,
+                               int32_t* perm, int64_t* seg_off, int64_t* piece_off,
+                               int32_t* piece_key, void* workspace, size_t workspace_bytes,
+                               void* stream);
+/* piece_key (nullable) i32[accel_group_max_pieces_blocked]: owning composite key
+ * of each piece. */
+/* Sorted per-row metadata of a grouping (fixed per batch): row_frame[r] =
+ * frame_of[perm[r] / K], row_tok[r] = tokens[perm[r]], pos[perm[r]] = r. */
+int accel_sorted_rows(const int32_t* perm, const int32_t* frame_of, const int32_t* tokens,
+                      int64_t R, int K, int32_t* row_frame, int32_t* row_tok, int32_t* pos,
+                      void* stream);
+/* accel_fact_group_sum over a blocked grouping with sorted metadata: one CTA
+ * per piece (in (block, key) order), the piece's rows contiguous in row_frame /
+ * row_tok / tsc_sorted (the loss kernel's token scalars at their sorted
+ * positions, accel_token_loss_fact2 with tsc_pos = pos). */
+int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* row_frame,
+                          const int32_t* row_tok, const void* tsc_sorted, const int64_t* seg_off,
+                          const int64_t* piece_off, const int32_t* piece_key, int nkeys,
+                          int key_mod, int A, int64_t n_pieces_max, float* piece_out,
+                          void* stream);
+/* out[nkeys, D] = sum over blocks (in order) of the pieces (in order) of the
+ * composite keys b * nkeys + key: the key pass of a blocked grouping. */
+int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off, int nkeys,
+                              int nblocks, int D, float* out, void* stream);
 int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
                            const int64_t* seg_off, const int64_t* piece_off, int nkeys,
                            int64_t n_pieces, float* piece_buf, float* out, void* stream);

@@ -102,16 +102,17 @@ class DeviceTrainBatch:
         return self._get("ret", lambda: self.ret.double().cpu().numpy())
 
     def ensure_groupings(self, n_steps: int, bad_count, factorized: bool = True,
-                         frame_space: bool = False) -> None:
+                         frame_space: bool = False, pk_cpb: int = 0) -> None:
         """Stable key sorts for the deterministic scatter-adds (fixed per batch):
         (prev token, chunk position) for the factorized head, prev token for the
         materialized head, step index for the value head's e_step (over
         transitions, or over all frames when the value backward runs in frame
-        space)."""
+        space).  pk_cpb > 0: the (prev, k) sort is frame-blocked (blocks of
+        pk_cpb 4096-token chunks) for the dz-recomputing grouped sums."""
         N, K, A = self.n_transitions, self.chunk_len, self.n_actions
-        if factorized and self.pk_group is None:
+        if factorized and (self.pk_group is None or self.pk_group.cpb != pk_cpb):
             self.pk_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A, with_pos=True),
-                                         (A + 1) * K)
+                                         (A + 1) * K, cpb=pk_cpb)
         if not factorized and self.prev_group is None:
             self.prev_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A), A + 1)
         if frame_space:

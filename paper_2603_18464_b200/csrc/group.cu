@@ -51,10 +51,16 @@ __global__ void step_keys_kernel(const int32_t* __restrict__ steps,
   if (nbad) atomicAdd(bad, nbad);  // integer count: order-independent
 }
 
-// counts[key * n_chunks + chunk]
+// counts[((chunk / cpb) * nkeys + key) * cpb + chunk % cpb]: the row range is cut
+// into blocks of cpb chunks and the scan order is block-major, key-minor, chunk
+// last (cpb = n_chunks: plain key-major order).  Composite key = block * nkeys + key.
+__device__ __forceinline__ int64_t count_idx(int64_t chunk, int key, int nkeys, int64_t cpb) {
+  return ((chunk / cpb) * nkeys + key) * cpb + chunk % cpb;
+}
+
 __global__ void __launch_bounds__(kThreads)
 chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
-                  int* __restrict__ counts) {
+                  int64_t cpb, int* __restrict__ counts) {
   extern __shared__ int s_hist[];  // [kWarps][nkeys]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* h = s_hist + warp * nkeys;
@@ -65,7 +71,7 @@ chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_
     const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
     for (int64_t r = r0 + lane; r < r1; r += 32) atomicAdd(h + __ldg(keys + r), 1);
     __syncwarp();
-    for (int j = lane; j < nkeys; j += 32) counts[(int64_t)j * n_chunks + chunk] = h[j];
+    for (int j = lane; j < nkeys; j += 32) counts[count_idx(chunk, j, nkeys, cpb)] = h[j];
   }
 }
 
@@ -75,6 +81,7 @@ chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_
 __global__ void __launch_bounds__(1024)
 segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks, int64_t R,
                        int64_t* __restrict__ seg_off, int64_t* __restrict__ piece_off) {
+  // (composite keys: nkeys = blocks * keys, n_chunks = chunks per block)
   __shared__ int64_t s_tot[1024];
   const int t = threadIdx.x;
   const int per = (nkeys + blockDim.x - 1) / blockDim.x;
@@ -110,13 +117,13 @@ segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks
 
 __global__ void __launch_bounds__(kThreads)
 stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
-                      const int* __restrict__ base, int32_t* __restrict__ perm) {
+                      int64_t cpb, const int* __restrict__ base, int32_t* __restrict__ perm) {
   extern __shared__ int s_ctr[];  // [kWarps][nkeys]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
   if (chunk >= n_chunks) return;
   int* ctr = s_ctr + warp * nkeys;
-  for (int j = lane; j < nkeys; j += 32) ctr[j] = base[(int64_t)j * n_chunks + chunk];
+  for (int j = lane; j < nkeys; j += 32) ctr[j] = base[count_idx(chunk, j, nkeys, cpb)];
   __syncwarp();
   const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
   const unsigned lt = (1u << lane) - 1u;
@@ -299,12 +306,98 @@ key_sum4_kernel(const float4* __restrict__ piece_out, const int64_t* __restrict_
   }
 }
 
+// Blocked grouping: Dk[key] = sum over blocks b (in order) of the pieces of the
+// composite key b * nkeys + key (in order).  One CTA per key: 64 float4 columns
+// x 16 block-lanes (lane l folds blocks b = l, l + 16, ...; a block's pieces
+// are a contiguous range, four loads in flight), lanes combined in order.
+constexpr int kFoldThreads = 1024;
+__global__ void __launch_bounds__(kFoldThreads)
+fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
+                           const int64_t* __restrict__ piece_off, int nkeys, int nblocks, int D4,
+                           float4* __restrict__ out) {
+  __shared__ float4 s4[kFoldThreads];
+  const int key = blockIdx.x;
+  const int span = D4 <= kFoldThreads && kFoldThreads % D4 == 0 ? D4 : kFoldThreads;
+  const int sub = kFoldThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  for (int d0 = 0; d0 < D4; d0 += span) {
+    const int d = d0 + lc;
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (d < D4) {
+      for (int b = lr; b < nblocks; b += sub) {
+        const int64_t ck = (int64_t)b * nkeys + key;
+        const int64_t p0 = __ldg(piece_off + ck), p1 = __ldg(piece_off + ck + 1);
+        int64_t p = p0;
+        for (; p + 3 < p1; p += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 x = __ldg(piece_out + (p + u) * D4 + d);
+            a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+          }
+        }
+        for (int u = 0; p < p1; ++p, ++u) {
+          const float4 x = __ldg(piece_out + p * D4 + d);
+          a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+        }
+      }
+    }
+    s4[threadIdx.x] = make_float4(((a[0].x + a[1].x) + a[2].x) + a[3].x,
+                                  ((a[0].y + a[1].y) + a[2].y) + a[3].y,
+                                  ((a[0].z + a[1].z) + a[2].z) + a[3].z,
+                                  ((a[0].w + a[1].w) + a[2].w) + a[3].w);
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D4) {
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s2 = 0; s2 < sub; ++s2) {
+        const float4 y = s4[s2 * span + threadIdx.x];
+        r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
+      }
+      out[(int64_t)key * D4 + d0 + threadIdx.x] = r;
+    }
+    __syncthreads();
+  }
+}
+
+// piece_key[p] = the composite key owning piece p
+__global__ void piece_keys_kernel(const int64_t* __restrict__ piece_off, int64_t nk,
+                                  int32_t* __restrict__ piece_key) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nk) return;
+  for (int64_t p = piece_off[j]; p < piece_off[j + 1]; ++p) piece_key[p] = (int32_t)j;
+}
+
+// Parallel segment offsets (many composite keys): seg_off[j] = base[j * cpb],
+// pcount[j] = pieces of key j; piece_off = exclusive scan of pcount (CUB).
+__global__ void seg_counts_kernel(const int* __restrict__ base, int64_t nk, int64_t cpb, int64_t R,
+                                  int64_t* __restrict__ seg_off, int64_t* __restrict__ pcount) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nk) return;
+  if (j == nk) {
+    seg_off[nk] = R;
+    pcount[nk] = 0;
+    return;
+  }
+  const int64_t a = base[j * cpb];
+  const int64_t b = j + 1 < nk ? (int64_t)base[(j + 1) * cpb] : R;
+  seg_off[j] = a;
+  pcount[j] = ceil_div(b - a, (int64_t)kPiece);
+}
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t cub_scan_bytes(int64_t n) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const int*>(nullptr),
                                 static_cast<int*>(nullptr), (int)std::max<int64_t>(n, 1));
+  return bytes;
+}
+
+size_t cub_scan64_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const int64_t*>(nullptr),
+                                static_cast<int64_t*>(nullptr), (int)std::max<int64_t>(n, 1));
   return bytes;
 }
 
@@ -334,32 +427,60 @@ extern "C" int accel_step_keys(const int32_t* steps, const int32_t* frame_of, in
   return post_launch("step_keys_kernel");
 }
 
-extern "C" size_t accel_group_workspace_size(int64_t R, int nkeys) {
+namespace {
+int64_t blocks_of(int64_t R, int64_t cpb) {
   const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
-  const int64_t n = (int64_t)nkeys * n_chunks;
-  return 2 * align256(sizeof(int) * (size_t)n) + align256(cub_scan_bytes(n)) + 256;
+  return cpb <= 0 ? 1 : ceil_div(n_chunks, cpb);
+}
+int64_t cpb_of(int64_t R, int64_t cpb) {
+  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
+  return cpb <= 0 ? n_chunks : std::min(cpb, n_chunks);
+}
+}  // namespace
+
+extern "C" size_t accel_group_workspace_size_blocked(int64_t R, int nkeys, int64_t cpb) {
+  const int64_t c = cpb_of(R, cpb), nb = blocks_of(R, c);
+  const int64_t n = (int64_t)nkeys * nb * c;
+  const int64_t nk = (int64_t)nkeys * nb + 1;
+  return 2 * align256(sizeof(int) * (size_t)n) +
+         std::max(align256(cub_scan_bytes(n)),
+                  align256(sizeof(int64_t) * (size_t)nk) + align256(cub_scan64_bytes(nk))) + 256;
+}
+
+extern "C" size_t accel_group_workspace_size(int64_t R, int nkeys) {
+  return accel_group_workspace_size_blocked(R, nkeys, 0);
+}
+
+extern "C" int64_t accel_group_blocks(int64_t R, int64_t cpb) { return blocks_of(R, cpb_of(R, cpb)); }
+
+extern "C" int64_t accel_group_max_pieces_blocked(int64_t R, int nkeys, int64_t cpb) {
+  return ceil_div(R, kPiece) + (int64_t)nkeys * blocks_of(R, cpb_of(R, cpb));
 }
 
 extern "C" int64_t accel_group_max_pieces(int64_t R, int nkeys) {
-  return ceil_div(R, kPiece) + nkeys;
+  return accel_group_max_pieces_blocked(R, nkeys, 0);
 }
 
-// perm[R]: row ids sorted stably by key; seg_off[nkeys+1]; piece_off[nkeys+1]
-extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
-                                  int64_t* seg_off, int64_t* piece_off, void* workspace,
-                                  size_t workspace_bytes, void* stream) {
+// perm[R]: row ids sorted stably by composite key (block of cpb 4096-row chunks,
+// key); seg_off / piece_off [blocks * nkeys + 1].  cpb <= 0: one block.
+extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nkeys, int64_t cpb,
+                                          int32_t* perm, int64_t* seg_off, int64_t* piece_off,
+                                          int32_t* piece_key, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
   if (R < 0 || nkeys < 1) return fail(kDimension, "group_by_key: bad sizes");
   if (nkeys * (size_t)kWarps * sizeof(int) > 200 * 1024)
     return fail(kDimension, "group_by_key: %d keys exceed the shared-memory histogram", nkeys);
   if (R >= ((int64_t)1 << 31)) return fail(kDimension, "group_by_key: R exceeds int32 range");
   if (!keys || !perm || !seg_off || !piece_off || !workspace)
     return fail(kDimension, "group_by_key: NULL buffer");
-  if (workspace_bytes < accel_group_workspace_size(R, nkeys))
+  if (workspace_bytes < accel_group_workspace_size_blocked(R, nkeys, cpb))
     return fail(kDimension, "group_by_key: workspace too small");
   cudaStream_t s = as_stream(stream);
   const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
-  const int64_t n = (int64_t)nkeys * n_chunks;
-  if (n >= ((int64_t)1 << 31)) return fail(kDimension, "group_by_key: too many counters");
+  const int64_t c = cpb_of(R, cpb), nb = blocks_of(R, c);
+  const int64_t n = (int64_t)nkeys * nb * c;
+  if (n >= ((int64_t)1 << 31) || nkeys * nb >= ((int64_t)1 << 31))
+    return fail(kDimension, "group_by_key: too many counters");
   char* ws = static_cast<char*>(workspace);
   int* counts = reinterpret_cast<int*>(ws);
   int* base = reinterpret_cast<int*>(ws + align256(sizeof(int) * (size_t)n));
@@ -373,16 +494,59 @@ extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int
     cudaFuncSetAttribute(stable_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   }
-  chunk_hist_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, counts);
+  if (nb * c != n_chunks) {  // the last block's missing chunks count zero rows
+    if ((st = check_cuda(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n, s), "group memset")))
+      return st;
+  }
+  chunk_hist_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, counts);
   if ((st = post_launch("chunk_hist_kernel"))) return st;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, counts, base, (int)n, s);
   if (e != cudaSuccess) return fail(kCuda, "DeviceScan: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  segment_offsets_kernel<<<1, 1024, 0, s>>>(base, nkeys, n_chunks, R, seg_off, piece_off);
-  if ((st = post_launch("segment_offsets_kernel"))) return st;
+  if (nb == 1) {
+    segment_offsets_kernel<<<1, 1024, 0, s>>>(base, nkeys, c, R, seg_off, piece_off);
+    if ((st = post_launch("segment_offsets_kernel"))) return st;
+  } else {  // many composite keys: parallel counts + a CUB scan of the piece counts
+    const int64_t nk = (int64_t)nkeys * nb;
+    int64_t* pcount = reinterpret_cast<int64_t*>(cub_tmp);
+    void* tmp2 = static_cast<char*>(cub_tmp) + align256(sizeof(int64_t) * (size_t)(nk + 1));
+    size_t b2 = cub_scan64_bytes(nk + 1);
+    seg_counts_kernel<<<(unsigned)ceil_div(nk + 1, 256), 256, 0, s>>>(base, nk, c, R, seg_off,
+                                                                       pcount);
+    if ((st = post_launch("seg_counts_kernel"))) return st;
+    e = cub::DeviceScan::ExclusiveSum(tmp2, b2, pcount, piece_off, (int)(nk + 1), s);
+    if (e != cudaSuccess) return fail(kCuda, "DeviceScan: %s", cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (piece_key != nullptr) {
+    const int64_t nk = (int64_t)nkeys * nb;
+    piece_keys_kernel<<<(unsigned)ceil_div(nk, 256), 256, 0, s>>>(piece_off, nk, piece_key);
+    if ((st = post_launch("piece_keys_kernel"))) return st;
+  }
   if (R == 0) return kOk;
-  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, base, perm);
+  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, base, perm);
   return post_launch("stable_scatter_kernel");
+}
+
+// perm[R]: row ids sorted stably by key; seg_off[nkeys+1]; piece_off[nkeys+1]
+extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
+                                  int64_t* seg_off, int64_t* piece_off, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  return accel_group_by_key_blocked(keys, R, nkeys, 0, perm, seg_off, piece_off, nullptr,
+                                    workspace, workspace_bytes, stream);
+}
+
+// out[nkeys, D] = sum over blocks of the piece sums of composite keys b * nkeys + key
+extern "C" int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off,
+                                         int nkeys, int nblocks, int D, float* out, void* stream) {
+  if (nkeys < 1 || nblocks < 1 || D < 4 || (D & 3)) return fail(kDimension, "fold_blocked: bad sizes");
+  if (!piece_buf || !piece_off || !out) return fail(kDimension, "fold_blocked: NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(piece_buf) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(kDimension, "fold_blocked: buffers must be 16B aligned");
+  fold_blocked_pieces_kernel<<<nkeys, kFoldThreads, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(piece_buf),
+                                                    piece_off, nkeys, nblocks, D / 4,
+                                                    reinterpret_cast<float4*>(out));
+  return post_launch("fold_blocked_pieces_kernel");
 }
 
 // out[nkeys, D] = grouped sums of vals[R, D] rows; piece_buf holds

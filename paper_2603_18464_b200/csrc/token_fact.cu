@@ -663,7 +663,9 @@ __host__ __device__ constexpr int fact2_warp_floats(int K, int A) { return (2 * 
 
 // KT > 0: K == KT at compile time (no per-token guards: the unrolled token loops
 // interleave); KT == 0: runtime K <= KMAX.
-template <int VPL, int KMAX, int KT>
+// SC: write the per-token scalars {nm2, Ac, Cc, coef} (tsc) instead of the dz
+// rows; the frame-blocked grouped sums recompute dz (fact_group_sum_kernel).
+template <int VPL, int KMAX, int KT, bool SC>
 __global__ void __launch_bounds__(kF2MaxWarps * 32, 2)
 token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
                         const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
@@ -671,7 +673,8 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
                         int64_t N, int K_rt, LossParams prm, const double* __restrict__ fix_stats,
                         float* __restrict__ dz, float* __restrict__ g_frame,
                         float* __restrict__ lp_new, double* __restrict__ stat_part,
-                        double* __restrict__ max_part, unsigned* __restrict__ work_ctr) {
+                        double* __restrict__ max_part, unsigned* __restrict__ work_ctr,
+                        float4* __restrict__ tsc, const int32_t* __restrict__ tsc_pos) {
   constexpr int A = VPL * 32;
   constexpr int Q = VPL / 4;  // float4 chunks per lane (column q * 128 + lane * 4 + r)
   constexpr int P = VPL / 2;  // float2 pairs per lane
@@ -863,6 +866,11 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
     const float Cc = -(Ac * sdn) - coef * inv_s;
     const float d2t = fmaf(z_tok, kLog2e, -mx_l * kLog2e);  // == the row's d2 at column tok
     const float patch = fmaf(ex2_ftz(d2t), fmaf(Ac, d2t, Cc), coef);
+    if (SC && own) {  // at the token's sorted position when the grouping provides it
+      const int64_t t = i * K + lane;
+      tsc[tsc_pos != nullptr ? (int64_t)__ldg(tsc_pos + t) : t] =
+          make_float4(-mx_l * kLog2e, Ac, Cc, coef);
+    }
     if (own && !cx.fixup) {
       lp_new[i * K + lane] = lpn;
       st_ent += (double)Hk;
@@ -883,7 +891,7 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
     float2 g2[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) g2[p] = make_float2(0.f, 0.f);
-    float* dz_i = dz + i * K * A;
+    float* dz_i = SC ? nullptr : dz + i * K * A;
     const float2 n20 = make_float2(-mx0 * kLog2e, -mx0 * kLog2e);
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
@@ -911,18 +919,20 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
           d2[p] = __fmul2_rn(e2, __ffma2_rn(A2, d2[p], C2));
           g2[p] = __fadd2_rn(g2[p], d2[p]);
         }
-        float* drow = dz_i + k * A;
+        if (!SC) {
+          float* drow = dz_i + k * A;
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
-          __stcs(reinterpret_cast<float4*>(drow + q * 128 + lane * 4),
-                 make_float4(d2[2 * q].x, d2[2 * q].y, d2[2 * q + 1].x, d2[2 * q + 1].y));
+          for (int q = 0; q < Q; ++q)
+            __stcs(reinterpret_cast<float4*>(drow + q * 128 + lane * 4),
+                   make_float4(d2[2 * q].x, d2[2 * q].y, d2[2 * q + 1].x, d2[2 * q + 1].y));
+        }
       }
     }
     // one-hot part: dz[tok_k] += coef_k (after every lane's row stores) and
     // G[tok_k] += coef_k, duplicates summed in token order by their first lane
     s_cf[warp][lane] = coef;
     __syncwarp();
-    if (own) dz_i[lane * A + tok] = patch;
+    if (!SC && own) dz_i[lane * A + tok] = patch;
     const unsigned same = __match_any_sync(0xffffffffu, own && !bad_tok ? tok : -1 - lane);
     if (own && !bad_tok && (same & ((1u << lane) - 1u)) == 0) {
       float acc = coef;
@@ -1025,7 +1035,8 @@ fact_group_sum_kernel(const float* __restrict__ h2w, const float* __restrict__ e
                       const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
                       const float4* __restrict__ tsc, const int32_t* __restrict__ perm,
                       const int64_t* __restrict__ seg_off, const int64_t* __restrict__ piece_off,
-                      int nkeys, int K, int A, int piece_rows, float* __restrict__ piece_out) {
+                      int nkeys, int key_mod, int K, int A, int piece_rows,
+                      float* __restrict__ piece_out) {
   // smem: epp row [A] | partials [kGsThreads] float4 | per-token frame, token, scalars
   extern __shared__ __align__(16) float s_gs[];
   __shared__ int s_frame[kGsRows], s_tok[kGsRows];
@@ -1042,7 +1053,9 @@ fact_group_sum_kernel(const float* __restrict__ h2w, const float* __restrict__ e
   const int nr = (int)min(seg_off[key + 1] - r0, (int64_t)piece_rows);
   float* s_ep = s_gs;
   float4* s_part = reinterpret_cast<float4*>(s_gs + A);
-  for (int c = threadIdx.x; c < A; c += kGsThreads) s_ep[c] = __ldg(epp + (int64_t)key * A + c);
+  // composite keys (frame-blocked grouping): the EPP row is key % key_mod
+  const int64_t erow = key_mod > 0 ? key % key_mod : key;
+  for (int c = threadIdx.x; c < A; c += kGsThreads) s_ep[c] = __ldg(epp + erow * A + c);
   // the piece's token metadata, gathered once (one token per thread)
   for (int r = threadIdx.x; r < nr; r += kGsThreads) {
     const int64_t t = __ldg(perm + r0 + r);
@@ -1100,6 +1113,111 @@ fact_group_sum_kernel(const float* __restrict__ h2w, const float* __restrict__ e
   }
 }
 
+// Recompute over a frame-blocked grouping with sorted metadata: one CTA per
+// piece, pieces in (block, key) order so concurrently running CTAs gather H2W
+// rows of one block of frames (L2-resident).  The piece's rows are contiguous
+// in the sorted arrays row_frame / row_tok (fixed per batch) and tsc_sorted
+// (written by the loss kernel at each token's sorted position), so the only
+// dependent load before the sums is piece_key -> (seg_off, piece_off).  Eight
+// row loads per lane are in flight; same float operations per element as the
+// loss kernel.
+constexpr int kGs2Threads = 256;
+__global__ void __launch_bounds__(kGs2Threads)
+fact_group_sum2_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
+                       const int32_t* __restrict__ row_frame, const int32_t* __restrict__ row_tok,
+                       const float4* __restrict__ tsc_sorted, const int64_t* __restrict__ seg_off,
+                       const int64_t* __restrict__ piece_off, const int32_t* __restrict__ piece_key,
+                       int nkeys, int key_mod, int A, float* __restrict__ piece_out) {
+  extern __shared__ __align__(16) float s_gs[];  // epp row [A] | partials [threads] float4
+  __shared__ int s_frame[kGsRows], s_tok[kGsRows];
+  __shared__ float4 s_sc[kGsRows];
+  const int64_t p = blockIdx.x;
+  if (p >= __ldg(piece_off + nkeys)) return;
+  const int tid = threadIdx.x;
+  const int key = __ldg(piece_key + p);
+  const int64_t r0 = __ldg(seg_off + key) + (p - __ldg(piece_off + key)) * kGsRows;
+  const int nr = (int)min(__ldg(seg_off + key + 1) - r0, (int64_t)kGsRows);
+  const int64_t erow = key_mod > 0 ? key % key_mod : key;
+  for (int c = tid; c < A; c += kGs2Threads) s_gs[c] = __ldg(epp + erow * A + c);
+  if (tid < nr) {
+    s_frame[tid] = __ldg(row_frame + r0 + tid);
+    s_tok[tid] = __ldg(row_tok + r0 + tid);
+    s_sc[tid] = __ldg(tsc_sorted + r0 + tid);
+  }
+  __syncthreads();
+  const int A4 = A >> 2;
+  const int span = A4 <= kGs2Threads && kGs2Threads % A4 == 0 ? A4 : kGs2Threads;
+  const int sub = kGs2Threads / span;
+  const int lr = tid / span, lc = tid % span;
+  float4* s_part = reinterpret_cast<float4*>(s_gs + A);
+  for (int c0 = 0; c0 < A4; c0 += span) {
+    const int c4 = c0 + lc;
+    float4 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c4 < A4) {
+      const float4 ep = reinterpret_cast<const float4*>(s_gs)[c4];
+      for (int r = lr; r < nr; r += 8 * sub) {
+        float4 h[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int rr = r + u * sub;
+          h[u] = rr < nr ? __ldg(reinterpret_cast<const float4*>(h2w + (int64_t)s_frame[rr] * A) + c4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int rr = r + u * sub;
+          if (rr < nr) {
+            const float4 sc = s_sc[rr];
+            const int tok = s_tok[rr];
+            const float d[4] = {h[u].x + ep.x, h[u].y + ep.y, h[u].z + ep.z, h[u].w + ep.w};
+            float o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float d2 = fmaf(d[q], kLog2e, sc.x);
+              o[q] = ex2_ftz(d2) * fmaf(sc.y, d2, sc.z);
+            }
+            if ((tok >> 2) == c4) o[tok & 3] += sc.w;
+            float4& a4 = acc[u & 3];
+            a4.x += o[0]; a4.y += o[1]; a4.z += o[2]; a4.w += o[3];
+          }
+        }
+      }
+    }
+    float4 t = acc[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) { t.x += acc[u].x; t.y += acc[u].y; t.z += acc[u].z; t.w += acc[u].w; }
+    s_part[tid] = t;
+    __syncthreads();
+    if (tid < span && c0 + tid < A4) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s2 = 0; s2 < sub; ++s2) {
+        const float4 y = s_part[s2 * span + tid];
+        a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
+      }
+      reinterpret_cast<float4*>(piece_out + p * A)[c0 + tid] = a;
+    }
+    __syncthreads();
+  }
+}
+
+// Sorted per-row metadata of a grouping (fixed per batch): row_frame[r] =
+// frame_of[perm[r] / K], row_tok[r] = tokens[perm[r]], pos[perm[r]] = r.
+__global__ void sorted_rows_kernel(const int32_t* __restrict__ perm,
+                                   const int32_t* __restrict__ frame_of,
+                                   const int32_t* __restrict__ tokens, int64_t R, int K,
+                                   int32_t* __restrict__ row_frame, int32_t* __restrict__ row_tok,
+                                   int32_t* __restrict__ pos) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    const int32_t t = __ldg(perm + r);
+    row_frame[r] = __ldg(frame_of + t / K);
+    row_tok[r] = __ldg(tokens + t);
+    pos[t] = (int32_t)r;
+  }
+}
+
 }  // namespace
 }  // namespace accel
 
@@ -1108,7 +1226,7 @@ using namespace accel;
 extern "C" int accel_fact_group_sum(const float* h2w, const float* epp, const int32_t* frame_of,
                                     const int32_t* tokens, const void* tsc, const int32_t* perm,
                                     const int64_t* seg_off, const int64_t* piece_off, int nkeys,
-                                    int K, int A, int piece_rows, int64_t n_pieces,
+                                    int key_mod, int K, int A, int piece_rows, int64_t n_pieces,
                                     float* piece_out, void* stream) {
   if (K < 1 || A < 4 || A % 4 || nkeys < 1 || piece_rows < 1 || piece_rows > kGsRows)
     return fail(kDimension, "fact_group_sum: bad sizes");
@@ -1120,8 +1238,41 @@ extern "C" int accel_fact_group_sum(const float* h2w, const float* epp, const in
   const size_t smem = (size_t)A * 4 + kGsThreads * sizeof(float4);
   fact_group_sum_kernel<<<(unsigned)n_pieces, kGsThreads, smem, as_stream(stream)>>>(
       h2w, epp, frame_of, tokens, static_cast<const float4*>(tsc), perm, seg_off, piece_off, nkeys,
-      K, A, piece_rows, piece_out);
+      key_mod, K, A, piece_rows, piece_out);
   return post_launch("fact_group_sum_kernel");
+}
+
+// Recompute over a frame-blocked grouping with sorted metadata (see the kernel).
+extern "C" int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* row_frame,
+                                     const int32_t* row_tok, const void* tsc_sorted,
+                                     const int64_t* seg_off, const int64_t* piece_off,
+                                     const int32_t* piece_key, int nkeys, int key_mod, int A,
+                                     int64_t n_pieces_max, float* piece_out, void* stream) {
+  if (A < 4 || A % 4 || nkeys < 1) return fail(kDimension, "fact_group_sum2: bad sizes");
+  if (n_pieces_max == 0) return kOk;
+  if (!h2w || !epp || !row_frame || !row_tok || !tsc_sorted || !seg_off || !piece_off ||
+      !piece_key || !piece_out)
+    return fail(kDimension, "fact_group_sum2: NULL buffer");
+  if (misaligned16(h2w) || misaligned16(epp) || misaligned16(tsc_sorted) || misaligned16(piece_out))
+    return fail(kDimension, "fact_group_sum2: buffers must be 16B aligned");
+  const size_t smem = (size_t)A * 4 + kGs2Threads * sizeof(float4);
+  fact_group_sum2_kernel<<<(unsigned)n_pieces_max, kGs2Threads, smem, as_stream(stream)>>>(
+      h2w, epp, row_frame, row_tok, static_cast<const float4*>(tsc_sorted), seg_off, piece_off,
+      piece_key, nkeys, key_mod, A, piece_out);
+  return post_launch("fact_group_sum2_kernel");
+}
+
+extern "C" int accel_sorted_rows(const int32_t* perm, const int32_t* frame_of,
+                                 const int32_t* tokens, int64_t R, int K, int32_t* row_frame,
+                                 int32_t* row_tok, int32_t* pos, void* stream) {
+  if (R < 0 || K < 1) return fail(kDimension, "sorted_rows: bad sizes");
+  if (R == 0) return kOk;
+  if (!perm || !frame_of || !tokens || !row_frame || !row_tok || !pos)
+    return fail(kDimension, "sorted_rows: NULL buffer");
+  const int grid = (int)std::min<int64_t>(ceil_div(R, 256), (int64_t)kNumSMs * 8);
+  sorted_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(perm, frame_of, tokens, R, K, row_frame,
+                                                          row_tok, pos);
+  return post_launch("sorted_rows_kernel");
 }
 
 extern "C" int accel_fact_grid(int64_t N) {
@@ -1144,6 +1295,18 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
                                      const double* fix_stats, float* dz, void* tsc,
                                      float* g_frame, float* lp_new, double* stat_part,
                                      double* max_part, void* stream) {
+  return accel_token_loss_fact2(h2w, epp, frame_of, tokens, lp_old, adv, N, K, A, algo, sigma,
+                                clip_eps, lambda_h, m_global, fix_stats, dz, tsc, nullptr, g_frame,
+                                lp_new, stat_part, max_part, stream);
+}
+
+extern "C" int accel_token_loss_fact2(const float* h2w, const float* epp, const int32_t* frame_of,
+                                      const int32_t* tokens, const float* lp_old, const float* adv,
+                                      int64_t N, int K, int A, int algo, double sigma,
+                                      double clip_eps, double lambda_h, double m_global,
+                                      const double* fix_stats, float* dz, void* tsc,
+                                      const int32_t* tsc_pos, float* g_frame, float* lp_new,
+                                      double* stat_part, double* max_part, void* stream) {
   if (algo != 0 && algo != 1) return fail(kDomain, "unknown algorithm %d", algo);
   if (!(sigma > 0)) return fail(kDomain, "sigma must be > 0, got %g", sigma);
   if (!(clip_eps > 0 && clip_eps < 1)) return fail(kDomain, "clip_eps must be in (0, 1)");
@@ -1225,13 +1388,24 @@ extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const i
     if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess)
       return fail(kCuda, "token_loss_fact2: counter reset");
     kernel<<<grid, nw * 32, smem, s>>>(h2w, epp, frame_of, tokens, lp_old, adv, N, K, prm,
-                                       fix_stats, dz, g_frame, lp_new, stat_part, max_part, ctr);
+                                       fix_stats, dz, g_frame, lp_new, stat_part, max_part, ctr,
+                                       static_cast<float4*>(tsc), tsc_pos);
     return post_launch("token_loss_fact2_kernel");
   };
-  if (!tsc && K == 7 && A == 256) return two_phase(token_loss_fact2_kernel<8, 8, 7>);
-  if (!tsc && K <= 8 && A == 256) return two_phase(token_loss_fact2_kernel<8, 8, 0>);
-  if (!tsc && K == 7 && A == 128) return two_phase(token_loss_fact2_kernel<4, 8, 7>);
-  if (!tsc && K <= 8 && A == 128) return two_phase(token_loss_fact2_kernel<4, 8, 0>);
+  if (K == 7 && A == 256)
+    return tsc ? two_phase(token_loss_fact2_kernel<8, 8, 7, true>)
+               : two_phase(token_loss_fact2_kernel<8, 8, 7, false>);
+  if (K <= 8 && A == 256)
+    return tsc ? two_phase(token_loss_fact2_kernel<8, 8, 0, true>)
+               : two_phase(token_loss_fact2_kernel<8, 8, 0, false>);
+  if (K == 7 && A == 128)
+    return tsc ? two_phase(token_loss_fact2_kernel<4, 8, 7, true>)
+               : two_phase(token_loss_fact2_kernel<4, 8, 7, false>);
+  if (K <= 8 && A == 128)
+    return tsc ? two_phase(token_loss_fact2_kernel<4, 8, 0, true>)
+               : two_phase(token_loss_fact2_kernel<4, 8, 0, false>);
+  if (tsc_pos != nullptr)
+    return fail(kDimension, "token_loss_fact: sorted scalar output needs K <= 8, A in {128, 256}");
   const bool full = A == 128 || A == 256 || A == 512 || A == 1024;
   // grouped kernel: 16 (32 at A = 1024) logits per lane, A / that lanes per transition
   if (A == 128 && K <= 8)

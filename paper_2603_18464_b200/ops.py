@@ -168,20 +168,44 @@ def tanh_grad_colsum(g, h, col_part, grid):
 
 
 class Grouping:
-    """A stable counting sort of R keys in [0, nkeys) (fixed per batch)."""
+    """A stable counting sort of R keys in [0, nkeys) (fixed per batch).
 
-    def __init__(self, keys, nkeys: int):
+    cpb > 0: frame-blocked order -- rows are cut into blocks of cpb 4096-row
+    chunks and sorted by (block, key), so a pass over the pieces in order
+    touches one block of rows at a time (accel_group_by_key_blocked); the key
+    sums then fold the blocks in order (accel_fold_blocked_pieces)."""
+
+    def __init__(self, keys, nkeys: int, cpb: int = 0):
         R = keys.numel()
         dev = keys.device
-        self.R, self.nkeys = R, int(nkeys)
+        lib = _lib.lib()
+        self.R, self.nkeys, self.cpb = R, int(nkeys), int(cpb)
+        self.nblocks = int(lib.accel_group_blocks(R, self.cpb)) if cpb > 0 else 1
+        nk = self.nkeys * self.nblocks
         self.perm = torch.empty(max(R, 1), dtype=I32, device=dev)
-        self.seg_off = torch.empty(nkeys + 1, dtype=I64, device=dev)
-        self.piece_off = torch.empty(nkeys + 1, dtype=I64, device=dev)
-        self.max_pieces = int(_lib.lib().accel_group_max_pieces(R, nkeys))
-        nbytes = _lib.lib().accel_group_workspace_size(R, nkeys)
+        self.seg_off = torch.empty(nk + 1, dtype=I64, device=dev)
+        self.piece_off = torch.empty(nk + 1, dtype=I64, device=dev)
+        self.max_pieces = int(lib.accel_group_max_pieces_blocked(R, nkeys, self.cpb))
+        self.piece_key = (torch.empty(max(self.max_pieces, 1), dtype=I32, device=dev)
+                          if cpb > 0 else None)
+        nbytes = lib.accel_group_workspace_size_blocked(R, nkeys, self.cpb)
         buf = workspace("group").get(nbytes)
-        _lib.call("accel_group_by_key", _p(keys), R, nkeys, _p(self.perm), _p(self.seg_off),
-                  _p(self.piece_off), _p(buf), buf.numel(), _stream())
+        _lib.call("accel_group_by_key_blocked", _p(keys), R, nkeys, self.cpb, _p(self.perm),
+                  _p(self.seg_off), _p(self.piece_off), _p(self.piece_key), _p(buf), buf.numel(),
+                  _stream())
+
+    def sort_rows(self, frame_of, tokens, K):
+        """Sorted per-row metadata of a (prev, k) grouping: row_frame, row_tok and
+        the inverse permutation pos (fixed per batch)."""
+        if getattr(self, "pos", None) is None:
+            dev = self.perm.device
+            R = self.R
+            self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
+            self.row_tok = torch.empty(max(R, 1), dtype=I32, device=dev)
+            self.pos = torch.empty(max(R, 1), dtype=I32, device=dev)
+            _lib.call("accel_sorted_rows", _p(self.perm), _p(frame_of), _p(tokens), R, int(K),
+                      _p(self.row_frame), _p(self.row_tok), _p(self.pos), _stream())
+        return self.pos
 
     def fact_rows_sum(self, h2w, epp, frame_of, tokens, tsc, K, out, piece_buf=None):
         """Grouped dz sums with dz recomputed from the loss pass's token scalars
@@ -189,22 +213,38 @@ class Grouping:
         A = h2w.shape[1]
         if piece_buf is None:
             piece_buf = workspace("group_pieces_f32").get(4 * max(self.max_pieces, 1) * A)
-        _lib.call("accel_fact_group_sum", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(tsc),
-                  _p(self.perm), _p(self.seg_off), _p(self.piece_off), self.nkeys, int(K), A, 256,
-                  self.max_pieces, _p(piece_buf), _stream())
-        _lib.call("accel_grouped_rows_sum", None, self.R, A, _p(self.perm), _p(self.seg_off),
-                  _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
-                  _stream())
+        nk = self.nkeys * self.nblocks
+        if self.cpb > 0:  # tsc holds the scalars at the sorted positions (sort_rows)
+            _lib.call("accel_fact_group_sum2", _p(h2w), _p(epp), _p(self.row_frame),
+                      _p(self.row_tok), _p(tsc), _p(self.seg_off), _p(self.piece_off),
+                      _p(self.piece_key), nk, self.nkeys, A, self.max_pieces, _p(piece_buf),
+                      _stream())
+        else:
+            _lib.call("accel_fact_group_sum", _p(h2w), _p(epp), _p(frame_of), _p(tokens),
+                      _p(tsc), _p(self.perm), _p(self.seg_off), _p(self.piece_off), nk, 0,
+                      int(K), A, 256, self.max_pieces, _p(piece_buf), _stream())
+        self._key_pass(piece_buf, A, out)
         return out
 
     def rows_sum(self, vals, out, piece_buf=None):
         D = vals.shape[1]
         if piece_buf is None:
             piece_buf = workspace("group_pieces_f32").get(4 * max(self.max_pieces, 1) * D)
+        if self.cpb > 0:
+            raise DimensionError("rows_sum needs a plain (unblocked) grouping")
         _lib.call("accel_grouped_rows_sum", _p(vals), self.R, D, _p(self.perm), _p(self.seg_off),
                   _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
                   _stream())
         return out
+
+    def _key_pass(self, piece_buf, D, out):
+        if self.cpb > 0:
+            _lib.call("accel_fold_blocked_pieces", _p(piece_buf), _p(self.piece_off), self.nkeys,
+                      self.nblocks, D, _p(out), _stream())
+        else:
+            _lib.call("accel_grouped_rows_sum", None, self.R, D, _p(self.perm), _p(self.seg_off),
+                      _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
+                      _stream())
 
 
 def prev_keys(tokens, N, K, A, with_pos=False, out=None):
@@ -225,14 +265,15 @@ def ep_plus(ep, pp, bias, K, out):
 
 def token_loss_fact(h2w, epp, frame_of, tokens, lp_old, adv, N, K, algo, sigma, clip_eps,
                     lambda_h, m_global, dz, g_frame, lp_new, stat_part, max_part,
-                    fix_stats=None, tsc=None):
-    """Factorized-head fused loss (see accel.h accel_token_loss_fact); dz=None
-    with tsc (f32[M, 4]) writes the per-token scalars instead of dz rows."""
+                    fix_stats=None, tsc=None, tsc_pos=None):
+    """Factorized-head fused loss (see accel.h accel_token_loss_fact2); dz=None
+    with tsc (f32[M, 4]) writes the per-token scalars instead of dz rows, at
+    tsc_pos[t] (a frame-blocked grouping's sorted positions) when given."""
     A = h2w.shape[1]
-    _lib.call("accel_token_loss_fact", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(lp_old),
+    _lib.call("accel_token_loss_fact2", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(lp_old),
               _p(adv), int(N), int(K), A, int(algo), float(sigma), float(clip_eps),
-              float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(tsc), _p(g_frame),
-              _p(lp_new), _p(stat_part), _p(max_part), _stream())
+              float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(tsc), _p(tsc_pos),
+              _p(g_frame), _p(lp_new), _p(stat_part), _p(max_part), _stream())
 
 
 def pk_marginals(dpk, K, A, dprev, dpos):

@@ -368,9 +368,21 @@ class Trainer:
         A, K = self.dims.n_actions, self.dims.chunk_len
         # factorized head (no [M, A] logits) wherever the kernel supports the shape
         self.factorized = A % 4 == 0 and 128 <= A <= 1024 and K <= 32
+        # recompute_dz: the loss kernel writes 16 B of token scalars instead of the
+        # 4A-byte dz row and the (prev, k) grouped sums recompute dz from the
+        # L2-resident H2W rows of one block of frames at a time (frame-blocked
+        # sort, group_block_chunks 4096-token chunks per block)
         self.recompute_dz = False
+        self.group_block_chunks = 64
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
+
+    def _pk_cpb(self) -> int:
+        # the frame-blocked recompute rides on the two-phase loss kernel's sorted
+        # scalar output (K <= 8, A in {128, 256})
+        A, K = self.dims.n_actions, self.dims.chunk_len
+        ok = self.recompute_dz and K <= 8 and A in (128, 256)
+        return self.group_block_chunks if ok else 0
 
     # -- bundle <-> device ---------------------------------------------------------
     @property
@@ -550,7 +562,7 @@ class Trainer:
             shard_sizes=_array_split_sizes(N, cfg.k_shards),
             behavior_lag_mean=float(np.mean(self.publish_version - np.asarray(behavior_version))))
         batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=self.factorized,
-                               frame_space=h_cache is not None)
+                               frame_space=h_cache is not None, pk_cpb=self._pk_cpb())
         batch.h_cache = h_cache
         # frame row of each trajectory's bootstrap observation (t = T)
         batch.boot_rows = b["traj_off"][1:] + torch.arange(n, dtype=torch.int64, device=dev)
@@ -658,7 +670,7 @@ class Trainer:
             vcache = hc[3:]        # (U, alpha, zm) over all frames
             batch.h_cache = None   # consumed: the value backward overwrites zm in place
         batch.ensure_groupings(d.n_steps, cnt[1:2], factorized=fact,
-                               frame_space=vcache is not None)
+                               frame_space=vcache is not None, pk_cpb=self._pk_cpb())
         if self.comm is None:
             N_glob, M_glob = N, M
         elif getattr(batch, "global_n", None) is not None:
@@ -698,8 +710,12 @@ class Trainer:
             max_part = S.get("st.max", (gf, 2), F64)
             loss_args = (h2w, epp, batch.frame_of, batch.tokens_dev, batch.lp_old, batch.adv, N,
                          K, algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dz, g_frame)
+            tsc_pos = None
+            if tsc is not None and batch.pk_group.cpb > 0:
+                tsc_pos = batch.pk_group.sort_rows(batch.frame_of, batch.tokens_dev, K)
             with self._timed("token_loss"):
-                ops.token_loss_fact(*loss_args, lp_new, stat_part, max_part, tsc=tsc)
+                ops.token_loss_fact(*loss_args, lp_new, stat_part, max_part, tsc=tsc,
+                                    tsc_pos=tsc_pos)
             gl = gf
         else:
             c = ops.build_c(h2, batch.frame_of, batch.tokens_dev, P["e_prev"], P["e_pos"], N, K,
@@ -721,7 +737,8 @@ class Trainer:
             self.comm.all_reduce_max(loss_max)
         # FIXUP: only does work when 0 < excluded < M_global (decided on the device)
         if fact:
-            ops.token_loss_fact(*loss_args, None, None, None, fix_stats=loss_sums, tsc=tsc)
+            ops.token_loss_fact(*loss_args, None, None, None, fix_stats=loss_sums, tsc=tsc,
+                                tsc_pos=tsc_pos)
         else:
             ops.token_loss(logits, P["b_head"], batch.tokens_dev, batch.lp_old, batch.adv, K,
                            algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None,

@@ -191,6 +191,27 @@ def test_loss_kernel_shapes_match_oracle(K, A):
     check_grads(dev_pol, dev_val, g_pol, g_val, (K, A))
 
 
+@pytest.mark.parametrize("algo", ["trust", "clip"])
+def test_frame_blocked_recompute_matches_oracle(algo):
+    """dz-free grouped sums over several frame blocks (one 4096-token chunk per
+    block): the loss kernel writes token scalars, the grouped pass recomputes dz
+    block by block and folds the blocks in order."""
+    tr, trajs, pol0, val0, cfg = _random_setup(seed=13, algo=algo, n_traj=40, max_len=90)
+    tr.recompute_dz = True
+    tr.group_block_chunks = 1
+    orc = _oracle_from(cfg, pol0, val0, 256, tr.dims.n_steps)
+    ob = orc.build_train_batch(trajs)
+    batch = tr.build_train_batch(trajs)
+    assert batch.n_tokens > 3 * 4096  # several blocks
+    rec = tr.train_step(batch)
+    assert batch.pk_group.nblocks > 2
+    orec, g_pol, g_val = orc.step_gradients(ob)
+    for k, v in orec.items():
+        assert abs(rec[k] - v) <= LOSS_TOL * max(1.0, abs(v)), (k, rec[k], v)
+    dev_pol, dev_val = tr.params.grads_to_host()
+    check_grads(dev_pol, dev_val, g_pol, g_val, ("blocked", algo))
+
+
 @pytest.mark.parametrize("factorized", [True, False, "recompute"])
 def test_partial_exclusion_runs_fixup_pass(factorized):
     """Some tokens with log-ratio < -745 are excluded: the surrogate mean is
