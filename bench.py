@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-traj", type=int, default=64, help="cpu_baseline sample size")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--dz", default="store", choices=["store", "recompute"],
+    ap.add_argument("--dz", default="recompute", choices=["store", "recompute"],
                     help="store: K4 writes dz rows; recompute: token scalars + frame-blocked "
                          "recomputing grouped sums")
     ap.add_argument("--block-chunks", type=int, default=64)
@@ -61,36 +61,50 @@ def dims():
     return dict(K=7, A=256, D=64, O=195, H=32)
 
 
-def trainer_roofline(N: int, n: int, peaks: dict) -> dict:
-    """T_roof = sum over the step's stages of max(bytes / BW, flops / F_peak)
-    (SURVEY 8(d)), with each stage's algorithmic bytes (fp32 activations, i32
-    indices) and, for the GEMMs, 3xTF32 tensor flops against half the measured
-    bf16 dense rate.  Passes a fused design avoids (the frame finiteness read,
-    the tanh derivatives) are not counted.  roofline time / achieved time is
-    the trainer's fraction of roofline."""
+def sfu_rate(peaks: dict) -> float:
+    """ex2 per second: 16 SFU ops per clock per SM (B200), 148 SMs, max SM clock."""
+    return 16 * 148 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+
+
+def trainer_roofline(N: int, n: int, peaks: dict, recompute: bool) -> dict:
+    """T_roof = sum over the step's stages of max(bytes / BW, flops / F_peak,
+    ex2 / SFU rate), with each stage's algorithmic bytes (fp32
+    activations, i32 indices), for the GEMMs 3xTF32 tensor flops against half
+    the measured bf16 dense rate, and for the softmax passes one ex2 per logit
+    and pass on the SFU.  Passes a fused design avoids (the frame finiteness
+    read, the tanh derivatives) are not counted.  recompute: the dz-free loss
+    path (token scalars + frame-blocked recomputing grouped sums).  roofline
+    time / achieved time is the trainer's fraction of roofline."""
     d = dims()
     K, A, D, O, H = d["K"], d["A"], d["D"], d["O"], d["H"]
     M, F = N * K, N + n
     bw = float(peaks["hbm_gbs"]) * 1e9
     tf32 = 0.5 * float(peaks.get("bf16_tflops_sustained", 1420.9)) * 1e12
+    sfu = sfu_rate(peaks)
     gemm = [  # (rows, K, N): backbone, values (revaluation), head, value head, backward
         (F, O, D), (F, D, D), (F, D, H), (F, D, A), (F, A, D), (F, D, D), (F, H, D),
         (F, A, D), (F, D, D), (F, O, D), (F, H, D)]
-    stages = {
-        "token_logp": (M * (4 * A + 8), 0.0),
-        "gae": (20 * N + 13 * n, 0.0),
-        "loss_fact": (M * (4 * A + 12) + N * (8 * A + 8), 0.0),
-        "grouped_sums": (M * (4 * A + 4), 0.0),
+    stages = {  # (bytes, tensor flops, SFU ex2)
+        "token_logp": (M * (4 * A + 8), 0.0, M * A),
+        "gae": (20 * N + 13 * n, 0.0, 0.0),
+        "loss_fact": (M * (16 + 12) + N * (8 * A + 8) if recompute
+                      else M * (4 * A + 12) + N * (8 * A + 8), 0.0, 2 * M * A),
+        "grouped_sums": (F * 4 * A + 24 * M, 0.0, M * A) if recompute
+        else (M * (4 * A + 4), 0.0, 0.0),
         "gemms": (sum(4 * r * (k + c) for r, k, c in gemm),
-                  sum(3 * 2 * r * k * c for r, k, c in gemm)),
+                  sum(3 * 2 * r * k * c for r, k, c in gemm), 0.0),
         "value_head": (4 * F * (2 * D + D) + 4 * 3 * F * H + 4 * F * (3 * D + 2) + 4 * F * (2 * D + 2),
-                       0.0),
+                       0.0, 0.0),
     }
-    t = sum(max(b / bw, f / tf32) for b, f in stages.values())
-    return {"t_roof_ms": t * 1e3, "bytes": sum(b for b, _ in stages.values()),
-            "tensor_flops": sum(f for _, f in stages.values()),
-            "stages_ms": {k: 1e3 * max(b / bw, f / tf32) for k, (b, f) in stages.items()},
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs; TF32 = bf16 dense sustained / 2"}
+    st = {k: max(b / bw, f / tf32, x / sfu) for k, (b, f, x) in stages.items()}
+    return {"t_roof_ms": sum(st.values()) * 1e3, "bytes": sum(v[0] for v in stages.values()),
+            "tensor_flops": sum(v[1] for v in stages.values()),
+            "sfu_ex2": sum(v[2] for v in stages.values()),
+            "stages_ms": {k: 1e3 * v for k, v in st.items()},
+            "loss_path": "dz-free (token scalars + frame-blocked recompute)" if recompute
+            else "dz stored and re-read by the grouped sums",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs; TF32 = bf16 dense sustained / 2; "
+                           "SFU = 16 ex2/clk/SM x 148 SMs x sm_max_mhz"}
 
 
 def make_bundle(seed: int, n_steps: int):
@@ -435,7 +449,7 @@ def main():
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
-    tr_roof = trainer_roofline(N, n, peaks)
+    tr_roof = trainer_roofline(N, n, peaks, tr.recompute_dz)
     peak = float(peaks["hbm_gbs"])
     A = d["A"]
     # factorized head (trainer default): per token dz write (4A) + token/lp_old/lp_new
@@ -452,7 +466,11 @@ def main():
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("token_loss_dram_bytes_per_launch")
+        tj = json.loads(tf.read_text())
+        traffic = tj.get("token_loss_sc_dram_bytes_per_launch" if tr.recompute_dz
+                         else "token_loss_dram_bytes_per_launch")
+    t_grp = float(np.mean(kern.get("group_sum", [float("nan")]))) / 1e3
+    ex2_loss = 2 * M * A  # one ex2 per logit in each of the loss kernel's two passes
     gae_bytes = 20 * N + 13 * n
     t_gae = float(np.mean(kern.get("gae", [float("nan")]))) / 1e3
     logp_bytes = M * (4 * A + 8)
@@ -478,7 +496,21 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_launch": loss_bytes, "ms_per_launch": t_loss * 1e3,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                     "sfu": {"ex2_per_launch": ex2_loss,
+                             "achieved_tops": ex2_loss / t_loss / 1e12,
+                             "peak_tops": sfu_rate(peaks) / 1e12,
+                             "frac": ex2_loss / t_loss / sfu_rate(peaks)},
+                     "note": ("dz-free loss path: the kernel writes 16 B of token scalars per "
+                              "token instead of the 1 KB dz row, so it is SFU/issue-bound, not "
+                              "HBM-bound (store mode: profiles/r1_bench_store_mode.json)")
+                     if tr.recompute_dz else "dz rows stored (HBM-bound)"},
+        "roofline_group_recompute": {
+            "kernel": "fact_group_sum2 (frame-blocked dz recompute + grouped sums)",
+            "ms_per_launch": t_grp * 1e3,
+            "bytes_per_launch": (N + n) * 4 * A + 24 * M,
+            "achieved": ((N + n) * 4 * A + 24 * M) / t_grp / 1e9, "unit": "GB/s",
+            "sfu_frac": M * A / t_grp / sfu_rate(peaks)} if tr.recompute_dz else None,
         "roofline_gae": {"bytes_per_launch": gae_bytes, "ms_per_launch": t_gae * 1e3,
                          "achieved": gae_bytes / t_gae / 1e9,
                          "frac": gae_bytes / t_gae / 1e9 / peak, "unit": "GB/s",

@@ -371,8 +371,9 @@ class Trainer:
         # recompute_dz: the loss kernel writes 16 B of token scalars instead of the
         # 4A-byte dz row and the (prev, k) grouped sums recompute dz from the
         # L2-resident H2W rows of one block of frames at a time (frame-blocked
-        # sort, group_block_chunks 4096-token chunks per block)
-        self.recompute_dz = False
+        # sort, group_block_chunks 4096-token chunks per block); on by default
+        # where the two-phase loss kernel serves the shape (K <= 8, A in {128, 256})
+        self.recompute_dz = self.factorized and K <= 8 and A in (128, 256)
         self.group_block_chunks = 64
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
