@@ -318,6 +318,28 @@ int accel_adam(const float* p_in, const float* g, const float* m_in, const float
                const double* group0, const double* group1, const int* skip,
                unsigned* bad, void* stream);
 
+/* ---- world-model training sub-steps (trainer.py:469-535), float64 ------- */
+
+/* Workspace bytes of accel_wm_mlp2_grad for n rows, hidden dh, output dout. */
+size_t accel_wm_workspace_size(int64_t n, int dh, int dout);
+/* One forward + backward of a 2-layer tanh MLP (numerics.py:174-220):
+ *   x f64[n, din], params f64 {w0 [dh, din], b0 [dh], w1 [dout, dh], b1 [dout]}
+ *   kind 0: target f64[n, dout], loss = mean((out - target)^2)
+ *           (train_obs_model_step, trainer.py:469-494)
+ *   kind 1: target = labels f64[n], dout = 1, loss = mean(softplus(z) - y z)
+ *           (train_reward_model_step, trainer.py:496-535)
+ * grads f64 (same layout as params), loss_out f64[1], nonfinite u32[1] =
+ * count of non-finite gradient entries (adam_step raises on them). */
+int accel_wm_mlp2_grad(const double* x, const double* target, int64_t n, int din, int dh,
+                       int dout, int kind, const double* params, double* grads,
+                       double* loss_out, unsigned* nonfinite, void* workspace,
+                       size_t workspace_bytes, void* stream);
+/* Adam step t (>= 1) over a flat float64 buffer (numerics.py:95-126);
+ * bad u32[1] = non-finite new parameters (ParamSet.check_finite). */
+int accel_wm_adam(double* params, const double* grads, double* m, double* v, int64_t n,
+                  double lr, double beta1, double beta2, double eps, int64_t t, unsigned* bad,
+                  void* stream);
+
 /* ---- tensor-core GEMM (tcgen05, 3xTF32: fp32-accurate) ----------------- */
 
 /* Streaming multiprocessors on the current device (persistent-grid size;

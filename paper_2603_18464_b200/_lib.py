@@ -59,6 +59,11 @@ _SIGNATURES = {
                                            P]),
     "accel_fact_group_sum2": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int64, P,
                                       P]),
+    "accel_wm_workspace_size": (c_size_t, [c_int64, c_int, c_int]),
+    "accel_wm_mlp2_grad": (c_int, [P, P, c_int64, c_int, c_int, c_int, c_int, P, P, P, P, P,
+                                   c_size_t, P]),
+    "accel_wm_adam": (c_int, [P, P, P, P, c_int64, c_double, c_double, c_double, c_double,
+                              c_int64, P, P]),
     "accel_sorted_rows": (c_int, [P, P, P, c_int64, c_int, P, P, P, P]),
     "accel_fold_blocked_pieces": (c_int, [P, P, c_int, c_int, c_int, P, P]),
     "accel_grouped_rows_sum": (c_int, [P, c_int64, c_int, P, P, P, c_int, c_int64, P, P, P]),

@@ -541,3 +541,23 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
               x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
     reduce_segments([(partial, out, kslices, n * k, n * k)])
     return out
+
+
+# ---------------------------------------------------------------------------
+# world-model training sub-steps (trainer.py:469-535), float64
+
+
+def wm_mlp2_grad(x, target, din, dh, dout, kind, params, grads, loss, nonfinite):
+    """Forward + backward of a 2-layer tanh MLP on the device (accel.h)."""
+    n = x.shape[0]
+    _check(x, "x", F64, (n, din))
+    _check(params, "params", F64)
+    nbytes = _lib.lib().accel_wm_workspace_size(n, dh, dout)
+    buf = workspace("wm").get(nbytes)
+    _lib.call("accel_wm_mlp2_grad", _p(x), _p(target), n, din, dh, dout, int(kind), _p(params),
+              _p(grads), _p(loss), _p(nonfinite), _p(buf), buf.numel(), _stream())
+
+
+def wm_adam(params, grads, m, v, lr, beta1, beta2, eps, t, bad):
+    _lib.call("accel_wm_adam", _p(params), _p(grads), _p(m), _p(v), params.numel(), float(lr),
+              float(beta1), float(beta2), float(eps), int(t), _p(bad), _stream())

@@ -29,7 +29,8 @@ from . import _lib, ops
 from .batch import DeviceTrainBatch
 from .errors import AccelError, DimensionError, DomainError, NonFiniteError
 from .params import AdamStateView, DeviceParams, Dims, FlatLayout, POLICY_NAMES, VALUE_NAMES
-from .publish import POLICY, VersionedWeights
+from .publish import OBS_MODEL, POLICY, REWARD_MODEL, VersionedWeights
+from .world_model import DeviceMlp2, obs_model_data, reward_model_data
 from .workload import PackedBatch, pack_trajectories
 
 F32, F64, I32 = torch.float32, torch.float64, torch.int32
@@ -335,10 +336,9 @@ class Trainer:
 
     def __init__(self, bundle, cfg: TrainerConfig, service: Any = None, metrics: Any = None,
                  seed: int = 0, comm: Any = None) -> None:
-        if cfg.world_model:
-            raise NotImplementedError(
-                "world-model training sub-steps (trainer.py:469-535) are outside this build's "
-                "hot path; run them with the reference trainer")
+        if cfg.world_model and (getattr(bundle, "obs_model", None) is None
+                                or getattr(bundle, "reward_model", None) is None):
+            raise DomainError("world_model=True needs a bundle with obs_model and reward_model")
         self.cfg = cfg
         self.service = service
         self.metrics = metrics
@@ -362,6 +362,9 @@ class Trainer:
         self.skipped = 0
         self.obs_updates = 0
         self.reward_updates = 0
+        # world-model sub-steps (trainer.py:469-535): float64 device MLPs, created
+        # on first use (the bundle's obs/reward models seed them)
+        self._wm = {}
         self.scratch = _Scratch(self.device)
         self._rec_host = torch.zeros(32, dtype=F64).pin_memory()
         self.profile_events = None  # list -> CUDA-event brackets of the hot kernels
@@ -388,6 +391,10 @@ class Trainer:
     # -- bundle <-> device ---------------------------------------------------------
     @property
     def bundle(self):
+        for kind, mlp in self._wm.items():  # world-model parameters updated on the device
+            model = getattr(self._bundle, kind)
+            if model.params is not mlp.params():
+                setattr(self._bundle, kind, model.with_params(mlp.params()))
         if self._host_stale:
             pol, val = self.params.to_host()
             b = self._bundle
@@ -418,12 +425,64 @@ class Trainer:
         self.service.update_weights(self.snapshot())
 
     def publish_world_model(self, kind: str) -> None:
+        """trainer.py:336-342: a snapshot of one world model at its own version."""
         if self.service is None or kind not in getattr(self.service, "configs", {}):
             return
-        raise NotImplementedError("world-model publication is outside this build's hot path")
+        model = getattr(self.bundle, kind)
+        snap = model.with_params(model.params.copy())
+        self.service.update_weights(VersionedWeights(kind, int(snap.params.version),
+                                                     **{kind: snap}))
 
     def publish_initial(self) -> None:
         self.publish_policy()
+        if self.cfg.world_model:
+            self.publish_world_model(OBS_MODEL)
+            self.publish_world_model(REWARD_MODEL)
+
+    # -- world-model sub-steps (trainer.py:469-535) ------------------------------------
+    def _wm_mlp(self, kind: str) -> DeviceMlp2:
+        if kind not in self._wm:
+            model = getattr(self._bundle, kind, None)
+            if model is None:
+                raise DomainError(f"the bundle has no {kind}")
+            cfg = self.cfg
+            self._wm[kind] = DeviceMlp2(model.params, cfg.lr, cfg.beta1, cfg.beta2, 1e-8,
+                                        self.device)
+        return self._wm[kind]
+
+    @property
+    def adam_obs(self):
+        return self._wm_mlp(OBS_MODEL).adam_state()
+
+    @property
+    def adam_reward(self):
+        return self._wm_mlp(REWARD_MODEL).adam_state()
+
+    def train_obs_model_step(self, trajs) -> float:
+        """MSE regression on (o_t, a_t) -> o_{t+1} transitions (trainer.py:469-494)."""
+        mlp = self._wm_mlp(OBS_MODEL)
+        x, y = obs_model_data(self._bundle.obs_model, trajs, self.cfg.wm_max_transitions,
+                              self.rng)
+        loss = mlp.update(x, y, 0)
+        self.obs_updates += 1
+        self.publish_world_model(OBS_MODEL)
+        if self.metrics is not None:
+            self.metrics.emit("obs_model_step", loss=loss, updates=self.obs_updates)
+        return loss
+
+    def train_reward_model_step(self, trajs) -> float:
+        """Binary cross-entropy on frames; positives are terminal frames of
+        successful episodes, negatives subsampled (trainer.py:496-535)."""
+        mlp = self._wm_mlp(REWARD_MODEL)
+        x, labels, single_class = reward_model_data(trajs, self.cfg.reward_neg_ratio,
+                                                    self.cfg.wm_max_transitions, self.rng)
+        loss = mlp.update(x, labels, 1)
+        self.reward_updates += 1
+        self.publish_world_model(REWARD_MODEL)
+        if self.metrics is not None:
+            self.metrics.emit("reward_model_step", loss=loss, updates=self.reward_updates,
+                              single_class=single_class)
+        return loss
 
     # -- shared forward pieces -------------------------------------------------------
     def _backbone(self, frames, tag: str | None, nonfinite=None):
@@ -950,7 +1009,17 @@ class Trainer:
                 continue
             if cfg.train_service_time > 0:
                 yield rt.Sleep(cfg.train_service_time)
-            self.train_step(item)
+            record = self.train_step(item)
+            # world-model updates every t_obs / t_reward optimizer cycles (trainer.py:552-560)
+            if record is not None and cfg.world_model and wm_buffer is not None:
+                if self.cycles % cfg.t_obs == 0:
+                    trajs = wm_buffer.sample(cfg.wm_batch_episodes, self.rng)
+                    if trajs:
+                        self.train_obs_model_step(trajs)
+                if self.cycles % cfg.t_reward == 0:
+                    trajs = wm_buffer.sample(cfg.wm_batch_episodes, self.rng)
+                    if trajs:
+                        self.train_reward_model_step(trajs)
 
 
 __all__ = [
