@@ -318,6 +318,17 @@ int accel_adam(const float* p_in, const float* g, const float* m_in, const float
                const double* group0, const double* group1, const int* skip,
                unsigned* bad, void* stream);
 
+/* Batched inference-service evaluation (inference.py:129-160, run_batch): one
+ * warp per request, all of one kind; weights / dims as accel_imagine (unused
+ * pointers of the other kinds may be dummies).  kind 0 policy: obs f64[n, O],
+ * steps i32[n], uniforms f64[n, K] (the request's ticket substream) ->
+ * tokens i32[n, K], logits f64[n, K, A], values f64[n]; kind 1 obs model:
+ * chunks i32[n, K] -> next_obs f64[n, O]; kind 2 reward model -> probs f64[n]. */
+int accel_serve(const void* const* weights, const int* dims, int kind, const double* obs,
+                const int32_t* steps, const int32_t* chunks, const double* uniforms, int64_t n,
+                int32_t* tokens_out, double* logits_out, double* values_out,
+                double* next_obs_out, double* probs_out, void* stream);
+
 /* ---- world-model training sub-steps (trainer.py:469-535), float64 ------- */
 
 /* Workspace bytes of accel_wm_mlp2_grad for n rows, hidden dh, output dout. */

@@ -109,6 +109,67 @@ __device__ double reward_prob(const ImagineWeights& w, const ImagineDims& d, con
   return 1.0 / (1.0 + exp(-z));
 }
 
+// K autoregressive tokens from h2 (models.py:135-150): logits of token k from
+// c = h2 + e_prev[prev] + e_pos[k], softmax, sequential cumsum, searchsorted
+// against the k-th uniform (u_k injected, else Philox), clamped to A - 1.
+// Writes toks[K] and the K x A logits (logits_out).
+__device__ void policy_chunk(const ImagineWeights& w, const ImagineDims& d, const double* h2,
+                             double* cvec, double* lg, const double* __restrict__ u_k,
+                             curandStatePhilox4_32_10_t* rng, int* toks,
+                             double* __restrict__ logits_out, int lane) {
+  const int K = d.K, A = d.A;
+  int prev = A;
+  for (int k = 0; k < K; ++k) {
+    for (int i = lane; i < d.D; i += 32)
+      cvec[i] = h2[i] + __ldg(w.e_prev + (int64_t)prev * d.D + i) +
+                __ldg(w.e_pos + (int64_t)k * d.D + i);
+    __syncwarp();
+    warp_matvec(w.w_headt, cvec, d.D, A, w.b_head, lg, false, lane);
+    double mx = -CUDART_INF;
+    for (int a = lane; a < A; a += 32) mx = fmax(mx, lg[a]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double u = u_k ? u_k[k] : (lane == 0 ? curand_uniform_double(rng) : 0.0);
+    int tok = 0;
+    if (lane == 0) {  // softmax + sequential cumsum + searchsorted (models.py:145-147)
+      double s = 0.0;
+      for (int a = 0; a < A; ++a) s += exp(lg[a] - mx);
+      double cum = 0.0;
+      tok = A;
+      for (int a = 0; a < A; ++a) {
+        cum += exp(lg[a] - mx) / s;
+        if (u <= cum) { tok = a; break; }
+      }
+      tok = min(tok, A - 1);
+    }
+    tok = __shfl_sync(0xffffffffu, tok, 0);
+    toks[k] = tok;
+    double* lo = logits_out + (int64_t)k * A;
+    for (int a = lane; a < A; a += 32) lo[a] = lg[a];
+    prev = tok;
+    __syncwarp();
+  }
+}
+
+// next observation of the obs model for (x, chunk tokens) (models.py:349-355),
+// the one-hot part of the input read as K weight rows
+__device__ void obs_predict(const ImagineWeights& w, const ImagineDims& d, const double* x,
+                            const int* toks, double* ho, double* nx, int lane) {
+  const int O = d.O;
+  for (int j0 = 0; j0 < d.HO; j0 += 32) {
+    const int j = j0 + lane;
+    if (j < d.HO) {
+      double acc = 0.0;
+      for (int i = 0; i < O; ++i) acc = fma(__ldg(w.ow0t + (int64_t)i * d.HO + j), x[i], acc);
+      for (int k = 0; k < d.K; ++k)
+        acc += __ldg(w.ow0t + (int64_t)(O + k * d.A + toks[k]) * d.HO + j);
+      ho[j] = tanh(acc + __ldg(w.ob0 + j));
+    }
+  }
+  __syncwarp();
+  warp_matvec(w.ow1t, ho, d.HO, O, w.ob1, nx, false, lane);
+}
+
 __global__ void __launch_bounds__(128)
 imagine_kernel(ImagineWeights w, ImagineDims d, const double* __restrict__ start_obs,
                const int32_t* __restrict__ start_step, const double* __restrict__ uniforms,
@@ -148,54 +209,13 @@ imagine_kernel(ImagineWeights w, ImagineDims d, const double* __restrict__ start
     // ---- policy request: backbone, AR token sampling, value ----------------------
     warp_matvec(w.w0t, x, O, d.D, w.b0, h1, true, lane);
     warp_matvec(w.w1t, h1, d.D, d.D, w.b1, h2, true, lane);
-    int prev = A;
     int toks[32];
-    for (int k = 0; k < K; ++k) {
-      for (int i = lane; i < d.D; i += 32)
-        cvec[i] = h2[i] + __ldg(w.e_prev + (int64_t)prev * d.D + i) +
-                  __ldg(w.e_pos + (int64_t)k * d.D + i);
-      __syncwarp();
-      warp_matvec(w.w_headt, cvec, d.D, A, w.b_head, lg, false, lane);
-      double mx = -CUDART_INF;
-      for (int a = lane; a < A; a += 32) mx = fmax(mx, lg[a]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const double u = uniforms ? uniforms[(t * (d.H + 1) + req) * K + k]
-                                : (lane == 0 ? curand_uniform_double(&rng) : 0.0);
-      int tok = 0;
-      if (lane == 0) {  // softmax + sequential cumsum + searchsorted (models.py:145-147)
-        double s = 0.0;
-        for (int a = 0; a < A; ++a) s += exp(lg[a] - mx);
-        double cum = 0.0;
-        tok = A;
-        for (int a = 0; a < A; ++a) {
-          cum += exp(lg[a] - mx) / s;
-          if (u <= cum) { tok = a; break; }
-        }
-        tok = min(tok, A - 1);
-      }
-      tok = __shfl_sync(0xffffffffu, tok, 0);
-      toks[k] = tok;
-      double* lo = logits_out + ((t * d.H + h) * K + k) * (int64_t)A;
-      for (int a = lane; a < A; a += 32) lo[a] = lg[a];
-      prev = tok;
-      __syncwarp();
-    }
+    policy_chunk(w, d, h2, cvec, lg, uniforms ? uniforms + (t * (d.H + 1) + req) * K : nullptr,
+                 &rng, toks, logits_out + (t * d.H + h) * K * (int64_t)A, lane);
     const double val = state_value(w, d, h1, h2, step, uv, mv, lane);
     ++req;
     // ---- obs request: [o, onehot(chunk)] -> HO -> O ------------------------------------
-    for (int j0 = 0; j0 < d.HO; j0 += 32) {
-      const int j = j0 + lane;
-      if (j < d.HO) {
-        double acc = 0.0;
-        for (int i = 0; i < O; ++i) acc = fma(__ldg(w.ow0t + (int64_t)i * d.HO + j), x[i], acc);
-        for (int k = 0; k < K; ++k)
-          acc += __ldg(w.ow0t + (int64_t)(O + k * A + toks[k]) * d.HO + j);
-        ho[j] = tanh(acc + __ldg(w.ob0 + j));
-      }
-    }
-    __syncwarp();
-    warp_matvec(w.ow1t, ho, d.HO, O, w.ob1, nx, false, lane);
+    obs_predict(w, d, x, toks, ho, nx, lane);
     bool finite = true;
     for (int i = lane; i < O; i += 32) finite &= isfinite(nx[i]);
     if (!__all_sync(0xffffffffu, finite)) { status = 1; break; }
@@ -247,6 +267,56 @@ imagine_kernel(ImagineWeights w, ImagineDims d, const double* __restrict__ start
     len_out[t] = len;
     done_out[t] = done ? 1 : 0;
     status_out[t] = status;
+  }
+}
+
+// Batched inference service evaluation (inference.py:129-160, run_batch): one
+// warp per request, all of one kind.  kind 0 policy: sample_chunk + state_value
+// (uniforms u[n, K] drawn by the host from the request's ticket substream, so
+// tokens equal the reference's whatever the batch composition); kind 1 obs
+// model: predict(o, chunk); kind 2 reward model: sigmoid probability.
+__global__ void __launch_bounds__(128)
+serve_kernel(ImagineWeights w, ImagineDims d, int kind, const double* __restrict__ obs,
+             const int32_t* __restrict__ steps, const int32_t* __restrict__ chunks,
+             const double* __restrict__ uniforms, int64_t n, int32_t* __restrict__ tokens_out,
+             double* __restrict__ logits_out, double* __restrict__ values_out,
+             double* __restrict__ next_obs_out, double* __restrict__ probs_out) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per_warp = 2 * d.O + 3 * d.D + d.HO + d.HR + d.HV + d.A + d.D;
+  double* x = sm + (size_t)warp * per_warp;
+  double* nx = x + d.O;
+  double* h1 = nx + d.O;
+  double* h2 = h1 + d.D;
+  double* cvec = h2 + d.D;
+  double* ho = cvec + d.D;
+  double* hr = ho + d.HO;
+  double* mv = hr + d.HR;
+  double* lg = mv + d.HV;
+  double* uv = lg + d.A;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
+  if (r >= n) return;
+  for (int i = lane; i < d.O; i += 32) x[i] = obs[r * d.O + i];
+  __syncwarp();
+  if (kind == 0) {
+    warp_matvec(w.w0t, x, d.O, d.D, w.b0, h1, true, lane);
+    warp_matvec(w.w1t, h1, d.D, d.D, w.b1, h2, true, lane);
+    int toks[32];
+    policy_chunk(w, d, h2, cvec, lg, uniforms + r * d.K, nullptr, toks,
+                 logits_out + r * d.K * (int64_t)d.A, lane);
+    const double val = state_value(w, d, h1, h2, steps[r], uv, mv, lane);
+    if (lane == 0) {
+      for (int k = 0; k < d.K; ++k) tokens_out[r * d.K + k] = toks[k];
+      values_out[r] = val;
+    }
+  } else if (kind == 1) {
+    int toks[32];
+    for (int k = 0; k < d.K; ++k) toks[k] = min(max(chunks[r * d.K + k], 0), d.A - 1);
+    obs_predict(w, d, x, toks, ho, nx, lane);
+    for (int i = lane; i < d.O; i += 32) next_obs_out[r * d.O + i] = nx[i];
+  } else {
+    const double pr = reward_prob(w, d, x, hr, lane);
+    if (lane == 0) probs_out[r] = pr;
   }
 }
 
@@ -305,4 +375,36 @@ extern "C" int accel_imagine(const void* const* weights, const int* dims, int H,
       w, d, start_obs, start_step, uniforms, n, obs_out, steps_out, tokens_out, logits_out,
       values_out, rewards_out, boot_out, len_out, done_out, status_out);
   return post_launch("imagine_kernel");
+}
+
+extern "C" int accel_serve(const void* const* weights, const int* dims, int kind, const double* obs,
+                           const int32_t* steps, const int32_t* chunks, const double* uniforms,
+                           int64_t n, int32_t* tokens_out, double* logits_out, double* values_out,
+                           double* next_obs_out, double* probs_out, void* stream) {
+  if (n < 0 || kind < 0 || kind > 2) return fail(kDimension, "serve: bad kind / size");
+  if (n == 0) return kOk;
+  if (!weights || !dims || !obs) return fail(kDimension, "serve: NULL buffer");
+  ImagineDims d{};
+  d.O = dims[0]; d.D = dims[1]; d.K = dims[2]; d.A = dims[3]; d.S = dims[4]; d.HV = dims[5];
+  d.HO = dims[6]; d.HR = dims[7];
+  if (d.O < 1 || d.D < 1 || d.K < 1 || d.K > 32 || d.A < 1 || d.S < 1)
+    return fail(kDimension, "serve: bad dims");
+  if (kind == 0 && (!steps || !uniforms || !tokens_out || !logits_out || !values_out))
+    return fail(kDimension, "serve: policy batch needs steps, uniforms and outputs");
+  if (kind == 1 && (!chunks || !next_obs_out)) return fail(kDimension, "serve: obs batch buffers");
+  if (kind == 2 && !probs_out) return fail(kDimension, "serve: reward batch buffers");
+  const double* const* p = reinterpret_cast<const double* const*>(weights);
+  ImagineWeights w{p[0],  p[1],  p[2],  p[3],  p[4],  p[5],  p[6],  p[7],
+                   p[8],  p[9],  p[10], p[11], p[12], p[13], p[14],
+                   p[15], p[16], p[17], p[18], p[19], p[20], p[21], p[22]};
+  const size_t smem = accel_imagine_smem_bytes(d.O, d.D, d.A, d.HV, d.HO, d.HR);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(serve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return fail(kCuda, "serve smem: %s", cudaGetErrorString(e));
+  }
+  serve_kernel<<<(unsigned)ceil_div(n, 4), 128, smem, as_stream(stream)>>>(
+      w, d, kind, obs, steps, chunks, uniforms, n, tokens_out, logits_out, values_out,
+      next_obs_out, probs_out);
+  return post_launch("serve_kernel");
 }

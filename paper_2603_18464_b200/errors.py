@@ -19,6 +19,10 @@ class NonFiniteError(ValueError):
     """NaN or infinity where a finite value is required (numerics.py:28-29)."""
 
 
+class PayloadError(ValueError):
+    """Malformed inference batch: empty or mixed kinds (inference.py:38-39)."""
+
+
 class AccelError(RuntimeError):
     """CUDA-side failure (status 4) or a missing native library."""
 

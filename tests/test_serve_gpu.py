@@ -1,0 +1,81 @@
+"""GPU batched serving (inference.run_batch, inference.py:129-160) against the
+reference's own responses (tests/golden/make_golden_serve.py): tokens
+bit-exact, logits / values / next observations / probabilities to 1e-12
+(float64 on the device); batched == solo (reference test_inference.py:148-159);
+empty / mixed batches and out-of-range steps raise like the reference."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from serve_fixture import ServeGolden
+
+pytestmark = pytest.mark.gpu
+
+
+def weights(g: ServeGolden, kind: str):
+    from paper_2603_18464_b200.publish import VersionedWeights
+    from paper_2603_18464_b200.types import (ObsModel, ObsModelConfig, ParamSet, PolicyConfig,
+                                             PolicyModel, RewardModel, ValueConfig, ValueHead)
+    m = g.meta
+    pc = PolicyConfig(obs_dim=m["O"], hidden_dim=m["D"], chunk_len=m["K"], n_actions=m["A"],
+                      vocab_size=m["vocab"], action_start=m["action_start"])
+    pol = PolicyModel(pc, ParamSet(g.params("pol_")))
+    val = ValueHead(ValueConfig(m["D"], m["n_steps"], m["mlp_hidden"]), ParamSet(g.params("val_")))
+    obs = ObsModel(ObsModelConfig(obs_dim=m["O"], chunk_len=m["K"], n_actions=m["A"],
+                                  hidden_dim=m["obs_hidden"]), ParamSet(g.params("obs_")))
+    rew = RewardModel(m["O"], ParamSet(g.params("rew_")), hidden_dim=m["reward_hidden"])
+    return VersionedWeights(kind, m["version"], policy=pol, value=val, obs_model=obs,
+                            reward_model=rew)
+
+
+def test_serve_matches_reference_run_batch():
+    from paper_2603_18464_b200.publish import OBS_MODEL, POLICY, REWARD_MODEL
+    from paper_2603_18464_b200.serve import DeviceServer
+    g = ServeGolden()
+    z, seed = g.z, g.meta["base_seed"]
+    srv = DeviceServer()
+    res = srv.run_batch(weights(g, POLICY), g.requests(POLICY), seed)
+    np.testing.assert_array_equal(np.stack([r.tokens for r in res]), z["tokens"])
+    np.testing.assert_allclose(np.stack([r.logits for r in res]), z["logits"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose([r.value for r in res], z["values"], rtol=0, atol=1e-12)
+    assert all(r.version == g.meta["version"] for r in res)
+    res = srv.run_batch(weights(g, OBS_MODEL), g.requests(OBS_MODEL), seed)
+    np.testing.assert_allclose(np.stack([r.next_obs for r in res]), z["next_obs"], rtol=0,
+                               atol=1e-12)
+    res = srv.run_batch(weights(g, REWARD_MODEL), g.requests(REWARD_MODEL), seed)
+    np.testing.assert_allclose([r.probability for r in res], z["probs"], rtol=0, atol=1e-12)
+
+
+def test_batched_equals_solo():
+    from paper_2603_18464_b200.publish import POLICY
+    from paper_2603_18464_b200.serve import DeviceServer
+    g = ServeGolden()
+    srv = DeviceServer()
+    w = weights(g, POLICY)
+    reqs = g.requests(POLICY)[:8]
+    together = srv.run_batch(w, reqs, 0)
+    for req, batched in zip(reqs, together):
+        solo = srv.run_batch(w, [req], 0)[0]
+        np.testing.assert_array_equal(batched.tokens, solo.tokens)
+        np.testing.assert_array_equal(batched.logits, solo.logits)
+        assert batched.value == solo.value
+
+
+def test_serve_errors():
+    from paper_2603_18464_b200.errors import DimensionError, PayloadError
+    from paper_2603_18464_b200.publish import POLICY, REWARD_MODEL
+    from paper_2603_18464_b200.serve import DeviceServer
+    g = ServeGolden()
+    srv = DeviceServer()
+    w = weights(g, POLICY)
+    with pytest.raises(PayloadError):
+        srv.run_batch(w, [], 0)
+    mixed = g.requests(POLICY)[:1] + g.requests(REWARD_MODEL)[:1]
+    with pytest.raises(PayloadError):
+        srv.run_batch(w, mixed, 0)
+    bad = g.requests(POLICY)[:2]
+    bad[1].obs.step = g.meta["n_steps"]
+    with pytest.raises(DimensionError, match="step index"):
+        srv.run_batch(w, bad, 0)
