@@ -81,6 +81,16 @@ class FlatLayout:
     def n_params(self, names) -> int:
         return int(sum(np.prod(self.shapes[k]) for k in names))
 
+    def split(self, flat: np.ndarray) -> tuple:
+        """Host flat buffer -> ({policy tensors}, {value tensors}) in float64."""
+        out = ({}, {})
+        for i, names in enumerate((POLICY_NAMES, VALUE_NAMES)):
+            for k in names:
+                off = self.offsets[k]
+                n = int(np.prod(self.shapes[k]))
+                out[i][k] = flat[off:off + n].astype(np.float64).reshape(self.shapes[k])
+        return out
+
 
 class DeviceParams:
     """Ping-pong parameter / moment buffers plus one gradient buffer."""
@@ -117,13 +127,7 @@ class DeviceParams:
         self.p[self.cur].copy_(torch.from_numpy(host))
 
     def _split(self, flat: np.ndarray) -> tuple:
-        out = ({}, {})
-        for i, names in enumerate((POLICY_NAMES, VALUE_NAMES)):
-            for k in names:
-                off = self.layout.offsets[k]
-                n = int(np.prod(self.layout.shapes[k]))
-                out[i][k] = flat[off:off + n].astype(np.float64).reshape(self.layout.shapes[k])
-        return out
+        return self.layout.split(flat)
 
     def to_host(self) -> tuple:
         return self._split(self.p[self.cur].cpu().numpy())

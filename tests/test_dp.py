@@ -147,3 +147,47 @@ def test_dp_gpu_two_ranks():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert "DP PARITY OK" in res.stdout
+
+
+def _bcast_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_18464_b200.params import Dims, FlatLayout
+        from paper_2603_18464_b200.publish import POLICY, VersionedWeights, broadcast_policy
+        from paper_2603_18464_b200.types import (ModelBundle, PolicyConfig, PolicyModel,
+                                                 ValueConfig, ValueHead)
+        rng = np.random.default_rng(0)  # same template on every rank
+        pc = PolicyConfig(obs_dim=9, hidden_dim=8, chunk_len=3, n_actions=5, vocab_size=5,
+                          action_start=0)
+        tpl = ModelBundle(PolicyModel.init(rng, pc), ValueHead.init(rng, ValueConfig(8, 12, 4)))
+        layout = FlatLayout(Dims.from_models(tpl.policy, tpl.value), pad_to=4)
+        snap = None
+        if rank == 0:
+            flat = torch.from_numpy(np.random.default_rng(1).normal(size=layout.total)
+                                    .astype(np.float32))
+            snap = VersionedWeights(POLICY, 17, flat=flat, split=layout.split, template=tpl)
+        got = broadcast_policy(snap, tpl, src=0)
+        q.put((rank, got.version, {k: v.copy() for k, v in got.policy.params.tensors.items()},
+               {k: v.copy() for k, v in got.value.params.tensors.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_policy_snapshot_broadcast_gloo():
+    """a versioned snapshot reaches every rank intact."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (v, pol, val)) for r, v, pol, val in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == res[1][0] == 17
+    for k in res[0][1]:
+        np.testing.assert_array_equal(res[0][1][k], res[1][1][k])
+    for k in res[0][2]:
+        np.testing.assert_array_equal(res[0][2][k], res[1][2][k])
