@@ -49,6 +49,37 @@ def torch_adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, g0, g1, skip, bad):
         v_out[lo:hi] = v.float()
 
 
+def _run_gloo(target, world: int, attempts: int = 3) -> dict:
+    """Spawn `world` gloo ranks running target(rank, world, port, queue) and
+    collect one (rank, ...) tuple per rank.  A rendezvous port picked by
+    _free_port can be taken by another process before the ranks bind it, so a
+    failed launch is retried on a fresh port."""
+    import queue as _queue
+    ctx = mp.get_context("spawn")
+    last = None
+    for _ in range(attempts):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res = {}
+        try:
+            for _ in range(world):
+                item = q.get(timeout=120)
+                res[item[0]] = item[1:]
+        except _queue.Empty as e:
+            last = e
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+        if len(res) == world and all(p.exitcode == 0 for p in procs):
+            return res
+        last = last or RuntimeError(f"exit codes {[p.exitcode for p in procs]}")
+    raise AssertionError(f"gloo ranks failed after {attempts} attempts: {last}")
+
+
 class _Params:
     def __init__(self, total, seed):
         gen = torch.Generator().manual_seed(seed)
@@ -90,19 +121,7 @@ def _worker(rank, world, port, out_q):
 
 def test_zero2_adam_and_collectives_gloo():
     world = 2
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = {}
-    for _ in range(world):
-        rank, p_new, sums, mx, bounds, counts = q.get(timeout=120)
-        res[rank] = (p_new, sums, mx, bounds, counts)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = _run_gloo(_worker, world)
     # single-process reference: full Adam on the summed gradients
     total, n_policy = 40, 22
     ref = _Params(total, seed=5)
@@ -176,16 +195,7 @@ def _bcast_worker(rank, world, port, q):
 
 def test_policy_snapshot_broadcast_gloo():
     """a versioned snapshot reaches every rank intact."""
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = dict((r, (v, pol, val)) for r, v, pol, val in (q.get(timeout=120) for _ in procs))
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = _run_gloo(_bcast_worker, 2)
     assert res[0][0] == res[1][0] == 17
     for k in res[0][1]:
         np.testing.assert_array_equal(res[0][1][k], res[1][1][k])
