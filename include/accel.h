@@ -226,8 +226,11 @@ int64_t accel_group_max_pieces_blocked(int64_t R, int nkeys, int64_t cpb);
 int64_t accel_group_blocks(int64_t R, int64_t cpb);
 int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nkeys, int64_t cpb,
                                int32_t* perm, int64_t* seg_off, int64_t* piece_off,
-                               int32_t* piece_key, void* workspace, size_t workspace_bytes,
-                               void* stream);
+                               int32_t* piece_key, const int32_t* frame_of, const int32_t* tokens,
+                               int K, int32_t* row_frame, int32_t* row_tok, int32_t* pos,
+                               void* workspace, size_t workspace_bytes, void* stream);
+/* pos != NULL: the scatter also writes the sorted per-row metadata of a
+ * (prev, k) grouping (as accel_sorted_rows): row_frame, row_tok, pos. */
 /* piece_key (nullable) i32[accel_group_max_pieces_blocked]: owning composite key
  * of each piece. */
 /* Sorted per-row metadata of a grouping (fixed per batch): row_frame[r] =
@@ -246,8 +249,9 @@ int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* row
                           void* stream);
 /* out[nkeys, D] = sum over blocks (in order) of the pieces (in order) of the
  * composite keys b * nkeys + key: the key pass of a blocked grouping. */
+size_t accel_fold_workspace_size(int nkeys, int D);
 int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off, int nkeys,
-                              int nblocks, int D, float* out, void* stream);
+                              int nblocks, int D, float* out, void* workspace, void* stream);
 int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
                            const int64_t* seg_off, const int64_t* piece_off, int nkeys,
                            int64_t n_pieces, float* piece_buf, float* out, void* stream);

@@ -55,8 +55,9 @@ _SIGNATURES = {
     "accel_group_workspace_size_blocked": (c_size_t, [c_int64, c_int, c_int64]),
     "accel_group_max_pieces_blocked": (c_int64, [c_int64, c_int, c_int64]),
     "accel_group_blocks": (c_int64, [c_int64, c_int64]),
-    "accel_group_by_key_blocked": (c_int, [P, c_int64, c_int, c_int64, P, P, P, P, P, c_size_t,
-                                           P]),
+    "accel_group_by_key_blocked": (c_int, [P, c_int64, c_int, c_int64, P, P, P, P, P, P, c_int,
+                                           P, P, P, P, c_size_t, P]),
+    "accel_fold_workspace_size": (c_size_t, [c_int, c_int]),
     "accel_fact_group_sum2": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int64, P,
                                       P]),
     "accel_wm_workspace_size": (c_size_t, [c_int64, c_int, c_int]),
@@ -66,7 +67,7 @@ _SIGNATURES = {
                               c_int64, P, P]),
     "accel_serve": (c_int, [P, P, c_int, P, P, P, P, c_int64, P, P, P, P, P, P]),
     "accel_sorted_rows": (c_int, [P, P, P, c_int64, c_int, P, P, P, P]),
-    "accel_fold_blocked_pieces": (c_int, [P, P, c_int, c_int, c_int, P, P]),
+    "accel_fold_blocked_pieces": (c_int, [P, P, c_int, c_int, c_int, P, P, P]),
     "accel_grouped_rows_sum": (c_int, [P, c_int64, c_int, P, P, P, c_int, c_int64, P, P, P]),
     "accel_warp_grid": (c_int, [c_int64]),
     "accel_value_pool": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P, P, c_int,

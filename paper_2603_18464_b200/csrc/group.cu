@@ -54,6 +54,16 @@ __global__ void step_keys_kernel(const int32_t* __restrict__ steps,
 // counts[((chunk / cpb) * nkeys + key) * cpb + chunk % cpb]: the row range is cut
 // into blocks of cpb chunks and the scan order is block-major, key-minor, chunk
 // last (cpb = n_chunks: plain key-major order).  Composite key = block * nkeys + key.
+// optional sorted per-row metadata written by the scatter (pos == nullptr: off)
+struct SortedRows {
+  const int32_t* frame_of;
+  const int32_t* tokens;
+  int K;
+  int32_t* row_frame;
+  int32_t* row_tok;
+  int32_t* pos;
+};
+
 __device__ __forceinline__ int64_t count_idx(int64_t chunk, int key, int nkeys, int64_t cpb) {
   return ((chunk / cpb) * nkeys + key) * cpb + chunk % cpb;
 }
@@ -117,7 +127,8 @@ segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks
 
 __global__ void __launch_bounds__(kThreads)
 stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
-                      int64_t cpb, const int* __restrict__ base, int32_t* __restrict__ perm) {
+                      int64_t cpb, const int* __restrict__ base, int32_t* __restrict__ perm,
+                      SortedRows sr) {
   extern __shared__ int s_ctr[];  // [kWarps][nkeys]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
@@ -134,7 +145,13 @@ stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, in
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     if (live) {
       const int rank = __popc(peers & lt);
-      perm[ctr[key] + rank] = (int32_t)r;
+      const int32_t dst = ctr[key] + rank;
+      perm[dst] = (int32_t)r;
+      if (sr.pos != nullptr) {  // sorted per-row metadata, fused (pos writes coalesced)
+        sr.row_frame[dst] = __ldg(sr.frame_of + r / sr.K);
+        sr.row_tok[dst] = __ldg(sr.tokens + r);
+        sr.pos[r] = dst;
+      }
     }
     __syncwarp();
     if (live && (peers & lt) == 0) ctr[key] += __popc(peers);
@@ -307,16 +324,22 @@ key_sum4_kernel(const float4* __restrict__ piece_out, const int64_t* __restrict_
 }
 
 // Blocked grouping: Dk[key] = sum over blocks b (in order) of the pieces of the
-// composite key b * nkeys + key (in order).  One CTA per key: 64 float4 columns
-// x 16 block-lanes (lane l folds blocks b = l, l + 16, ...; a block's pieces
-// are a contiguous range, four loads in flight), lanes combined in order.
-constexpr int kFoldThreads = 1024;
+// composite key b * nkeys + key (in order).  Grid (key, split): CTA (key, q)
+// folds the contiguous block range q of the key into part[q][key] (64 float4
+// columns x 4 block-lanes, four loads in flight, lanes combined in order);
+// fold_parts_kernel then sums the kFoldSplit parts in order.  The chunk-start
+// key holds a piece per 256 transitions of every block: splitting its blocks
+// over CTAs keeps it off the critical path.
+constexpr int kFoldThreads = 256;
+constexpr int kFoldSplit = 8;
 __global__ void __launch_bounds__(kFoldThreads)
 fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
                            const int64_t* __restrict__ piece_off, int nkeys, int nblocks, int D4,
-                           float4* __restrict__ out) {
+                           float4* __restrict__ part) {
   __shared__ float4 s4[kFoldThreads];
-  const int key = blockIdx.x;
+  const int key = blockIdx.x, q = blockIdx.y;
+  const int b0 = (int)((int64_t)nblocks * q / kFoldSplit);
+  const int b1 = (int)((int64_t)nblocks * (q + 1) / kFoldSplit);
   const int span = D4 <= kFoldThreads && kFoldThreads % D4 == 0 ? D4 : kFoldThreads;
   const int sub = kFoldThreads / span;
   const int lr = threadIdx.x / span, lc = threadIdx.x % span;
@@ -326,7 +349,7 @@ fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
 #pragma unroll
     for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (d < D4) {
-      for (int b = lr; b < nblocks; b += sub) {
+      for (int b = b0 + lr; b < b1; b += sub) {
         const int64_t ck = (int64_t)b * nkeys + key;
         const int64_t p0 = __ldg(piece_off + ck), p1 = __ldg(piece_off + ck + 1);
         int64_t p = p0;
@@ -354,10 +377,22 @@ fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
         const float4 y = s4[s2 * span + threadIdx.x];
         r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
       }
-      out[(int64_t)key * D4 + d0 + threadIdx.x] = r;
+      part[((int64_t)q * nkeys + key) * D4 + d0 + threadIdx.x] = r;
     }
     __syncthreads();
   }
+}
+
+__global__ void fold_parts_kernel(const float4* __restrict__ part, int64_t n4, int64_t stride4,
+                                  float4* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  float4 r = part[i];
+  for (int q = 1; q < kFoldSplit; ++q) {
+    const float4 y = part[q * stride4 + i];
+    r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
+  }
+  out[i] = r;
 }
 
 // piece_key[p] = the composite key owning piece p
@@ -465,7 +500,9 @@ extern "C" int64_t accel_group_max_pieces(int64_t R, int nkeys) {
 // key); seg_off / piece_off [blocks * nkeys + 1].  cpb <= 0: one block.
 extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nkeys, int64_t cpb,
                                           int32_t* perm, int64_t* seg_off, int64_t* piece_off,
-                                          int32_t* piece_key, void* workspace,
+                                          int32_t* piece_key, const int32_t* frame_of,
+                                          const int32_t* tokens, int K, int32_t* row_frame,
+                                          int32_t* row_tok, int32_t* pos, void* workspace,
                                           size_t workspace_bytes, void* stream) {
   if (R < 0 || nkeys < 1) return fail(kDimension, "group_by_key: bad sizes");
   if (nkeys * (size_t)kWarps * sizeof(int) > 200 * 1024)
@@ -524,7 +561,10 @@ extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nk
     if ((st = post_launch("piece_keys_kernel"))) return st;
   }
   if (R == 0) return kOk;
-  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, base, perm);
+  SortedRows sr{frame_of, tokens, K, row_frame, row_tok, pos};
+  if (pos != nullptr && (!frame_of || !tokens || !row_frame || !row_tok || K < 1))
+    return fail(kDimension, "group_by_key: sorted rows need frame_of, tokens, outputs, K");
+  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, base, perm, sr);
   return post_launch("stable_scatter_kernel");
 }
 
@@ -532,21 +572,35 @@ extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nk
 extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int32_t* perm,
                                   int64_t* seg_off, int64_t* piece_off, void* workspace,
                                   size_t workspace_bytes, void* stream) {
-  return accel_group_by_key_blocked(keys, R, nkeys, 0, perm, seg_off, piece_off, nullptr,
-                                    workspace, workspace_bytes, stream);
+  return accel_group_by_key_blocked(keys, R, nkeys, 0, perm, seg_off, piece_off, nullptr, nullptr,
+                                    nullptr, 1, nullptr, nullptr, nullptr, workspace,
+                                    workspace_bytes, stream);
+}
+
+extern "C" size_t accel_fold_workspace_size(int nkeys, int D) {
+  return sizeof(float) * (size_t)kFoldSplit * nkeys * D;
 }
 
 // out[nkeys, D] = sum over blocks of the piece sums of composite keys b * nkeys + key
 extern "C" int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off,
-                                         int nkeys, int nblocks, int D, float* out, void* stream) {
+                                         int nkeys, int nblocks, int D, float* out,
+                                         void* workspace, void* stream) {
   if (nkeys < 1 || nblocks < 1 || D < 4 || (D & 3)) return fail(kDimension, "fold_blocked: bad sizes");
-  if (!piece_buf || !piece_off || !out) return fail(kDimension, "fold_blocked: NULL buffer");
-  if ((reinterpret_cast<uintptr_t>(piece_buf) | reinterpret_cast<uintptr_t>(out)) & 15)
+  if (!piece_buf || !piece_off || !out || !workspace)
+    return fail(kDimension, "fold_blocked: NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(piece_buf) | reinterpret_cast<uintptr_t>(out) |
+       reinterpret_cast<uintptr_t>(workspace)) & 15)
     return fail(kDimension, "fold_blocked: buffers must be 16B aligned");
-  fold_blocked_pieces_kernel<<<nkeys, kFoldThreads, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(piece_buf),
-                                                    piece_off, nkeys, nblocks, D / 4,
-                                                    reinterpret_cast<float4*>(out));
-  return post_launch("fold_blocked_pieces_kernel");
+  cudaStream_t s = as_stream(stream);
+  float4* part = static_cast<float4*>(workspace);
+  fold_blocked_pieces_kernel<<<dim3(nkeys, kFoldSplit), kFoldThreads, 0, s>>>(
+      reinterpret_cast<const float4*>(piece_buf), piece_off, nkeys, nblocks, D / 4, part);
+  int st = post_launch("fold_blocked_pieces_kernel");
+  if (st) return st;
+  const int64_t n4 = (int64_t)nkeys * (D / 4);
+  fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(part, n4, n4,
+                                                                reinterpret_cast<float4*>(out));
+  return post_launch("fold_parts_kernel");
 }
 
 // out[nkeys, D] = grouped sums of vals[R, D] rows; piece_buf holds

@@ -1122,83 +1122,116 @@ fact_group_sum_kernel(const float* __restrict__ h2w, const float* __restrict__ e
 // row loads per lane are in flight; same float operations per element as the
 // loss kernel.
 constexpr int kGs2Threads = 256;
+constexpr int kGs2Warps = kGs2Threads / 32;
+// LPR = A / 8 lanes per row (8 columns per lane, packed fp32x2 math), 32 / LPR
+// rows per warp, four rows in flight per lane.  The one-hot coef of a row is
+// added by the single lane owning the token's column into that lane's private
+// shared-memory slots (row order: deterministic), folded in at the end.
+template <int LPR>
 __global__ void __launch_bounds__(kGs2Threads)
 fact_group_sum2_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
                        const int32_t* __restrict__ row_frame, const int32_t* __restrict__ row_tok,
                        const float4* __restrict__ tsc_sorted, const int64_t* __restrict__ seg_off,
                        const int64_t* __restrict__ piece_off, const int32_t* __restrict__ piece_key,
-                       int nkeys, int key_mod, int A, float* __restrict__ piece_out) {
-  extern __shared__ __align__(16) float s_gs[];  // epp row [A] | partials [threads] float4
+                       int nkeys, int key_mod, float* __restrict__ piece_out) {
+  constexpr int A = LPR * 8;
+  constexpr int RPW = 32 / LPR;             // rows per warp
+  constexpr int RPC = RPW * kGs2Warps;      // rows in parallel per CTA
+  __shared__ __align__(16) float s_ep[A];
   __shared__ int s_frame[kGsRows], s_tok[kGsRows];
   __shared__ float4 s_sc[kGsRows];
+  __shared__ __align__(16) float s_patch[kGs2Threads][8];
+  __shared__ __align__(16) float4 s_part[kGs2Threads][2];
   const int64_t p = blockIdx.x;
   if (p >= __ldg(piece_off + nkeys)) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int key = __ldg(piece_key + p);
   const int64_t r0 = __ldg(seg_off + key) + (p - __ldg(piece_off + key)) * kGsRows;
   const int nr = (int)min(__ldg(seg_off + key + 1) - r0, (int64_t)kGsRows);
   const int64_t erow = key_mod > 0 ? key % key_mod : key;
-  for (int c = tid; c < A; c += kGs2Threads) s_gs[c] = __ldg(epp + erow * A + c);
+  for (int c = tid; c < A; c += kGs2Threads) s_ep[c] = __ldg(epp + erow * A + c);
   if (tid < nr) {
     s_frame[tid] = __ldg(row_frame + r0 + tid);
     s_tok[tid] = __ldg(row_tok + r0 + tid);
     s_sc[tid] = __ldg(tsc_sorted + r0 + tid);
   }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s_patch[tid][q] = 0.f;
   __syncthreads();
-  const int A4 = A >> 2;
-  const int span = A4 <= kGs2Threads && kGs2Threads % A4 == 0 ? A4 : kGs2Threads;
-  const int sub = kGs2Threads / span;
-  const int lr = tid / span, lc = tid % span;
-  float4* s_part = reinterpret_cast<float4*>(s_gs + A);
-  for (int c0 = 0; c0 < A4; c0 += span) {
-    const int c4 = c0 + lc;
-    float4 acc[4];
+  const int lc = lane % LPR;               // this lane's 8 columns: 8 lc .. 8 lc + 7
+  const int rw = warp * RPW + lane / LPR;  // first row of this lane
+  float2 ep2[4];
+  {
+    const float4 e0 = reinterpret_cast<const float4*>(s_ep)[2 * lc];
+    const float4 e1 = reinterpret_cast<const float4*>(s_ep)[2 * lc + 1];
+    ep2[0] = make_float2(e0.x, e0.y); ep2[1] = make_float2(e0.z, e0.w);
+    ep2[2] = make_float2(e1.x, e1.y); ep2[3] = make_float2(e1.z, e1.w);
+  }
+  const float2 l2e2 = make_float2(kLog2e, kLog2e);
+  float2 acc[2][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (c4 < A4) {
-      const float4 ep = reinterpret_cast<const float4*>(s_gs)[c4];
-      for (int r = lr; r < nr; r += 8 * sub) {
-        float4 h[8];
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int rr = r + u * sub;
-          h[u] = rr < nr ? __ldg(reinterpret_cast<const float4*>(h2w + (int64_t)s_frame[rr] * A) + c4)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+    for (int q = 0; q < 4; ++q) acc[u][q] = make_float2(0.f, 0.f);
+  auto row = [&](int r, const float4& h0, const float4& h1, float2 (&a)[4]) {
+    const float4 sc = s_sc[r];
+    const float2 h[4] = {make_float2(h0.x, h0.y), make_float2(h0.z, h0.w),
+                         make_float2(h1.x, h1.y), make_float2(h1.z, h1.w)};
+    const float2 n2 = make_float2(sc.x, sc.x), A2 = make_float2(sc.y, sc.y),
+                 C2 = make_float2(sc.z, sc.z);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int rr = r + u * sub;
-          if (rr < nr) {
-            const float4 sc = s_sc[rr];
-            const int tok = s_tok[rr];
-            const float d[4] = {h[u].x + ep.x, h[u].y + ep.y, h[u].z + ep.z, h[u].w + ep.w};
-            float o[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float d2 = fmaf(d[q], kLog2e, sc.x);
-              o[q] = ex2_ftz(d2) * fmaf(sc.y, d2, sc.z);
-            }
-            if ((tok >> 2) == c4) o[tok & 3] += sc.w;
-            float4& a4 = acc[u & 3];
-            a4.x += o[0]; a4.y += o[1]; a4.z += o[2]; a4.w += o[3];
-          }
-        }
-      }
+    for (int q = 0; q < 4; ++q) {
+      const float2 d2 = __ffma2_rn(__fadd2_rn(h[q], ep2[q]), l2e2, n2);
+      const float2 e2 = make_float2(ex2_ftz(d2.x), ex2_ftz(d2.y));
+      a[q] = __fadd2_rn(a[q], __fmul2_rn(e2, __ffma2_rn(A2, d2, C2)));
     }
-    float4 t = acc[0];
+    const int tok = s_tok[r];
+    if ((tok >> 3) == lc) s_patch[tid][tok & 7] += sc.w;  // one lane per row
+  };
+  auto hrow = [&](int r, float4& h0, float4& h1) {
+    const float4* hp = reinterpret_cast<const float4*>(h2w + (int64_t)s_frame[r] * A) + 2 * lc;
+    h0 = __ldg(hp);
+    h1 = __ldg(hp + 1);
+  };
+  int r = rw;
+  for (; r + 3 * RPC < nr; r += 4 * RPC) {  // four rows in flight, no predicates
+    float4 h[4][2];
 #pragma unroll
-    for (int u = 1; u < 4; ++u) { t.x += acc[u].x; t.y += acc[u].y; t.z += acc[u].z; t.w += acc[u].w; }
-    s_part[tid] = t;
-    __syncthreads();
-    if (tid < span && c0 + tid < A4) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s2 = 0; s2 < sub; ++s2) {
-        const float4 y = s_part[s2 * span + tid];
-        a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
-      }
-      reinterpret_cast<float4*>(piece_out + p * A)[c0 + tid] = a;
+    for (int u = 0; u < 4; ++u) hrow(r + u * RPC, h[u][0], h[u][1]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) row(r + u * RPC, h[u][0], h[u][1], acc[u & 1]);
+  }
+  for (; r < nr; r += RPC) {
+    float4 h0, h1;
+    hrow(r, h0, h1);
+    row(r, h0, h1, acc[0]);
+  }
+  // this lane's sums (+ its patch slots), then the RPC row-lanes of each column
+  // group are combined in a fixed order
+  {
+    float pt[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pt[q] = s_patch[tid][q];
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[2 * q] = (acc[0][q].x + acc[1][q].x) + pt[2 * q];
+      v[2 * q + 1] = (acc[0][q].y + acc[1][q].y) + pt[2 * q + 1];
     }
-    __syncthreads();
+    s_part[tid][0] = make_float4(v[0], v[1], v[2], v[3]);
+    s_part[tid][1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+  __syncthreads();
+  // thread t < 2 LPR: float4 column group t; sums the RPC row-lanes in order
+  if (tid < 2 * LPR) {
+    const int col = tid >> 1, half = tid & 1;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < RPC; ++j) {
+      const int t = (j / RPW) * 32 + (j % RPW) * LPR + col;  // lane holding row-lane j, column col
+      const float4 y = s_part[t][half];
+      o.x += y.x; o.y += y.y; o.z += y.z; o.w += y.w;
+    }
+    reinterpret_cast<float4*>(piece_out + p * A)[tid] = o;
   }
 }
 
@@ -1255,11 +1288,14 @@ extern "C" int accel_fact_group_sum2(const float* h2w, const float* epp, const i
     return fail(kDimension, "fact_group_sum2: NULL buffer");
   if (misaligned16(h2w) || misaligned16(epp) || misaligned16(tsc_sorted) || misaligned16(piece_out))
     return fail(kDimension, "fact_group_sum2: buffers must be 16B aligned");
-  const size_t smem = (size_t)A * 4 + kGs2Threads * sizeof(float4);
-  fact_group_sum2_kernel<<<(unsigned)n_pieces_max, kGs2Threads, smem, as_stream(stream)>>>(
-      h2w, epp, row_frame, row_tok, static_cast<const float4*>(tsc_sorted), seg_off, piece_off,
-      piece_key, nkeys, key_mod, A, piece_out);
-  return post_launch("fact_group_sum2_kernel");
+  if (A != 128 && A != 256) return fail(kDimension, "fact_group_sum2: A must be 128 or 256");
+  auto go = [&](auto kernel) {
+    kernel<<<(unsigned)n_pieces_max, kGs2Threads, 0, as_stream(stream)>>>(
+        h2w, epp, row_frame, row_tok, static_cast<const float4*>(tsc_sorted), seg_off, piece_off,
+        piece_key, nkeys, key_mod, piece_out);
+    return post_launch("fact_group_sum2_kernel");
+  };
+  return A == 256 ? go(fact_group_sum2_kernel<32>) : go(fact_group_sum2_kernel<16>);
 }
 
 extern "C" int accel_sorted_rows(const int32_t* perm, const int32_t* frame_of,

@@ -175,7 +175,9 @@ class Grouping:
     touches one block of rows at a time (accel_group_by_key_blocked); the key
     sums then fold the blocks in order (accel_fold_blocked_pieces)."""
 
-    def __init__(self, keys, nkeys: int, cpb: int = 0):
+    def __init__(self, keys, nkeys: int, cpb: int = 0, rows=None):
+        """rows = (frame_of, tokens, K): also build the sorted per-row metadata
+        (row_frame, row_tok, pos) inside the scatter (see sort_rows)."""
         R = keys.numel()
         dev = keys.device
         lib = _lib.lib()
@@ -190,14 +192,23 @@ class Grouping:
                           if cpb > 0 else None)
         nbytes = lib.accel_group_workspace_size_blocked(R, nkeys, self.cpb)
         buf = workspace("group").get(nbytes)
+        fo = tk = None
+        K = 1
+        self.row_frame = self.row_tok = self.pos = None
+        if rows is not None:
+            fo, tk, K = rows
+            self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
+            self.row_tok = torch.empty(max(R, 1), dtype=I32, device=dev)
+            self.pos = torch.empty(max(R, 1), dtype=I32, device=dev)
         _lib.call("accel_group_by_key_blocked", _p(keys), R, nkeys, self.cpb, _p(self.perm),
-                  _p(self.seg_off), _p(self.piece_off), _p(self.piece_key), _p(buf), buf.numel(),
-                  _stream())
+                  _p(self.seg_off), _p(self.piece_off), _p(self.piece_key), _p(fo), _p(tk),
+                  int(K), _p(self.row_frame), _p(self.row_tok), _p(self.pos), _p(buf),
+                  buf.numel(), _stream())
 
     def sort_rows(self, frame_of, tokens, K):
         """Sorted per-row metadata of a (prev, k) grouping: row_frame, row_tok and
         the inverse permutation pos (fixed per batch)."""
-        if getattr(self, "pos", None) is None:
+        if self.pos is None:
             dev = self.perm.device
             R = self.R
             self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
@@ -239,8 +250,9 @@ class Grouping:
 
     def _key_pass(self, piece_buf, D, out):
         if self.cpb > 0:
+            wsb = workspace("fold").get(_lib.lib().accel_fold_workspace_size(self.nkeys, D))
             _lib.call("accel_fold_blocked_pieces", _p(piece_buf), _p(self.piece_off), self.nkeys,
-                      self.nblocks, D, _p(out), _stream())
+                      self.nblocks, D, _p(out), _p(wsb), _stream())
         else:
             _lib.call("accel_grouped_rows_sum", None, self.R, D, _p(self.perm), _p(self.seg_off),
                       _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
