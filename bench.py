@@ -32,6 +32,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+WORKLOAD_CFG4 = ("cfg4 trainer step: OpenVLA-7B-shaped policy/value heads (obs = hidden = 4096, "
+                 "K=7, A=256 slim head, value mlp 32), 64 trajectories x 128 steps per GPU, GIPO "
+                 "trust arm, revalue on")
 METRIC = "trainer transitions/sec"
 UNIT = "transitions/s"
 WORKLOAD = ("cfg2 trainer step: LIBERO-Long ragged trajectories (50% success T~U[1,520] done, "
@@ -53,11 +56,19 @@ def parse():
                     help="store: K4 writes dz rows; recompute: token scalars + frame-blocked "
                          "recomputing grouped sums")
     ap.add_argument("--block-chunks", type=int, default=64)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"],
+                    help="cfg2: LIBERO-Long ragged batch, D = 64 (the headline); cfg4: "
+                         "OpenVLA-7B-shaped heads O = D = 4096, 64 x 128 transitions per GPU")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
+_WL = {"name": "cfg2"}
+
+
 def dims():
+    if _WL["name"] == "cfg4":  # OpenVLA-7B-shaped heads
+        return dict(K=7, A=256, D=4096, O=4096, H=32)
     return dict(K=7, A=256, D=64, O=195, H=32)
 
 
@@ -119,6 +130,8 @@ def make_bundle(seed: int, n_steps: int):
 
 
 def lengths_for(seed: int, rank: int, n: int, horizon: int):
+    if _WL["name"] == "cfg4":  # 64 trajectories x 128 steps per GPU, done alternating
+        return np.full(64, 128, dtype=np.int64), np.arange(64) % 2 == 0
     from paper_2603_18464_b200.workload import libero_long_lengths
     return libero_long_lengths(np.random.default_rng(np.random.SeedSequence([seed, rank, 11])), n,
                                horizon)
@@ -291,7 +304,7 @@ def run_reference(args, rank: int, world: int):
     import torch  # noqa: F401  (device-free: generation on the host)
     d = dims()
     lens, done = lengths_for(args.seed, 0, args.n_traj, args.horizon)
-    n_steps = args.horizon + 2
+    n_steps = 522 if args.workload == "cfg4" else args.horizon + 2
     bundle = make_bundle(args.seed, n_steps)
     from paper_2603_18464_b200.workload import synthetic_packed, unpack_trajectories
     from threadpoolctl import threadpool_limits
@@ -332,6 +345,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    _WL["name"] = args.workload
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -352,7 +366,7 @@ def main():
         from paper_2603_18464_b200.dp import DataParallel
         comm = DataParallel()
     d = dims()
-    n_steps = args.horizon + 2
+    n_steps = 522 if args.workload == "cfg4" else args.horizon + 2
     lens, done = lengths_for(args.seed, rank, args.n_traj, args.horizon)
     N = int(lens.sum())
     n = len(lens)
@@ -488,7 +502,8 @@ def main():
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded N(0,1) obs/values/rewards/behavior logits, U[0,A) tokens, "
                 "random-init policy/value heads)",
-        "config": {"workload": WORKLOAD, "trajectories_per_gpu": n, "transitions_per_gpu": N,
+        "config": {"workload": WORKLOAD if args.workload == "cfg2" else WORKLOAD_CFG4,
+                   "trajectories_per_gpu": n, "transitions_per_gpu": N,
                    "tokens_per_gpu": M, "parallelism": f"dp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (behavior logits alone 11+ GB per GPU)"},
         "roofline": {"kernel": "token_loss_fact (fused GIPO fwd+bwd, factorized head)"
