@@ -355,6 +355,11 @@ int accel_wm_adam(double* params, const double* grads, double* m, double* v, int
                   double lr, double beta1, double beta2, double eps, int64_t t, unsigned* bad,
                   void* stream);
 
+/* 3xTF32 operand split (x f32[n], n % 4 == 0): hi = x rounded to TF32, lo =
+ * x - hi; products wider than the resident-weight tcgen05 kernels run as
+ * hi.hi + hi.lo + lo.hi TF32 library GEMMs accumulated in fp32. */
+int accel_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream);
+
 /* ---- tensor-core GEMM (tcgen05, 3xTF32: fp32-accurate) ----------------- */
 
 /* Streaming multiprocessors on the current device (persistent-grid size;

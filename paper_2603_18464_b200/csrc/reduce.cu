@@ -273,3 +273,48 @@ extern "C" int accel_count_nonfinite_rows(const float* x, const int32_t* rows, i
   count_nonfinite_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, rows, R, C, ld, count);
   return post_launch("count_nonfinite_rows_kernel");
 }
+
+// ---- 3xTF32 operand split for the wide-layer library GEMMs ------------------
+// hi = x rounded to TF32 (10-bit mantissa, round-half-away on the magnitude
+// bits), lo = x - hi (exact in fp32).  A product then runs as three TF32
+// tensor-core GEMMs, hi.hi + hi.lo + lo.hi, accumulated in fp32: about fp32
+// accuracy (the dropped lo.lo term and the TF32 truncation of lo are below
+// 2^-20 relative) at tensor-core rate.  Non-finite inputs pass through hi.
+namespace accel {
+namespace {
+__global__ void split_tf32_kernel(const float4* __restrict__ x, int64_t n4, float4* __restrict__ hi,
+                                  float4* __restrict__ lo) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = x[i];
+    float h[4];
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned b = __float_as_uint(e[j]);
+      const bool fin = (b & 0x7f800000u) != 0x7f800000u;
+      h[j] = fin ? __uint_as_float((b + 0x1000u) & 0xffffe000u) : e[j];
+    }
+    hi[i] = make_float4(h[0], h[1], h[2], h[3]);
+    lo[i] = make_float4(isfinite(e[0]) ? e[0] - h[0] : 0.f, isfinite(e[1]) ? e[1] - h[1] : 0.f,
+                        isfinite(e[2]) ? e[2] - h[2] : 0.f, isfinite(e[3]) ? e[3] - h[3] : 0.f);
+  }
+}
+}  // namespace
+}  // namespace accel
+
+extern "C" int accel_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream) {
+  using namespace accel;
+  if (n < 0 || (n & 3)) return fail(kDimension, "split_tf32: n must be a multiple of 4");
+  if (n == 0) return kOk;
+  if (!x || !hi || !lo) return fail(kDimension, "split_tf32: NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
+       reinterpret_cast<uintptr_t>(lo)) & 15)
+    return fail(kDimension, "split_tf32: buffers must be 16B aligned");
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>(ceil_div(n4, 256), (int64_t)kNumSMs * 8);
+  split_tf32_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(x), n4,
+                                                         reinterpret_cast<float4*>(hi),
+                                                         reinterpret_cast<float4*>(lo));
+  return post_launch("split_tf32_kernel");
+}

@@ -439,11 +439,55 @@ def tc_rows_supported(K: int, N: int) -> bool:
     return K <= 256 and N <= 256
 
 
+def split_tf32(x):
+    """(hi, lo) of a float32 tensor (accel_split_tf32); same shape, contiguous."""
+    x = x.contiguous()
+    if x.numel() % 4 or x.data_ptr() % 16:
+        x = x.clone()
+    n = x.numel()
+    pad = (-n) % 4
+    src = x.reshape(-1) if not pad else torch.cat([x.reshape(-1), x.new_zeros(pad)])
+    hi, lo = torch.empty_like(src), torch.empty_like(src)
+    _lib.call("accel_split_tf32", _p(src), src.numel(), _p(hi), _p(lo), _stream())
+    return hi[:n].view(x.shape), lo[:n].view(x.shape)
+
+
+class _TF32:
+    """Temporarily let cuBLAS use TF32 tensor cores (the trainer keeps it off)."""
+
+    def __enter__(self):
+        self.prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+
+    def __exit__(self, *exc):
+        torch.backends.cuda.matmul.allow_tf32 = self.prev
+        return False
+
+
+def mm_3xtf32(a, b, out, accumulate=False):
+    """out (+)= a @ b for wide float32 products: three TF32 tensor-core library
+    GEMMs on split operands, hi.hi + hi.lo + lo.hi, fp32 accumulation (about
+    fp32 accuracy: tests/test_trainer_gpu.py::test_wide_layers_match_oracle).
+    a / b may be transposed views of contiguous tensors: the split keeps it."""
+    def split(t):
+        if not t.is_contiguous() and t.t().is_contiguous():  # a transposed view
+            hi, lo = split_tf32(t.t())
+            return hi.t(), lo.t()
+        return split_tf32(t)
+    ah, al = split(a)
+    bh, bl = split(b)
+    with _TF32():
+        if accumulate:
+            out.addmm_(ah, bh)
+        else:
+            torch.mm(ah, bh, out=out)
+        out.addmm_(ah, bl)
+        out.addmm_(al, bh)
+    return out
+
+
 def _mm_fallback(x, w_t, out, bias=None, tanh=False, accumulate=False):
-    if accumulate:
-        out.addmm_(x, w_t)
-    else:
-        torch.mm(x, w_t, out=out)
+    mm_3xtf32(x, w_t, out, accumulate=accumulate)
     if bias is not None:
         out.add_(bias)
     if tanh:
@@ -532,7 +576,7 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     F, n = dy.shape
     k = x.shape[1]
     if n > 256 or k > 256:
-        return torch.mm(dy.t(), x, out=out)
+        return mm_3xtf32(dy.t(), x, out)
     dy, x = pitched(dy), pitched(x)
     if kslices is None:
         kslices = max(1, min(tc_sm_count(), -(-F // 32)))

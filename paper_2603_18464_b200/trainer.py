@@ -682,9 +682,9 @@ class Trainer:
         the caller fills); returns the reduce_segments entry that sums them."""
         F, n = dy.shape
         k = x.shape[1]
-        if n > 256 or k > 256:  # wide layers (cfg4): cuBLAS fp32, one "partial" = the result
+        if n > 256 or k > 256:  # wide layers (cfg4): 3xTF32 library GEMMs, one "partial"
             part = self.scratch.get("wg." + tag, (1 + extra, n, k))
-            torch.mm(dy.t(), x, out=part[0])
+            ops.mm_3xtf32(dy.t(), x, part[0])
             return (part, out, 1 + extra, n * k, n * k)
         dy, x = ops.pitched(dy), ops.pitched(x)  # no-ops at aligned widths
         ks = max(1, min(ops.tc_sm_count(), -(-F // 32)))
