@@ -1,0 +1,221 @@
+"""On-device replay buffer for the train-batch prefetcher.
+
+Reference: `ReplayBuffer` (buffers.py:44-94) -- a bounded FIFO of immutable
+trajectories, uniform sampling with replacement -- feeding `Prefetcher`
+(buffers.py:125-186), whose builder packs the sampled trajectories on the host
+and (here) uploads them every batch.  `DeviceReplayBuffer` keeps the same API
+(`push`, `sample(n, rng)`, `stats`, `len`, kind checks, FIFO eviction at
+`capacity` trajectories) but copies each trajectory into HBM once, on push, into
+contiguous frame / transition spans of a ring arena.  `sample` draws exactly as
+the reference (`rng.integers`) and returns `DeviceTrajectory` handles; the
+trainer's `build_train_batch` recognises them and assembles the packed batch
+with on-device row gathers (`gather`), so neither the host pack nor the
+per-batch host-to-device copy sits on the build path.  The reference
+`Prefetcher` runs unchanged on top (it only calls stats / sample / builder).
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .errors import DimensionError
+
+_ACCEPTED_SOURCE = {"main": "real", "world_model": "real", "imagined": "imagined"}
+
+
+class BufferKindError(ValueError):
+    """A trajectory of the wrong source for the buffer (buffers.py:30-31)."""
+
+
+@dataclass(frozen=True)
+class BufferStats:  # buffers.py:34-40
+    size: int
+    pushed: int
+    sampled: int
+    evicted: int
+
+
+class SpanRing:
+    """Ring allocator of contiguous spans (host logic, CPU-testable).
+
+    alloc(n) returns the start of n contiguous slots; a span never wraps (it
+    restarts at 0 when the tail is too short) and every live span it overlaps
+    is reported for eviction.  With an arena of at least capacity x (longest
+    trajectory + 1) slots no span is ever evicted this way, and the buffer's
+    contents (hence its sampling) follow the reference's FIFO exactly."""
+
+    def __init__(self, size: int) -> None:
+        self.size = int(size)
+        self.head = 0
+        self.live: list = []  # (start, length, owner) oldest first
+
+    def alloc(self, n: int, owner) -> tuple:
+        if n > self.size:
+            raise DimensionError(f"span of {n} exceeds the arena ({self.size})")
+        start = self.head if self.head + n <= self.size else 0
+        end = start + n
+        evicted = [o for s, ln, o in self.live if s < end and start < s + ln]
+        if evicted:
+            self.live = [x for x in self.live if not (x[0] < end and start < x[0] + x[1])]
+        self.live.append((start, n, owner))
+        self.head = end
+        return start, evicted
+
+    def release(self, owner) -> None:
+        self.live = [x for x in self.live if x[2] is not owner]
+
+
+class DeviceTrajectory:
+    """Handle of a trajectory resident in a DeviceReplayBuffer arena (duck-types
+    the reference Trajectory's metadata: t_len, done, source, task_id,
+    behavior_version, episode_return)."""
+
+    __slots__ = ("buffer", "f0", "t0", "t_len", "done", "source", "task_id", "behavior_version",
+                 "episode_return", "alive")
+
+    def __init__(self, buffer, f0, t0, traj) -> None:
+        self.buffer = buffer
+        self.f0, self.t0 = f0, t0
+        self.t_len = int(traj.tokens.shape[0])
+        self.done = bool(traj.done)
+        self.source = traj.source
+        self.task_id = int(getattr(traj, "task_id", 0))
+        self.behavior_version = int(getattr(traj, "behavior_version", 0))
+        self.episode_return = float(np.sum(traj.rewards))
+        self.alive = True
+
+
+class DeviceReplayBuffer:
+    """Bounded FIFO of trajectories resident in HBM, uniform sampling."""
+
+    def __init__(self, kind: str, capacity: int, obs_dim: int, chunk_len: int, n_actions: int,
+                 max_transitions: int, device=None) -> None:
+        if kind not in _ACCEPTED_SOURCE:
+            raise BufferKindError(f"unknown buffer kind {kind!r}")
+        if capacity < 1:
+            raise ValueError(f"capacity must be >= 1, got {capacity}")
+        self.kind, self.capacity = kind, int(capacity)
+        self.O, self.K, self.A = int(obs_dim), int(chunk_len), int(n_actions)
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        cap_t = int(max_transitions)
+        cap_f = cap_t + self.capacity  # a bootstrap frame per trajectory
+        f32 = torch.float32
+        self.frames = ops.alloc_pitched(cap_f, self.O, dev)   # [cap_f, O] view, aligned rows
+        self.steps = torch.zeros(cap_f, dtype=torch.int32, device=dev)
+        self.values = torch.zeros(cap_f, dtype=f32, device=dev)  # values + bootstrap last
+        self.rewards = torch.zeros(cap_t, dtype=f32, device=dev)
+        self.tokens = torch.zeros(cap_t, self.K, dtype=torch.int32, device=dev)
+        self.mu = torch.zeros(cap_t, self.K * self.A, dtype=f32, device=dev)
+        self._fring, self._tring = SpanRing(cap_f), SpanRing(cap_t)
+        self._items: list = []
+        self._lock = threading.Lock()
+        self._pushed = self._sampled = self._evicted = 0
+
+    # -- reference API ---------------------------------------------------------------
+    def push(self, traj) -> None:
+        """Append one completed trajectory (one host-to-device copy per field)."""
+        expected = _ACCEPTED_SOURCE[self.kind]
+        if traj.source != expected:
+            raise BufferKindError(
+                f"buffer {self.kind!r} accepts source {expected!r}, got {traj.source!r}")
+        T = int(traj.tokens.shape[0])
+        obs = np.asarray(traj.observations)
+        if obs.shape != (T + 1, self.O) or np.asarray(traj.behavior_logits).shape != (T, self.K,
+                                                                                        self.A):
+            raise DimensionError("trajectory shapes do not match the buffer")
+        with self._lock:
+            if len(self._items) >= self.capacity:
+                self._evict(self._items[0])
+            h = DeviceTrajectory(self, 0, 0, traj)
+            f0, ev_f = self._fring.alloc(T + 1, h)
+            t0, ev_t = self._tring.alloc(T, h)
+            for o in ev_f + ev_t:
+                if o.alive:
+                    self._evict(o)
+            h.f0, h.t0 = f0, t0
+            dev = self.device
+            t = lambda a, dt: torch.tensor(np.asarray(a), dtype=dt).to(dev)
+            self.frames[f0:f0 + T + 1].copy_(t(obs, torch.float32))
+            self.steps[f0:f0 + T + 1].copy_(t(traj.steps, torch.int32))
+            self.values[f0:f0 + T].copy_(t(traj.values, torch.float32))
+            self.values[f0 + T] = float(traj.bootstrap_value)
+            self.rewards[t0:t0 + T].copy_(t(traj.rewards, torch.float32))
+            self.tokens[t0:t0 + T].copy_(t(traj.tokens, torch.int32))
+            self.mu[t0:t0 + T].copy_(t(np.asarray(traj.behavior_logits).reshape(T, -1),
+                                       torch.float32))
+            self._items.append(h)
+            self._pushed += 1
+
+    def _evict(self, h) -> None:
+        h.alive = False
+        self._items.remove(h)
+        self._fring.release(h)
+        self._tring.release(h)
+        self._evicted += 1
+
+    def sample(self, n: int, rng: np.random.Generator):
+        """n uniform picks with replacement; None signals not-ready (buffers.py:74-86)."""
+        if n < 0:
+            raise ValueError(f"sample size must be >= 0, got {n}")
+        if n == 0:
+            return []
+        with self._lock:
+            if len(self._items) < n:
+                return None
+            idx = rng.integers(0, len(self._items), size=n)
+            picks = [self._items[i] for i in idx]
+            self._sampled += n
+        return picks
+
+    def __len__(self) -> int:
+        with self._lock:
+            return len(self._items)
+
+    def stats(self) -> BufferStats:
+        with self._lock:
+            return BufferStats(len(self._items), self._pushed, self._sampled, self._evicted)
+
+    # -- batch assembly on the device --------------------------------------------------
+    def gather(self, handles) -> dict:
+        """Packed CSR batch (the layout of trainer.upload) of the sampled handles,
+        by on-device row gathers of their arena spans."""
+        if any(not h.alive for h in handles):
+            raise DimensionError("a sampled trajectory was evicted before the batch was built")
+        dev = self.device
+        lens = np.array([h.t_len for h in handles], dtype=np.int64)
+        n = len(handles)
+        off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens, out=off[1:])
+        N = int(off[-1])
+        lens_d = torch.from_numpy(lens).to(dev)
+        f0 = torch.tensor([h.f0 for h in handles], dtype=torch.int64, device=dev)
+        t0 = torch.tensor([h.t0 for h in handles], dtype=torch.int64, device=dev)
+        off_d = torch.from_numpy(off).to(dev)
+        # frame rows: f0[s] + j for j in [0, T_s]; transition rows: t0[s] + j, j < T_s
+        fcount = lens_d + 1
+        fstart = torch.repeat_interleave(f0 - (off_d[:-1] + torch.arange(n, device=dev)), fcount)
+        fidx = fstart + torch.arange(N + n, device=dev)
+        tstart = torch.repeat_interleave(t0 - off_d[:-1], lens_d)
+        tidx = tstart + torch.arange(N, device=dev)
+        frames = ops.alloc_pitched(N + n, self.O, dev)
+        full = self.frames.as_strided((self.frames.shape[0], self.frames.stride(0)),
+                                      (self.frames.stride(0), 1))  # the pitched rows
+        torch.index_select(full, 0, fidx, out=frames.as_strided(
+            (N + n, frames.stride(0)), (frames.stride(0), 1)))
+        return {
+            "traj_off": off_d,
+            "frames": frames,
+            "steps": self.steps.index_select(0, fidx),
+            "values": self.values.index_select(0, fidx),
+            "tokens": self.tokens.index_select(0, tidx).reshape(-1),
+            "rewards": self.rewards.index_select(0, tidx),
+            "mu": self.mu.index_select(0, tidx).reshape(N * self.K, self.A),
+            "done": torch.tensor([h.done for h in handles], dtype=torch.uint8, device=dev),
+        }, int(sum(h.source == "real" for h in handles)), \
+            np.array([h.behavior_version for h in handles], dtype=np.int64)

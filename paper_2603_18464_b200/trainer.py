@@ -30,6 +30,7 @@ from .batch import DeviceTrainBatch
 from .errors import AccelError, DimensionError, DomainError, NonFiniteError
 from .params import AdamStateView, DeviceParams, Dims, FlatLayout, POLICY_NAMES, VALUE_NAMES
 from .publish import OBS_MODEL, POLICY, REWARD_MODEL, VersionedWeights
+from .replay import DeviceTrajectory
 from .world_model import DeviceMlp2, obs_model_data, reward_model_data
 from .workload import PackedBatch, pack_trajectories
 
@@ -570,6 +571,16 @@ class Trainer:
         """Recompute, estimate advantages, normalize globally, tensorize."""
         if isinstance(trajs, PackedBatch):
             pb = trajs
+        elif trajs and isinstance(trajs[0], DeviceTrajectory):
+            # sampled from a DeviceReplayBuffer: the batch is gathered in HBM
+            buf = trajs[0].buffer
+            if any(not isinstance(t, DeviceTrajectory) or t.buffer is not buf for t in trajs):
+                raise DimensionError("a batch mixes trajectories of different replay buffers")
+            if self.cfg.revalue:
+                for t in trajs:
+                    assert self.publish_version >= t.behavior_version
+            b, n_real, bver = buf.gather(trajs)
+            return self.build_from_device(b, n_real=n_real, behavior_version=bver)
         else:
             for t in trajs:
                 if self.cfg.revalue:
