@@ -66,4 +66,10 @@ def test_device_replay_matches_host_build():
         np.testing.assert_array_equal(getattr(bd, k), getattr(bh, k), err_msg=k)
     assert (bd.n_real, bd.behavior_lag_mean) == (bh.n_real, bh.behavior_lag_mean)
     rd, rh = tr_dev.train_step(bd), tr_host.train_step(bh)
-    assert rd == rh
+    # parameters are bitwise equal; the loss kernel's float64 statistics are summed
+    # in the order its dynamic schedule hands out transitions (last-bit differences)
+    assert set(rd) == set(rh)
+    for k in rd:
+        assert abs(rd[k] - rh[k]) <= 1e-12 * max(1.0, abs(rh[k])), k
+    np.testing.assert_array_equal(tr_dev.params.p[tr_dev.params.cur].cpu().numpy(),
+                                  tr_host.params.p[tr_host.params.cur].cpu().numpy())
