@@ -93,7 +93,9 @@ class DataParallel:
 
     def adam(self, params, n_policy: int, hyp: tuple, skip, bad, adam_fn=None) -> None:
         """Reduce-scatter the gradients, Adam on this rank's shard (ping-pong
-        generation cur -> nxt), all-gather the new parameters and moments."""
+        generation cur -> nxt), all-gather the new parameters.  The Adam moments
+        stay sharded (ZeRO-2: a rank only ever reads its own shard of them);
+        `gather_moments` assembles them when a caller needs the full state."""
         fn = adam_fn or self._adam_fn
         cur, nxt = params.cur, params.cur ^ 1
         total = params.p[cur].numel()
@@ -103,7 +105,14 @@ class DataParallel:
         fn(params.p[cur][lo:hi], g_shard, params.m[cur][lo:hi], params.v[cur][lo:hi],
            params.p[nxt][lo:hi], params.m[nxt][lo:hi], params.v[nxt][lo:hi], n0, hyp[0], hyp[1],
            skip, bad)
-        for buf in (params.p[nxt], params.m[nxt], params.v[nxt]):
+        self.all_gather(params.p[nxt][lo:hi].clone(), params.p[nxt])
+
+    def gather_moments(self, params) -> None:
+        """Collective: every rank's shard of the current Adam moments into the
+        full buffers (for inspection / checkpointing; not on the step path)."""
+        cur = params.cur
+        lo, hi = self.shard_bounds(params.m[cur].numel())
+        for buf in (params.m[cur], params.v[cur]):
             self.all_gather(buf[lo:hi].clone(), buf)
 
 

@@ -382,6 +382,12 @@ class Trainer:
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
 
+    def gather_moments(self) -> None:
+        """Collective under data parallelism: assemble the sharded Adam moments
+        so `adam_policy.m` / `.v` show the full state (a no-op on one GPU)."""
+        if self.comm is not None:
+            self.comm.gather_moments(self.params)
+
     def _pk_cpb(self) -> int:
         # the frame-blocked recompute rides on the two-phase loss kernel's sorted
         # scalar output (K <= 8, A in {128, 256})

@@ -106,6 +106,8 @@ def _worker(rank, world, port, out_q):
         skip = torch.zeros(1, dtype=torch.int32)
         bad = torch.zeros(1, dtype=torch.int32)
         dp.adam(params, n_policy, hyp, skip, bad)
+        params.cur = 1  # the trainer flips to the new generation
+        dp.gather_moments(params)  # moments stay sharded on the step path
         # C1: pooled statistics from per-rank sums
         x = torch.arange(10, dtype=torch.float64) * (rank + 1)
         sums = torch.tensor([x.sum().item(), (x * x).sum().item(), float(x.numel())],
@@ -114,7 +116,7 @@ def _worker(rank, world, port, out_q):
         mx = torch.tensor([float(rank)], dtype=torch.float64)
         dp.all_reduce_max(mx)
         out_q.put((rank, params.p[1].clone(), sums, mx, dp.shard_bounds(total),
-                   dp.global_counts(7 + rank, 3)))
+                   dp.global_counts(7 + rank, 3), params.m[1].clone(), params.v[1].clone()))
     finally:
         dist.destroy_process_group()
 
@@ -133,6 +135,8 @@ def test_zero2_adam_and_collectives_gloo():
                hyp[0], hyp[1], torch.zeros(1, dtype=torch.int32), None)
     for r in range(world):
         torch.testing.assert_close(res[r][0], ref.p[1], rtol=0, atol=1e-7)
+        torch.testing.assert_close(res[r][5], ref.m[1], rtol=0, atol=1e-7)
+        torch.testing.assert_close(res[r][6], ref.v[1], rtol=0, atol=1e-9)
         xs = [torch.arange(10, dtype=torch.float64) * (q_ + 1) for q_ in range(world)]
         allx = torch.cat(xs)
         assert res[r][1].tolist() == pytest.approx([allx.sum().item(), (allx * allx).sum().item(),
