@@ -134,6 +134,11 @@ int accel_token_loss(const float* logits, const float* bias, const int32_t* toke
  * rows), lp_new, stat_part/max_part as accel_token_loss (grid =
  * accel_fact_grid(N)).  fix_stats: FIXUP pass as accel_token_loss. */
 int accel_fact_grid(int64_t N);
+/* Rows of stat_part / max_part accel_token_loss_fact(2) writes for these sizes:
+ * one per 32-transition chunk for the two-phase kernel (K <= 8, A in {128, 256};
+ * fixed rows under its dynamic schedule, so the pooled statistics are bitwise
+ * reproducible), accel_fact_grid(N) per-CTA rows otherwise. */
+int64_t accel_fact_partials(int64_t N, int K, int A, int scalar_out);
 /* epp[(prev*K+k)*A + a] = ep[prev*A + a] + pp[k*A + a] + bias[a] */
 int accel_ep_plus(const float* ep, const float* pp, const float* bias, int A, int K,
                   float* epp, void* stream);

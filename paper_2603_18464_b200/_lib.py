@@ -38,6 +38,7 @@ _SIGNATURES = {
     "accel_tanh_grad_colsum": (c_int, [P, P, c_int64, c_int, P, c_int, P]),
     "accel_prev_keys": (c_int, [P, c_int64, c_int, c_int, c_int, P, P]),
     "accel_fact_grid": (c_int, [c_int64]),
+    "accel_fact_partials": (c_int64, [c_int64, c_int, c_int, c_int]),
     "accel_ep_plus": (c_int, [P, P, P, c_int, c_int, P, P]),
     "accel_token_loss_fact": (c_int, [P, P, P, P, P, P, c_int64, c_int, c_int, c_int,
                                       c_double, c_double, c_double, c_double, P, P, P, P, P, P,

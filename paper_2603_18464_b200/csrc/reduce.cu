@@ -101,6 +101,44 @@ reduce_f64_kernel(const double* __restrict__ part, int64_t parts, int width, int
   }
 }
 
+// Level 1 of the two-level reduction for many partial rows: CTA b folds the
+// contiguous rows [b per, (b+1) per) (all <= 8 columns per pass, thread order
+// fixed, shared-memory tree per column) into tmp[b][width].
+constexpr int kRedThreads = 256;
+constexpr int kRedMaxCtas = 296;
+__device__ double g_red_tmp[kRedMaxCtas * 8];  // level-1 partials (one stream at a time)
+
+__global__ void __launch_bounds__(kRedThreads)
+reduce_f64_rows_kernel(const double* __restrict__ part, int64_t parts, int width, int mode,
+                       int64_t per, double* __restrict__ tmp) {
+  __shared__ double s[kRedThreads];
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(parts, r0 + per);
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = mode ? -CUDART_INF : 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += kRedThreads) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < width) {
+        const double v = __ldg(part + r * width + c);
+        acc[c] = mode ? fmax(acc[c], v) : acc[c] + v;
+      }
+    }
+  }
+  for (int c = 0; c < width; ++c) {
+    s[threadIdx.x] = acc[c];
+    __syncthreads();
+    for (int o = kRedThreads / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o)
+        s[threadIdx.x] = mode ? fmax(s[threadIdx.x], s[threadIdx.x + o])
+                              : s[threadIdx.x] + s[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) tmp[(int64_t)blockIdx.x * width + c] = s[0];
+    __syncthreads();
+  }
+}
+
 struct FinalizeParams {
   int algo;
   double lambda_v, lambda_h, n_tokens, n_transitions;
@@ -213,7 +251,20 @@ extern "C" int accel_reduce_f64(const double* part, int64_t parts, int width, in
   if (parts < 0 || width < 1 || (mode != 0 && mode != 1))
     return fail(kDimension, "reduce_f64: bad arguments");
   if (!part || !out) return fail(kDimension, "reduce_f64: NULL buffer");
-  reduce_f64_kernel<<<1, 1024, 0, as_stream(stream)>>>(part, parts, width, mode, out);
+  cudaStream_t s = as_stream(stream);
+  if (parts > 8192 && width <= 8) {  // many rows: two levels, both in a fixed order
+    const int ctas = (int)std::min<int64_t>(kRedMaxCtas, ceil_div(parts, 4096));
+    const int64_t per = ceil_div(parts, ctas);
+    double* tmp = nullptr;
+    int st = check_cuda(cudaGetSymbolAddress(reinterpret_cast<void**>(&tmp), g_red_tmp),
+                        "reduce_f64 scratch");
+    if (st) return st;
+    reduce_f64_rows_kernel<<<ctas, kRedThreads, 0, s>>>(part, parts, width, mode, per, tmp);
+    if ((st = post_launch("reduce_f64_rows_kernel"))) return st;
+    reduce_f64_kernel<<<1, 1024, 0, s>>>(tmp, ctas, width, mode, out);
+    return post_launch("reduce_f64_kernel");
+  }
+  reduce_f64_kernel<<<1, 1024, 0, s>>>(part, parts, width, mode, out);
   return post_launch("reduce_f64_kernel");
 }
 

@@ -632,7 +632,7 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
 // copy, double-buffered a whole transition ahead (one mbarrier per buffer);
 // the chunk-start row EPP[A, 0] (every transition's token 0) is resident per CTA.
 constexpr int kF2MaxWarps = 7;
-constexpr int kF2Chunk = 8;  // transitions per dynamically claimed chunk
+constexpr int kF2Chunk = 32;  // transitions per dynamically claimed chunk (and statistics row)
 __device__ unsigned g_fact2_ctr[2];  // work counters (main pass, fixup pass)
 
 // After the call lane l holds the warp total of value index l / (32 / NV).
@@ -683,7 +683,6 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
   static_assert(NV <= 32 && VPL % 4 == 0 && KT <= KMAX, "layout");
   const int K = KT > 0 ? KT : K_rt;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_stat[kF2MaxWarps][kNumStat + kNumMax];
   __shared__ __align__(16) float s_e0[A];       // EPP[A, 0]: token 0 of every transition
   __shared__ float s_cf[kF2MaxWarps][32];       // per-lane coef (one-hot part of G)
   RowCtx cx;
@@ -950,54 +949,45 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
     }
     __syncwarp();
     if (own && !bad_tok) s_oh[tok] = 0.f;
+    // a chunk of kF2Chunk transitions is done: its statistics go to the chunk's own
+    // partial row (warp-reduced in a fixed order), so the pooled sums do not
+    // depend on which warp the dynamic schedule handed the chunk to
+    if (!cx.fixup && ((i + 1) % kF2Chunk == 0 || i + 1 == N)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
+        st_ent += __shfl_xor_sync(0xffffffffu, st_ent, o);
+        st_r += __shfl_xor_sync(0xffffffffu, st_r, o);
+        st_w += __shfl_xor_sync(0xffffffffu, st_w, o);
+        st_rmax = fmax(st_rmax, __shfl_xor_sync(0xffffffffu, st_rmax, o));
+        st_negw = fmax(st_negw, __shfl_xor_sync(0xffffffffu, st_negw, o));
+      }
+      st_out = __reduce_add_sync(0xffffffffu, st_out);
+      st_excl = __reduce_add_sync(0xffffffffu, st_excl);
+      st_bad = __reduce_add_sync(0xffffffffu, st_bad);
+      st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
+      if (lane == 0) {
+        const int64_t c = i / kF2Chunk;
+        double* st = stat_part + c * kNumStat;
+        st[kLossNum] = st_loss;
+        st[kEntSum] = st_ent;
+        st[kRatioSum] = st_r;
+        st[kWSum] = st_w;
+        st[kOutside] = st_out;
+        st[kExcluded] = st_excl;
+        st[kBadRows] = st_bad;
+        st[kBadTok] = st_badtok;
+        max_part[c * kNumMax + kRatioMax] = st_rmax;
+        max_part[c * kNumMax + kNegWMin] = st_negw;
+      }
+      st_loss = st_ent = st_r = st_w = 0.0;
+      st_rmax = st_negw = -CUDART_INF;
+      st_out = st_excl = st_bad = st_badtok = 0;
+    }
     cur = nxt;
     nxt = nn;
     i = i1;
     i1 = i2;
-  }
-  if (cx.fixup) return;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
-    st_ent += __shfl_xor_sync(0xffffffffu, st_ent, o);
-    st_r += __shfl_xor_sync(0xffffffffu, st_r, o);
-    st_w += __shfl_xor_sync(0xffffffffu, st_w, o);
-    st_rmax = fmax(st_rmax, __shfl_xor_sync(0xffffffffu, st_rmax, o));
-    st_negw = fmax(st_negw, __shfl_xor_sync(0xffffffffu, st_negw, o));
-  }
-  st_out = __reduce_add_sync(0xffffffffu, st_out);
-  st_excl = __reduce_add_sync(0xffffffffu, st_excl);
-  st_bad = __reduce_add_sync(0xffffffffu, st_bad);
-  st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
-  if (lane == 0) {
-    double* st = s_stat[warp];
-    st[kLossNum] = st_loss;
-    st[kEntSum] = st_ent;
-    st[kRatioSum] = st_r;
-    st[kWSum] = st_w;
-    st[kOutside] = st_out;
-    st[kExcluded] = st_excl;
-    st[kBadRows] = st_bad;
-    st[kBadTok] = st_badtok;
-    st[kNumStat + kRatioMax] = st_rmax;
-    st[kNumStat + kNegWMin] = st_negw;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // warps in fixed order: deterministic
-    double sum[kNumStat + kNumMax];
-#pragma unroll
-    for (int q = 0; q < kNumStat; ++q) sum[q] = 0.0;
-    sum[kNumStat + kRatioMax] = sum[kNumStat + kNegWMin] = -CUDART_INF;
-    for (int w = 0; w < nwarps; ++w) {
-#pragma unroll
-      for (int q = 0; q < kNumStat; ++q) sum[q] += s_stat[w][q];
-#pragma unroll
-      for (int q = kNumStat; q < kNumStat + kNumMax; ++q) sum[q] = fmax(sum[q], s_stat[w][q]);
-    }
-#pragma unroll
-    for (int q = 0; q < kNumStat; ++q) stat_part[(int64_t)blockIdx.x * kNumStat + q] = sum[q];
-    max_part[(int64_t)blockIdx.x * kNumMax + kRatioMax] = sum[kNumStat + kRatioMax];
-    max_part[(int64_t)blockIdx.x * kNumMax + kNegWMin] = sum[kNumStat + kNegWMin];
   }
 }
 
@@ -1309,6 +1299,15 @@ extern "C" int accel_sorted_rows(const int32_t* perm, const int32_t* frame_of,
   sorted_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(perm, frame_of, tokens, R, K, row_frame,
                                                           row_tok, pos);
   return post_launch("sorted_rows_kernel");
+}
+
+// Rows of stat_part / max_part the loss kernel for (N, K, A, scalar output)
+// writes: one per 32-transition chunk for the two-phase kernel (deterministic
+// under its dynamic schedule), one per CTA (accel_fact_grid) otherwise.
+extern "C" int64_t accel_fact_partials(int64_t N, int K, int A, int scalar_out) {
+  (void)scalar_out;
+  if (K <= 8 && (A == 128 || A == 256)) return std::max<int64_t>(1, ceil_div(N, kF2Chunk));
+  return accel_fact_grid(N);
 }
 
 extern "C" int accel_fact_grid(int64_t N) {

@@ -269,6 +269,11 @@ def fact_grid(N: int) -> int:
     return int(_lib.lib().accel_fact_grid(int(N)))
 
 
+def fact_partials(N: int, K: int, A: int, scalar_out: bool) -> int:
+    """Rows of the loss kernel's statistics partials (accel_fact_partials)."""
+    return int(_lib.lib().accel_fact_partials(int(N), int(K), int(A), int(bool(scalar_out))))
+
+
 def ep_plus(ep, pp, bias, K, out):
     A = ep.shape[1]
     _lib.call("accel_ep_plus", _p(ep), _p(pp), _p(bias), A, int(K), _p(out), _stream())

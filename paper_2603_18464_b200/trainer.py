@@ -767,7 +767,7 @@ class Trainer:
             ep = _mm(P["e_prev"], P["w_head"].t(), S.get("st.ep", (A + 1, A)))
             pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
             epp = ops.ep_plus(ep, pp, P["b_head"], K, S.get("st.epp", ((A + 1) * K, A)))
-            gf = ops.fact_grid(N)
+            gf = ops.fact_partials(N, K, A, self.recompute_dz)
             # recompute_dz: per-token scalars instead of dz rows, the grouped sums
             # recompute dz (saves the 4A bytes/token dz write+read, costs the
             # recompute; off by default: the loss kernel is issue-bound, so the

@@ -247,13 +247,18 @@ def test_all_excluded_batch_is_skipped():
 
 
 def test_train_step_is_bitwise_deterministic():
-    outs = []
+    """Parameters (reference test_trainer.py:572-583) and the records: the loss
+    kernel's statistics go to fixed per-chunk rows under its dynamic schedule."""
+    outs, recs = [], []
     for _ in range(2):
-        tr, trajs, *_ = _random_setup(seed=9)
+        tr, trajs, *_ = _random_setup(seed=9, n_traj=40, max_len=90)
+        rr = []
         for _ in range(2):
-            tr.train_step(tr.build_train_batch(trajs))
+            rr.append(tr.train_step(tr.build_train_batch(trajs)))
         outs.append(tr.params.p[tr.params.cur].cpu().numpy())
+        recs.append(rr)
     np.testing.assert_array_equal(outs[0], outs[1])
+    assert recs[0] == recs[1]
 
 
 def test_build_rejects_nonfinite_and_bad_domains():
