@@ -18,7 +18,12 @@
  *     non-zero status;
  *   - domain errors that depend on device data (e.g. a negative pooled
  *     variance) are reported through flag words in the output buffers that
- *     the caller reads at its next (already required) host sync.
+ *     the caller reads at its next (already required) host sync;
+ *   - two entry points keep small device-global scratch instead of a
+ *     caller workspace: accel_token_loss_fact(2)'s chunk counters (reset by a
+ *     memset on the call's stream) and accel_reduce_f64's level-1 partials
+ *     (> 8192 rows).  Calls of each on one device must therefore be ordered
+ *     (one stream, or events between streams), as the trainer issues them.
  */
 #ifndef ACCEL_H_
 #define ACCEL_H_
