@@ -152,6 +152,74 @@ class DeviceReplayBuffer:
             self._items.append(h)
             self._pushed += 1
 
+    def push_imagined(self, out: dict, task_ids=None, version: int = 0) -> int:
+        """Push a batch of imagined episodes straight from `Imaginer.imagine_device`
+        outputs (device tensors; rollout.py:345-362 builds the same records on the
+        host): episodes with status 0 (the reference keeps them) enter in order,
+        their spans filled by a handful of on-device row copies.  Returns the
+        number pushed."""
+        if self.kind != "imagined":
+            raise BufferKindError(f"buffer {self.kind!r} does not accept imagined episodes")
+        status = out["status"].cpu().numpy()
+        t_len = out["t_len"].cpu().numpy()
+        done = out["done"].cpu().numpy()
+        rew = out["rewards"].double().sum(dim=1).cpu().numpy()
+        H1 = out["observations"].shape[1]
+        H = H1 - 1
+        keep = [e for e in range(len(status)) if status[e] == 0]
+        src_f, dst_f, src_t, dst_t, dst_v, boot_dst, boot_src = [], [], [], [], [], [], []
+        fresh = set()
+        with self._lock:
+            for e in keep:
+                T = int(t_len[e])
+                if len(self._items) >= self.capacity:
+                    self._evict(self._items[0])
+                meta = type("M", (), {"tokens": np.zeros((T, self.K)), "done": bool(done[e]),
+                                      "source": "imagined", "rewards": np.array([rew[e]]),
+                                      "task_id": int(task_ids[e]) if task_ids is not None else 0,
+                                      "behavior_version": int(version)})
+                h = DeviceTrajectory(self, 0, 0, meta)
+                f0, ev_f = self._fring.alloc(T + 1, h)
+                t0, ev_t = self._tring.alloc(T, h)
+                for o in ev_f + ev_t:
+                    if o in fresh:
+                        raise DimensionError("the replay arena is smaller than one imagination "
+                                             "batch (raise max_transitions)")
+                    if o.alive:
+                        self._evict(o)
+                h.f0, h.t0 = f0, t0
+                fresh.add(h)
+                src_f.append(e * H1 + np.arange(T + 1))
+                dst_f.append(f0 + np.arange(T + 1))
+                src_t.append(e * H + np.arange(T))
+                dst_t.append(t0 + np.arange(T))
+                dst_v.append(f0 + np.arange(T))  # values of transitions sit on their frames
+                boot_dst.append(f0 + T)
+                boot_src.append(e)
+                self._items.append(h)
+                self._pushed += 1
+        if not keep:
+            return 0
+        dev = self.device
+        ix = lambda parts: torch.from_numpy(np.concatenate(parts).astype(np.int64)).to(dev)
+        sf, df, st, dt = ix(src_f), ix(dst_f), ix(src_t), ix(dst_t)
+        O, K, A = self.O, self.K, self.A
+        obs = out["observations"].reshape(-1, O).float()
+        self.frames.index_copy_(0, df, obs.index_select(0, sf))
+        self.steps.index_copy_(0, df, out["steps"].reshape(-1).index_select(0, sf).int())
+        vals = out["values"].reshape(-1).float()
+        if st.numel():
+            self.values.index_copy_(0, ix(dst_v), vals.index_select(0, st))
+        bd = torch.tensor(boot_dst, dtype=torch.int64, device=dev)
+        self.values.index_copy_(0, bd, out["bootstrap_value"].float().index_select(
+            0, torch.tensor(boot_src, dtype=torch.int64, device=dev)))
+        if st.numel():
+            self.rewards.index_copy_(0, dt, out["rewards"].reshape(-1).float().index_select(0, st))
+            self.tokens.index_copy_(0, dt, out["tokens"].reshape(-1, K).int().index_select(0, st))
+            self.mu.index_copy_(0, dt, out["behavior_logits"].reshape(-1, K * A).float()
+                                .index_select(0, st))
+        return len(keep)
+
     def _evict(self, h) -> None:
         h.alive = False
         self._items.remove(h)

@@ -73,3 +73,42 @@ def test_device_replay_matches_host_build():
         assert abs(rd[k] - rh[k]) <= 1e-12 * max(1.0, abs(rh[k])), k
     np.testing.assert_array_equal(tr_dev.params.p[tr_dev.params.cur].cpu().numpy(),
                                   tr_host.params.p[tr_host.params.cur].cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_push_imagined_equals_host_records():
+    """Imagination outputs pushed on the device == the same episodes pushed as
+    host Trajectory records (imagine_trajectories)."""
+    from paper_2603_18464_b200.imagine import Imaginer
+    from paper_2603_18464_b200.replay import DeviceReplayBuffer
+    from paper_2603_18464_b200.types import (ModelBundle, ObsModel, ObsModelConfig, PolicyConfig,
+                                             PolicyModel, RewardModel, ValueConfig, ValueHead)
+    from types import SimpleNamespace
+    rng = np.random.default_rng(2)
+    O, K, A = 51, 2, 7
+    pc = PolicyConfig(obs_dim=O, hidden_dim=16, chunk_len=K, n_actions=A)
+    b = ModelBundle(PolicyModel.init(rng, pc), ValueHead.init(rng, ValueConfig(16, 30, 8)),
+                    ObsModel.init(rng, ObsModelConfig(obs_dim=O, chunk_len=K, hidden_dim=24)),
+                    RewardModel.init(rng, O, hidden_dim=12))
+    n, H = 24, 6
+    starts = np.zeros((n, O))
+    for e in range(n):
+        for c in range(3):
+            starts[e, c * 16 + rng.integers(16)] = 1.0
+        starts[e, 48 + e % 3] = 1.0
+    im = Imaginer(b, grid=(4, 4))
+    u = rng.random((n, H + 1, K))
+    out = im.imagine_device(starts, np.arange(n) % 5, H, uniforms=u)
+    dev_buf = DeviceReplayBuffer("imagined", 64, O, K, A, max_transitions=64 * H)
+    host_buf = DeviceReplayBuffer("imagined", 64, O, K, A, max_transitions=64 * H)
+    pushed = dev_buf.push_imagined(out)
+    host = im.imagine_trajectories([SimpleNamespace(vec=starts[e], step=e % 5, task_id=0)
+                                    for e in range(n)], H, uniforms=u)
+    kept = [t for t in host if t is not None]
+    for t in kept:
+        host_buf.push(t)
+    assert pushed == len(kept) == len(dev_buf) == len(host_buf)
+    a, _, _ = dev_buf.gather(list(dev_buf._items))
+    c, _, _ = host_buf.gather(list(host_buf._items))
+    for k in a:
+        np.testing.assert_array_equal(a[k].cpu().numpy(), c[k].cpu().numpy(), err_msg=k)
