@@ -178,7 +178,14 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
         }
       }
     }
-    if (lane == 0) cp_async4(s_buf[warp][b][1] + nv, vc + nv);
+    // the value after the chunk; a successful trajectory's bootstrap value is 0
+    // (trainer.py:92-93), written here so the scan needs no last-step test
+    if (lane == 0) {
+      if (c.dn && c.e == c.T)
+        s_buf[warp][b][1][nv] = 0.f;
+      else
+        cp_async4(s_buf[warp][b][1] + nv, vc + nv);
+    }
   };
 
   Ck cur = first_chunk(sa);
@@ -196,9 +203,10 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     const int kd = (nv + 31) >> 5;  // steps per lane (warp-uniform)
     float* sr = s_buf[warp][b][0] + kd * lane;  // this lane's steps kd*l .. kd*l + kd - 1
     float* sv = s_buf[warp][b][1] + kd * lane;
-    const int nl = nv - kd * lane;                          // this lane's valid steps
-    const int kl = (int)(cur.T - 1 - cur.cb) - kd * lane;   // lane-relative last step
-    const bool dn = cur.dn;
+    const int nl = nv - kd * lane;  // this lane's valid steps
+    // A chunk never spans two trajectories and the carry into a trajectory's
+    // last chunk is 0, so the last step needs no special map: (d, decay)
+    // applied to A = 0 is d, as the reference's zero continuation gives.
     float dl[kItems];
     float vnext = sv[min(kd, max(nl, 0))];  // v after the lane's last valid step
     float B = 0.f, C = 1.f;  // the lane's composed map (right to left)
@@ -208,14 +216,12 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
         const float vi = sv[k];
         const float ri = sr[k];
         const bool ok = k < nl;
-        const bool last = k == kl;
         // delta = r + gamma v' - v with gamma = g_hi + g_lo: fma(g_hi, v', -v) is
         // exact before its one rounding, so the error is relative to the TD
-        // error, not to |v| (done: the bootstrap value is 0, trainer.py:92-93)
-        const float vx = (last && dn) ? 0.f : vnext;
-        const float d = fmaf(g_lo, vx, fmaf(g_hi, vx, -vi)) + ri;
+        // error, not to |v|
+        const float d = fmaf(g_lo, vnext, fmaf(g_hi, vnext, -vi)) + ri;
         dl[k] = ok ? d : 0.f;
-        const float ck = ok ? (last ? 0.f : decay) : 1.f;
+        const float ck = ok ? decay : 1.f;
         vnext = vi;
         B = fmaf(ck, B, dl[k]);
         C *= ck;
@@ -239,7 +245,7 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
 #pragma unroll
     for (int k = kItems - 1; k >= 0; --k) {
       if (k < kd && k < nl) {
-        A = fmaf(k == kl ? 0.f : decay, A, dl[k]);
+        A = fmaf(decay, A, dl[k]);
         const float rt = A + sv[k];
         sr[k] = A;
         sv[k] = rt;
