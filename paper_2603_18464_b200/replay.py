@@ -16,8 +16,10 @@ per-batch host-to-device copy sits on the build path.  The reference
 
 from __future__ import annotations
 
+import bisect
 import threading
 from dataclasses import dataclass
+from types import SimpleNamespace
 
 import numpy as np
 import torch
@@ -45,29 +47,52 @@ class SpanRing:
 
     alloc(n) returns the start of n contiguous slots; a span never wraps (it
     restarts at 0 when the tail is too short) and every live span it overlaps
-    is reported for eviction.  With an arena of at least capacity x (longest
-    trajectory + 1) slots no span is ever evicted this way, and the buffer's
-    contents (hence its sampling) follow the reference's FIFO exactly."""
+    is reported for eviction (oldest first).  With an arena of at least
+    capacity x (longest trajectory + 1) slots no span is ever evicted this way,
+    and the buffer's contents (hence its sampling) follow the reference's FIFO
+    exactly.  Live spans never overlap, so they are kept sorted by start and an
+    alloc / release costs a bisection, not a scan of every live span (a push of
+    a 4096-episode imagination batch into an 8192-episode buffer was quadratic)."""
 
     def __init__(self, size: int) -> None:
         self.size = int(size)
         self.head = 0
-        self.live: list = []  # (start, length, owner) oldest first
+        self._starts: list = []   # sorted starts of the live spans
+        self._spans: dict = {}    # start -> (length, owner, allocation seq)
+        self._where: dict = {}    # id(owner) -> start
+        self._seq = 0
 
     def alloc(self, n: int, owner) -> tuple:
         if n > self.size:
             raise DimensionError(f"span of {n} exceeds the arena ({self.size})")
         start = self.head if self.head + n <= self.size else 0
         end = start + n
-        evicted = [o for s, ln, o in self.live if s < end and start < s + ln]
-        if evicted:
-            self.live = [x for x in self.live if not (x[0] < end and start < x[0] + x[1])]
-        self.live.append((start, n, owner))
         self.head = end
-        return start, evicted
+        if n == 0:  # occupies nothing, overlaps nothing
+            return start, []
+        st = self._starts
+        i = bisect.bisect_left(st, start)
+        if i > 0 and st[i - 1] + self._spans[st[i - 1]][0] > start:
+            i -= 1
+        j = i
+        while j < len(st) and st[j] < end:
+            j += 1
+        gone = [self._spans.pop(x) for x in st[i:j]]
+        del st[i:j]
+        for _, o, _ in gone:
+            del self._where[id(o)]
+        st.insert(i, start)
+        self._spans[start] = (n, owner, self._seq)
+        self._where[id(owner)] = start
+        self._seq += 1
+        return start, [o for _, o, _ in sorted(gone, key=lambda g: g[2])]
 
     def release(self, owner) -> None:
-        self.live = [x for x in self.live if x[2] is not owner]
+        x = self._where.pop(id(owner), None)
+        if x is None:
+            return
+        del self._spans[x]
+        del self._starts[bisect.bisect_left(self._starts, x)]
 
 
 class DeviceTrajectory:
@@ -174,10 +199,10 @@ class DeviceReplayBuffer:
                 T = int(t_len[e])
                 if len(self._items) >= self.capacity:
                     self._evict(self._items[0])
-                meta = type("M", (), {"tokens": np.zeros((T, self.K)), "done": bool(done[e]),
-                                      "source": "imagined", "rewards": np.array([rew[e]]),
-                                      "task_id": int(task_ids[e]) if task_ids is not None else 0,
-                                      "behavior_version": int(version)})
+                meta = SimpleNamespace(tokens=np.empty((T, 0)), done=bool(done[e]),
+                                       source="imagined", rewards=(rew[e],),
+                                       task_id=int(task_ids[e]) if task_ids is not None else 0,
+                                       behavior_version=int(version))
                 h = DeviceTrajectory(self, 0, 0, meta)
                 f0, ev_f = self._fring.alloc(T + 1, h)
                 t0, ev_t = self._tring.alloc(T, h)

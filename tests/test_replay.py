@@ -29,6 +29,42 @@ def test_span_ring_allocates_wraps_and_evicts_overlaps():
         r.alloc(11, "f")
 
 
+def test_span_ring_matches_linear_scan_allocator():
+    """The bisection ring reports exactly the overlaps (oldest first) that a scan
+    of every live span does, under random allocs and releases with wraps."""
+    class ScanRing:
+        def __init__(self, size):
+            self.size, self.head, self.live = size, 0, []
+
+        def alloc(self, n, owner):
+            start = self.head if self.head + n <= self.size else 0
+            end = start + n
+            ev = [o for s, ln, o in self.live if s < end and start < s + ln]
+            self.live = [x for x in self.live if not (x[0] < end and start < x[0] + x[1])]
+            self.live.append((start, n, owner))
+            self.head = end
+            return start, ev
+
+        def release(self, owner):
+            self.live = [x for x in self.live if x[2] is not owner]
+
+    rng = np.random.default_rng(5)
+    for size in (17, 64, 500):
+        a, b = SpanRing(size), ScanRing(size)
+        owners = []
+        for step in range(3000):
+            if owners and rng.random() < 0.3:
+                o = owners.pop(int(rng.integers(len(owners))))
+                a.release(o)
+                b.release(o)
+                continue
+            o = object()
+            n = int(rng.integers(1, size // 3 + 2))
+            ra, rb = a.alloc(n, o), b.alloc(n, o)
+            assert ra[0] == rb[0] and ra[1] == rb[1], (size, step)
+            owners = [x for x in owners if x not in ra[1]] + [o]
+
+
 def _trajs(rng, n, K, A, O):
     from paper_2603_18464_b200.workload import synthetic_trajectories
     lens = rng.integers(1, 30, size=n)
