@@ -95,6 +95,13 @@ class SpanRing:
         del self._starts[bisect.bisect_left(self._starts, x)]
 
 
+def _spans(starts: np.ndarray, lens: np.ndarray) -> np.ndarray:
+    """Concatenation of arange(s, s + n) over (starts, lens), vectorized."""
+    total = int(lens.sum())
+    base = np.repeat(starts - (np.cumsum(lens) - lens), lens)
+    return base + np.arange(total, dtype=np.int64)
+
+
 class DeviceTrajectory:
     """Handle of a trajectory resident in a DeviceReplayBuffer arena (duck-types
     the reference Trajectory's metadata: t_len, done, source, task_id,
@@ -191,8 +198,8 @@ class DeviceReplayBuffer:
         rew = out["rewards"].double().sum(dim=1).cpu().numpy()
         H1 = out["observations"].shape[1]
         H = H1 - 1
-        keep = [e for e in range(len(status)) if status[e] == 0]
-        src_f, dst_f, src_t, dst_t, dst_v, boot_dst, boot_src = [], [], [], [], [], [], []
+        keep = np.flatnonzero(status == 0).tolist()
+        f0s, t0s = [], []
         fresh = set()
         with self._lock:
             for e in keep:
@@ -214,20 +221,21 @@ class DeviceReplayBuffer:
                         self._evict(o)
                 h.f0, h.t0 = f0, t0
                 fresh.add(h)
-                src_f.append(e * H1 + np.arange(T + 1))
-                dst_f.append(f0 + np.arange(T + 1))
-                src_t.append(e * H + np.arange(T))
-                dst_t.append(t0 + np.arange(T))
-                dst_v.append(f0 + np.arange(T))  # values of transitions sit on their frames
-                boot_dst.append(f0 + T)
-                boot_src.append(e)
+                f0s.append(f0)
+                t0s.append(t0)
                 self._items.append(h)
                 self._pushed += 1
         if not keep:
             return 0
         dev = self.device
-        ix = lambda parts: torch.from_numpy(np.concatenate(parts).astype(np.int64)).to(dev)
-        sf, df, st, dt = ix(src_f), ix(dst_f), ix(src_t), ix(dst_t)
+        ke = np.asarray(keep, dtype=np.int64)
+        T = t_len[ke].astype(np.int64)
+        f0a, t0a = np.asarray(f0s, dtype=np.int64), np.asarray(t0s, dtype=np.int64)
+        ix = lambda a: torch.from_numpy(a).to(dev)
+        sf, df = ix(_spans(ke * H1, T + 1)), ix(_spans(f0a, T + 1))
+        st, dt = ix(_spans(ke * H, T)), ix(_spans(t0a, T))
+        dst_v = _spans(f0a, T)  # values of transitions sit on their frames
+        boot_dst, boot_src = (f0a + T).tolist(), keep
         O, K, A = self.O, self.K, self.A
         obs = out["observations"].reshape(-1, O).float()
         self.frames.index_copy_(0, df, obs.index_select(0, sf))
