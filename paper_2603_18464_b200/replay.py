@@ -87,6 +87,54 @@ class SpanRing:
         self._seq += 1
         return start, [o for _, o, _ in sorted(gone, key=lambda g: g[2])]
 
+    def alloc_many(self, ns, owners) -> tuple:
+        """alloc(n, owner) for every pair in order, as one operation: the starts,
+        and every previously live span any of them overlaps (oldest first).  The
+        new spans must not overlap each other (DimensionError: the arena is
+        smaller than the batch)."""
+        starts, runs = [], []
+        head, size = self.head, self.size
+        for n in ns:
+            if n > size:
+                raise DimensionError(f"span of {n} exceeds the arena ({size})")
+            s = head if head + n <= size else 0
+            if runs and s == runs[-1][1]:
+                runs[-1][1] = s + n
+            else:
+                runs.append([s, s + n])
+            starts.append(s)
+            head = s + n
+        for a in range(len(runs)):
+            for b in range(a):
+                if runs[a][0] < runs[b][1] and runs[b][0] < runs[a][1] \
+                        and runs[a][0] < runs[a][1] and runs[b][0] < runs[b][1]:
+                    raise DimensionError("the replay arena is smaller than one batch")
+        st, gone = self._starts, []
+        for r0, r1 in runs:
+            if r0 == r1:
+                continue
+            i = bisect.bisect_left(st, r0)
+            if i > 0 and st[i - 1] + self._spans[st[i - 1]][0] > r0:
+                i -= 1
+            j = i
+            while j < len(st) and st[j] < r1:
+                j += 1
+            gone += [self._spans.pop(x) for x in st[i:j]]
+            del st[i:j]
+        for _, o, _ in gone:
+            del self._where[id(o)]
+        seq = self._seq
+        for s, n, o in zip(starts, ns, owners):
+            if n:
+                st.append(s)
+                self._spans[s] = (n, o, seq)
+                self._where[id(o)] = s
+                seq += 1
+        st.sort()
+        self._seq = seq
+        self.head = head
+        return starts, [o for _, o, _ in sorted(gone, key=lambda g: g[2])]
+
     def release(self, owner) -> None:
         x = self._where.pop(id(owner), None)
         if x is None:
@@ -199,32 +247,38 @@ class DeviceReplayBuffer:
         H1 = out["observations"].shape[1]
         H = H1 - 1
         keep = np.flatnonzero(status == 0).tolist()
-        f0s, t0s = [], []
-        fresh = set()
+        n_keep = len(keep)
         with self._lock:
-            for e in keep:
-                T = int(t_len[e])
-                if len(self._items) >= self.capacity:
-                    self._evict(self._items[0])
+            # the reference's bounded FIFO: the oldest leave first; episodes of this
+            # batch beyond the capacity would leave at once, so they never enter
+            self._pushed += n_keep
+            if n_keep > self.capacity:
+                self._evicted += n_keep - self.capacity
+                keep = keep[n_keep - self.capacity:]
+            n_over = len(self._items) + len(keep) - self.capacity
+            if n_over > 0:
+                for h in self._items[:n_over]:
+                    h.alive = False
+                    self._fring.release(h)
+                    self._tring.release(h)
+                del self._items[:n_over]
+                self._evicted += n_over
+            T_l = t_len[keep].astype(np.int64).tolist()
+            hs = []
+            for e, T in zip(keep, T_l):
                 meta = SimpleNamespace(tokens=np.empty((T, 0)), done=bool(done[e]),
                                        source="imagined", rewards=(rew[e],),
                                        task_id=int(task_ids[e]) if task_ids is not None else 0,
                                        behavior_version=int(version))
-                h = DeviceTrajectory(self, 0, 0, meta)
-                f0, ev_f = self._fring.alloc(T + 1, h)
-                t0, ev_t = self._tring.alloc(T, h)
-                for o in ev_f + ev_t:
-                    if o in fresh:
-                        raise DimensionError("the replay arena is smaller than one imagination "
-                                             "batch (raise max_transitions)")
-                    if o.alive:
-                        self._evict(o)
+                hs.append(DeviceTrajectory(self, 0, 0, meta))
+            f0s, ev_f = self._fring.alloc_many([T + 1 for T in T_l], hs)
+            t0s, ev_t = self._tring.alloc_many(T_l, hs)
+            for o in ev_f + ev_t:
+                if o.alive:
+                    self._evict(o)
+            for h, f0, t0 in zip(hs, f0s, t0s):
                 h.f0, h.t0 = f0, t0
-                fresh.add(h)
-                f0s.append(f0)
-                t0s.append(t0)
-                self._items.append(h)
-                self._pushed += 1
+            self._items.extend(hs)
         if not keep:
             return 0
         dev = self.device
@@ -251,7 +305,7 @@ class DeviceReplayBuffer:
             self.tokens.index_copy_(0, dt, out["tokens"].reshape(-1, K).int().index_select(0, st))
             self.mu.index_copy_(0, dt, out["behavior_logits"].reshape(-1, K * A).float()
                                 .index_select(0, st))
-        return len(keep)
+        return n_keep
 
     def _evict(self, h) -> None:
         h.alive = False

@@ -39,6 +39,9 @@ def test_span_ring_matches_linear_scan_allocator():
         def alloc(self, n, owner):
             start = self.head if self.head + n <= self.size else 0
             end = start + n
+            if n == 0:  # an empty span occupies nothing
+                self.head = end
+                return start, []
             ev = [o for s, ln, o in self.live if s < end and start < s + ln]
             self.live = [x for x in self.live if not (x[0] < end and start < x[0] + x[1])]
             self.live.append((start, n, owner))
@@ -48,8 +51,8 @@ def test_span_ring_matches_linear_scan_allocator():
         def release(self, owner):
             self.live = [x for x in self.live if x[2] is not owner]
 
-    rng = np.random.default_rng(5)
-    for size in (17, 64, 500):
+    def run(size, seed):
+        rng = np.random.default_rng(seed)
         a, b = SpanRing(size), ScanRing(size)
         owners = []
         for step in range(3000):
@@ -58,11 +61,31 @@ def test_span_ring_matches_linear_scan_allocator():
                 a.release(o)
                 b.release(o)
                 continue
+            if rng.random() < 0.2:  # a batch: alloc_many == the same allocs in order
+                k = int(rng.integers(1, 6))
+                ns = [int(rng.integers(0, size // 4 + 2)) for _ in range(k)]
+                os_ = [object() for _ in range(k)]
+                seq = [b.alloc(n, o) for n, o in zip(ns, os_)]
+                ev_b = [x for _, ev in seq for x in ev]
+                if any(x in os_ for x in ev_b):  # the batch overlaps itself
+                    with pytest.raises(Exception):
+                        a.alloc_many(ns, os_)
+                    return
+                starts, ev_a = a.alloc_many(ns, os_)
+                assert starts == [st for st, _ in seq], (size, step)
+                assert set(map(id, ev_a)) == set(map(id, ev_b)), (size, step)
+                owners = [x for x in owners if x not in ev_a]
+                owners += [o for n, o in zip(ns, os_) if n]
+                continue
             o = object()
             n = int(rng.integers(1, size // 3 + 2))
             ra, rb = a.alloc(n, o), b.alloc(n, o)
             assert ra[0] == rb[0] and ra[1] == rb[1], (size, step)
             owners = [x for x in owners if x not in ra[1]] + [o]
+
+    for size in (17, 64, 500):
+        for seed in range(4):
+            run(size, seed)
 
 
 def _trajs(rng, n, K, A, O):
