@@ -135,6 +135,17 @@ class SpanRing:
         self.head = head
         return starts, [o for _, o, _ in sorted(gone, key=lambda g: g[2])]
 
+    def release_many(self, owners) -> None:
+        """release(o) for every o, with one pass over the live spans."""
+        gone = set()
+        for o in owners:
+            x = self._where.pop(id(o), None)
+            if x is not None:
+                del self._spans[x]
+                gone.add(x)
+        if gone:
+            self._starts = [x for x in self._starts if x not in gone]
+
     def release(self, owner) -> None:
         x = self._where.pop(id(owner), None)
         if x is None:
@@ -257,10 +268,11 @@ class DeviceReplayBuffer:
                 keep = keep[n_keep - self.capacity:]
             n_over = len(self._items) + len(keep) - self.capacity
             if n_over > 0:
-                for h in self._items[:n_over]:
+                old = self._items[:n_over]
+                for h in old:
                     h.alive = False
-                    self._fring.release(h)
-                    self._tring.release(h)
+                self._fring.release_many(old)
+                self._tring.release_many(old)
                 del self._items[:n_over]
                 self._evicted += n_over
             T_l = t_len[keep].astype(np.int64).tolist()

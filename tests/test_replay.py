@@ -61,6 +61,13 @@ def test_span_ring_matches_linear_scan_allocator():
                 a.release(o)
                 b.release(o)
                 continue
+            if len(owners) > 2 and rng.random() < 0.05:  # release_many == releases in order
+                k = int(rng.integers(1, len(owners)))
+                gone, owners = owners[:k], owners[k:]
+                a.release_many(gone)
+                for o in gone:
+                    b.release(o)
+                continue
             if rng.random() < 0.2:  # a batch: alloc_many == the same allocs in order
                 k = int(rng.integers(1, 6))
                 ns = [int(rng.integers(0, size // 4 + 2)) for _ in range(k)]
