@@ -19,7 +19,6 @@ from __future__ import annotations
 import bisect
 import threading
 from dataclasses import dataclass
-from types import SimpleNamespace
 
 import numpy as np
 import torch
@@ -180,6 +179,17 @@ class DeviceTrajectory:
         self.episode_return = float(np.sum(traj.rewards))
         self.alive = True
 
+    @classmethod
+    def imagined(cls, buffer, t_len: int, done: bool, task_id: int, version: int,
+                 episode_return: float):
+        """Handle of an imagined episode from its scalars (push_imagined's batch path)."""
+        h = cls.__new__(cls)
+        h.buffer, h.f0, h.t0 = buffer, 0, 0
+        h.t_len, h.done, h.source = t_len, done, "imagined"
+        h.task_id, h.behavior_version = task_id, version
+        h.episode_return, h.alive = episode_return, True
+        return h
+
 
 class DeviceReplayBuffer:
     """Bounded FIFO of trajectories resident in HBM, uniform sampling."""
@@ -276,13 +286,12 @@ class DeviceReplayBuffer:
                 del self._items[:n_over]
                 self._evicted += n_over
             T_l = t_len[keep].astype(np.int64).tolist()
-            hs = []
-            for e, T in zip(keep, T_l):
-                meta = SimpleNamespace(tokens=np.empty((T, 0)), done=bool(done[e]),
-                                       source="imagined", rewards=(rew[e],),
-                                       task_id=int(task_ids[e]) if task_ids is not None else 0,
-                                       behavior_version=int(version))
-                hs.append(DeviceTrajectory(self, 0, 0, meta))
+            tid = (np.asarray(task_ids)[keep].astype(np.int64).tolist() if task_ids is not None
+                   else [0] * len(keep))
+            mk, v = DeviceTrajectory.imagined, int(version)
+            # the episode return is the sum of one float64 (rollout.py:345-362 stores it)
+            hs = [mk(self, T, d, t, v, r) for T, d, t, r in
+                  zip(T_l, done[keep].astype(bool).tolist(), tid, rew[keep].tolist())]
             f0s, ev_f = self._fring.alloc_many([T + 1 for T in T_l], hs)
             t0s, ev_t = self._tring.alloc_many(T_l, hs)
             for o in ev_f + ev_t:
