@@ -91,18 +91,28 @@ class SpanRing:
         and every previously live span any of them overlaps (oldest first).  The
         new spans must not overlap each other (DimensionError: the arena is
         smaller than the batch)."""
-        starts, runs = [], []
-        head, size = self.head, self.size
-        for n in ns:
-            if n > size:
-                raise DimensionError(f"span of {n} exceeds the arena ({size})")
-            s = head if head + n <= size else 0
-            if runs and s == runs[-1][1]:
-                runs[-1][1] = s + n
+        size = self.size
+        ns_a = np.asarray(ns, dtype=np.int64).reshape(-1)
+        k = len(ns_a)
+        if k and int(ns_a.max()) > size:
+            raise DimensionError(f"span of {int(ns_a.max())} exceeds the arena ({size})")
+        starts_a = np.empty(k, dtype=np.int64)
+        runs, head, i = [], self.head, 0
+        while i < k:  # one pass per wrap: every span that fits from head on
+            ends = head + np.cumsum(ns_a[i:])
+            over = np.flatnonzero(ends > size)
+            m = int(over[0]) if len(over) else k - i
+            if m == 0:  # span i does not fit in the tail: it restarts at 0
+                head = 0
+                continue
+            starts_a[i:i + m] = ends[:m] - ns_a[i:i + m]
+            if runs and runs[-1][1] == head:
+                runs[-1][1] = int(ends[m - 1])
             else:
-                runs.append([s, s + n])
-            starts.append(s)
-            head = s + n
+                runs.append([head, int(ends[m - 1])])
+            head = int(ends[m - 1])
+            i += m
+        starts = starts_a.tolist()
         for a in range(len(runs)):
             for b in range(a):
                 if runs[a][0] < runs[b][1] and runs[b][0] < runs[a][1] \
@@ -122,15 +132,15 @@ class SpanRing:
             del st[i:j]
         for _, o, _ in gone:
             del self._where[id(o)]
+        nz = np.flatnonzero(ns_a).tolist()
+        s_nz = [starts[q] for q in nz]
+        o_nz = [owners[q] for q in nz]
         seq = self._seq
-        for s, n, o in zip(starts, ns, owners):
-            if n:
-                st.append(s)
-                self._spans[s] = (n, o, seq)
-                self._where[id(o)] = s
-                seq += 1
+        self._spans.update(zip(s_nz, zip(ns_a[nz].tolist(), o_nz, range(seq, seq + len(nz)))))
+        self._where.update(zip(map(id, o_nz), s_nz))
+        st.extend(s_nz)
         st.sort()
-        self._seq = seq
+        self._seq = seq + len(nz)
         self.head = head
         return starts, [o for _, o, _ in sorted(gone, key=lambda g: g[2])]
 
