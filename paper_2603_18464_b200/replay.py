@@ -385,9 +385,11 @@ class DeviceReplayBuffer:
         off_d = torch.from_numpy(off).to(dev)
         # frame rows: f0[s] + j for j in [0, T_s]; transition rows: t0[s] + j, j < T_s
         fcount = lens_d + 1
-        fstart = torch.repeat_interleave(f0 - (off_d[:-1] + torch.arange(n, device=dev)), fcount)
+        # output sizes known on the host: no device-to-host sync inside the gathers
+        fstart = torch.repeat_interleave(f0 - (off_d[:-1] + torch.arange(n, device=dev)), fcount,
+                                         output_size=N + n)
         fidx = fstart + torch.arange(N + n, device=dev)
-        tstart = torch.repeat_interleave(t0 - off_d[:-1], lens_d)
+        tstart = torch.repeat_interleave(t0 - off_d[:-1], lens_d, output_size=N)
         tidx = tstart + torch.arange(N, device=dev)
         frames = ops.alloc_pitched(N + n, self.O, dev)
         full = self.frames.as_strided((self.frames.shape[0], self.frames.stride(0)),
