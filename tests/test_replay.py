@@ -178,3 +178,49 @@ def test_push_imagined_equals_host_records():
     c, _, _ = host_buf.gather(list(host_buf._items))
     for k in a:
         np.testing.assert_array_equal(a[k].cpu().numpy(), c[k].cpu().numpy(), err_msg=k)
+
+
+@pytest.mark.gpu
+def test_push_imagined_fifo_overflow_equals_host_pushes():
+    """Batches larger than the free capacity (and one larger than the capacity
+    itself) leave the buffer, its counters and its arena contents as the
+    reference's bounded FIFO of one-by-one pushes does."""
+    from paper_2603_18464_b200.imagine import Imaginer
+    from paper_2603_18464_b200.replay import DeviceReplayBuffer
+    from paper_2603_18464_b200.types import (ModelBundle, ObsModel, ObsModelConfig, PolicyConfig,
+                                             PolicyModel, RewardModel, ValueConfig, ValueHead)
+    from types import SimpleNamespace
+    rng = np.random.default_rng(4)
+    O, K, A = 51, 2, 7
+    pc = PolicyConfig(obs_dim=O, hidden_dim=16, chunk_len=K, n_actions=A)
+    b = ModelBundle(PolicyModel.init(rng, pc), ValueHead.init(rng, ValueConfig(16, 30, 8)),
+                    ObsModel.init(rng, ObsModelConfig(obs_dim=O, chunk_len=K, hidden_dim=24)),
+                    RewardModel.init(rng, O, hidden_dim=12))
+    im = Imaginer(b, grid=(4, 4))
+    H, cap = 5, 10
+    dev_buf = DeviceReplayBuffer("imagined", cap, O, K, A, max_transitions=cap * H)
+    host_buf = DeviceReplayBuffer("imagined", cap, O, K, A, max_transitions=cap * H)
+    for n in (6, 7, 13, 3):  # the third batch alone exceeds the capacity
+        starts = np.zeros((n, O))
+        for e in range(n):
+            for c in range(3):
+                starts[e, c * 16 + rng.integers(16)] = 1.0
+            starts[e, 48 + e % 3] = 1.0
+        u = rng.random((n, H + 1, K))
+        out = im.imagine_device(starts, np.arange(n) % 5, H, uniforms=u)
+        dev_buf.push_imagined(out)
+        host = im.imagine_trajectories([SimpleNamespace(vec=starts[e], step=e % 5, task_id=0)
+                                        for e in range(n)], H, uniforms=u)
+        for t in host:
+            if t is not None:
+                host_buf.push(t)
+        assert dev_buf.stats() == host_buf.stats()
+        a, _, _ = dev_buf.gather(list(dev_buf._items))
+        c, _, _ = host_buf.gather(list(host_buf._items))
+        for k in a:
+            np.testing.assert_array_equal(a[k].cpu().numpy(), c[k].cpu().numpy(), err_msg=k)
+        np.testing.assert_allclose([h.episode_return for h in dev_buf._items],
+                                   [h.episode_return for h in host_buf._items], rtol=1e-12,
+                                   atol=1e-12)
+        assert [(h.t_len, h.done) for h in dev_buf._items] == \
+            [(h.t_len, h.done) for h in host_buf._items]
