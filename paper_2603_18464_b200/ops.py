@@ -591,17 +591,6 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
               x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
     reduce_segments([(partial, out, 2 * kslices, n * k, n * k)])
     return out
-    if partial is None:
-        partial = torch.empty(kslices, n, k, dtype=F32, device=dy.device)
-    _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
-              x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
-    reduce_segments([(partial, out, kslices, n * k, n * k)])
-    return out
-    partial = torch.empty(kslices, n, k, dtype=F32, device=dy.device) if partial is None else partial
-    _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
-              x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
-    reduce_segments([(partial, out, kslices, n * k, n * k)])
-    return out
 
 
 # ---------------------------------------------------------------------------

@@ -86,11 +86,12 @@ class SpanRing:
         self._seq += 1
         return start, [o for _, o, _ in sorted(gone, key=lambda g: g[2])]
 
-    def alloc_many(self, ns, owners) -> tuple:
-        """alloc(n, owner) for every pair in order, as one operation: the starts,
-        and every previously live span any of them overlaps (oldest first).  The
-        new spans must not overlap each other (DimensionError: the arena is
-        smaller than the batch)."""
+    def plan(self, ns) -> tuple:
+        """Placement of spans of lengths ns from the current head, without
+        changing the ring: (starts, runs, new head).  Raises DimensionError when
+        a span exceeds the arena or the new spans would overlap each other (the
+        arena is smaller than the batch), so callers can check a batch fits
+        before mutating anything."""
         size = self.size
         ns_a = np.asarray(ns, dtype=np.int64).reshape(-1)
         k = len(ns_a)
@@ -118,6 +119,15 @@ class SpanRing:
                 if runs[a][0] < runs[b][1] and runs[b][0] < runs[a][1] \
                         and runs[a][0] < runs[a][1] and runs[b][0] < runs[b][1]:
                     raise DimensionError("the replay arena is smaller than one batch")
+        return starts, runs, head
+
+    def alloc_many(self, ns, owners) -> tuple:
+        """alloc(n, owner) for every pair in order, as one operation: the starts,
+        and every previously live span any of them overlaps (oldest first).  The
+        new spans must not overlap each other (DimensionError: the arena is
+        smaller than the batch; the ring is then unchanged)."""
+        starts, runs, head = self.plan(ns)
+        ns_a = np.asarray(ns, dtype=np.int64).reshape(-1)
         st, gone = self._starts, []
         for r0, r1 in runs:
             if r0 == r1:
@@ -208,6 +218,12 @@ class DeviceReplayBuffer:
                  max_transitions: int, device=None) -> None:
         if kind not in _ACCEPTED_SOURCE:
             raise BufferKindError(f"unknown buffer kind {kind!r}")
+        if kind == "world_model":
+            # the world-model sub-steps read observations / tokens of the sampled
+            # trajectories on the host (world_model.obs_model_data): that buffer
+            # stays a host ReplayBuffer
+            raise BufferKindError("the world-model buffer must be a host ReplayBuffer "
+                                  "(its sub-steps read trajectory fields on the host)")
         if capacity < 1:
             raise ValueError(f"capacity must be >= 1, got {capacity}")
         self.kind, self.capacity = kind, int(capacity)
@@ -226,6 +242,7 @@ class DeviceReplayBuffer:
         self._fring, self._tring = SpanRing(cap_f), SpanRing(cap_t)
         self._items: list = []
         self._lock = threading.Lock()
+        self._ready = None  # event after the last queued arena write
         self._pushed = self._sampled = self._evicted = 0
 
     # -- reference API ---------------------------------------------------------------
@@ -240,6 +257,8 @@ class DeviceReplayBuffer:
         if obs.shape != (T + 1, self.O) or np.asarray(traj.behavior_logits).shape != (T, self.K,
                                                                                         self.A):
             raise DimensionError("trajectory shapes do not match the buffer")
+        if T + 1 > self._fring.size or T > self._tring.size:
+            raise DimensionError(f"a trajectory of {T} steps exceeds the replay arena")
         with self._lock:
             if len(self._items) >= self.capacity:
                 self._evict(self._items[0])
@@ -260,6 +279,8 @@ class DeviceReplayBuffer:
             self.tokens[t0:t0 + T].copy_(t(traj.tokens, torch.int32))
             self.mu[t0:t0 + T].copy_(t(np.asarray(traj.behavior_logits).reshape(T, -1),
                                        torch.float32))
+            self._ready = torch.cuda.Event()
+            self._ready.record()
             self._items.append(h)
             self._pushed += 1
 
@@ -277,15 +298,19 @@ class DeviceReplayBuffer:
         rew = out["rewards"].double().sum(dim=1).cpu().numpy()
         H1 = out["observations"].shape[1]
         H = H1 - 1
-        keep = np.flatnonzero(status == 0).tolist()
-        n_keep = len(keep)
+        keep_all = np.flatnonzero(status == 0).tolist()
+        n_keep = len(keep_all)
+        # the reference's bounded FIFO: the oldest leave first; episodes of this
+        # batch beyond the capacity would leave at once, so they never enter
+        keep = keep_all[n_keep - self.capacity:] if n_keep > self.capacity else keep_all
+        T_l = t_len[keep].astype(np.int64).tolist()
         with self._lock:
-            # the reference's bounded FIFO: the oldest leave first; episodes of this
-            # batch beyond the capacity would leave at once, so they never enter
+            # placement first: a batch the arena cannot hold raises here, before
+            # any counter, eviction or ring state changes
+            self._fring.plan([T + 1 for T in T_l])
+            self._tring.plan(T_l)
             self._pushed += n_keep
-            if n_keep > self.capacity:
-                self._evicted += n_keep - self.capacity
-                keep = keep[n_keep - self.capacity:]
+            self._evicted += n_keep - len(keep)
             n_over = len(self._items) + len(keep) - self.capacity
             if n_over > 0:
                 old = self._items[:n_over]
@@ -295,7 +320,6 @@ class DeviceReplayBuffer:
                 self._tring.release_many(old)
                 del self._items[:n_over]
                 self._evicted += n_over
-            T_l = t_len[keep].astype(np.int64).tolist()
             tid = (np.asarray(task_ids)[keep].astype(np.int64).tolist() if task_ids is not None
                    else [0] * len(keep))
             mk, v = DeviceTrajectory.imagined, int(version)
@@ -309,9 +333,17 @@ class DeviceReplayBuffer:
                     self._evict(o)
             for h, f0, t0 in zip(hs, f0s, t0s):
                 h.f0, h.t0 = f0, t0
+            if keep:
+                # the arena rows are queued BEFORE the handles become visible to
+                # sample(); consumers on other streams wait on the event (gather)
+                self._copy_imagined(out, keep, t_len, f0s, t0s, H1)
+                self._ready = torch.cuda.Event()
+                self._ready.record()
             self._items.extend(hs)
-        if not keep:
-            return 0
+        return n_keep
+
+    def _copy_imagined(self, out, keep, t_len, f0s, t0s, H1) -> None:
+        H = H1 - 1
         dev = self.device
         ke = np.asarray(keep, dtype=np.int64)
         T = t_len[ke].astype(np.int64)
@@ -336,7 +368,6 @@ class DeviceReplayBuffer:
             self.tokens.index_copy_(0, dt, out["tokens"].reshape(-1, K).int().index_select(0, st))
             self.mu.index_copy_(0, dt, out["behavior_logits"].reshape(-1, K * A).float()
                                 .index_select(0, st))
-        return n_keep
 
     def _evict(self, h) -> None:
         h.alive = False
@@ -370,9 +401,19 @@ class DeviceReplayBuffer:
     # -- batch assembly on the device --------------------------------------------------
     def gather(self, handles) -> dict:
         """Packed CSR batch (the layout of trainer.upload) of the sampled handles,
-        by on-device row gathers of their arena spans."""
-        if any(not h.alive for h in handles):
-            raise DimensionError("a sampled trajectory was evicted before the batch was built")
+        by on-device row gathers of their arena spans; None (a dropped batch, as
+        the reference Prefetcher handles a None from its builder) when a sampled
+        trajectory was evicted before the batch was built.  The liveness check
+        and the gathers are queued under the buffer lock, so a concurrent push
+        cannot overwrite a span between the check and the reads."""
+        with self._lock:
+            if any(not h.alive for h in handles):
+                return None
+            if self._ready is not None:  # pushes queued on another stream
+                torch.cuda.current_stream().wait_event(self._ready)
+            return self._gather_locked(handles)
+
+    def _gather_locked(self, handles):
         dev = self.device
         lens = np.array([h.t_len for h in handles], dtype=np.int64)
         n = len(handles)

@@ -6,9 +6,10 @@ Same public surface as the reference module (`trainer.py:44-560`):
 `chunk_ratio`, `policy_surrogate`, `entropy_bonus`, `total_loss`,
 `behavior_log_probs` and `Trainer` with `build_train_batch`, `train_step`,
 `recompute_values`, `run`, `publish_*` and the same attributes, record keys,
-metric events and error types.  The math runs in libaccel.so (sm_100a); the
-GEMMs between the custom kernels are plain cuBLAS calls through torch with
-TF32 disabled.  There is no CPU path.
+metric events and error types.  The math runs in libaccel.so (sm_100a): the
+dense products on its tcgen05 3xTF32 GEMM kernels, the rest on its row /
+segment kernels; torch provides device memory, streams and three tiny
+(<= 257-row) products.  There is no CPU path.
 
 `Trainer.build_train_batch` accepts the reference's `list[Trajectory]` (any
 objects with those fields) or an already packed `workload.PackedBatch`, and
@@ -585,7 +586,10 @@ class Trainer:
             if self.cfg.revalue:
                 for t in trajs:
                     assert self.publish_version >= t.behavior_version
-            b, n_real, bver = buf.gather(trajs)
+            got = buf.gather(trajs)
+            if got is None:  # a sampled trajectory was evicted meanwhile: dropped batch
+                return None
+            b, n_real, bver = got
             return self.build_from_device(b, n_real=n_real, behavior_version=bver)
         else:
             for t in trajs:
@@ -768,10 +772,10 @@ class Trainer:
             pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
             epp = ops.ep_plus(ep, pp, P["b_head"], K, S.get("st.epp", ((A + 1) * K, A)))
             gf = ops.fact_partials(N, K, A, self.recompute_dz)
-            # recompute_dz: per-token scalars instead of dz rows, the grouped sums
-            # recompute dz (saves the 4A bytes/token dz write+read, costs the
-            # recompute; off by default: the loss kernel is issue-bound, so the
-            # dz stores are nearly free and the gathered recompute is slower)
+            # recompute_dz (default where K <= 8, A in {128, 256}): per-token
+            # scalars instead of dz rows; the frame-blocked grouped sums
+            # recompute dz from L2-resident H2W rows (saves the 4A bytes/token
+            # dz write + read)
             if self.recompute_dz:
                 tsc, dz = S.get("st.tsc", (M, 4)), None
             else:

@@ -224,3 +224,59 @@ def test_push_imagined_fifo_overflow_equals_host_pushes():
                                    atol=1e-12)
         assert [(h.t_len, h.done) for h in dev_buf._items] == \
             [(h.t_len, h.done) for h in host_buf._items]
+
+
+def test_span_ring_plan_does_not_mutate_on_failure():
+    """A batch the arena cannot hold raises before any ring state changes
+    (push_imagined checks both rings this way before touching its counters)."""
+    from paper_2603_18464_b200.errors import DimensionError
+    r = SpanRing(10)
+    r.alloc(4, "a")
+    state = (r.head, list(r._starts), dict(r._spans))
+    with pytest.raises(DimensionError):
+        r.plan([4, 4, 4])  # 12 slots > 10: the spans would overlap each other
+    with pytest.raises(DimensionError):
+        r.alloc_many([4, 4, 4], ["x", "y", "z"])
+    assert (r.head, list(r._starts), dict(r._spans)) == state
+    starts, _, head = r.plan([3, 3])
+    assert starts == [4, 7] and head == 10 and r.head == 4
+
+
+def test_world_model_kind_is_rejected():
+    from paper_2603_18464_b200.replay import BufferKindError, DeviceReplayBuffer
+    with pytest.raises(BufferKindError):
+        DeviceReplayBuffer("world_model", 4, 3, 2, 7, max_transitions=16)
+
+
+@pytest.mark.gpu
+def test_gather_of_evicted_handle_is_a_dropped_batch():
+    """A sampled handle evicted before the build gives a None batch (the
+    reference Prefetcher drops None batches) instead of an exception or mixed
+    data; the trainer's build returns None for it."""
+    from paper_2603_18464_b200.replay import DeviceReplayBuffer
+    from paper_2603_18464_b200.workload import synthetic_trajectories
+    rng = np.random.default_rng(3)
+    buf = DeviceReplayBuffer("main", 2, 6, 2, 8, max_transitions=64)
+    for t in synthetic_trajectories(rng, [3, 4], [True, False], 2, 8, 6):
+        buf.push(t)
+    picks = buf.sample(2, np.random.default_rng(0))
+    assert buf.gather(picks) is not None
+    for t in synthetic_trajectories(rng, [5, 2], [False, True], 2, 8, 6):
+        buf.push(t)  # FIFO: both sampled handles leave
+    assert buf.gather(picks) is None
+
+
+@pytest.mark.gpu
+def test_push_imagined_too_large_for_arena_changes_nothing():
+    import torch
+    from paper_2603_18464_b200.errors import DimensionError
+    from paper_2603_18464_b200.replay import DeviceReplayBuffer
+    O, K, A, H, n = 5, 2, 3, 4, 6
+    buf = DeviceReplayBuffer("imagined", 8, O, K, A, max_transitions=10)
+    out = {"status": torch.zeros(n, dtype=torch.int32), "t_len": torch.full((n,), H),
+           "done": torch.zeros(n, dtype=torch.bool), "rewards": torch.zeros(n, H),
+           "observations": torch.zeros(n, H + 1, O)}
+    before = buf.stats()
+    with pytest.raises(DimensionError):
+        buf.push_imagined(out)  # 24 transitions do not fit a 10-transition arena
+    assert buf.stats() == before and len(buf) == 0
