@@ -366,9 +366,39 @@ int accel_wm_adam(double* params, const double* grads, double* m, double* v, int
                   void* stream);
 
 /* 3xTF32 operand split (x f32[n], n % 4 == 0): hi = x rounded to TF32, lo =
- * x - hi; products wider than the resident-weight tcgen05 kernels run as
- * hi.hi + hi.lo + lo.hi TF32 library GEMMs accumulated in fp32. */
+ * x - hi (diagnostics; the wide GEMMs below use accel_tf32_pairs). */
 int accel_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream);
+
+/* ---- wide tensor-core GEMM (cfg4: O = D = 4096; csrc/tc_wide.cu) -------- */
+
+/* bf16 "pair" operand of an fp32 matrix X [rows, cols] (pitch ld elements):
+ * per 8-element group along K, [bf16(hi) x8 | bf16(lo) x8] ([lo | hi] when
+ * lo_first), hi = trunc19(x) (the value a tf32 MMA reads from the raw word),
+ * lo = x - hi.  row_pair = 0 (K = cols): out bf16[rows, 2*ceil8(cols)];
+ * row_pair = 1 (K = rows): out bf16[2*ceil8(rows), cols]; pitch ldo elements,
+ * ldo % 8 == 0, zero padding past K. */
+int accel_tf32_pairs(const float* X, int64_t rows, int64_t cols, int64_t ld, void* out,
+                     int64_t ldo, int row_pair, int lo_first, void* stream);
+/* Work tiles (128 x BN, BN <= 256) of an M x N product (split-K sizing). */
+int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn);
+/* C = A . B^T with fp32-class accuracy from two tensor-core passes per 8-k
+ * step: a tf32 MMA on the raw fp32 tiles (A_hi B_hi) plus a bf16 MMA on the
+ * pair operands (A_hi B_lo + A_lo B_hi).  The dense products of the
+ * OpenVLA-7B-shaped heads, forward and backward (models.py:176-209,
+ * :283-314), where both dimensions exceed the resident-weight kernels.
+ *   A: a_mn = 0 -> [M, K] (pitch lda), 1 -> stored [K, M];  Ap its pair array
+ *      (accel_tf32_pairs with lo_first = 0, row_pair = a_mn), pitch ldap.
+ *   B: b_mn = 0 -> [N, K], 1 -> stored [K, N];  Bp (lo_first = 1, row_pair =
+ *      b_mn), pitch ldbp.
+ *   epi 0: C[M, N] (ldc) = acc;  1: tanh(acc + bias[N]);  2: acc (1 - H^2)
+ *      (H pitch ldh) and col_part f32[ceil(M/128)][N] = per-128-row-tile column
+ *      sums of C (bias gradient, reduced in fixed order by the caller);
+ *   3: split-K, C = f32[kslices][M][N] partial slices (caller reduces). */
+int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B, const void* Bp, float* C,
+                       const float* bias, const float* H, float* col_part, int64_t M, int64_t N,
+                       int64_t K, int64_t lda, int64_t ldap, int64_t ldb, int64_t ldbp,
+                       int64_t ldc, int64_t ldh, int a_mn, int b_mn, int epi, int kslices,
+                       void* stream);
 
 /* ---- tensor-core GEMM (tcgen05, 3xTF32: fp32-accurate) ----------------- */
 

@@ -1,0 +1,492 @@
+// Wide fp32-accurate GEMMs on tcgen05 (cfg4: the OpenVLA-7B-shaped heads, O = D = 4096).
+//
+// The row kernels of tc_gemm.cu keep the whole (<= 256 x 256) weight resident in
+// shared memory; at cfg4 every product of the policy / value heads has two
+// dimensions of 4096 (models.py:176-182 forward, :191-204 backward; value head
+// :283-314), so here both operands stream through a TMA ring, tile by tile:
+//
+//   C[M, N] = A[M, K] . B[N, K]^T      (UMMA: D[m, n] = sum_k A[m, k] B[n, k])
+//
+// with each operand K-major (k contiguous: activations in a forward product,
+// weights [out, in]) or MN-major (m / n contiguous: a weight used as [in, out],
+// or both operands of a weight gradient, whose reduction runs over the rows).
+//
+// Accuracy (the 1e-4 gradient tolerance rules out plain TF32).  Every fp32 x is
+// x = hi + lo with hi = trunc19(x), the value the tensor core reads from a raw
+// fp32 word.  Per 8-wide k step the kernel issues TWO MMAs into one fp32 TMEM
+// accumulator:
+//   kind::tf32  A_raw . B_raw                       = A_hi B_hi
+//   kind::f16   [bf16(A_hi) x8 | bf16(A_lo) x8] . [bf16(B_lo) x8 | bf16(B_hi) x8]
+//                                                   = A_hi B_lo + A_lo B_hi
+// The correction terms are ~2^-10 of the main term, so rounding them to bf16
+// costs ~2^-19 relative (the dropped lo.lo is ~2^-20): fp32-class accuracy for
+// two tensor-core passes instead of 3xTF32's three (a K = 16 bf16 MMA takes the
+// cycles of a K = 8 tf32 one).  The bf16 "pair" operands are written by
+// accel_tf32_pairs (one HBM-bound elementwise pass per operand).
+//
+// Persistent, warp-specialised (192 threads, one CTA per SM): warp 0 lane 0
+// issues the TMA loads of a 4..8-stage ring (16 k per stage: raw fp32 tiles
+// with 64 B-swizzled K-major rows or 128 B-swizzled MN-major slabs, bf16 pair
+// tiles alike); warp 1 issues the MMAs (one elected lane) into double-buffered
+// TMEM accumulators (128 x BN fp32, BN <= 256); warps 2-5 drain them
+// (tcgen05.ld, 32 columns at a time) through the epilogue: plain store, bias +
+// tanh, the tanh derivative (Y = acc (1 - H^2)) with per-tile column sums for
+// the bias gradient, or split-K partial slices (reduced by the caller in fixed
+// order: deterministic).  Work units (m tile, n tile, k slice) are dealt n-tile
+// fastest, so CTAs running together share the A tile rows through L2.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "tc_common.cuh"
+
+namespace accel {
+namespace {
+
+using namespace tc;
+
+constexpr int kWThreads = 192;  // 6 warps
+constexpr int kWEpi0 = 2;       // epilogue warps 2..5
+constexpr int kBK = 16;         // fp32 k per stage (two 8-k MMA steps)
+constexpr int kMaxStages = 8;
+constexpr size_t kWideSmem = 222 * 1024;  // dynamic (ring); + ~5 KB static
+
+enum Epi : int { kStore = 0, kBiasTanh = 1, kDtanh = 2, kPartial = 3 };
+
+struct WideArgs {
+  float* C;
+  const float* bias;
+  const float* H;
+  float* col_part;  // kDtanh: [m_tiles][N] column sums of Y (per m tile, fixed order)
+  int64_t M, N, ldc, ldh;
+  int BN, m_tiles, n_tiles, kslices, kblocks, a_mn, b_mn, epi, nstages, vec, hvec;
+  uint32_t stage_bytes, a_pair_off, b_raw_off, b_pair_off, tx_bytes, tmem_cols;
+};
+
+__device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// kind::f16 with bf16 A/B, fp32 D, M = 128, N = n
+__device__ __forceinline__ uint32_t make_idesc_bf16(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  const float t = __expf(2.f * x);
+  return 1.f - __fdividef(2.f, t + 1.f);
+}
+
+// operand descriptors at k step s of a stage (see the layouts in launch_wide)
+__device__ __forceinline__ uint64_t raw_desc(uint32_t base, int mn, int s) {
+  return mn ? make_sdesc(base + s * 1024, kBK * 128, 512, 1)   // 32-col slabs of 16 rows
+            : make_sdesc(base + s * 32, 16, 512, 4);           // 64 B rows, SWIZZLE_64B
+}
+__device__ __forceinline__ uint64_t pair_desc(uint32_t base, int mn, int s) {
+  return mn ? make_sdesc(base + s * 2048, 2 * kBK * 128, 1024, 2)  // 64-col atoms of 32 rows
+            : make_sdesc(base + s * 32, 16, 512, 4);
+}
+
+// TMA loads of one operand tile (rows r0.. of the MN dimension, k block kb)
+__device__ __forceinline__ void load_operand(unsigned char* raw, unsigned char* pair,
+                                             const CUtensorMap* rmap, const CUtensorMap* pmap,
+                                             int mn, int r0, int rows, int kb, uint64_t* bar) {
+  if (mn) {
+    for (int j = 0; j < rows / 32; ++j)  // fp32 slabs: 32 columns x 16 k rows
+      tma_load_2d(raw + j * (kBK * 128), rmap, r0 + 32 * j, kb * kBK, bar);
+    for (int j = 0; j < rows / 64; ++j)  // bf16 atoms: 64 columns x 32 pair rows
+      tma_load_2d(pair + j * (2 * kBK * 128), pmap, r0 + 64 * j, kb * 2 * kBK, bar);
+  } else {
+    tma_load_2d(raw, rmap, kb * kBK, r0, bar);        // rows x 16 fp32
+    tma_load_2d(pair, pmap, kb * 2 * kBK, r0, bar);   // rows x 32 bf16
+  }
+}
+
+struct WideBars {
+  uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+};
+
+__global__ void __launch_bounds__(kWThreads, 1)
+tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant__ CUtensorMap a_pair,
+               const __grid_constant__ CUtensorMap b_raw, const __grid_constant__ CUtensorMap b_pair,
+               WideArgs p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ WideBars bars;
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(16) float s_col[4][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (smem_u32(smem) & 1023) __trap();
+  const int BN = p.BN;
+  if (warp == 1) tmem_alloc(&tmem_base, p.tmem_cols);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstages; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.tfull[b], 1);
+      mbar_init(&bars.tempty[b], 4);
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a_raw)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&b_raw)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int64_t units = (int64_t)p.m_tiles * p.n_tiles * p.kslices;
+  const int64_t my_units = units > (int64_t)blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // unit u -> (k slice, m tile, n tile), n fastest; its k-block range
+  auto decode = [&](int64_t u, int& ks, int& mt, int& nt, int& kb0, int& kb1) {
+    const int64_t mn = (int64_t)p.m_tiles * p.n_tiles;
+    ks = (int)(u / mn);
+    const int64_t r = u - (int64_t)ks * mn;
+    mt = (int)(r / p.n_tiles);
+    nt = (int)(r - (int64_t)mt * p.n_tiles);
+    kb0 = (int)((int64_t)ks * p.kblocks / p.kslices);
+    kb1 = (int)((int64_t)(ks + 1) * p.kblocks / p.kslices);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      int slot = 0;
+      unsigned ph = 0;
+      for (int64_t t = 0; t < my_units; ++t) {
+        int ks, mt, nt, kb0, kb1;
+        decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&bars.empty[slot], ph ^ 1u);
+          unsigned char* st = smem + (size_t)slot * p.stage_bytes;
+          uint64_t* bar = &bars.full[slot];
+          mbar_expect_tx(bar, p.tx_bytes);
+          load_operand(st, st + p.a_pair_off, &a_raw, &a_pair, p.a_mn, mt * kBM, kBM, kb, bar);
+          load_operand(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn, nt * BN, BN,
+                       kb, bar);
+          if (++slot == p.nstages) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (warp-wide loop, one elected lane issues)
+    const uint32_t id_tf = make_idesc(BN, p.a_mn, p.b_mn);
+    const uint32_t id_bf = make_idesc_bf16(BN, p.a_mn, p.b_mn);
+    int slot = 0;
+    unsigned ph = 0;
+    for (int64_t t = 0; t < my_units; ++t) {
+      int ks, mt, nt, kb0, kb1;
+      decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
+      const int b = (int)(t & 1);
+      mbar_wait(&bars.tempty[b], ((unsigned)(t >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(b * BN);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&bars.full[slot], ph);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + (size_t)slot * p.stage_bytes);
+#pragma unroll
+        for (int s = 0; s < kBK / 8; ++s) {
+          mma_tf32_w(d, raw_desc(st, p.a_mn, s), raw_desc(st + p.b_raw_off, p.b_mn, s), id_tf,
+                     (kb > kb0 || s > 0) ? 1u : 0u);
+          mma_bf16_w(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
+                     pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf, 1u);
+        }
+        mma_commit_w(&bars.empty[slot]);
+        if (++slot == p.nstages) {
+          slot = 0;
+          ph ^= 1u;
+        }
+      }
+      mma_commit_w(&bars.tfull[b]);
+    }
+  } else {
+    // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows
+    const int q = warp & 3, ew = warp - kWEpi0;
+    for (int64_t t = 0; t < my_units; ++t) {
+      int ks, mt, nt, kb0, kb1;
+      decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
+      const int b = (int)(t & 1);
+      mbar_wait(&bars.tfull[b], (unsigned)(t >> 1) & 1u);
+      tc_fence_after();
+      const int64_t row = (int64_t)mt * kBM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      const int64_t n0 = (int64_t)nt * BN;
+      float* out = p.epi == kPartial ? p.C + (int64_t)ks * p.M * p.N + row * p.N
+                                     : p.C + row * p.ldc;
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        float v[32];
+        tmem_ld32(tb + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int64_t cb = n0 + c0;
+        if (p.epi == kBiasTanh) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            v[j] = tanh_fast(v[j] + (cb + j < p.N ? __ldg(p.bias + cb + j) : 0.f));
+        } else if (p.epi == kDtanh) {
+          const float* h = p.H + row * p.ldh + cb;
+          if (row_ok && p.hvec && cb + 32 <= p.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 hv = __ldg(reinterpret_cast<const float4*>(h + j));
+              v[j] *= 1.f - hv.x * hv.x;
+              v[j + 1] *= 1.f - hv.y * hv.y;
+              v[j + 2] *= 1.f - hv.z * hv.z;
+              v[j + 3] *= 1.f - hv.w * hv.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float hv = (row_ok && cb + j < p.N) ? __ldg(h + j) : 0.f;
+              v[j] = row_ok ? v[j] * (1.f - hv * hv) : 0.f;
+            }
+          }
+        }
+        if (row_ok) {
+          if (p.vec && cb + 32 <= p.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(out + cb + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (cb + j < p.N) out[cb + j] = v[j];
+          }
+        }
+        if (p.epi == kDtanh) {
+          // column sums of this warp's 32 rows: transposed butterfly, lane j ends
+          // with column c0 + j (31 shuffles; fixed order)
+#pragma unroll
+          for (int sft = 16; sft >= 1; sft >>= 1) {
+            const bool up = (lane & sft) != 0;
+#pragma unroll
+            for (int i = 0; i < sft; ++i) {
+              const float send = up ? v[i] : v[i + sft];
+              const float keep = up ? v[i + sft] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+            }
+          }
+          s_col[ew][c0 + lane] = v[0];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.tempty[b]);
+      if (p.epi == kDtanh) {  // the tile's column sums, epilogue warps in fixed order
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int e = threadIdx.x - kWEpi0 * 32;
+        for (int c = e; c < BN; c += 128)
+          if (n0 + c < p.N)
+            p.col_part[(int64_t)mt * p.N + n0 + c] =
+                ((s_col[0][c] + s_col[1][c]) + s_col[2][c]) + s_col[3][c];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// ---- bf16 pair operands --------------------------------------------------------
+
+__device__ __forceinline__ void split_pair(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  hi = __float2bfloat16_rn(h);
+  lo = __float2bfloat16_rn(x - h);
+}
+
+// K along the columns: out[r, 16 g + j] = first(x[r, 8 g + j]), out[r, 16 g + 8 + j] = second
+__global__ void pairs_col_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                                 __nv_bfloat16* __restrict__ out, int64_t ldo, int lo_first) {
+  const int64_t groups = (cols + 7) / 8;
+  const int64_t n = rows * groups;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / groups, g = i - r * groups;
+    const float* src = X + r * ld + g * 8;
+    float x[8];
+    if (g * 8 + 8 <= cols && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+      const float4 u = *reinterpret_cast<const float4*>(src);
+      const float4 w = *reinterpret_cast<const float4*>(src + 4);
+      x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+      x[4] = w.x; x[5] = w.y; x[6] = w.z; x[7] = w.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = g * 8 + j < cols ? src[j] : 0.f;
+    }
+    __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) split_pair(x[j], hi[j], lo[j]);
+    uint4* dst = reinterpret_cast<uint4*>(out + r * ldo + g * 16);
+    dst[0] = *reinterpret_cast<const uint4*>(lo_first ? lo : hi);
+    dst[1] = *reinterpret_cast<const uint4*>(lo_first ? hi : lo);
+  }
+}
+
+// K along the rows: out[16 g + j, c] = first(x[8 g + j, c]), out[16 g + 8 + j, c] = second
+__global__ void pairs_row_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                                 __nv_bfloat16* __restrict__ out, int64_t ldo, int lo_first) {
+  const int64_t groups = (rows + 7) / 8;
+  const int64_t cq = (cols + 3) / 4;  // 4 columns per thread
+  const int64_t n = groups * cq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = i / cq, c = (i - g * cq) * 4;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t r = g * 8 + j;
+      float x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = (r < rows && c + u < cols) ? X[r * ld + c + u] : 0.f;
+      __align__(8) __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) split_pair(x[u], hi[u], lo[u]);
+      __nv_bfloat16* d0 = out + (g * 16 + j) * ldo + c;
+      __nv_bfloat16* d1 = out + (g * 16 + 8 + j) * ldo + c;
+      *reinterpret_cast<uint2*>(d0) = *reinterpret_cast<const uint2*>(lo_first ? lo : hi);
+      *reinterpret_cast<uint2*>(d1) = *reinterpret_cast<const uint2*>(lo_first ? hi : lo);
+    }
+  }
+}
+
+// ---- host ------------------------------------------------------------------------
+
+int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, float* C,
+                const float* bias, const float* H, float* col_part, int64_t M, int64_t N, int64_t K,
+                int64_t lda, int64_t ldap, int64_t ldb, int64_t ldbp, int64_t ldc, int64_t ldh,
+                int a_mn, int b_mn, int epi, int kslices, cudaStream_t st) {
+  WideArgs p{};
+  p.BN = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);
+  if (b_mn) p.BN = (p.BN + 63) / 64 * 64;  // MN-major pair tiles come in 64-column atoms
+  p.C = C; p.bias = bias; p.H = H; p.col_part = col_part;
+  p.M = M; p.N = N; p.ldc = ldc; p.ldh = ldh;
+  p.m_tiles = (int)ceil_div(M, kBM);
+  p.n_tiles = (int)ceil_div(N, p.BN);
+  p.kblocks = (int)ceil_div(K, kBK);
+  p.kslices = std::max(1, std::min(kslices, p.kblocks));
+  p.a_mn = a_mn; p.b_mn = b_mn; p.epi = epi;
+  const bool c_al = (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+  p.vec = (c_al && (epi == kPartial ? N % 4 == 0 : ldc % 4 == 0)) ? 1 : 0;
+  p.hvec = (H && (reinterpret_cast<uintptr_t>(H) & 15) == 0 && ldh % 4 == 0) ? 1 : 0;
+  // stage layout: [A raw | A pair | B raw | B pair], each region 1 KB aligned
+  auto al = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
+  const uint32_t a_bytes = kBM * kBK * 4, b_bytes = (uint32_t)p.BN * kBK * 4;  // raw == pair bytes
+  p.a_pair_off = al(a_bytes);
+  p.b_raw_off = p.a_pair_off + al(a_bytes);
+  p.b_pair_off = p.b_raw_off + al(b_bytes);
+  p.stage_bytes = p.b_pair_off + al(b_bytes);
+  p.tx_bytes = 2 * (a_bytes + b_bytes);
+  p.nstages = (int)std::min<size_t>(kMaxStages, kWideSmem / p.stage_bytes);
+  if (p.nstages < 2) return fail(kDimension, "tc_wide: stage too large");
+  p.tmem_cols = tmem_cols_for(2 * p.BN);
+  // tensor maps: K-major operands as [rows = M|N, cols = K] with 64 B-swizzled
+  // boxes; MN-major ones as [rows = K, cols = M|N] in 128 B-swizzled slabs / atoms
+  const int64_t K8 = (K + 7) / 8 * 8;
+  CUtensorMap am, apm, bm, bpm;
+  auto mk = [&](CUtensorMap* raw, CUtensorMap* pair, const float* X, const void* Xp, int64_t mnrows,
+                int64_t ld, int64_t ldp, int mn, int tile_rows) -> int {
+    if (mn) {
+      if (int e = make_map_dt(raw, X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, K, mnrows, ld, 32, kBK,
+                              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return e;
+      return make_map_dt(pair, Xp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2 * K8, mnrows, ldp, 64,
+                         2 * kBK, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    if (int e = make_map_dt(raw, X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, mnrows, K, ld, kBK, tile_rows,
+                            CU_TENSOR_MAP_SWIZZLE_64B))
+      return e;
+    return make_map_dt(pair, Xp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, mnrows, 2 * K8, ldp, 2 * kBK,
+                       tile_rows, CU_TENSOR_MAP_SWIZZLE_64B);
+  };
+  if (int e = mk(&am, &apm, A, Ap, M, lda, ldap, a_mn, kBM)) return e;
+  if (int e = mk(&bm, &bpm, B, Bp, N, ldb, ldbp, b_mn, p.BN)) return e;
+  const size_t smem = (size_t)p.nstages * p.stage_bytes;
+  cudaError_t e = cudaFuncSetAttribute(tc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return fail(kCuda, "tc_wide smem: %s", cudaGetErrorString(e));
+  const int64_t units = (int64_t)p.m_tiles * p.n_tiles * p.kslices;
+  const int grid = (int)std::min<int64_t>(units, sm_count());
+  tc_wide_kernel<<<grid, kWThreads, smem, st>>>(am, apm, bm, bpm, p);
+  return post_launch("tc_wide_kernel");
+}
+
+}  // namespace
+}  // namespace accel
+
+using namespace accel;
+
+// C = A . B^T over fp32 operands with fp32-class accuracy (see the file comment).
+//   a_mn = 0: A is [M, K] (row pitch lda), else [K, M];  b_mn = 0: B is [N, K], else [K, N].
+//   Ap / Bp: the operands' bf16 pair arrays (accel_tf32_pairs: A with lo_first = 0,
+//   B with lo_first = 1; column pairs for K-major, row pairs for MN-major), pitch in
+//   elements.  epi: 0 store C[M, N] (ldc); 1 tanh(acc + bias); 2 acc (1 - H^2) with
+//   col_part[ceil(M / 128)][N] = per-128-row-tile column sums of C; 3 split-K:
+//   C = [kslices][M][N] partial slices (the caller sums them in order).
+extern "C" int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B, const void* Bp,
+                                  float* C, const float* bias, const float* H, float* col_part,
+                                  int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldap,
+                                  int64_t ldb, int64_t ldbp, int64_t ldc, int64_t ldh, int a_mn,
+                                  int b_mn, int epi, int kslices, void* stream) {
+  if (M < 0 || N < 1 || K < 1 || kslices < 1 || epi < 0 || epi > 3)
+    return fail(kDimension, "tc_gemm_wide: bad sizes M=%lld N=%lld K=%lld", (long long)M,
+                (long long)N, (long long)K);
+  if (M == 0) return kOk;
+  if (!A || !Ap || !B || !Bp || !C) return fail(kDimension, "tc_gemm_wide: NULL operand");
+  if (epi == kBiasTanh && !bias) return fail(kDimension, "tc_gemm_wide: bias+tanh needs bias");
+  if (epi == kDtanh && (!H || !col_part)) return fail(kDimension, "tc_gemm_wide: dtanh needs H, col_part");
+  if (epi != kPartial && kslices != 1) return fail(kDimension, "tc_gemm_wide: split-K needs epi 3");
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return fail(kDimension, "tc_gemm_wide: too large");
+  return launch_wide(A, Ap, B, Bp, C, bias, H, col_part, M, N, K, lda, ldap, ldb, ldbp, ldc, ldh,
+                     a_mn, b_mn, epi, kslices, as_stream(stream));
+}
+
+extern "C" int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn) {
+  int bn = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);
+  if (b_mn) bn = (bn + 63) / 64 * 64;
+  return (int)(ceil_div(M, kBM) * ceil_div(N, bn));
+}
+
+// bf16 pair operand of an fp32 matrix X [rows, cols] (pitch ld): per 8-element group
+// along K, [bf16(hi) x8 | bf16(lo) x8] (lo_first: [lo | hi]), hi = trunc19(x), lo = x - hi.
+// row_pair = 0 (K = cols): out [rows, 2 * ceil8(cols)], pitch ldo >= 2 * ceil8(cols);
+// row_pair = 1 (K = rows): out [2 * ceil8(rows), cols], pitch ldo >= cols (ldo % 8 == 0).
+extern "C" int accel_tf32_pairs(const float* X, int64_t rows, int64_t cols, int64_t ld, void* out,
+                                int64_t ldo, int row_pair, int lo_first, void* stream) {
+  if (rows < 0 || cols < 1 || ld < cols) return fail(kDimension, "tf32_pairs: bad sizes");
+  if (rows == 0) return kOk;
+  if (!X || !out) return fail(kDimension, "tf32_pairs: NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(out) & 15) || ldo % 8)
+    return fail(kDimension, "tf32_pairs: output needs 16-byte aligned rows");
+  auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+  cudaStream_t st = as_stream(stream);
+  const int threads = 256;
+  if (row_pair) {
+    if (ldo < cols) return fail(kDimension, "tf32_pairs: ldo < cols");
+    const int64_t n = (rows + 7) / 8 * ((cols + 3) / 4);
+    const int grid = (int)std::min<int64_t>(ceil_div(n, threads), 148 * 16);
+    pairs_row_kernel<<<grid, threads, 0, st>>>(X, rows, cols, ld, o, ldo, lo_first);
+  } else {
+    if (ldo < 2 * ((cols + 7) / 8 * 8)) return fail(kDimension, "tf32_pairs: ldo too small");
+    const int64_t n = rows * ((cols + 7) / 8);
+    const int grid = (int)std::min<int64_t>(ceil_div(n, threads), 148 * 16);
+    pairs_col_kernel<<<grid, threads, 0, st>>>(X, rows, cols, ld, o, ldo, lo_first);
+  }
+  return post_launch("tf32_pairs");
+}

@@ -444,59 +444,82 @@ def tc_rows_supported(K: int, N: int) -> bool:
     return K <= 256 and N <= 256
 
 
-def split_tf32(x):
-    """(hi, lo) of a float32 tensor (accel_split_tf32); same shape, contiguous."""
-    x = x.contiguous()
-    if x.numel() % 4 or x.data_ptr() % 16:
-        x = x.clone()
-    n = x.numel()
-    pad = (-n) % 4
-    src = x.reshape(-1) if not pad else torch.cat([x.reshape(-1), x.new_zeros(pad)])
-    hi, lo = torch.empty_like(src), torch.empty_like(src)
-    _lib.call("accel_split_tf32", _p(src), src.numel(), _p(hi), _p(lo), _stream())
-    return hi[:n].view(x.shape), lo[:n].view(x.shape)
+# ---- wide products (cfg4: O = D = 4096): streamed tcgen05 tf32 + bf16-pair GEMM ----
 
 
-class _TF32:
-    """Temporarily let cuBLAS use TF32 tensor cores (the trainer keeps it off)."""
-
-    def __enter__(self):
-        self.prev = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = True
-
-    def __exit__(self, *exc):
-        torch.backends.cuda.matmul.allow_tf32 = self.prev
-        return False
+def _pair_shape(rows: int, cols: int, row_pair: bool) -> tuple:
+    c8 = -(-int(cols) // 8) * 8
+    if row_pair:
+        return (2 * (-(-int(rows) // 8) * 8), c8)
+    return (int(rows), 2 * c8)
 
 
-def mm_3xtf32(a, b, out, accumulate=False):
-    """out (+)= a @ b for wide float32 products: three TF32 tensor-core library
-    GEMMs on split operands, hi.hi + hi.lo + lo.hi, fp32 accumulation (about
-    fp32 accuracy: tests/test_trainer_gpu.py::test_wide_layers_match_oracle).
-    a / b may be transposed views of contiguous tensors: the split keeps it."""
-    def split(t):
-        if not t.is_contiguous() and t.t().is_contiguous():  # a transposed view
-            hi, lo = split_tf32(t.t())
-            return hi.t(), lo.t()
-        return split_tf32(t)
-    ah, al = split(a)
-    bh, bl = split(b)
-    with _TF32():
-        if accumulate:
-            out.addmm_(ah, bh)
-        else:
-            torch.mm(ah, bh, out=out)
-        out.addmm_(ah, bl)
-        out.addmm_(al, bh)
+def tf32_pairs(x, row_pair: bool, lo_first: bool, out=None):
+    """bf16 pair operand of fp32 x (accel_tf32_pairs): per 8-group along K,
+    [bf16(hi) | bf16(lo)] ([lo | hi] with lo_first), hi = trunc19(x).  K runs
+    along the columns (row_pair False, K-major use) or the rows (MN-major use)."""
+    rows, cols = x.shape
+    if x.stride(1) != 1:
+        raise DimensionError("tf32_pairs: unit column stride required")
+    shape = _pair_shape(rows, cols, row_pair)
+    out = torch.empty(shape, dtype=torch.bfloat16, device=x.device) if out is None else out
+    _lib.call("accel_tf32_pairs", _p(x), rows, cols, x.stride(0), _p(out), out.stride(0),
+              int(row_pair), int(lo_first), _stream())
     return out
 
 
-def _mm_fallback(x, w_t, out, bias=None, tanh=False, accumulate=False):
-    mm_3xtf32(x, w_t, out, accumulate=accumulate)
+def _pairs_ws(tag: str, x, row_pair: bool, lo_first: bool):
+    shape = _pair_shape(x.shape[0], x.shape[1], row_pair)
+    n = shape[0] * shape[1]
+    buf = workspace("pair." + tag).get(2 * n)
+    return tf32_pairs(x, row_pair, lo_first, buf[:2 * n].view(torch.bfloat16).view(shape))
+
+
+def wide_tiles(M: int, N: int, b_mn: bool) -> int:
+    return int(_lib.lib().accel_tc_wide_tiles(int(M), int(N), int(bool(b_mn))))
+
+
+def wide_gemm(a, b, out, *, a_mn: bool, b_mn: bool, epi: int = 0, bias=None, h=None,
+              col_part=None, kslices: int = 1, tag: str = ""):
+    """out = A . B^T on the streamed tensor-core kernel (accel_tc_gemm_wide):
+    a is A [M, K] (a_mn False) or A^T stored [K, M]; b is B [N, K] (b_mn False)
+    or B^T stored [K, N].  epi 0 store, 1 tanh(. + bias), 2 (.)(1 - h^2) with
+    col_part[m_tiles, N] column sums, 3 split-K partial slices out[kslices, M, N]."""
+    M = a.shape[1] if a_mn else a.shape[0]
+    K = a.shape[0] if a_mn else a.shape[1]
+    N = b.shape[1] if b_mn else b.shape[0]
+    if (b.shape[0] if b_mn else b.shape[1]) != K:
+        raise DimensionError(f"wide_gemm: inner dims {K} and {tuple(b.shape)}")
+    a, b = pitched(a), pitched(b)
+    ap = _pairs_ws(tag + "a", a, a_mn, False)
+    bp = _pairs_ws(tag + "b", b, b_mn, True)
+    ldc = N if epi == 3 else out.stride(0)
+    _lib.call("accel_tc_gemm_wide", _p(a), _p(ap), _p(b), _p(bp), _p(out), _p(bias), _p(h),
+              _p(col_part), M, N, K, a.stride(0), ap.stride(0), b.stride(0), bp.stride(0), ldc,
+              h.stride(0) if h is not None else 0, int(a_mn), int(b_mn), int(epi), int(kslices),
+              _stream())
+    return out
+
+
+def _wide_rows(x, b, out, b_mn: bool, bias=None, tanh=False):
+    """out = act(x . B^T + bias) for wide shapes; few output tiles -> split-K
+    partial slices summed in fixed order (deterministic)."""
+    M, N = x.shape[0], out.shape[1]
+    tiles = wide_tiles(M, N, b_mn)
+    sms = tc_sm_count()
+    if tanh:
+        if bias is None:
+            raise DimensionError("tanh epilogue needs the bias")
+        return wide_gemm(x, b, out, a_mn=False, b_mn=b_mn, epi=1, bias=bias, tag="rows")
+    ks = max(1, sms // tiles) if tiles < sms // 2 and out.is_contiguous() else 1
+    if ks > 1:
+        part = workspace("wide_part").get(4 * ks * M * N)[:4 * ks * M * N].view(F32)
+        wide_gemm(x, b, part, a_mn=False, b_mn=b_mn, epi=3, kslices=ks, tag="rows")
+        reduce_segments([(part, out, ks, M * N, M * N)])
+    else:
+        wide_gemm(x, b, out, a_mn=False, b_mn=b_mn, epi=0, tag="rows")
     if bias is not None:
         out.add_(bias)
-    if tanh:
-        out.tanh_()
     return out
 
 
@@ -506,7 +529,9 @@ def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
     N = w.shape[0]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
     if not tc_rows_supported(K, N):
-        return _mm_fallback(x, w.t(), out, bias, tanh, accumulate)
+        if accumulate:
+            raise DimensionError("wide products do not accumulate")
+        return _wide_rows(x, w, out, False, bias, tanh)
     x = pitched(x)
     _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
               w.stride(0), out.stride(0), 0, 0, int(tanh), int(accumulate), 1, _stream())
@@ -520,7 +545,7 @@ def tc_linear_checked(x, w, out, nonfinite, bias=None, tanh=False):
     N = w.shape[0]
     if not tc_rows_supported(K, N):
         count_nonfinite_rows(x, None, M, nonfinite)  # counts rows, same decision
-        return _mm_fallback(x, w.t(), out, bias, tanh)
+        return _wide_rows(x, w, out, False, bias, tanh)
     x = pitched(x)
     _lib.call("accel_tc_linear_checked", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
               w.stride(0), out.stride(0), int(tanh), _p(nonfinite), _stream())
@@ -533,7 +558,9 @@ def tc_matmul_nn(x, w, out=None, accumulate=False):
     N = w.shape[1]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
     if not tc_rows_supported(K, N):
-        return _mm_fallback(x, w, out, accumulate=accumulate)
+        if accumulate:
+            raise DimensionError("wide products do not accumulate")
+        return _wide_rows(x, w, out, True)
     x = pitched(x)
     _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), None, M, K, N, x.stride(0), w.stride(0),
               out.stride(0), 0, 1, 0, int(accumulate), 1, _stream())
@@ -557,6 +584,12 @@ def tc_matmul_nn_dtanh(x, w, h, out, part_fn):
     N = w.shape[1]
     # fused for short K (the resident [W_hi; W_lo] leaves room for two staging boxes
     # per epilogue warp); at K = 256 the unfused pair is faster
+    if not tc_rows_supported(K, N):  # wide: the tanh derivative rides in the epilogue
+        n = -(-M // 128)
+        part = part_fn(n)
+        wide_gemm(x, w, out, a_mn=False, b_mn=True, epi=2, h=pitched(h), col_part=part,
+                  tag="dtanh")
+        return out, part, n
     if N <= 256 and K <= 128 and _aligned_rows(out) and _aligned_rows(h):
         n = tc_rows_grid(M)
         part = part_fn(n)
@@ -574,6 +607,13 @@ def tc_sm_count() -> int:
     return int(_lib.lib().accel_tc_sm_count())
 
 
+def wide_kslices(n: int, k: int) -> int:
+    """k slices of a wide weight gradient dW[n, k] (reduction over the rows):
+    enough work units to fill the SMs."""
+    tiles = wide_tiles(n, k, True)
+    return max(1, tc_sm_count() // tiles)
+
+
 def tc_wgrad(dy, x, out, kslices=None, partial=None):
     """out[n, k] = dy[F, n]^T . x[F, k] (reduction over the F rows): `kslices`
     persistent CTAs each produce two fp32 partials, reduced in fixed order
@@ -581,7 +621,11 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     F, n = dy.shape
     k = x.shape[1]
     if n > 256 or k > 256:
-        return mm_3xtf32(dy.t(), x, out)
+        ks = wide_kslices(n, k)
+        part = torch.empty(ks, n, k, dtype=F32, device=dy.device)
+        wide_gemm(dy, x, part, a_mn=True, b_mn=True, epi=3, kslices=ks, tag="wgrad")
+        reduce_segments([(part, out, ks, n * k, n * k)])
+        return out
     dy, x = pitched(dy), pitched(x)
     if kslices is None:
         kslices = max(1, min(tc_sm_count(), -(-F // 32)))

@@ -703,10 +703,11 @@ class Trainer:
         the caller fills); returns the reduce_segments entry that sums them."""
         F, n = dy.shape
         k = x.shape[1]
-        if n > 256 or k > 256:  # wide layers (cfg4): 3xTF32 library GEMMs, one "partial"
-            part = self.scratch.get("wg." + tag, (1 + extra, n, k))
-            ops.mm_3xtf32(dy.t(), x, part[0])
-            return (part, out, 1 + extra, n * k, n * k)
+        if n > 256 or k > 256:  # wide layers (cfg4): streamed tcgen05 GEMM, split-K slices
+            ks = ops.wide_kslices(n, k)
+            part = self.scratch.get("wg." + tag, (ks + extra, n, k))
+            ops.wide_gemm(dy, x, part, a_mn=True, b_mn=True, epi=3, kslices=ks, tag="wgrad")
+            return (part, out, ks + extra, n * k, n * k)
         dy, x = ops.pitched(dy), ops.pitched(x)  # no-ops at aligned widths
         ks = max(1, min(ops.tc_sm_count(), -(-F // 32)))
         part = self.scratch.get("wg." + tag, (2 * ks + extra, n, k))

@@ -1,0 +1,130 @@
+"""Wide tensor-core GEMM (csrc/tc_wide.cu, cfg4 widths) against float64.
+
+Every operand layout (A / B K-major or MN-major), every epilogue (store, bias
++ tanh, tanh derivative with column sums, split-K slices), ragged tiles (M,
+N, K not multiples of the tile), narrow N (BN = 32).  Accuracy target: the
+3xTF32 class, |err| <= 2e-5 of max |C| (the trainer's tolerance is 1e-4).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-5
+
+
+def _mats(M, N, K, a_mn, b_mn, seed=0):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    B = torch.randn(N, K, device="cuda", generator=g)
+    a = A.t().contiguous() if a_mn else A
+    b = B.t().contiguous() if b_mn else B
+    return A, B, a, b
+
+
+def _err(got, want):
+    got, want = got.double().cpu().numpy(), want.cpu().numpy()
+    return float(np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-30))
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", [(300, 320, 300), (128, 256, 16), (1000, 4096, 40),
+                                   (257, 32, 4100), (64, 512, 1029)])
+def test_store_matches_float64(a_mn, b_mn, M, N, K):
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    A, B, a, b = _mats(M, N, K, a_mn, b_mn, seed=M + N + K)
+    out = torch.full((M, N), float("nan"), device="cuda")
+    ops.wide_gemm(a, b, out, a_mn=bool(a_mn), b_mn=bool(b_mn))
+    want = A.double() @ B.double().t()
+    assert _err(out, want) < TOL
+
+
+@pytest.mark.parametrize("ks", [2, 5])
+def test_split_k_slices_sum_to_product(ks):
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    M, N, K = 256, 300, 2000
+    A, B, a, b = _mats(M, N, K, 1, 1, seed=ks)
+    part = torch.full((ks, M, N), float("nan"), device="cuda")
+    ops.wide_gemm(a, b, part, a_mn=True, b_mn=True, epi=3, kslices=ks)
+    want = A.double() @ B.double().t()
+    assert _err(part.double().sum(0), want) < TOL
+    out = torch.empty(M, N, device="cuda")
+    ops.reduce_segments([(part, out, ks, M * N, M * N)])
+    assert _err(out, want) < TOL
+
+
+def test_bias_tanh_and_dtanh_epilogues():
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    M, N, K = 700, 512, 600
+    A, B, a, b = _mats(M, N, K, 0, 0, seed=3)
+    A = A * 0.05
+    a = A
+    bias = torch.randn(N, device="cuda")
+    out = torch.empty(M, N, device="cuda")
+    ops.wide_gemm(a, b, out, a_mn=False, b_mn=False, epi=1, bias=bias)
+    want = torch.tanh(A.double() @ B.double().t() + bias.double())
+    assert float((out.double() - want).abs().max()) < 2e-6
+    # dtanh: Y = (A . W) (1 - H^2), W stored [K, N] (MN-major B), column sums per 128-row tile
+    W = torch.randn(K, N, device="cuda")
+    H = torch.tanh(torch.randn(M, N, device="cuda"))
+    y = torch.empty(M, N, device="cuda")
+    nt = -(-M // 128)
+    part = torch.full((nt, N), float("nan"), device="cuda")
+    ops.wide_gemm(A, W, y, a_mn=False, b_mn=True, epi=2, h=H, col_part=part)
+    want = (A.double() @ W.double()) * (1 - H.double() ** 2)
+    assert _err(y, want) < TOL
+    assert _err(part.double().sum(0), want.sum(0)) < TOL
+    # public wrappers route wide shapes here
+    y2, part2, n2 = ops.tc_matmul_nn_dtanh(A, W, H, torch.empty(M, N, device="cuda"),
+                                          lambda n: torch.empty(n, N, device="cuda"))
+    assert n2 == nt and _err(y2, want) < TOL
+
+
+def test_public_wrappers_use_the_wide_kernel():
+    import torch
+
+    from paper_2603_18464_b200 import _lib, ops
+    M, K, N = 513, 4096, 256
+    x = torch.randn(M, K, device="cuda")
+    w = torch.randn(N, K, device="cuda")
+    n0 = _lib.launch_count()
+    y = ops.tc_linear(x, w)
+    assert _lib.launch_count() > n0  # libaccel launched it (pairs + GEMM + reduce)
+    assert _err(y, x.double() @ w.double().t()) < TOL
+    dy = torch.randn(M, 300, device="cuda")
+    g = ops.tc_wgrad(dy, x, torch.empty(300, K, device="cuda"))
+    assert _err(g, dy.double().t() @ x.double()) < TOL
+
+
+def test_pairs_hold_the_tf32_split():
+    """Per 8-group: bf16(hi) and bf16(lo) with hi = trunc19(x) (the tf32 value
+    of the raw word) and lo = x - hi, in either order, along rows or columns."""
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    x = torch.randn(37, 45, device="cuda") * 3.0
+    hi_t = (x.view(torch.int32) & -8192).view(torch.float32)
+    lo_t = x - hi_t
+    for row_pair in (False, True):
+        for lo_first in (False, True):
+            p = ops.tf32_pairs(x, row_pair, lo_first).float()
+            if row_pair:
+                grp = p.view(-1, 2, 8, p.shape[1])
+                f, s_ = grp[:, 0].reshape(-1, p.shape[1]), grp[:, 1].reshape(-1, p.shape[1])
+                f, s_ = f[:37, :45], s_[:37, :45]
+            else:
+                grp = p.view(p.shape[0], -1, 2, 8)
+                f = grp[:, :, 0].reshape(p.shape[0], -1)[:, :45]
+                s_ = grp[:, :, 1].reshape(p.shape[0], -1)[:, :45]
+            hi, lo = (s_, f) if lo_first else (f, s_)
+            assert float(((hi - hi_t).abs() / hi_t.abs().clamp_min(1e-30)).max()) <= 2 ** -8
+            assert float((lo - lo_t).abs().max()) <= float(lo_t.abs().max()) * 2 ** -8
