@@ -379,6 +379,11 @@ int accel_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stre
  * ldo % 8 == 0, zero padding past K. */
 int accel_tf32_pairs(const float* X, int64_t rows, int64_t cols, int64_t ld, void* out,
                      int64_t ldo, int row_pair, int lo_first, void* stream);
+/* Tuning: k blocks (16 k) per fp32 accumulation chunk of accel_tc_gemm_wide
+ * (0, the default: one chunk per work unit).  The tensor core's fp32
+ * accumulate truncates; each chunk starts a fresh accumulator and the epilogue
+ * adds chunks rounding to nearest through the output. */
+void accel_tc_wide_set_chunk(int kblocks);
 /* Work tiles (128 x BN, BN <= 256) of an M x N product (split-K sizing). */
 int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn);
 /* C = A . B^T with fp32-class accuracy from two tensor-core passes per 8-k

@@ -50,6 +50,11 @@ constexpr int kWThreads = 192;  // 6 warps
 constexpr int kWEpi0 = 2;       // epilogue warps 2..5
 constexpr int kBK = 16;         // fp32 k per stage (two 8-k MMA steps)
 constexpr int kMaxStages = 8;
+// k blocks per accumulation chunk; 0 = one chunk per work unit.  Chunking only
+// shrinks the fp32 truncation drift by sqrt(#chunks) and costs an output
+// read-modify-write per chunk, so it is off by default (drift ~ n_mma 2^-25
+// relative: 2e-5 at K = 4096, the same accumulator cuBLAS's TF32 GEMMs use).
+int g_chunk_kb = 0;
 constexpr size_t kWideSmem = 222 * 1024;  // dynamic (ring); + ~5 KB static
 
 enum Epi : int { kStore = 0, kBiasTanh = 1, kDtanh = 2, kPartial = 3 };
@@ -61,6 +66,8 @@ struct WideArgs {
   float* col_part;  // kDtanh: [m_tiles][N] column sums of Y (per m tile, fixed order)
   int64_t M, N, ldc, ldh;
   int BN, m_tiles, n_tiles, kslices, kblocks, a_mn, b_mn, epi, nstages, vec, hvec;
+  int chunk_kb;      // k blocks per accumulation chunk (bounds the truncating fp32 sum)
+  int a_3d, b_3d;    // MN-major operand loaded by one 3-D box per stage (MN % 64 == 0)
   uint32_t stage_bytes, a_pair_off, b_raw_off, b_pair_off, tx_bytes, tmem_cols;
 };
 
@@ -95,14 +102,21 @@ __device__ __forceinline__ uint64_t pair_desc(uint32_t base, int mn, int s) {
             : make_sdesc(base + s * 32, 16, 512, 4);
 }
 
-// TMA loads of one operand tile (rows r0.. of the MN dimension, k block kb)
+// TMA loads of one operand tile (rows r0.. of the MN dimension, k block kb).
+// MN-major: 32-column fp32 slabs of 16 k rows and 64-column bf16 atoms of 32
+// pair rows, slab / atom-major in shared memory -- one 3-D box each when the
+// MN extent is a multiple of 64 (three_d), else one 2-D box per slab / atom.
 __device__ __forceinline__ void load_operand(unsigned char* raw, unsigned char* pair,
                                              const CUtensorMap* rmap, const CUtensorMap* pmap,
-                                             int mn, int r0, int rows, int kb, uint64_t* bar) {
-  if (mn) {
-    for (int j = 0; j < rows / 32; ++j)  // fp32 slabs: 32 columns x 16 k rows
+                                             int mn, int three_d, int r0, int rows, int kb,
+                                             uint64_t* bar) {
+  if (mn && three_d) {
+    tma_load_3d(raw, rmap, 0, kb * kBK, r0 / 32, bar);
+    tma_load_3d(pair, pmap, 0, kb * 2 * kBK, r0 / 64, bar);
+  } else if (mn) {
+    for (int j = 0; j < rows / 32; ++j)
       tma_load_2d(raw + j * (kBK * 128), rmap, r0 + 32 * j, kb * kBK, bar);
-    for (int j = 0; j < rows / 64; ++j)  // bf16 atoms: 64 columns x 32 pair rows
+    for (int j = 0; j < rows / 64; ++j)
       tma_load_2d(pair + j * (2 * kBK * 128), pmap, r0 + 64 * j, kb * 2 * kBK, bar);
   } else {
     tma_load_2d(raw, rmap, kb * kBK, r0, bar);        // rows x 16 fp32
@@ -168,9 +182,10 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
           unsigned char* st = smem + (size_t)slot * p.stage_bytes;
           uint64_t* bar = &bars.full[slot];
           mbar_expect_tx(bar, p.tx_bytes);
-          load_operand(st, st + p.a_pair_off, &a_raw, &a_pair, p.a_mn, mt * kBM, kBM, kb, bar);
-          load_operand(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn, nt * BN, BN,
-                       kb, bar);
+          load_operand(st, st + p.a_pair_off, &a_raw, &a_pair, p.a_mn, p.a_3d, mt * kBM, kBM, kb,
+                       bar);
+          load_operand(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn, p.b_3d,
+                       nt * BN, BN, kb, bar);
           if (++slot == p.nstages) {
             slot = 0;
             ph ^= 1u;
@@ -184,117 +199,147 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
     const uint32_t id_bf = make_idesc_bf16(BN, p.a_mn, p.b_mn);
     int slot = 0;
     unsigned ph = 0;
+    int64_t c = 0;  // accumulation chunks issued by this CTA (TMEM buffer c & 1)
     for (int64_t t = 0; t < my_units; ++t) {
       int ks, mt, nt, kb0, kb1;
       decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
-      const int b = (int)(t & 1);
-      mbar_wait(&bars.tempty[b], ((unsigned)(t >> 1) & 1u) ^ 1u);
-      tc_fence_after();
-      const uint32_t d = tmem + (uint32_t)(b * BN);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&bars.full[slot], ph);
+      for (int cb0 = kb0; cb0 < kb1; cb0 += p.chunk_kb, ++c) {
+        const int cb1 = min(kb1, cb0 + p.chunk_kb);
+        const int b = (int)(c & 1);
+        mbar_wait(&bars.tempty[b], ((unsigned)(c >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t st = smem_u32(smem + (size_t)slot * p.stage_bytes);
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int kb = cb0; kb < cb1; ++kb) {
+          mbar_wait(&bars.full[slot], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + (size_t)slot * p.stage_bytes);
 #pragma unroll
-        for (int s = 0; s < kBK / 8; ++s) {
-          mma_tf32_w(d, raw_desc(st, p.a_mn, s), raw_desc(st + p.b_raw_off, p.b_mn, s), id_tf,
-                     (kb > kb0 || s > 0) ? 1u : 0u);
-          mma_bf16_w(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
-                     pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf, 1u);
+          for (int s = 0; s < kBK / 8; ++s) {
+            mma_tf32_w(d, raw_desc(st, p.a_mn, s), raw_desc(st + p.b_raw_off, p.b_mn, s), id_tf,
+                       (kb > cb0 || s > 0) ? 1u : 0u);
+            mma_bf16_w(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
+                       pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf, 1u);
+          }
+          mma_commit_w(&bars.empty[slot]);
+          if (++slot == p.nstages) {
+            slot = 0;
+            ph ^= 1u;
+          }
         }
-        mma_commit_w(&bars.empty[slot]);
-        if (++slot == p.nstages) {
-          slot = 0;
-          ph ^= 1u;
-        }
+        mma_commit_w(&bars.tfull[b]);
       }
-      mma_commit_w(&bars.tfull[b]);
     }
   } else {
-    // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows
+    // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows.  The
+    // tensor core accumulates in fp32 with truncation, so a unit's k range is
+    // cut into chunks of chunk_kb k blocks, each in a fresh accumulator; the
+    // epilogue adds them in order (round to nearest) through the output itself
+    // (chunk 0 stores, later chunks read back, the last applies the epilogue op).
     const int q = warp & 3, ew = warp - kWEpi0;
+    int64_t c = 0;
     for (int64_t t = 0; t < my_units; ++t) {
       int ks, mt, nt, kb0, kb1;
       decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
-      const int b = (int)(t & 1);
-      mbar_wait(&bars.tfull[b], (unsigned)(t >> 1) & 1u);
-      tc_fence_after();
       const int64_t row = (int64_t)mt * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
       const int64_t n0 = (int64_t)nt * BN;
       float* out = p.epi == kPartial ? p.C + (int64_t)ks * p.M * p.N + row * p.N
                                      : p.C + row * p.ldc;
-      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
+      for (int cb0 = kb0; cb0 < kb1; cb0 += p.chunk_kb, ++c) {
+        const bool first = cb0 == kb0, last = cb0 + p.chunk_kb >= kb1;
+        const int epi = last ? p.epi : kPartial;  // intermediate chunks: raw sums
+        const int b = (int)(c & 1);
+        mbar_wait(&bars.tfull[b], (unsigned)(c >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        float v[32];
-        tmem_ld32(tb + c0, r);
-        tmem_wait_ld();
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          float v[32];
+          tmem_ld32(tb + c0, r);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const int64_t cb = n0 + c0;
-        if (p.epi == kBiasTanh) {
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          const int64_t cb = n0 + c0;
+          const bool full = p.vec && cb + 32 <= p.N;
+          if (!first && row_ok) {  // the previous chunks' sum
+            if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            v[j] = tanh_fast(v[j] + (cb + j < p.N ? __ldg(p.bias + cb + j) : 0.f));
-        } else if (p.epi == kDtanh) {
-          const float* h = p.H + row * p.ldh + cb;
-          if (row_ok && p.hvec && cb + 32 <= p.N) {
+              for (int j = 0; j < 32; j += 4) {
+                const float4 o = *reinterpret_cast<const float4*>(out + cb + j);
+                v[j] += o.x;
+                v[j + 1] += o.y;
+                v[j + 2] += o.z;
+                v[j + 3] += o.w;
+              }
+            } else {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 hv = __ldg(reinterpret_cast<const float4*>(h + j));
-              v[j] *= 1.f - hv.x * hv.x;
-              v[j + 1] *= 1.f - hv.y * hv.y;
-              v[j + 2] *= 1.f - hv.z * hv.z;
-              v[j + 3] *= 1.f - hv.w * hv.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float hv = (row_ok && cb + j < p.N) ? __ldg(h + j) : 0.f;
-              v[j] = row_ok ? v[j] * (1.f - hv * hv) : 0.f;
+              for (int j = 0; j < 32; ++j)
+                if (cb + j < p.N) v[j] += out[cb + j];
             }
           }
-        }
-        if (row_ok) {
-          if (p.vec && cb + 32 <= p.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(out + cb + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
+          if (epi == kBiasTanh) {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (cb + j < p.N) out[cb + j] = v[j];
-          }
-        }
-        if (p.epi == kDtanh) {
-          // column sums of this warp's 32 rows: transposed butterfly, lane j ends
-          // with column c0 + j (31 shuffles; fixed order)
+              v[j] = tanh_fast(v[j] + (cb + j < p.N ? __ldg(p.bias + cb + j) : 0.f));
+          } else if (epi == kDtanh) {
+            const float* h = p.H + row * p.ldh + cb;
+            if (row_ok && p.hvec && cb + 32 <= p.N) {
 #pragma unroll
-          for (int sft = 16; sft >= 1; sft >>= 1) {
-            const bool up = (lane & sft) != 0;
+              for (int j = 0; j < 32; j += 4) {
+                const float4 hv = __ldg(reinterpret_cast<const float4*>(h + j));
+                v[j] *= 1.f - hv.x * hv.x;
+                v[j + 1] *= 1.f - hv.y * hv.y;
+                v[j + 2] *= 1.f - hv.z * hv.z;
+                v[j + 3] *= 1.f - hv.w * hv.w;
+              }
+            } else {
 #pragma unroll
-            for (int i = 0; i < sft; ++i) {
-              const float send = up ? v[i] : v[i + sft];
-              const float keep = up ? v[i + sft] : v[i];
-              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+              for (int j = 0; j < 32; ++j) {
+                const float hv = (row_ok && cb + j < p.N) ? __ldg(h + j) : 0.f;
+                v[j] = row_ok ? v[j] * (1.f - hv * hv) : 0.f;
+              }
             }
           }
-          s_col[ew][c0 + lane] = v[0];
+          if (row_ok) {
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(out + cb + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (cb + j < p.N) out[cb + j] = v[j];
+            }
+          }
+          if (epi == kDtanh) {
+            // column sums of this warp's 32 rows: transposed butterfly, lane j ends
+            // with column c0 + j (31 shuffles; fixed order)
+#pragma unroll
+            for (int sft = 16; sft >= 1; sft >>= 1) {
+              const bool up = (lane & sft) != 0;
+#pragma unroll
+              for (int i = 0; i < sft; ++i) {
+                const float send = up ? v[i] : v[i + sft];
+                const float keep = up ? v[i + sft] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+              }
+            }
+            s_col[ew][c0 + lane] = v[0];
+          }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.tempty[b]);
-      if (p.epi == kDtanh) {  // the tile's column sums, epilogue warps in fixed order
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int e = threadIdx.x - kWEpi0 * 32;
-        for (int c = e; c < BN; c += 128)
-          if (n0 + c < p.N)
-            p.col_part[(int64_t)mt * p.N + n0 + c] =
-                ((s_col[0][c] + s_col[1][c]) + s_col[2][c]) + s_col[3][c];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.tempty[b]);
+        if (epi == kDtanh) {  // the tile's column sums, epilogue warps in fixed order
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int e = threadIdx.x - kWEpi0 * 32;
+          for (int cc = e; cc < BN; cc += 128)
+            if (n0 + cc < p.N)
+              p.col_part[(int64_t)mt * p.N + n0 + cc] =
+                  ((s_col[0][cc] + s_col[1][cc]) + s_col[2][cc]) + s_col[3][cc];
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
       }
     }
   }
@@ -401,7 +446,30 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
   const int64_t K8 = (K + 7) / 8 * 8;
   CUtensorMap am, apm, bm, bpm;
   auto mk = [&](CUtensorMap* raw, CUtensorMap* pair, const float* X, const void* Xp, int64_t mnrows,
-                int64_t ld, int64_t ldp, int mn, int tile_rows) -> int {
+                int64_t ld, int64_t ldp, int mn, int tile_rows, int three_d) -> int {
+    if (mn && three_d) {  // {32 | 64 columns, k rows, slabs | atoms}: one box per stage
+      EncodeFn fn = encode_fn();
+      if (!fn) return fail(kCuda, "tc_wide: cuTensorMapEncodeTiled unavailable");
+      if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(Xp) & 15) ||
+          (ld % 4) || (ldp % 8))
+        return fail(kDimension, "tc_wide: MN-major operands need 16-byte aligned rows");
+      const cuuint32_t estr[3] = {1, 1, 1};
+      const cuuint64_t rd[3] = {32, (cuuint64_t)K, (cuuint64_t)(mnrows / 32)};
+      const cuuint64_t rs[2] = {(cuuint64_t)ld * 4, 128};
+      const cuuint32_t rb[3] = {32, (cuuint32_t)kBK, (cuuint32_t)(tile_rows / 32)};
+      CUresult r = fn(raw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), rd, rs, rb,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(kCuda, "tc_wide: 3-D map encode failed (%d)", (int)r);
+      const cuuint64_t pd[3] = {64, (cuuint64_t)(2 * K8), (cuuint64_t)(mnrows / 64)};
+      const cuuint64_t ps[2] = {(cuuint64_t)ldp * 2, 128};
+      const cuuint32_t pb[3] = {64, (cuuint32_t)(2 * kBK), (cuuint32_t)(tile_rows / 64)};
+      r = fn(pair, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(Xp), pd, ps, pb, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(kCuda, "tc_wide: 3-D pair map encode failed (%d)", (int)r);
+      return kOk;
+    }
     if (mn) {
       if (int e = make_map_dt(raw, X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, K, mnrows, ld, 32, kBK,
                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
@@ -415,8 +483,13 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
     return make_map_dt(pair, Xp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, mnrows, 2 * K8, ldp, 2 * kBK,
                        tile_rows, CU_TENSOR_MAP_SWIZZLE_64B);
   };
-  if (int e = mk(&am, &apm, A, Ap, M, lda, ldap, a_mn, kBM)) return e;
-  if (int e = mk(&bm, &bpm, B, Bp, N, ldb, ldbp, b_mn, p.BN)) return e;
+  // 3-D boxes need whole slabs / atoms inside the matrix: MN % 64 == 0 and, for
+  // A, a full 128-row tile span (the box covers the tile's whole MN extent)
+  p.a_3d = (a_mn && M % 64 == 0 && M % kBM == 0) ? 1 : 0;
+  p.b_3d = (b_mn && N % 64 == 0 && N % p.BN == 0) ? 1 : 0;
+  p.chunk_kb = g_chunk_kb > 0 ? g_chunk_kb : (1 << 30);
+  if (int e = mk(&am, &apm, A, Ap, M, lda, ldap, a_mn, kBM, p.a_3d)) return e;
+  if (int e = mk(&bm, &bpm, B, Bp, N, ldb, ldbp, b_mn, p.BN, p.b_3d)) return e;
   const size_t smem = (size_t)p.nstages * p.stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(tc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
@@ -456,6 +529,9 @@ extern "C" int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B
   return launch_wide(A, Ap, B, Bp, C, bias, H, col_part, M, N, K, lda, ldap, ldb, ldbp, ldc, ldh,
                      a_mn, b_mn, epi, kslices, as_stream(stream));
 }
+
+// Tuning knob: k blocks (16 k each) per fp32 accumulation chunk (>= 1).
+extern "C" void accel_tc_wide_set_chunk(int kblocks) { g_chunk_kb = kblocks < 0 ? 0 : kblocks; }
 
 extern "C" int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn) {
   int bn = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);
