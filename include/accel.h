@@ -398,7 +398,8 @@ int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn);
  *   epi 0: C[M, N] (ldc) = acc;  1: tanh(acc + bias[N]);  2: acc (1 - H^2)
  *      (H pitch ldh) and col_part f32[ceil(M/128)][N] = per-128-row-tile column
  *      sums of C (bias gradient, reduced in fixed order by the caller);
- *   3: split-K, C = f32[kslices][M][N] partial slices (caller reduces). */
+ *   3: split-K, C = f32[kslices][M][N] partial slices (caller reduces),
+ *      kslices <= ceil(K / 16). */
 int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B, const void* Bp, float* C,
                        const float* bias, const float* H, float* col_part, int64_t M, int64_t N,
                        int64_t K, int64_t lda, int64_t ldap, int64_t ldb, int64_t ldbp,

@@ -425,7 +425,7 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
   p.m_tiles = (int)ceil_div(M, kBM);
   p.n_tiles = (int)ceil_div(N, p.BN);
   p.kblocks = (int)ceil_div(K, kBK);
-  p.kslices = std::max(1, std::min(kslices, p.kblocks));
+  p.kslices = kslices;
   p.a_mn = a_mn; p.b_mn = b_mn; p.epi = epi;
   const bool c_al = (reinterpret_cast<uintptr_t>(C) & 15) == 0;
   p.vec = (c_al && (epi == kPartial ? N % 4 == 0 : ldc % 4 == 0)) ? 1 : 0;
@@ -525,6 +525,9 @@ extern "C" int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B
   if (epi == kBiasTanh && !bias) return fail(kDimension, "tc_gemm_wide: bias+tanh needs bias");
   if (epi == kDtanh && (!H || !col_part)) return fail(kDimension, "tc_gemm_wide: dtanh needs H, col_part");
   if (epi != kPartial && kslices != 1) return fail(kDimension, "tc_gemm_wide: split-K needs epi 3");
+  if (kslices > ceil_div(K, kBK))  // every slice owns >= one 16-k block (else its slice is unwritten)
+    return fail(kDimension, "tc_gemm_wide: kslices %d > ceil(K / 16) = %lld", kslices,
+                (long long)ceil_div(K, kBK));
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return fail(kDimension, "tc_gemm_wide: too large");
   return launch_wide(A, Ap, B, Bp, C, bias, H, col_part, M, N, K, lda, ldap, ldb, ldbp, ldc, ldh,
                      a_mn, b_mn, epi, kslices, as_stream(stream));

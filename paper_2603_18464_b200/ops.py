@@ -511,7 +511,7 @@ def _wide_rows(x, b, out, b_mn: bool, bias=None, tanh=False):
         if bias is None:
             raise DimensionError("tanh epilogue needs the bias")
         return wide_gemm(x, b, out, a_mn=False, b_mn=b_mn, epi=1, bias=bias, tag="rows")
-    ks = max(1, sms // tiles) if tiles < sms // 2 and out.is_contiguous() else 1
+    ks = _wide_split(tiles, x.shape[1]) if tiles < sms // 2 and out.is_contiguous() else 1
     if ks > 1:
         part = workspace("wide_part").get(4 * ks * M * N)[:4 * ks * M * N].view(F32)
         wide_gemm(x, b, part, a_mn=False, b_mn=b_mn, epi=3, kslices=ks, tag="rows")
@@ -607,11 +607,15 @@ def tc_sm_count() -> int:
     return int(_lib.lib().accel_tc_sm_count())
 
 
-def wide_kslices(n: int, k: int) -> int:
-    """k slices of a wide weight gradient dW[n, k] (reduction over the rows):
-    enough work units to fill the SMs."""
-    tiles = wide_tiles(n, k, True)
-    return max(1, tc_sm_count() // tiles)
+def _wide_split(tiles: int, K: int) -> int:
+    """Split-K slices filling the SMs, at most one per 16-k block (the kernel
+    gives every slice at least one block)."""
+    return max(1, min(tc_sm_count() // max(tiles, 1), -(-int(K) // 16)))
+
+
+def wide_kslices(n: int, k: int, rows: int) -> int:
+    """k slices of a wide weight gradient dW[n, k] = dy[rows, n]^T x[rows, k]."""
+    return _wide_split(wide_tiles(n, k, True), rows)
 
 
 def tc_wgrad(dy, x, out, kslices=None, partial=None):
@@ -621,7 +625,7 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     F, n = dy.shape
     k = x.shape[1]
     if n > 256 or k > 256:
-        ks = wide_kslices(n, k)
+        ks = wide_kslices(n, k, F)
         part = torch.empty(ks, n, k, dtype=F32, device=dy.device)
         wide_gemm(dy, x, part, a_mn=True, b_mn=True, epi=3, kslices=ks, tag="wgrad")
         reduce_segments([(part, out, ks, n * k, n * k)])

@@ -704,7 +704,7 @@ class Trainer:
         F, n = dy.shape
         k = x.shape[1]
         if n > 256 or k > 256:  # wide layers (cfg4): streamed tcgen05 GEMM, split-K slices
-            ks = ops.wide_kslices(n, k)
+            ks = ops.wide_kslices(n, k, F)
             part = self.scratch.get("wg." + tag, (ks + extra, n, k))
             ops.wide_gemm(dy, x, part, a_mn=True, b_mn=True, epi=3, kslices=ks, tag="wgrad")
             return (part, out, ks + extra, n * k, n * k)
