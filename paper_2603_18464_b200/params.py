@@ -54,22 +54,38 @@ class Dims:
                    vc.mlp_hidden)
 
 
+# Gradient buckets in flat order (ZeRO-2 reduce-scatter units), each complete
+# at a distinct point of the backward: the value head first, then the head
+# (e_prev, e_pos, w_head, b_head), then layer 1, then layer 0.
+BUCKETS = (("w0", "b0"), ("w1", "b1"), ("e_prev", "e_pos", "w_head", "b_head"), VALUE_NAMES)
+
+
 class FlatLayout:
     def __init__(self, dims: Dims, pad_to: int = 4) -> None:
-        """pad_to: the total is rounded up to a multiple of it (4 * world for
-        ZeRO-2 so every rank's shard is equal and 16-byte aligned)."""
+        """pad_to: every bucket (BUCKETS) is padded to a multiple of it -- 4 *
+        world under ZeRO-2, so each rank's slice of each bucket is equal and
+        16-byte aligned (the reduce-scatter / all-gather unit)."""
         self.dims = dims
+        self.pad_to = int(pad_to)
         shapes = dims.shapes()
         self.offsets, self.shapes = {}, {}
+        self.buckets = []  # (lo, hi, is_policy)
         off = 0
-        for name in POLICY_NAMES + VALUE_NAMES:
-            if name == VALUE_NAMES[0]:
+        for names in BUCKETS:
+            lo = off
+            if names is VALUE_NAMES:
                 self.n_policy = off
-            n = int(np.prod(shapes[name]))
-            self.offsets[name] = off
-            self.shapes[name] = shapes[name]
-            off += (n + 3) // 4 * 4
-        self.total = (off + pad_to - 1) // pad_to * pad_to
+            for name in names:
+                n = int(np.prod(shapes[name]))
+                self.offsets[name] = off
+                self.shapes[name] = shapes[name]
+                off += (n + 3) // 4 * 4
+            off = (off + self.pad_to - 1) // self.pad_to * self.pad_to
+            self.buckets.append((lo, off, names is not VALUE_NAMES))
+        self.total = off
+
+    def bucket_of(self, name: str) -> int:
+        return next(i for i, names in enumerate(BUCKETS) if name in names)
 
     def views(self, buf: torch.Tensor) -> dict:
         out = {}
@@ -93,18 +109,40 @@ class FlatLayout:
 
 
 class DeviceParams:
-    """Ping-pong parameter / moment buffers plus one gradient buffer."""
+    """Ping-pong parameter / moment buffers plus one gradient buffer.
 
-    def __init__(self, layout: FlatLayout, device) -> None:
+    shard = (rank, world) (ZeRO-2): the Adam moments exist only for this
+    rank's slice of every bucket, stored back to back in bucket order
+    (`shard_slices`); parameters and gradients stay full (the forward and
+    backward need all parameters; the gradients are reduce-scattered)."""
+
+    def __init__(self, layout: FlatLayout, device, shard=None) -> None:
         self.layout = layout
-        z = lambda: torch.zeros(layout.total, dtype=torch.float32, device=device)
-        self.p = [z(), z()]
-        self.m = [z(), z()]
-        self.v = [z(), z()]
-        self.g = z()
+        self.rank, self.world = shard if shard is not None else (0, 1)
+        z = lambda n: torch.zeros(n, dtype=torch.float32, device=device)
+        self.p = [z(layout.total), z(layout.total)]
+        n_mom = layout.total // self.world
+        self.m = [z(n_mom), z(n_mom)]
+        self.v = [z(n_mom), z(n_mom)]
+        self.g = z(layout.total)
         self.cur = 0
+        self.generation = 0  # bumps on every flip (moments snapshots are tagged with it)
+        self._moments_host = None
         self._views = [layout.views(self.p[0]), layout.views(self.p[1])]
         self.gv = layout.views(self.g)
+
+    @property
+    def sharded(self) -> bool:
+        return self.world > 1
+
+    def shard_slices(self) -> list:
+        """Per bucket: (flat lo, flat hi, shard offset, is_policy) of this rank's slice."""
+        out, s_off = [], 0
+        for lo, hi, pol in self.layout.buckets:
+            per = (hi - lo) // self.world
+            out.append((lo + self.rank * per, lo + (self.rank + 1) * per, s_off, pol))
+            s_off += per
+        return out
 
     @property
     def pv(self) -> dict:
@@ -112,6 +150,7 @@ class DeviceParams:
 
     def flip(self) -> None:
         self.cur ^= 1
+        self.generation += 1
 
     def load(self, policy_tensors: dict, value_tensors: dict) -> None:
         host = np.zeros(self.layout.total, dtype=np.float32)
@@ -133,7 +172,22 @@ class DeviceParams:
         return self._split(self.p[self.cur].cpu().numpy())
 
     def moments_to_host(self) -> tuple:
-        return self._split(self.m[self.cur].cpu().numpy()), self._split(self.v[self.cur].cpu().numpy())
+        """({policy m}, {value m}), ({policy v}, {value v}) in float64.  Under
+        ZeRO-2 the moments are sharded: only a snapshot assembled by the
+        collective `Trainer.gather_moments()` at the current generation is
+        returned (a stale or missing one raises instead of mixing shards)."""
+        if not self.sharded:
+            return (self._split(self.m[self.cur].cpu().numpy()),
+                    self._split(self.v[self.cur].cpu().numpy()))
+        if self._moments_host is None or self._moments_host[0] != self.generation:
+            from .errors import AccelError
+            raise AccelError("Adam moments are sharded across data-parallel ranks: call the "
+                             "collective Trainer.gather_moments() on every rank first")
+        m, v = self._moments_host[1]
+        return self._split(m), self._split(v)
+
+    def set_gathered_moments(self, m_full: np.ndarray, v_full: np.ndarray) -> None:
+        self._moments_host = (self.generation, (m_full, v_full))
 
     def grads_to_host(self) -> tuple:
         return self._split(self.g.cpu().numpy())

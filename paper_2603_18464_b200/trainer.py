@@ -350,7 +350,8 @@ class Trainer:
         self._bundle = bundle
         self.dims = Dims.from_models(bundle.policy, bundle.value)
         self.layout = FlatLayout(self.dims, pad_to=4 * (comm.world if comm is not None else 1))
-        self.params = DeviceParams(self.layout, self.device)
+        self.params = DeviceParams(self.layout, self.device,
+                                   shard=(comm.rank, comm.world) if comm is not None else None)
         self.params.load(bundle.policy.params.tensors, bundle.value.params.tensors)
         self._policy_version = int(getattr(bundle.policy.params, "version", 0))
         self._value_version = int(getattr(bundle.value.params, "version", 0))
@@ -385,7 +386,8 @@ class Trainer:
 
     def gather_moments(self) -> None:
         """Collective under data parallelism: assemble the sharded Adam moments
-        so `adam_policy.m` / `.v` show the full state (a no-op on one GPU)."""
+        (ZeRO-2 keeps only this rank's slices) so `adam_policy.m` / `.v` show
+        the full state at the current generation (a no-op on one GPU)."""
         if self.comm is not None:
             self.comm.gather_moments(self.params)
 
@@ -649,11 +651,14 @@ class Trainer:
         batch.boot_rows = b["traj_off"][1:] + torch.arange(n, dtype=torch.int64, device=dev)
         if cfg.loss.value_clip is not None:  # rollout-time V per transition
             batch.v_old = b["values"].index_select(0, frame_of)
-        host_dev = torch.cat([flags, cnt.double()])
+        lags = self.publish_version - np.asarray(behavior_version, dtype=np.int64)
+        counts = torch.tensor([float(n_real), float(n), float(lags.sum())], dtype=F64, device=dev)
+        host_dev = torch.cat([flags, cnt.double(), counts])
         if self.comm is not None:
             # data parallel: the batch is one shard of the global batch; every
-            # accept/reject decision and the count are global (all ranks agree)
-            idx = torch.tensor([3, 8, 9, 10, 11, 16, 17], device=dev)
+            # accept/reject decision, the transition count and the record's
+            # trajectory counts / behavior lag are global (all ranks agree)
+            idx = torch.tensor([3, 8, 9, 10, 11, 16, 17, 20, 21, 22], device=dev)
             dec = host_dev.index_select(0, idx)
             self.comm.all_reduce_sum(dec)
             host_dev.index_copy_(0, idx, dec)
@@ -674,6 +679,10 @@ class Trainer:
         batch.norm_mean, batch.norm_std = float(host[4]), float(host[5])
         batch.norm_count = int(host[2])
         batch.global_n = int(host[2])
+        if self.comm is not None:  # the global batch's record fields (trainer.py:385-403)
+            batch.n_real, batch.n_imagined = int(host[20]), int(host[21] - host[20])
+            batch.behavior_lag_mean = float(host[22] / host[21])
+            batch.shard_sizes = _array_split_sizes(int(host[2]), cfg.k_shards)
         finite = host[3] == 0 and host[16] == 0
         batch._finite = bool(finite)
         return batch if finite else None
@@ -714,6 +723,10 @@ class Trainer:
         _lib.call("accel_tc_gemm", ops._p(dy), ops._p(x), ops._p(part), None, n, F, k,
                   dy.stride(0), x.stride(0), k, 1, 1, 0, 0, ks, ops._stream())
         return (part, out, 2 * ks + extra, n * k, n * k)
+
+    def _bucket_done(self, tensor_name: str) -> None:
+        if self.comm is not None:
+            self.comm.bucket_ready(self.layout.bucket_of(tensor_name))
 
     def _allreduce_sum(self, t):
         return self.comm.all_reduce_sum(t) if self.comm is not None else t
@@ -826,6 +839,17 @@ class Trainer:
                            algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None,
                            dbias_part, None, None, fix_stats=loss_sums)
 
+        # ZeRO-2: each gradient bucket is reduce-scattered, updated (Adam on this
+        # rank's slice, speculative: the host adopts generation nxt only if the
+        # record accepts the step) and all-gathered as soon as the backward has
+        # written it, on a side stream (dp.DataParallel)
+        t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
+        hyp = (self.adam_policy.hyper(t_pol), self.adam_value.hyper(t_val))
+        adam_bad = cnt[2:3]
+        if self.comm is not None:
+            self.comm.begin_step(self.params, hyp, S.get("st.noskip", (1,), torch.int32).zero_(),
+                                 adam_bad, adam_fn=ops.adam)
+
         # value head (hiddens detached)
         vclip = {}
         if lc.value_clip is not None:
@@ -862,7 +886,7 @@ class Trainer:
                            vpart, vdpart, gw, **vclip)
             R, row_frame, step_group = N, batch.frame_of, batch.step_group
             ga = gw
-        segs = [self._wgrad(zm, U, G["w0v"], "w0v")]  # dzm^T U
+        w0v_seg = self._wgrad(zm, U, G["w0v"], "w0v")  # dzm^T U
         dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (R, D)))
         de = S.get("st.de", (R, 2))
         battn_part = S.get("st.battn", (ga,))
@@ -871,6 +895,16 @@ class Trainer:
         wattn_part = S.get("st.wattn", (gr, D))
         ops.value_attn_wgrad(de, h1, h2, row_frame, R, wattn_part, gr)
         step_group.rows_sum(dU, G["e_step"])
+        # the value bucket is complete: its ZeRO-2 exchange starts now (dp)
+        ops.reduce_segments([
+            w0v_seg,
+            (vpart, G["w1v"], gw, H, 2 * H + 1),
+            (vpart[:, H:], G["b0v"], gw, H, 2 * H + 1),
+            (vpart[:, 2 * H:], G["b1v"], gw, 1, 2 * H + 1),
+            (battn_part, G["b_attn"], ga, 1, 1),
+            (wattn_part, G["w_attn"], gr, D, D),
+        ])
+        self._bucket_done("w_attn")
 
         # policy backward
         if fact:
@@ -891,16 +925,16 @@ class Trainer:
             small = seg[0][seg[2] - 1]
             torch.mm(dprev.t(), P["e_prev"], out=small)
             small.addmm_(dpos.t(), P["e_pos"])
-            segs.append(seg)
             _mm(dprev, P["w_head"], G["e_prev"])
             _mm(dpos, P["w_head"], G["e_pos"])
+            ops.reduce_segments([seg, (dpos, G["b_head"], K, A, A)])
+            self._bucket_done("w_head")
             # dpre2 = (G W_head) (1 - h2^2) and its column sums (db1), one kernel
             dz2, db1_part, gd = ops.tc_matmul_nn_dtanh(
                 g_frame, P["w_head"], h2, S.get("st.dz2", (F, D)),
                 lambda n: S.get("st.db1", (n, D)))
-            segs.append((dpos, G["b_head"], K, A, A))
         else:
-            segs.append(self._wgrad(dlogits, c, G["w_head"], "w_head"))
+            seg = self._wgrad(dlogits, c, G["w_head"], "w_head")
             dc = ops.tc_matmul_nn(dlogits, P["w_head"], c)  # c is dead after dW_head: reuse it
             dz2 = S.get("st.dz2", (F, D))
             if F != N:
@@ -910,22 +944,17 @@ class Trainer:
             db1_part = S.get("st.db1", (gd, D))
             ops.dc_reduce(dc, h2, batch.frame_of, N, K, D, dz2, pos_part, db1_part, gd)
             batch.prev_group.rows_sum(dc, G["e_prev"])
-            segs += [(dbias_part, G["b_head"], gl, A, A), (pos_part, G["e_pos"], gd, K * D, K * D)]
-        segs.append(self._wgrad(dz2, h1, G["w1"], "w1"))
+            ops.reduce_segments([seg, (dbias_part, G["b_head"], gl, A, A),
+                                 (pos_part, G["e_pos"], gd, K * D, K * D)])
+            self._bucket_done("w_head")
+        ops.reduce_segments([self._wgrad(dz2, h1, G["w1"], "w1"), (db1_part, G["b1"], gd, D, D)])
+        self._bucket_done("w1")
         # dpre1 = (dpre2 W1) (1 - h1^2) and its column sums (db0)
         dh1, db0_part, gt = ops.tc_matmul_nn_dtanh(dz2, P["w1"], h1, S.get("st.dh1", (F, D)),
                                                    lambda n: S.get("st.db0", (n, D)))
-        segs.append(self._wgrad(dh1, batch.frames, G["w0"], "w0"))
-
-        ops.reduce_segments(segs + [
-            (db1_part, G["b1"], gd, D, D),
-            (db0_part, G["b0"], gt, D, D),
-            (vpart, G["w1v"], gw, H, 2 * H + 1),
-            (vpart[:, H:], G["b0v"], gw, H, 2 * H + 1),
-            (vpart[:, 2 * H:], G["b1v"], gw, 1, 2 * H + 1),
-            (battn_part, G["b_attn"], ga, 1, 1),
-            (wattn_part, G["w_attn"], gr, D, D),
-        ])
+        ops.reduce_segments([self._wgrad(dh1, batch.frames, G["w0"], "w0"),
+                             (db0_part, G["b0"], gt, D, D)])
+        self._bucket_done("w0")
         value_sums = S.get("st.vsum", (2,), F64)
         attn_bad = S.get("st.abad", (2,), F64)
         ops.reduce_f64(vdpart, gw, 2, 0, value_sums)
@@ -945,14 +974,9 @@ class Trainer:
                           lc.lambda_h, M_glob, N_glob, record, skip)
 
         # Adam on both groups (ping-pong; no-op when skip)
-        t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
-        hyp = (self.adam_policy.hyper(t_pol), self.adam_value.hyper(t_val))
         cur, nxt = self.params.cur, self.params.cur ^ 1
-        adam_bad = cnt[2:3]
         if self.comm is not None:
-            # ZeRO-2: reduce-scatter grads, Adam on this rank's shard, all-gather
-            self.comm.adam(self.params, self.layout.n_policy, hyp, skip, adam_bad,
-                           adam_fn=ops.adam)
+            self.comm.finish_step()  # the last buckets' exchange; the stream waits for it
             ops.count_nonfinite(self.params.p[nxt], adam_bad)
         else:
             ops.adam(self.params.p[cur], self.params.g, self.params.m[cur], self.params.v[cur],

@@ -40,34 +40,49 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
     rng = np.random.default_rng(21)
     lens = rng.integers(1, 60, size=24)
-    trajs = synthetic_trajectories(rng, lens, rng.random(24) < 0.5, 7, 256, 40)
     a, b = partition_trajectories(lens, world, rank)
     dp_tr = Trainer(bundle(), TrainerConfig(), comm=DataParallel())
     ref_tr = Trainer(bundle(), TrainerConfig()) if rank == 0 else None
     ok = True
-    for step in range(2):
+    for step in range(3):
+        # imagined trajectories and a behavior lag make the record's counts non-trivial
+        trajs = synthetic_trajectories(np.random.default_rng(100 + step), lens,
+                                       np.arange(24) % 3 == 0, 7, 256, 40, imagined_every=3,
+                                       behavior_version=max(0, step - 1))
         rec = dp_tr.train_step(dp_tr.build_train_batch(trajs[a:b]))
         if rank == 0:
             ref = ref_tr.train_step(ref_tr.build_train_batch(trajs))
             for k, v in ref.items():
                 if isinstance(v, float):
                     good = abs(rec[k] - v) <= 1e-5 * max(1.0, abs(v))
-                elif k in ("n_real", "n_imagined"):
-                    good = True  # per-rank counts (the reference counts the whole batch)
-                else:
+                else:  # n_real, n_imagined, versions, excluded tokens: exact, global
                     good = rec[k] == v
                 if not good:
                     print(f"step {step} record {k}: dp {rec[k]} vs single {v}")
                     ok = False
-            p_dp = dp_tr.params.p[dp_tr.params.cur][:dp_tr.layout.total].cpu()
-            p_ref = ref_tr.params.p[ref_tr.params.cur].cpu()
-            n = min(p_dp.numel(), p_ref.numel())
-            diff = (p_dp[:n] - p_ref[:n]).abs()
-            frac_exact = float((diff <= 1e-6).double().mean())
-            print(f"step {step}: max|dp-single| {float(diff.max()):.3g}, "
+            pd, vd = dp_tr.params.to_host()
+            pr, vr = ref_tr.params.to_host()
+            diffs = np.concatenate([np.abs(x[k] - y[k]).ravel() for x, y in ((pd, pr), (vd, vr))
+                                    for k in y])
+            frac_exact = float(np.mean(diffs <= 1e-6))
+            print(f"step {step}: max|dp-single| {diffs.max():.3g}, "
                   f"fraction within 1e-6: {frac_exact:.5f}")
-            if float(diff.max()) > 2 * 3e-4 + 1e-6 or frac_exact < 0.99:
+            if diffs.max() > 2 * 3e-4 + 1e-6 or frac_exact < 0.99:
                 ok = False
+    # ZeRO-2 moments: sharded on the step path, assembled by the collective gather
+    dp_tr.gather_moments()
+    if rank == 0:
+        for mine, want in zip(dp_tr.params.moments_to_host(), ref_tr.params.moments_to_host()):
+            for grp_m, grp_w in zip(mine, want):
+                for k in grp_w:
+                    err = float(np.max(np.abs(grp_m[k] - grp_w[k])))
+                    scale = float(np.max(np.abs(grp_w[k]))) + 1e-30
+                    if err > 1e-3 * scale + 1e-9:
+                        print(f"moment {k}: {err:.3g} vs scale {scale:.3g}")
+                        ok = False
+        n_mom = dp_tr.params.m[0].numel()
+        print(f"moments per rank: {n_mom} of {dp_tr.layout.total}")
+        ok = ok and n_mom * world == dp_tr.layout.total
     flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if rank == 0:

@@ -80,14 +80,22 @@ def _run_gloo(target, world: int, attempts: int = 3) -> dict:
     raise AssertionError(f"gloo ranks failed after {attempts} attempts: {last}")
 
 
-class _Params:
-    def __init__(self, total, seed):
-        gen = torch.Generator().manual_seed(seed)
-        self.p = [torch.randn(total, generator=gen), torch.zeros(total)]
-        self.m = [torch.randn(total, generator=gen).abs() * 1e-3, torch.zeros(total)]
-        self.v = [torch.rand(total, generator=gen) * 1e-4, torch.zeros(total)]
-        self.g = torch.zeros(total)
-        self.cur = 0
+def _layout(world):
+    from paper_2603_18464_b200.params import Dims, FlatLayout
+    return FlatLayout(Dims(obs_dim=5, hidden=3, chunk_len=2, n_actions=3, n_steps=4,
+                           mlp_hidden=2), pad_to=4 * world)
+
+
+def _init_params(params, seed):
+    gen = torch.Generator().manual_seed(seed)
+    total = params.layout.total
+    params.p[0].copy_(torch.randn(total, generator=gen))
+    m0 = torch.randn(total, generator=gen).abs() * 1e-3
+    v0 = torch.rand(total, generator=gen) * 1e-4
+    return m0, v0
+
+
+HYP = ((3e-4, 0.9, 0.999, 1e-8, 1 - 0.9, 1 - 0.999), (1e-3, 0.8, 0.99, 1e-8, 1 - 0.8, 1 - 0.99))
 
 
 def _worker(rank, world, port, out_q):
@@ -95,19 +103,31 @@ def _worker(rank, world, port, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2603_18464_b200.dp import DataParallel
+        from paper_2603_18464_b200.params import DeviceParams
         dp = DataParallel(adam_fn=torch_adam)
-        total, n_policy = 40, 22  # padded to a multiple of 4 * world
-        params = _Params(total, seed=5)
-        grads = [torch.randn(total, generator=torch.Generator().manual_seed(100 + r))
+        layout = _layout(world)
+        params = DeviceParams(layout, "cpu", shard=(rank, world))
+        m0, v0 = _init_params(params, seed=5)
+        for (s_lo, s_hi, s_off, _) in params.shard_slices():  # this rank's moment slices
+            params.m[0][s_off:s_off + s_hi - s_lo] = m0[s_lo:s_hi]
+            params.v[0][s_off:s_off + s_hi - s_lo] = v0[s_lo:s_hi]
+        grads = [torch.randn(layout.total, generator=torch.Generator().manual_seed(100 + r))
                  for r in range(world)]
         params.g.copy_(grads[rank])
-        hyp = ((3e-4, 0.9, 0.999, 1e-8, 1 - 0.9, 1 - 0.999),
-               (1e-3, 0.8, 0.99, 1e-8, 1 - 0.8, 1 - 0.99))
         skip = torch.zeros(1, dtype=torch.int32)
         bad = torch.zeros(1, dtype=torch.int32)
-        dp.adam(params, n_policy, hyp, skip, bad)
-        params.cur = 1  # the trainer flips to the new generation
-        dp.gather_moments(params)  # moments stay sharded on the step path
+        dp.begin_step(params, HYP, skip, bad)
+        for b in (3, 2, 1, 0):  # buckets in backward order, as the trainer fires them
+            dp.bucket_ready(b)
+        dp.finish_step()
+        params.flip()  # the trainer adopts the new generation
+        try:
+            params.moments_to_host()
+            stale_raised = False
+        except Exception:
+            stale_raised = True
+        dp.gather_moments(params)
+        mp_, vp_ = params.moments_to_host()
         # C1: pooled statistics from per-rank sums
         x = torch.arange(10, dtype=torch.float64) * (rank + 1)
         sums = torch.tensor([x.sum().item(), (x * x).sum().item(), float(x.numel())],
@@ -115,35 +135,44 @@ def _worker(rank, world, port, out_q):
         dp.all_reduce_sum(sums)
         mx = torch.tensor([float(rank)], dtype=torch.float64)
         dp.all_reduce_max(mx)
-        out_q.put((rank, params.p[1].clone(), sums, mx, dp.shard_bounds(total),
-                   dp.global_counts(7 + rank, 3), params.m[1].clone(), params.v[1].clone()))
+        out_q.put((rank, params.p[1].clone(), sums, mx, dp.global_counts(7 + rank, 3),
+                   params._moments_host[1][0].copy(), params._moments_host[1][1].copy(),
+                   params.m[1].numel(), stale_raised))
     finally:
         dist.destroy_process_group()
 
 
 def test_zero2_adam_and_collectives_gloo():
+    """Bucketed ZeRO-2 on 2 gloo ranks == one Adam over the summed gradients;
+    moments are held only for each rank's slices and are readable only after
+    the collective gather at the current generation."""
+    from paper_2603_18464_b200.params import DeviceParams
     world = 2
     res = _run_gloo(_worker, world)
-    # single-process reference: full Adam on the summed gradients
-    total, n_policy = 40, 22
-    ref = _Params(total, seed=5)
-    g_sum = sum(torch.randn(total, generator=torch.Generator().manual_seed(100 + r))
+    layout = _layout(world)
+    ref = DeviceParams(layout, "cpu")
+    m0, v0 = _init_params(ref, seed=5)
+    ref.m[0].copy_(m0)
+    ref.v[0].copy_(v0)
+    g_sum = sum(torch.randn(layout.total, generator=torch.Generator().manual_seed(100 + r))
                 for r in range(world))
-    hyp = ((3e-4, 0.9, 0.999, 1e-8, 1 - 0.9, 1 - 0.999),
-           (1e-3, 0.8, 0.99, 1e-8, 1 - 0.8, 1 - 0.99))
-    torch_adam(ref.p[0], g_sum, ref.m[0], ref.v[0], ref.p[1], ref.m[1], ref.v[1], n_policy,
-               hyp[0], hyp[1], torch.zeros(1, dtype=torch.int32), None)
+    torch_adam(ref.p[0], g_sum, ref.m[0], ref.v[0], ref.p[1], ref.m[1], ref.v[1], layout.n_policy,
+               HYP[0], HYP[1], torch.zeros(1, dtype=torch.int32), None)
     for r in range(world):
         torch.testing.assert_close(res[r][0], ref.p[1], rtol=0, atol=1e-7)
-        torch.testing.assert_close(res[r][5], ref.m[1], rtol=0, atol=1e-7)
-        torch.testing.assert_close(res[r][6], ref.v[1], rtol=0, atol=1e-9)
+        torch.testing.assert_close(torch.from_numpy(res[r][4]), ref.m[1], rtol=0, atol=1e-7)
+        torch.testing.assert_close(torch.from_numpy(res[r][5]), ref.v[1], rtol=0, atol=1e-9)
+        assert res[r][6] == layout.total // world  # moments: this rank's slices only
+        assert res[r][7]  # reading unsharded moments without the gather raises
         xs = [torch.arange(10, dtype=torch.float64) * (q_ + 1) for q_ in range(world)]
         allx = torch.cat(xs)
         assert res[r][1].tolist() == pytest.approx([allx.sum().item(), (allx * allx).sum().item(),
                                                     20.0])
         assert res[r][2].item() == world - 1
-        assert res[r][4] == (7 + 8, (7 + 8) * 3)
-    assert res[0][3] == (0, 20) and res[1][3] == (20, 40)
+        assert res[r][3] == (7 + 8, (7 + 8) * 3)
+    # every bucket is a whole number of 16-byte rank slices
+    for lo, hi, _ in layout.buckets:
+        assert (hi - lo) % (4 * world) == 0
 
 
 def test_partition_trajectories_is_contiguous_and_balanced():
