@@ -47,6 +47,7 @@ class DataParallel:
         self._stream = None
         self._g_shard = None
         self._step = None
+        self.timeline = None  # list -> (bucket, ready, start, end) CUDA events per bucket
 
     # -- small collectives ----------------------------------------------------------
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
@@ -139,11 +140,18 @@ class DataParallel:
         if not self.overlap:
             self._bucket(b)
             return
-        ev = torch.cuda.Event()
+        timed = self.timeline is not None
+        ev = torch.cuda.Event(enable_timing=timed)
         ev.record()
         with torch.cuda.stream(self._stream):
             self._stream.wait_event(ev)
+            if timed:
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record()
             self._bucket(b)
+            if timed:
+                t1.record()
+                self.timeline.append((b, ev, t0, t1))
 
     def finish_step(self) -> None:
         """Every bucket exchanged; the current stream waits for the side stream."""
