@@ -331,6 +331,12 @@ int accel_adam(const float* p_in, const float* g, const float* m_in, const float
                float* p_out, float* m_out, float* v_out, int64_t n, int64_t n0,
                const double* group0, const double* group1, const int* skip,
                unsigned* bad, void* stream);
+/* accel_adam with hyper f64[12] = {group 0, group 1} x {lr, beta1, beta2, eps,
+ * 1 - beta1^t, 1 - beta2^t} in DEVICE memory, read at run time (CUDA-graph
+ * replays of successive steps; the host refreshes hyper before each). */
+int accel_adam_dev(const float* p_in, const float* g, const float* m_in, const float* v_in,
+                   float* p_out, float* m_out, float* v_out, int64_t n, int64_t n0,
+                   const double* hyper, const int* skip, unsigned* bad, void* stream);
 
 /* Batched inference-service evaluation (inference.py:129-160, run_batch): one
  * warp per request, all of one kind; weights / dims as accel_imagine (unused

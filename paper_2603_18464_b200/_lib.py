@@ -86,6 +86,7 @@ _SIGNATURES = {
                                     c_double, P, P, P]),
     "accel_count_nonfinite": (c_int, [P, c_int64, P, P]),
     "accel_adam": (c_int, [P, P, P, P, P, P, P, c_int64, c_int64, P, P, P, P, P]),
+    "accel_adam_dev": (c_int, [P, P, P, P, P, P, P, c_int64, c_int64, P, P, P, P]),
     "accel_tc_sm_count": (c_int, []),
     "accel_tc_gemm_wide": (c_int, [P, P, P, P, P, P, P, P, c_int64, c_int64, c_int64, c_int64,
                                    c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_int,

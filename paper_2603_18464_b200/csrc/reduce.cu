@@ -197,9 +197,13 @@ __global__ void adam_kernel(const float* __restrict__ p_in, const float* __restr
                             const float* __restrict__ m_in, const float* __restrict__ v_in,
                             float* __restrict__ p_out, float* __restrict__ m_out,
                             float* __restrict__ v_out, int64_t n, int64_t n0, AdamGroup g0,
-                            AdamGroup g1, const int* __restrict__ skip,
-                            unsigned* __restrict__ bad) {
+                            AdamGroup g1, const double* __restrict__ hyper,
+                            const int* __restrict__ skip, unsigned* __restrict__ bad) {
   if (*skip) return;
+  if (hyper) {  // {group 0, group 1} from device memory (graph-replayable steps)
+    g0 = AdamGroup{hyper[0], hyper[1], hyper[2], hyper[3], hyper[4], hyper[5]};
+    g1 = AdamGroup{hyper[6], hyper[7], hyper[8], hyper[9], hyper[10], hyper[11]};
+  }
   unsigned nb = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -303,7 +307,23 @@ extern "C" int accel_adam(const float* p_in, const float* g, const float* m_in, 
   if (n == 0) return kOk;
   const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 4);
   adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(p_in, g, m_in, v_in, p_out, m_out, v_out, n,
-                                                   n0, a, b, skip, bad);
+                                                   n0, a, b, nullptr, skip, bad);
+  return post_launch("adam_kernel");
+}
+
+// accel_adam with the two groups' {lr, beta1, beta2, eps, 1 - beta1^t, 1 - beta2^t}
+// read from DEVICE memory (hyper f64[12]) at run time, so a captured CUDA graph
+// replays successive optimizer steps (the host refreshes hyper before each replay).
+extern "C" int accel_adam_dev(const float* p_in, const float* g, const float* m_in,
+                              const float* v_in, float* p_out, float* m_out, float* v_out,
+                              int64_t n, int64_t n0, const double* hyper, const int* skip,
+                              unsigned* bad, void* stream) {
+  if (n < 0 || n0 < 0 || n0 > n) return fail(kDimension, "adam: bad sizes");
+  if (!hyper || !skip || !bad) return fail(kDimension, "adam: NULL buffer");
+  if (n == 0) return kOk;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 4);
+  adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(p_in, g, m_in, v_in, p_out, m_out, v_out, n,
+                                                   n0, AdamGroup{}, AdamGroup{}, hyper, skip, bad);
   return post_launch("adam_kernel");
 }
 

@@ -102,8 +102,10 @@ class DataParallel:
     # -- the bucketed ZeRO-2 update -----------------------------------------------------
     def begin_step(self, params, hyp: tuple, skip, bad, adam_fn=None) -> None:
         """Arm the per-bucket exchange of one optimizer step (generation
-        params.cur -> cur ^ 1).  skip: device int (Adam does nothing when set);
-        bad: device counter of non-finite new parameters."""
+        params.cur -> cur ^ 1).  hyp: the Adam hyperparameters handed to
+        adam_fn(p_in, g, m_in, v_in, p_out, m_out, v_out, n_policy, hyp, skip,
+        bad) (ops.adam_dev: a device f64[12]); skip: device int (Adam does
+        nothing when set); bad: device counter of non-finite new parameters."""
         if params.world != self.world or params.rank != self.rank:
             raise ValueError("DeviceParams shard does not match the communicator")
         n_shard = params.layout.total // self.world
@@ -126,7 +128,7 @@ class DataParallel:
         ms = slice(s_off, s_off + per)
         fn(params.p[cur][s_lo:s_hi], g, params.m[cur][ms], params.v[cur][ms],
            params.p[nxt][s_lo:s_hi], params.m[nxt][ms], params.v[nxt][ms],
-           per if policy else 0, hyp[0], hyp[1], skip, bad)
+           per if policy else 0, hyp, skip, bad)
         self.all_gather(params.p[nxt][s_lo:s_hi], params.p[nxt][lo:hi])
 
     def bucket_ready(self, b: int) -> None:

@@ -381,6 +381,14 @@ def step_finalize(loss_sums, loss_max, value_sums, bad_counts, attn_bad, algo, l
               float(n_transitions), _p(record), _p(skip), _stream())
 
 
+def adam_dev(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, hyper, skip, bad):
+    """hyper: DEVICE f64[12], {lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t} of the
+    two groups, read at run time (graph-replayable)."""
+    _check(hyper, "hyper", F64, (12,))
+    _lib.call("accel_adam_dev", _p(p_in), _p(g), _p(m_in), _p(v_in), _p(p_out), _p(m_out),
+              _p(v_out), p_in.numel(), int(n0), _p(hyper), _p(skip), _p(bad), _stream())
+
+
 def adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, group0, group1, skip, bad):
     """group0/group1: HOST sequences {lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t}."""
     n = p_in.numel()

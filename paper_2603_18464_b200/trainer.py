@@ -33,7 +33,7 @@ from .params import AdamStateView, DeviceParams, Dims, FlatLayout, POLICY_NAMES,
 from .publish import OBS_MODEL, POLICY, REWARD_MODEL, VersionedWeights
 from .replay import DeviceTrajectory
 from .world_model import DeviceMlp2, obs_model_data, reward_model_data
-from .workload import PackedBatch, pack_trajectories
+from .workload import PackedBatch, PinnedStaging, pack_trajectories
 
 F32, F64, I32 = torch.float32, torch.float64, torch.int32
 
@@ -369,7 +369,12 @@ class Trainer:
         # on first use (the bundle's obs/reward models seed them)
         self._wm = {}
         self.scratch = _Scratch(self.device)
-        self._rec_host = torch.zeros(32, dtype=F64).pin_memory()
+        self._staging = PinnedStaging()
+        self._rec_host = torch.zeros(64, dtype=F64).pin_memory()
+        # Adam hyperparameters of the next step, refreshed on the host and copied
+        # to the device inside the step (so a captured CUDA graph replays steps)
+        self._hyper_host = torch.zeros(12, dtype=F64).pin_memory()
+        self._hyper_dev = torch.zeros(12, dtype=F64, device=self.device)
         self.profile_events = None  # list -> CUDA-event brackets of the hot kernels
         A, K = self.dims.n_actions, self.dims.chunk_len
         # factorized head (no [M, A] logits) wherever the kernel supports the shape
@@ -597,7 +602,9 @@ class Trainer:
             for t in trajs:
                 if self.cfg.revalue:
                     assert self.publish_version >= t.behavior_version
-            pb = pack_trajectories(trajs)
+            # one threaded pass casting into page-locked staging; the upload below
+            # is asynchronous DMA (the build's one host sync orders its reuse)
+            pb = pack_trajectories(trajs, staging=self._staging)
         dev_batch = self.upload(pb)
         return self.build_from_device(dev_batch, n_real=int(pb.real.sum()),
                                       behavior_version=pb.behavior_version)
@@ -724,6 +731,12 @@ class Trainer:
                   dy.stride(0), x.stride(0), k, 1, 1, 0, 0, ks, ops._stream())
         return (part, out, 2 * ks + extra, n * k, n * k)
 
+    def _write_hyper(self) -> None:
+        """Both Adam groups' {lr, beta1, beta2, eps, 1 - beta^t} for the next step."""
+        t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
+        self._hyper_host.numpy()[:] = (self.adam_policy.hyper(t_pol)
+                                       + self.adam_value.hyper(t_val))
+
     def _bucket_done(self, tensor_name: str) -> None:
         if self.comm is not None:
             self.comm.bucket_ready(self.layout.bucket_of(tensor_name))
@@ -843,12 +856,13 @@ class Trainer:
         # rank's slice, speculative: the host adopts generation nxt only if the
         # record accepts the step) and all-gathered as soon as the backward has
         # written it, on a side stream (dp.DataParallel)
-        t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
-        hyp = (self.adam_policy.hyper(t_pol), self.adam_value.hyper(t_val))
+        self._write_hyper()
+        self._hyper_dev.copy_(self._hyper_host, non_blocking=True)
         adam_bad = cnt[2:3]
         if self.comm is not None:
-            self.comm.begin_step(self.params, hyp, S.get("st.noskip", (1,), torch.int32).zero_(),
-                                 adam_bad, adam_fn=ops.adam)
+            self.comm.begin_step(self.params, self._hyper_dev,
+                                 S.get("st.noskip", (1,), torch.int32).zero_(), adam_bad,
+                                 adam_fn=ops.adam_dev)
 
         # value head (hiddens detached)
         vclip = {}
@@ -979,9 +993,10 @@ class Trainer:
             self.comm.finish_step()  # the last buckets' exchange; the stream waits for it
             ops.count_nonfinite(self.params.p[nxt], adam_bad)
         else:
-            ops.adam(self.params.p[cur], self.params.g, self.params.m[cur], self.params.v[cur],
-                     self.params.p[nxt], self.params.m[nxt], self.params.v[nxt],
-                     self.layout.n_policy, hyp[0], hyp[1], skip, adam_bad)
+            ops.adam_dev(self.params.p[cur], self.params.g, self.params.m[cur],
+                         self.params.v[cur], self.params.p[nxt], self.params.m[nxt],
+                         self.params.v[nxt], self.layout.n_policy, self._hyper_dev, skip,
+                         adam_bad)
         out = S.get("st.out", (18,), F64)
         out[:17].copy_(record)
         out[17:18].copy_(adam_bad.double())

@@ -84,8 +84,48 @@ class PackedBatch:
                                       self.tokens, self.rewards, self.mu, self.done))
 
 
-def pack_trajectories(trajs) -> PackedBatch:
-    """Flatten duck-typed trajectories into the CSR wire format (float32)."""
+class PinnedStaging:
+    """Grow-only page-locked host buffers for the packed batch: the pack writes
+    float32 straight into them and the upload is one asynchronous DMA per field
+    (a pageable source makes every host-to-device copy synchronous and staged)."""
+
+    def __init__(self) -> None:
+        self._bufs: dict = {}
+
+    def get(self, name: str, shape, dtype) -> np.ndarray:
+        import torch
+        n = int(np.prod(shape))
+        tdt = {np.float32: torch.float32, np.int32: torch.int32, np.int64: torch.int64,
+               np.uint8: torch.uint8}[np.dtype(dtype).type]
+        buf = self._bufs.get(name)
+        if buf is None or buf.dtype != tdt or buf.numel() < n:
+            buf = torch.empty(max(n, 1) + (n >> 3), dtype=tdt, pin_memory=True)
+            self._bufs[name] = buf
+        return buf[:n].numpy().reshape(shape)
+
+
+def _pack_rows(trajs, lens, off, frames, steps, values, tokens, rewards, mu, lo, hi) -> None:
+    """Trajectories [lo, hi) into their CSR rows (float64 -> float32 casts in place)."""
+    for s in range(lo, hi):
+        t = trajs[s]
+        a, b = int(off[s]), int(off[s + 1])
+        fa, fb = a + s, b + s + 1
+        np.copyto(frames[fa:fb], np.asarray(t.observations), casting="unsafe")
+        np.copyto(steps[fa:fb], np.asarray(t.steps), casting="unsafe")
+        np.copyto(values[fa:fb - 1], np.asarray(t.values), casting="unsafe")
+        values[fb - 1] = t.bootstrap_value
+        np.copyto(tokens[a:b], np.asarray(t.tokens), casting="unsafe")
+        np.copyto(rewards[a:b], np.asarray(t.rewards), casting="unsafe")
+        np.copyto(mu[a:b], np.asarray(t.behavior_logits), casting="unsafe")
+
+
+def pack_trajectories(trajs, staging: PinnedStaging | None = None,
+                      threads: int | None = None) -> PackedBatch:
+    """Flatten duck-typed trajectories into the CSR wire format (float32).
+
+    Every field is written once, cast in place, into preallocated rows (with
+    `staging`: page-locked buffers, so the upload is asynchronous DMA); the
+    copies run on a thread pool over trajectories (NumPy releases the GIL)."""
     if not trajs:
         raise DimensionError("cannot pack an empty trajectory list")
     k = int(np.asarray(trajs[0].tokens).shape[1])
@@ -98,20 +138,39 @@ def pack_trajectories(trajs) -> PackedBatch:
         if (np.asarray(t.tokens).shape[1] != k or np.asarray(t.behavior_logits).shape[2] != a
                 or np.asarray(t.observations).shape[1] != o):
             raise DimensionError("trajectories disagree on chunk_len / n_actions / obs_dim")
-    off = np.zeros(len(trajs) + 1, dtype=np.int64)
+    n = len(trajs)
+    off = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(lens, out=off[1:])
-    steps = np.concatenate([np.asarray(t.steps) for t in trajs])
-    if steps.size and (steps.min() < np.iinfo(np.int32).min or steps.max() > np.iinfo(np.int32).max):
-        raise DimensionError("step index outside int32 range")
+    for t in trajs:
+        st = np.asarray(t.steps)
+        if st.size and (st.min() < np.iinfo(np.int32).min or st.max() > np.iinfo(np.int32).max):
+            raise DimensionError("step index outside int32 range")
+    N = int(off[-1])
+    F = N + n
+    if staging is None:
+        alloc = lambda name, shape, dt: np.empty(shape, dtype=dt)
+    else:
+        alloc = staging.get
+    frames = alloc("frames", (F, o), np.float32)
+    steps = alloc("steps", (F,), np.int32)
+    values = alloc("values", (F,), np.float32)
+    tokens = alloc("tokens", (N, k), np.int32)
+    rewards = alloc("rewards", (N,), np.float32)
+    mu = alloc("mu", (N, k, a), np.float32)
+    args = (trajs, lens, off, frames, steps, values, tokens, rewards, mu)
+    workers = min(threads or 8, max(1, N // 4096), n)
+    if workers <= 1:
+        _pack_rows(*args, 0, n)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        # contiguous trajectory ranges balanced by transition count
+        cuts = np.searchsorted(off, np.linspace(0, N, workers + 1)[1:-1]).tolist()
+        bounds = [0] + cuts + [n]
+        with ThreadPoolExecutor(workers) as ex:
+            list(ex.map(lambda i: _pack_rows(*args, bounds[i], bounds[i + 1]), range(workers)))
     return PackedBatch(
-        traj_off=off,
-        frames=np.concatenate([np.asarray(t.observations, dtype=np.float32) for t in trajs]),
-        steps=steps.astype(np.int32),
-        values=np.concatenate([np.append(np.asarray(t.values), t.bootstrap_value)
-                               for t in trajs]).astype(np.float32),
-        tokens=np.concatenate([np.asarray(t.tokens) for t in trajs]).astype(np.int32),
-        rewards=np.concatenate([np.asarray(t.rewards) for t in trajs]).astype(np.float32),
-        mu=np.concatenate([np.asarray(t.behavior_logits, dtype=np.float32) for t in trajs]),
+        traj_off=off, frames=frames, steps=steps, values=values, tokens=tokens, rewards=rewards,
+        mu=mu,
         done=np.array([bool(t.done) for t in trajs], dtype=np.uint8),
         real=np.array([t.source == "real" for t in trajs], dtype=np.uint8),
         behavior_version=np.array([int(t.behavior_version) for t in trajs], dtype=np.int64),

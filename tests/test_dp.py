@@ -31,8 +31,10 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def torch_adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, g0, g1, skip, bad):
-    """float64 restatement of accel_adam on CPU tensors (numerics.py:95-126)."""
+def torch_adam(p_in, g, m_in, v_in, p_out, m_out, v_out, n0, hyp, skip, bad):
+    """float64 restatement of accel_adam on CPU tensors (numerics.py:95-126);
+    hyp = (group 0, group 1) host tuples."""
+    g0, g1 = hyp
     if int(skip[0]):
         return
     n = p_in.numel()
@@ -68,7 +70,7 @@ def _run_gloo(target, world: int, attempts: int = 3) -> dict:
             for _ in range(world):
                 item = q.get(timeout=120)
                 res[item[0]] = item[1:]
-        except _queue.Empty as e:
+        except (_queue.Empty, OSError) as e:  # a rank died (e.g. a port race): retry
             last = e
         for p in procs:
             p.join(timeout=60)
@@ -157,7 +159,7 @@ def test_zero2_adam_and_collectives_gloo():
     g_sum = sum(torch.randn(layout.total, generator=torch.Generator().manual_seed(100 + r))
                 for r in range(world))
     torch_adam(ref.p[0], g_sum, ref.m[0], ref.v[0], ref.p[1], ref.m[1], ref.v[1], layout.n_policy,
-               HYP[0], HYP[1], torch.zeros(1, dtype=torch.int32), None)
+               HYP, torch.zeros(1, dtype=torch.int32), None)
     for r in range(world):
         torch.testing.assert_close(res[r][0], ref.p[1], rtol=0, atol=1e-7)
         torch.testing.assert_close(torch.from_numpy(res[r][4]), ref.m[1], rtol=0, atol=1e-7)
