@@ -37,6 +37,21 @@ def _check(t, name, dtype, shape=None):
         raise DimensionError(f"{name} must be contiguous")
 
 
+_RETAIN = []  # grown-out buffers kept alive once a CUDA graph may reference them
+
+
+def retain_workspaces() -> None:
+    """From now on a grow-only buffer that is replaced is kept alive instead of
+    freed: a captured CUDA graph may still point into it (trainer.CapturedStep)."""
+    if not _RETAIN:
+        _RETAIN.append(None)
+
+
+def retire(buf) -> None:
+    if _RETAIN and buf is not None:
+        _RETAIN.append(buf)
+
+
 class Workspace:
     """Grow-only scratch buffer reused across calls on one device."""
 
@@ -46,6 +61,7 @@ class Workspace:
     def get(self, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 16)
         if self._buf is None or self._buf.numel() < nbytes:
+            retire(self._buf)
             self._buf = torch.empty(nbytes + (nbytes >> 3), dtype=U8, device="cuda")
         return self._buf
 

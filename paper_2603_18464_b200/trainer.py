@@ -310,6 +310,7 @@ class _Scratch:
         n = int(np.prod(shape)) if len(shape) else 1
         buf = self._bufs.get(name)
         if buf is None or buf.dtype != dtype or buf.numel() < n:
+            ops.retire(buf)
             buf = torch.empty(max(n, 1) + (n >> 4), dtype=dtype, device=self.device)
             self._bufs[name] = buf
         return buf[:n].view(*shape) if len(shape) else buf[:1]
@@ -611,6 +612,11 @@ class Trainer:
 
     def build_from_device(self, b: dict, n_real: int, behavior_version) -> DeviceTrainBatch | None:
         """The device half of build_train_batch on an uploaded CSR batch."""
+        batch, host_dev = self._build_device(b, n_real, behavior_version)
+        return self._build_finish(batch, host_dev.cpu().numpy())  # the one host sync
+
+    def _build_device(self, b: dict, n_real: int, behavior_version) -> tuple:
+        """Every launch of the build, no host sync: (batch, device flag vector)."""
         cfg, d = self.cfg, self.dims
         n = int(b["traj_off"].shape[0] - 1)
         N = int(b["rewards"].shape[0])
@@ -658,10 +664,12 @@ class Trainer:
         batch.boot_rows = b["traj_off"][1:] + torch.arange(n, dtype=torch.int64, device=dev)
         if cfg.loss.value_clip is not None:  # rollout-time V per transition
             batch.v_old = b["values"].index_select(0, frame_of)
-        lags = self.publish_version - np.asarray(behavior_version, dtype=np.int64)
-        counts = torch.tensor([float(n_real), float(n), float(lags.sum())], dtype=F64, device=dev)
-        host_dev = torch.cat([flags, cnt.double(), counts])
+        host_dev = torch.cat([flags, cnt.double()])
         if self.comm is not None:
+            lags = self.publish_version - np.asarray(behavior_version, dtype=np.int64)
+            counts = torch.tensor([float(n_real), float(n), float(lags.sum())], dtype=F64,
+                                  device=dev)
+            host_dev = torch.cat([host_dev, counts])
             # data parallel: the batch is one shard of the global batch; every
             # accept/reject decision, the transition count and the record's
             # trajectory counts / behavior lag are global (all ranks agree)
@@ -670,7 +678,12 @@ class Trainer:
             self.comm.all_reduce_sum(dec)
             host_dev.index_copy_(0, idx, dec)
             host_dev[2:3].copy_(sums[2:3])
-        host = host_dev.cpu().numpy()  # the one host sync
+        return batch, host_dev
+
+    def _build_finish(self, batch, host) -> DeviceTrainBatch | None:
+        """The host half: the reference's domain errors and the finite check
+        (trainer.py:392-402) from the build's flag vector."""
+        cfg, d = self.cfg, self.dims
         if host[7] == 1:
             raise DomainError("cannot normalize zero advantages")
         if host[7] == 2:
@@ -1002,11 +1015,12 @@ class Trainer:
         out[17:18].copy_(adam_bad.double())
         return out
 
-    def _finish_step(self, batch, record_dev: torch.Tensor) -> dict | None:
-        host = self._rec_host[:18]
-        host.copy_(record_dev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        rec = host.numpy().copy()
+    def _finish_step(self, batch, record_dev: torch.Tensor | None, rec=None) -> dict | None:
+        if rec is None:
+            host = self._rec_host[:18]
+            host.copy_(record_dev, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            rec = host.numpy().copy()
         if rec[11] > 0:
             raise DomainError("log_softmax input contains non-finite values")
         if rec[12] > 0:
@@ -1052,6 +1066,13 @@ class Trainer:
             self.metrics.emit("train_step", **out)
         return out
 
+    # -- CUDA graphs ------------------------------------------------------------------
+    def capture_step(self, inputs: dict, n_real: int, behavior_version) -> "CapturedStep":
+        """build_from_device + train_step of a fixed-shape device batch as CUDA
+        graphs (see CapturedStep): the launch-bound small configurations (cfg1)
+        run as one graph launch and one pinned readback per step."""
+        return CapturedStep(self, inputs, n_real, behavior_version)
+
     # -- loop (trainer.py:539-560) -------------------------------------------------------
     def run(self, cache, wm_buffer, stop) -> Generator:
         """Consume TrainBatches from the prefetch channel until stopped.
@@ -1083,8 +1104,83 @@ class Trainer:
                         self.train_reward_model_step(trajs)
 
 
+class CapturedStep:
+    """One optimizer step (build_from_device + train_step) on a fixed set of
+    device input buffers, captured as CUDA graphs.
+
+    Every launch of the step -- revaluation, GAE, normalization, behavior
+    log-probs, the fused loss, backward, Adam, the record -- is stream-ordered
+    with its decisions made on the device (the FIXUP pass, the skip flag), so
+    the only host work per step is one replay, one pinned readback of the
+    build flags + the record, and the reference's record / error logic.  The
+    parameters are ping-ponged (Adam reads generation cur, writes cur ^ 1), so
+    one graph is captured per parity, on first use; the Adam step counters
+    enter through device memory (Trainer._hyper_dev, refreshed before each
+    replay).  Refill the `inputs` tensors in place between runs (same shapes);
+    the trainer must not be given other batch shapes while a CapturedStep is
+    live (its scratch buffers are the graphs' buffers).  Single GPU only.
+    """
+
+    def __init__(self, trainer: Trainer, inputs: dict, n_real: int, behavior_version) -> None:
+        if trainer.comm is not None:
+            raise DomainError("graph capture is single-GPU (the ZeRO-2 path has host-side "
+                              "collectives)")
+        if trainer.profile_events is not None:
+            raise DomainError("disable profile_events before capturing")
+        self.tr = trainer
+        self.inputs = inputs
+        self.n_real = int(n_real)
+        self.bver = np.asarray(behavior_version, dtype=np.int64)
+        self.n = int(inputs["traj_off"].shape[0] - 1)
+        self._graphs: dict = {}
+        ops.retain_workspaces()  # captured addresses must stay valid
+        self._out_host = torch.zeros(64, dtype=F64).pin_memory()
+
+    def _run_eager(self):
+        tr = self.tr
+        batch, host_dev = tr._build_device(self.inputs, self.n_real, self.bver)
+        rec = tr._step_device(batch)
+        return batch, torch.cat([host_dev, rec])
+
+    def _capture(self):
+        # warm-up on a side stream (every scratch buffer and workspace sized),
+        # then capture; neither result is adopted (the host does not flip)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._run_eager()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            batch, out = self._run_eager()
+        return g, batch, out
+
+    def run(self) -> dict | None:
+        """Replay one step; returns the train_step record, or None when the
+        batch is rejected (non-finite) or dropped (every token excluded)."""
+        tr = self.tr
+        cur = tr.params.cur
+        if cur not in self._graphs:
+            self._graphs[cur] = self._capture()
+        g, batch, out = self._graphs[cur]
+        tr._write_hyper()  # the graph copies it to the device first
+        g.replay()
+        host = self._out_host[:out.numel()]
+        host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        vals = host.numpy().copy()
+        nb = out.numel() - 18
+        batch.critic_version = tr.publish_version
+        batch.behavior_lag_mean = float(np.mean(tr.publish_version - self.bver))
+        if tr._build_finish(batch, vals[:nb]) is None:
+            return None
+        return tr._finish_step(batch, None, rec=vals[nb:])
+
+
 __all__ = [
     "GaeConfig", "LossConfig", "TrainerConfig", "Trainer", "ShardStats", "compute_gae",
     "shard_statistics", "global_normalize", "trust_weight", "chunk_ratio", "policy_surrogate",
     "entropy_bonus", "total_loss", "behavior_log_probs", "POLICY_NAMES", "VALUE_NAMES",
+    "CapturedStep",
 ]

@@ -221,3 +221,37 @@ def test_bench_workload_sample_matches_oracle():
     tr, batch = _oracle_vs_gpu(trajs, (195, 64, 7, 256, 522, 32), OracleConfig(), 522,
                                setup=setup)
     assert batch.n_transitions == int(lens.sum()) and batch.pk_group.nblocks > 8
+
+
+@pytest.mark.gpu
+def test_cfg1_captured_graph_equals_eager_steps():
+    """cfg1 (64 x 128) as CUDA-graph replays (Trainer.capture_step): records and
+    parameters bitwise equal to the eager build_from_device + train_step over
+    three steps (both parameter-generation parities), and a rejected batch
+    (non-finite reward refilled into the captured inputs) returns None without
+    touching the parameters."""
+    import torch
+
+    from paper_2603_18464_b200.trainer import Trainer
+    from paper_2603_18464_b200.workload import pack_trajectories
+
+    g = Cfg1Golden("trainer_cfg1_full_trust")
+    m = g.meta
+    mk = lambda: Trainer(_bundle(g.params("init.", "policy"), g.params("init.", "value"), m["o"],
+                                 m["d"], m["k"], m["a"], m["n_steps"], m["mlp_hidden"]),
+                         _trainer_cfg(g.oracle_cfg()))
+    eager, graphed = mk(), mk()
+    trajs = g.trajectories(0)
+    pb = pack_trajectories(trajs)
+    bver = np.zeros(len(trajs), dtype=np.int64)
+    step = graphed.capture_step(graphed.upload(pb), len(trajs), bver)
+    for _ in range(3):
+        want = eager.train_step(eager.build_from_device(eager.upload(pb), len(trajs), bver))
+        got = step.run()
+        assert got == want
+        assert torch.equal(graphed.params.p[graphed.params.cur], eager.params.p[eager.params.cur])
+    assert graphed.cycles == eager.cycles == 3 and graphed.publish_version == 3
+    before = graphed.params.p[graphed.params.cur].clone()
+    step.inputs["rewards"][5] = float("nan")
+    assert step.run() is None
+    assert torch.equal(graphed.params.p[graphed.params.cur], before) and graphed.cycles == 3
