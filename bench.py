@@ -60,16 +60,42 @@ def parse():
                     help="cfg2: LIBERO-Long ragged batch, D = 64 (the headline); cfg4: "
                          "OpenVLA-7B-shaped heads O = D = 4096, 64 x 128 transitions per GPU")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the cfg1 / cfg4 / drop-in-call lines (extra keys)")
     return ap.parse_args()
 
 
 _WL = {"name": "cfg2"}
 
 
+class workload:
+    """Temporarily switch the workload the helpers below describe."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        self.prev, _WL["name"] = _WL["name"], self.name
+
+    def __exit__(self, *exc):
+        _WL["name"] = self.prev
+        return False
+
+
 def dims():
     if _WL["name"] == "cfg4":  # OpenVLA-7B-shaped heads (SURVEY 8(d) cfg4)
         return dict(K=7, A=256, D=4096, O=4096, H=32)
-    return dict(K=7, A=256, D=64, O=195, H=32)
+    return dict(K=7, A=256, D=64, O=195, H=32)  # cfg1 and the cfg2 headline
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def sfu_rate(peaks: dict) -> float:
@@ -130,7 +156,7 @@ def make_bundle(seed: int, n_steps: int):
 
 
 def lengths_for(seed: int, rank: int, n: int, horizon: int):
-    if _WL["name"] == "cfg4":  # 64 trajectories x 128 steps per GPU, done alternating
+    if _WL["name"] in ("cfg1", "cfg4"):  # 64 trajectories x 128 steps per GPU, done alternating
         return np.full(64, 128, dtype=np.int64), np.arange(64) % 2 == 0
     from paper_2603_18464_b200.workload import libero_long_lengths
     return libero_long_lengths(np.random.default_rng(np.random.SeedSequence([seed, rank, 11])), n,
@@ -260,8 +286,11 @@ def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20) -> d
             "rows": rows}
 
 
-def cpu_baseline(bundle, inputs_host, lens, done, n_cpu: int, n_steps: int, reps: int = 1):
-    """The float64 oracle (reference restatement) on a bounded sample, host cores."""
+def cpu_baseline(bundle, inputs_host, lens, done, n_cpu: int, n_steps: int, reps: int = 3,
+                 threads: int | None = None):
+    """The float64 oracle (reference restatement) on a bounded sample of the
+    same batch, host cores: best of `reps` timed build_train_batch +
+    train_step after one warm-up, OpenBLAS limited to `threads` (default all)."""
     from threadpoolctl import threadpool_limits
 
     from oracle.trainer_ref import OracleConfig, OracleTrainer
@@ -280,7 +309,7 @@ def cpu_baseline(bundle, inputs_host, lens, done, n_cpu: int, n_steps: int, reps
                      done=np.asarray(done[:n], dtype=np.uint8), real=np.ones(n, np.uint8),
                      behavior_version=np.zeros(n, np.int64))
     trajs = unpack_trajectories(pb)
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     best = None
     with threadpool_limits(limits=cores):
         for _ in range(reps + 1):
@@ -292,9 +321,129 @@ def cpu_baseline(bundle, inputs_host, lens, done, n_cpu: int, n_steps: int, reps
             dt = time.perf_counter() - t0
             best = dt if best is None else min(best, dt)
     return {"value": N / best, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{n} trajectories / {N} transitions of the same workload, oracle "
-                      f"build_train_batch + train_step (float64 NumPy, OpenBLAS {cores} threads), "
-                      f"best of {reps} after 1 warm-up"}
+                      f"build_train_batch + train_step (float64 NumPy, OpenBLAS {cores} "
+                      f"thread{'s' if cores > 1 else ''}), best of {reps} after 1 warm-up"}
+
+
+def timed_steps(fn, steps: int, warmup: int) -> float:
+    """ms per call of fn over `steps` calls after `warmup`, CUDA events."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_cfg1(dev, seed: int, steps: int, warmup: int, cpu: bool) -> dict:
+    """BASELINE configs[0] (cfg1: 64 x 128, K = 7, A = 256, D = 64, obs 195) on
+    one GPU, eager and as a CUDA-graph replay of the whole step
+    (Trainer.capture_step), beside the float64 CPU oracle on the identical
+    batch at 1 thread and at every host core (best of 3)."""
+    import torch
+
+    from paper_2603_18464_b200 import _lib
+    from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
+    with workload("cfg1"):
+        lens, done = lengths_for(seed, 0, 64, 128)
+        n, N = len(lens), int(lens.sum())
+        bundle = make_bundle(seed, 130)
+        inputs = device_inputs(lens, done, seed + 17, dev)
+        bver = np.zeros(n, dtype=np.int64)
+        tr = Trainer(bundle, TrainerConfig())
+        c0 = _lib.launch_count()
+        tr.train_step(tr.build_from_device(inputs, n_real=n, behavior_version=bver))
+        launches = _lib.launch_count() - c0
+        ms_eager = timed_steps(
+            lambda: tr.train_step(tr.build_from_device(inputs, n_real=n, behavior_version=bver)),
+            steps, warmup)
+        graphed = Trainer(make_bundle(seed, 130), TrainerConfig())
+        cap = graphed.capture_step(inputs, n, bver)
+        ms_graph = timed_steps(cap.run, steps, max(warmup, 2))
+        out = {"workload": "cfg1: 64 trajectories x 128 steps (N = 8192, M = 57,344 tokens), "
+                           "K=7, A=256, D=64, obs 195, GIPO trust arm, revalue on",
+               "value": N / (ms_graph / 1e3), "unit": UNIT, "ms_per_step": ms_graph,
+               "ms_per_step_eager": ms_eager, "value_eager": N / (ms_eager / 1e3),
+               "libaccel_launches_per_step": int(launches), "cuda_graph": True,
+               "host_syncs_per_step": 1}
+        if cpu:
+            host = {k: v.cpu().numpy() for k, v in inputs.items()}
+            host["frames"] = np.ascontiguousarray(host["frames"])
+            for thr in (1, None):
+                c = cpu_baseline(bundle, host, lens, done, n, 130, reps=3, threads=thr)
+                out["cpu_1thread" if thr == 1 else "cpu_all_cores"] = c
+        return out
+
+
+def run_cfg4(dev, seed: int, rank: int, steps: int, warmup: int, comm) -> dict:
+    """BASELINE configs[3] (cfg4: OpenVLA-7B-shaped heads, O = D = 4096, 64 x 128
+    transitions per GPU) -- ZeRO-2 data parallel under torchrun (weak scaling);
+    every GEMM on the wide tcgen05 kernel (csrc/tc_wide.cu)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
+    with workload("cfg4"):
+        lens, done = lengths_for(seed, rank, 64, 128)
+        n, N = len(lens), int(lens.sum())
+        tr = Trainer(make_bundle(seed, 522), TrainerConfig(), comm=comm)
+        inputs = device_inputs(lens, done, seed * 1000 + rank, dev)
+        bver = np.zeros(n, dtype=np.int64)
+        if comm is not None:
+            dist.barrier()
+        ms = timed_steps(
+            lambda: tr.train_step(tr.build_from_device(inputs, n_real=n, behavior_version=bver)),
+            steps, warmup)
+        t = torch.tensor([ms, float(N)], dtype=torch.float64, device=dev)
+        if comm is not None:
+            mx = t[:1].clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            ms, tot = float(mx.item()), float(t[1].item())
+        else:
+            tot = float(N)
+        world = comm.world if comm is not None else 1
+        del tr, inputs
+        torch.cuda.empty_cache()
+        return {"workload": WORKLOAD_CFG4, "value": tot / (ms / 1e3), "unit": UNIT,
+                "ms_per_step": ms, "n_gpus": world, "scaling": "weak",
+                "parallelism": f"dp{world} (ZeRO-2)" if world > 1 else "single",
+                "gemms": "accel_tc_gemm_wide (tf32 + bf16-pair tcgen05), no cuBLAS on the step"}
+
+
+def e2e_api(tr, seed: int, n_traj: int = 256, reps: int = 3) -> dict:
+    """The drop-in call itself: Trainer.build_train_batch(list[Trajectory]) +
+    train_step on reference-style float64 Trajectory objects (a sample of the
+    headline workload), wall clock per step -- the threaded pack into pinned
+    staging, the H2D upload, the device build and step, the record readback."""
+    from paper_2603_18464_b200.workload import synthetic_packed, unpack_trajectories
+    d = dims()
+    lens, done = lengths_for(seed + 7, 0, n_traj, 520)
+    pb = synthetic_packed(seed + 7, lens, done, d["K"], d["A"], d["O"])
+    trajs = unpack_trajectories(pb)  # float64 arrays, as the reference's Trajectory holds
+    del pb
+    N = int(lens.sum())
+    tr.train_step(tr.build_train_batch(trajs))
+    best, tot = None, 0.0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        tr.train_step(tr.build_train_batch(trajs))
+        dt = time.perf_counter() - t0
+        tot += dt
+        best = dt if best is None else min(best, dt)
+    f64_bytes = sum(t.observations.nbytes + t.behavior_logits.nbytes + t.rewards.nbytes
+                    + t.values.nbytes + t.tokens.nbytes + t.steps.nbytes for t in trajs)
+    return {"value": N / (tot / reps), "unit": UNIT, "ms_per_step": 1e3 * tot / reps,
+            "best_ms": 1e3 * best, "sample": f"{n_traj} trajectories / {N} transitions",
+            "call": "Trainer.build_train_batch(list[Trajectory float64]) + Trainer.train_step",
+            "host_input_bytes_f64": int(f64_bytes)}
 
 
 def run_reference(args, rank: int, world: int):
@@ -456,6 +605,14 @@ def main():
                "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
         del dev_in
 
+    extra = {}
+    if not args.no_extra and args.workload == "cfg2":
+        extra["e2e_api"] = e2e_api(tr, args.seed + rank)
+        extra["cfg4"] = run_cfg4(dev, args.seed, rank, 10, 3, comm)
+        if rank == 0:
+            extra["cfg1"] = run_cfg1(dev, args.seed, 50, 5, not args.no_cpu)
+        if comm is not None:
+            dist.barrier()
     if rank != 0:
         if comm is not None:
             dist.destroy_process_group()
@@ -491,10 +648,11 @@ def main():
     t_logp = float(np.mean(kern.get("token_logp", [float("nan")]))) / 1e3
 
     sweep = gae_sweep(dev, peak)
-    cpu = None
+    cpu = cpu1 = None
     if not args.no_cpu:
         host_np = {k: v.numpy() for k, v in host.items()}
-        cpu = cpu_baseline(bundle, host_np, lens, done, args.cpu_traj, n_steps)
+        cpu = cpu_baseline(bundle, host_np, lens, done, args.cpu_traj, n_steps, reps=3)
+        cpu1 = cpu_baseline(bundle, host_np, lens, done, 16, n_steps, reps=3, threads=1)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -506,20 +664,26 @@ def main():
                    "trajectories_per_gpu": n, "transitions_per_gpu": N,
                    "tokens_per_gpu": M, "parallelism": f"dp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (behavior logits alone 11+ GB per GPU)"},
-        "roofline": {"kernel": "token_loss_fact (fused GIPO fwd+bwd, factorized head)"
-                     if tr.factorized else "token_loss (fused GIPO fwd+bwd)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "bytes_per_launch": loss_bytes, "ms_per_launch": t_loss * 1e3,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                     "sfu": {"ex2_per_launch": ex2_loss,
-                             "achieved_tops": ex2_loss / t_loss / 1e12,
-                             "peak_tops": sfu_rate(peaks) / 1e12,
-                             "frac": ex2_loss / t_loss / sfu_rate(peaks)},
-                     "note": ("dz-free loss path: the kernel writes 16 B of token scalars per "
-                              "token instead of the 1 KB dz row, so it is SFU/issue-bound, not "
-                              "HBM-bound (store mode: profiles/r1_bench_store_mode.json)")
-                     if tr.recompute_dz else "dz rows stored (HBM-bound)"},
+        "roofline": ({"kernel": "token_loss_fact2 (fused GIPO fwd+bwd, factorized head, "
+                                "dz-free scalar mode)", "bound": "sfu",
+                      "achieved": ex2_loss / t_loss / 1e12, "peak": sfu_rate(peaks) / 1e12,
+                      "unit": "Tex2/s", "frac": ex2_loss / t_loss / sfu_rate(peaks),
+                      "traffic": traffic, "ex2_per_launch": ex2_loss,
+                      "ms_per_launch": t_loss * 1e3,
+                      "peak_source": "16 MUFU ex2 / clk / SM x 148 SMs x sm_max_mhz (B200)",
+                      "hbm": {"bytes_per_launch": loss_bytes, "achieved": achieved,
+                              "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                      "note": "dz-free loss path: the kernel writes 16 B of token scalars per "
+                              "token instead of the 1 KB dz row, so its binding resource is the "
+                              "SFU (2 ex2 per logit), not HBM (store mode, HBM-bound: "
+                              "profiles/r1_bench_store_mode.json)"}
+                     if tr.recompute_dz else
+                     {"kernel": "token_loss_fact (fused GIPO fwd+bwd, factorized head)",
+                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                      "frac": achieved / peak, "traffic": traffic,
+                      "bytes_per_launch": loss_bytes, "ms_per_launch": t_loss * 1e3,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}),
         "roofline_group_recompute": {
             "kernel": "fact_group_sum2 (frame-blocked dz recompute + grouped sums)",
             "ms_per_launch": t_grp * 1e3,
@@ -537,7 +701,9 @@ def main():
                                 "achieved": logp_bytes / t_logp / 1e9,
                                 "frac": logp_bytes / t_logp / 1e9 / peak, "unit": "GB/s"},
         "cpu_baseline": cpu,
+        "cpu_baseline_1thread": cpu1,
         "e2e": e2e,
+        **extra,
         "gpu_launches": int(launches),
         "clocks": clocks.summary,
         "last_record": {k: rec[k] for k in ("loss", "policy_loss", "value_loss", "entropy")},
