@@ -19,11 +19,12 @@
  *   - domain errors that depend on device data (e.g. a negative pooled
  *     variance) are reported through flag words in the output buffers that
  *     the caller reads at its next (already required) host sync;
- *   - two entry points keep small device-global scratch instead of a
- *     caller workspace: accel_token_loss_fact(2)'s chunk counters (reset by a
- *     memset on the call's stream) and accel_reduce_f64's level-1 partials
- *     (> 8192 rows).  Calls of each on one device must therefore be ordered
- *     (one stream, or events between streams), as the trainer issues them.
+ *   - no entry point allocates or keeps device-global scratch: work
+ *     counters and multi-level partials live in caller buffers (e.g. the
+ *     `counters` of accel_token_loss_fact2, the `scratch` of
+ *     accel_reduce_f64), so calls on different streams are independent when
+ *     their buffers are; host-side caches (grid sizes, SM counts) are per
+ *     device.
  */
 #ifndef ACCEL_H_
 #define ACCEL_H_
@@ -40,6 +41,8 @@ const char* accel_last_error(void);
 /* number of kernels this library has launched in the process (for the
  * bench's gpu_launches claim) */
 unsigned long long accel_launch_count(void);
+/* Hash of the sources + flags this library was built from (build.py). */
+const char* accel_build_id(void);
 int accel_version(void);
 
 /* One strided copy (cudaMemcpy2DAsync, any direction): `height` rows of
@@ -139,7 +142,7 @@ int accel_token_loss(const float* logits, const float* bias, const int32_t* toke
  * rows), lp_new, stat_part/max_part as accel_token_loss (grid =
  * accel_fact_grid(N)).  fix_stats: FIXUP pass as accel_token_loss. */
 int accel_fact_grid(int64_t N);
-/* Rows of stat_part / max_part accel_token_loss_fact(2) writes for these sizes:
+/* Rows of stat_part / max_part accel_token_loss_fact2 writes for these sizes:
  * one per 32-transition chunk for the two-phase kernel (K <= 8, A in {128, 256};
  * fixed rows under its dynamic schedule, so the pooled statistics are bitwise
  * reproducible), accel_fact_grid(N) per-CTA rows otherwise. */
@@ -147,20 +150,17 @@ int64_t accel_fact_partials(int64_t N, int K, int A, int scalar_out);
 /* epp[(prev*K+k)*A + a] = ep[prev*A + a] + pp[k*A + a] + bias[a] */
 int accel_ep_plus(const float* ep, const float* pp, const float* bias, int A, int K,
                   float* epp, void* stream);
-/* accel_token_loss_fact with tsc_pos (nullable): token t's scalars go to
- * tsc[tsc_pos[t]] (the sorted position of a frame-blocked grouping). */
+/* tsc_pos (nullable): token t's scalars go to tsc[tsc_pos[t]] (the sorted
+ * position of a frame-blocked grouping).  counters: u32[2] caller workspace
+ * (the dynamic schedule's work counters of the main / fix-up pass; reset on
+ * the call's stream). */
 int accel_token_loss_fact2(const float* h2w, const float* epp, const int32_t* frame_of,
                            const int32_t* tokens, const float* lp_old, const float* adv,
                            int64_t N, int K, int A, int algo, double sigma, double clip_eps,
                            double lambda_h, double m_global, const double* fix_stats, float* dz,
                            void* tsc, const int32_t* tsc_pos, float* g_frame, float* lp_new,
-                           double* stat_part, double* max_part, void* stream);
-int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* frame_of,
-                          const int32_t* tokens, const float* lp_old, const float* adv,
-                          int64_t N, int K, int A, int algo, double sigma, double clip_eps,
-                          double lambda_h, double m_global, const double* fix_stats,
-                          float* dz, void* tsc, float* g_frame, float* lp_new, double* stat_part,
-                          double* max_part, void* stream);
+                           double* stat_part, double* max_part, unsigned* counters,
+                           void* stream);
 /* Grouped dz sums over the (prev, position) keys without dz in HBM: piece
  * partials f32[n_pieces, A] (then accel_grouped_rows_sum's key pass) of the dz
  * rows recomputed from h2w/epp and the tsc scalars, rows in the stable key
@@ -310,9 +310,12 @@ int accel_segment_moments(const float* x, const int64_t* off, int64_t nseg,
  * (buffers.py:120-122). */
 int accel_count_nonfinite_rows(const float* x, const int32_t* rows, int64_t R, int C,
                                 int64_t ld, unsigned* count, void* stream);
-/* out[c] = sum (mode 0) or max (mode 1) over p of part[p * width + c]. */
+/* out[c] = sum (mode 0) or max (mode 1) over p of part[p * width + c], in a
+ * fixed order.  scratch: accel_reduce_f64_scratch_size(parts, width) bytes
+ * (level-1 partials of the two-level path; NULL when that size is 0). */
+size_t accel_reduce_f64_scratch_size(int64_t parts, int width);
 int accel_reduce_f64(const double* part, int64_t parts, int width, int mode,
-                     double* out, void* stream);
+                     double* out, double* scratch, void* stream);
 /* train_step record (trainer.py:417-464) -> record f64[17]:
  * {loss, policy_loss, value_loss, entropy, excluded_tokens, ratio_mean,
  *  ratio_max, trust_weight_mean, trust_weight_min, clipped_fraction,

@@ -21,6 +21,7 @@ _SIGNATURES = {
     "accel_last_error": (ctypes.c_char_p, []),
     "accel_launch_count": (ctypes.c_ulonglong, []),
     "accel_version": (c_int, []),
+    "accel_build_id": (ctypes.c_char_p, []),
     "accel_copy_2d": (c_int, [P, c_size_t, P, c_size_t, c_size_t, c_size_t, P]),
     "accel_gae_workspace_size": (c_size_t, [c_int64, c_int64]),
     "accel_gae_segmented": (c_int, [P, P, P, P, c_int64, c_int64, c_double, c_double,
@@ -40,12 +41,9 @@ _SIGNATURES = {
     "accel_fact_grid": (c_int, [c_int64]),
     "accel_fact_partials": (c_int64, [c_int64, c_int, c_int, c_int]),
     "accel_ep_plus": (c_int, [P, P, P, c_int, c_int, P, P]),
-    "accel_token_loss_fact": (c_int, [P, P, P, P, P, P, c_int64, c_int, c_int, c_int,
-                                      c_double, c_double, c_double, c_double, P, P, P, P, P, P,
-                                      P, P]),
     "accel_token_loss_fact2": (c_int, [P, P, P, P, P, P, c_int64, c_int, c_int, c_int,
                                        c_double, c_double, c_double, c_double, P, P, P, P, P, P,
-                                       P, P, P]),
+                                       P, P, P, P]),
     "accel_fact_group_sum": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_int,
                                      c_int64, P, P]),
     "accel_pk_marginals": (c_int, [P, c_int, c_int, P, P, P]),
@@ -81,7 +79,8 @@ _SIGNATURES = {
     "accel_reduce_segments": (c_int, [P, P, P, P, P, c_int, P]),
     "accel_segment_moments": (c_int, [P, P, c_int64, P, P]),
     "accel_count_nonfinite_rows": (c_int, [P, P, c_int64, c_int, c_int64, P, P]),
-    "accel_reduce_f64": (c_int, [P, c_int64, c_int, c_int, P, P]),
+    "accel_reduce_f64": (c_int, [P, c_int64, c_int, c_int, P, P, P]),
+    "accel_reduce_f64_scratch_size": (c_size_t, [c_int64, c_int]),
     "accel_step_finalize": (c_int, [P, P, P, P, P, c_int, c_double, c_double, c_double,
                                     c_double, P, P, P]),
     "accel_count_nonfinite": (c_int, [P, c_int64, P, P]),
@@ -119,8 +118,26 @@ def lib() -> ctypes.CDLL:
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
+        _check_build(handle)
         _lib = handle
     return _lib
+
+
+def _check_build(handle) -> None:
+    """The library must be built from the sources beside it (build.py's id);
+    a stale libaccel.so raises instead of running old kernels."""
+    from . import build as _build
+    if not _build.CSRC.exists():  # an installed copy without sources: nothing to compare
+        return
+    have = handle.accel_build_id().decode()
+    want = _build.build_id()
+    if have != want:
+        raise AccelError(f"{LIB_PATH} is stale (built from {have}, sources are {want}); "
+                         "run `python -m paper_2603_18464_b200.build`")
+
+
+def build_id() -> str:
+    return lib().accel_build_id().decode()
 
 
 def call(name: str, *args) -> None:

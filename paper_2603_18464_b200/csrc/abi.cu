@@ -28,7 +28,14 @@ extern "C" unsigned long long accel_launch_count(void) {
   return accel::g_launches.load(std::memory_order_relaxed);
 }
 
-extern "C" int accel_version(void) { return 1; }
+extern "C" int accel_version(void) { return 2; }
+
+#ifndef ACCEL_BUILD_ID
+#define ACCEL_BUILD_ID "unknown"
+#endif
+// Hash of the sources and flags this library was built from (build.py):
+// the Python loader refuses a library whose id does not match its sources.
+extern "C" const char* accel_build_id(void) { return ACCEL_BUILD_ID; }
 
 // One strided DMA (host <-> device or device <-> device): uploads row-major
 // host arrays into pitched device storage (16-byte aligned rows for TMA).

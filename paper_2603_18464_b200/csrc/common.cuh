@@ -36,6 +36,7 @@ inline int check_cuda(cudaError_t e, const char* what) {
 }
 
 constexpr int kNumSMs = 148;
+constexpr int kMaxDevices = 64;  // per-device host caches (grid sizes, SM counts)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -386,14 +386,18 @@ extern "C" int accel_gae_segmented(const float* rewards, const float* values_fra
   Workspace ws = carve(workspace);
   int st = check_cuda(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), s), "gae counter");
   if (st) return st;
-  static int grid = 0;
+  // grid per device (a process may drive several GPUs)
+  static int grids[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return fail(kDimension, "gae: device ordinal %d", dev);
+  int& grid = grids[dev];
   if (grid == 0) {
     st = check_cuda(cudaFuncSetAttribute(gae_warp_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kGaeSmem), "gae smem");
     if (st) return st;
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaGetDevice(&dev);
+    int per_sm = 0, sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_warp_kernel,
                                                                   kThreads, kGaeSmem),

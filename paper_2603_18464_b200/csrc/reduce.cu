@@ -106,7 +106,6 @@ reduce_f64_kernel(const double* __restrict__ part, int64_t parts, int width, int
 // fixed, shared-memory tree per column) into tmp[b][width].
 constexpr int kRedThreads = 256;
 constexpr int kRedMaxCtas = 296;
-__device__ double g_red_tmp[kRedMaxCtas * 8];  // level-1 partials (one stream at a time)
 
 __global__ void __launch_bounds__(kRedThreads)
 reduce_f64_rows_kernel(const double* __restrict__ part, int64_t parts, int width, int mode,
@@ -250,8 +249,12 @@ extern "C" int accel_reduce_segments(const void* const* srcs, void* const* dsts,
   return post_launch("reduce_segments_kernel");
 }
 
+extern "C" size_t accel_reduce_f64_scratch_size(int64_t parts, int width) {
+  return (parts > 8192 && width <= 8) ? (size_t)kRedMaxCtas * 8 * sizeof(double) : 0;
+}
+
 extern "C" int accel_reduce_f64(const double* part, int64_t parts, int width, int mode,
-                                double* out, void* stream) {
+                                double* out, double* scratch, void* stream) {
   if (parts < 0 || width < 1 || (mode != 0 && mode != 1))
     return fail(kDimension, "reduce_f64: bad arguments");
   if (!part || !out) return fail(kDimension, "reduce_f64: NULL buffer");
@@ -259,10 +262,10 @@ extern "C" int accel_reduce_f64(const double* part, int64_t parts, int width, in
   if (parts > 8192 && width <= 8) {  // many rows: two levels, both in a fixed order
     const int ctas = (int)std::min<int64_t>(kRedMaxCtas, ceil_div(parts, 4096));
     const int64_t per = ceil_div(parts, ctas);
-    double* tmp = nullptr;
-    int st = check_cuda(cudaGetSymbolAddress(reinterpret_cast<void**>(&tmp), g_red_tmp),
-                        "reduce_f64 scratch");
-    if (st) return st;
+    double* tmp = scratch;  // level-1 partials, caller workspace
+    if (!tmp) return fail(kDimension, "reduce_f64: %lld rows need the level-1 scratch",
+                          (long long)parts);
+    int st;
     reduce_f64_rows_kernel<<<ctas, kRedThreads, 0, s>>>(part, parts, width, mode, per, tmp);
     if ((st = post_launch("reduce_f64_rows_kernel"))) return st;
     reduce_f64_kernel<<<1, 1024, 0, s>>>(tmp, ctas, width, mode, out);

@@ -142,15 +142,16 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
 
 // ---- host -----------------------------------------------------------------------
 
-inline int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+inline int sm_count() {  // SMs of the current device (cached per device)
+  static int n[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  if (n[dev] == 0) {
+    cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (n[dev] <= 0) n[dev] = 148;
   }
-  return n;
+  return n[dev];
 }
 
 inline uint32_t tmem_cols_for(int cols) {

@@ -633,7 +633,6 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
 // the chunk-start row EPP[A, 0] (every transition's token 0) is resident per CTA.
 constexpr int kF2MaxWarps = 7;
 constexpr int kF2Chunk = 32;  // transitions per dynamically claimed chunk (and statistics row)
-__device__ unsigned g_fact2_ctr[2];  // work counters (main pass, fixup pass)
 
 // After the call lane l holds the warp total of value index l / (32 / NV).
 template <int NV>
@@ -1323,17 +1322,6 @@ extern "C" int accel_ep_plus(const float* ep, const float* pp, const float* bias
   return post_launch("ep_plus_kernel");
 }
 
-extern "C" int accel_token_loss_fact(const float* h2w, const float* epp, const int32_t* frame_of,
-                                     const int32_t* tokens, const float* lp_old, const float* adv,
-                                     int64_t N, int K, int A, int algo, double sigma,
-                                     double clip_eps, double lambda_h, double m_global,
-                                     const double* fix_stats, float* dz, void* tsc,
-                                     float* g_frame, float* lp_new, double* stat_part,
-                                     double* max_part, void* stream) {
-  return accel_token_loss_fact2(h2w, epp, frame_of, tokens, lp_old, adv, N, K, A, algo, sigma,
-                                clip_eps, lambda_h, m_global, fix_stats, dz, tsc, nullptr, g_frame,
-                                lp_new, stat_part, max_part, stream);
-}
 
 extern "C" int accel_token_loss_fact2(const float* h2w, const float* epp, const int32_t* frame_of,
                                       const int32_t* tokens, const float* lp_old, const float* adv,
@@ -1341,7 +1329,8 @@ extern "C" int accel_token_loss_fact2(const float* h2w, const float* epp, const 
                                       double clip_eps, double lambda_h, double m_global,
                                       const double* fix_stats, float* dz, void* tsc,
                                       const int32_t* tsc_pos, float* g_frame, float* lp_new,
-                                      double* stat_part, double* max_part, void* stream) {
+                                      double* stat_part, double* max_part, unsigned* counters,
+                                      void* stream) {
   if (algo != 0 && algo != 1) return fail(kDomain, "unknown algorithm %d", algo);
   if (!(sigma > 0)) return fail(kDomain, "sigma must be > 0, got %g", sigma);
   if (!(clip_eps > 0 && clip_eps < 1)) return fail(kDomain, "clip_eps must be in (0, 1)");
@@ -1416,10 +1405,8 @@ extern "C" int accel_token_loss_fact2(const float* h2w, const float* epp, const 
     }
     // the work counter of this pass (a fix-up launch uses the second one, so a
     // skipped fix-up never races the next step's main pass)
-    unsigned* ctr = nullptr;
-    if (cudaGetSymbolAddress(reinterpret_cast<void**>(&ctr), g_fact2_ctr) != cudaSuccess)
-      return fail(kCuda, "token_loss_fact2: counter symbol");
-    ctr += fix_stats ? 1 : 0;
+    if (!counters) return fail(kDimension, "token_loss_fact2: NULL work counters");
+    unsigned* ctr = counters + (fix_stats ? 1 : 0);
     if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess)
       return fail(kCuda, "token_loss_fact2: counter reset");
     kernel<<<grid, nw * 32, smem, s>>>(h2w, epp, frame_of, tokens, lp_old, adv, N, K, prm,

@@ -303,10 +303,11 @@ def token_loss_fact(h2w, epp, frame_of, tokens, lp_old, adv, N, K, algo, sigma, 
     with tsc (f32[M, 4]) writes the per-token scalars instead of dz rows, at
     tsc_pos[t] (a frame-blocked grouping's sorted positions) when given."""
     A = h2w.shape[1]
+    counters = _stream_workspace("fact2_ctr", 8)  # main-pass / fix-up work counters
     _lib.call("accel_token_loss_fact2", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(lp_old),
               _p(adv), int(N), int(K), A, int(algo), float(sigma), float(clip_eps),
               float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(tsc), _p(tsc_pos),
-              _p(g_frame), _p(lp_new), _p(stat_part), _p(max_part), _stream())
+              _p(g_frame), _p(lp_new), _p(stat_part), _p(max_part), _p(counters), _stream())
 
 
 def pk_marginals(dpk, K, A, dprev, dpos):
@@ -368,8 +369,17 @@ def reduce_segments(segs):
     _lib.call("accel_reduce_segments", srcs, dsts, parts, lens, pitches, n, _stream())
 
 
+def _stream_workspace(tag: str, nbytes: int):
+    """Scratch private to the current stream (calls on different streams may
+    run concurrently; calls on one stream are ordered)."""
+    return workspace(f"{tag}@{torch.cuda.current_stream().cuda_stream}").get(nbytes)
+
+
 def reduce_f64(part, parts, width, mode, out):
-    _lib.call("accel_reduce_f64", _p(part), int(parts), int(width), int(mode), _p(out), _stream())
+    nbytes = _lib.lib().accel_reduce_f64_scratch_size(int(parts), int(width))
+    scratch = _stream_workspace("reduce_f64", nbytes) if nbytes else None
+    _lib.call("accel_reduce_f64", _p(part), int(parts), int(width), int(mode), _p(out),
+              _p(scratch), _stream())
     return out
 
 

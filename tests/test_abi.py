@@ -72,3 +72,15 @@ def test_packing_roundtrip_and_layout(rng):
         np.testing.assert_array_equal(a.tokens, b.tokens)
         np.testing.assert_allclose(a.rewards, b.rewards, rtol=1e-6)
         assert a.done == b.done and a.t_len == b.t_len
+
+
+def test_library_matches_its_sources(monkeypatch):
+    """Build provenance: the loaded library reports the hash of the sources it
+    was built from, and a library whose id does not match them is refused."""
+    from paper_2603_18464_b200 import _lib, build
+    from paper_2603_18464_b200.errors import AccelError
+    assert _lib.build_id() == build.build_id()
+    handle = _lib.lib()
+    monkeypatch.setattr(build, "build_id", lambda: "0000000000000000")
+    with pytest.raises(AccelError, match="stale"):
+        _lib._check_build(handle)
