@@ -19,10 +19,12 @@ class VersionedWeights:
     """Duck-types inference.VersionedWeights (kind, version, policy, value, ...)."""
 
     def __init__(self, kind: str, version: int, flat=None, owner=None, policy=None, value=None,
-                 obs_model=None, reward_model=None, split=None, template=None) -> None:
+                 obs_model=None, reward_model=None, split=None, template=None,
+                 layout=None) -> None:
         self.kind = kind
         self.version = version
         self.flat = flat          # device snapshot of the flat parameter buffer
+        self.layout = layout      # params.FlatLayout of `flat` (device consumers slice it)
         self._owner = owner
         self._split = split       # host flat -> (policy, value) tensors (receivers)
         self._template = template  # bundle whose model classes / configs the views reuse
@@ -34,7 +36,7 @@ class VersionedWeights:
     @classmethod
     def from_device(cls, kind: str, version: int, trainer) -> "VersionedWeights":
         flat = trainer.params.p[trainer.params.cur].clone()
-        return cls(kind, version, flat=flat, owner=trainer)
+        return cls(kind, version, flat=flat, owner=trainer, layout=trainer.layout)
 
     def _materialize(self) -> None:
         if self._policy is not None or (self._owner is None and self._split is None):
@@ -99,4 +101,5 @@ def broadcast_policy(snapshot, template, src: int = 0, group=None, device=None,
                    group=group)
     if rank == src:
         return snapshot
-    return VersionedWeights(POLICY, version, flat=flat, split=layout.split, template=template)
+    return VersionedWeights(POLICY, version, flat=flat, split=layout.split, template=template,
+                            layout=layout)

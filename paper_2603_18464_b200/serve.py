@@ -76,7 +76,26 @@ class DeviceServer:
         z = torch.zeros(1, dtype=F64, device=self.device)
         w = [z] * 23
         dims = [1] * 8
-        if weights.kind == POLICY:
+        flat, layout = getattr(weights, "flat", None), getattr(weights, "layout", None)
+        if (weights.kind == POLICY and layout is not None and isinstance(flat, torch.Tensor)
+                and flat.is_cuda and flat.device == self.device):
+            # device-resident snapshot (Trainer.snapshot / broadcast_policy): the
+            # serving layout (f64, [in][out]) is sliced, transposed and widened
+            # from the flat fp32 buffer on the device -- no host round trip; the
+            # values equal the host path's (the same fp32 parameters, widened)
+            def dv(name, transpose=False, ravel=False):
+                off = layout.offsets[name]
+                shape = layout.shapes[name]
+                x = flat[off:off + int(np.prod(shape))].view(shape)
+                x = x.t() if transpose else x
+                return (x.reshape(-1) if ravel else x).to(F64).contiguous()
+            w[0:8] = [dv("w0", True), dv("b0"), dv("w1", True), dv("b1"), dv("e_prev"),
+                      dv("e_pos"), dv("w_head", True), dv("b_head")]
+            w[8:15] = [dv("w_attn"), dv("b_attn"), dv("e_step"), dv("w0v", True), dv("b0v"),
+                       dv("w1v", ravel=True), dv("b1v")]
+            d = layout.dims
+            dims[:6] = [d.obs_dim, d.hidden, d.chunk_len, d.n_actions, d.n_steps, d.mlp_hidden]
+        elif weights.kind == POLICY:
             pol, val = weights.policy, weights.value
             p, v = pol.params.tensors, val.params.tensors
             pc = pol.cfg

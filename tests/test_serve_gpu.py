@@ -79,3 +79,38 @@ def test_serve_errors():
     bad[1].obs.step = g.meta["n_steps"]
     with pytest.raises(DimensionError, match="step index"):
         srv.run_batch(w, bad, 0)
+
+
+def test_device_snapshot_serves_without_host_round_trip():
+    """SURVEY 8(f) rows 1+2: a trainer's device snapshot (Trainer.snapshot) is
+    served straight from its flat fp32 buffer -- the snapshot's host models are
+    never materialized -- with responses identical to serving the same weights
+    through host model objects."""
+    from paper_2603_18464_b200.publish import POLICY, VersionedWeights
+    from paper_2603_18464_b200.serve import DeviceServer
+    from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
+    from paper_2603_18464_b200.types import (ModelBundle, PolicyConfig, PolicyModel, ValueConfig,
+                                             ValueHead)
+    from paper_2603_18464_b200.workload import synthetic_trajectories
+    g = ServeGolden()
+    m = g.meta
+    rng = np.random.default_rng(3)
+    pc = PolicyConfig(obs_dim=m["O"], hidden_dim=m["D"], chunk_len=m["K"], n_actions=m["A"],
+                      vocab_size=m["vocab"], action_start=m["action_start"])
+    bundle = ModelBundle(PolicyModel.init(rng, pc),
+                         ValueHead.init(rng, ValueConfig(m["D"], m["n_steps"], m["mlp_hidden"])))
+    tr = Trainer(bundle, TrainerConfig())
+    trajs = synthetic_trajectories(rng, [5, 9, 3], [True, False, True], m["K"], m["A"], m["O"],
+                                   n_steps=m["n_steps"])
+    tr.train_step(tr.build_train_batch(trajs))  # the snapshot is of trained parameters
+    snap = tr.snapshot()
+    reqs = g.requests(POLICY)
+    got = DeviceServer().run_batch(snap, reqs, m["base_seed"])
+    assert snap._policy is None and snap._value is None  # no host materialization
+    host_w = VersionedWeights(POLICY, snap.version, policy=tr.bundle.policy, value=tr.bundle.value)
+    want = DeviceServer().run_batch(host_w, reqs, m["base_seed"])
+    np.testing.assert_array_equal(np.stack([r.tokens for r in got]),
+                                  np.stack([r.tokens for r in want]))
+    np.testing.assert_array_equal(np.stack([r.logits for r in got]),
+                                  np.stack([r.logits for r in want]))
+    np.testing.assert_array_equal([r.value for r in got], [r.value for r in want])
