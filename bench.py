@@ -238,7 +238,8 @@ class ClockSampler:
         return False
 
 
-def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20) -> dict:
+def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20,
+              frame_of: bool = False) -> dict:
     """cfg2 (BASELINE.json configs[1]): K1 over LIBERO-Long mixes of 4K-64K
     trajectories (up to 25.5 M transitions, 0.5 GB), device-resident inputs,
     CUDA events over `reps` back-to-back launches (inputs > L2 at 16K+)."""
@@ -263,8 +264,8 @@ def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20) -> d
         sums = torch.empty(4, dtype=torch.float64, device=dev)
 
         def run():
-            ops.gae_segmented(r, v, t_off, d_dev, 0.99, 0.95, adv=adv, ret=ret, frame_of=fo,
-                              sums=sums)
+            ops.gae_segmented(r, v, t_off, d_dev, 0.99, 0.95, adv=adv, ret=ret,
+                              frame_of=fo if frame_of else None, sums=sums)
 
         for _ in range(3):
             run()
@@ -276,12 +277,15 @@ def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20) -> d
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        byt = 20 * N + 13 * n
+        byt = 16 * N + 13 * n + (4 * N if frame_of else 0)  # SURVEY 8(d) (+ frame_of)
         rows.append({"trajectories": n, "transitions": N, "bytes_per_launch": byt,
                      "ms_per_launch": ms, "achieved": byt / ms / 1e6,
                      "frac": byt / ms / 1e6 / peak})
         del r, v, adv, ret, fo
-    return {"kernel": "accel_gae_segmented (K1)", "unit": "GB/s", "peak": peak,
+    return {"kernel": "accel_gae_segmented (K1: frame-space tile scan + pooled-statistics "
+                      "partials)", "unit": "GB/s", "peak": peak,
+            "bytes": "16 N + 13 n (SURVEY 8(d): r, v in; adv, ret out; offsets, done, "
+                     "bootstrap v)" + (" + 4 N frame_of" if frame_of else ""),
             "config": "cfg2: LIBERO-Long mix (50% done T~U[1,520], 50% truncated at 520)",
             "rows": rows}
 
