@@ -35,6 +35,11 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
          "--expt-relaxed-constexpr", "-I", str(INCLUDE)]
 
 
+def _flags_key() -> bytes:
+    """The compiler flags without machine-specific paths (the repo moves)."""
+    return " ".join(ARCH + [f for f in FLAGS if f != str(INCLUDE)]).encode()
+
+
 def _sha(*parts: bytes) -> str:
     h = hashlib.sha256()
     for p in parts:
@@ -51,13 +56,13 @@ def _deps_hash() -> str:
 def build_id() -> str:
     """Hash of every source and the flags: what the library must report."""
     srcs = sorted(CSRC.glob("*.cu"))
-    return _sha(_deps_hash().encode(), " ".join(ARCH + FLAGS).encode(),
+    return _sha(_deps_hash().encode(), _flags_key(),
                 *(f.name.encode() + f.read_bytes() for f in srcs))
 
 
 def _key(src: Path, deps: str, bid: str) -> str:
     extra = bid.encode() if src.name == "abi.cu" else b""
-    return _sha(src.read_bytes(), deps.encode(), " ".join(ARCH + FLAGS).encode(), extra)
+    return _sha(src.read_bytes(), deps.encode(), _flags_key(), extra)
 
 
 def _compile(src: Path, key: str, old: dict, bid: str, verbose: bool):
