@@ -282,7 +282,7 @@ def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20,
                      "ms_per_launch": ms, "achieved": byt / ms / 1e6,
                      "frac": byt / ms / 1e6 / peak})
         del r, v, adv, ret, fo
-    return {"kernel": "accel_gae_segmented (K1: frame-space tile scan + pooled-statistics "
+    return {"kernel": "accel_gae_segmented (K1: warp per trajectory range + pooled-statistics "
                       "partials)", "unit": "GB/s", "peak": peak,
             "bytes": "16 N + 13 n (SURVEY 8(d): r, v in; adv, ret out; offsets, done, "
                      "bootstrap v)" + (" + 4 N frame_of" if frame_of else ""),

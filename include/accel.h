@@ -73,9 +73,6 @@ size_t accel_gae_workspace_size(int64_t n_traj, int64_t n_transitions);
  *   frame_of_out   i32[N] or NULL  frame row of each transition (i + traj)
  *   sums_out       f64[4]          {sum A, sum A^2, N, #non-finite A/ret}
  */
-/* Tuning: 0 = frame-space tile scan (default: 2048-frame tiles, decoupled
- * look-back), 1 = warp-per-trajectory-range scan. */
-void accel_gae_set_variant(int variant);
 int accel_gae_segmented(const float* rewards, const float* values_frames,
                         const int64_t* traj_off, const uint8_t* done,
                         int64_t n_traj, int64_t n_transitions,

@@ -24,7 +24,6 @@ _SIGNATURES = {
     "accel_build_id": (ctypes.c_char_p, []),
     "accel_copy_2d": (c_int, [P, c_size_t, P, c_size_t, c_size_t, c_size_t, P]),
     "accel_gae_workspace_size": (c_size_t, [c_int64, c_int64]),
-    "accel_gae_set_variant": (None, [c_int]),
     "accel_gae_segmented": (c_int, [P, P, P, P, c_int64, c_int64, c_double, c_double,
                                     P, P, P, P, P, c_size_t, P]),
     "accel_normalize_finalize": (c_int, [P, c_double, P, P]),

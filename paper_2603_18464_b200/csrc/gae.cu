@@ -308,322 +308,6 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
   }
 }
 
-// ---------------------------------------------------------------------------
-// Frame-space tile scan (the production kernel).
-//
-// In FRAME space the whole ragged batch is ONE reverse affine scan: frame f of
-// trajectory s is a transition frame (t = f - s, map A_f = delta_t + gl A_{f+1})
-// or s's bootstrap frame (map A = 0: a reset, so no segment bookkeeping enters
-// the scan).  delta_t = r_t + gamma v'_{f+1} - v_f with v' = 0 at a done
-// trajectory's bootstrap frame (trainer.py:92-94).  The frames are cut into
-// fixed 2048-frame tiles, one 256-thread CTA each, 8 consecutive frames per
-// thread loaded straight into registers (two float4), the tile's rewards
-// (a contiguous transition range) staged through shared memory by coalesced
-// loads.  Thread maps -> warp shuffle suffix scan -> block scan of the 8 warp
-// maps -> the tile's carry-in from a decoupled look-back over the tiles to its
-// right (tiles are claimed right to left; a tile whose map contains a
-// bootstrap frame ends every look-back chain).  Outputs go back to transition
-// space through shared memory as coalesced row stores.  Per-tile float64
-// (sum A, sum A^2, bad) partials, summed in tile order by the last tile:
-// bitwise deterministic.  HBM bytes: 16 per transition (+4 for frame_of) plus
-// the 13 per trajectory of the offsets, done flags and bootstrap values.
-
-int g_gae_variant = 0;
-
-constexpr int kTT = 256;              // threads per tile
-constexpr int kIPT = 8;               // frames per thread
-constexpr int kTileF = kTT * kIPT;    // 2048 frames per tile
-constexpr int kMaskW = kTileF / 32 + 2;  // bootstrap / done bit words (+ frame f1)
-
-struct TileStatus {                   // decoupled look-back record of one tile
-  unsigned flag;                      // 0 none, 1 aggregate, 2 inclusive
-  float agg_b, agg_c, incl;
-};
-
-struct TileWs {
-  int32_t* tile_first;   // [ntiles] trajectory containing the tile's first frame
-  TileStatus* status;    // [ntiles]
-  double* partials;      // [ntiles][3]
-  unsigned* counters;    // [2] tile ticket, arrival
-};
-
-size_t tile_ws_bytes(int64_t ntiles) {
-  return (size_t)ntiles * (4 + sizeof(TileStatus) + 3 * sizeof(double)) + 64;
-}
-
-TileWs tile_carve(void* base, int64_t ntiles) {
-  TileWs w;
-  char* p = static_cast<char*>(base);
-  w.partials = reinterpret_cast<double*>(p);
-  p += (size_t)ntiles * 3 * sizeof(double);
-  w.status = reinterpret_cast<TileStatus*>(p);
-  p += (size_t)ntiles * sizeof(TileStatus);
-  w.tile_first = reinterpret_cast<int32_t*>(p);
-  p += (size_t)ntiles * 4;
-  w.counters = reinterpret_cast<unsigned*>((reinterpret_cast<uintptr_t>(p) + 15) & ~(uintptr_t)15);
-  return w;
-}
-
-// tile_first[k] = the trajectory whose frames contain frame k * kTileF; each
-// tile start lies in exactly one trajectory's frame range [off[s] + s, off[s+1] + s + 1)
-__global__ void gae_tile_index_kernel(const int64_t* __restrict__ off, int64_t n_traj,
-                                      int64_t ntiles, int32_t* __restrict__ tile_first) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_traj;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t fs = __ldg(off + s) + s, fe = __ldg(off + s + 1) + s + 1;
-    for (int64_t k = (fs + kTileF - 1) / kTileF; k * kTileF < fe && k < ntiles; ++k)
-      tile_first[k] = (int32_t)s;
-  }
-}
-
-__device__ __forceinline__ void st_release_status(TileStatus* st, unsigned flag) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&st->flag), "r"(flag) : "memory");
-}
-
-__global__ void __launch_bounds__(kTT, 4)
-gae_tile_kernel(const float* __restrict__ rewards, const float* __restrict__ vals,
-                const int64_t* __restrict__ off, const uint8_t* __restrict__ done,
-                int64_t n_traj, int64_t n_frames, int64_t ntiles, float g_hi, float g_lo,
-                float decay, float* __restrict__ adv_out, float* __restrict__ ret_out,
-                int32_t* __restrict__ frame_out, TileWs ws, int64_t n_transitions,
-                double* __restrict__ sums_out) {
-  __shared__ unsigned s_boot[kMaskW], s_done[kMaskW];
-  __shared__ __align__(16) float s_r[kTileF];     // rewards in, advantages out
-  __shared__ __align__(16) float s_ret[kTileF];
-  __shared__ int32_t s_fr[kTileF];
-  __shared__ float s_wb[kTT / 32], s_wc[kTT / 32];
-  __shared__ int s_wcnt[kTT / 32];
-  __shared__ double s_red[(kTT / 32) * 3];
-  __shared__ int64_t s_tile;
-  __shared__ float s_carry;
-  __shared__ int s_more;
-  __shared__ bool s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (int64_t)ntiles - 1 - atomicAdd(ws.counters, 1u);  // right to left
-  for (int i = tid; i < kMaskW; i += kTT) s_boot[i] = s_done[i] = 0u;
-  __syncthreads();
-  const int64_t k = s_tile;
-  const int64_t f0 = k * kTileF;
-  const int64_t nf = min((int64_t)kTileF, n_frames - f0);  // frames of this tile
-  const int64_t s0 = __ldg(ws.tile_first + k);
-  // bootstrap (and done) frames in [f0, f0 + nf]: the ends of trajectories s0, s0+1, ...
-  for (int64_t sb = s0;; sb += kTT) {
-    const int64_t s = sb + tid;
-    int more = 0;
-    if (s < n_traj) {
-      const int64_t fb = __ldg(off + s + 1) + s;  // bootstrap frame of s
-      if (fb <= f0 + nf) {
-        more = 1;
-        if (fb >= f0) {
-          const int b = (int)(fb - f0);
-          atomicOr(&s_boot[b >> 5], 1u << (b & 31));
-          if (__ldg(done + s)) atomicOr(&s_done[b >> 5], 1u << (b & 31));
-        }
-      }
-    }
-    if (!__syncthreads_or(more)) break;
-  }
-  // this thread's 8 frames and the one after them
-  const int j0 = tid * kIPT;
-  const unsigned bw = s_boot[j0 >> 5], dw = s_done[j0 >> 5];
-  const int sh = j0 & 31;
-  const unsigned bits = (bw >> sh) & 0xFFu, dbits = (dw >> sh) & 0xFFu;
-  const unsigned nbit = ((sh + 8 < 32 ? bw >> (sh + 8) : s_boot[(j0 + 8) >> 5]) & 1u);
-  const unsigned ndbit = ((sh + 8 < 32 ? dw >> (sh + 8) : s_done[(j0 + 8) >> 5]) & 1u);
-  int valid = (int)min((int64_t)kIPT, max((int64_t)0, nf - j0));  // frames inside the batch
-  const unsigned vmask = valid >= 8 ? 0xFFu : ((1u << valid) - 1u);
-  const int ntr = __popc(~bits & vmask);  // this thread's transition frames
-  // exclusive count of transition frames before the thread (block scan)
-  int incl = ntr;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_wcnt[warp] = incl;
-  // values: 8 frames in registers (+ the next frame's), two float4 when aligned
-  float v[kIPT];
-  const float* vp = vals + f0 + j0;
-  if (valid == kIPT && ((reinterpret_cast<uintptr_t>(vp) & 15) == 0)) {
-    const float4 a = __ldcs(reinterpret_cast<const float4*>(vp));
-    const float4 b = __ldcs(reinterpret_cast<const float4*>(vp) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int j = 0; j < kIPT; ++j) v[j] = j < valid ? __ldcs(vp + j) : 0.f;
-  }
-  const float vn = (f0 + j0 + kIPT < n_frames) ? __ldg(vp + kIPT) : 0.f;
-  __syncthreads();
-  int wbase = 0, ttile = 0;
-#pragma unroll
-  for (int w = 0; w < kTT / 32; ++w) {
-    wbase += w < warp ? s_wcnt[w] : 0;
-    ttile += s_wcnt[w];
-  }
-  const int tx = wbase + incl - ntr;          // tile-local index of the first transition
-  const int64_t t_first = f0 - s0;            // the tile's first transition index
-  // rewards of the tile's transitions, coalesced, into shared memory
-  for (int i = tid; i < ttile; i += kTT) s_r[i] = __ldcs(rewards + t_first + i);
-  __syncthreads();
-  // thread map, right to left
-  float dl[kIPT];
-  float B = 0.f, C = 1.f;
-  float vnext = (nbit && ndbit) ? 0.f : vn;  // value after the thread's last frame
-  int ti = tx + ntr;                          // transition index after the thread's frames
-#pragma unroll
-  for (int j = kIPT - 1; j >= 0; --j) {
-    const bool in = j < valid;
-    const bool boot = (bits >> j) & 1u;
-    if (in && boot) {  // bootstrap frame: A = 0 (reset); v' for the frame on its left
-      dl[j] = 0.f;
-      B = 0.f;
-      C = 0.f;
-      vnext = ((dbits >> j) & 1u) ? 0.f : v[j];
-    } else if (in) {
-      --ti;
-      const float d = fmaf(g_lo, vnext, fmaf(g_hi, vnext, -v[j])) + s_r[ti];
-      dl[j] = d;
-      B = fmaf(decay, B, d);
-      C *= decay;
-      vnext = v[j];
-    } else {
-      dl[j] = 0.f;
-    }
-  }
-  // suffix scan of the thread maps: warp level, then the 8 warp maps
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const float ob = __shfl_down_sync(0xffffffffu, B, o);
-    const float oc = __shfl_down_sync(0xffffffffu, C, o);
-    if (lane + o < 32) {
-      B = fmaf(C, ob, B);
-      C *= oc;
-    }
-  }
-  if (lane == 0) {
-    s_wb[warp] = B;
-    s_wc[warp] = C;
-  }
-  float eb = __shfl_down_sync(0xffffffffu, B, 1), ec = __shfl_down_sync(0xffffffffu, C, 1);
-  if (lane == 31) {
-    eb = 0.f;
-    ec = 1.f;
-  }
-  __syncthreads();
-  // the map of the warps right of this one, and the tile aggregate (thread 0)
-  float rb = 0.f, rc = 1.f;
-  for (int w = kTT / 32 - 1; w > warp; --w) {  // right to left: (rb, rc) = map(w) o (rb, rc)
-    rb = fmaf(s_wc[w], rb, s_wb[w]);
-    rc *= s_wc[w];
-  }
-  if (tid == 0) {
-    // aggregate = warp 0's inclusive map composed with the warps right of it
-    const float ab = fmaf(s_wc[0], rb, s_wb[0]), ac = s_wc[0] * rc;
-    TileStatus* me = ws.status + k;
-    float carry = 0.f;  // A at frame f0 + nf (the first frame of tile k + 1)
-    if (k + 1 < ntiles) {
-      // publish what the tiles on the left need first: the inclusive value when
-      // the tile holds a reset (its left edge is then independent of the carry),
-      // else the aggregate map
-      if (ac == 0.f) {
-        me->incl = ab;
-        __threadfence();
-        st_release_status(me, 2u);
-      } else {
-        me->agg_b = ab;
-        me->agg_c = ac;
-        __threadfence();
-        st_release_status(me, 1u);
-      }
-      // look back for this tile's own carry (frames right of its last reset need it)
-      float lb = 0.f, lc = 1.f;  // composed maps of the tiles looked at
-      for (int64_t j = k + 1;; ++j) {
-        unsigned fl;
-        do {
-          fl = ld_acquire_u32(&ws.status[j].flag);
-        } while (fl == 0u);
-        if (fl == 2u) {
-          carry = fmaf(lc, __ldcg(&ws.status[j].incl), lb);
-          break;
-        }
-        const float jb = __ldcg(&ws.status[j].agg_b), jc = __ldcg(&ws.status[j].agg_c);
-        lb = fmaf(lc, jb, lb);
-        lc *= jc;
-        if (lc == 0.f || j + 1 >= ntiles) {  // a reset (or the end): nothing further matters
-          carry = lb;
-          break;
-        }
-      }
-      if (ac != 0.f) {
-        me->incl = fmaf(ac, carry, ab);
-        __threadfence();
-        st_release_status(me, 2u);
-      }
-    } else {
-      me->incl = ab;
-      __threadfence();
-      st_release_status(me, 2u);
-    }
-    s_carry = carry;
-  }
-  __syncthreads();
-  // A right of this thread's frames, then resolve right to left
-  float A = fmaf(rc, s_carry, rb);           // A right of this warp
-  A = fmaf(ec, A, eb);                       // ... right of this thread
-  float Sf = 0.f, Qf = 0.f;
-  int nbad = 0;
-  ti = tx + ntr;
-  const int32_t fbase = (int32_t)(f0 + j0);
-#pragma unroll
-  for (int j = kIPT - 1; j >= 0; --j) {
-    if (j < valid) {
-      if ((bits >> j) & 1u) {
-        A = 0.f;
-      } else {
-        A = fmaf(decay, A, dl[j]);
-        const float rt = A + v[j];
-        --ti;
-        s_r[ti] = A;
-        s_ret[ti] = rt;
-        s_fr[ti] = fbase + j;
-        Sf += A;
-        Qf = fmaf(A, A, Qf);
-        nbad += (fabsf(A) <= FLT_MAX && fabsf(rt) <= FLT_MAX) ? 0 : 1;
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < ttile; i += kTT) {
-    __stcs(adv_out + t_first + i, s_r[i]);
-    __stcs(ret_out + t_first + i, s_ret[i]);
-    if (frame_out) __stcs(frame_out + t_first + i, s_fr[i]);
-  }
-  // statistics: the tile's partial, then the last tile sums them in tile order
-  double v3[3] = {(double)Sf, (double)Qf, (double)nbad};
-  block_sum_d<3>(v3, s_red);
-  if (tid == 0) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) ws.partials[3 * k + c] = v3[c];
-    __threadfence();
-    s_last = atomicAdd(ws.counters + 1, 1u) == (unsigned)ntiles - 1u;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  double z[3] = {0.0, 0.0, 0.0};
-  for (int64_t t = tid; t < ntiles; t += kTT)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) z[c] += __ldcg(ws.partials + 3 * t + c);
-  block_sum_d<3>(z, s_red);
-  if (tid == 0) {
-    sums_out[0] = z[0];
-    sums_out[1] = z[1];
-    sums_out[2] = (double)n_transitions;
-    sums_out[3] = z[2];
-  }
-}
-
 __global__ void normalize_finalize_kernel(const double* sums, double eps, double* stats) {
   const double S = sums[0], Q = sums[1], N = sums[2];
   double flags = 0.0, mean = 0.0, var = 0.0;
@@ -667,11 +351,10 @@ __global__ void normalize_apply_kernel(const float* __restrict__ adv, int64_t n,
 using namespace accel;
 
 extern "C" size_t accel_gae_workspace_size(int64_t n_traj, int64_t n_transitions) {
-  return std::max(workspace_bytes(), tile_ws_bytes(ceil_div(n_transitions + n_traj, kTileF)));
+  (void)n_traj;
+  (void)n_transitions;
+  return workspace_bytes();
 }
-
-// Tuning knob: 0 = frame-space tile scan (default), 1 = warp-per-trajectory-range kernel.
-extern "C" void accel_gae_set_variant(int v) { g_gae_variant = v ? 1 : 0; }
 
 extern "C" int accel_gae_segmented(const float* rewards, const float* values_frames,
                                    const int64_t* traj_off, const uint8_t* done,
@@ -690,9 +373,6 @@ extern "C" int accel_gae_segmented(const float* rewards, const float* values_fra
   if (n_transitions >= (int64_t)1 << 31)
     return fail(kDimension, "N=%lld exceeds the int32 frame index range",
                 (long long)n_transitions);
-  if (n_transitions + n_traj >= (int64_t)1 << 31)
-    return fail(kDimension, "F=%lld frames exceed the int32 frame index range",
-                (long long)(n_transitions + n_traj));
   if (!sums_out) return fail(kDimension, "sums_out is NULL");
   cudaStream_t s = as_stream(stream);
   if (n_transitions == 0) {
@@ -700,27 +380,9 @@ extern "C" int accel_gae_segmented(const float* rewards, const float* values_fra
   }
   if (!rewards || !values_frames || !traj_off || !done || !adv_out || !ret_out || !workspace)
     return fail(kDimension, "NULL buffer passed to accel_gae_segmented");
-  const size_t need_ws = std::max(workspace_bytes(),
-                                  tile_ws_bytes(ceil_div(n_transitions + n_traj, kTileF)));
-  if (workspace_bytes_ < need_ws)
-    return fail(kDimension, "GAE workspace too small (%zu < %zu)", workspace_bytes_, need_ws);
-  if (g_gae_variant == 0) {  // frame-space tile scan
-    const int64_t F = n_transitions + n_traj, ntiles = ceil_div(F, kTileF);
-    TileWs tw = tile_carve(workspace, ntiles);
-    int st = check_cuda(cudaMemsetAsync(tw.counters, 0, 2 * sizeof(unsigned), s), "gae counters");
-    if (st) return st;
-    st = check_cuda(cudaMemsetAsync(tw.status, 0, (size_t)ntiles * sizeof(TileStatus), s),
-                    "gae status");
-    if (st) return st;
-    const int ib = (int)std::min<int64_t>(ceil_div(n_traj, 256), (int64_t)kNumSMs * 4);
-    gae_tile_index_kernel<<<ib, 256, 0, s>>>(traj_off, n_traj, ntiles, tw.tile_first);
-    if ((st = post_launch("gae_tile_index_kernel"))) return st;
-    gae_tile_kernel<<<(unsigned)ntiles, kTT, 0, s>>>(
-        rewards, values_frames, traj_off, done, n_traj, F, ntiles, (float)gamma,
-        (float)(gamma - (double)(float)gamma), (float)(gamma * lam), adv_out, ret_out,
-        frame_of_out, tw, n_transitions, sums_out);
-    return post_launch("gae_tile_kernel");
-  }
+  if (workspace_bytes_ < workspace_bytes())
+    return fail(kDimension, "GAE workspace too small (%zu < %zu)", workspace_bytes_,
+                workspace_bytes());
   Workspace ws = carve(workspace);
   int st = check_cuda(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), s), "gae counter");
   if (st) return st;

@@ -18,15 +18,6 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-@pytest.fixture(params=["tile", "warp"], autouse=True)
-def gae_variant(request):
-    """Both scans: the frame-space tile scan (default) and the warp kernel."""
-    from paper_2603_18464_b200 import _lib
-    _lib.lib().accel_gae_set_variant(0 if request.param == "tile" else 1)
-    yield request.param
-    _lib.lib().accel_gae_set_variant(0)
-
-
 def _run(lengths, done, gamma=0.99, lam=0.95, seed=0):
     import torch
 
