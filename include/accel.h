@@ -378,6 +378,14 @@ int accel_wm_adam(double* params, const double* grads, double* m, double* v, int
  * x - hi (diagnostics; the wide GEMMs below use accel_tf32_pairs). */
 int accel_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream);
 
+/* Small products (<= a few hundred rows: e_prev / e_pos x W_head and their
+ * gradients around the factorized head): C[M, N] = op(A) op(B)^T with A(m, k)
+ * = a_trans ? A[k][m] : A[m][k], B(n, k) = b_trans ? B[k][n] : B[n][k]; fp32
+ * FMA in a fixed k order. */
+int accel_small_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                     int64_t lda, int64_t ldb, int64_t ldc, int a_trans, int b_trans,
+                     void* stream);
+
 /* ---- wide tensor-core GEMM (cfg4: O = D = 4096; csrc/tc_wide.cu) -------- */
 
 /* bf16 "pair" operand of an fp32 matrix X [rows, cols] (pitch ld elements):

@@ -91,6 +91,8 @@ _SIGNATURES = {
                                    c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_int,
                                    c_int, c_int, P]),
     "accel_tc_wide_tiles": (c_int, [c_int64, c_int64, c_int]),
+    "accel_small_gemm": (c_int, [P, P, P, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
+                                 c_int, c_int, P]),
     "accel_tc_wide_set_chunk": (None, [c_int]),
     "accel_tf32_pairs": (c_int, [P, c_int64, c_int64, c_int64, P, c_int64, c_int, c_int, P]),
     "accel_tc_rows_grid": (c_int, [c_int64]),

@@ -327,3 +327,75 @@ extern "C" int accel_tanh_grad_colsum(float* g, const float* h, int64_t R, int C
   tanh_grad_colsum_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(g, h, R, C, col_part);
   return post_launch("tanh_grad_colsum_kernel");
 }
+
+// ---- small products -------------------------------------------------------------
+// C[M, N] = sum_k A(m, k) B(n, k) for the handful of tiny products around the
+// factorized head (e_prev / e_pos times W_head and their gradients: <= 264
+// rows, models.py:181-182, :191-197): 32 x 32 output tiles through shared
+// memory, fp32 FMA in a fixed k order (exact like a SIMT library GEMM, and
+// one short launch instead of a persistent tensor-core kernel's prologue).
+namespace accel {
+namespace {
+
+constexpr int kSgT = 32;
+
+__global__ void __launch_bounds__(256)
+small_gemm_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+                  int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
+                  int b_trans) {
+  __shared__ float sa[kSgT][kSgT + 1], sb[kSgT][kSgT + 1];  // [k][m], [k][n]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int m0 = blockIdx.y * kSgT, n0 = blockIdx.x * kSgT;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};  // rows ty, ty + 8, ty + 16, ty + 24; column tx
+  for (int k0 = 0; k0 < K; k0 += kSgT) {
+    for (int i = threadIdx.x; i < kSgT * kSgT; i += 256) {
+      const int r = i >> 5, c = i & 31;  // loads walk the contiguous dimension
+      // A tile: element (m0 + mm, k0 + kk)
+      {
+        const int mm = a_trans ? c : r, kk = a_trans ? r : c;
+        const int m = m0 + mm, k = k0 + kk;
+        sa[kk][mm] = (m < M && k < K) ? (a_trans ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k])
+                                      : 0.f;
+      }
+      {
+        const int nn = b_trans ? c : r, kk = b_trans ? r : c;
+        const int n = n0 + nn, k = k0 + kk;
+        sb[kk][nn] = (n < N && k < K) ? (b_trans ? B[(int64_t)k * ldb + n] : B[(int64_t)n * ldb + k])
+                                      : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kSgT; ++kk) {
+      const float b = sb[kk][tx];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = fmaf(sa[kk][ty + 8 * r], b, acc[r]);
+    }
+    __syncthreads();
+  }
+  const int n = n0 + tx;
+  if (n < N)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int m = m0 + ty + 8 * r;
+      if (m < M) C[(int64_t)m * ldc + n] = acc[r];
+    }
+}
+
+}  // namespace
+}  // namespace accel
+
+// C[M, N] = op(A) op(B)^T: A(m, k) = a_trans ? A[k][m] : A[m][k], B(n, k) =
+// b_trans ? B[k][n] : B[n][k]; fp32, fixed order, for small products.
+extern "C" int accel_small_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N,
+                                int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
+                                int b_trans, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+    return accel::fail(accel::kDimension, "small_gemm: bad sizes");
+  if (M == 0 || N == 0) return accel::kOk;
+  if (!A || !B || !C) return accel::fail(accel::kDimension, "small_gemm: NULL buffer");
+  dim3 grid((unsigned)accel::ceil_div(N, accel::kSgT), (unsigned)accel::ceil_div(M, accel::kSgT));
+  accel::small_gemm_kernel<<<grid, 256, 0, accel::as_stream(stream)>>>(
+      A, B, C, (int)M, (int)N, (int)K, lda, ldb, ldc, a_trans, b_trans);
+  return accel::post_launch("small_gemm_kernel");
+}

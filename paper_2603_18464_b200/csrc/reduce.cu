@@ -31,15 +31,75 @@ struct Segs {
   int64_t pitch[kMaxSegs];
 };
 
-__global__ void reduce_segments_kernel(Segs s) {
+// Two fixed-order schedules (chosen by the segment's part count only, so every
+// launch of a segment sums in the same order):
+//  * few parts (< 16): a lane owns 4 columns and adds the parts in order;
+//  * many parts (the per-CTA weight-gradient partials): the 8 warps of a block
+//    each add a fixed 1/8 of the parts for the same 128 columns, then the warp
+//    sums are added in warp order -- 8x the loads in flight of one chain.
+__device__ __forceinline__ void load4(const float* p, bool vec, int64_t j, int64_t len, double* a) {
+  if (vec && j + 3 < len) {
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(p + j));
+    a[0] += (double)x.x;
+    a[1] += (double)x.y;
+    a[2] += (double)x.z;
+    a[3] += (double)x.w;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (j + c < len) a[c] += (double)p[j + c];
+  }
+}
+
+__device__ __forceinline__ void store4(float* p, bool vec, int64_t j, int64_t len, const double* a) {
+  if (vec && j + 3 < len) {
+    *reinterpret_cast<float4*>(p + j) = make_float4((float)a[0], (float)a[1], (float)a[2], (float)a[3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (j + c < len) p[j + c] = (float)a[c];
+  }
+}
+
+__global__ void __launch_bounds__(256) reduce_segments_kernel(Segs s) {
+  __shared__ double red[8][32][4];
   const int seg = blockIdx.y;
   const int64_t len = s.len[seg], parts = s.parts[seg], pitch = s.pitch[seg];
   const float* src = s.src[seg];
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int64_t p = 0; p < parts; ++p) acc += (double)src[p * pitch + j];
-    s.dst[seg][j] = (float)acc;
+  float* dst = s.dst[seg];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool vec = ((pitch & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (parts < 16) {
+    for (int64_t j = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); j < len;
+         j += 4 * (int64_t)gridDim.x * blockDim.x) {
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int64_t p = 0; p < parts; ++p) load4(src + p * pitch, vec, j, len, a);
+      store4(dst, vec, j, len, a);
+    }
+    return;
+  }
+  const int64_t p0 = warp * parts / 8, p1 = (warp + 1) * parts / 8;
+  for (int64_t c0 = (int64_t)blockIdx.x * 128; c0 < len; c0 += (int64_t)gridDim.x * 128) {
+    const int64_t j = c0 + 4 * lane;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t p = p0;
+    for (; p + 4 <= p1; p += 4) {  // four independent rows in flight
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load4(src + (p + u) * pitch, vec, j, len, a);
+    }
+    for (; p < p1; ++p) load4(src + p * pitch, vec, j, len, a);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) red[warp][lane][c] = a[c];
+    __syncthreads();
+    if (warp == 0) {
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int w = 0; w < 8; ++w)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) t[c] += red[w][lane][c];
+      store4(dst, vec, j, len, t);
+    }
+    __syncthreads();
   }
 }
 
@@ -204,18 +264,49 @@ __global__ void adam_kernel(const float* __restrict__ p_in, const float* __restr
     g1 = AdamGroup{hyper[6], hyper[7], hyper[8], hyper[9], hyper[10], hyper[11]};
   }
   unsigned nb = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  auto one = [&](int64_t i, float pi, float gi, float mi, float vi, float& po, float& mo,
+                 float& vo) {
     const AdamGroup& G = i < n0 ? g0 : g1;
-    const double gr = g[i];
-    const double m = G.beta1 * (double)m_in[i] + (1.0 - G.beta1) * gr;
-    const double v = G.beta2 * (double)v_in[i] + (1.0 - G.beta2) * gr * gr;
+    const double gr = gi;
+    const double m = G.beta1 * (double)mi + (1.0 - G.beta1) * gr;
+    const double v = G.beta2 * (double)vi + (1.0 - G.beta2) * gr * gr;
     const double mh = m / G.bc1, vh = v / G.bc2;
-    const double w = (double)p_in[i] - G.lr * mh / (sqrt(vh) + G.eps);
-    p_out[i] = (float)w;
-    m_out[i] = (float)m;
-    v_out[i] = (float)v;
-    nb += !isfinite((float)w);
+    const double w = (double)pi - G.lr * mh / (sqrt(vh) + G.eps);
+    po = (float)w;
+    mo = (float)m;
+    vo = (float)v;
+    nb += !isfinite(po);
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool vec = (n & 3) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(p_in) | reinterpret_cast<uintptr_t>(g) |
+                     reinterpret_cast<uintptr_t>(m_in) | reinterpret_cast<uintptr_t>(v_in) |
+                     reinterpret_cast<uintptr_t>(p_out) | reinterpret_cast<uintptr_t>(m_out) |
+                     reinterpret_cast<uintptr_t>(v_out)) & 15) == 0;
+  if (vec) {  // 16-byte loads / stores, the same float64 math per element
+    for (int64_t i = 4 * t0; i < n; i += 4 * stride) {
+      const float4 p4 = __ldcs(reinterpret_cast<const float4*>(p_in + i));
+      const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + i));
+      const float4 m4 = __ldcs(reinterpret_cast<const float4*>(m_in + i));
+      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(v_in + i));
+      float4 po, mo, vo;
+      one(i, p4.x, g4.x, m4.x, v4.x, po.x, mo.x, vo.x);
+      one(i + 1, p4.y, g4.y, m4.y, v4.y, po.y, mo.y, vo.y);
+      one(i + 2, p4.z, g4.z, m4.z, v4.z, po.z, mo.z, vo.z);
+      one(i + 3, p4.w, g4.w, m4.w, v4.w, po.w, mo.w, vo.w);
+      *reinterpret_cast<float4*>(p_out + i) = po;
+      *reinterpret_cast<float4*>(m_out + i) = mo;
+      *reinterpret_cast<float4*>(v_out + i) = vo;
+    }
+  } else {
+    for (int64_t i = t0; i < n; i += stride) {
+      float po, mo, vo;
+      one(i, p_in[i], g[i], m_in[i], v_in[i], po, mo, vo);
+      p_out[i] = po;
+      m_out[i] = mo;
+      v_out[i] = vo;
+    }
   }
   nb = __reduce_add_sync(0xffffffffu, nb);
   if ((threadIdx.x & 31) == 0 && nb) atomicAdd(bad, nb);
@@ -244,7 +335,10 @@ extern "C" int accel_reduce_segments(const void* const* srcs, void* const* dsts,
     if (s.pitch[i] < lens[i]) return fail(kDimension, "reduce_segments: pitch < len");
     maxlen = std::max(maxlen, lens[i]);
   }
-  dim3 grid((unsigned)std::min<int64_t>(ceil_div(maxlen, 256), 64), (unsigned)nseg);
+  // enough CTAs to stream the largest segment at full bandwidth (wide weight
+  // gradients are 16.7 M floats at cfg4)
+  dim3 grid((unsigned)std::min<int64_t>(ceil_div(maxlen, 128), std::max(64, 2368 / nseg)),
+            (unsigned)nseg);
   reduce_segments_kernel<<<grid, 256, 0, as_stream(stream)>>>(s);
   return post_launch("reduce_segments_kernel");
 }
@@ -308,7 +402,7 @@ extern "C" int accel_adam(const float* p_in, const float* g, const float* m_in, 
     if (!(G->bc1 > 0 && G->bc2 > 0)) return fail(kDomain, "adam: bias correction must be > 0");
   }
   if (n == 0) return kOk;
-  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 4);
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 1024), (int64_t)kNumSMs * 16);
   adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(p_in, g, m_in, v_in, p_out, m_out, v_out, n,
                                                    n0, a, b, nullptr, skip, bad);
   return post_launch("adam_kernel");
@@ -324,7 +418,7 @@ extern "C" int accel_adam_dev(const float* p_in, const float* g, const float* m_
   if (n < 0 || n0 < 0 || n0 > n) return fail(kDimension, "adam: bad sizes");
   if (!hyper || !skip || !bad) return fail(kDimension, "adam: NULL buffer");
   if (n == 0) return kOk;
-  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 4);
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 1024), (int64_t)kNumSMs * 16);
   adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(p_in, g, m_in, v_in, p_out, m_out, v_out, n,
                                                    n0, AdamGroup{}, AdamGroup{}, hyper, skip, bad);
   return post_launch("adam_kernel");

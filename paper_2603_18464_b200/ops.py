@@ -73,6 +73,13 @@ def workspace(tag: str) -> Workspace:
     return _WS.setdefault(tag, Workspace())
 
 
+def stream_workspace(tag: str, nbytes: int) -> torch.Tensor:
+    """Grow-only scratch private to the current stream: launches on one stream
+    are ordered, so reuse is safe; launches on different streams (the trainer
+    runs the value-head backward beside the policy's) never share a buffer."""
+    return workspace(f"{tag}@{torch.cuda.current_stream().cuda_stream}").get(nbytes)
+
+
 # ---------------------------------------------------------------------------
 # (a) advantages
 
@@ -92,7 +99,7 @@ def gae_segmented(rewards, values_frames, traj_off, done, gamma, lam, *, adv=Non
     if frame_of is not None:
         _check(frame_of, "frame_of", I32, (n,))
     nbytes = _lib.lib().accel_gae_workspace_size(n_traj, n)
-    buf = (ws or workspace("gae")).get(nbytes)
+    buf = ws.get(nbytes) if ws is not None else stream_workspace("gae", nbytes)
     _lib.call("accel_gae_segmented", _p(rewards), _p(values_frames), _p(traj_off), _p(done),
               n_traj, n, float(gamma), float(lam), _p(adv), _p(ret), _p(frame_of), _p(sums),
               _p(buf), buf.numel(), _stream())
@@ -207,7 +214,7 @@ class Grouping:
         self.piece_key = (torch.empty(max(self.max_pieces, 1), dtype=I32, device=dev)
                           if cpb > 0 else None)
         nbytes = lib.accel_group_workspace_size_blocked(R, nkeys, self.cpb)
-        buf = workspace("group").get(nbytes)
+        buf = stream_workspace("group", nbytes)
         fo = tk = None
         K = 1
         self.row_frame = self.row_tok = self.pos = None
@@ -239,7 +246,7 @@ class Grouping:
         (accel_fact_group_sum, then the key pass)."""
         A = h2w.shape[1]
         if piece_buf is None:
-            piece_buf = workspace("group_pieces_f32").get(4 * max(self.max_pieces, 1) * A)
+            piece_buf = stream_workspace("group_pieces_f32", 4 * max(self.max_pieces, 1) * A)
         nk = self.nkeys * self.nblocks
         if self.cpb > 0:  # tsc holds the scalars at the sorted positions (sort_rows)
             _lib.call("accel_fact_group_sum2", _p(h2w), _p(epp), _p(self.row_frame),
@@ -256,7 +263,7 @@ class Grouping:
     def rows_sum(self, vals, out, piece_buf=None):
         D = vals.shape[1]
         if piece_buf is None:
-            piece_buf = workspace("group_pieces_f32").get(4 * max(self.max_pieces, 1) * D)
+            piece_buf = stream_workspace("group_pieces_f32", 4 * max(self.max_pieces, 1) * D)
         if self.cpb > 0:
             raise DimensionError("rows_sum needs a plain (unblocked) grouping")
         _lib.call("accel_grouped_rows_sum", _p(vals), self.R, D, _p(self.perm), _p(self.seg_off),
@@ -266,7 +273,7 @@ class Grouping:
 
     def _key_pass(self, piece_buf, D, out):
         if self.cpb > 0:
-            wsb = workspace("fold").get(_lib.lib().accel_fold_workspace_size(self.nkeys, D))
+            wsb = stream_workspace("fold", _lib.lib().accel_fold_workspace_size(self.nkeys, D))
             _lib.call("accel_fold_blocked_pieces", _p(piece_buf), _p(self.piece_off), self.nkeys,
                       self.nblocks, D, _p(out), _p(wsb), _stream())
         else:
@@ -303,7 +310,7 @@ def token_loss_fact(h2w, epp, frame_of, tokens, lp_old, adv, N, K, algo, sigma, 
     with tsc (f32[M, 4]) writes the per-token scalars instead of dz rows, at
     tsc_pos[t] (a frame-blocked grouping's sorted positions) when given."""
     A = h2w.shape[1]
-    counters = _stream_workspace("fact2_ctr", 8)  # main-pass / fix-up work counters
+    counters = stream_workspace("fact2_ctr", 8)  # main-pass / fix-up work counters
     _lib.call("accel_token_loss_fact2", _p(h2w), _p(epp), _p(frame_of), _p(tokens), _p(lp_old),
               _p(adv), int(N), int(K), A, int(algo), float(sigma), float(clip_eps),
               float(lambda_h), float(m_global), _p(fix_stats), _p(dz), _p(tsc), _p(tsc_pos),
@@ -369,15 +376,9 @@ def reduce_segments(segs):
     _lib.call("accel_reduce_segments", srcs, dsts, parts, lens, pitches, n, _stream())
 
 
-def _stream_workspace(tag: str, nbytes: int):
-    """Scratch private to the current stream (calls on different streams may
-    run concurrently; calls on one stream are ordered)."""
-    return workspace(f"{tag}@{torch.cuda.current_stream().cuda_stream}").get(nbytes)
-
-
 def reduce_f64(part, parts, width, mode, out):
     nbytes = _lib.lib().accel_reduce_f64_scratch_size(int(parts), int(width))
-    scratch = _stream_workspace("reduce_f64", nbytes) if nbytes else None
+    scratch = stream_workspace("reduce_f64", nbytes) if nbytes else None
     _lib.call("accel_reduce_f64", _p(part), int(parts), int(width), int(mode), _p(out),
               _p(scratch), _stream())
     return out
@@ -505,7 +506,7 @@ def tf32_pairs(x, row_pair: bool, lo_first: bool, out=None):
 def _pairs_ws(tag: str, x, row_pair: bool, lo_first: bool):
     shape = _pair_shape(x.shape[0], x.shape[1], row_pair)
     n = shape[0] * shape[1]
-    buf = workspace("pair." + tag).get(2 * n)
+    buf = stream_workspace("pair." + tag, 2 * n)
     return tf32_pairs(x, row_pair, lo_first, buf[:2 * n].view(torch.bfloat16).view(shape))
 
 
@@ -547,7 +548,7 @@ def _wide_rows(x, b, out, b_mn: bool, bias=None, tanh=False):
         return wide_gemm(x, b, out, a_mn=False, b_mn=b_mn, epi=1, bias=bias, tag="rows")
     ks = _wide_split(tiles, x.shape[1]) if tiles < sms // 2 and out.is_contiguous() else 1
     if ks > 1:
-        part = workspace("wide_part").get(4 * ks * M * N)[:4 * ks * M * N].view(F32)
+        part = stream_workspace("wide_part", 4 * ks * M * N)[:4 * ks * M * N].view(F32)
         wide_gemm(x, b, part, a_mn=False, b_mn=b_mn, epi=3, kslices=ks, tag="rows")
         reduce_segments([(part, out, ks, M * N, M * N)])
     else:
@@ -557,11 +558,34 @@ def _wide_rows(x, b, out, b_mn: bool, bias=None, tanh=False):
     return out
 
 
+SMALL_FMAS = 1 << 26  # products up to 64 M FMAs with a short output run the SIMT kernel
+
+
+def _small(M, N, K) -> bool:
+    return M <= 512 and M * N * K <= SMALL_FMAS
+
+
+def small_gemm(a, b, out, a_trans: bool, b_trans: bool):
+    """out[M, N] = op(a) op(b)^T (accel_small_gemm): a is [M, K] or (a_trans) [K, M],
+    b is [N, K] or (b_trans) [K, N]; unit column strides, any row pitch."""
+    M = a.shape[1] if a_trans else a.shape[0]
+    K = a.shape[0] if a_trans else a.shape[1]
+    N = b.shape[1] if b_trans else b.shape[0]
+    for t, nm in ((a, "a"), (b, "b"), (out, "out")):
+        if t.stride(1) != 1:
+            raise DimensionError(f"small_gemm: {nm} needs unit column stride")
+    _lib.call("accel_small_gemm", _p(a), _p(b), _p(out), M, N, K, a.stride(0), b.stride(0),
+              out.stride(0), int(a_trans), int(b_trans), _stream())
+    return out
+
+
 def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
     """out[M, N] = act(x[M, K] . w[N, K]^T + bias) (+ out): y = x W^T as in models.py."""
     M, K = x.shape
     N = w.shape[0]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
+    if bias is None and not tanh and not accumulate and _small(M, N, K):
+        return small_gemm(x, w, out, False, False)
     if not tc_rows_supported(K, N):
         if accumulate:
             raise DimensionError("wide products do not accumulate")
@@ -591,6 +615,8 @@ def tc_matmul_nn(x, w, out=None, accumulate=False):
     M, K = x.shape
     N = w.shape[1]
     out = torch.empty(M, N, dtype=F32, device=x.device) if out is None else out
+    if not accumulate and _small(M, N, K):
+        return small_gemm(x, w, out, False, True)
     if not tc_rows_supported(K, N):
         if accumulate:
             raise DimensionError("wide products do not accumulate")
@@ -658,6 +684,8 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     (deterministic)."""
     F, n = dy.shape
     k = x.shape[1]
+    if _small(n, k, F):
+        return small_gemm(dy, x, out, True, True)
     if n > 256 or k > 256:
         ks = wide_kslices(n, k, F)
         part = torch.empty(ks, n, k, dtype=F32, device=dy.device)
@@ -685,7 +713,7 @@ def wm_mlp2_grad(x, target, din, dh, dout, kind, params, grads, loss, nonfinite)
     _check(x, "x", F64, (n, din))
     _check(params, "params", F64)
     nbytes = _lib.lib().accel_wm_workspace_size(n, dh, dout)
-    buf = workspace("wm").get(nbytes)
+    buf = stream_workspace("wm", nbytes)
     _lib.call("accel_wm_mlp2_grad", _p(x), _p(target), n, din, dh, dout, int(kind), _p(params),
               _p(grads), _p(loss), _p(nonfinite), _p(buf), buf.numel(), _stream())
 

@@ -144,6 +144,24 @@ class DeviceParams:
             s_off += per
         return out
 
+    def rows(self, first: str, n_rows: int) -> torch.Tensor:
+        """[n_rows, D] view of the current parameters starting at tensor `first`
+        and running into the tensors after it (they are contiguous when each
+        tensor's size is a multiple of 4 floats, as for e_prev -> e_pos)."""
+        off = self.layout.offsets[first]
+        d = self.layout.shapes[first][-1]
+        names = list(self.layout.offsets)
+        i, rows, parts, contiguous = names.index(first), 0, [], True
+        while rows < n_rows:  # the tensors the rows run through
+            name = names[i]
+            r = int(np.prod(self.layout.shapes[name])) // d
+            contiguous &= self.layout.offsets[name] == off + rows * d
+            parts.append(self._views[self.cur][name].view(r, d))
+            rows, i = rows + r, i + 1
+        if contiguous:
+            return self.p[self.cur][off:off + n_rows * d].view(n_rows, d)
+        return torch.cat(parts)[:n_rows]  # padding between them: a small copy
+
     @property
     def pv(self) -> dict:
         return self._views[self.cur]

@@ -316,11 +316,6 @@ class _Scratch:
         return buf[:n].view(*shape) if len(shape) else buf[:1]
 
 
-def _mm(a, b, out):
-    torch.mm(a, b, out=out)
-    return out
-
-
 def _array_split_sizes(n: int, k: int) -> tuple:
     base, extra = divmod(n, k)
     return tuple(base + 1 if i < extra else base for i in range(k))
@@ -744,6 +739,12 @@ class Trainer:
                   dy.stride(0), x.stride(0), k, 1, 1, 0, 0, ks, ops._stream())
         return (part, out, 2 * ks + extra, n * k, n * k)
 
+    def _side_stream(self):
+        """The stream the value-head branch of a step runs on (per device)."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
+
     def _write_hyper(self) -> None:
         """Both Adam groups' {lr, beta1, beta2, eps, 1 - beta^t} for the next step."""
         t_pol, t_val = self.adam_policy.step + 1, self.adam_value.step + 1
@@ -805,11 +806,86 @@ class Trainer:
 
         if vcache is None:
             h1, h2 = self._backbone(batch.frames, "st.")
+
+        # ZeRO-2: each gradient bucket is reduce-scattered, updated (Adam on this
+        # rank's slice, speculative: the host adopts generation nxt only if the
+        # record accepts the step) and all-gathered as soon as the backward has
+        # written it, on a side stream (dp.DataParallel)
+        self._write_hyper()
+        self._hyper_dev.copy_(self._hyper_host, non_blocking=True)
+        adam_bad = cnt[2:3]
+        if self.comm is not None:
+            self.comm.begin_step(self.params, self._hyper_dev,
+                                 S.get("st.noskip", (1,), torch.int32).zero_(), adam_bad,
+                                 adam_fn=ops.adam_dev)
+
+        # the value-head forward / backward depends only on the (detached) hiddens
+        # and the targets: it runs on a side stream beside the policy's loss and
+        # backward (joined before the record)
+        side = self._side_stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            # value head (hiddens detached)
+            vclip = {}
+            if lc.value_clip is not None:
+                v_old = getattr(batch, "v_old", None)
+                if v_old is None:
+                    raise DomainError("value_clip needs the rollout-time values of the batch")
+                vclip = {"v_old": v_old, "vclip": lc.value_clip}
+            gw = ops.warp_grid(N)
+            vpart = S.get("st.vpart", (gw, 2 * H + 1))
+            vdpart = S.get("st.vdpart", (gw, 2), F64)
+            if vcache is not None:
+                # frame space: the revaluation pass already pooled (U, alpha) and ran the
+                # first layer (zm) on every frame; the loss covers the transition
+                # frames, bootstrap rows carry zero gradient
+                U, alpha, zm = vcache
+                ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
+                               vpart, vdpart, gw, row_frame=batch.frame_of, rows=N, **vclip)
+                if F != N:
+                    zm.index_fill_(0, batch.boot_rows, 0.0)
+                R, row_frame, step_group = F, None, batch.frame_step_group
+                ga = ops.warp_grid(F)
+                vbad_part = S.get("st.vbad", (1, 2), F64)
+                vbad_part.zero_()  # attention / step checks ran in the revaluation pass
+                nbad = 1
+            else:
+                U = S.get("st.U", (N, D))
+                alpha = S.get("st.alpha", (N, 2))
+                vbad_part = S.get("st.vbad", (gw, 2), F64)
+                nbad = gw
+                ops.value_pool(h1, h2, batch.frame_of, batch.frame_steps, N, d.n_steps, P["w_attn"],
+                               P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
+                zm = ops.tc_linear(U, P["w0v"], S.get("st.zm", (N, H)))
+                ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
+                               vpart, vdpart, gw, **vclip)
+                R, row_frame, step_group = N, batch.frame_of, batch.step_group
+                ga = gw
+            w0v_seg = self._wgrad(zm, U, G["w0v"], "w0v")  # dzm^T U
+            dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (R, D)))
+            de = S.get("st.de", (R, 2))
+            battn_part = S.get("st.battn", (ga,))
+            ops.value_attn_grad(dU, h1, h2, row_frame, alpha, de, battn_part, ga)
+            gr = ops.rows_grid(R)
+            wattn_part = S.get("st.wattn", (gr, D))
+            ops.value_attn_wgrad(de, h1, h2, row_frame, R, wattn_part, gr)
+            step_group.rows_sum(dU, G["e_step"])
+            # the value bucket is complete: its ZeRO-2 exchange starts now (dp)
+            ops.reduce_segments([
+                w0v_seg,
+                (vpart, G["w1v"], gw, H, 2 * H + 1),
+                (vpart[:, H:], G["b0v"], gw, H, 2 * H + 1),
+                (vpart[:, 2 * H:], G["b1v"], gw, 1, 2 * H + 1),
+                (battn_part, G["b_attn"], ga, 1, 1),
+                (wattn_part, G["w_attn"], gr, D, D),
+            ])
+            self._bucket_done("w_attn")
+
         if fact:
             # logits = H2W[frame] + EP[prev] + PP[k] + b: three small GEMMs, no [M, A] logits
             h2w = ops.tc_linear(h2, P["w_head"], S.get("st.h2w", (F, A)))
-            ep = _mm(P["e_prev"], P["w_head"].t(), S.get("st.ep", (A + 1, A)))
-            pp = _mm(P["e_pos"], P["w_head"].t(), S.get("st.pp", (K, A)))
+            ep = ops.tc_linear(P["e_prev"], P["w_head"], S.get("st.ep", (A + 1, A)))
+            pp = ops.tc_linear(P["e_pos"], P["w_head"], S.get("st.pp", (K, A)))
             epp = ops.ep_plus(ep, pp, P["b_head"], K, S.get("st.epp", ((A + 1) * K, A)))
             gf = ops.fact_partials(N, K, A, self.recompute_dz)
             # recompute_dz (default where K <= 8, A in {128, 256}): per-token
@@ -865,73 +941,6 @@ class Trainer:
                            algo, lc.sigma, lc.clip_eps, lc.lambda_h, M_glob, dlogits, None,
                            dbias_part, None, None, fix_stats=loss_sums)
 
-        # ZeRO-2: each gradient bucket is reduce-scattered, updated (Adam on this
-        # rank's slice, speculative: the host adopts generation nxt only if the
-        # record accepts the step) and all-gathered as soon as the backward has
-        # written it, on a side stream (dp.DataParallel)
-        self._write_hyper()
-        self._hyper_dev.copy_(self._hyper_host, non_blocking=True)
-        adam_bad = cnt[2:3]
-        if self.comm is not None:
-            self.comm.begin_step(self.params, self._hyper_dev,
-                                 S.get("st.noskip", (1,), torch.int32).zero_(), adam_bad,
-                                 adam_fn=ops.adam_dev)
-
-        # value head (hiddens detached)
-        vclip = {}
-        if lc.value_clip is not None:
-            v_old = getattr(batch, "v_old", None)
-            if v_old is None:
-                raise DomainError("value_clip needs the rollout-time values of the batch")
-            vclip = {"v_old": v_old, "vclip": lc.value_clip}
-        gw = ops.warp_grid(N)
-        vpart = S.get("st.vpart", (gw, 2 * H + 1))
-        vdpart = S.get("st.vdpart", (gw, 2), F64)
-        if vcache is not None:
-            # frame space: the revaluation pass already pooled (U, alpha) and ran the
-            # first layer (zm) on every frame; the loss covers the transition
-            # frames, bootstrap rows carry zero gradient
-            U, alpha, zm = vcache
-            ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
-                           vpart, vdpart, gw, row_frame=batch.frame_of, rows=N, **vclip)
-            if F != N:
-                zm.index_fill_(0, batch.boot_rows, 0.0)
-            R, row_frame, step_group = F, None, batch.frame_step_group
-            ga = ops.warp_grid(F)
-            vbad_part = S.get("st.vbad", (1, 2), F64)
-            vbad_part.zero_()  # attention / step checks ran in the revaluation pass
-            nbad = 1
-        else:
-            U = S.get("st.U", (N, D))
-            alpha = S.get("st.alpha", (N, 2))
-            vbad_part = S.get("st.vbad", (gw, 2), F64)
-            nbad = gw
-            ops.value_pool(h1, h2, batch.frame_of, batch.frame_steps, N, d.n_steps, P["w_attn"],
-                           P["b_attn"], P["e_step"], U, alpha, vbad_part, gw)
-            zm = ops.tc_linear(U, P["w0v"], S.get("st.zm", (N, H)))
-            ops.value_head(zm, P["b0v"], P["w1v"], P["b1v"], batch.ret, lc.lambda_v, N_glob, None,
-                           vpart, vdpart, gw, **vclip)
-            R, row_frame, step_group = N, batch.frame_of, batch.step_group
-            ga = gw
-        w0v_seg = self._wgrad(zm, U, G["w0v"], "w0v")  # dzm^T U
-        dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (R, D)))
-        de = S.get("st.de", (R, 2))
-        battn_part = S.get("st.battn", (ga,))
-        ops.value_attn_grad(dU, h1, h2, row_frame, alpha, de, battn_part, ga)
-        gr = ops.rows_grid(R)
-        wattn_part = S.get("st.wattn", (gr, D))
-        ops.value_attn_wgrad(de, h1, h2, row_frame, R, wattn_part, gr)
-        step_group.rows_sum(dU, G["e_step"])
-        # the value bucket is complete: its ZeRO-2 exchange starts now (dp)
-        ops.reduce_segments([
-            w0v_seg,
-            (vpart, G["w1v"], gw, H, 2 * H + 1),
-            (vpart[:, H:], G["b0v"], gw, H, 2 * H + 1),
-            (vpart[:, 2 * H:], G["b1v"], gw, 1, 2 * H + 1),
-            (battn_part, G["b_attn"], ga, 1, 1),
-            (wattn_part, G["w_attn"], gr, D, D),
-        ])
-        self._bucket_done("w_attn")
 
         # policy backward
         if fact:
@@ -943,17 +952,18 @@ class Trainer:
                                                        tsc, K, dpk_buf)
                 else:
                     dpk = batch.pk_group.rows_sum(dz, dpk_buf)
-            dprev = S.get("st.dprev", (A + 1, A))
-            dpos = S.get("st.dpos", (K, A))
+            dpp = S.get("st.dpp", (A + 1 + K, A))  # [Dprev; Dpos]
+            dprev, dpos = dpp[:A + 1], dpp[A + 1:]
             ops.pk_marginals(dpk, K, A, dprev, dpos)
             # dW_head = G^T h2 + Dprev^T e_prev + Dpos^T e_pos   (sum_t dz_t (x) c_t):
             # the two small products ride along as one extra partial slice
             seg = self._wgrad(g_frame, h2, G["w_head"], "w_head", extra=1)
             small = seg[0][seg[2] - 1]
-            torch.mm(dprev.t(), P["e_prev"], out=small)
-            small.addmm_(dpos.t(), P["e_pos"])
-            _mm(dprev, P["w_head"], G["e_prev"])
-            _mm(dpos, P["w_head"], G["e_pos"])
+            # [Dprev; Dpos]^T [e_prev; e_pos] in one reduction (e_prev and e_pos are
+            # adjacent in the flat parameter buffer)
+            ops.tc_wgrad(dpp, self.params.rows("e_prev", A + 1 + K), small)
+            ops.tc_matmul_nn(dprev, P["w_head"], G["e_prev"])
+            ops.tc_matmul_nn(dpos, P["w_head"], G["e_pos"])
             ops.reduce_segments([seg, (dpos, G["b_head"], K, A, A)])
             self._bucket_done("w_head")
             # dpre2 = (G W_head) (1 - h2^2) and its column sums (db1), one kernel
@@ -982,6 +992,7 @@ class Trainer:
         ops.reduce_segments([self._wgrad(dh1, batch.frames, G["w0"], "w0"),
                              (db0_part, G["b0"], gt, D, D)])
         self._bucket_done("w0")
+        torch.cuda.current_stream().wait_stream(side)  # the value branch has finished
         value_sums = S.get("st.vsum", (2,), F64)
         attn_bad = S.get("st.abad", (2,), F64)
         ops.reduce_f64(vdpart, gw, 2, 0, value_sums)

@@ -73,3 +73,19 @@ def test_tc_dtanh_fused_epilogue(M, K, N):
     assert rel_err(y, ref) < 4e-6
     colsum = part[:n].double().sum(0)
     assert float((colsum - ref.sum(0)).abs().max()) < 1e-4 * float(ref.abs().sum(0).max())
+
+
+@pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_small_gemm_all_layouts(a_trans, b_trans):
+    """accel_small_gemm (the <= 264-row products around the factorized head)."""
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    M, N, K = 257, 70, 264
+    A = torch.randn(M, K, device="cuda")
+    B = torch.randn(N, K, device="cuda")
+    a = A.t().contiguous() if a_trans else A
+    b = B.t().contiguous() if b_trans else B
+    out = torch.empty(M, N, device="cuda")
+    ops.small_gemm(a, b, out, bool(a_trans), bool(b_trans))
+    assert rel_err(out, A.double() @ B.double().t()) < 1e-6
