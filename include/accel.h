@@ -401,6 +401,9 @@ int accel_tf32_pairs(const float* X, int64_t rows, int64_t cols, int64_t ld, voi
  * accumulate truncates; each chunk starts a fresh accumulator and the epilogue
  * adds chunks rounding to nearest through the output. */
 void accel_tc_wide_set_chunk(int kblocks);
+/* Tuning: 1 (default) = pairs of m tiles run as 2-CTA clusters that share each
+ * 256-wide B tile through TMA multicast; 0 = one CTA per tile. */
+void accel_tc_wide_set_multicast(int on);
 /* Work tiles (128 x BN, BN <= 256) of an M x N product (split-K sizing). */
 int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn);
 /* C = A . B^T with fp32-class accuracy from two tensor-core passes per 8-k

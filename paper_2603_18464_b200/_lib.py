@@ -94,6 +94,7 @@ _SIGNATURES = {
     "accel_small_gemm": (c_int, [P, P, P, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
                                  c_int, c_int, P]),
     "accel_tc_wide_set_chunk": (None, [c_int]),
+    "accel_tc_wide_set_multicast": (None, [c_int]),
     "accel_tf32_pairs": (c_int, [P, c_int64, c_int64, c_int64, P, c_int64, c_int, c_int, P]),
     "accel_tc_rows_grid": (c_int, [c_int64]),
     "accel_tc_linear_checked": (c_int, [P, P, P, P, c_int64, c_int64, c_int, c_int64, c_int64,

@@ -55,6 +55,7 @@ constexpr int kMaxStages = 8;
 // read-modify-write per chunk, so it is off by default (drift ~ n_mma 2^-25
 // relative: 2e-5 at K = 4096, the same accumulator cuBLAS's TF32 GEMMs use).
 int g_chunk_kb = 0;
+int g_wide_multicast = 1;  // 2-CTA clusters sharing the B tile (accel_tc_wide_set_multicast)
 constexpr size_t kWideSmem = 222 * 1024;  // dynamic (ring); + ~5 KB static
 
 enum Epi : int { kStore = 0, kBiasTanh = 1, kDtanh = 2, kPartial = 3 };
@@ -67,6 +68,7 @@ struct WideArgs {
   int64_t M, N, ldc, ldh;
   int BN, m_tiles, n_tiles, kslices, kblocks, a_mn, b_mn, epi, nstages, vec, hvec;
   int chunk_kb;      // k blocks per accumulation chunk (bounds the truncating fp32 sum)
+  int mc;            // 2-CTA clusters: m tiles 2g, 2g + 1 share (multicast) each B tile
   int a_3d, b_3d;    // MN-major operand loaded by one 3-D box per stage (MN % 64 == 0)
   uint32_t stage_bytes, a_pair_off, b_raw_off, b_pair_off, tx_bytes, tmem_cols;
 };
@@ -79,6 +81,39 @@ __device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t adesc, uint
       "setp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// ---- 2-CTA clusters sharing the B tile (TMA multicast) ----
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                               uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                               int c2, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// the MMAs of this CTA that read a stage are done: arrive on that stage's empty
+// barrier in every CTA of `mask` (the peer's B half lives in this stage too)
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}\n" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 
 // kind::f16 with bf16 A/B, fp32 D, M = 128, N = n
@@ -124,6 +159,32 @@ __device__ __forceinline__ void load_operand(unsigned char* raw, unsigned char* 
   }
 }
 
+// One CTA's half of a cluster-shared B tile (rows r0 + half * rows/2 ..), written
+// into both CTAs' shared memory at the half's offset (TMA multicast, mask 0b11).
+__device__ __forceinline__ void load_operand_half(unsigned char* raw, unsigned char* pair,
+                                                  const CUtensorMap* rmap,
+                                                  const CUtensorMap* pmap, int mn, int three_d,
+                                                  int r0, int rows, int kb, int half,
+                                                  uint64_t* bar) {
+  const int hr = rows / 2;
+  const uint32_t hoff = (uint32_t)hr * kBK * 4;  // bytes of half a tile (raw == pair)
+  raw += half * hoff;
+  pair += half * hoff;
+  r0 += half * hr;
+  if (mn && three_d) {
+    tma_load_3d_mc(raw, rmap, 0, kb * kBK, r0 / 32, bar, 3);
+    tma_load_3d_mc(pair, pmap, 0, kb * 2 * kBK, r0 / 64, bar, 3);
+  } else if (mn) {
+    for (int j = 0; j < hr / 32; ++j)
+      tma_load_2d_mc(raw + j * (kBK * 128), rmap, r0 + 32 * j, kb * kBK, bar, 3);
+    for (int j = 0; j < hr / 64; ++j)
+      tma_load_2d_mc(pair + j * (2 * kBK * 128), pmap, r0 + 64 * j, kb * 2 * kBK, bar, 3);
+  } else {
+    tma_load_2d_mc(raw, rmap, kb * kBK, r0, bar, 3);
+    tma_load_2d_mc(pair, pmap, kb * 2 * kBK, r0, bar, 3);
+  }
+}
+
 struct WideBars {
   uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
 };
@@ -143,7 +204,7 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstages; ++s) {
       mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.empty[s], 1);
+      mbar_init(&bars.empty[s], p.mc ? 2 : 1);  // both CTAs' MMAs read a shared stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.tfull[b], 1);
@@ -154,18 +215,28 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&b_raw)) : "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if (p.mc)
+    cluster_sync_all();  // the peer's barriers exist before anything is multicast into them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
-  const int64_t units = (int64_t)p.m_tiles * p.n_tiles * p.kslices;
-  const int64_t my_units = units > (int64_t)blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  // unit u -> (k slice, m tile, n tile), n fastest; its k-block range
-  auto decode = [&](int64_t u, int& ks, int& mt, int& nt, int& kb0, int& kb1) {
-    const int64_t mn = (int64_t)p.m_tiles * p.n_tiles;
+  // work units (k slice, m group, n tile), n fastest; an m group is one m tile, or
+  // the two m tiles of a cluster (rank r takes tile 2g + r, both share B)
+  const int mstep = p.mc ? 2 : 1, rank = p.mc ? (int)(blockIdx.x & 1) : 0;
+  const int64_t worker = p.mc ? blockIdx.x >> 1 : blockIdx.x;
+  const int64_t nworkers = p.mc ? gridDim.x >> 1 : gridDim.x;
+  const int64_t m_groups = (p.m_tiles + mstep - 1) / mstep;
+  const int64_t units = m_groups * p.n_tiles * p.kslices;
+  const int64_t my_units = units > worker ? (units - 1 - worker) / nworkers + 1 : 0;
+  auto decode = [&](int64_t t, int& ks, int& mt, int& nt, int& kb0, int& kb1) {
+    const int64_t u = worker + t * nworkers;
+    const int64_t mn = m_groups * p.n_tiles;
     ks = (int)(u / mn);
     const int64_t r = u - (int64_t)ks * mn;
-    mt = (int)(r / p.n_tiles);
-    nt = (int)(r - (int64_t)mt * p.n_tiles);
+    const int mg = (int)(r / p.n_tiles);
+    nt = (int)(r - (int64_t)mg * p.n_tiles);
+    mt = mg * mstep + rank;
     kb0 = (int)((int64_t)ks * p.kblocks / p.kslices);
     kb1 = (int)((int64_t)(ks + 1) * p.kblocks / p.kslices);
   };
@@ -176,7 +247,7 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
       unsigned ph = 0;
       for (int64_t t = 0; t < my_units; ++t) {
         int ks, mt, nt, kb0, kb1;
-        decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
+        decode(t, ks, mt, nt, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&bars.empty[slot], ph ^ 1u);
           unsigned char* st = smem + (size_t)slot * p.stage_bytes;
@@ -184,8 +255,12 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
           mbar_expect_tx(bar, p.tx_bytes);
           load_operand(st, st + p.a_pair_off, &a_raw, &a_pair, p.a_mn, p.a_3d, mt * kBM, kBM, kb,
                        bar);
-          load_operand(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn, p.b_3d,
-                       nt * BN, BN, kb, bar);
+          if (p.mc)
+            load_operand_half(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn,
+                              p.b_3d, nt * BN, BN, kb, rank, bar);
+          else
+            load_operand(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn, p.b_3d,
+                         nt * BN, BN, kb, bar);
           if (++slot == p.nstages) {
             slot = 0;
             ph ^= 1u;
@@ -202,7 +277,7 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
     int64_t c = 0;  // accumulation chunks issued by this CTA (TMEM buffer c & 1)
     for (int64_t t = 0; t < my_units; ++t) {
       int ks, mt, nt, kb0, kb1;
-      decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
+      decode(t, ks, mt, nt, kb0, kb1);
       for (int cb0 = kb0; cb0 < kb1; cb0 += p.chunk_kb, ++c) {
         const int cb1 = min(kb1, cb0 + p.chunk_kb);
         const int b = (int)(c & 1);
@@ -220,7 +295,10 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
             mma_bf16_w(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
                        pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf, 1u);
           }
-          mma_commit_w(&bars.empty[slot]);
+          if (p.mc)
+            mma_commit_mc(&bars.empty[slot], 3);
+          else
+            mma_commit_w(&bars.empty[slot]);
           if (++slot == p.nstages) {
             slot = 0;
             ph ^= 1u;
@@ -239,7 +317,7 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
     int64_t c = 0;
     for (int64_t t = 0; t < my_units; ++t) {
       int ks, mt, nt, kb0, kb1;
-      decode(blockIdx.x + t * gridDim.x, ks, mt, nt, kb0, kb1);
+      decode(t, ks, mt, nt, kb0, kb1);
       const int64_t row = (int64_t)mt * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
       const int64_t n0 = (int64_t)nt * BN;
@@ -345,7 +423,10 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
   }
   __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  if (p.mc)
+    cluster_sync_all();  // no multicast or remote arrive still targets this CTA
+  else
+    __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
 }
 
@@ -488,16 +569,38 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
   p.a_3d = (a_mn && M % 64 == 0 && M % kBM == 0) ? 1 : 0;
   p.b_3d = (b_mn && N % 64 == 0 && N % p.BN == 0) ? 1 : 0;
   p.chunk_kb = g_chunk_kb > 0 ? g_chunk_kb : (1 << 30);
+  // 2-CTA clusters share each 256-wide B tile: each CTA loads half of it and
+  // multicasts it to both (1/3 less L2 -> SM traffic per stage); used when the
+  // halves are whole 64-column atoms and there are m tiles to pair
+  p.mc = (g_wide_multicast && p.BN == 256 && p.m_tiles >= 2 && sm_count() >= 2) ? 1 : 0;
   if (int e = mk(&am, &apm, A, Ap, M, lda, ldap, a_mn, kBM, p.a_3d)) return e;
-  if (int e = mk(&bm, &bpm, B, Bp, N, ldb, ldbp, b_mn, p.BN, p.b_3d)) return e;
+  if (int e = mk(&bm, &bpm, B, Bp, N, ldb, ldbp, b_mn, p.mc ? p.BN / 2 : p.BN, p.b_3d)) return e;
   const size_t smem = (size_t)p.nstages * p.stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(tc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return fail(kCuda, "tc_wide smem: %s", cudaGetErrorString(e));
-  const int64_t units = (int64_t)p.m_tiles * p.n_tiles * p.kslices;
-  const int grid = (int)std::min<int64_t>(units, sm_count());
-  tc_wide_kernel<<<grid, kWThreads, smem, st>>>(am, apm, bm, bpm, p);
-  return post_launch("tc_wide_kernel");
+  if (!p.mc) {
+    const int64_t units = (int64_t)p.m_tiles * p.n_tiles * p.kslices;
+    const int grid = (int)std::min<int64_t>(units, sm_count());
+    tc_wide_kernel<<<grid, kWThreads, smem, st>>>(am, apm, bm, bpm, p);
+    return post_launch("tc_wide_kernel");
+  }
+  const int64_t pairs = ceil_div(p.m_tiles, 2) * p.n_tiles * p.kslices;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(pairs, sm_count() / 2)));
+  cfg.blockDim = dim3(kWThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, tc_wide_kernel, am, apm, bm, bpm, p);
+  if (e != cudaSuccess) return fail(kCuda, "tc_wide cluster launch: %s", cudaGetErrorString(e));
+  return post_launch("tc_wide_kernel (2-CTA clusters)");
 }
 
 }  // namespace
@@ -535,6 +638,9 @@ extern "C" int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B
 
 // Tuning knob: k blocks (16 k each) per fp32 accumulation chunk (>= 1).
 extern "C" void accel_tc_wide_set_chunk(int kblocks) { g_chunk_kb = kblocks < 0 ? 0 : kblocks; }
+
+// Tuning knob: 1 (default) = 2-CTA clusters multicasting the shared B tile, 0 = off.
+extern "C" void accel_tc_wide_set_multicast(int on) { g_wide_multicast = on ? 1 : 0; }
 
 extern "C" int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn) {
   int bn = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);

@@ -63,8 +63,10 @@ def main():
                   H.stride(0) if H is not None else 0, a_mn, b_mn, epi, 1, ops._stream())
 
     from paper_2603_18464_b200 import _lib
-    chunk = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    chunk = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    mcast = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     _lib.lib().accel_tc_wide_set_chunk(chunk)
+    _lib.lib().accel_tc_wide_set_multicast(mcast)
     case("fwd x.W^T + b, tanh (K-major x K-major)",
          lambda: call(x, ap, w, bp, out, 1, 0, 0, F, D, D, bias=b),
          lambda: (ops.tf32_pairs(x, False, False, ap), ops.tf32_pairs(w, False, True, bp)))
@@ -79,7 +81,8 @@ def main():
     t3 = timed(lambda: (torch.mm(x, w.t(), out=out), out.addmm_(x, w.t()), out.addmm_(x, w.t())))
     torch.backends.cuda.matmul.allow_tf32 = False
     t32 = timed(lambda: torch.mm(x, w.t(), out=out), reps=3)
-    print(json.dumps({"shape": {"F": F, "D": D}, "chunk_kblocks": chunk, "rows": rows,
+    print(json.dumps({"shape": {"F": F, "D": D}, "chunk_kblocks": chunk, "multicast": mcast,
+                      "rows": rows,
                       "cublas_tf32_x1_ms": t1, "cublas_3xtf32_ms": t3, "cublas_fp32_ms": t32,
                       "tf32_dense_peak_tflops_at_1965mhz": 148 * 4096 * 1.965e9 / 1e12}))
 
