@@ -401,9 +401,10 @@ int accel_tf32_pairs(const float* X, int64_t rows, int64_t cols, int64_t ld, voi
  * accumulate truncates; each chunk starts a fresh accumulator and the epilogue
  * adds chunks rounding to nearest through the output. */
 void accel_tc_wide_set_chunk(int kblocks);
-/* Tuning: 1 (default) = pairs of m tiles run as 2-CTA clusters that share each
- * 256-wide B tile through TMA multicast; 0 = one CTA per tile. */
-void accel_tc_wide_set_multicast(int on);
+/* Tuning: 2 (default) = pairs of m tiles run as one 2-SM UMMA unit
+ * (cta_group::2, clusters of 2, each CTA streaming half of the B tile);
+ * 1 = 1-SM MMAs with the shared B tile multicast; 0 = one CTA per tile. */
+void accel_tc_wide_set_multicast(int mode);
 /* Work tiles (128 x BN, BN <= 256) of an M x N product (split-K sizing). */
 int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn);
 /* C = A . B^T with fp32-class accuracy from two tensor-core passes per 8-k

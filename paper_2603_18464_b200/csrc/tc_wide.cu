@@ -55,7 +55,7 @@ constexpr int kMaxStages = 8;
 // read-modify-write per chunk, so it is off by default (drift ~ n_mma 2^-25
 // relative: 2e-5 at K = 4096, the same accumulator cuBLAS's TF32 GEMMs use).
 int g_chunk_kb = 0;
-int g_wide_multicast = 1;  // 2-CTA clusters sharing the B tile (accel_tc_wide_set_multicast)
+int g_wide_multicast = 2;  // 2-CTA clusters: 2 = 2-SM UMMA, 1 = B multicast, 0 = off
 constexpr size_t kWideSmem = 222 * 1024;  // dynamic (ring); + ~5 KB static
 
 enum Epi : int { kStore = 0, kBiasTanh = 1, kDtanh = 2, kPartial = 3 };
@@ -114,6 +114,99 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
+}
+
+// ---- 2-SM UMMA (cta_group::2): the pair computes one 256 x BN tile ----
+// The leader (cluster rank 0) issues every MMA; each CTA holds its own 128 A
+// rows and half of the B tile in its shared memory and its 128 accumulator rows
+// in its TMEM.  TMA loads of both CTAs complete on the LEADER's full barrier (the
+// peer's barrier address with the cluster-rank bit cleared).
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & kPeerMask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_cg2(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar) & kPeerMask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_w2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_bf16_w2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc));
+}
+__device__ __forceinline__ void commit2_mc(uint64_t* bar) {  // both CTAs' barrier at this offset
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}\n" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t base, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
+               : "memory");
+}
+// instruction descriptor with an explicit M (256 for cta_group::2); bf16: kind::f16 / BF16
+__device__ __forceinline__ uint32_t make_idesc_m(int n, int m, int a_mn, int b_mn, int bf16) {
+  const uint32_t fmt = bf16 ? 1u : 2u;
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+// This CTA's share of a 2-SM B tile (rows r0, rows of them) into its own B region;
+// completes on the leader's barrier.
+__device__ __forceinline__ void load_operand_cg2(unsigned char* raw, unsigned char* pair,
+                                                 const CUtensorMap* rmap, const CUtensorMap* pmap,
+                                                 int mn, int three_d, int r0, int rows, int kb,
+                                                 uint64_t* bar) {
+  if (mn && three_d) {
+    tma_load_3d_cg2(raw, rmap, 0, kb * kBK, r0 / 32, bar);
+    tma_load_3d_cg2(pair, pmap, 0, kb * 2 * kBK, r0 / 64, bar);
+  } else if (mn) {
+    for (int j = 0; j < rows / 32; ++j)
+      tma_load_2d_cg2(raw + j * (kBK * 128), rmap, r0 + 32 * j, kb * kBK, bar);
+    for (int j = 0; j < rows / 64; ++j)
+      tma_load_2d_cg2(pair + j * (2 * kBK * 128), pmap, r0 + 64 * j, kb * 2 * kBK, bar);
+  } else {
+    tma_load_2d_cg2(raw, rmap, kb * kBK, r0, bar);
+    tma_load_2d_cg2(pair, pmap, kb * 2 * kBK, r0, bar);
+  }
 }
 
 // kind::f16 with bf16 A/B, fp32 D, M = 128, N = n
@@ -189,6 +282,7 @@ struct WideBars {
   uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
 };
 
+template <int MODE>  // 0 one CTA per tile, 1 B multicast pairs, 2 2-SM UMMA pairs
 __global__ void __launch_bounds__(kWThreads, 1)
 tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant__ CUtensorMap a_pair,
                const __grid_constant__ CUtensorMap b_raw, const __grid_constant__ CUtensorMap b_pair,
@@ -200,22 +294,28 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (smem_u32(smem) & 1023) __trap();
   const int BN = p.BN;
-  if (warp == 1) tmem_alloc(&tmem_base, p.tmem_cols);
+  constexpr bool cg2 = MODE == 2;  // 2-SM UMMA; MODE 1: 1-SM MMAs, B tile multicast
+  if (warp == 1) {
+    if constexpr (cg2)
+      tmem_alloc2(&tmem_base, p.tmem_cols);
+    else
+      tmem_alloc(&tmem_base, p.tmem_cols);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstages; ++s) {
       mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.empty[s], p.mc ? 2 : 1);  // both CTAs' MMAs read a shared stage
+      mbar_init(&bars.empty[s], MODE == 1 ? 2 : 1);  // multicast: both CTAs' MMAs read it
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.tfull[b], 1);
-      mbar_init(&bars.tempty[b], 4);
+      mbar_init(&bars.tempty[b], cg2 ? 8 : 4);  // cg2: both CTAs' epilogue warps (leader's)
     }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a_raw)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&b_raw)) : "memory");
   }
   tc_fence_before();
-  if (p.mc)
+  if constexpr (MODE != 0)
     cluster_sync_all();  // the peer's barriers exist before anything is multicast into them
   else
     __syncthreads();
@@ -223,9 +323,9 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
   const uint32_t tmem = tmem_base;
   // work units (k slice, m group, n tile), n fastest; an m group is one m tile, or
   // the two m tiles of a cluster (rank r takes tile 2g + r, both share B)
-  const int mstep = p.mc ? 2 : 1, rank = p.mc ? (int)(blockIdx.x & 1) : 0;
-  const int64_t worker = p.mc ? blockIdx.x >> 1 : blockIdx.x;
-  const int64_t nworkers = p.mc ? gridDim.x >> 1 : gridDim.x;
+  const int mstep = MODE ? 2 : 1, rank = MODE ? (int)(blockIdx.x & 1) : 0;
+  const int64_t worker = MODE ? blockIdx.x >> 1 : blockIdx.x;
+  const int64_t nworkers = MODE ? gridDim.x >> 1 : gridDim.x;
   const int64_t m_groups = (p.m_tiles + mstep - 1) / mstep;
   const int64_t units = m_groups * p.n_tiles * p.kslices;
   const int64_t my_units = units > worker ? (units - 1 - worker) / nworkers + 1 : 0;
@@ -252,10 +352,22 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
           mbar_wait(&bars.empty[slot], ph ^ 1u);
           unsigned char* st = smem + (size_t)slot * p.stage_bytes;
           uint64_t* bar = &bars.full[slot];
+          if constexpr (cg2) {  // both CTAs' loads complete on the leader's barrier
+            if (rank == 0) mbar_expect_tx(bar, p.tx_bytes);
+            load_operand_cg2(st, st + p.a_pair_off, &a_raw, &a_pair, p.a_mn, p.a_3d, mt * kBM,
+                             kBM, kb, bar);
+            load_operand_cg2(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn,
+                             p.b_3d, nt * BN + rank * (BN / 2), BN / 2, kb, bar);
+            if (++slot == p.nstages) {
+              slot = 0;
+              ph ^= 1u;
+            }
+            continue;
+          }
           mbar_expect_tx(bar, p.tx_bytes);
           load_operand(st, st + p.a_pair_off, &a_raw, &a_pair, p.a_mn, p.a_3d, mt * kBM, kBM, kb,
                        bar);
-          if (p.mc)
+          if constexpr (MODE == 1)
             load_operand_half(st + p.b_raw_off, st + p.b_pair_off, &b_raw, &b_pair, p.b_mn,
                               p.b_3d, nt * BN, BN, kb, rank, bar);
           else
@@ -269,13 +381,16 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer (warp-wide loop, one elected lane issues)
-    const uint32_t id_tf = make_idesc(BN, p.a_mn, p.b_mn);
-    const uint32_t id_bf = make_idesc_bf16(BN, p.a_mn, p.b_mn);
+    // ---- MMA issuer (warp-wide loop, one elected lane issues); under cg2 the
+    // leader issues the pair's MMAs (M = 256) and the peer's MMA warp idles
+    const uint32_t id_tf = cg2 ? make_idesc_m(BN, 256, p.a_mn, p.b_mn, 0)
+                               : make_idesc(BN, p.a_mn, p.b_mn);
+    const uint32_t id_bf = cg2 ? make_idesc_m(BN, 256, p.a_mn, p.b_mn, 1)
+                               : make_idesc_bf16(BN, p.a_mn, p.b_mn);
     int slot = 0;
     unsigned ph = 0;
     int64_t c = 0;  // accumulation chunks issued by this CTA (TMEM buffer c & 1)
-    for (int64_t t = 0; t < my_units; ++t) {
+    for (int64_t t = 0; t < (cg2 && rank != 0 ? 0 : my_units); ++t) {
       int ks, mt, nt, kb0, kb1;
       decode(t, ks, mt, nt, kb0, kb1);
       for (int cb0 = kb0; cb0 < kb1; cb0 += p.chunk_kb, ++c) {
@@ -288,23 +403,37 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
           mbar_wait(&bars.full[slot], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + (size_t)slot * p.stage_bytes);
+          if constexpr (cg2) {
 #pragma unroll
-          for (int s = 0; s < kBK / 8; ++s) {
-            mma_tf32_w(d, raw_desc(st, p.a_mn, s), raw_desc(st + p.b_raw_off, p.b_mn, s), id_tf,
-                       (kb > cb0 || s > 0) ? 1u : 0u);
-            mma_bf16_w(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
-                       pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf, 1u);
+            for (int s = 0; s < kBK / 8; ++s) {
+              mma_tf32_w2(d, raw_desc(st, p.a_mn, s), raw_desc(st + p.b_raw_off, p.b_mn, s),
+                          id_tf, (kb > cb0 || s > 0) ? 1u : 0u);
+              mma_bf16_w2(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
+                          pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf);
+            }
+            commit2_mc(&bars.empty[slot]);  // both CTAs' slot is free
+          } else {
+#pragma unroll
+            for (int s = 0; s < kBK / 8; ++s) {
+              mma_tf32_w(d, raw_desc(st, p.a_mn, s), raw_desc(st + p.b_raw_off, p.b_mn, s),
+                         id_tf, (kb > cb0 || s > 0) ? 1u : 0u);
+              mma_bf16_w(d, pair_desc(st + p.a_pair_off, p.a_mn, s),
+                         pair_desc(st + p.b_pair_off, p.b_mn, s), id_bf, 1u);
+            }
+            if constexpr (MODE == 1)
+              mma_commit_mc(&bars.empty[slot], 3);
+            else
+              mma_commit_w(&bars.empty[slot]);
           }
-          if (p.mc)
-            mma_commit_mc(&bars.empty[slot], 3);
-          else
-            mma_commit_w(&bars.empty[slot]);
           if (++slot == p.nstages) {
             slot = 0;
             ph ^= 1u;
           }
         }
-        mma_commit_w(&bars.tfull[b]);
+        if constexpr (cg2)
+          commit2_mc(&bars.tfull[b]);  // both CTAs' epilogues
+        else
+          mma_commit_w(&bars.tfull[b]);
       }
     }
   } else {
@@ -408,7 +537,12 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.tempty[b]);
+        if (lane == 0) {
+          if constexpr (cg2)
+            arrive_leader(&bars.tempty[b]);  // the leader's MMA reuses the pair's buffer
+          else
+            mbar_arrive(&bars.tempty[b]);
+        }
         if (epi == kDtanh) {  // the tile's column sums, epilogue warps in fixed order
           asm volatile("bar.sync 1, 128;" ::: "memory");
           const int e = threadIdx.x - kWEpi0 * 32;
@@ -423,11 +557,16 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
   }
   __syncwarp();
   tc_fence_before();
-  if (p.mc)
+  if constexpr (MODE != 0)
     cluster_sync_all();  // no multicast or remote arrive still targets this CTA
   else
     __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, p.tmem_cols);
+  if (warp == 1) {
+    if constexpr (cg2)
+      tmem_dealloc2(tmem, p.tmem_cols);
+    else
+      tmem_dealloc(tmem, p.tmem_cols);
+  }
 }
 
 // ---- bf16 pair operands --------------------------------------------------------
@@ -513,12 +652,17 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
   p.hvec = (H && (reinterpret_cast<uintptr_t>(H) & 15) == 0 && ldh % 4 == 0) ? 1 : 0;
   // stage layout: [A raw | A pair | B raw | B pair], each region 1 KB aligned
   auto al = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
-  const uint32_t a_bytes = kBM * kBK * 4, b_bytes = (uint32_t)p.BN * kBK * 4;  // raw == pair bytes
+  // mode: 2 = 2-SM UMMA pairs (each CTA holds half the B tile), 1 = B multicast, 0 = single
+  const int m_tiles = (int)ceil_div(M, kBM);
+  p.mc = (g_wide_multicast && p.BN == 256 && m_tiles >= 2 && sm_count() >= 2) ? g_wide_multicast
+                                                                                : 0;
+  const uint32_t a_bytes = kBM * kBK * 4;  // raw == pair bytes
+  const uint32_t b_bytes = (uint32_t)(p.mc == 2 ? p.BN / 2 : p.BN) * kBK * 4;
   p.a_pair_off = al(a_bytes);
   p.b_raw_off = p.a_pair_off + al(a_bytes);
   p.b_pair_off = p.b_raw_off + al(b_bytes);
   p.stage_bytes = p.b_pair_off + al(b_bytes);
-  p.tx_bytes = 2 * (a_bytes + b_bytes);
+  p.tx_bytes = (p.mc == 2 ? 4 : 2) * (a_bytes + b_bytes);  // cg2: both CTAs' loads
   p.nstages = (int)std::min<size_t>(kMaxStages, kWideSmem / p.stage_bytes);
   if (p.nstages < 2) return fail(kDimension, "tc_wide: stage too large");
   p.tmem_cols = tmem_cols_for(2 * p.BN);
@@ -572,17 +716,17 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
   // 2-CTA clusters share each 256-wide B tile: each CTA loads half of it and
   // multicasts it to both (1/3 less L2 -> SM traffic per stage); used when the
   // halves are whole 64-column atoms and there are m tiles to pair
-  p.mc = (g_wide_multicast && p.BN == 256 && p.m_tiles >= 2 && sm_count() >= 2) ? 1 : 0;
   if (int e = mk(&am, &apm, A, Ap, M, lda, ldap, a_mn, kBM, p.a_3d)) return e;
   if (int e = mk(&bm, &bpm, B, Bp, N, ldb, ldbp, b_mn, p.mc ? p.BN / 2 : p.BN, p.b_3d)) return e;
   const size_t smem = (size_t)p.nstages * p.stage_bytes;
-  cudaError_t e = cudaFuncSetAttribute(tc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = p.mc == 2 ? tc_wide_kernel<2> : p.mc == 1 ? tc_wide_kernel<1> : tc_wide_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return fail(kCuda, "tc_wide smem: %s", cudaGetErrorString(e));
   if (!p.mc) {
     const int64_t units = (int64_t)p.m_tiles * p.n_tiles * p.kslices;
     const int grid = (int)std::min<int64_t>(units, sm_count());
-    tc_wide_kernel<<<grid, kWThreads, smem, st>>>(am, apm, bm, bpm, p);
+    kern<<<grid, kWThreads, smem, st>>>(am, apm, bm, bpm, p);
     return post_launch("tc_wide_kernel");
   }
   const int64_t pairs = ceil_div(p.m_tiles, 2) * p.n_tiles * p.kslices;
@@ -598,9 +742,9 @@ int launch_wide(const float* A, const void* Ap, const float* B, const void* Bp, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, tc_wide_kernel, am, apm, bm, bpm, p);
+  e = cudaLaunchKernelEx(&cfg, kern, am, apm, bm, bpm, p);
   if (e != cudaSuccess) return fail(kCuda, "tc_wide cluster launch: %s", cudaGetErrorString(e));
-  return post_launch("tc_wide_kernel (2-CTA clusters)");
+  return post_launch(p.mc == 2 ? "tc_wide_kernel<2> (2-SM UMMA)" : "tc_wide_kernel<1> (multicast)");
 }
 
 }  // namespace
@@ -639,8 +783,11 @@ extern "C" int accel_tc_gemm_wide(const float* A, const void* Ap, const float* B
 // Tuning knob: k blocks (16 k each) per fp32 accumulation chunk (>= 1).
 extern "C" void accel_tc_wide_set_chunk(int kblocks) { g_chunk_kb = kblocks < 0 ? 0 : kblocks; }
 
-// Tuning knob: 1 (default) = 2-CTA clusters multicasting the shared B tile, 0 = off.
-extern "C" void accel_tc_wide_set_multicast(int on) { g_wide_multicast = on ? 1 : 0; }
+// Tuning knob: 2 (default) = 2-SM UMMA pairs (cta_group::2), 1 = 1-SM MMAs with the
+// shared B tile multicast, 0 = one CTA per tile.
+extern "C" void accel_tc_wide_set_multicast(int mode) {
+  g_wide_multicast = mode < 0 ? 0 : (mode > 2 ? 2 : mode);
+}
 
 extern "C" int accel_tc_wide_tiles(int64_t M, int64_t N, int b_mn) {
   int bn = (int)std::min<int64_t>(256, (N + 31) / 32 * 32);

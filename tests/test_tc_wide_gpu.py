@@ -67,12 +67,13 @@ def test_accumulation_chunks_bound_the_drift():
     assert errs[64] < errs[0] and errs[64] < TOL
 
 
-@pytest.mark.parametrize("multicast", [0, 1])
+@pytest.mark.parametrize("multicast", [0, 1, 2])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(1000, 512, 300), (384, 4096, 64), (8256, 256, 48)])
 def test_cluster_multicast_matches_single_cta(multicast, a_mn, b_mn, M, N, K):
-    """2-CTA clusters sharing the B tile (TMA multicast, odd m-tile counts
-    included) == the one-CTA kernel == float64."""
+    """2-CTA clusters -- 1-SM MMAs with the B tile multicast (1) or 2-SM UMMA
+    pairs, cta_group::2 (2) -- odd m-tile counts included, == the one-CTA
+    kernel == float64."""
     import torch
 
     from paper_2603_18464_b200 import _lib, ops
@@ -85,7 +86,7 @@ def test_cluster_multicast_matches_single_cta(multicast, a_mn, b_mn, M, N, K):
             ops.wide_gemm(a, b, out, a_mn=bool(a_mn), b_mn=bool(b_mn))
             outs.append(out)
     finally:
-        _lib.lib().accel_tc_wide_set_multicast(1)
+        _lib.lib().accel_tc_wide_set_multicast(2)
     assert _err(outs[1], A.double() @ B.double().t()) < TOL
     assert torch.equal(outs[0], outs[1])  # same accumulation order either way
 
