@@ -131,10 +131,12 @@ class DataParallel:
            per if policy else 0, hyp, skip, bad)
         self.all_gather(params.p[nxt][s_lo:s_hi], params.p[nxt][lo:hi])
 
-    def bucket_ready(self, b: int) -> None:
-        """Bucket b's local gradients are complete on the current stream:
-        reduce-scatter it, Adam on this rank's slice, all-gather the slice
-        (on the side stream under NCCL, overlapping the caller's next kernels)."""
+    def bucket_ready(self, b: int, after=None) -> None:
+        """Bucket b's local gradients are complete on the current stream (or at
+        CUDA event `after`): reduce-scatter it, Adam on this rank's slice,
+        all-gather the slice (on the side stream under NCCL, overlapping the
+        caller's next kernels).  Collectives of one process group run in issue
+        order, so a caller issues this where the exchange should queue."""
         done = self._step[6]
         if b in done:
             return
@@ -143,8 +145,11 @@ class DataParallel:
             self._bucket(b)
             return
         timed = self.timeline is not None
-        ev = torch.cuda.Event(enable_timing=timed)
-        ev.record()
+        if after is not None:
+            ev = after
+        else:
+            ev = torch.cuda.Event(enable_timing=timed)
+            ev.record()
         with torch.cuda.stream(self._stream):
             self._stream.wait_event(ev)
             if timed:

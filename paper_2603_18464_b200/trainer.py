@@ -879,7 +879,9 @@ class Trainer:
                 (battn_part, G["b_attn"], ga, 1, 1),
                 (wattn_part, G["w_attn"], gr, D, D),
             ])
-            self._bucket_done("w_attn")
+            value_done = torch.cuda.Event(enable_timing=self.comm is not None
+                                          and self.comm.timeline is not None)
+            value_done.record()
 
         if fact:
             # logits = H2W[frame] + EP[prev] + PP[k] + b: three small GEMMs, no [M, A] logits
@@ -932,6 +934,11 @@ class Trainer:
         if self.comm is not None:
             self.comm.all_reduce_sum(loss_sums)
             self.comm.all_reduce_max(loss_max)
+        # the value bucket's exchange queues after the loss all-reduces above (one
+        # process group runs collectives in issue order: issued earlier, it would
+        # hold the FIXUP pass behind the whole value-head branch)
+        if self.comm is not None:
+            self.comm.bucket_ready(self.layout.bucket_of("w_attn"), after=value_done)
         # FIXUP: only does work when 0 < excluded < M_global (decided on the device)
         if fact:
             ops.token_loss_fact(*loss_args, None, None, None, fix_stats=loss_sums, tsc=tsc,
