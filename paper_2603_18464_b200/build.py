@@ -17,6 +17,7 @@ from __future__ import annotations
 import hashlib
 import json
 import os
+import shlex
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -31,8 +32,10 @@ INCLUDE = PKG.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# ACCEL_NVCC_DEFS: extra -D tuning defines (part of the build id), e.g. for sweeps
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-         "--expt-relaxed-constexpr", "-I", str(INCLUDE)]
+         "--expt-relaxed-constexpr", "-I", str(INCLUDE)] + \
+    shlex.split(os.environ.get("ACCEL_NVCC_DEFS", ""))
 
 
 def _flags_key() -> bytes:

@@ -546,8 +546,10 @@ tc_wide_kernel(const __grid_constant__ CUtensorMap a_raw, const __grid_constant_
         if (epi == kDtanh) {  // the tile's column sums, epilogue warps in fixed order
           asm volatile("bar.sync 1, 128;" ::: "memory");
           const int e = threadIdx.x - kWEpi0 * 32;
+          // (a 2-SM pair's second tile can lie wholly past M: col_part has no row for it)
+          const bool tile_ok = (int64_t)mt * kBM < p.M;
           for (int cc = e; cc < BN; cc += 128)
-            if (n0 + cc < p.N)
+            if (tile_ok && n0 + cc < p.N)
               p.col_part[(int64_t)mt * p.N + n0 + cc] =
                   ((s_col[0][cc] + s_col[1][cc]) + s_col[2][cc]) + s_col[3][cc];
           asm volatile("bar.sync 1, 128;" ::: "memory");

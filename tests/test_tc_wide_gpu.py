@@ -137,6 +137,29 @@ def test_bias_tanh_and_dtanh_epilogues():
     assert n2 == nt and _err(y2, want) < TOL
 
 
+@pytest.mark.parametrize("M", [528, 129, 17])
+def test_dtanh_column_sums_stay_inside_col_part(M):
+    """An odd number of 128-row tiles: the 2-SM pair's second tile lies past M
+    and must not write a column-sum row (col_part has ceil(M / 128) rows)."""
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    N, K = 512, 256
+    A = torch.randn(M, K, device="cuda") * 0.05
+    W = torch.randn(K, N, device="cuda")
+    H = torch.tanh(torch.randn(M, N, device="cuda"))
+    nt = -(-M // 128)
+    buf = torch.full((nt + 2, N), float("nan"), device="cuda")
+    buf[nt:] = 12345.0  # canary rows right after the parts
+    y = torch.empty(M, N, device="cuda")
+    ops.wide_gemm(A, W, y, a_mn=False, b_mn=True, epi=2, h=H, col_part=buf[:nt])
+    torch.cuda.synchronize()
+    assert bool((buf[nt:] == 12345.0).all())
+    want = (A.double() @ W.double()) * (1 - H.double() ** 2)
+    assert _err(y, want) < TOL
+    assert _err(buf[:nt].double().sum(0), want.sum(0)) < TOL
+
+
 def test_public_wrappers_use_the_wide_kernel():
     import torch
 
