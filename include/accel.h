@@ -293,6 +293,12 @@ int accel_value_attn_grad(const float* dU, const float* h1, const float* h2,
 int accel_value_attn_wgrad(const float* de, const float* h1, const float* h2,
                            const int32_t* row_frame, int64_t R, int D, float* part,
                            int grid, void* stream);
+/* Both of the above in one pass over (dU, h1, h2): bpart f32[grid] (db_attn),
+ * wpart f32[grid][D] (dw_attn), de f32[R, 2] optional (NULL: not written;
+ * required at widths other than D in {16, 32, 64, 128} with 16-B aligned rows). */
+int accel_value_attn_backward(const float* dU, const float* h1, const float* h2,
+                              const int32_t* row_frame, const float* alpha, int64_t R, int D,
+                              float* de, float* bpart, float* wpart, int grid, void* stream);
 
 /* ---- reductions, record, optimizer ------------------------------------- */
 
@@ -384,7 +390,12 @@ int accel_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stre
  * FMA in a fixed k order. */
 int accel_small_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
                      int64_t lda, int64_t ldb, int64_t ldc, int a_trans, int b_trans,
-                     void* stream);
+                     float* ws, int64_t ws_floats, void* stream);
+/* Workspace (floats) for split-K slices of accel_small_gemm: > 0 when the
+ * product's output tiles leave SMs idle and k is long (e.g. e_pos [7, 4096] x
+ * W_head^T at cfg4); the slices are summed in order (deterministic).  With a
+ * smaller / NULL ws the product runs unsplit. */
+int64_t accel_small_gemm_ws_floats(int64_t M, int64_t N, int64_t K);
 
 /* ---- wide tensor-core GEMM (cfg4: O = D = 4096; csrc/tc_wide.cu) -------- */
 

@@ -76,6 +76,7 @@ _SIGNATURES = {
                                  c_double, P, P, P, c_int, P]),
     "accel_value_attn_grad": (c_int, [P, P, P, P, P, c_int64, c_int, P, P, c_int, P]),
     "accel_value_attn_wgrad": (c_int, [P, P, P, P, c_int64, c_int, P, c_int, P]),
+    "accel_value_attn_backward": (c_int, [P, P, P, P, P, c_int64, c_int, P, P, P, c_int, P]),
     "accel_reduce_segments": (c_int, [P, P, P, P, P, c_int, P]),
     "accel_segment_moments": (c_int, [P, P, c_int64, P, P]),
     "accel_count_nonfinite_rows": (c_int, [P, P, c_int64, c_int, c_int64, P, P]),
@@ -92,7 +93,8 @@ _SIGNATURES = {
                                    c_int, c_int, P]),
     "accel_tc_wide_tiles": (c_int, [c_int64, c_int64, c_int]),
     "accel_small_gemm": (c_int, [P, P, P, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
-                                 c_int, c_int, P]),
+                                 c_int, c_int, P, c_int64, P]),
+    "accel_small_gemm_ws_floats": (c_int64, [c_int64, c_int64, c_int64]),
     "accel_tc_wide_set_chunk": (None, [c_int]),
     "accel_tc_wide_set_multicast": (None, [c_int]),
     "accel_tf32_pairs": (c_int, [P, c_int64, c_int64, c_int64, P, c_int64, c_int, c_int, P]),

@@ -342,25 +342,29 @@ constexpr int kSgT = 32;
 __global__ void __launch_bounds__(256)
 small_gemm_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
                   int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
-                  int b_trans) {
+                  int b_trans, int kper) {
   __shared__ float sa[kSgT][kSgT + 1], sb[kSgT][kSgT + 1];  // [k][m], [k][n]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const int m0 = blockIdx.y * kSgT, n0 = blockIdx.x * kSgT;
+  // split-K: slice blockIdx.z covers k in [z kper, (z + 1) kper) and writes its
+  // own [M, N] partial (C + z M ldc); the caller sums the slices in order
+  const int kb = blockIdx.z * kper, ke = min(K, kb + kper);
+  C += (int64_t)blockIdx.z * M * ldc;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};  // rows ty, ty + 8, ty + 16, ty + 24; column tx
-  for (int k0 = 0; k0 < K; k0 += kSgT) {
+  for (int k0 = kb; k0 < ke; k0 += kSgT) {
     for (int i = threadIdx.x; i < kSgT * kSgT; i += 256) {
       const int r = i >> 5, c = i & 31;  // loads walk the contiguous dimension
       // A tile: element (m0 + mm, k0 + kk)
       {
         const int mm = a_trans ? c : r, kk = a_trans ? r : c;
         const int m = m0 + mm, k = k0 + kk;
-        sa[kk][mm] = (m < M && k < K) ? (a_trans ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k])
+        sa[kk][mm] = (m < M && k < ke) ? (a_trans ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k])
                                       : 0.f;
       }
       {
         const int nn = b_trans ? c : r, kk = b_trans ? r : c;
         const int n = n0 + nn, k = k0 + kk;
-        sb[kk][nn] = (n < N && k < K) ? (b_trans ? B[(int64_t)k * ldb + n] : B[(int64_t)n * ldb + k])
+        sb[kk][nn] = (n < N && k < ke) ? (b_trans ? B[(int64_t)k * ldb + n] : B[(int64_t)n * ldb + k])
                                       : 0.f;
       }
     }
@@ -382,20 +386,63 @@ small_gemm_kernel(const float* __restrict__ A, const float* __restrict__ B, floa
     }
 }
 
+// C[m, n] = sum_z part[z][m][n] (slices in order: deterministic)
+__global__ void small_gemm_sum_kernel(const float* __restrict__ part, int ks, int M, int N,
+                                      float* __restrict__ C, int64_t ldc) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float a = 0.f;
+    for (int z = 0; z < ks; ++z) a += part[z * total + e];
+    C[(e / N) * ldc + e % N] = a;
+  }
+}
+
+// k slices of a small product: when its output tiles leave SMs idle and the
+// reduction is long, split k (>= 256 per slice) until ~2 waves of blocks
+int small_gemm_slices(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ceil_div(M, (int64_t)kSgT) * ceil_div(N, (int64_t)kSgT);
+  if (tiles >= kNumSMs || K < 512) return 1;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, (int64_t)256),
+                                                     2 * kNumSMs / tiles));
+}
+
 }  // namespace
 }  // namespace accel
 
 // C[M, N] = op(A) op(B)^T: A(m, k) = a_trans ? A[k][m] : A[m][k], B(n, k) =
 // b_trans ? B[k][n] : B[n][k]; fp32, fixed order, for small products.
+extern "C" int64_t accel_small_gemm_ws_floats(int64_t M, int64_t N, int64_t K) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  const int ks = accel::small_gemm_slices(M, N, K);
+  return ks > 1 ? (int64_t)ks * M * N : 0;
+}
+
 extern "C" int accel_small_gemm(const float* A, const float* B, float* C, int64_t M, int64_t N,
                                 int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int a_trans,
-                                int b_trans, void* stream) {
+                                int b_trans, float* ws, int64_t ws_floats, void* stream) {
   if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     return accel::fail(accel::kDimension, "small_gemm: bad sizes");
   if (M == 0 || N == 0) return accel::kOk;
   if (!A || !B || !C) return accel::fail(accel::kDimension, "small_gemm: NULL buffer");
-  dim3 grid((unsigned)accel::ceil_div(N, accel::kSgT), (unsigned)accel::ceil_div(M, accel::kSgT));
-  accel::small_gemm_kernel<<<grid, 256, 0, accel::as_stream(stream)>>>(
-      A, B, C, (int)M, (int)N, (int)K, lda, ldb, ldc, a_trans, b_trans);
-  return accel::post_launch("small_gemm_kernel");
+  cudaStream_t s = accel::as_stream(stream);
+  int ks = accel::small_gemm_slices(M, N, K);
+  if (ks > 1 && (!ws || ws_floats < (int64_t)ks * M * N)) ks = 1;  // no workspace: one slice
+  const int kper = (int)(accel::ceil_div(accel::ceil_div(K, (int64_t)ks), (int64_t)accel::kSgT) *
+                         accel::kSgT);
+  ks = (int)accel::ceil_div(K, (int64_t)kper);
+  dim3 grid((unsigned)accel::ceil_div(N, accel::kSgT), (unsigned)accel::ceil_div(M, accel::kSgT),
+            (unsigned)ks);
+  if (ks == 1) {
+    accel::small_gemm_kernel<<<grid, 256, 0, s>>>(A, B, C, (int)M, (int)N, (int)K, lda, ldb, ldc,
+                                                  a_trans, b_trans, (int)K);
+    return accel::post_launch("small_gemm_kernel");
+  }
+  accel::small_gemm_kernel<<<grid, 256, 0, s>>>(A, B, ws, (int)M, (int)N, (int)K, lda, ldb, N,
+                                                a_trans, b_trans, kper);
+  int rc = accel::post_launch("small_gemm_kernel");
+  if (rc != accel::kOk) return rc;
+  const int g2 = (int)std::min<int64_t>(accel::ceil_div(M * N, (int64_t)256), 1184);
+  accel::small_gemm_sum_kernel<<<g2, 256, 0, s>>>(ws, ks, (int)M, (int)N, C, ldc);
+  return accel::post_launch("small_gemm_sum_kernel");
 }

@@ -631,7 +631,10 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
 // The transition's H2W row and EPP rows k >= 1 land in shared memory by bulk
 // copy, double-buffered a whole transition ahead (one mbarrier per buffer);
 // the chunk-start row EPP[A, 0] (every transition's token 0) is resident per CTA.
-constexpr int kF2MaxWarps = 7;
+#ifndef ACCEL_F2_WARPS
+#define ACCEL_F2_WARPS 7
+#endif
+constexpr int kF2MaxWarps = ACCEL_F2_WARPS;
 constexpr int kF2Chunk = 32;  // transitions per dynamically claimed chunk (and statistics row)
 
 // After the call lane l holds the warp total of value index l / (32 / NV).

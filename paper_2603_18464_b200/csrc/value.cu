@@ -244,6 +244,91 @@ value_attn_grad4_kernel(const float* __restrict__ dU, const float* __restrict__ 
   }
 }
 
+// Fused attention backward (value_attn_grad4 + value_attn_wgrad4 in one pass):
+// the row's h1 / h2 chunks are already in registers for dalpha, so the score
+// gradients de feed the dw_attn sums directly instead of a second pass over
+// h1, h2 and de.  Every lane of a row group holds the butterfly totals, so
+// each accumulates de_0 h1 + de_1 h2 for its float4 of columns; the block's
+// lanes are then summed in thread order (deterministic for a fixed grid).
+// wpart f32[grid][4 LPR], bpart f32[grid]; de (optional) f32[R, 2].
+template <int LPR>
+__global__ void __launch_bounds__(kThreads)
+value_attn_bwd4_kernel(const float* __restrict__ dU, const float* __restrict__ h1,
+                       const float* __restrict__ h2, const int32_t* __restrict__ row_frame,
+                       const float* __restrict__ alpha, int64_t R, float* __restrict__ de,
+                       float* __restrict__ bpart, float* __restrict__ wpart) {
+  constexpr int RPW = 32 / LPR;
+  constexpr int D4 = LPR;
+  __shared__ float s_b[kWarps];
+  __shared__ float4 s_w[kThreads];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sl = lane % LPR;
+  float gb = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t step = (int64_t)gridDim.x * kWarps * RPW * 2;
+  for (int64_t r0 = gw * RPW * 2; r0 < R; r0 += step) {
+    int64_t r[2] = {r0 + slot, r0 + RPW + slot};
+    float d0[2], d1[2];
+    float4 a[2], c[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const bool ok = r[q] < R;
+      const int64_t rr = ok ? r[q] : 0;
+      const int64_t f = row_frame ? __ldg(row_frame + rr) : rr;
+      const float4 g = __ldg(reinterpret_cast<const float4*>(dU + rr * 4 * D4) + sl);
+      a[q] = __ldg(reinterpret_cast<const float4*>(h1 + f * 4 * D4) + sl);
+      c[q] = __ldg(reinterpret_cast<const float4*>(h2 + f * 4 * D4) + sl);
+      d0[q] = g.x * a[q].x + g.y * a[q].y + g.z * a[q].z + g.w * a[q].w;
+      d1[q] = g.x * c[q].x + g.y * c[q].y + g.z * c[q].z + g.w * c[q].w;
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        d0[q] += __shfl_xor_sync(0xffffffffu, d0[q], o);
+        d1[q] += __shfl_xor_sync(0xffffffffu, d1[q], o);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (r[q] >= R) continue;
+      const float a0 = __ldg(alpha + 2 * r[q]), a1 = __ldg(alpha + 2 * r[q] + 1);
+      const float s = a0 * d0[q] + a1 * d1[q];
+      const float x0 = a0 * (d0[q] - s), x1 = a1 * (d1[q] - s);
+      acc.x = fmaf(x0, a[q].x, fmaf(x1, c[q].x, acc.x));
+      acc.y = fmaf(x0, a[q].y, fmaf(x1, c[q].y, acc.y));
+      acc.z = fmaf(x0, a[q].z, fmaf(x1, c[q].z, acc.z));
+      acc.w = fmaf(x0, a[q].w, fmaf(x1, c[q].w, acc.w));
+      if (sl == 0) {
+        if (de) {
+          de[2 * r[q]] = x0;
+          de[2 * r[q] + 1] = x1;
+        }
+        gb += x0 + x1;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) gb += __shfl_xor_sync(0xffffffffu, gb, o);
+  if (lane == 0) s_b[warp] = gb;
+  s_w[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = 0.f;
+    for (int w2 = 0; w2 < kWarps; ++w2) b += s_b[w2];
+    bpart[blockIdx.x] = b;
+  }
+  if (threadIdx.x < D4) {  // column group t: the block's row lanes in thread order
+    float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = threadIdx.x; u < kThreads; u += D4) {
+      const float4 y = s_w[u];
+      w.x += y.x; w.y += y.y; w.z += y.z; w.w += y.w;
+    }
+    reinterpret_cast<float4*>(wpart + (int64_t)blockIdx.x * D4 * 4)[threadIdx.x] = w;
+  }
+}
+
 // part layout per block: [dw1v (H) | db0v (H) | db1v (1)]; dpart: [sum err^2, non-finite v]
 __global__ void __launch_bounds__(kThreads)
 value_head_kernel(float* __restrict__ zm, const int32_t* __restrict__ row_frame,
@@ -668,3 +753,31 @@ extern "C" int accel_value_attn_wgrad(const float* de, const float* h1, const fl
                                                                              R, D, part);
   return post_launch("value_attn_wgrad_kernel");
 }
+
+extern "C" int accel_value_attn_backward(const float* dU, const float* h1, const float* h2,
+                                         const int32_t* row_frame, const float* alpha, int64_t R,
+                                         int D, float* de, float* bpart, float* wpart, int grid,
+                                         void* stream) {
+  if (R < 0 || D < 1 || grid < 1) return fail(kDimension, "value_attn_backward: bad sizes");
+  if (R == 0) return kOk;
+  if (!dU || !h1 || !h2 || !alpha || !bpart || !wpart)
+    return fail(kDimension, "value_attn_backward: NULL buffer");
+  const uintptr_t al = reinterpret_cast<uintptr_t>(h1) | reinterpret_cast<uintptr_t>(h2) |
+                       reinterpret_cast<uintptr_t>(dU) | reinterpret_cast<uintptr_t>(wpart);
+  if ((al & 15) != 0 || !(D == 16 || D == 32 || D == 64 || D == 128)) {
+    // general widths: the two-pass kernels (they need the de rows)
+    if (!de) return fail(kDimension, "value_attn_backward: de buffer needed at this width");
+    const int rc = accel_value_attn_grad(dU, h1, h2, row_frame, alpha, R, D, de, bpart, grid, stream);
+    if (rc != kOk) return rc;
+    return accel_value_attn_wgrad(de, h1, h2, row_frame, R, D, wpart, grid, stream);
+  }
+  cudaStream_t s = as_stream(stream);
+  switch (D / 4) {
+    case 4: value_attn_bwd4_kernel<4><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, bpart, wpart); break;
+    case 8: value_attn_bwd4_kernel<8><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, bpart, wpart); break;
+    case 16: value_attn_bwd4_kernel<16><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, bpart, wpart); break;
+    default: value_attn_bwd4_kernel<32><<<grid, kThreads, 0, s>>>(dU, h1, h2, row_frame, alpha, R, de, bpart, wpart); break;
+  }
+  return post_launch("value_attn_bwd4_kernel");
+}
+

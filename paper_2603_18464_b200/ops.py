@@ -354,6 +354,12 @@ def value_attn_grad(dU, h1, h2, row_frame, alpha, de, part, grid):
               dU.shape[0], dU.shape[1], _p(de), _p(part), int(grid), _stream())
 
 
+def value_attn_backward(dU, h1, h2, row_frame, alpha, bpart, wpart, grid, de=None):
+    """value_attn_grad + value_attn_wgrad in one pass (de rows optional)."""
+    _lib.call("accel_value_attn_backward", _p(dU), _p(h1), _p(h2), _p(row_frame), _p(alpha),
+              dU.shape[0], dU.shape[1], _p(de), _p(bpart), _p(wpart), int(grid), _stream())
+
+
 def value_attn_wgrad(de, h1, h2, row_frame, R, part, grid):
     _lib.call("accel_value_attn_wgrad", _p(de), _p(h1), _p(h2), _p(row_frame), R, h1.shape[1],
               _p(part), int(grid), _stream())
@@ -574,8 +580,10 @@ def small_gemm(a, b, out, a_trans: bool, b_trans: bool):
     for t, nm in ((a, "a"), (b, "b"), (out, "out")):
         if t.stride(1) != 1:
             raise DimensionError(f"small_gemm: {nm} needs unit column stride")
+    nws = int(_lib.lib().accel_small_gemm_ws_floats(M, N, K))
+    ws = stream_workspace("small_gemm", 4 * nws) if nws else None
     _lib.call("accel_small_gemm", _p(a), _p(b), _p(out), M, N, K, a.stride(0), b.stride(0),
-              out.stride(0), int(a_trans), int(b_trans), _stream())
+              out.stride(0), int(a_trans), int(b_trans), _p(ws), nws, _stream())
     return out
 
 

@@ -863,12 +863,13 @@ class Trainer:
                 ga = gw
             w0v_seg = self._wgrad(zm, U, G["w0v"], "w0v")  # dzm^T U
             dU = ops.tc_matmul_nn(zm, P["w0v"], S.get("st.dU", (R, D)))
-            de = S.get("st.de", (R, 2))
             battn_part = S.get("st.battn", (ga,))
-            ops.value_attn_grad(dU, h1, h2, row_frame, alpha, de, battn_part, ga)
-            gr = ops.rows_grid(R)
-            wattn_part = S.get("st.wattn", (gr, D))
-            ops.value_attn_wgrad(de, h1, h2, row_frame, R, wattn_part, gr)
+            wattn_part = S.get("st.wattn", (ga, D))
+            gr = ga
+            # dalpha, de and the dw_attn / db_attn partials in one pass over (dU, h1, h2)
+            # (the de rows are only needed by the two-pass fallback at other widths)
+            ops.value_attn_backward(dU, h1, h2, row_frame, alpha, battn_part, wattn_part, ga,
+                                    de=S.get("st.de", (R, 2)))
             step_group.rows_sum(dU, G["e_step"])
             # the value bucket is complete: its ZeRO-2 exchange starts now (dp)
             ops.reduce_segments([
