@@ -202,9 +202,9 @@ int accel_dc_reduce(const float* dc, const float* h2, const int32_t* frame_of,
                     int64_t N, int K, int D, float* dz2, float* pos_part,
                     float* db1_part, int grid, void* stream);
 
-/* g = g (1 - h^2) in place over f32[R, C]; col_part f32[grid][C] —
- * models.py:202-204 (dz1 and db0). */
-int accel_tanh_grad_colsum(float* g, const float* h, int64_t R, int C,
+/* g = g (1 - h^2) in place over f32[R, C] (row pitches ldg, ldh >= C);
+ * col_part f32[grid][C] — models.py:202-204 (dz1 and db0). */
+int accel_tanh_grad_colsum(float* g, int64_t ldg, const float* h, int64_t ldh, int64_t R, int C,
                            float* col_part, int grid, void* stream);
 
 /* ---- deterministic scatter-add (np.add.at, models.py:195 and :305) ------ */

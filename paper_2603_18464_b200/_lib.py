@@ -36,7 +36,7 @@ _SIGNATURES = {
     "accel_build_c": (c_int, [P, P, P, P, P, c_int64, c_int, c_int, c_int, P, P]),
     "accel_rows_grid": (c_int, [c_int64]),
     "accel_dc_reduce": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, P, c_int, P]),
-    "accel_tanh_grad_colsum": (c_int, [P, P, c_int64, c_int, P, c_int, P]),
+    "accel_tanh_grad_colsum": (c_int, [P, c_int64, P, c_int64, c_int64, c_int, P, c_int, P]),
     "accel_prev_keys": (c_int, [P, c_int64, c_int, c_int, c_int, P, P]),
     "accel_fact_grid": (c_int, [c_int64]),
     "accel_fact_partials": (c_int64, [c_int64, c_int, c_int, c_int]),

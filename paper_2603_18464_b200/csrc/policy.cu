@@ -156,8 +156,8 @@ dc_reduce_kernel(const float* __restrict__ dc, const float* __restrict__ h2,
 
 // g <- g * (1 - h^2) in place over [R, C]; per-CTA column sums of the result.
 __global__ void __launch_bounds__(kThreads)
-tanh_grad_colsum_kernel(float* __restrict__ g, const float* __restrict__ h, int64_t R, int C,
-                        float* __restrict__ col_part) {
+tanh_grad_colsum_kernel(float* __restrict__ g, int64_t ldg, const float* __restrict__ h,
+                        int64_t ldh, int64_t R, int C, float* __restrict__ col_part) {
   extern __shared__ float s_acc[];  // [sub][span]
   const ColLayout L = ColLayout::make(C);
   const int lane_row = threadIdx.x / L.span, lane_col = threadIdx.x % L.span;
@@ -168,9 +168,9 @@ tanh_grad_colsum_kernel(float* __restrict__ g, const float* __restrict__ h, int6
     float acc = 0.f;
     if (c < C) {
       for (int64_t r = r_begin + lane_row; r < r_end; r += L.sub) {
-        const float hv = __ldg(h + r * C + c);
-        const float v = g[r * C + c] * (1.f - hv * hv);
-        g[r * C + c] = v;
+        const float hv = __ldg(h + r * ldh + c);
+        const float v = g[r * ldg + c] * (1.f - hv * hv);
+        g[r * ldg + c] = v;
         acc += v;
       }
     }
@@ -190,8 +190,8 @@ tanh_grad_colsum_kernel(float* __restrict__ g, const float* __restrict__ h, int6
 // float4 variant (C % 4 == 0, 256 % (C/4) == 0): same fixed summation order
 // per (row-lane, column), four rows in flight per thread.
 __global__ void __launch_bounds__(kThreads)
-tanh_grad_colsum4_kernel(float4* __restrict__ g, const float4* __restrict__ h, int64_t R, int C4,
-                         float* __restrict__ col_part) {
+tanh_grad_colsum4_kernel(float4* __restrict__ g, int64_t ldg4, const float4* __restrict__ h,
+                         int64_t ldh4, int64_t R, int C4, float* __restrict__ col_part) {
   extern __shared__ float4 s_acc4[];  // [sub][C4]
   const int sub = kThreads / C4;
   const int lr = threadIdx.x / C4, lc = threadIdx.x % C4;
@@ -203,8 +203,8 @@ tanh_grad_colsum4_kernel(float4* __restrict__ g, const float4* __restrict__ h, i
     float4 gv[4], hv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      gv[u] = g[(r + u * sub) * C4 + lc];
-      hv[u] = __ldg(h + (r + u * sub) * C4 + lc);
+      gv[u] = g[(r + u * sub) * ldg4 + lc];
+      hv[u] = __ldg(h + (r + u * sub) * ldh4 + lc);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -213,18 +213,18 @@ tanh_grad_colsum4_kernel(float4* __restrict__ g, const float4* __restrict__ h, i
       v.y = gv[u].y * (1.f - hv[u].y * hv[u].y);
       v.z = gv[u].z * (1.f - hv[u].z * hv[u].z);
       v.w = gv[u].w * (1.f - hv[u].w * hv[u].w);
-      g[(r + u * sub) * C4 + lc] = v;
+      g[(r + u * sub) * ldg4 + lc] = v;
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
   }
   for (; r < r1; r += sub) {
-    const float4 gv = g[r * C4 + lc], hv = __ldg(h + r * C4 + lc);
+    const float4 gv = g[r * ldg4 + lc], hv = __ldg(h + r * ldh4 + lc);
     float4 v;
     v.x = gv.x * (1.f - hv.x * hv.x);
     v.y = gv.y * (1.f - hv.y * hv.y);
     v.z = gv.z * (1.f - hv.z * hv.z);
     v.w = gv.w * (1.f - hv.w * hv.w);
-    g[r * C4 + lc] = v;
+    g[r * ldg4 + lc] = v;
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
   }
   s_acc4[threadIdx.x] = acc;
@@ -309,22 +309,25 @@ extern "C" int accel_dc_reduce(const float* dc, const float* h2, const int32_t* 
   return post_launch("dc_reduce_kernel");
 }
 
-extern "C" int accel_tanh_grad_colsum(float* g, const float* h, int64_t R, int C,
-                                      float* col_part, int grid, void* stream) {
-  if (R < 0 || C < 1) return fail(kDimension, "tanh_grad_colsum: bad sizes");
+extern "C" int accel_tanh_grad_colsum(float* g, int64_t ldg, const float* h, int64_t ldh,
+                                      int64_t R, int C, float* col_part, int grid, void* stream) {
+  if (R < 0 || C < 1 || ldg < C || ldh < C) return fail(kDimension, "tanh_grad_colsum: bad sizes");
   if (R == 0) return kOk;
   if (!g || !h || !col_part) return fail(kDimension, "tanh_grad_colsum: NULL buffer");
   if (grid < 1) return fail(kDimension, "tanh_grad_colsum: grid < 1");
   const uintptr_t al = reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(h) |
                        reinterpret_cast<uintptr_t>(col_part);
-  if (C % 4 == 0 && C / 4 <= kThreads && kThreads % (C / 4) == 0 && (al & 15) == 0) {
+  if (C % 4 == 0 && C / 4 <= kThreads && kThreads % (C / 4) == 0 && (al & 15) == 0 &&
+      ldg % 4 == 0 && ldh % 4 == 0) {
     tanh_grad_colsum4_kernel<<<grid, kThreads, kThreads * sizeof(float4), as_stream(stream)>>>(
-        reinterpret_cast<float4*>(g), reinterpret_cast<const float4*>(h), R, C / 4, col_part);
+        reinterpret_cast<float4*>(g), ldg / 4, reinterpret_cast<const float4*>(h), ldh / 4, R,
+        C / 4, col_part);
     return post_launch("tanh_grad_colsum4_kernel");
   }
   const ColLayout L = ColLayout::make(C);
   const size_t smem = sizeof(float) * (size_t)L.sub * L.span;
-  tanh_grad_colsum_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(g, h, R, C, col_part);
+  tanh_grad_colsum_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(g, ldg, h, ldh, R, C,
+                                                                      col_part);
   return post_launch("tanh_grad_colsum_kernel");
 }
 

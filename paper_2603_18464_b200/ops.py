@@ -19,7 +19,24 @@ F32, F64, I32, I64, U8 = torch.float32, torch.float64, torch.int32, torch.int64,
 
 
 def _p(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    """Pointer of a dense tensor (the kernel assumes its packed row-major layout):
+    a strided view would be read or written as if it were packed, so refuse it."""
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise DimensionError(f"dense operand expected, got strides {tuple(t.stride())} "
+                             f"for shape {tuple(t.shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _pp(t):
+    """Pointer of a row-pitched operand (unit column stride; the wrapper passes
+    its row pitch to the kernel)."""
+    if t is None:
+        return None
+    if t.dim() == 2 and t.shape[0] > 1 and t.stride(1) != 1:
+        raise DimensionError(f"pitched operand needs unit column stride, got {tuple(t.stride())}")
+    return ctypes.c_void_p(t.data_ptr())
 
 
 def _stream():
@@ -182,8 +199,11 @@ def dc_reduce(dc, h2, frame_of, N, K, D, dz2, pos_part, db1_part, grid):
 
 
 def tanh_grad_colsum(g, h, col_part, grid):
-    _lib.call("accel_tanh_grad_colsum", _p(g), _p(h), g.shape[0], g.shape[1], _p(col_part),
-              int(grid), _stream())
+    for t, nm in ((g, "g"), (h, "h")):
+        if t.stride(1) != 1:
+            raise DimensionError(f"tanh_grad_colsum: {nm} needs unit column stride")
+    _lib.call("accel_tanh_grad_colsum", _pp(g), g.stride(0), _pp(h), h.stride(0), g.shape[0],
+              g.shape[1], _pp(col_part), int(grid), _stream())
 
 
 # ---------------------------------------------------------------------------
@@ -223,9 +243,9 @@ class Grouping:
             self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
             self.row_tok = torch.empty(max(R, 1), dtype=I32, device=dev)
             self.pos = torch.empty(max(R, 1), dtype=I32, device=dev)
-        _lib.call("accel_group_by_key_blocked", _p(keys), R, nkeys, self.cpb, _p(self.perm),
-                  _p(self.seg_off), _p(self.piece_off), _p(self.piece_key), _p(fo), _p(tk),
-                  int(K), _p(self.row_frame), _p(self.row_tok), _p(self.pos), _p(buf),
+        _lib.call("accel_group_by_key_blocked", _pp(keys), R, nkeys, self.cpb, _pp(self.perm),
+                  _pp(self.seg_off), _pp(self.piece_off), _pp(self.piece_key), _pp(fo), _pp(tk),
+                  int(K), _pp(self.row_frame), _pp(self.row_tok), _pp(self.pos), _pp(buf),
                   buf.numel(), _stream())
 
     def sort_rows(self, frame_of, tokens, K):
@@ -237,8 +257,8 @@ class Grouping:
             self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
             self.row_tok = torch.empty(max(R, 1), dtype=I32, device=dev)
             self.pos = torch.empty(max(R, 1), dtype=I32, device=dev)
-            _lib.call("accel_sorted_rows", _p(self.perm), _p(frame_of), _p(tokens), R, int(K),
-                      _p(self.row_frame), _p(self.row_tok), _p(self.pos), _stream())
+            _lib.call("accel_sorted_rows", _pp(self.perm), _pp(frame_of), _pp(tokens), R, int(K),
+                      _pp(self.row_frame), _pp(self.row_tok), _pp(self.pos), _stream())
         return self.pos
 
     def fact_rows_sum(self, h2w, epp, frame_of, tokens, tsc, K, out, piece_buf=None):
@@ -249,14 +269,14 @@ class Grouping:
             piece_buf = stream_workspace("group_pieces_f32", 4 * max(self.max_pieces, 1) * A)
         nk = self.nkeys * self.nblocks
         if self.cpb > 0:  # tsc holds the scalars at the sorted positions (sort_rows)
-            _lib.call("accel_fact_group_sum2", _p(h2w), _p(epp), _p(self.row_frame),
-                      _p(self.row_tok), _p(tsc), _p(self.seg_off), _p(self.piece_off),
-                      _p(self.piece_key), nk, self.nkeys, A, self.max_pieces, _p(piece_buf),
+            _lib.call("accel_fact_group_sum2", _pp(h2w), _pp(epp), _pp(self.row_frame),
+                      _pp(self.row_tok), _pp(tsc), _pp(self.seg_off), _pp(self.piece_off),
+                      _pp(self.piece_key), nk, self.nkeys, A, self.max_pieces, _pp(piece_buf),
                       _stream())
         else:
-            _lib.call("accel_fact_group_sum", _p(h2w), _p(epp), _p(frame_of), _p(tokens),
-                      _p(tsc), _p(self.perm), _p(self.seg_off), _p(self.piece_off), nk, 0,
-                      int(K), A, 256, self.max_pieces, _p(piece_buf), _stream())
+            _lib.call("accel_fact_group_sum", _pp(h2w), _pp(epp), _pp(frame_of), _pp(tokens),
+                      _pp(tsc), _pp(self.perm), _pp(self.seg_off), _pp(self.piece_off), nk, 0,
+                      int(K), A, 256, self.max_pieces, _pp(piece_buf), _stream())
         self._key_pass(piece_buf, A, out)
         return out
 
@@ -266,19 +286,19 @@ class Grouping:
             piece_buf = stream_workspace("group_pieces_f32", 4 * max(self.max_pieces, 1) * D)
         if self.cpb > 0:
             raise DimensionError("rows_sum needs a plain (unblocked) grouping")
-        _lib.call("accel_grouped_rows_sum", _p(vals), self.R, D, _p(self.perm), _p(self.seg_off),
-                  _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
+        _lib.call("accel_grouped_rows_sum", _pp(vals), self.R, D, _pp(self.perm), _pp(self.seg_off),
+                  _pp(self.piece_off), self.nkeys, self.max_pieces, _pp(piece_buf), _pp(out),
                   _stream())
         return out
 
     def _key_pass(self, piece_buf, D, out):
         if self.cpb > 0:
             wsb = stream_workspace("fold", _lib.lib().accel_fold_workspace_size(self.nkeys, D))
-            _lib.call("accel_fold_blocked_pieces", _p(piece_buf), _p(self.piece_off), self.nkeys,
-                      self.nblocks, D, _p(out), _p(wsb), _stream())
+            _lib.call("accel_fold_blocked_pieces", _pp(piece_buf), _pp(self.piece_off), self.nkeys,
+                      self.nblocks, D, _pp(out), _pp(wsb), _stream())
         else:
-            _lib.call("accel_grouped_rows_sum", None, self.R, D, _p(self.perm), _p(self.seg_off),
-                      _p(self.piece_off), self.nkeys, self.max_pieces, _p(piece_buf), _p(out),
+            _lib.call("accel_grouped_rows_sum", None, self.R, D, _pp(self.perm), _pp(self.seg_off),
+                      _pp(self.piece_off), self.nkeys, self.max_pieces, _pp(piece_buf), _pp(out),
                       _stream())
 
 
@@ -374,6 +394,12 @@ def reduce_segments(segs):
     n = len(segs)
     if n == 0:
         return
+    for src, dst, parts, ln, pitch in segs:  # the kernel writes len packed floats from dst
+        if not dst.is_contiguous() or dst.numel() < ln:
+            raise DimensionError(f"reduce_segments: dst must be packed with >= {ln} elements")
+        need = (int(parts) - 1) * int(pitch) + int(ln) if parts else 0
+        if src.storage_offset() + need > src.untyped_storage().nbytes() // src.element_size():
+            raise DimensionError("reduce_segments: src parts exceed their storage")
     srcs = (ctypes.c_void_p * n)(*[s[0].data_ptr() for s in segs])
     dsts = (ctypes.c_void_p * n)(*[s[1].data_ptr() for s in segs])
     parts = (ctypes.c_int64 * n)(*[int(s[2]) for s in segs])
@@ -398,8 +424,8 @@ def segment_moments(x, off, out=None):
 
 
 def count_nonfinite_rows(x, rows, R, count):
-    _lib.call("accel_count_nonfinite_rows", _p(x), _p(rows), int(R), x.shape[1], x.stride(0),
-              _p(count),
+    _lib.call("accel_count_nonfinite_rows", _pp(x), _pp(rows), int(R), x.shape[1], x.stride(0),
+              _pp(count),
               _stream())
 
 
@@ -453,7 +479,7 @@ def copy_2d(dst, src):
     if dst.shape != src.shape or dst.stride(1) != 1 or src.stride(1) != 1:
         raise DimensionError("copy_2d: shapes/strides")
     es = dst.element_size()
-    _lib.call("accel_copy_2d", _p(dst), dst.stride(0) * es, _p(src), src.stride(0) * es,
+    _lib.call("accel_copy_2d", _pp(dst), dst.stride(0) * es, _pp(src), src.stride(0) * es,
               dst.shape[1] * es, dst.shape[0], _stream())
     return dst
 
@@ -504,7 +530,7 @@ def tf32_pairs(x, row_pair: bool, lo_first: bool, out=None):
         raise DimensionError("tf32_pairs: unit column stride required")
     shape = _pair_shape(rows, cols, row_pair)
     out = torch.empty(shape, dtype=torch.bfloat16, device=x.device) if out is None else out
-    _lib.call("accel_tf32_pairs", _p(x), rows, cols, x.stride(0), _p(out), out.stride(0),
+    _lib.call("accel_tf32_pairs", _pp(x), rows, cols, x.stride(0), _pp(out), out.stride(0),
               int(row_pair), int(lo_first), _stream())
     return out
 
@@ -535,8 +561,8 @@ def wide_gemm(a, b, out, *, a_mn: bool, b_mn: bool, epi: int = 0, bias=None, h=N
     ap = _pairs_ws(tag + "a", a, a_mn, False)
     bp = _pairs_ws(tag + "b", b, b_mn, True)
     ldc = N if epi == 3 else out.stride(0)
-    _lib.call("accel_tc_gemm_wide", _p(a), _p(ap), _p(b), _p(bp), _p(out), _p(bias), _p(h),
-              _p(col_part), M, N, K, a.stride(0), ap.stride(0), b.stride(0), bp.stride(0), ldc,
+    _lib.call("accel_tc_gemm_wide", _pp(a), _pp(ap), _pp(b), _pp(bp), _pp(out), _pp(bias), _pp(h),
+              _pp(col_part), M, N, K, a.stride(0), ap.stride(0), b.stride(0), bp.stride(0), ldc,
               h.stride(0) if h is not None else 0, int(a_mn), int(b_mn), int(epi), int(kslices),
               _stream())
     return out
@@ -582,8 +608,8 @@ def small_gemm(a, b, out, a_trans: bool, b_trans: bool):
             raise DimensionError(f"small_gemm: {nm} needs unit column stride")
     nws = int(_lib.lib().accel_small_gemm_ws_floats(M, N, K))
     ws = stream_workspace("small_gemm", 4 * nws) if nws else None
-    _lib.call("accel_small_gemm", _p(a), _p(b), _p(out), M, N, K, a.stride(0), b.stride(0),
-              out.stride(0), int(a_trans), int(b_trans), _p(ws), nws, _stream())
+    _lib.call("accel_small_gemm", _pp(a), _pp(b), _pp(out), M, N, K, a.stride(0), b.stride(0),
+              out.stride(0), int(a_trans), int(b_trans), _pp(ws), nws, _stream())
     return out
 
 
@@ -599,7 +625,7 @@ def tc_linear(x, w, out=None, bias=None, tanh=False, accumulate=False):
             raise DimensionError("wide products do not accumulate")
         return _wide_rows(x, w, out, False, bias, tanh)
     x = pitched(x)
-    _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
+    _lib.call("accel_tc_gemm", _pp(x), _pp(w), _pp(out), _pp(bias), M, K, N, x.stride(0),
               w.stride(0), out.stride(0), 0, 0, int(tanh), int(accumulate), 1, _stream())
     return out
 
@@ -613,8 +639,8 @@ def tc_linear_checked(x, w, out, nonfinite, bias=None, tanh=False):
         count_nonfinite_rows(x, None, M, nonfinite)  # counts rows, same decision
         return _wide_rows(x, w, out, False, bias, tanh)
     x = pitched(x)
-    _lib.call("accel_tc_linear_checked", _p(x), _p(w), _p(out), _p(bias), M, K, N, x.stride(0),
-              w.stride(0), out.stride(0), int(tanh), _p(nonfinite), _stream())
+    _lib.call("accel_tc_linear_checked", _pp(x), _pp(w), _pp(out), _pp(bias), M, K, N, x.stride(0),
+              w.stride(0), out.stride(0), int(tanh), _pp(nonfinite), _stream())
     return out
 
 
@@ -630,7 +656,7 @@ def tc_matmul_nn(x, w, out=None, accumulate=False):
             raise DimensionError("wide products do not accumulate")
         return _wide_rows(x, w, out, True)
     x = pitched(x)
-    _lib.call("accel_tc_gemm", _p(x), _p(w), _p(out), None, M, K, N, x.stride(0), w.stride(0),
+    _lib.call("accel_tc_gemm", _pp(x), _pp(w), _pp(out), None, M, K, N, x.stride(0), w.stride(0),
               out.stride(0), 0, 1, 0, int(accumulate), 1, _stream())
     return out
 
@@ -661,7 +687,7 @@ def tc_matmul_nn_dtanh(x, w, h, out, part_fn):
     if N <= 256 and K <= 128 and _aligned_rows(out) and _aligned_rows(h):
         n = tc_rows_grid(M)
         part = part_fn(n)
-        _lib.call("accel_tc_gemm_dtanh", _p(x), _p(w), _p(out), _p(h), _p(part), M, K, N,
+        _lib.call("accel_tc_gemm_dtanh", _pp(x), _pp(w), _pp(out), _pp(h), _pp(part), M, K, N,
                   x.stride(0), w.stride(0), out.stride(0), h.stride(0), 1, _stream())
         return out, part, n
     tc_matmul_nn(x, w, out)
@@ -694,21 +720,22 @@ def tc_wgrad(dy, x, out, kslices=None, partial=None):
     k = x.shape[1]
     if _small(n, k, F):
         return small_gemm(dy, x, out, True, True)
+    dst = out if out.is_contiguous() else torch.empty(n, k, dtype=F32, device=dy.device)
     if n > 256 or k > 256:
         ks = wide_kslices(n, k, F)
         part = torch.empty(ks, n, k, dtype=F32, device=dy.device)
         wide_gemm(dy, x, part, a_mn=True, b_mn=True, epi=3, kslices=ks, tag="wgrad")
-        reduce_segments([(part, out, ks, n * k, n * k)])
-        return out
+        reduce_segments([(part, dst, ks, n * k, n * k)])
+        return out if dst is out else out.copy_(dst)
     dy, x = pitched(dy), pitched(x)
     if kslices is None:
         kslices = max(1, min(tc_sm_count(), -(-F // 32)))
     if partial is None:
         partial = torch.empty(2 * kslices, n, k, dtype=F32, device=dy.device)
-    _lib.call("accel_tc_gemm", _p(dy), _p(x), _p(partial), None, n, F, k, dy.stride(0),
+    _lib.call("accel_tc_gemm", _pp(dy), _pp(x), _p(partial), None, n, F, k, dy.stride(0),
               x.stride(0), k, 1, 1, 0, 0, int(kslices), _stream())
-    reduce_segments([(partial, out, 2 * kslices, n * k, n * k)])
-    return out
+    reduce_segments([(partial, dst, 2 * kslices, n * k, n * k)])
+    return out if dst is out else out.copy_(dst)
 
 
 # ---------------------------------------------------------------------------

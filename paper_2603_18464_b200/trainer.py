@@ -735,7 +735,7 @@ class Trainer:
         dy, x = ops.pitched(dy), ops.pitched(x)  # no-ops at aligned widths
         ks = max(1, min(ops.tc_sm_count(), -(-F // 32)))
         part = self.scratch.get("wg." + tag, (2 * ks + extra, n, k))
-        _lib.call("accel_tc_gemm", ops._p(dy), ops._p(x), ops._p(part), None, n, F, k,
+        _lib.call("accel_tc_gemm", ops._pp(dy), ops._pp(x), ops._p(part), None, n, F, k,
                   dy.stride(0), x.stride(0), k, 1, 1, 0, 0, ks, ops._stream())
         return (part, out, 2 * ks + extra, n * k, n * k)
 

@@ -107,3 +107,49 @@ def test_small_gemm_split_k(M, N, K):
     assert rel_err(out, A.double() @ B.double().t()) < 1e-6
     if M * N <= 2048:
         assert _lib.lib().accel_small_gemm_ws_floats(M, N, K) > 0  # the split path ran
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 64, 64), (129, 195, 64), (1000, 64, 256), (4099, 256, 64)])
+def test_row_gemms_write_only_their_outputs(M, K, N):
+    """Row transform (TMA-store and dtanh epilogues) and weight gradient at
+    ragged sizes: pitched outputs with canaries around them stay untouched."""
+    from paper_2603_18464_b200 import ops
+    CAN = 4242.0
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    x = torch.randn(M, K, device="cuda", generator=g) * 0.1
+    w = torch.randn(N, K, device="cuda", generator=g)
+    buf = torch.full((M + 3, N + 8), CAN, device="cuda")
+    out = buf[1:M + 1, 4:N + 4]
+    ops.tc_linear(x, w, out=out)
+    torch.cuda.synchronize()
+    mask = torch.ones_like(buf, dtype=torch.bool)
+    mask[1:M + 1, 4:N + 4] = False
+    assert bool((buf[mask] == CAN).all())
+    assert rel_err(out, x.double() @ w.double().t()) < 4e-6
+    # dtanh: (x . w2) (1 - h^2) with column-sum parts
+    w2 = torch.randn(K, N, device="cuda", generator=g)
+    h = torch.tanh(torch.randn(M, N, device="cuda", generator=g))
+    buf.fill_(CAN)
+    parts = {}
+
+    def part_fn(n):
+        parts["buf"] = torch.full((n + 2, N), CAN, device="cuda")
+        parts["n"] = n
+        return parts["buf"][:n]
+    y, part, n = ops.tc_matmul_nn_dtanh(x, w2, h, out, part_fn)
+    torch.cuda.synchronize()
+    assert bool((buf[mask] == CAN).all())
+    assert bool((parts["buf"][parts["n"]:] == CAN).all())
+    want = (x.double() @ w2.double()) * (1 - h.double() ** 2)
+    assert rel_err(out, want) < 4e-6
+    assert float((part.double().sum(0) - want.sum(0)).abs().max()) < 1e-5 * float(want.abs().sum(0).max())
+    # weight gradient into a pitched [N, K] block
+    dy = torch.randn(M, N, device="cuda", generator=g)
+    gbuf = torch.full((N + 2, K + 8), CAN, device="cuda")
+    gout = gbuf[1:N + 1, 4:K + 4]
+    ops.tc_wgrad(dy, x, gout)
+    torch.cuda.synchronize()
+    gmask = torch.ones_like(gbuf, dtype=torch.bool)
+    gmask[1:N + 1, 4:K + 4] = False
+    assert bool((gbuf[gmask] == CAN).all())
+    assert rel_err(gout, dy.double().t() @ x.double()) < 4e-6

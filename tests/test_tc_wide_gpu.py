@@ -199,3 +199,51 @@ def test_pairs_hold_the_tf32_split():
             hi, lo = (s_, f) if lo_first else (f, s_)
             assert float(((hi - hi_t).abs() / hi_t.abs().clamp_min(1e-30)).max()) <= 2 ** -8
             assert float((lo - lo_t).abs().max()) <= float(lo_t.abs().max()) * 2 ** -8
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 32, 16), (129, 96, 200), (385, 300, 40), (641, 544, 72)])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_epilogues_write_only_their_outputs(M, N, K, epi):
+    """Ragged M / N / K (odd tile counts, so a 2-SM pair's second tile can lie
+    past M): every epilogue writes exactly its [M, N] block (pitched output with
+    canary rows and columns around it), its column-sum rows and its split-K
+    slices -- nothing else."""
+    import torch
+
+    from paper_2603_18464_b200 import ops
+    CAN = 7777.0
+    A, W, a, w = _mats(M, N, K, 0, 1, seed=M * 7 + N)
+    A = A * 0.05
+    a = A
+    want = A.double() @ W.double().t()
+    nt = -(-M // 128)
+    if epi == 3:
+        ks = 3 if K >= 48 else 1
+        buf = torch.full((ks * M * N + 1024,), CAN, device="cuda")
+        ops.wide_gemm(a, w, buf, a_mn=False, b_mn=True, epi=3, kslices=ks)
+        torch.cuda.synchronize()
+        assert bool((buf[ks * M * N:] == CAN).all())
+        got = buf[:ks * M * N].view(ks, M, N).double().sum(0)
+        assert _err(got, want) < TOL
+        return
+    buf = torch.full((M + 3, N + 12), CAN, device="cuda")
+    out = buf[1:M + 1, 4:N + 4]  # pitched, with canaries on every side
+    bias = torch.randn(N, device="cuda") if epi == 1 else None
+    H = torch.tanh(torch.randn(M, N, device="cuda")) if epi == 2 else None
+    part = torch.full((nt + 2, N), CAN, device="cuda") if epi == 2 else None
+    ops.wide_gemm(a, w, out, a_mn=False, b_mn=True, epi=epi, bias=bias, h=H,
+                  col_part=part[:nt] if part is not None else None)
+    torch.cuda.synchronize()
+    mask = torch.ones_like(buf, dtype=torch.bool)
+    mask[1:M + 1, 4:N + 4] = False
+    assert bool((buf[mask] == CAN).all())
+    if epi == 0:
+        assert _err(out, want) < TOL
+    elif epi == 1:
+        pre = want + bias.double()
+        assert float((out.double() - torch.tanh(pre)).abs().max()) < TOL * float(pre.abs().max())
+    else:
+        y = want * (1 - H.double() ** 2)
+        assert _err(out, y) < TOL
+        assert bool((part[nt:] == CAN).all())
+        assert _err(part[:nt].double().sum(0), y.sum(0)) < TOL
