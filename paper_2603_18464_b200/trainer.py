@@ -300,20 +300,42 @@ def behavior_log_probs(behavior_logits, tokens):
 
 
 class _Scratch:
-    """Grow-only named device buffers (shapes change with every batch)."""
+    """Grow-only named device buffers (shapes change with every batch).
+
+    Guard mode (tests): every buffer handed out is followed by >= 4 KB of a
+    byte pattern, re-armed at each get(); check_guards() lists the buffers
+    whose tail a kernel wrote past its shape."""
+
+    GUARD_BYTE = 0xA5
+    GUARD_BYTES = 4096
 
     def __init__(self, device) -> None:
         self.device = device
         self._bufs: dict = {}
+        self.guard = False
+        self._armed: dict = {}
 
     def get(self, name: str, shape, dtype=F32) -> torch.Tensor:
         n = int(np.prod(shape)) if len(shape) else 1
         buf = self._bufs.get(name)
-        if buf is None or buf.dtype != dtype or buf.numel() < n:
+        pad = -(-self.GUARD_BYTES // torch.empty((), dtype=dtype).element_size()) if self.guard else 0
+        if buf is None or buf.dtype != dtype or buf.numel() < n + pad:
             ops.retire(buf)
-            buf = torch.empty(max(n, 1) + (n >> 4), dtype=dtype, device=self.device)
+            buf = torch.empty(max(n, 1) + (n >> 4) + pad, dtype=dtype, device=self.device)
             self._bufs[name] = buf
+        if self.guard:
+            buf.view(torch.uint8)[n * buf.element_size():].fill_(self.GUARD_BYTE)
+            self._armed[name] = n
         return buf[:n].view(*shape) if len(shape) else buf[:1]
+
+    def check_guards(self) -> list:
+        bad = []
+        for name, n in self._armed.items():
+            buf = self._bufs[name]
+            tail = buf.view(torch.uint8)[n * buf.element_size():]
+            if not bool((tail == self.GUARD_BYTE).all()):
+                bad.append(name)
+        return bad
 
 
 def _array_split_sizes(n: int, k: int) -> tuple:

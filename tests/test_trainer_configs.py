@@ -255,3 +255,49 @@ def test_cfg1_captured_graph_equals_eager_steps():
     step.inputs["rewards"][5] = float("nan")
     assert step.run() is None
     assert torch.equal(graphed.params.p[graphed.params.cur], before) and graphed.cycles == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["libero_recompute", "libero_store", "libero_clip_vclip",
+                                  "cfg4_widths", "narrow_unfactorized"])
+def test_no_kernel_writes_past_its_scratch_buffer(case):
+    """Every trainer scratch buffer is followed by a 4 KB guard pattern (guard
+    mode); after build + two train steps no guard byte may have changed."""
+    from paper_2603_18464_b200.trainer import Trainer
+    from paper_2603_18464_b200.types import (ModelBundle, PolicyConfig, PolicyModel, ValueConfig,
+                                             ValueHead)
+    from paper_2603_18464_b200.workload import (libero_long_lengths, synthetic_packed,
+                                                unpack_trajectories)
+
+    rng = np.random.default_rng(5)
+    if case == "cfg4_widths":
+        o, d, k, a, n_steps, mlp, n_traj, horizon = 4096, 4096, 7, 256, 34, 32, 8, 32
+    elif case == "narrow_unfactorized":
+        o, d, k, a, n_steps, mlp, n_traj, horizon = 37, 48, 3, 40, 70, 16, 24, 66
+    else:
+        o, d, k, a, n_steps, mlp, n_traj, horizon = 195, 64, 7, 256, 522, 32, 40, 520
+    lens, done = libero_long_lengths(rng, n_traj, horizon)
+    pb = synthetic_packed(11, lens, done, k, a, o)
+    trajs = unpack_trajectories(pb)
+    pc = PolicyConfig(obs_dim=o, hidden_dim=d, chunk_len=k, n_actions=a, vocab_size=32000,
+                      action_start=31744)
+    bundle = ModelBundle(PolicyModel.init(rng, pc),
+                         ValueHead.init(rng, ValueConfig(hidden_dim=d, n_steps=n_steps,
+                                                         mlp_hidden=mlp)))
+    oc = OracleConfig(algorithm="clip" if case == "libero_clip_vclip" else "trust")
+    cfg = _trainer_cfg(oc)
+    if case == "libero_clip_vclip":
+        import dataclasses
+        cfg = dataclasses.replace(cfg, loss=dataclasses.replace(cfg.loss, value_clip=0.2))
+    tr = Trainer(bundle, cfg)
+    tr.scratch.guard = True
+    tr.recompute_dz = case != "libero_store"
+    tr.group_block_chunks = 1
+    if case == "narrow_unfactorized":
+        tr.factorized = False  # materialized logits + dense loss kernel
+    for step in range(2):
+        batch = tr.build_train_batch(trajs)
+        rec = tr.train_step(batch)
+        assert rec is not None and np.isfinite(rec["loss"])
+        bad = tr.scratch.check_guards()
+        assert not bad, f"step {step}: kernels wrote past {bad}"
