@@ -239,8 +239,9 @@ int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nkeys, int64_
                                int32_t* piece_key, const int32_t* frame_of, const int32_t* tokens,
                                int K, int32_t* row_frame, int32_t* row_tok, int32_t* pos,
                                void* workspace, size_t workspace_bytes, void* stream);
-/* pos != NULL: the scatter also writes the sorted per-row metadata of a
- * (prev, k) grouping (as accel_sorted_rows): row_frame, row_tok, pos. */
+/* pos != NULL: the scatter also writes the inverse permutation pos[perm[r]] = r
+ * (coalesced); row_frame / row_tok != NULL (with frame_of, tokens, K): also the
+ * sorted per-row metadata of a (prev, k) grouping, as accel_sorted_rows. */
 /* piece_key (nullable) i32[accel_group_max_pieces_blocked]: owning composite key
  * of each piece. */
 /* Sorted per-row metadata of a grouping (fixed per batch): row_frame[r] =
@@ -248,12 +249,14 @@ int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nkeys, int64_
 int accel_sorted_rows(const int32_t* perm, const int32_t* frame_of, const int32_t* tokens,
                       int64_t R, int K, int32_t* row_frame, int32_t* row_tok, int32_t* pos,
                       void* stream);
-/* accel_fact_group_sum over a blocked grouping with sorted metadata: one CTA
- * per piece (in (block, key) order), the piece's rows contiguous in row_frame /
- * row_tok / tsc_sorted (the loss kernel's token scalars at their sorted
- * positions, accel_token_loss_fact2 with tsc_pos = pos). */
-int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* row_frame,
-                          const int32_t* row_tok, const void* tsc_sorted, const int64_t* seg_off,
+/* accel_fact_group_sum over a blocked grouping: one CTA per piece (in (block,
+ * key) order); a piece's token rows are perm[r] (frame frame_of[perm[r] / K],
+ * token tokens[perm[r]]) and their scalars are contiguous in tsc_sorted (the
+ * loss kernel's token scalars at their sorted positions, accel_token_loss_fact2
+ * with tsc_pos = pos). */
+int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* perm,
+                          const int32_t* frame_of, const int32_t* tokens, int K,
+                          const void* tsc_sorted, const int64_t* seg_off,
                           const int64_t* piece_off, const int32_t* piece_key, int nkeys,
                           int key_mod, int A, int64_t n_pieces_max, float* piece_out,
                           void* stream);

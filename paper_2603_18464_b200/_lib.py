@@ -57,8 +57,8 @@ _SIGNATURES = {
     "accel_group_by_key_blocked": (c_int, [P, c_int64, c_int, c_int64, P, P, P, P, P, P, c_int,
                                            P, P, P, P, c_size_t, P]),
     "accel_fold_workspace_size": (c_size_t, [c_int, c_int]),
-    "accel_fact_group_sum2": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int64, P,
-                                      P]),
+    "accel_fact_group_sum2": (c_int, [P, P, P, P, P, c_int, P, P, P, P, c_int, c_int, c_int,
+                                      c_int64, P, P]),
     "accel_wm_workspace_size": (c_size_t, [c_int64, c_int, c_int]),
     "accel_wm_mlp2_grad": (c_int, [P, P, c_int64, c_int, c_int, c_int, c_int, P, P, P, P, P,
                                    c_size_t, P]),

@@ -111,8 +111,10 @@ class DeviceTrainBatch:
         pk_cpb 4096-token chunks) for the dz-recomputing grouped sums."""
         N, K, A = self.n_transitions, self.chunk_len, self.n_actions
         if factorized and (self.pk_group is None or self.pk_group.cpb != pk_cpb):
+            # the scatter also writes the inverse permutation (the loss kernel's
+            # scalar positions) when the grouping is frame-blocked
             self.pk_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A, with_pos=True),
-                                         (A + 1) * K, cpb=pk_cpb)
+                                         (A + 1) * K, cpb=pk_cpb, rows=pk_cpb > 0)
         if not factorized and self.prev_group is None:
             self.prev_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A), A + 1)
         if frame_space:

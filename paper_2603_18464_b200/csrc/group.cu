@@ -79,7 +79,14 @@ chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_
   const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
   if (chunk < n_chunks) {
     const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
-    for (int64_t r = r0 + lane; r < r1; r += 32) atomicAdd(h + __ldg(keys + r), 1);
+    for (int64_t r = r0 + lane; r < r1; r += 32 * 8) {  // eight key loads in flight per lane
+      int kk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) kk[u] = r + 32 * u < r1 ? __ldg(keys + r + 32 * u) : -1;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (kk[u] >= 0) atomicAdd(h + kk[u], 1);
+    }
     __syncwarp();
     for (int j = lane; j < nkeys; j += 32) counts[count_idx(chunk, j, nkeys, cpb)] = h[j];
   }
@@ -134,28 +141,67 @@ stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, in
   const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
   if (chunk >= n_chunks) return;
   int* ctr = s_ctr + warp * nkeys;
-  for (int j = lane; j < nkeys; j += 32) ctr[j] = base[count_idx(chunk, j, nkeys, cpb)];
+  for (int j0 = lane; j0 < nkeys; j0 += 32 * 8) {  // eight strided loads in flight per lane
+    int v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + 32 * u;
+      v[u] = j < nkeys ? __ldg(base + count_idx(chunk, j, nkeys, cpb)) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + 32 * u < nkeys) ctr[j0 + 32 * u] = v[u];
+  }
   __syncwarp();
   const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t g = r0; g < r1; g += 32) {
-    const int64_t r = g + lane;
-    const bool live = r < r1;
-    const int key = live ? __ldg(keys + r) : -1 - lane;  // dead lanes never match
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (live) {
-      const int rank = __popc(peers & lt);
-      const int32_t dst = ctr[key] + rank;
-      perm[dst] = (int32_t)r;
-      if (sr.pos != nullptr) {  // sorted per-row metadata, fused (pos writes coalesced)
-        sr.row_frame[dst] = __ldg(sr.frame_of + r / sr.K);
-        sr.row_tok[dst] = __ldg(sr.tokens + r);
-        sr.pos[r] = dst;
-      }
+  const int kbits = nkeys > 1 ? 32 - __clz(nkeys - 1) : 1;  // bits of the largest key
+  for (int64_t g0 = r0; g0 < r1; g0 += 32 * 8) {
+    int kk[8];  // the keys of eight 32-row groups, loaded together (latency once per 256 rows)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t r = g0 + 32 * u + lane;
+      kk[u] = r < r1 ? __ldg(keys + r) : -1 - lane;  // dead lanes never match
     }
-    __syncwarp();
-    if (live && (peers & lt) == 0) ctr[key] += __popc(peers);
-    __syncwarp();
+    // peer masks (lanes holding the same key) from one ballot per key bit:
+    // cheaper than MATCH.ANY, whose cost grows with the number of distinct
+    // keys in the group (here nearly all 32 differ)
+    unsigned pm[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int key = kk[u];
+      const bool live = key >= 0;
+      unsigned m = __ballot_sync(0xffffffffu, live);
+      m = live ? m : ~m;
+      for (int b = 0; b < kbits; ++b) {
+        const bool bit = (key >> b) & 1;
+        const unsigned bb = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bb : ~bb;
+      }
+      pm[u] = live ? m : (1u << lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t g = g0 + 32 * u;
+      if (g >= r1) break;  // warp-uniform
+      const int64_t r = g + lane;
+      const bool live = r < r1;
+      const int key = kk[u];
+      const unsigned peers = pm[u];
+      if (live) {
+        const int rank = __popc(peers & lt);
+        const int32_t dst = ctr[key] + rank;
+        perm[dst] = (int32_t)r;
+        if (sr.pos != nullptr) sr.pos[r] = dst;  // inverse permutation (coalesced writes)
+        if (sr.row_frame != nullptr) {           // sorted per-row metadata (scattered writes)
+          sr.row_frame[dst] = __ldg(sr.frame_of + r / sr.K);
+          sr.row_tok[dst] = __ldg(sr.tokens + r);
+        }
+      }
+      __syncwarp();
+      if (live && (peers & lt) == 0) ctr[key] += __popc(peers);
+      __syncwarp();
+    }
   }
 }
 
@@ -562,8 +608,10 @@ extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nk
   }
   if (R == 0) return kOk;
   SortedRows sr{frame_of, tokens, K, row_frame, row_tok, pos};
-  if (pos != nullptr && (!frame_of || !tokens || !row_frame || !row_tok || K < 1))
+  if (row_frame != nullptr && (!frame_of || !tokens || !row_tok || K < 1))
     return fail(kDimension, "group_by_key: sorted rows need frame_of, tokens, outputs, K");
+  if ((row_frame == nullptr) != (row_tok == nullptr))
+    return fail(kDimension, "group_by_key: row_frame and row_tok go together");
   stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, base, perm, sr);
   return post_launch("stable_scatter_kernel");
 }

@@ -1122,7 +1122,8 @@ constexpr int kGs2Warps = kGs2Threads / 32;
 template <int LPR>
 __global__ void __launch_bounds__(kGs2Threads)
 fact_group_sum2_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
-                       const int32_t* __restrict__ row_frame, const int32_t* __restrict__ row_tok,
+                       const int32_t* __restrict__ perm, const int32_t* __restrict__ frame_of,
+                       const int32_t* __restrict__ tokens, int K,
                        const float4* __restrict__ tsc_sorted, const int64_t* __restrict__ seg_off,
                        const int64_t* __restrict__ piece_off, const int32_t* __restrict__ piece_key,
                        int nkeys, int key_mod, float* __restrict__ piece_out) {
@@ -1142,9 +1143,10 @@ fact_group_sum2_kernel(const float* __restrict__ h2w, const float* __restrict__ 
   const int nr = (int)min(__ldg(seg_off + key + 1) - r0, (int64_t)kGsRows);
   const int64_t erow = key_mod > 0 ? key % key_mod : key;
   for (int c = tid; c < A; c += kGs2Threads) s_ep[c] = __ldg(epp + erow * A + c);
-  if (tid < nr) {
-    s_frame[tid] = __ldg(row_frame + r0 + tid);
-    s_tok[tid] = __ldg(row_tok + r0 + tid);
+  if (tid < nr) {  // the piece's token rows through the permutation (L2-resident gathers)
+    const int32_t t = __ldg(perm + r0 + tid);
+    s_frame[tid] = __ldg(frame_of + t / K);
+    s_tok[tid] = __ldg(tokens + t);
     s_sc[tid] = __ldg(tsc_sorted + r0 + tid);
   }
 #pragma unroll
@@ -1268,14 +1270,15 @@ extern "C" int accel_fact_group_sum(const float* h2w, const float* epp, const in
 }
 
 // Recompute over a frame-blocked grouping with sorted metadata (see the kernel).
-extern "C" int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* row_frame,
-                                     const int32_t* row_tok, const void* tsc_sorted,
-                                     const int64_t* seg_off, const int64_t* piece_off,
-                                     const int32_t* piece_key, int nkeys, int key_mod, int A,
-                                     int64_t n_pieces_max, float* piece_out, void* stream) {
-  if (A < 4 || A % 4 || nkeys < 1) return fail(kDimension, "fact_group_sum2: bad sizes");
+extern "C" int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* perm,
+                                     const int32_t* frame_of, const int32_t* tokens, int K,
+                                     const void* tsc_sorted, const int64_t* seg_off,
+                                     const int64_t* piece_off, const int32_t* piece_key, int nkeys,
+                                     int key_mod, int A, int64_t n_pieces_max, float* piece_out,
+                                     void* stream) {
+  if (A < 4 || A % 4 || nkeys < 1 || K < 1) return fail(kDimension, "fact_group_sum2: bad sizes");
   if (n_pieces_max == 0) return kOk;
-  if (!h2w || !epp || !row_frame || !row_tok || !tsc_sorted || !seg_off || !piece_off ||
+  if (!h2w || !epp || !perm || !frame_of || !tokens || !tsc_sorted || !seg_off || !piece_off ||
       !piece_key || !piece_out)
     return fail(kDimension, "fact_group_sum2: NULL buffer");
   if (misaligned16(h2w) || misaligned16(epp) || misaligned16(tsc_sorted) || misaligned16(piece_out))
@@ -1283,8 +1286,8 @@ extern "C" int accel_fact_group_sum2(const float* h2w, const float* epp, const i
   if (A != 128 && A != 256) return fail(kDimension, "fact_group_sum2: A must be 128 or 256");
   auto go = [&](auto kernel) {
     kernel<<<(unsigned)n_pieces_max, kGs2Threads, 0, as_stream(stream)>>>(
-        h2w, epp, row_frame, row_tok, static_cast<const float4*>(tsc_sorted), seg_off, piece_off,
-        piece_key, nkeys, key_mod, piece_out);
+        h2w, epp, perm, frame_of, tokens, K, static_cast<const float4*>(tsc_sorted), seg_off,
+        piece_off, piece_key, nkeys, key_mod, piece_out);
     return post_launch("fact_group_sum2_kernel");
   };
   return A == 256 ? go(fact_group_sum2_kernel<32>) : go(fact_group_sum2_kernel<16>);

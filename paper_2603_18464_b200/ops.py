@@ -219,8 +219,8 @@ class Grouping:
     sums then fold the blocks in order (accel_fold_blocked_pieces)."""
 
     def __init__(self, keys, nkeys: int, cpb: int = 0, rows=None):
-        """rows = (frame_of, tokens, K): also build the sorted per-row metadata
-        (row_frame, row_tok, pos) inside the scatter (see sort_rows)."""
+        """rows: also write the inverse permutation pos inside the scatter (see
+        sort_rows)."""
         R = keys.numel()
         dev = keys.device
         lib = _lib.lib()
@@ -235,30 +235,22 @@ class Grouping:
                           if cpb > 0 else None)
         nbytes = lib.accel_group_workspace_size_blocked(R, nkeys, self.cpb)
         buf = stream_workspace("group", nbytes)
-        fo = tk = None
-        K = 1
-        self.row_frame = self.row_tok = self.pos = None
-        if rows is not None:
-            fo, tk, K = rows
-            self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
-            self.row_tok = torch.empty(max(R, 1), dtype=I32, device=dev)
+        self.pos = None
+        if rows:  # the inverse permutation, written coalesced by the scatter
             self.pos = torch.empty(max(R, 1), dtype=I32, device=dev)
         _lib.call("accel_group_by_key_blocked", _pp(keys), R, nkeys, self.cpb, _pp(self.perm),
-                  _pp(self.seg_off), _pp(self.piece_off), _pp(self.piece_key), _pp(fo), _pp(tk),
-                  int(K), _pp(self.row_frame), _pp(self.row_tok), _pp(self.pos), _pp(buf),
-                  buf.numel(), _stream())
+                  _pp(self.seg_off), _pp(self.piece_off), _pp(self.piece_key), None, None, 1,
+                  None, None, _pp(self.pos), _pp(buf), buf.numel(), _stream())
 
-    def sort_rows(self, frame_of, tokens, K):
-        """Sorted per-row metadata of a (prev, k) grouping: row_frame, row_tok and
-        the inverse permutation pos (fixed per batch)."""
+    def sort_rows(self, frame_of=None, tokens=None, K=None):
+        """The inverse permutation pos (pos[perm[r]] = r, fixed per batch): where
+        the loss kernel writes each token's scalars for the grouped recompute."""
         if self.pos is None:
-            dev = self.perm.device
             R = self.R
-            self.row_frame = torch.empty(max(R, 1), dtype=I32, device=dev)
-            self.row_tok = torch.empty(max(R, 1), dtype=I32, device=dev)
-            self.pos = torch.empty(max(R, 1), dtype=I32, device=dev)
+            self.pos = torch.empty(max(R, 1), dtype=I32, device=self.perm.device)
+            scratch = torch.empty(2 * max(R, 1), dtype=I32, device=self.perm.device)
             _lib.call("accel_sorted_rows", _pp(self.perm), _pp(frame_of), _pp(tokens), R, int(K),
-                      _pp(self.row_frame), _pp(self.row_tok), _pp(self.pos), _stream())
+                      _pp(scratch[:max(R, 1)]), _pp(scratch[max(R, 1):]), _pp(self.pos), _stream())
         return self.pos
 
     def fact_rows_sum(self, h2w, epp, frame_of, tokens, tsc, K, out, piece_buf=None):
@@ -269,8 +261,8 @@ class Grouping:
             piece_buf = stream_workspace("group_pieces_f32", 4 * max(self.max_pieces, 1) * A)
         nk = self.nkeys * self.nblocks
         if self.cpb > 0:  # tsc holds the scalars at the sorted positions (sort_rows)
-            _lib.call("accel_fact_group_sum2", _pp(h2w), _pp(epp), _pp(self.row_frame),
-                      _pp(self.row_tok), _pp(tsc), _pp(self.seg_off), _pp(self.piece_off),
+            _lib.call("accel_fact_group_sum2", _pp(h2w), _pp(epp), _pp(self.perm), _pp(frame_of),
+                      _pp(tokens), int(K), _pp(tsc), _pp(self.seg_off), _pp(self.piece_off),
                       _pp(self.piece_key), nk, self.nkeys, A, self.max_pieces, _pp(piece_buf),
                       _stream())
         else:
