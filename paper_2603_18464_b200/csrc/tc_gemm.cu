@@ -51,6 +51,11 @@ constexpr int BK = 32;                     // row kernel: fp32 K elements per st
 constexpr int kThreads = 320;              // 10 warps
 constexpr int kConvWarp0 = 2, kConvWarps = 4, kConv = kConvWarps * 32;
 constexpr int kEpiWarp0 = 6, kEpiWarps = 4;
+// tc_rows may run 8 epilogue warps (two per TMEM lane quarter, each draining
+// half of the column chunks) when its ring keeps enough stages: its epilogue
+// (bias, tanh, swizzled staging, TMA stores) is the longer pole at narrow K
+constexpr int kRowsEpiMax = 8;
+constexpr int kRowsThreads = (kEpiWarp0 + kRowsEpiMax) * 32;  // 14 warps
 constexpr int kMaxRaw = 12;                // raw (TMA) ring slots
 constexpr int kNL = 2;                     // lo ring slots
 constexpr size_t kSmemBudget = 225 * 1024;  // dynamic shared memory (wgrad)
@@ -149,10 +154,10 @@ struct Ring {
 // double-buffered TMEM accumulators (MMA -> epilogue).
 struct Bars {
   uint64_t raw_full[kMaxRaw], raw_empty[kMaxRaw], lo_full[kNL], lo_empty[kNL], tfull[2], tempty[2];
-  uint64_t hbar[kEpiWarps][2];  // dtanh epilogue: per-warp H box loads
+  uint64_t hbar[kRowsEpiMax][2];  // dtanh epilogue: per-warp H box loads
 };
 
-__device__ __forceinline__ void init_bars(Bars& b, int nraw) {
+__device__ __forceinline__ void init_bars(Bars& b, int nraw, int nepi = kEpiWarps) {
   for (int s = 0; s < nraw; ++s) {
     mbar_init(&b.raw_full[s], 1);
     mbar_init(&b.raw_empty[s], 1);
@@ -163,9 +168,9 @@ __device__ __forceinline__ void init_bars(Bars& b, int nraw) {
   }
   for (int s = 0; s < 2; ++s) {
     mbar_init(&b.tfull[s], 1);
-    mbar_init(&b.tempty[s], kEpiWarps);
+    mbar_init(&b.tempty[s], nepi);
   }
-  for (int w = 0; w < kEpiWarps; ++w) {
+  for (int w = 0; w < nepi; ++w) {
     mbar_init(&b.hbar[w][0], 1);
     mbar_init(&b.hbar[w][1], 1);
   }
@@ -186,9 +191,10 @@ struct RowArgs {
   float* col_part;    // [gridDim.x][N]
   unsigned* nonfinite;  // optional: += number of non-finite elements of X
   uint32_t tmem_cols, acc_cols;
+  int nepi;           // epilogue warps: 4 (warps 6-9) or 8 (6-13)
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kRowsThreads, 1)
 tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                const __grid_constant__ CUtensorMap hmap, RowArgs p) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -203,12 +209,13 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
   unsigned char* raw_ring = smem + (size_t)p.kblocks * wblk;
   unsigned char* lo_ring = raw_ring + (size_t)p.nraw * kTile;
   unsigned char* staging = lo_ring + (size_t)kNL * kTile;  // epilogue: nstg boxes per warp
-  // dtanh only: per-epilogue-warp column sums [kEpiWarps][256] after the staging boxes
-  float (*s_csum)[256] = reinterpret_cast<float (*)[256]>(staging + (size_t)kEpiWarps * p.nstg * 4096);
+  const int nepi = p.nepi;
+  // dtanh only: per-epilogue-warp column sums [nepi][256] after the staging boxes
+  float (*s_csum)[256] = reinterpret_cast<float (*)[256]>(staging + (size_t)nepi * p.nstg * 4096);
 
   // W resident: split once, K-major, [hi rows | lo rows] per K block
   const int Kpad = p.kblocks * BK;
-  for (int idx = threadIdx.x; idx < Npad * Kpad; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < Npad * Kpad; idx += kRowsThreads) {
     const int n = idx / Kpad, k = idx - n * Kpad;
     float v = 0.f;
     if (n < p.N && k < p.K)
@@ -219,11 +226,11 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     *reinterpret_cast<float*>(blk + canon_k(n, k % BK)) = h;
     *reinterpret_cast<float*>(blk + canon_k(Npad + n, k % BK)) = l;
   }
-  for (int c = threadIdx.x; c < 256; c += kThreads)
+  for (int c = threadIdx.x; c < 256; c += kRowsThreads)
     s_bias[c] = (p.bias && c < p.N) ? __ldg(p.bias + c) : 0.f;
   if (warp == 1) tmem_alloc(&tmem_base, p.tmem_cols);
   if (threadIdx.x == 0) {
-    init_bars(bars, p.nraw);
+    init_bars(bars, p.nraw, nepi);
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
   }
   fence_proxy_async();
@@ -309,13 +316,17 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
       nbad = __reduce_add_sync(0xffffffffu, nbad);
       if (lane == 0 && nbad) atomicAdd(p.nonfinite, nbad);  // integer: order-independent
     }
-  } else {
+  } else if (warp - kEpiWarp0 < nepi) {
     // ---- epilogue: warp q drains TMEM lanes [32q, 32q + 32) = tile rows, 32
-    // columns at a time; rows go out through a swizzled staging box + TMA store.
+    // columns at a time (with 8 epilogue warps, warps 6-9 take the even and
+    // warps 10-13 the odd 32-column chunks); rows go out through a swizzled
+    // staging box + TMA store.
     // dtanh: the box is first filled with the matching H box by TMA, read back
     // (same swizzle), overwritten with y = acc (1 - h^2), stored; column sums of
     // y are read column-wise from the box (conflict-free) into lane registers.
     const int q = warp & 3, ew = warp - kEpiWarp0;
+    const int cfirst = nepi == 8 ? (ew >> 2) * 32 : 0, cstep = nepi == 8 ? 64 : 32;
+    const int nch = Npad > cfirst ? (Npad - cfirst + cstep - 1) / cstep : 0;  // this warp's chunks
     unsigned char* stg0 = staging + (size_t)ew * p.nstg * 4096;
     int sb = 0;
     unsigned hph = 0;  // per-box H barrier phases
@@ -324,12 +335,12 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     // dtanh with all of a tile's chunks fitting the boxes: H boxes of the next
     // tile are loaded as soon as this tile's stores have read the boxes, so the
     // load latency hides behind the MMAs instead of stalling every chunk
-    const bool hpre = p.dtanh && Npad == 32 * p.nstg;
+    const bool hpre = p.dtanh && nch == p.nstg;
     auto load_h = [&](int64_t tt) {
       const int64_t r0h = (blockIdx.x + tt * gridDim.x) * BM + q * 32;
-      for (int c = 0; c < p.nstg; ++c) {
+      for (int c = 0; c < nch; ++c) {
         mbar_expect_tx(&bars.hbar[ew][c], 4096);
-        tma_load_2d(stg0 + c * 4096, &hmap, c * 32, (int)r0h, &bars.hbar[ew][c]);
+        tma_load_2d(stg0 + c * 4096, &hmap, cfirst + c * cstep, (int)r0h, &bars.hbar[ew][c]);
       }
     };
     if (hpre && my_tiles > 0 && lane == 0) load_h(0);
@@ -341,7 +352,7 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
       const int64_t row = row0 + lane;
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)b * p.acc_cols;
 #pragma unroll 1
-      for (int c0 = 0; c0 < Npad; c0 += 32) {
+      for (int c0 = cfirst; c0 < Npad; c0 += cstep) {
         unsigned char* stg = stg0 + sb * 4096;
         if (p.tma_store) {
           if (lane == 0 && !hpre) tma_store_wait_read();  // this box's previous store has read it
@@ -429,9 +440,9 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   if (p.dtanh) {  // the CTA's column sums, epilogue warps in fixed order
-    for (int c = threadIdx.x; c < p.N; c += kThreads) {
+    for (int c = threadIdx.x; c < p.N; c += kRowsThreads) {
       float a = 0.f;
-      for (int w = 0; w < kEpiWarps; ++w) a += s_csum[w][c];
+      for (int w = 0; w < nepi; ++w) a += s_csum[w][c];
       p.col_part[(int64_t)blockIdx.x * p.N + c] = a;
     }
   }
@@ -703,18 +714,28 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   p.ntiles = ceil_div(M, BM);
   p.acc_cols = p.concat ? 2 * Npad : Npad;
   p.tmem_cols = tmem_cols_for(2 * (int)p.acc_cols);
+  // epilogue warps: 8 when the ring still keeps >= 6 slots beside their two
+  // staging boxes each (narrow K: the epilogue is the longer pole), else 4;
   // staging: two boxes per epilogue warp when the raw ring keeps >= 6 slots
-  p.nstg = p.tma_store ? 2 : 0;
-  if (p.tma_store && wbytes + (size_t)kNL * kTile + (size_t)kEpiWarps * 2 * 4096 + 6 * kTile > kRowsBudget)
-    p.nstg = 1;
-  const size_t sbytes = (size_t)kEpiWarps * p.nstg * 4096 + (H ? (size_t)kEpiWarps * 256 * 4 : 0);
+  auto ring_left = [&](int nepi, int nstg) -> int64_t {
+    const size_t sb = (size_t)nepi * nstg * 4096 + (H ? (size_t)nepi * 256 * 4 : 0);
+    const size_t used = wbytes + (size_t)kNL * kTile + sb;
+    return used > kRowsBudget ? -1 : (int64_t)((kRowsBudget - used) / kTile);
+  };
+  // (with 8 warps a warp drains ceil(Npad / 64) chunks per tile: one box each, up to two)
+  const int nstg8 = std::min(2, (Npad + 63) / 64);
+  p.nepi = (p.tma_store && Npad >= 64 && ring_left(kRowsEpiMax, nstg8) >= 4) ? kRowsEpiMax
+                                                                              : kEpiWarps;
+  p.nstg = p.tma_store ? (p.nepi == kRowsEpiMax ? nstg8 : 2) : 0;
+  if (p.tma_store && p.nstg == 2 && ring_left(p.nepi, 2) < 6) p.nstg = 1;
+  const size_t sbytes = (size_t)p.nepi * p.nstg * 4096 + (H ? (size_t)p.nepi * 256 * 4 : 0);
   p.nraw = (int)std::min<size_t>(kMaxRaw, (kRowsBudget - wbytes - sbytes - kNL * kTile) / kTile);
   const size_t smem = wbytes + (size_t)(p.nraw + kNL) * kTile + sbytes;
   cudaError_t e = cudaFuncSetAttribute(tc_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return fail(kCuda, "tc_rows smem: %s", cudaGetErrorString(e));
   const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
-  tc_rows_kernel<<<grid, kThreads, smem, st>>>(xmap, ymap, hmap, p);
+  tc_rows_kernel<<<grid, kRowsThreads, smem, st>>>(xmap, ymap, hmap, p);
   return post_launch("tc_rows_kernel");
 }
 
