@@ -265,9 +265,12 @@ int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* per
 size_t accel_fold_workspace_size(int nkeys, int D);
 int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off, int nkeys,
                               int nblocks, int D, float* out, void* workspace, void* stream);
+/* piece_key (nullable, from accel_group_by_key_blocked): the key of each piece
+ * (else found by a binary search over piece_off per piece). */
 int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
-                           const int64_t* seg_off, const int64_t* piece_off, int nkeys,
-                           int64_t n_pieces, float* piece_buf, float* out, void* stream);
+                           const int64_t* seg_off, const int64_t* piece_off,
+                           const int32_t* piece_key, int nkeys, int64_t n_pieces,
+                           float* piece_buf, float* out, void* stream);
 
 /* ---- value head (models.py:273-314, trainer.py:438-443) ---------------- */
 

@@ -209,17 +209,22 @@ stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, in
 __global__ void __launch_bounds__(kThreads)
 piece_sum_kernel(const float* __restrict__ vals, const int32_t* __restrict__ perm,
                  const int64_t* __restrict__ seg_off, const int64_t* __restrict__ piece_off,
-                 int nkeys, int D, float* __restrict__ piece_out) {
+                 const int32_t* __restrict__ piece_key, int nkeys, int D,
+                 float* __restrict__ piece_out) {
   extern __shared__ float s_acc[];
   const int64_t piece = blockIdx.x;
   if (piece >= piece_off[nkeys]) return;  // grid is sized for the worst case
-  // key of this piece: last j with piece_off[j] <= piece
-  int lo = 0, hi = nkeys;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (piece_off[mid] <= piece) lo = mid; else hi = mid;
+  int key;
+  if (piece_key != nullptr) {  // one load instead of a dependent binary search
+    key = __ldg(piece_key + piece);
+  } else {  // last j with piece_off[j] <= piece
+    int lo = 0, hi = nkeys;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (piece_off[mid] <= piece) lo = mid; else hi = mid;
+    }
+    key = lo;
   }
-  const int key = lo;
   const int64_t r0 = seg_off[key] + (piece - piece_off[key]) * kPiece;
   const int64_t r1 = min(seg_off[key + 1], r0 + kPiece);
   if ((D & 3) == 0) {
@@ -655,8 +660,8 @@ extern "C" int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* 
 // accel_group_max_pieces(R, nkeys) * D floats.
 extern "C" int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,
                                       const int64_t* seg_off, const int64_t* piece_off,
-                                      int nkeys, int64_t n_pieces, float* piece_buf, float* out,
-                                      void* stream) {
+                                      const int32_t* piece_key, int nkeys, int64_t n_pieces,
+                                      float* piece_buf, float* out, void* stream) {
   if (R < 0 || D < 1 || nkeys < 1 || n_pieces < 0) return fail(kDimension, "grouped_rows_sum: bad sizes");
   if (!perm || !seg_off || !piece_off || !piece_buf || !out)
     return fail(kDimension, "grouped_rows_sum: NULL buffer");
@@ -666,7 +671,7 @@ extern "C" int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const
   int st;
   if (vals && n_pieces > 0) {  // vals == NULL: piece_buf already holds the piece sums
     piece_sum_kernel<<<(unsigned)n_pieces, kThreads, kThreads * sizeof(float4), s>>>(
-        vals, perm, seg_off, piece_off, nkeys, D, piece_buf);
+        vals, perm, seg_off, piece_off, piece_key, nkeys, D, piece_buf);
     if ((st = post_launch("piece_sum_kernel"))) return st;
   }
   if ((D & 3) == 0 && ((reinterpret_cast<uintptr_t>(piece_buf) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {

@@ -231,8 +231,7 @@ class Grouping:
         self.seg_off = torch.empty(nk + 1, dtype=I64, device=dev)
         self.piece_off = torch.empty(nk + 1, dtype=I64, device=dev)
         self.max_pieces = int(lib.accel_group_max_pieces_blocked(R, nkeys, self.cpb))
-        self.piece_key = (torch.empty(max(self.max_pieces, 1), dtype=I32, device=dev)
-                          if cpb > 0 else None)
+        self.piece_key = torch.empty(max(self.max_pieces, 1), dtype=I32, device=dev)
         nbytes = lib.accel_group_workspace_size_blocked(R, nkeys, self.cpb)
         buf = stream_workspace("group", nbytes)
         self.pos = None
@@ -279,8 +278,8 @@ class Grouping:
         if self.cpb > 0:
             raise DimensionError("rows_sum needs a plain (unblocked) grouping")
         _lib.call("accel_grouped_rows_sum", _pp(vals), self.R, D, _pp(self.perm), _pp(self.seg_off),
-                  _pp(self.piece_off), self.nkeys, self.max_pieces, _pp(piece_buf), _pp(out),
-                  _stream())
+                  _pp(self.piece_off), _pp(self.piece_key), self.nkeys, self.max_pieces,
+                  _pp(piece_buf), _pp(out), _stream())
         return out
 
     def _key_pass(self, piece_buf, D, out):
@@ -290,8 +289,8 @@ class Grouping:
                       self.nblocks, D, _pp(out), _pp(wsb), _stream())
         else:
             _lib.call("accel_grouped_rows_sum", None, self.R, D, _pp(self.perm), _pp(self.seg_off),
-                      _pp(self.piece_off), self.nkeys, self.max_pieces, _pp(piece_buf), _pp(out),
-                      _stream())
+                      _pp(self.piece_off), _pp(self.piece_key), self.nkeys, self.max_pieces,
+                      _pp(piece_buf), _pp(out), _stream())
 
 
 def prev_keys(tokens, N, K, A, with_pos=False, out=None):
