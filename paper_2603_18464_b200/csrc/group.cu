@@ -22,7 +22,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 4096;   // rows per warp chunk (more chunks: more warps in the scatter)
+constexpr int kChunk = 4096;   // rows per block unit (the caller's cpb counts these)
+// rows per warp chunk of the histogram / scatter: 4096, or fewer for small R so
+// that enough warps take part (a chunk is walked serially by one warp)
+inline int chunk_rows(int64_t R) {
+  int c = kChunk;
+  while (c > 256 && ceil_div(R, (int64_t)c) < (int64_t)kNumSMs * 8) c >>= 1;
+  return c;
+}
 constexpr int kPiece = 256;    // rows per grouped-sum piece
 
 // key = prev (with_pos == 0) or prev * K + k (with_pos == 1); prev = A at k == 0
@@ -70,7 +77,7 @@ __device__ __forceinline__ int64_t count_idx(int64_t chunk, int key, int nkeys, 
 
 __global__ void __launch_bounds__(kThreads)
 chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
-                  int64_t cpb, int* __restrict__ counts) {
+                  int64_t cpb, int crows, int* __restrict__ counts) {
   extern __shared__ int s_hist[];  // [kWarps][nkeys]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* h = s_hist + warp * nkeys;
@@ -78,7 +85,7 @@ chunk_hist_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_
   __syncwarp();
   const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
   if (chunk < n_chunks) {
-    const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
+    const int64_t r0 = chunk * crows, r1 = min(R, r0 + crows);
     for (int64_t r = r0 + lane; r < r1; r += 32 * 8) {  // eight key loads in flight per lane
       int kk[8];
 #pragma unroll
@@ -134,8 +141,8 @@ segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks
 
 __global__ void __launch_bounds__(kThreads)
 stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, int64_t n_chunks,
-                      int64_t cpb, const int* __restrict__ base, int32_t* __restrict__ perm,
-                      SortedRows sr) {
+                      int64_t cpb, int crows, const int* __restrict__ base,
+                      int32_t* __restrict__ perm, SortedRows sr) {
   extern __shared__ int s_ctr[];  // [kWarps][nkeys]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t chunk = (int64_t)blockIdx.x * kWarps + warp;
@@ -153,7 +160,7 @@ stable_scatter_kernel(const int32_t* __restrict__ keys, int64_t R, int nkeys, in
       if (j0 + 32 * u < nkeys) ctr[j0 + 32 * u] = v[u];
   }
   __syncwarp();
-  const int64_t r0 = chunk * kChunk, r1 = min(R, r0 + kChunk);
+  const int64_t r0 = chunk * crows, r1 = min(R, r0 + crows);
   const unsigned lt = (1u << lane) - 1u;
   const int kbits = nkeys > 1 ? 32 - __clz(nkeys - 1) : 1;  // bits of the largest key
   for (int64_t g0 = r0; g0 < r1; g0 += 32 * 8) {
@@ -514,13 +521,15 @@ extern "C" int accel_step_keys(const int32_t* steps, const int32_t* frame_of, in
 }
 
 namespace {
+// the caller's cpb counts 4096-row units; internally a block is cpb * (4096 /
+// chunk_rows) warp chunks (the same rows)
 int64_t blocks_of(int64_t R, int64_t cpb) {
-  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
+  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, (int64_t)chunk_rows(R)));
   return cpb <= 0 ? 1 : ceil_div(n_chunks, cpb);
 }
 int64_t cpb_of(int64_t R, int64_t cpb) {
-  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
-  return cpb <= 0 ? n_chunks : std::min(cpb, n_chunks);
+  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, (int64_t)chunk_rows(R)));
+  return cpb <= 0 ? n_chunks : std::min(cpb * (kChunk / chunk_rows(R)), n_chunks);
 }
 }  // namespace
 
@@ -564,7 +573,8 @@ extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nk
   if (workspace_bytes < accel_group_workspace_size_blocked(R, nkeys, cpb))
     return fail(kDimension, "group_by_key: workspace too small");
   cudaStream_t s = as_stream(stream);
-  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, kChunk));
+  const int crows = chunk_rows(R);
+  const int64_t n_chunks = std::max<int64_t>(1, ceil_div(R, (int64_t)crows));
   const int64_t c = cpb_of(R, cpb), nb = blocks_of(R, c);
   const int64_t n = (int64_t)nkeys * nb * c;
   if (n >= ((int64_t)1 << 31) || nkeys * nb >= ((int64_t)1 << 31))
@@ -586,7 +596,7 @@ extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nk
     if ((st = check_cuda(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n, s), "group memset")))
       return st;
   }
-  chunk_hist_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, counts);
+  chunk_hist_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, crows, counts);
   if ((st = post_launch("chunk_hist_kernel"))) return st;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, counts, base, (int)n, s);
   if (e != cudaSuccess) return fail(kCuda, "DeviceScan: %s", cudaGetErrorString(e));
@@ -617,7 +627,8 @@ extern "C" int accel_group_by_key_blocked(const int32_t* keys, int64_t R, int nk
     return fail(kDimension, "group_by_key: sorted rows need frame_of, tokens, outputs, K");
   if ((row_frame == nullptr) != (row_tok == nullptr))
     return fail(kDimension, "group_by_key: row_frame and row_tok go together");
-  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, base, perm, sr);
+  stable_scatter_kernel<<<grid, kThreads, smem, s>>>(keys, R, nkeys, n_chunks, c, crows, base, perm,
+                                                     sr);
   return post_launch("stable_scatter_kernel");
 }
 

@@ -402,11 +402,11 @@ __global__ void small_gemm_sum_kernel(const float* __restrict__ part, int ks, in
 }
 
 // k slices of a small product: when its output tiles leave SMs idle and the
-// reduction is long, split k (>= 256 per slice) until ~2 waves of blocks
+// reduction is long, split k (>= 128 per slice) until ~2 waves of blocks
 int small_gemm_slices(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ceil_div(M, (int64_t)kSgT) * ceil_div(N, (int64_t)kSgT);
-  if (tiles >= kNumSMs || K < 512) return 1;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, (int64_t)256),
+  if (tiles >= kNumSMs || K < 256) return 1;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, (int64_t)128),
                                                      2 * kNumSMs / tiles));
 }
 

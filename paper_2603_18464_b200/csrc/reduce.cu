@@ -34,9 +34,9 @@ struct Segs {
 // Two fixed-order schedules (chosen by the segment's part count only, so every
 // launch of a segment sums in the same order):
 //  * few parts (< 16): a lane owns 4 columns and adds the parts in order;
-//  * many parts (the per-CTA weight-gradient partials): the 8 warps of a block
-//    each add a fixed 1/8 of the parts for the same 128 columns, then the warp
-//    sums are added in warp order -- 8x the loads in flight of one chain.
+//  * many parts (the per-CTA weight-gradient partials): the 16 warps of a block
+//    each add a fixed 1/16 of the parts for the same 128 columns (eight rows in
+//    flight), then the warp sums are added in warp order.
 __device__ __forceinline__ void load4(const float* p, bool vec, int64_t j, int64_t len, double* a) {
   if (vec && j + 3 < len) {
     const float4 x = __ldcs(reinterpret_cast<const float4*>(p + j));
@@ -61,8 +61,10 @@ __device__ __forceinline__ void store4(float* p, bool vec, int64_t j, int64_t le
   }
 }
 
-__global__ void __launch_bounds__(256) reduce_segments_kernel(Segs s) {
-  __shared__ double red[8][32][4];
+constexpr int kSegThreads = 512;
+constexpr int kSegWarps = kSegThreads / 32;
+__global__ void __launch_bounds__(kSegThreads) reduce_segments_kernel(Segs s) {
+  __shared__ double red[kSegWarps][32][4];
   const int seg = blockIdx.y;
   const int64_t len = s.len[seg], parts = s.parts[seg], pitch = s.pitch[seg];
   const float* src = s.src[seg];
@@ -79,14 +81,14 @@ __global__ void __launch_bounds__(256) reduce_segments_kernel(Segs s) {
     }
     return;
   }
-  const int64_t p0 = warp * parts / 8, p1 = (warp + 1) * parts / 8;
+  const int64_t p0 = warp * parts / kSegWarps, p1 = (warp + 1) * parts / kSegWarps;
   for (int64_t c0 = (int64_t)blockIdx.x * 128; c0 < len; c0 += (int64_t)gridDim.x * 128) {
     const int64_t j = c0 + 4 * lane;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     int64_t p = p0;
-    for (; p + 4 <= p1; p += 4) {  // four independent rows in flight
+    for (; p + 8 <= p1; p += 8) {  // eight independent rows in flight
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load4(src + (p + u) * pitch, vec, j, len, a);
+      for (int u = 0; u < 8; ++u) load4(src + (p + u) * pitch, vec, j, len, a);
     }
     for (; p < p1; ++p) load4(src + p * pitch, vec, j, len, a);
 #pragma unroll
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(256) reduce_segments_kernel(Segs s) {
     __syncthreads();
     if (warp == 0) {
       double t[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int w = 0; w < 8; ++w)
+      for (int w = 0; w < kSegWarps; ++w)
 #pragma unroll
         for (int c = 0; c < 4; ++c) t[c] += red[w][lane][c];
       store4(dst, vec, j, len, t);
@@ -339,7 +341,7 @@ extern "C" int accel_reduce_segments(const void* const* srcs, void* const* dsts,
   // gradients are 16.7 M floats at cfg4)
   dim3 grid((unsigned)std::min<int64_t>(ceil_div(maxlen, 128), std::max(64, 2368 / nseg)),
             (unsigned)nseg);
-  reduce_segments_kernel<<<grid, 256, 0, as_stream(stream)>>>(s);
+  reduce_segments_kernel<<<grid, kSegThreads, 0, as_stream(stream)>>>(s);
   return post_launch("reduce_segments_kernel");
 }
 
