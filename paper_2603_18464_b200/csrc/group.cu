@@ -395,9 +395,9 @@ fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
                            const int64_t* __restrict__ piece_off, int nkeys, int nblocks, int D4,
                            float4* __restrict__ part) {
   __shared__ float4 s4[kFoldThreads];
-  const int key = blockIdx.x, q = blockIdx.y;
-  const int b0 = (int)((int64_t)nblocks * q / kFoldSplit);
-  const int b1 = (int)((int64_t)nblocks * (q + 1) / kFoldSplit);
+  const int key = blockIdx.x, q = blockIdx.y, split = gridDim.y;
+  const int b0 = (int)((int64_t)nblocks * q / split);
+  const int b1 = (int)((int64_t)nblocks * (q + 1) / split);
   const int span = D4 <= kFoldThreads && kFoldThreads % D4 == 0 ? D4 : kFoldThreads;
   const int sub = kFoldThreads / span;
   const int lr = threadIdx.x / span, lc = threadIdx.x % span;
@@ -442,11 +442,11 @@ fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
 }
 
 __global__ void fold_parts_kernel(const float4* __restrict__ part, int64_t n4, int64_t stride4,
-                                  float4* __restrict__ out) {
+                                  int split, float4* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   float4 r = part[i];
-  for (int q = 1; q < kFoldSplit; ++q) {
+  for (int q = 1; q < split; ++q) {
     const float4 y = part[q * stride4 + i];
     r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
   }
@@ -657,12 +657,14 @@ extern "C" int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* 
     return fail(kDimension, "fold_blocked: buffers must be 16B aligned");
   cudaStream_t s = as_stream(stream);
   float4* part = static_cast<float4*>(workspace);
-  fold_blocked_pieces_kernel<<<dim3(nkeys, kFoldSplit), kFoldThreads, 0, s>>>(
-      reinterpret_cast<const float4*>(piece_buf), piece_off, nkeys, nblocks, D / 4, part);
+  const int split = std::min(kFoldSplit, nblocks);  // fixed by nblocks: deterministic
+  float4* dst = split == 1 ? reinterpret_cast<float4*>(out) : part;
+  fold_blocked_pieces_kernel<<<dim3(nkeys, split), kFoldThreads, 0, s>>>(
+      reinterpret_cast<const float4*>(piece_buf), piece_off, nkeys, nblocks, D / 4, dst);
   int st = post_launch("fold_blocked_pieces_kernel");
-  if (st) return st;
+  if (st || split == 1) return st;
   const int64_t n4 = (int64_t)nkeys * (D / 4);
-  fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(part, n4, n4,
+  fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(part, n4, n4, split,
                                                                 reinterpret_cast<float4*>(out));
   return post_launch("fold_parts_kernel");
 }

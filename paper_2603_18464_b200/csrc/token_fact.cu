@@ -636,6 +636,15 @@ token_loss_fact_grp_kernel(const float* __restrict__ h2w, const float* __restric
 #endif
 constexpr int kF2MaxWarps = ACCEL_F2_WARPS;
 constexpr int kF2Chunk = 32;  // transitions per dynamically claimed chunk (and statistics row)
+static_assert(kF2Chunk == 1 << 5, "the compile-time chunk shift below is 5");
+// small batches: shorter chunks so every warp of the persistent grid gets work
+// (a chunk's transitions run serially in one warp); fixed by N, so the
+// statistics rows -- and the pooled sums -- are still deterministic
+inline int fact2_chunk(int64_t N) {
+  int c = kF2Chunk;
+  while (c > 4 && ceil_div(N, (int64_t)c) < (int64_t)kNumSMs * 2 * kF2MaxWarps) c >>= 1;
+  return c;
+}
 
 // After the call lane l holds the warp total of value index l / (32 / NV).
 template <int NV>
@@ -667,7 +676,9 @@ __host__ __device__ constexpr int fact2_warp_floats(int K, int A) { return (2 * 
 // interleave); KT == 0: runtime K <= KMAX.
 // SC: write the per-token scalars {nm2, Ac, Cc, coef} (tsc) instead of the dz
 // rows; the frame-blocked grouped sums recompute dz (fact_group_sum_kernel).
-template <int VPL, int KMAX, int KT, bool SC>
+// CS >= 0: the chunk shift as a compile-time constant (the full-chunk case of
+// large batches); CS < 0: chunk_shift at run time
+template <int VPL, int KMAX, int KT, bool SC, int CS = -1>
 __global__ void __launch_bounds__(kF2MaxWarps * 32, 2)
 token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__ epp,
                         const int32_t* __restrict__ frame_of, const int32_t* __restrict__ tokens,
@@ -676,7 +687,9 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
                         float* __restrict__ dz, float* __restrict__ g_frame,
                         float* __restrict__ lp_new, double* __restrict__ stat_part,
                         double* __restrict__ max_part, unsigned* __restrict__ work_ctr,
-                        float4* __restrict__ tsc, const int32_t* __restrict__ tsc_pos) {
+                        float4* __restrict__ tsc, const int32_t* __restrict__ tsc_pos,
+                        int chunk_shift_rt) {
+  const int chunk_shift = CS >= 0 ? CS : chunk_shift_rt;
   constexpr int A = VPL * 32;
   constexpr int Q = VPL / 4;  // float4 chunks per lane (column q * 128 + lane * 4 + r)
   constexpr int P = VPL / 2;  // float2 pairs per lane
@@ -750,16 +763,17 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[b]))
                  : "memory");
   };
-  // dynamic schedule: warps claim chunks of kF2Chunk consecutive transitions
+  // dynamic schedule: warps claim chunks of `chunk` consecutive transitions
   // from a device counter (zeroed by the host before the launch), one chunk
   // ahead, so SMs that run faster take more chunks; next(x) is the transition
   // after x in this warp's sequence (N = none)
+  const int64_t cmask = ((int64_t)1 << chunk_shift) - 1;  // chunks are powers of two
   unsigned pend = 0;  // lane 0: the pre-claimed next chunk (resolved lazily)
   auto claim = [&]() -> unsigned { return lane == 0 ? atomicAdd(work_ctr, 1u) : 0u; };
   auto next_of = [&](int64_t x) -> int64_t {
     if (x >= N) return N;
-    if ((x + 1) % kF2Chunk != 0 && x + 1 < N) return x + 1;
-    const int64_t y = (int64_t)__shfl_sync(0xffffffffu, pend, 0) * kF2Chunk;
+    if (((x + 1) & cmask) != 0 && x + 1 < N) return x + 1;
+    const int64_t y = (int64_t)__shfl_sync(0xffffffffu, pend, 0) << chunk_shift;
     pend = claim();
     return y < N ? y : N;
   };
@@ -769,7 +783,7 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
   double st_rmax = -CUDART_INF, st_negw = -CUDART_INF;
   int st_out = 0, st_excl = 0, st_bad = 0, st_badtok = 0;
 
-  int64_t i = (int64_t)__shfl_sync(0xffffffffu, claim(), 0) * kF2Chunk;
+  int64_t i = (int64_t)__shfl_sync(0xffffffffu, claim(), 0) << chunk_shift;
   i = i < N ? i : N;
   pend = claim();
   int64_t i1 = next_of(i);
@@ -951,10 +965,10 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
     }
     __syncwarp();
     if (own && !bad_tok) s_oh[tok] = 0.f;
-    // a chunk of kF2Chunk transitions is done: its statistics go to the chunk's own
+    // a chunk of `chunk` transitions is done: its statistics go to the chunk's own
     // partial row (warp-reduced in a fixed order), so the pooled sums do not
     // depend on which warp the dynamic schedule handed the chunk to
-    if (!cx.fixup && ((i + 1) % kF2Chunk == 0 || i + 1 == N)) {
+    if (!cx.fixup && (((i + 1) & cmask) == 0 || i + 1 == N)) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         st_loss += __shfl_xor_sync(0xffffffffu, st_loss, o);
@@ -969,7 +983,7 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
       st_bad = __reduce_add_sync(0xffffffffu, st_bad);
       st_badtok = __reduce_add_sync(0xffffffffu, st_badtok);
       if (lane == 0) {
-        const int64_t c = i / kF2Chunk;
+        const int64_t c = i >> chunk_shift;
         double* st = stat_part + c * kNumStat;
         st[kLossNum] = st_loss;
         st[kEntSum] = st_ent;
@@ -994,22 +1008,50 @@ token_loss_fact2_kernel(const float* __restrict__ h2w, const float* __restrict__
 }
 
 // Dprev[j] = sum_k Dpk[j, k], Dpos[k] = sum_j Dpk[j, k]  (Dpk f32[(A+1), K, A])
+// Dprev: a thread per output (K terms).  Dpos: a block per (k, 32-column
+// group): 8 warps each sum a fixed 1/8 of the nprev rows (eight loads in
+// flight), the warp sums are added in warp order -- the long column sums run
+// 8-way parallel instead of as one 257-load chain per thread.
 __global__ void pk_marginals_kernel(const float* __restrict__ dpk, int K, int A, int nprev,
-                                    float* __restrict__ dprev, float* __restrict__ dpos) {
-  const int64_t total = (int64_t)(nprev + K) * A;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(e % A);
-    const int64_t r = e / A;
-    float s = 0.f;
-    if (r < nprev) {
-      for (int k = 0; k < K; ++k) s += dpk[(r * K + k) * A + a];
+                                    int dprev_blocks, float* __restrict__ dprev,
+                                    float* __restrict__ dpos) {
+  if ((int)blockIdx.x < dprev_blocks) {
+    const int64_t total = (int64_t)nprev * A;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)dprev_blocks * blockDim.x) {
+      const int a = (int)(e % A);
+      const int64_t r = e / A;
+      float s = 0.f;
+      for (int k = 0; k < K; ++k) s += __ldg(dpk + (r * K + k) * A + a);
       dprev[r * A + a] = s;
-    } else {
-      const int k = (int)(r - nprev);
-      for (int jj = 0; jj < nprev; ++jj) s += dpk[((int64_t)jj * K + k) * A + a];
-      dpos[(int64_t)k * A + a] = s;
     }
+    return;
+  }
+  __shared__ float s_part[8][32];
+  const int groups = (A + 31) / 32;
+  const int bid = (int)blockIdx.x - dprev_blocks;
+  const int k = bid / groups, a = (bid % groups) * 32 + (threadIdx.x & 31);
+  const int w = threadIdx.x >> 5;
+  const int j0 = w * nprev / 8, j1 = (w + 1) * nprev / 8;
+  float s = 0.f;
+  if (a < A) {
+    int jj = j0;
+    for (; jj + 8 <= j1; jj += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(dpk + ((int64_t)(jj + u) * K + k) * A + a);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; jj < j1; ++jj) s += __ldg(dpk + ((int64_t)jj * K + k) * A + a);
+  }
+  s_part[w][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (w == 0 && a < A) {
+    float t = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += s_part[u][threadIdx.x];
+    dpos[(int64_t)k * A + a] = t;
   }
 }
 
@@ -1311,7 +1353,7 @@ extern "C" int accel_sorted_rows(const int32_t* perm, const int32_t* frame_of,
 // under its dynamic schedule), one per CTA (accel_fact_grid) otherwise.
 extern "C" int64_t accel_fact_partials(int64_t N, int K, int A, int scalar_out) {
   (void)scalar_out;
-  if (K <= 8 && (A == 128 || A == 256)) return std::max<int64_t>(1, ceil_div(N, kF2Chunk));
+  if (K <= 8 && (A == 128 || A == 256)) return std::max<int64_t>(1, ceil_div(N, (int64_t)fact2_chunk(N)));
   return accel_fact_grid(N);
 }
 
@@ -1417,11 +1459,13 @@ extern "C" int accel_token_loss_fact2(const float* h2w, const float* epp, const 
       return fail(kCuda, "token_loss_fact2: counter reset");
     kernel<<<grid, nw * 32, smem, s>>>(h2w, epp, frame_of, tokens, lp_old, adv, N, K, prm,
                                        fix_stats, dz, g_frame, lp_new, stat_part, max_part, ctr,
-                                       static_cast<float4*>(tsc), tsc_pos);
+                                       static_cast<float4*>(tsc), tsc_pos,
+                                       __builtin_ctz((unsigned)fact2_chunk(N)));
     return post_launch("token_loss_fact2_kernel");
   };
   if (K == 7 && A == 256)
-    return tsc ? two_phase(token_loss_fact2_kernel<8, 8, 7, true>)
+    return tsc ? (fact2_chunk(N) == kF2Chunk ? two_phase(token_loss_fact2_kernel<8, 8, 7, true, 5>)
+                                             : two_phase(token_loss_fact2_kernel<8, 8, 7, true>))
                : two_phase(token_loss_fact2_kernel<8, 8, 7, false>);
   if (K <= 8 && A == 256)
     return tsc ? two_phase(token_loss_fact2_kernel<8, 8, 0, true>)
@@ -1459,8 +1503,9 @@ extern "C" int accel_pk_marginals(const float* dpk, int K, int A, float* dprev, 
                                   void* stream) {
   if (K < 1 || A < 1 || !dpk || !dprev || !dpos) return fail(kDimension, "pk_marginals: bad args");
   const int nprev = A + 1;
-  const int64_t total = (int64_t)(nprev + K) * A;
-  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)kNumSMs * 4);
-  pk_marginals_kernel<<<grid, 256, 0, as_stream(stream)>>>(dpk, K, A, nprev, dprev, dpos);
+  const int dprev_blocks = (int)std::min<int64_t>(ceil_div((int64_t)nprev * A, 256), (int64_t)kNumSMs * 2);
+  const int grid = dprev_blocks + K * ((A + 31) / 32);
+  pk_marginals_kernel<<<grid, 256, 0, as_stream(stream)>>>(dpk, K, A, nprev, dprev_blocks, dprev,
+                                                           dpos);
   return post_launch("pk_marginals_kernel");
 }

@@ -642,8 +642,10 @@ value_attn_wgrad4_kernel(const float* __restrict__ de, const float4* __restrict_
   }
 }
 
+// CTAs of the warp-per-row value kernels: >= 8 rows per warp (fewer partial rows
+// to reduce at small batches), at most 8 CTAs per SM
 int warp_grid(int64_t rows) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, kWarps), (int64_t)kNumSMs * 8));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, kWarps * 8), (int64_t)kNumSMs * 8));
 }
 
 }  // namespace
