@@ -573,21 +573,48 @@ def main():
     e2e = None
     host = {k: v.cpu().pin_memory() if k != "traj_off" else v.cpu() for k, v in inputs.items()}
     if not args.no_e2e:
+        # every step copies its own inputs from pinned host memory and reads its
+        # record back; two device input sets and a copy stream let step i + 1's
+        # upload run under step i's kernels (the copy is still inside the timed
+        # region of every step -- the PCIe link is the bound)
         h2d = sum(v.numel() * v.element_size() for v in host.values())
-        dev_in = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
-        staging = dev_in["frames"]  # contiguous landing buffer for the frame rows
-        dev_in["frames"] = ops.alloc_pitched(*host["frames"].shape, dev)
+        bufs, stagings = [], []
+        for _ in range(2):
+            b = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+            stagings.append(b["frames"])  # contiguous landing buffer for the frame rows
+            b["frames"] = ops.alloc_pitched(*host["frames"].shape, dev)
+            bufs.append(b)
+        copy_stream = torch.cuda.Stream(device=dev)
 
-        def upload():
-            for k in host:
-                if k == "frames":  # contiguous DMA, then re-pitch on the device
-                    staging.copy_(host[k], non_blocking=True)
-                    dev_in[k].copy_(staging)
-                else:
-                    dev_in[k].copy_(host[k], non_blocking=True)
+        def upload(i):
+            with torch.cuda.stream(copy_stream):
+                for k in host:
+                    if k == "frames":  # contiguous DMA, then re-pitch on the device
+                        stagings[i].copy_(host[k], non_blocking=True)
+                        bufs[i][k].copy_(stagings[i])
+                    else:
+                        bufs[i][k].copy_(host[k], non_blocking=True)
 
-        upload()
-        step(dev_in)
+        def run_pipelined(nsteps, start_event=None):
+            ready = [torch.cuda.Event(), torch.cuda.Event()]
+            free = [torch.cuda.Event(), torch.cuda.Event()]
+            main = torch.cuda.current_stream()
+            if start_event is not None:
+                copy_stream.wait_event(start_event)
+            upload(0)
+            ready[0].record(copy_stream)
+            for i in range(nsteps):
+                b = i & 1
+                if i + 1 < nsteps:  # the next step's inputs, once its buffer is free
+                    if i >= 1:
+                        copy_stream.wait_event(free[b ^ 1])
+                    upload(b ^ 1)
+                    ready[b ^ 1].record(copy_stream)
+                main.wait_event(ready[b])
+                step(bufs[b])
+                free[b].record(main)
+
+        run_pipelined(2)  # warm-up
         if comm is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -595,9 +622,7 @@ def main():
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()
-        for _ in range(args.steps):
-            upload()
-            step(dev_in)
+        run_pipelined(args.steps, a0)
         a1.record()
         torch.cuda.synchronize()
         e_ms = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device=dev)
@@ -606,8 +631,9 @@ def main():
         e_ms = float(e_ms.item())
         e2e = {"value": float(tot.item()) / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": (18 + 20) * 8, "ms_per_step": e_ms,
-               "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
-        del dev_in
+               "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps,
+               "pipelined": "double-buffered inputs, uploads on a copy stream under the previous step"}
+        del bufs, stagings
 
     extra = {}
     if not args.no_extra and args.workload == "cfg2":
