@@ -581,26 +581,37 @@ class Trainer:
         return out.double().cpu().numpy()
 
     # -- batch construction (trainer.py:358-403) --------------------------------------
-    def upload(self, pb: PackedBatch) -> dict:
+    def upload(self, pb: PackedBatch, pre: dict | None = None) -> dict:
+        """Device copies of a packed batch; `pre` holds fields already uploaded
+        while the pack ran ("mu", and "frames_c": contiguous frame rows)."""
         d = self.dims
         if pb.obs_dim != d.obs_dim or pb.chunk_len != d.chunk_len or pb.n_actions != d.n_actions:
             raise DimensionError(
                 f"batch (obs {pb.obs_dim}, K {pb.chunk_len}, A {pb.n_actions}) does not match "
                 f"the policy (obs {d.obs_dim}, K {d.chunk_len}, A {d.n_actions})")
         dev = self.device
+        pre = pre or {}
+        if "frames_c" in pre:  # re-pitch the contiguous rows on the device
+            fc = pre["frames_c"]
+            frames = ops.alloc_pitched(fc.shape[0], fc.shape[1], dev)
+            frames = frames.copy_(fc) if not frames.is_contiguous() else fc
+        else:
+            frames = ops.upload_pitched(np.asarray(pb.frames, dtype=np.float32), dev)
         return {
             "traj_off": _dev(pb.traj_off, np.int64, dev),
-            "frames": ops.upload_pitched(np.asarray(pb.frames, dtype=np.float32), dev),
+            "frames": frames,
             "steps": _dev(pb.steps, np.int32, dev),
             "values": _dev(pb.values, np.float32, dev),
             "tokens": _dev(pb.tokens.reshape(-1), np.int32, dev),
             "rewards": _dev(pb.rewards, np.float32, dev),
-            "mu": _dev(pb.mu.reshape(-1, pb.n_actions), np.float32, dev),
+            "mu": pre["mu"] if "mu" in pre else _dev(pb.mu.reshape(-1, pb.n_actions), np.float32,
+                                                       dev),
             "done": _dev(pb.done, np.uint8, dev),
         }
 
     def build_train_batch(self, trajs) -> DeviceTrainBatch | None:
         """Recompute, estimate advantages, normalize globally, tensorize."""
+        pre = None
         if isinstance(trajs, PackedBatch):
             pb = trajs
         elif trajs and isinstance(trajs[0], DeviceTrajectory):
@@ -620,10 +631,26 @@ class Trainer:
             for t in trajs:
                 if self.cfg.revalue:
                     assert self.publish_version >= t.behavior_version
-            # one threaded pass casting into page-locked staging; the upload below
-            # is asynchronous DMA (the build's one host sync orders its reuse)
-            pb = pack_trajectories(trajs, staging=self._staging)
-        dev_batch = self.upload(pb)
+            # one threaded pass casting into page-locked staging, in four chunks:
+            # each chunk's behavior logits and frame rows (the bulk of the bytes)
+            # go to the device as asynchronous DMA while the next chunk is packed
+            # (the build's one host sync orders the staging's reuse)
+            pre = {}
+
+            def on_chunk(lo, hi, off, frames, mu):
+                if not pre:
+                    pre["mu"] = torch.empty(mu.shape[0] * mu.shape[1], mu.shape[2],
+                                            dtype=F32, device=self.device)
+                    pre["frames_c"] = torch.empty(frames.shape, dtype=F32, device=self.device)
+                a, b = int(off[lo]), int(off[hi])
+                K = mu.shape[1]
+                pre["mu"][a * K:b * K].copy_(torch.from_numpy(mu[a:b].reshape(-1, mu.shape[2])),
+                                             non_blocking=True)
+                pre["frames_c"][a + lo:b + hi].copy_(torch.from_numpy(frames[a + lo:b + hi]),
+                                                     non_blocking=True)
+
+            pb = pack_trajectories(trajs, staging=self._staging, chunks=4, on_chunk=on_chunk)
+        dev_batch = self.upload(pb, pre)
         return self.build_from_device(dev_batch, n_real=int(pb.real.sum()),
                                       behavior_version=pb.behavior_version)
 

@@ -120,12 +120,17 @@ def _pack_rows(trajs, lens, off, frames, steps, values, tokens, rewards, mu, lo,
 
 
 def pack_trajectories(trajs, staging: PinnedStaging | None = None,
-                      threads: int | None = None) -> PackedBatch:
+                      threads: int | None = None, chunks: int = 1,
+                      on_chunk=None) -> PackedBatch:
     """Flatten duck-typed trajectories into the CSR wire format (float32).
 
     Every field is written once, cast in place, into preallocated rows (with
     `staging`: page-locked buffers, so the upload is asynchronous DMA); the
-    copies run on a thread pool over trajectories (NumPy releases the GIL)."""
+    copies run on a thread pool over trajectories (NumPy releases the GIL).
+    chunks > 1: the trajectories are packed in that many consecutive ranges
+    (balanced by transitions) and on_chunk(lo, hi, off, frames, mu) is called
+    after each, so the caller can start that range's upload while the next one
+    is packed."""
     if not trajs:
         raise DimensionError("cannot pack an empty trajectory list")
     k = int(np.asarray(trajs[0].tokens).shape[1])
@@ -158,16 +163,30 @@ def pack_trajectories(trajs, staging: PinnedStaging | None = None,
     rewards = alloc("rewards", (N,), np.float32)
     mu = alloc("mu", (N, k, a), np.float32)
     args = (trajs, lens, off, frames, steps, values, tokens, rewards, mu)
-    workers = min(threads or 8, max(1, N // 4096), n)
-    if workers <= 1:
-        _pack_rows(*args, 0, n)
-    else:
-        from concurrent.futures import ThreadPoolExecutor
-        # contiguous trajectory ranges balanced by transition count
-        cuts = np.searchsorted(off, np.linspace(0, N, workers + 1)[1:-1]).tolist()
-        bounds = [0] + cuts + [n]
-        with ThreadPoolExecutor(workers) as ex:
-            list(ex.map(lambda i: _pack_rows(*args, bounds[i], bounds[i + 1]), range(workers)))
+    # consecutive chunks of trajectories (balanced by transition count)
+    cb = sorted(set([0] + np.searchsorted(off, np.linspace(0, N, max(1, chunks) + 1)[1:-1]).tolist()
+                    + [n]))
+    ex = None
+    try:
+        for lo, hi in zip(cb[:-1], cb[1:]):
+            n_c = int(off[hi] - off[lo])
+            workers = min(threads or 8, max(1, n_c // 4096), hi - lo)
+            if workers <= 1:
+                _pack_rows(*args, lo, hi)
+            else:
+                if ex is None:
+                    from concurrent.futures import ThreadPoolExecutor
+                    ex = ThreadPoolExecutor(threads or 8)
+                # contiguous trajectory ranges balanced by transition count
+                cuts = np.searchsorted(off, np.linspace(off[lo], off[hi], workers + 1)[1:-1]).tolist()
+                bounds = [lo] + [min(max(c, lo), hi) for c in cuts] + [hi]
+                list(ex.map(lambda i: _pack_rows(*args, bounds[i], bounds[i + 1]),
+                            range(workers)))
+            if on_chunk is not None:
+                on_chunk(lo, hi, off, frames, mu)
+    finally:
+        if ex is not None:
+            ex.shutdown()
     return PackedBatch(
         traj_off=off, frames=frames, steps=steps, values=values, tokens=tokens, rewards=rewards,
         mu=mu,

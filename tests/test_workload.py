@@ -51,3 +51,28 @@ def test_pack_into_pinned_staging_reuses_buffers():
         _check(pb, trajs)
     import torch
     assert torch.from_numpy(pb.mu).is_pinned()
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 7])
+def test_chunked_pack_reports_consecutive_ranges(chunks):
+    """chunks > 1 (the drop-in uploads each chunk while the next is packed):
+    the same arrays, and on_chunk sees consecutive trajectory ranges covering
+    the batch, each already packed when reported."""
+    rng = np.random.default_rng(5)
+    trajs = synthetic_trajectories(rng, rng.integers(1, 300, size=23), rng.random(23) < 0.5,
+                                   3, 16, 9)
+    seen = []
+
+    def on_chunk(lo, hi, off, frames, mu):
+        a, b = int(off[lo]), int(off[hi])
+        want = np.concatenate([t.behavior_logits for t in trajs[lo:hi]]).astype(np.float32)
+        np.testing.assert_array_equal(mu[a:b], want)
+        wf = np.concatenate([t.observations for t in trajs[lo:hi]]).astype(np.float32)
+        np.testing.assert_array_equal(frames[a + lo:b + hi], wf)
+        seen.append((lo, hi))
+
+    pb = pack_trajectories(trajs, threads=4, chunks=chunks, on_chunk=on_chunk)
+    _check(pb, trajs)
+    assert seen[0][0] == 0 and seen[-1][1] == len(trajs)
+    assert all(a[1] == b[0] for a, b in zip(seen, seen[1:]))
+    assert len(seen) <= chunks
