@@ -641,6 +641,8 @@ def main():
         extra["cfg4"] = run_cfg4(dev, args.seed, rank, 10, 3, comm)
         if rank == 0:
             extra["cfg1"] = run_cfg1(dev, args.seed, 50, 5, not args.no_cpu)
+            import bench_imagine  # cfg3: the imagination step
+            extra["cfg3"] = bench_imagine.run(4096, 16, 5, 16 if not args.no_cpu else 0)
         if comm is not None:
             dist.barrier()
     if rank != 0:

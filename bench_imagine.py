@@ -31,7 +31,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--cpu-sample", type=int, default=64)
     args = ap.parse_args()
+    print(json.dumps(run(args.n, args.h, args.steps, args.cpu_sample)))
+
+
+def run(n: int = 4096, h: int = 16, steps: int = 5, cpu_sample: int = 64) -> dict:
+    """The cfg3 line (bench.py carries it as its `cfg3` extra)."""
     import torch
+    args = argparse.Namespace(n=n, h=h, steps=steps, cpu_sample=cpu_sample)
 
     from paper_2603_18464_b200.imagine import Imaginer
     from paper_2603_18464_b200.types import (ModelBundle, ObsModel, ObsModelConfig,
@@ -79,8 +85,8 @@ def main():
                               b.obs_model.params.tensors, b.reward_model.params.tensors, A,
                               starts[e], int(steps[e]), u[e], args.h, 0.9, (8, 8))
         cpu_steps += out["t_len"]
-    cpu_rate = cpu_steps / (time.perf_counter() - t1)
-    print(json.dumps({
+    cpu_rate = cpu_steps / (time.perf_counter() - t1) if args.cpu_sample else None
+    return ({
         "metric": "imagined steps/s", "unit": "steps/s",
         "value": imagined / e2e_s,
         "config": {"workload": f"cfg3 imagination {args.n} x H{args.h}, obs 195, K 4, A 7, D 64",
@@ -88,9 +94,10 @@ def main():
         "e2e_ms_per_batch": e2e_s * 1e3,
         "device_ms_per_batch": ev0.elapsed_time(ev1) / args.steps,
         "device_steps_per_s": imagined / (ev0.elapsed_time(ev1) / args.steps / 1e3),
-        "cpu_baseline": {"value": cpu_rate, "unit": "steps/s", "cores": 1, "kind": "port",
-                         "sample": f"{args.cpu_sample} episodes x H{args.h}, float64 per-request loop"},
-    }))
+        "cpu_baseline": None if cpu_rate is None else {
+            "value": cpu_rate, "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": f"{args.cpu_sample} episodes x H{args.h}, float64 per-request loop"},
+    })
 
 
 if __name__ == "__main__":

@@ -62,9 +62,17 @@ class Imaginer:
         self.version = version
 
     def imagine(self, start_vecs, start_steps, h_img: int, uniforms=None, seed: int = 0) -> dict:
-        """One batch; returns host numpy arrays keyed like the kernel outputs."""
+        """One batch; returns host numpy arrays keyed like the kernel outputs.
+
+        The outputs come back as asynchronous copies into page-locked buffers
+        (from torch's caching host allocator, so a returned array owns its
+        buffer until it is dropped) with one synchronization for the batch."""
         out = self.imagine_device(start_vecs, start_steps, h_img, uniforms, seed)
-        return {k: v.cpu().numpy() for k, v in out.items()}
+        host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
+        for k, v in out.items():
+            host[k].copy_(v, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return {k: v.numpy() for k, v in host.items()}
 
     def imagine_device(self, start_vecs, start_steps, h_img: int, uniforms=None,
                        seed: int = 0) -> dict:
