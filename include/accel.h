@@ -43,6 +43,9 @@ const char* accel_last_error(void);
 unsigned long long accel_launch_count(void);
 /* Hash of the sources + flags this library was built from (build.py). */
 const char* accel_build_id(void);
+/* ABI version: 3 (row pitches on accel_tanh_grad_colsum, caller workspace on
+ * accel_small_gemm, perm-based accel_fact_group_sum2, piece keys on
+ * accel_grouped_rows_sum, accel_value_attn_backward). */
 int accel_version(void);
 
 /* One strided copy (cudaMemcpy2DAsync, any direction): `height` rows of
