@@ -406,6 +406,16 @@ int accel_small_gemm(const float* A, const float* B, float* C, int64_t M, int64_
  * smaller / NULL ws the product runs unsplit. */
 int64_t accel_small_gemm_ws_floats(int64_t M, int64_t N, int64_t K);
 
+/* ---- serving: per-ticket sampling uniforms (csrc/ticket_rng.cu) --------- */
+
+/* out f64[n, K]: request i's uniforms as np.random.default_rng(SeedSequence(
+ * [base_seed, tickets[i]])).random(K) (inference.py:146-159), one thread per
+ * ticket; tickets >= 0.  The _host variant computes the same on the CPU. */
+int accel_ticket_uniforms(uint64_t base_seed, const int64_t* tickets, int64_t n, int K,
+                          double* out, void* stream);
+int accel_ticket_uniforms_host(uint64_t base_seed, const int64_t* tickets, int64_t n, int K,
+                               double* out);
+
 /* ---- wide tensor-core GEMM (cfg4: O = D = 4096; csrc/tc_wide.cu) -------- */
 
 /* bf16 "pair" operand of an fp32 matrix X [rows, cols] (pitch ld elements):

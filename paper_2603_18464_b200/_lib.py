@@ -95,6 +95,8 @@ _SIGNATURES = {
     "accel_small_gemm": (c_int, [P, P, P, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
                                  c_int, c_int, P, c_int64, P]),
     "accel_small_gemm_ws_floats": (c_int64, [c_int64, c_int64, c_int64]),
+    "accel_ticket_uniforms": (c_int, [ctypes.c_uint64, P, c_int64, c_int, P, P]),
+    "accel_ticket_uniforms_host": (c_int, [ctypes.c_uint64, P, c_int64, c_int, P]),
     "accel_tc_wide_set_chunk": (None, [c_int]),
     "accel_tc_wide_set_multicast": (None, [c_int]),
     "accel_tf32_pairs": (c_int, [P, c_int64, c_int64, c_int64, P, c_int64, c_int, c_int, P]),

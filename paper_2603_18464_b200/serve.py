@@ -57,6 +57,21 @@ def ticket_uniforms(base_seed: int, tickets, K: int) -> np.ndarray:
                      for t in tickets]) if len(tickets) else np.zeros((0, K))
 
 
+def _device_ticket_uniforms(base_seed: int, tickets, K: int, dev) -> torch.Tensor:
+    """ticket_uniforms computed on the device (accel_ticket_uniforms: the same
+    SeedSequence + PCG64 arithmetic, one thread per ticket); integers outside
+    the kernel's 64-bit range take the host path."""
+    n = len(tickets)
+    if 0 <= int(base_seed) < 2 ** 64 and all(0 <= int(t) < 2 ** 63 for t in tickets):
+        tk = torch.tensor([int(t) for t in tickets], dtype=torch.int64).to(dev)
+        u = torch.empty(n, K, dtype=F64, device=dev)
+        _lib.call("accel_ticket_uniforms", ctypes.c_uint64(int(base_seed)),
+                  ctypes.c_void_p(tk.data_ptr()), n, int(K), ctypes.c_void_p(u.data_ptr()),
+                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        return u
+    return torch.from_numpy(ticket_uniforms(base_seed, tickets, K)).to(dev)
+
+
 class DeviceServer:
     """Evaluates request batches on the device; drop-in for `run_batch`."""
 
@@ -143,7 +158,7 @@ class DeviceServer:
             if np.any(st < 0) or np.any(st >= dims[4]):  # ValueHead._check_steps (models.py:261-267)
                 raise DimensionError(f"step index outside value-step table [0, {dims[4]})")
             steps = torch.from_numpy(st.astype(np.int32)).to(dev)
-            u = torch.from_numpy(ticket_uniforms(base_seed, [r.ticket for r in requests], K)).to(dev)
+            u = _device_ticket_uniforms(base_seed, [r.ticket for r in requests], K, dev)
             tok = torch.empty(n, K, dtype=I32, device=dev)
             lg = torch.empty(n, K, A, dtype=F64, device=dev)
             val = torch.empty(n, dtype=F64, device=dev)

@@ -114,3 +114,17 @@ def test_device_snapshot_serves_without_host_round_trip():
     np.testing.assert_array_equal(np.stack([r.logits for r in got]),
                                   np.stack([r.logits for r in want]))
     np.testing.assert_array_equal([r.value for r in got], [r.value for r in want])
+
+
+def test_device_ticket_uniforms_equal_the_host_draws():
+    """The serving kernel's per-ticket uniforms == numpy's SeedSequence draws."""
+    import torch
+
+    from paper_2603_18464_b200.serve import _device_ticket_uniforms, ticket_uniforms
+    tickets = [0, 5, 2 ** 32, 2 ** 40 + 3] + list(range(1000, 5096))
+    for base in (3, 2 ** 33 + 1):
+        got = _device_ticket_uniforms(base, tickets, 4, torch.device("cuda")).cpu().numpy()
+        np.testing.assert_array_equal(got, ticket_uniforms(base, tickets, 4))
+    # integers past the kernel's range take the host path, same values
+    big = _device_ticket_uniforms(2 ** 70, [1, 2], 3, torch.device("cuda")).cpu().numpy()
+    np.testing.assert_array_equal(big, ticket_uniforms(2 ** 70, [1, 2], 3))
