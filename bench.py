@@ -450,6 +450,46 @@ def e2e_api(tr, seed: int, n_traj: int = 256, reps: int = 3) -> dict:
             "host_input_bytes_f64": int(f64_bytes)}
 
 
+def loss_sweep(dev, seed: int, sfu_peak: float, sizes=(16, 64, 256, 1024, 4096)) -> dict:
+    """SURVEY 8(d) loss-kernel sweep: the dz-free loss kernel (K4) and the grouped
+    recompute over token counts from ~50 K to ~11 M (cfg2 LIBERO-Long mixes of
+    16 ... 4096 trajectories), in-step CUDA-event times (mean of 3 steps)."""
+    import torch
+
+    from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
+    d = dims()
+    rows = []
+    for nt in sizes:
+        lens, done = lengths_for(seed + nt, 0, nt, 520)
+        N = int(lens.sum())
+        M = N * d["K"]
+        tr = Trainer(make_bundle(seed, 522), TrainerConfig())
+        inputs = device_inputs(lens, done, seed + 31 * nt, dev)
+        bver = np.zeros(len(lens), dtype=np.int64)
+        for _ in range(2):
+            tr.train_step(tr.build_from_device(inputs, n_real=len(lens), behavior_version=bver))
+        tr.profile_events = []
+        for _ in range(3):
+            tr.train_step(tr.build_from_device(inputs, n_real=len(lens), behavior_version=bver))
+        torch.cuda.synchronize()
+        kern = {}
+        for name, a, b in tr.profile_events:
+            kern.setdefault(name, []).append(a.elapsed_time(b))
+        t_loss = float(np.mean(kern.get("token_loss", [float("nan")])))
+        t_grp = float(np.mean(kern.get("group_sum", [float("nan")])))
+        ex2 = 2 * M * d["A"]
+        rows.append({"trajectories": nt, "transitions": N, "tokens": M,
+                     "loss_ms": t_loss, "loss_tex2_s": ex2 / t_loss / 1e9,
+                     "loss_sfu_frac": ex2 / t_loss / 1e9 / sfu_peak,
+                     "recompute_ms": t_grp,
+                     "recompute_sfu_frac": (M * d["A"]) / t_grp / 1e9 / sfu_peak})
+        del tr, inputs
+        torch.cuda.empty_cache()
+    return {"kernels": "token_loss_fact2 (K4, dz-free) + fact_group_sum2 (grouped recompute)",
+            "bound": "sfu (2 ex2 per logit in K4, 1 in the recompute); latency-bound in practice",
+            "peak_tex2_s": sfu_peak, "rows": rows}
+
+
 def run_reference(args, rank: int, world: int):
     """--impl reference: the CPU restatement of the reference trainer (rank 0)."""
     if rank != 0:
@@ -680,6 +720,10 @@ def main():
     t_logp = float(np.mean(kern.get("token_logp", [float("nan")]))) / 1e3
 
     sweep = gae_sweep(dev, peak)
+    lsweep = None
+    if not args.no_extra:
+        sm_mhz = (clocks.summary or {}).get("sm_max_mhz") or 1965.0
+        lsweep = loss_sweep(dev, args.seed, 16 * 148 * sm_mhz * 1e6 / 1e12)
     cpu = cpu1 = None
     if not args.no_cpu:
         host_np = {k: v.numpy() for k, v in host.items()}
@@ -728,6 +772,7 @@ def main():
                          "note": "in-step size (32 MB, L2-resident, latency-bound); "
                                  "see gae_sweep for the cfg2 sizes"},
         "gae_sweep": sweep,
+        "loss_sweep": lsweep,
         "trainer_roofline": dict(tr_roof, achieved_ms=ms, frac=tr_roof["t_roof_ms"] / ms),
         "roofline_token_logp": {"bytes_per_launch": logp_bytes, "ms_per_launch": t_logp * 1e3,
                                 "achieved": logp_bytes / t_logp / 1e9,
