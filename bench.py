@@ -249,8 +249,9 @@ def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20,
     from paper_2603_18464_b200.workload import libero_long_lengths
 
     rows = []
-    for n in sizes:
-        lens, dn = libero_long_lengths(np.random.default_rng(n), n)
+    for n, pure in [(n, False) for n in sizes] + [(sizes[-1], True)]:
+        # (the last row: SURVEY 8(d)'s pure U[1, 520] length variant)
+        lens, dn = libero_long_lengths(np.random.default_rng(n), n, pure_uniform=pure)
         off = np.zeros(n + 1, dtype=np.int64)
         np.cumsum(lens, out=off[1:])
         N = int(off[-1])
@@ -278,7 +279,8 @@ def gae_sweep(dev, peak: float, sizes=(4096, 16384, 65536), reps: int = 20,
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         byt = 16 * N + 13 * n + (4 * N if frame_of else 0)  # SURVEY 8(d) (+ frame_of)
-        rows.append({"trajectories": n, "transitions": N, "bytes_per_launch": byt,
+        rows.append({"trajectories": n, "lengths": "U[1,520]" if pure else "LIBERO-Long mix",
+                     "transitions": N, "bytes_per_launch": byt,
                      "ms_per_launch": ms, "achieved": byt / ms / 1e6,
                      "frac": byt / ms / 1e6 / peak})
         del r, v, adv, ret, fo
