@@ -156,8 +156,8 @@ def make_bundle(seed: int, n_steps: int):
 
 
 def lengths_for(seed: int, rank: int, n: int, horizon: int):
-    if _WL["name"] in ("cfg1", "cfg4"):  # 64 trajectories x 128 steps per GPU, done alternating
-        return np.full(64, 128, dtype=np.int64), np.arange(64) % 2 == 0
+    if _WL["name"] in ("cfg1", "cfg4"):  # n (64) trajectories x 128 steps, done alternating
+        return np.full(n, 128, dtype=np.int64), np.arange(n) % 2 == 0
     from paper_2603_18464_b200.workload import libero_long_lengths
     return libero_long_lengths(np.random.default_rng(np.random.SeedSequence([seed, rank, 11])), n,
                                horizon)
@@ -388,16 +388,19 @@ def run_cfg1(dev, seed: int, steps: int, warmup: int, cpu: bool) -> dict:
         return out
 
 
-def run_cfg4(dev, seed: int, rank: int, steps: int, warmup: int, comm) -> dict:
+def run_cfg4(dev, seed: int, rank: int, steps: int, warmup: int, comm,
+             strong: bool = False) -> dict:
     """BASELINE configs[3] (cfg4: OpenVLA-7B-shaped heads, O = D = 4096, 64 x 128
-    transitions per GPU) -- ZeRO-2 data parallel under torchrun (weak scaling);
-    every GEMM on the wide tcgen05 kernel (csrc/tc_wide.cu)."""
+    transitions per GPU) -- ZeRO-2 data parallel under torchrun (weak scaling;
+    strong=True: the 64 x 128 global batch split over the ranks); every GEMM on
+    the wide tcgen05 kernel (csrc/tc_wide.cu)."""
     import torch
     import torch.distributed as dist
 
     from paper_2603_18464_b200.trainer import Trainer, TrainerConfig
+    world = comm.world if comm is not None else 1
     with workload("cfg4"):
-        lens, done = lengths_for(seed, rank, 64, 128)
+        lens, done = lengths_for(seed, rank, 64 // world if strong else 64, 128)
         n, N = len(lens), int(lens.sum())
         tr = Trainer(make_bundle(seed, 522), TrainerConfig(), comm=comm)
         inputs = device_inputs(lens, done, seed * 1000 + rank, dev)
@@ -415,11 +418,13 @@ def run_cfg4(dev, seed: int, rank: int, steps: int, warmup: int, comm) -> dict:
             ms, tot = float(mx.item()), float(t[1].item())
         else:
             tot = float(N)
-        world = comm.world if comm is not None else 1
         del tr, inputs
         torch.cuda.empty_cache()
-        return {"workload": WORKLOAD_CFG4, "value": tot / (ms / 1e3), "unit": UNIT,
-                "ms_per_step": ms, "n_gpus": world, "scaling": "weak",
+        return {"workload": WORKLOAD_CFG4 if not strong else
+                WORKLOAD_CFG4.replace("64 trajectories x 128 steps per GPU",
+                                      "64 x 128 global batch split over the GPUs"),
+                "value": tot / (ms / 1e3), "unit": UNIT,
+                "ms_per_step": ms, "n_gpus": world, "scaling": "strong" if strong else "weak",
                 "parallelism": f"dp{world} (ZeRO-2)" if world > 1 else "single",
                 "gemms": "accel_tc_gemm_wide (tf32 + bf16-pair tcgen05), no cuBLAS on the step"}
 
@@ -562,7 +567,8 @@ def main():
         comm = DataParallel()
     d = dims()
     n_steps = 522 if args.workload == "cfg4" else args.horizon + 2
-    lens, done = lengths_for(args.seed, rank, args.n_traj, args.horizon)
+    lens, done = lengths_for(args.seed, rank, 64 if args.workload == "cfg4" else args.n_traj,
+                             args.horizon)
     N = int(lens.sum())
     n = len(lens)
     M = N * d["K"]
@@ -681,6 +687,8 @@ def main():
     if not args.no_extra and args.workload == "cfg2":
         extra["e2e_api"] = e2e_api(tr, args.seed + rank)
         extra["cfg4"] = run_cfg4(dev, args.seed, rank, 10, 3, comm)
+        if world > 1:  # cfg4 also at a fixed global batch
+            extra["cfg4_strong"] = run_cfg4(dev, args.seed, rank, 10, 3, comm, strong=True)
         if rank == 0:
             extra["cfg1"] = run_cfg1(dev, args.seed, 50, 5, not args.no_cpu)
             import bench_imagine  # cfg3: the imagination step

@@ -37,7 +37,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     bench._WL["name"] = os.environ.get("WORKLOAD", "cfg4")
     comm = DataParallel()
-    lens, done = bench.lengths_for(0, rank, 4096, 520)
+    lens, done = bench.lengths_for(0, rank, 64 if bench._WL["name"] == "cfg4" else 4096, 520)
     n = len(lens)
     tr = Trainer(bench.make_bundle(0, 522), TrainerConfig(), comm=comm)
     inputs = bench.device_inputs(lens, done, rank, dev)
