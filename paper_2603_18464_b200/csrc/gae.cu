@@ -11,9 +11,9 @@
 //     step of a trajectory, is a linear recurrence; its scan operator is the
 //     affine map (b, c): A_left = b + c * A_right.
 //   * A warp owns a contiguous range of whole trajectories: the ones whose
-//     first transition falls in its 1/W share of [0, N) (found by a 16-ary
-//     half-warp search on the offsets; balanced by transition count and fixed
-//     for a given grid, so the pooled sums are bitwise deterministic).
+//     start cost (transitions + kTrajCost per trajectory) falls in its 1/W share
+//     (found by a 16-ary half-warp search on the offsets; fixed for a given
+//     grid, so the pooled sums are bitwise deterministic).
 //   * A trajectory is one chunk when it has <= 544 steps (longer ones: 544-step
 //     chunks from the right, carry between them).  The chunk's r and v land in
 //     shared memory by 4-byte cp.async copies (coalesced rows), double-buffered
@@ -63,9 +63,18 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
                : "memory");
 }
 
-// First s in [0, n] with off[s] >= target (off[n] >= target), searched by the
+// First s in [0, n] with off[s] + kTrajCost*s >= target, searched by the
 // 16 lanes of a half-warp: 16-ary narrowing, one dependent load per round.  The
 // two half-warps search different targets; the loop runs until both are done.
+// Warp ranges balance transitions + kTrajCost per trajectory: a chunk's fixed
+// cost (offsets, staging setup, the shuffle scan, the partial rows) is worth
+// about that many steps of the serial scan, so ranges of short trajectories
+// would otherwise finish last.
+#ifndef ACCEL_GAE_TRAJ_COST
+#define ACCEL_GAE_TRAJ_COST 256
+#endif
+constexpr int64_t kTrajCost = ACCEL_GAE_TRAJ_COST;
+
 __device__ __forceinline__ int64_t half_warp_lower_bound(const int64_t* __restrict__ off,
                                                          int64_t n, int64_t target, int hl,
                                                          unsigned hmask, int hshift) {
@@ -77,7 +86,7 @@ __device__ __forceinline__ int64_t half_warp_lower_bound(const int64_t* __restri
     if (!fin) {
       step = (hi - lo + 16) / 16;  // ceil((hi - lo + 1) / 16)
       q = min(lo + (int64_t)(hl + 1) * step - 1, hi);
-      ge = __ldg(off + q) >= target;
+      ge = __ldg(off + q) + kTrajCost * q >= target;
     }
     const unsigned m = (__ballot_sync(0xffffffffu, ge) & hmask) >> hshift;
     const int f = __ffs(m) - 1;  // lane 15 probes hi: always set
@@ -111,11 +120,12 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int64_t w = (int64_t)blockIdx.x * kWarps + warp;
   // this warp's trajectories [sa, sb): the ones starting in its 1/W share of
-  // the transitions (balanced by transition count, fixed for a given grid)
+  // the cost (transitions + kTrajCost per trajectory, fixed for a given grid)
   int64_t sa, sb;
   {
     const int half = lane >> 4, hl = lane & 15;
-    const int64_t target = (int64_t)(((__int128)(w + half) * n_transitions + W - 1) / W);
+    const int64_t target =
+        (int64_t)(((__int128)(w + half) * (n_transitions + kTrajCost * n_traj) + W - 1) / W);
     const int64_t x = half_warp_lower_bound(off, n_traj, target, hl,
                                             half ? 0xffff0000u : 0x0000ffffu, half ? 16 : 0);
     sa = __shfl_sync(0xffffffffu, x, 0);
@@ -169,14 +179,17 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     const float* vc = vals + c.t0 + c.s + c.cb;
     float* sr = s_buf[warp][b][0] + lane;
     float* sv = s_buf[warp][b][1] + lane;
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      if (32 * j < nv) {  // warp-uniform row guard, lane predicate inside
-        if (32 * j + lane < nv) {
-          cp_async4(sr + 32 * j, rc + 32 * j);
-          cp_async4(sv + 32 * j, vc + lane + 32 * j);
-        }
-      }
+    const float* vl = vc + lane;
+    // full rows without a lane predicate, then the partial row
+    const int nfull = nv >> 5;
+#pragma unroll 4
+    for (int j = 0; j < nfull; ++j) {
+      cp_async4(sr + 32 * j, rc + 32 * j);
+      cp_async4(sv + 32 * j, vl + 32 * j);
+    }
+    if (32 * nfull + lane < nv) {
+      cp_async4(sr + 32 * nfull, rc + 32 * nfull);
+      cp_async4(sv + 32 * nfull, vl + 32 * nfull);
     }
     // the value after the chunk; a successful trajectory's bootstrap value is 0
     // (trainer.py:92-93), written here so the scan needs no last-step test
@@ -263,16 +276,24 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     const float* sv0 = s_buf[warp][b][1] + lane;
     float* ac = adv_out + cur.t0 + cur.cb + lane;
     float* rtc = ret_out + cur.t0 + cur.cb + lane;
-    int32_t* fc = frame_out != nullptr ? frame_out + cur.t0 + cur.cb + lane : nullptr;
-    const int32_t fb = (int32_t)(cur.t0 + cur.s + cur.cb) + lane;
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      if (32 * j >= nv) break;  // warp-uniform
-      if (32 * j + lane < nv) {
-        __stcs(ac + 32 * j, sr0[32 * j]);
-        __stcs(rtc + 32 * j, sv0[32 * j]);
-        if (fc != nullptr) __stcs(fc + 32 * j, fb + 32 * j);
-      }
+    // full rows without a lane predicate, then the partial row
+    const int nfull = nv >> 5;
+#pragma unroll 4
+    for (int j = 0; j < nfull; ++j) {
+      __stcs(ac + 32 * j, sr0[32 * j]);
+      __stcs(rtc + 32 * j, sv0[32 * j]);
+    }
+    const bool part = 32 * nfull + lane < nv;
+    if (part) {
+      __stcs(ac + 32 * nfull, sr0[32 * nfull]);
+      __stcs(rtc + 32 * nfull, sv0[32 * nfull]);
+    }
+    if (frame_out != nullptr) {
+      int32_t* fc = frame_out + cur.t0 + cur.cb + lane;
+      const int32_t fb = (int32_t)(cur.t0 + cur.s + cur.cb) + lane;
+#pragma unroll 4
+      for (int j = 0; j < nfull; ++j) __stcs(fc + 32 * j, fb + 32 * j);
+      if (part) __stcs(fc + 32 * nfull, fb + 32 * nfull);
     }
     __syncwarp();  // the buffer is restaged two chunks on
     if (nxt.s != cur.s) carry = 0.f;  // next chunk starts a new trajectory at its end
