@@ -363,6 +363,7 @@ class Trainer:
         self.service = service
         self.metrics = metrics
         self.comm = comm
+        self._dec_idx = None  # data parallel: the build's summed flag entries (device)
         self.device = _device()
         self.rng = np.random.default_rng(np.random.SeedSequence([seed, 7]))
         self._bundle = bundle
@@ -686,9 +687,11 @@ class Trainer:
             adv_raw, ret, _ = ops.gae_segmented(b["rewards"], values, b["traj_off"], b["done"],
                                                 cfg.gae.gamma, cfg.gae.lam, frame_of=frame_of,
                                                 sums=flags[0:4])
-        sums = self._allreduce_sum(flags[0:3].clone()) if self.comm is not None else flags[0:3]
-        ops.normalize_finalize(sums, cfg.eps_norm, flags[4:8])
-        adv = ops.normalize_apply(adv_raw, flags[4:8])
+        if self.comm is None:
+            ops.normalize_finalize(flags[0:3], cfg.eps_norm, flags[4:8])
+            adv = ops.normalize_apply(adv_raw, flags[4:8])
+        # (data parallel: the pooled (sum, sum of squares, count) ride on the one
+        # decision all-reduce at the end of the build; normalization follows it)
         with self._timed("token_logp"):
             lp_old, lbad = ops.token_logp(b["mu"], b["tokens"])
         ops.reduce_f64(lbad, ops.token_grid(M), 2, 0, flags[8:10])
@@ -696,7 +699,8 @@ class Trainer:
             ops.count_nonfinite_rows(b["frames"], frame_of, N, cnt[0:1])
         batch = DeviceTrainBatch(
             frames=b["frames"], steps=b["steps"], tokens=b["tokens"], frame_of=frame_of,
-            lp_old=lp_old, adv=adv, ret=ret, n_actions=d.n_actions, chunk_len=d.chunk_len,
+            lp_old=lp_old, adv=adv if self.comm is None else None, ret=ret,
+            n_actions=d.n_actions, chunk_len=d.chunk_len,
             critic_version=self.publish_version, n_real=n_real, n_imagined=n - n_real,
             norm_mean=0.0, norm_std=0.0, norm_count=N,
             shard_sizes=_array_split_sizes(N, cfg.k_shards),
@@ -711,17 +715,24 @@ class Trainer:
         host_dev = torch.cat([flags, cnt.double()])
         if self.comm is not None:
             lags = self.publish_version - np.asarray(behavior_version, dtype=np.int64)
-            counts = torch.tensor([float(n_real), float(n), float(lags.sum())], dtype=F64,
-                                  device=dev)
+            # (page-locked source, asynchronous: a pageable torch.tensor(..., device=)
+            # here would block the host until the stream drained)
+            counts = torch.tensor([float(n_real), float(n), float(lags.sum())],
+                                  dtype=F64).pin_memory().to(dev, non_blocking=True)
             host_dev = torch.cat([host_dev, counts])
-            # data parallel: the batch is one shard of the global batch; every
-            # accept/reject decision, the transition count and the record's
-            # trajectory counts / behavior lag are global (all ranks agree)
-            idx = torch.tensor([3, 8, 9, 10, 11, 16, 17, 20, 21, 22], device=dev)
+            # data parallel: the batch is one shard of the global batch; the pooled
+            # advantage statistics, every accept/reject decision, the transition
+            # count and the record's trajectory counts / behavior lag are global
+            # (all ranks agree) -- one all-reduce of the entries that sum
+            idx = self._dec_idx
+            if idx is None or idx.device != host_dev.device:
+                idx = self._dec_idx = torch.tensor([0, 1, 2, 3, 8, 9, 10, 11, 16, 17, 20, 21, 22],
+                                                   device=dev)
             dec = host_dev.index_select(0, idx)
             self.comm.all_reduce_sum(dec)
             host_dev.index_copy_(0, idx, dec)
-            host_dev[2:3].copy_(sums[2:3])
+            ops.normalize_finalize(host_dev[0:3], cfg.eps_norm, host_dev[4:8])
+            batch.adv = ops.normalize_apply(adv_raw, host_dev[4:8])
         return batch, host_dev
 
     def _build_finish(self, batch, host) -> DeviceTrainBatch | None:
@@ -803,9 +814,6 @@ class Trainer:
     def _bucket_done(self, tensor_name: str) -> None:
         if self.comm is not None:
             self.comm.bucket_ready(self.layout.bucket_of(tensor_name))
-
-    def _allreduce_sum(self, t):
-        return self.comm.all_reduce_sum(t) if self.comm is not None else t
 
     def train_step(self, batch) -> dict | None:
         """One policy + value update from a TrainBatch; publishes.
