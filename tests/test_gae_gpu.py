@@ -60,7 +60,7 @@ def test_gae_matches_oracle_small_ragged():
 
 
 @pytest.mark.parametrize("case", ["one_long", "all_ones", "libero_mix", "tile_edges",
-                                  "pass_edges", "with_empty"])
+                                  "pass_edges", "with_empty", "skewed", "fewer_than_warps"])
 def test_gae_matches_c_oracle_edge_cases(case):
     rng = np.random.default_rng(7)
     if case == "one_long":          # one trajectory spanning many tiles (look-back chain)
@@ -77,6 +77,11 @@ def test_gae_matches_c_oracle_edge_cases(case):
         lens[:7] = 0
         lens[-5:] = 0
         done = rng.random(3000) < 0.5
+    elif case == "skewed":          # the warp ranges balance steps + a per-trajectory cost:
+        lens = [20_000] + [1] * 20_000 + [0] * 300 + [15_000] + [2] * 7000  # long and tiny mixed
+        done = rng.random(len(lens)) < 0.5
+    elif case == "fewer_than_warps":  # most warps own no trajectory
+        lens, done = [5, 700, 3], [True, False, False]
     else:
         from paper_2603_18464_b200.workload import libero_long_lengths
         lens, done = libero_long_lengths(rng, 512)
