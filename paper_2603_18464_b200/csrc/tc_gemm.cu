@@ -58,6 +58,9 @@ constexpr int kRowsEpiMax = 8;
 constexpr int kRowsThreads = (kEpiWarp0 + kRowsEpiMax) * 32;  // 14 warps
 constexpr int kMaxRaw = 12;                // raw (TMA) ring slots
 constexpr int kNL = 2;                     // lo ring slots
+#ifndef ACCEL_ROWS_HDIRECT_WBYTES
+#define ACCEL_ROWS_HDIRECT_WBYTES (96 * 1024)  // dtanh: H from global memory from this weight size
+#endif
 constexpr size_t kSmemBudget = 225 * 1024;  // dynamic shared memory (wgrad)
 constexpr size_t kRowsBudget = 224 * 1024;  // tc_rows also holds ~2 KB of static smem (<= 227 KB)
 constexpr uint32_t kTile = BM * BK * 4;    // one 128 x 32 fp32 tile (16 KB)
@@ -192,6 +195,12 @@ struct RowArgs {
   unsigned* nonfinite;  // optional: += number of non-finite elements of X
   uint32_t tmem_cols, acc_cols;
   int nepi;           // epilogue warps: 4 (warps 6-9) or 8 (6-13)
+  // dtanh with H read straight from global memory by the epilogue lanes (no H
+  // boxes in shared memory: a large resident weight keeps its ring), column sums
+  // in lane registers (<= 2 chunks per warp); hdirect needs N % 32 == 0
+  int hdirect;
+  const float* Hp;
+  int64_t ldh;
 };
 
 __global__ void __launch_bounds__(kRowsThreads, 1)
@@ -330,12 +339,14 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     unsigned char* stg0 = staging + (size_t)ew * p.nstg * 4096;
     int sb = 0;
     unsigned hph = 0;  // per-box H barrier phases
-    if (p.dtanh)
+    if (p.dtanh && !p.hdirect)
       for (int c = lane; c < 256; c += 32) s_csum[ew][c] = 0.f;  // dtanh column sums
     // dtanh with all of a tile's chunks fitting the boxes: H boxes of the next
     // tile are loaded as soon as this tile's stores have read the boxes, so the
     // load latency hides behind the MMAs instead of stalling every chunk
-    const bool hpre = p.dtanh && nch == p.nstg;
+    const bool hdir = p.dtanh && p.hdirect;
+    const bool hpre = p.dtanh && !hdir && nch == p.nstg;
+    float cs_acc[2] = {0.f, 0.f};  // hdirect: this lane's column sums of chunks 0 and 1
     auto load_h = [&](int64_t tt) {
       const int64_t r0h = (blockIdx.x + tt * gridDim.x) * BM + q * 32;
       for (int c = 0; c < nch; ++c) {
@@ -357,9 +368,21 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         if (p.tma_store) {
           if (lane == 0 && !hpre) tma_store_wait_read();  // this box's previous store has read it
           __syncwarp();
-          if (p.dtanh && !hpre && lane == 0) {
+          if (p.dtanh && !hdir && !hpre && lane == 0) {
             mbar_expect_tx(&bars.hbar[ew][sb], 4096);
             tma_load_2d(stg, &hmap, c0, (int)row0, &bars.hbar[ew][sb]);
+          }
+        }
+        float4 hv[8];  // hdirect: this lane's row of H, columns c0 .. c0 + 31 (loads in flight
+                       // while the accumulator is read)
+        if (hdir) {
+          if (row < p.M) {
+            const float4* hp = reinterpret_cast<const float4*>(p.Hp + row * p.ldh + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hv[j] = __ldg(hp + j);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
         uint32_t r[32];
@@ -390,11 +413,15 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         }
         if (p.tma_store) {
           if (p.dtanh) {
-            mbar_wait(&bars.hbar[ew][sb], (hph >> sb) & 1u);
-            hph ^= 1u << sb;
+            if (!hdir) {
+              mbar_wait(&bars.hbar[ew][sb], (hph >> sb) & 1u);
+              hph ^= 1u << sb;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float4 h = *reinterpret_cast<const float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16));
+              const float4 h =
+                  hdir ? hv[j]
+                       : *reinterpret_cast<const float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16));
               v[4 * j] *= 1.f - h.x * h.x;
               v[4 * j + 1] *= 1.f - h.y * h.y;
               v[4 * j + 2] *= 1.f - h.z * h.z;
@@ -416,7 +443,11 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             float cs = 0.f;
             for (int rr = 0; rr < 32; ++rr)
               cs += *reinterpret_cast<const float*>(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7)) * 16) + (lane & 3) * 4));
-            s_csum[ew][c0 + lane] += cs;  // lane-owned slot
+            if (hdir) {
+              if (c0 == cfirst) cs_acc[0] += cs; else cs_acc[1] += cs;
+            } else {
+              s_csum[ew][c0 + lane] += cs;  // lane-owned slot
+            }
           }
           if (++sb == p.nstg) sb = 0;
         } else if (row < p.M) {
@@ -435,6 +466,12 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
       }
     }
     if (p.tma_store && lane == 0) tma_store_wait_all();
+    if (hdir) {  // the warp's column sums into its (drained) staging box
+      __syncwarp();
+      float* sc = reinterpret_cast<float*>(stg0);
+      if (nch > 0) sc[cfirst + lane] = cs_acc[0];
+      if (nch > 1) sc[cfirst + cstep + lane] = cs_acc[1];
+    }
   }
   __syncwarp();
   tc_fence_before();
@@ -442,7 +479,9 @@ tc_rows_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
   if (p.dtanh) {  // the CTA's column sums, epilogue warps in fixed order
     for (int c = threadIdx.x; c < p.N; c += kRowsThreads) {
       float a = 0.f;
-      for (int w = 0; w < nepi; ++w) a += s_csum[w][c];
+      for (int w = 0; w < nepi; ++w)
+        a += p.hdirect ? reinterpret_cast<const float*>(staging + (size_t)w * p.nstg * 4096)[c]
+                       : s_csum[w][c];
       p.col_part[(int64_t)blockIdx.x * p.N + c] = a;
     }
   }
@@ -702,14 +741,21 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   } else {
     ymap = xmap;  // unused
   }
-  CUtensorMap hmap = xmap;  // unused unless dtanh
+  CUtensorMap hmap = xmap;  // unused unless dtanh (H boxes)
   p.dtanh = H ? 1 : 0;
   p.col_part = col_part;
   p.nonfinite = nonfinite;
+  // a large resident weight: H straight from global memory, no H boxes (the ring
+  // keeps the stages the plain product has)
+  p.hdirect = (H && wbytes >= (size_t)ACCEL_ROWS_HDIRECT_WBYTES && Npad <= 64 && N % 32 == 0 &&
+               ldh % 4 == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0) ? 1 : 0;
+  p.Hp = H;
+  p.ldh = ldh;
   if (H) {
     if (!p.tma_store || !col_part || act_tanh || bias || N > 256)
       return fail(kDimension, "tc_gemm dtanh: needs an aligned output, col_part, no bias/act");
-    if (int e = make_map(&hmap, H, M, N, ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return e;
+    if (!p.hdirect)
+      if (int e = make_map(&hmap, H, M, N, ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return e;
   }
   p.ntiles = ceil_div(M, BM);
   p.acc_cols = p.concat ? 2 * Npad : Npad;
@@ -717,18 +763,20 @@ int launch_rows(const float* X, const float* W, float* Y, const float* bias, int
   // epilogue warps: 8 when the ring still keeps >= 6 slots beside their two
   // staging boxes each (narrow K: the epilogue is the longer pole), else 4;
   // staging: two boxes per epilogue warp when the raw ring keeps >= 6 slots
+  const bool hbox = H && !p.hdirect;  // H boxes + shared-memory column sums
   auto ring_left = [&](int nepi, int nstg) -> int64_t {
-    const size_t sb = (size_t)nepi * nstg * 4096 + (H ? (size_t)nepi * 256 * 4 : 0);
+    const size_t sb = (size_t)nepi * nstg * 4096 + (hbox ? (size_t)nepi * 256 * 4 : 0);
     const size_t used = wbytes + (size_t)kNL * kTile + sb;
     return used > kRowsBudget ? -1 : (int64_t)((kRowsBudget - used) / kTile);
   };
   // (with 8 warps a warp drains ceil(Npad / 64) chunks per tile: one box each, up to two)
   const int nstg8 = std::min(2, (Npad + 63) / 64);
-  p.nepi = (p.tma_store && Npad >= 64 && ring_left(kRowsEpiMax, nstg8) >= 4) ? kRowsEpiMax
-                                                                              : kEpiWarps;
+  p.nepi = (p.tma_store && !p.hdirect && Npad >= 64 && ring_left(kRowsEpiMax, nstg8) >= 4)
+               ? kRowsEpiMax
+               : kEpiWarps;
   p.nstg = p.tma_store ? (p.nepi == kRowsEpiMax ? nstg8 : 2) : 0;
   if (p.tma_store && p.nstg == 2 && ring_left(p.nepi, 2) < 6) p.nstg = 1;
-  const size_t sbytes = (size_t)p.nepi * p.nstg * 4096 + (H ? (size_t)p.nepi * 256 * 4 : 0);
+  const size_t sbytes = (size_t)p.nepi * p.nstg * 4096 + (hbox ? (size_t)p.nepi * 256 * 4 : 0);
   p.nraw = (int)std::min<size_t>(kMaxRaw, (kRowsBudget - wbytes - sbytes - kNL * kTile) / kTile);
   const size_t smem = wbytes + (size_t)(p.nraw + kNL) * kTile + sbytes;
   cudaError_t e = cudaFuncSetAttribute(tc_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -667,15 +667,17 @@ def tc_matmul_nn_dtanh(x, w, h, out, part_fn):
     x = pitched(x)
     M, K = x.shape
     N = w.shape[1]
-    # fused for short K (the resident [W_hi; W_lo] leaves room for two staging boxes
-    # per epilogue warp); at K = 256 the unfused pair is faster
+    # fused for short K (the resident [W_hi; W_lo] leaves room for two H staging
+    # boxes per epilogue warp) and, with H read by the epilogue lanes straight from
+    # global memory, for narrow N (<= 64, whole 32-column chunks) up to K = 256
     if not tc_rows_supported(K, N):  # wide: the tanh derivative rides in the epilogue
         n = -(-M // 128)
         part = part_fn(n)
         wide_gemm(x, w, out, a_mn=False, b_mn=True, epi=2, h=pitched(h), col_part=part,
                   tag="dtanh")
         return out, part, n
-    if N <= 256 and K <= 128 and _aligned_rows(out) and _aligned_rows(h):
+    if (N <= 256 and (K <= 128 or (N <= 64 and N % 32 == 0)) and _aligned_rows(out)
+            and _aligned_rows(h)):
         n = tc_rows_grid(M)
         part = part_fn(n)
         _lib.call("accel_tc_gemm_dtanh", _pp(x), _pp(w), _pp(out), _pp(h), _pp(part), M, K, N,

@@ -57,7 +57,8 @@ def test_tc_wgrad_matches_fp64(F, n, k, slices):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("M,K,N", [(5000, 256, 64), (3001, 64, 64), (700, 64, 32)])
+@pytest.mark.parametrize("M,K,N", [(5000, 256, 64), (3001, 64, 64), (700, 64, 32), (1, 256, 64),
+                                   (777, 200, 64), (130, 256, 32)])
 def test_tc_dtanh_fused_epilogue(M, K, N):
     """(x.w) * (1 - h^2) and its column sums in the GEMM epilogue (dpre = dh (1 - h^2))."""
     from paper_2603_18464_b200 import ops
