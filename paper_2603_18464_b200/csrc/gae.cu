@@ -254,7 +254,7 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     if (lane == 31) { eb = 0.f; ec = 1.f; }
     float A = fmaf(ec, carry, eb);
     __syncwarp();  // every lane has read its neighbour's v before slots turn into outputs
-    float Sf = 0.f, Qf = 0.f;
+    float Sf = 0.f, Qf = 0.f, Rf = 0.f;
 #pragma unroll
     for (int k = kItems - 1; k >= 0; --k) {
       if (k < kd && k < nl) {
@@ -264,8 +264,15 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
         sv[k] = rt;
         Sf += A;
         Qf = fmaf(A, A, Qf);
-        nbad += (fabsf(A) <= FLT_MAX && fabsf(rt) <= FLT_MAX) ? 0 : 1;
+        Rf += rt;
       }
+    }
+    // non-finite outputs: a finite sum has only finite terms, so the per-step
+    // test runs only when a lane's sums are not finite (an inf / NaN output, or
+    // an overflowing sum of finite ones: the recount then finds none)
+    if (!(fabsf(Sf) <= FLT_MAX && fabsf(Rf) <= FLT_MAX)) {
+      for (int k = 0; k < min(kd, nl); ++k)
+        nbad += (fabsf(sr[k]) <= FLT_MAX && fabsf(sv[k]) <= FLT_MAX) ? 0 : 1;
     }
     S += (double)Sf;
     Q += (double)Qf;

@@ -150,3 +150,41 @@ def test_gae_validation_errors():
     with pytest.raises(DimensionError):
         ops.gae_segmented(z(2, torch.float32), z(4, torch.float32), off, z(1, torch.uint8),
                           0.9, 0.95)
+
+
+@pytest.mark.parametrize("case", ["nan_reward", "inf_value", "huge_finite"])
+def test_gae_nonfinite_count(case):
+    """sums[3] = number of steps whose advantage or return is not finite (the
+    build's check_finite input); finite outputs whose per-lane sums overflow
+    count as finite."""
+    import torch
+
+    from paper_2603_18464_b200 import ops
+
+    rng = np.random.default_rng(5)
+    lens = np.array([300, 17, 544, 545, 1, 90] * 40, dtype=np.int64)
+    off = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    n, nt = int(off[-1]), len(lens)
+    r = rng.normal(size=n).astype(np.float32)
+    v = rng.normal(size=n + nt).astype(np.float32)
+    lam = 0.95
+    if case == "nan_reward":
+        r[[5, 400, 1000, n - 1]] = np.nan
+    elif case == "inf_value":
+        v[[3, 777, 2000]] = np.inf
+    else:  # |A| ~ 1e38 on many consecutive steps: finite, but their sums overflow
+        r[:] = 1e38
+        v[:] = 0.0
+        lam = 0.0
+    d = (rng.random(nt) < 0.5).astype(np.uint8)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    adv, ret, sums = ops.gae_segmented(dev(r), dev(v), dev(off), dev(d), 0.99, lam)
+    torch.cuda.synchronize()
+    adv, ret, sums = adv.cpu().numpy(), ret.cpu().numpy(), sums.cpu().numpy()
+    want = int(np.sum(~np.isfinite(adv) | ~np.isfinite(ret)))
+    assert int(sums[3]) == want
+    if case == "huge_finite":
+        assert want == 0 and np.all(np.isfinite(adv))
+    else:
+        assert want > 0
