@@ -223,21 +223,35 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     float dl[kItems];
     float vnext = sv[min(kd, max(nl, 0))];  // v after the lane's last valid step
     float B = 0.f, C = 1.f;  // the lane's composed map (right to left)
+    // steps in groups of 4 (a warp-uniform test per group, the group's shared-memory
+    // loads issued together); steps past the lane's last valid one are identities
 #pragma unroll
-    for (int k = kItems - 1; k >= 0; --k) {
-      if (k < kd) {
-        const float vi = sv[k];
-        const float ri = sr[k];
-        const bool ok = k < nl;
-        // delta = r + gamma v' - v with gamma = g_hi + g_lo: fma(g_hi, v', -v) is
-        // exact before its one rounding, so the error is relative to the TD
-        // error, not to |v|
-        const float d = fmaf(g_lo, vnext, fmaf(g_hi, vnext, -vi)) + ri;
-        dl[k] = ok ? d : 0.f;
-        const float ck = ok ? decay : 1.f;
-        vnext = vi;
-        B = fmaf(ck, B, dl[k]);
-        C *= ck;
+    for (int g = (kItems - 1) / 4; g >= 0; --g) {
+      const int k0 = 4 * g;
+      if (k0 < kd) {
+        float vv[4], rr[4];
+#pragma unroll
+        for (int u = 3; u >= 0; --u)
+          if (k0 + u < kItems) {
+            vv[u] = sv[k0 + u];
+            rr[u] = sr[k0 + u];
+          }
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          const int k = k0 + u;
+          if (k < kItems) {
+            const bool ok = k < nl && k < kd;
+            // delta = r + gamma v' - v with gamma = g_hi + g_lo: fma(g_hi, v', -v) is
+            // exact before its one rounding, so the error is relative to the TD
+            // error, not to |v|
+            const float d = fmaf(g_lo, vnext, fmaf(g_hi, vnext, -vv[u])) + rr[u];
+            dl[k] = ok ? d : 0.f;
+            const float ck = ok ? decay : 1.f;
+            vnext = ok ? vv[u] : vnext;
+            B = fmaf(ck, B, dl[k]);
+            C *= ck;
+          }
+        }
       }
     }
     // exclusive suffix scan of the lane maps: the map of lanes (lane, 31]
@@ -256,15 +270,26 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     __syncwarp();  // every lane has read its neighbour's v before slots turn into outputs
     float Sf = 0.f, Qf = 0.f, Rf = 0.f;
 #pragma unroll
-    for (int k = kItems - 1; k >= 0; --k) {
-      if (k < kd && k < nl) {
-        A = fmaf(decay, A, dl[k]);
-        const float rt = A + sv[k];
-        sr[k] = A;
-        sv[k] = rt;
-        Sf += A;
-        Qf = fmaf(A, A, Qf);
-        Rf += rt;
+    for (int g = (kItems - 1) / 4; g >= 0; --g) {
+      const int k0 = 4 * g;
+      if (k0 < kd) {
+        float vv[4];
+#pragma unroll
+        for (int u = 3; u >= 0; --u)
+          if (k0 + u < kItems) vv[u] = sv[k0 + u];
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          const int k = k0 + u;
+          if (k < kItems && k < kd && k < nl) {
+            A = fmaf(decay, A, dl[k]);
+            const float rt = A + vv[u];
+            sr[k] = A;
+            sv[k] = rt;
+            Sf += A;
+            Qf = fmaf(A, A, Qf);
+            Rf += rt;
+          }
+        }
       }
     }
     // non-finite outputs: a finite sum has only finite terms, so the per-step
