@@ -39,6 +39,10 @@ constexpr int kItems = 17;                 // max consecutive steps per lane
 constexpr int kChunkSteps = 32 * kItems;   // max steps per warp chunk (one chunk per
                                            // trajectory up to 544 steps)
 constexpr int kPitch = kChunkSteps + 4;
+#ifndef ACCEL_GAE_GRP
+#define ACCEL_GAE_GRP 4
+#endif
+constexpr int kGrp = ACCEL_GAE_GRP;  // steps per group in the fold / resolve
 constexpr int kMaxGrid = 148 * 8;          // persistent grid bound (partials capacity)
 
 struct Workspace {
@@ -226,18 +230,18 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     // steps in groups of 4 (a warp-uniform test per group, the group's shared-memory
     // loads issued together); steps past the lane's last valid one are identities
 #pragma unroll
-    for (int g = (kItems - 1) / 4; g >= 0; --g) {
-      const int k0 = 4 * g;
+    for (int g = (kItems - 1) / kGrp; g >= 0; --g) {
+      const int k0 = kGrp * g;
       if (k0 < kd) {
-        float vv[4], rr[4];
+        float vv[kGrp], rr[kGrp];
 #pragma unroll
-        for (int u = 3; u >= 0; --u)
+        for (int u = kGrp - 1; u >= 0; --u)
           if (k0 + u < kItems) {
             vv[u] = sv[k0 + u];
             rr[u] = sr[k0 + u];
           }
 #pragma unroll
-        for (int u = 3; u >= 0; --u) {
+        for (int u = kGrp - 1; u >= 0; --u) {
           const int k = k0 + u;
           if (k < kItems) {
             const bool ok = k < nl && k < kd;
@@ -270,15 +274,15 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     __syncwarp();  // every lane has read its neighbour's v before slots turn into outputs
     float Sf = 0.f, Qf = 0.f, Rf = 0.f;
 #pragma unroll
-    for (int g = (kItems - 1) / 4; g >= 0; --g) {
-      const int k0 = 4 * g;
+    for (int g = (kItems - 1) / kGrp; g >= 0; --g) {
+      const int k0 = kGrp * g;
       if (k0 < kd) {
-        float vv[4];
+        float vv[kGrp];
 #pragma unroll
-        for (int u = 3; u >= 0; --u)
+        for (int u = kGrp - 1; u >= 0; --u)
           if (k0 + u < kItems) vv[u] = sv[k0 + u];
 #pragma unroll
-        for (int u = 3; u >= 0; --u) {
+        for (int u = kGrp - 1; u >= 0; --u) {
           const int k = k0 + u;
           if (k < kItems && k < kd && k < nl) {
             A = fmaf(decay, A, dl[k]);
