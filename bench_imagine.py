@@ -56,8 +56,11 @@ def run(n: int = 4096, h: int = 16, steps: int = 5, cpu_sample: int = 64) -> dic
         starts[e, 192 + e % 3] = 1.0
     steps = rng.integers(0, 16, size=args.n)
     im = Imaginer(b, grid=(8, 8))
-    for _ in range(2):
-        im.imagine(starts, steps, args.h, seed=1)
+    # warm-up until torch's page-locked host cache holds two live result sets (the
+    # returned arrays own their buffers; a loop keeps the previous batch while the
+    # next one lands)
+    for _ in range(4):
+        res = im.imagine(starts, steps, args.h, seed=1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for s in range(args.steps):
