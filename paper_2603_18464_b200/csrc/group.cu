@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(1024)
 segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks, int64_t R,
                        int64_t* __restrict__ seg_off, int64_t* __restrict__ piece_off) {
   // (composite keys: nkeys = blocks * keys, n_chunks = chunks per block)
-  __shared__ int64_t s_tot[1024];
-  const int t = threadIdx.x;
+  __shared__ int64_t s_warp[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int per = (nkeys + blockDim.x - 1) / blockDim.x;
   const int j0 = min(nkeys, t * per), j1 = min(nkeys, j0 + per);
   int64_t mine = 0;
@@ -117,20 +117,31 @@ segment_offsets_kernel(const int* __restrict__ base, int nkeys, int64_t n_chunks
     seg_off[j] = a;
     mine += ceil_div(b - a, (int64_t)kPiece);
   }
-  s_tot[t] = mine;
+  // exclusive block scan of the per-thread piece totals (integers: exact in any
+  // order): warp scans, then a scan of the 32 warp totals
+  int64_t x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
   __syncthreads();
-  if (t == 0) {
-    int64_t run = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      const int64_t v = s_tot[i];
-      s_tot[i] = run;
-      run += v;
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
     }
-    seg_off[nkeys] = R;
-    piece_off[nkeys] = run;
+    s_warp[lane] = w;  // inclusive over warps
   }
   __syncthreads();
-  int64_t p = s_tot[t];
+  if (t == 0) {
+    seg_off[nkeys] = R;
+    piece_off[nkeys] = s_warp[(blockDim.x >> 5) - 1];
+  }
+  int64_t p = (x - mine) + (warp > 0 ? s_warp[warp - 1] : 0);
   for (int j = j0; j < j1; ++j) {
     piece_off[j] = p;
     const int64_t a = seg_off[j];
