@@ -144,6 +144,39 @@ __global__ void __launch_bounds__(1024)
 reduce_f64_kernel(const double* __restrict__ part, int64_t parts, int width, int mode,
                   double* __restrict__ out) {
   __shared__ double s[1024];
+  if (width <= 8) {  // every column at once: thread rows, warp trees, warps in order
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = mode ? -CUDART_INF : 0.0;
+    for (int64_t p = threadIdx.x; p < parts; p += blockDim.x) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < width) {
+          const double v = __ldg(part + p * width + c);
+          acc[c] = mode ? fmax(acc[c], v) : acc[c] + v;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double y = __shfl_down_sync(0xffffffffu, acc[c], o);
+        acc[c] = mode ? fmax(acc[c], y) : acc[c] + y;
+      }
+    double* s8 = s;  // [warp][8]
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s8[warp * 8 + c] = acc[c];
+    __syncthreads();
+    if ((int)threadIdx.x < width) {
+      double r = mode ? -CUDART_INF : 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        r = mode ? fmax(r, s8[w * 8 + threadIdx.x]) : r + s8[w * 8 + threadIdx.x];
+      out[threadIdx.x] = r;
+    }
+    return;
+  }
   for (int c = 0; c < width; ++c) {
     double acc = mode ? -CUDART_INF : 0.0;
     for (int64_t p = threadIdx.x; p < parts; p += blockDim.x) {
@@ -165,7 +198,7 @@ reduce_f64_kernel(const double* __restrict__ part, int64_t parts, int width, int
 
 // Level 1 of the two-level reduction for many partial rows: CTA b folds the
 // contiguous rows [b per, (b+1) per) (all <= 8 columns per pass, thread order
-// fixed, shared-memory tree per column) into tmp[b][width].
+// fixed, warp shuffle trees, warps in order) into tmp[b][width].
 constexpr int kRedThreads = 256;
 constexpr int kRedMaxCtas = 296;
 
@@ -186,17 +219,24 @@ reduce_f64_rows_kernel(const double* __restrict__ part, int64_t parts, int width
       }
     }
   }
-  for (int c = 0; c < width; ++c) {
-    s[threadIdx.x] = acc[c];
-    __syncthreads();
-    for (int o = kRedThreads / 2; o > 0; o >>= 1) {
-      if ((int)threadIdx.x < o)
-        s[threadIdx.x] = mode ? fmax(s[threadIdx.x], s[threadIdx.x + o])
-                              : s[threadIdx.x] + s[threadIdx.x + o];
-      __syncthreads();
+  // warp trees, then the warps in order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_down_sync(0xffffffffu, acc[c], o);
+      acc[c] = mode ? fmax(acc[c], y) : acc[c] + y;
     }
-    if (threadIdx.x == 0) tmp[(int64_t)blockIdx.x * width + c] = s[0];
-    __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s[warp * 8 + c] = acc[c];
+  __syncthreads();
+  if ((int)threadIdx.x < width) {
+    double r = mode ? -CUDART_INF : 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w)
+      r = mode ? fmax(r, s[w * 8 + threadIdx.x]) : r + s[w * 8 + threadIdx.x];
+    tmp[(int64_t)blockIdx.x * width + threadIdx.x] = r;
   }
 }
 
@@ -349,6 +389,13 @@ extern "C" size_t accel_reduce_f64_scratch_size(int64_t parts, int width) {
   return (parts > 8192 && width <= 8) ? (size_t)kRedMaxCtas * 8 * sizeof(double) : 0;
 }
 
+// single-block reduction width: <= 8 columns run warp trees (any warp count: about
+// two rows per thread, short rows on one warp); wider rows keep the 1024-thread tree
+static int red_threads(int64_t parts, int width) {
+  if (width > 8) return 1024;
+  return (int)std::min<int64_t>(1024, std::max<int64_t>(32, ceil_div(ceil_div(parts, 2), 32) * 32));
+}
+
 extern "C" int accel_reduce_f64(const double* part, int64_t parts, int width, int mode,
                                 double* out, double* scratch, void* stream) {
   if (parts < 0 || width < 1 || (mode != 0 && mode != 1))
@@ -364,10 +411,10 @@ extern "C" int accel_reduce_f64(const double* part, int64_t parts, int width, in
     int st;
     reduce_f64_rows_kernel<<<ctas, kRedThreads, 0, s>>>(part, parts, width, mode, per, tmp);
     if ((st = post_launch("reduce_f64_rows_kernel"))) return st;
-    reduce_f64_kernel<<<1, 1024, 0, s>>>(tmp, ctas, width, mode, out);
+    reduce_f64_kernel<<<1, red_threads(ctas, width), 0, s>>>(tmp, ctas, width, mode, out);
     return post_launch("reduce_f64_kernel");
   }
-  reduce_f64_kernel<<<1, 1024, 0, s>>>(part, parts, width, mode, out);
+  reduce_f64_kernel<<<1, red_threads(parts, width), 0, s>>>(part, parts, width, mode, out);
   return post_launch("reduce_f64_kernel");
 }
 
