@@ -43,9 +43,10 @@ const char* accel_last_error(void);
 unsigned long long accel_launch_count(void);
 /* Hash of the sources + flags this library was built from (build.py). */
 const char* accel_build_id(void);
-/* ABI version: 3 (row pitches on accel_tanh_grad_colsum, caller workspace on
+/* ABI version: 4 (3: row pitches on accel_tanh_grad_colsum, caller workspace on
  * accel_small_gemm, perm-based accel_fact_group_sum2, piece keys on
- * accel_grouped_rows_sum, accel_value_attn_backward). */
+ * accel_grouped_rows_sum, accel_value_attn_backward; 4: heavy_key on
+ * accel_fold_blocked_pieces). */
 int accel_version(void);
 
 /* One strided copy (cudaMemcpy2DAsync, any direction): `height` rows of
@@ -264,10 +265,14 @@ int accel_fact_group_sum2(const float* h2w, const float* epp, const int32_t* per
                           int key_mod, int A, int64_t n_pieces_max, float* piece_out,
                           void* stream);
 /* out[nkeys, D] = sum over blocks (in order) of the pieces (in order) of the
- * composite keys b * nkeys + key: the key pass of a blocked grouping. */
+ * composite keys b * nkeys + key: the key pass of a blocked grouping.
+ * heavy_key (-1: none): a key holding a large share of the rows (the factorized
+ * head's chunk-start key A * K), folded over more CTAs (a fixed partition:
+ * deterministic). */
 size_t accel_fold_workspace_size(int nkeys, int D);
 int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off, int nkeys,
-                              int nblocks, int D, float* out, void* workspace, void* stream);
+                              int nblocks, int D, int heavy_key, float* out, void* workspace,
+                              void* stream);
 /* piece_key (nullable, from accel_group_by_key_blocked): the key of each piece
  * (else found by a binary search over piece_off per piece). */
 int accel_grouped_rows_sum(const float* vals, int64_t R, int D, const int32_t* perm,

@@ -67,7 +67,7 @@ _SIGNATURES = {
     "accel_serve": (c_int, [P, P, c_int, P, P, P, P, c_int64, P, P, P, P, P, P]),
     "accel_split_tf32": (c_int, [P, c_int64, P, P, P]),
     "accel_sorted_rows": (c_int, [P, P, P, c_int64, c_int, P, P, P, P]),
-    "accel_fold_blocked_pieces": (c_int, [P, P, c_int, c_int, c_int, P, P, P]),
+    "accel_fold_blocked_pieces": (c_int, [P, P, c_int, c_int, c_int, c_int, P, P, P]),
     "accel_grouped_rows_sum": (c_int, [P, c_int64, c_int, P, P, P, P, c_int, c_int64, P, P, P]),
     "accel_warp_grid": (c_int, [c_int64]),
     "accel_value_pool": (c_int, [P, P, P, P, c_int64, c_int, c_int, P, P, P, P, P, P, c_int,

@@ -113,8 +113,11 @@ class DeviceTrainBatch:
         if factorized and (self.pk_group is None or self.pk_group.cpb != pk_cpb):
             # the scatter also writes the inverse permutation (the loss kernel's
             # scalar positions) when the grouping is frame-blocked
+            # key prev * K + k; every transition's token 0 falls in the chunk-start
+            # key A * K (1/K of all tokens): the heavy key of the fold
             self.pk_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A, with_pos=True),
-                                         (A + 1) * K, cpb=pk_cpb, rows=pk_cpb > 0)
+                                         (A + 1) * K, cpb=pk_cpb, rows=pk_cpb > 0,
+                                         heavy_key=A * K)
         if not factorized and self.prev_group is None:
             self.prev_group = ops.Grouping(ops.prev_keys(self.tokens_dev, N, K, A), A + 1)
         if frame_space:

@@ -28,7 +28,7 @@ extern "C" unsigned long long accel_launch_count(void) {
   return accel::g_launches.load(std::memory_order_relaxed);
 }
 
-extern "C" int accel_version(void) { return 3; }
+extern "C" int accel_version(void) { return 4; }
 
 #ifndef ACCEL_BUILD_ID
 #define ACCEL_BUILD_ID "unknown"

@@ -396,17 +396,21 @@ key_sum4_kernel(const float4* __restrict__ piece_out, const int64_t* __restrict_
 // composite key b * nkeys + key (in order).  Grid (key, split): CTA (key, q)
 // folds the contiguous block range q of the key into part[q][key] (64 float4
 // columns x 4 block-lanes, four loads in flight, lanes combined in order);
-// fold_parts_kernel then sums the kFoldSplit parts in order.  The chunk-start
-// key holds a piece per 256 transitions of every block: splitting its blocks
-// over CTAs keeps it off the critical path.
+// fold_parts_kernel then sums the kFoldSplit parts in order.  One key may be
+// heavy (the factorized head's chunk-start key holds every transition's token 0:
+// a piece per 256 of them in every block); it is skipped here and folded by
+// fold_heavy_parts_kernel over ~kHeavySplit CTAs instead.
 constexpr int kFoldThreads = 256;
-constexpr int kFoldSplit = 8;
+constexpr int kFoldSplit = 2;
+constexpr int kHeavySplit = 64;
+constexpr int kHeavyMaxParts = 2 * kHeavySplit;
 __global__ void __launch_bounds__(kFoldThreads)
 fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
                            const int64_t* __restrict__ piece_off, int nkeys, int nblocks, int D4,
-                           float4* __restrict__ part) {
+                           int heavy_key, float4* __restrict__ part) {
   __shared__ float4 s4[kFoldThreads];
   const int key = blockIdx.x, q = blockIdx.y, split = gridDim.y;
+  if (key == heavy_key) return;
   const int b0 = (int)((int64_t)nblocks * q / split);
   const int b1 = (int)((int64_t)nblocks * (q + 1) / split);
   const int span = D4 <= kFoldThreads && kFoldThreads % D4 == 0 ? D4 : kFoldThreads;
@@ -447,6 +451,107 @@ fold_blocked_pieces_kernel(const float4* __restrict__ piece_out,
         r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
       }
       part[((int64_t)q * nkeys + key) * D4 + d0 + threadIdx.x] = r;
+    }
+    __syncthreads();
+  }
+}
+
+// The heavy key: nq CTAs; with nblocks >= kHeavySplit CTA q takes a contiguous
+// block range, else (r = ceil(kHeavySplit / nblocks) CTAs per block) sub-range
+// q % r of block q / r's pieces.  The 4 lane-rows take every 4th piece of the
+// range (four loads in flight each); lanes combined in order into hpart[q].
+__global__ void __launch_bounds__(kFoldThreads)
+fold_heavy_parts_kernel(const float4* __restrict__ piece_out, const int64_t* __restrict__ piece_off,
+                        int nkeys, int nblocks, int D4, int key, int r, float4* __restrict__ hpart) {
+  __shared__ float4 s4[kFoldThreads];
+  const int q = blockIdx.x, nq = gridDim.x;
+  const int b0 = r == 1 ? (int)((int64_t)nblocks * q / nq) : q / r;
+  const int b1 = r == 1 ? (int)((int64_t)nblocks * (q + 1) / nq) : b0 + 1;
+  const int j = q % r;
+  const int span = D4 <= kFoldThreads && kFoldThreads % D4 == 0 ? D4 : kFoldThreads;
+  const int sub = kFoldThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  for (int d0 = 0; d0 < D4; d0 += span) {
+    const int d = d0 + lc;
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (d < D4) {
+      for (int b = b0; b < b1; ++b) {
+        const int64_t ck = (int64_t)b * nkeys + key;
+        const int64_t p0 = __ldg(piece_off + ck), p1 = __ldg(piece_off + ck + 1), n = p1 - p0;
+        const int64_t pa = p0 + n * j / r, pb = p0 + n * (j + 1) / r;
+        int64_t p = pa + lr;
+        for (; p + 3 * sub < pb; p += 4 * sub) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 x = __ldg(piece_out + (p + u * sub) * D4 + d);
+            a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+          }
+        }
+        for (int u = 0; p < pb; p += sub, ++u) {
+          const float4 x = __ldg(piece_out + p * D4 + d);
+          a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+        }
+      }
+    }
+    s4[threadIdx.x] = make_float4(((a[0].x + a[1].x) + a[2].x) + a[3].x,
+                                  ((a[0].y + a[1].y) + a[2].y) + a[3].y,
+                                  ((a[0].z + a[1].z) + a[2].z) + a[3].z,
+                                  ((a[0].w + a[1].w) + a[2].w) + a[3].w);
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D4) {
+      float4 rr = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s2 = 0; s2 < sub; ++s2) {
+        const float4 y = s4[s2 * span + threadIdx.x];
+        rr.x += y.x; rr.y += y.y; rr.z += y.z; rr.w += y.w;
+      }
+      hpart[(int64_t)q * D4 + d0 + threadIdx.x] = rr;
+    }
+    __syncthreads();
+  }
+}
+
+// out[key] = the heavy key's nq parts: column group i's parts in 4 strided
+// accumulators per lane-row, lane-rows and accumulators combined in a fixed order
+__global__ void __launch_bounds__(kFoldThreads)
+fold_heavy_kernel(const float4* __restrict__ hpart, int nq, int D4, int key,
+                  float4* __restrict__ out) {
+  __shared__ float4 s4[kFoldThreads];
+  const int span = D4 <= kFoldThreads && kFoldThreads % D4 == 0 ? D4 : kFoldThreads;
+  const int sub = kFoldThreads / span;
+  const int lr = threadIdx.x / span, lc = threadIdx.x % span;
+  for (int d0 = 0; d0 < D4; d0 += span) {
+    const int d = d0 + lc;
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (d < D4) {
+      int q = lr;
+      for (; q + 3 * sub < nq; q += 4 * sub) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 y = hpart[(int64_t)(q + u * sub) * D4 + d];
+          a[u].x += y.x; a[u].y += y.y; a[u].z += y.z; a[u].w += y.w;
+        }
+      }
+      for (int u = 0; q < nq; q += sub, ++u) {
+        const float4 y = hpart[(int64_t)q * D4 + d];
+        a[u].x += y.x; a[u].y += y.y; a[u].z += y.z; a[u].w += y.w;
+      }
+    }
+    s4[threadIdx.x] = make_float4(((a[0].x + a[1].x) + a[2].x) + a[3].x,
+                                  ((a[0].y + a[1].y) + a[2].y) + a[3].y,
+                                  ((a[0].z + a[1].z) + a[2].z) + a[3].z,
+                                  ((a[0].w + a[1].w) + a[2].w) + a[3].w);
+    __syncthreads();
+    if (threadIdx.x < span && d0 + threadIdx.x < D4) {
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s2 = 0; s2 < sub; ++s2) {
+        const float4 y = s4[s2 * span + threadIdx.x];
+        r.x += y.x; r.y += y.y; r.z += y.z; r.w += y.w;
+      }
+      out[(int64_t)key * D4 + d0 + threadIdx.x] = r;
     }
     __syncthreads();
   }
@@ -653,31 +758,51 @@ extern "C" int accel_group_by_key(const int32_t* keys, int64_t R, int nkeys, int
 }
 
 extern "C" size_t accel_fold_workspace_size(int nkeys, int D) {
-  return sizeof(float) * (size_t)kFoldSplit * nkeys * D;
+  return sizeof(float) * ((size_t)kFoldSplit * nkeys + kHeavyMaxParts) * D;
 }
 
 // out[nkeys, D] = sum over blocks of the piece sums of composite keys b * nkeys + key
 extern "C" int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* piece_off,
-                                         int nkeys, int nblocks, int D, float* out,
+                                         int nkeys, int nblocks, int D, int heavy_key, float* out,
                                          void* workspace, void* stream) {
-  if (nkeys < 1 || nblocks < 1 || D < 4 || (D & 3)) return fail(kDimension, "fold_blocked: bad sizes");
+  if (nkeys < 1 || nblocks < 1 || D < 4 || (D & 3) || heavy_key < -1 || heavy_key >= nkeys)
+    return fail(kDimension, "fold_blocked: bad sizes");
   if (!piece_buf || !piece_off || !out || !workspace)
     return fail(kDimension, "fold_blocked: NULL buffer");
   if ((reinterpret_cast<uintptr_t>(piece_buf) | reinterpret_cast<uintptr_t>(out) |
        reinterpret_cast<uintptr_t>(workspace)) & 15)
     return fail(kDimension, "fold_blocked: buffers must be 16B aligned");
   cudaStream_t s = as_stream(stream);
+  const int D4 = D / 4;
   float4* part = static_cast<float4*>(workspace);
-  const int split = std::min(kFoldSplit, nblocks);  // fixed by nblocks: deterministic
+  float4* hpart = part + (size_t)kFoldSplit * nkeys * D4;
+  // every split is fixed by nblocks and the caller's heavy key: deterministic
+  const int split = std::min(kFoldSplit, nblocks);
   float4* dst = split == 1 ? reinterpret_cast<float4*>(out) : part;
+  const auto pieces = reinterpret_cast<const float4*>(piece_buf);
   fold_blocked_pieces_kernel<<<dim3(nkeys, split), kFoldThreads, 0, s>>>(
-      reinterpret_cast<const float4*>(piece_buf), piece_off, nkeys, nblocks, D / 4, dst);
+      pieces, piece_off, nkeys, nblocks, D4, nblocks > 1 ? heavy_key : -1, dst);
   int st = post_launch("fold_blocked_pieces_kernel");
-  if (st || split == 1) return st;
-  const int64_t n4 = (int64_t)nkeys * (D / 4);
-  fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(part, n4, n4, split,
-                                                                reinterpret_cast<float4*>(out));
-  return post_launch("fold_parts_kernel");
+  if (st) return st;
+  if (split > 1) {
+    const int64_t n4 = (int64_t)nkeys * D4;
+    fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(part, n4, n4, split,
+                                                                  reinterpret_cast<float4*>(out));
+    if ((st = post_launch("fold_parts_kernel"))) return st;
+  }
+  // (a single block: the plain pass already runs every key on its own CTAs)
+  const int heavy = nblocks > 1 ? heavy_key : -1;
+  if (heavy >= 0) {  // after fold_parts: it wrote an unused row for the heavy key
+    const int r = nblocks >= kHeavySplit ? 1 : (kHeavySplit + nblocks - 1) / nblocks;
+    const int nq = r == 1 ? kHeavySplit : nblocks * r;  // <= kHeavyMaxParts
+    fold_heavy_parts_kernel<<<nq, kFoldThreads, 0, s>>>(pieces, piece_off, nkeys, nblocks, D4,
+                                                        heavy, r, hpart);
+    if ((st = post_launch("fold_heavy_parts_kernel"))) return st;
+    fold_heavy_kernel<<<1, kFoldThreads, 0, s>>>(hpart, nq, D4, heavy,
+                                                 reinterpret_cast<float4*>(out));
+    st = post_launch("fold_heavy_kernel");
+  }
+  return st;
 }
 
 // out[nkeys, D] = grouped sums of vals[R, D] rows; piece_buf holds

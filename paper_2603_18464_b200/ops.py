@@ -218,13 +218,15 @@ class Grouping:
     touches one block of rows at a time (accel_group_by_key_blocked); the key
     sums then fold the blocks in order (accel_fold_blocked_pieces)."""
 
-    def __init__(self, keys, nkeys: int, cpb: int = 0, rows=None):
+    def __init__(self, keys, nkeys: int, cpb: int = 0, rows=None, heavy_key: int = -1):
         """rows: also write the inverse permutation pos inside the scatter (see
-        sort_rows)."""
+        sort_rows).  heavy_key: a key expected to hold a large share of the rows
+        (its key pass runs over more CTAs; -1: none)."""
         R = keys.numel()
         dev = keys.device
         lib = _lib.lib()
         self.R, self.nkeys, self.cpb = R, int(nkeys), int(cpb)
+        self.heavy_key = int(heavy_key)
         self.nblocks = int(lib.accel_group_blocks(R, self.cpb)) if cpb > 0 else 1
         nk = self.nkeys * self.nblocks
         self.perm = torch.empty(max(R, 1), dtype=I32, device=dev)
@@ -286,7 +288,7 @@ class Grouping:
         if self.cpb > 0:
             wsb = stream_workspace("fold", _lib.lib().accel_fold_workspace_size(self.nkeys, D))
             _lib.call("accel_fold_blocked_pieces", _pp(piece_buf), _pp(self.piece_off), self.nkeys,
-                      self.nblocks, D, _pp(out), _pp(wsb), _stream())
+                      self.nblocks, D, self.heavy_key, _pp(out), _pp(wsb), _stream())
         else:
             _lib.call("accel_grouped_rows_sum", None, self.R, D, _pp(self.perm), _pp(self.seg_off),
                       _pp(self.piece_off), _pp(self.piece_key), self.nkeys, self.max_pieces,
