@@ -58,6 +58,23 @@ class DataParallel:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return t
 
+    def all_reduce_sum_max(self, s: torch.Tensor, m: torch.Tensor) -> None:
+        """s <- sum over ranks, m <- max over ranks (1-D float64), in ONE
+        collective: both are gathered and every rank reduces the [world, n]
+        rows in rank order (identical results on every rank)."""
+        ns = s.numel()
+        buf = torch.cat([s, m])
+        if self.backend == "nccl":
+            rows = torch.empty(self.world * buf.numel(), dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(rows, buf, group=self.group)
+            rows = rows.view(self.world, -1)
+        else:
+            parts = [torch.empty_like(buf) for _ in range(self.world)]
+            dist.all_gather(parts, buf, group=self.group)
+            rows = torch.stack(parts)
+        s.copy_(rows[:, :ns].sum(0))
+        m.copy_(rows[:, ns:].amax(0))
+
     def global_counts(self, n_local: int, k: int) -> tuple:
         t = torch.tensor([float(n_local)], dtype=torch.float64, device=self._device())
         self.all_reduce_sum(t)

@@ -989,9 +989,8 @@ class Trainer:
                                dbias_part, stat_part, max_part)
         ops.reduce_f64(stat_part, gl, 8, 0, loss_sums)
         ops.reduce_f64(max_part, gl, 2, 1, loss_max)
-        if self.comm is not None:
-            self.comm.all_reduce_sum(loss_sums)
-            self.comm.all_reduce_max(loss_max)
+        if self.comm is not None:  # C5: token sums and maxima in one collective
+            self.comm.all_reduce_sum_max(loss_sums, loss_max)
         # the value bucket's exchange queues after the loss all-reduces above (one
         # process group runs collectives in issue order: issued earlier, it would
         # hold the FIXUP pass behind the whole value-head branch)

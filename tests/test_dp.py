@@ -137,9 +137,13 @@ def _worker(rank, world, port, out_q):
         dp.all_reduce_sum(sums)
         mx = torch.tensor([float(rank)], dtype=torch.float64)
         dp.all_reduce_max(mx)
+        # C5: token sums and maxima in one collective
+        ls = torch.tensor([1.5 * (rank + 1), -2.0 * rank], dtype=torch.float64)
+        lm = torch.tensor([float(rank), -float(rank)], dtype=torch.float64)
+        dp.all_reduce_sum_max(ls, lm)
         out_q.put((rank, params.p[1].clone(), sums, mx, dp.global_counts(7 + rank, 3),
                    params._moments_host[1][0].copy(), params._moments_host[1][1].copy(),
-                   params.m[1].numel(), stale_raised))
+                   params.m[1].numel(), stale_raised, ls, lm))
     finally:
         dist.destroy_process_group()
 
@@ -172,6 +176,8 @@ def test_zero2_adam_and_collectives_gloo():
                                                     20.0])
         assert res[r][2].item() == world - 1
         assert res[r][3] == (7 + 8, (7 + 8) * 3)
+        assert res[r][8].tolist() == [1.5 + 3.0, -2.0]
+        assert res[r][9].tolist() == [1.0, 0.0]
     # every bucket is a whole number of 16-byte rank slices
     for lo, hi, _ in layout.buckets:
         assert (hi - lo) % (4 * world) == 0
