@@ -557,10 +557,12 @@ fold_heavy_kernel(const float4* __restrict__ hpart, int nq, int D4, int key,
   }
 }
 
+// (skip: [skip_lo, skip_hi) float4s -- the heavy key's row, folded separately)
 __global__ void fold_parts_kernel(const float4* __restrict__ part, int64_t n4, int64_t stride4,
-                                  int split, float4* __restrict__ out) {
+                                  int split, float4* __restrict__ out, int64_t skip_lo = 0,
+                                  int64_t skip_hi = 0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n4) return;
+  if (i >= n4 || (i >= skip_lo && i < skip_hi)) return;
   float4 r = part[i];
   for (int q = 1; q < split; ++q) {
     const float4 y = part[q * stride4 + i];
@@ -784,15 +786,16 @@ extern "C" int accel_fold_blocked_pieces(const float* piece_buf, const int64_t* 
       pieces, piece_off, nkeys, nblocks, D4, nblocks > 1 ? heavy_key : -1, dst);
   int st = post_launch("fold_blocked_pieces_kernel");
   if (st) return st;
-  if (split > 1) {
-    const int64_t n4 = (int64_t)nkeys * D4;
-    fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(part, n4, n4, split,
-                                                                  reinterpret_cast<float4*>(out));
-    if ((st = post_launch("fold_parts_kernel"))) return st;
-  }
   // (a single block: the plain pass already runs every key on its own CTAs)
   const int heavy = nblocks > 1 ? heavy_key : -1;
-  if (heavy >= 0) {  // after fold_parts: it wrote an unused row for the heavy key
+  if (split > 1) {
+    const int64_t n4 = (int64_t)nkeys * D4;
+    const int64_t h0 = heavy >= 0 ? (int64_t)heavy * D4 : 0;
+    fold_parts_kernel<<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>(
+        part, n4, n4, split, reinterpret_cast<float4*>(out), h0, heavy >= 0 ? h0 + D4 : 0);
+    if ((st = post_launch("fold_parts_kernel"))) return st;
+  }
+  if (heavy >= 0) {
     const int r = nblocks >= kHeavySplit ? 1 : (kHeavySplit + nblocks - 1) / nblocks;
     const int nq = r == 1 ? kHeavySplit : nblocks * r;  // <= kHeavyMaxParts
     fold_heavy_parts_kernel<<<nq, kFoldThreads, 0, s>>>(pieces, piece_off, nkeys, nblocks, D4,
