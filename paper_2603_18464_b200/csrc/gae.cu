@@ -227,7 +227,7 @@ gae_warp_kernel(const float* __restrict__ rewards, const float* __restrict__ val
     float dl[kItems];
     float vnext = sv[min(kd, max(nl, 0))];  // v after the lane's last valid step
     float B = 0.f, C = 1.f;  // the lane's composed map (right to left)
-    // steps in groups of 4 (a warp-uniform test per group, the group's shared-memory
+    // steps in groups of kGrp (a warp-uniform test per group, the group's shared-memory
     // loads issued together); steps past the lane's last valid one are identities
 #pragma unroll
     for (int g = (kItems - 1) / kGrp; g >= 0; --g) {
