@@ -800,7 +800,11 @@ int launch_wgrad(const float* dY, const float* X, float* C, int64_t F, int n, in
     if (stacked) return mc <= 64 ? (concat ? mma(2 * nsl * 32) : 2 * mma(npad)) : 1 << 30;
     const int mt = (mc + BM - 1) / BM;
     if (mt > 2 || nsl > 8) return 1 << 30;
-    return mt * (concat ? mma(2 * nsl * 32) + mma(npad) : 3 * mma(npad));
+    const int c = mt * (concat ? mma(2 * nsl * 32) + mma(npad) : 3 * mma(npad));
+    // two M tiles also convert and stage the wide P's lo halves through the lo
+    // ring: measured slower than the MMA count says (G^T h2, 256 x 64: split 543 us,
+    // stacked with the operands swapped 480 us)
+    return mt == 2 ? c + c / 4 : c;
   };
   int best = 1 << 30;
   bool swap = false, stacked = false;
