@@ -193,43 +193,61 @@ def device_inputs(lens, done, seed: int, device):
 
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks / throttle reasons at 50 ms intervals.  start() launches the
+    poller early (its start-up takes ~0.1 s); the `with` block marks the timed
+    region, and only samples stamped inside it (+ one interval) are summarised."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        if self.proc is None:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                     "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                    stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                self.proc = None
+        return self
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+        import datetime
+        self.start()
+        self.t0 = datetime.datetime.now()
         return self
 
     def __exit__(self, *exc):
+        import datetime
+        self.t1 = datetime.datetime.now()
         self.summary = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         if self.proc is None:
             return False
-        time.sleep(0.25)
+        time.sleep(0.12)
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        lo = self.t0 - datetime.timedelta(milliseconds=10)
+        hi = self.t1 + datetime.timedelta(milliseconds=60)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                if not lo <= ts <= hi:
+                    continue
+                sm.append(float(parts[2]))
+                smax.append(float(parts[3]))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
+            for nm, val in zip(names, parts[6:10]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         if sm:
@@ -583,6 +601,7 @@ def main():
         batch = tr.build_from_device(inp, n_real=n, behavior_version=bver)
         return tr.train_step(batch)
 
+    clocks = ClockSampler(local).start()  # the poller is up before the timed region
     for _ in range(args.warmup):
         step(inputs)
     torch.cuda.synchronize()
@@ -593,7 +612,7 @@ def main():
     if comm is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with clocks:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
